@@ -1,0 +1,162 @@
+/* swamp_gpu.h — C-ABI of the B200-native GPU-HWFV1 adaptive time-step loop.
+ *
+ * This is the drop-in boundary for the reference's adaptive solver path
+ * (SPEC.md "engine" module) built on the
+ * reference's Z-order index algebra (/root/reference/proj/include/swamp/
+ * zorder.hpp:9-133). The reference ships no compiled engine; its interface is
+ * the spec's  SimConfig, SimState,
+ * StepReport, initialise, step_adaptive
+ * (SPEC.md:399), step_uniform, run. Each entry
+ * point below names the operation it replaces.
+ *
+ * ABI rules: plain C types only; every function returns a status (0 = ok,
+ * <0 = error, see SWAMP_E_*); no exceptions cross; the handle owns all device
+ * memory, the caller owns every host buffer; one handle per engine, driven
+ * from one control thread. The include/swamp/engine.hpp facade
+ * rethrows errors as std::runtime_error / std::out_of_range.
+ *
+ * Conventions shared with the reference:
+ *   - finest-level input rasters are row-major with row j = 0 the SOUTH row
+ *     and column i = 0 the WEST column (j up, zorder.hpp:11-12, 123-128);
+ *   - hierarchy exports are indexed by z-index z = (4^n-1)/3 + m
+ *     (zorder.hpp:68-73) and hold SCALE COEFFICIENTS s (physical value =
+ *     s * 2^(n-L));
+ *   - neighbour descriptors are z-indices, or
+ *     SWAMP_BOUNDARY_BASE + boundary kind for an edge of the domain;
+ *   - leaves are listed in ascending first-covered-Morton order.
+ */
+#ifndef SWAMP_GPU_H
+#define SWAMP_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SWAMP_OK 0
+#define SWAMP_E_ARG (-1)      /* invalid argument / config         */
+#define SWAMP_E_CUDA (-2)     /* CUDA runtime failure                            */
+#define SWAMP_E_NONFINITE (-3) /* non-finite coefficient / flux */
+#define SWAMP_E_DT (-4)       /* dt <= 0 or non-finite             */
+#define SWAMP_E_STATE (-5)    /* call not valid in the current state             */
+#define SWAMP_E_NOMEM (-6)    /* device allocation failed                        */
+
+/* boundary kinds */
+#define SWAMP_BC_REFLECTIVE 0
+#define SWAMP_BC_TRANSMISSIVE 1
+#define SWAMP_BC_INFLOW 2
+
+/* refinement safety band (D3) */
+#define SWAMP_BAND_NONE 0       /* strict-paper mode              */
+#define SWAMP_BAND_PARENTS 1    /* SPEC.md:195 literal: neighbours' parents     */
+#define SWAMP_BAND_NEIGHBOURS 2 /* default: same-level face neighbours          */
+
+#define SWAMP_INFLOW_DEPTH 0
+#define SWAMP_INFLOW_ETA 1
+
+#define SWAMP_BOUNDARY_BASE 0xFFFFFFF0u /* descriptor = BASE + kind            */
+
+/* SimConfig. The hierarchy is the 2^L x 2^L square of side
+ * `width` with lower-left corner (x0, y0). */
+typedef struct swamp_config {
+    int32_t L;             /* finest level, 1..13 (zorder.hpp:21)              */
+    int32_t band_mode;     /* SWAMP_BAND_*                                      */
+    double epsilon;        /* error threshold >= 0                              */
+    double width;          /* side W of the square domain (m)                   */
+    double x0, y0;         /* lower-left corner (m)                             */
+    double cfl;            /* CFL number C (default 0.5)           */
+    double g;              /* gravity (default 9.80665)            */
+    double manning;        /* n_M (s m^-1/3)                                    */
+    double h_dry;          /* dry threshold (default 1e-6)         */
+    double t_end;          /* simulation end time (s)                           */
+    double dt_fallback;    /* all-dry time step                   */
+    int32_t bc[4];         /* W, E, N, S edge kinds: SWAMP_BC_*                 */
+    int32_t inflow_mode;   /* SWAMP_INFLOW_DEPTH or SWAMP_INFLOW_ETA            */
+    int32_t inflow_n;      /* number of (t, v) samples                          */
+    int32_t n_outputs;     /* number of output times                            */
+    const double* inflow_t; /* inflow series times, ascending                   */
+    const double* inflow_v; /* inflow series values                             */
+    const double* output_times; /* ascending; dt is clipped to hit them        */
+} swamp_config;
+
+/* StepReport. Stage times are device times in ms measured
+ * with CUDA events when the handle was created with profiling enabled
+ * (swamp_gpu_set_profiling), otherwise 0. */
+typedef struct swamp_step_report {
+    int64_t step;          /* steps taken so far                                */
+    double t;              /* simulation time after the step                    */
+    double dt;             /* dt that the NEXT step will use                    */
+    double dt_used;        /* dt of the step just taken                         */
+    int64_t n_leaves;      /* leaves of the grid the step was computed on       */
+    int64_t n_leaves_next; /* leaves after re-adaptation (next step's grid)     */
+    double ms_encode_flag; /* zero_details_and_reencode + significance          */
+    double ms_band_closure;/* band + ancestor closure + leaf-count scan         */
+    double ms_decode_traverse; /* decode + PTT + compaction                     */
+    double ms_neighbours;  /* fused into FV1 on this build: always 0            */
+    double ms_fv1;         /* FV1 + friction + write-back + CFL reduce          */
+    double ms_total;
+} swamp_step_report;
+
+typedef struct swamp_gpu swamp_gpu;
+
+/* initialise: upload the finest-level fields (row-major,
+ * south row first, length 4^L each), full bottom-up encode, DEM mask,
+ * significance, traversal, first dt. `device` is the CUDA ordinal. */
+int swamp_gpu_create(const swamp_config* cfg, const double* h, const double* qx, const double* qy,
+                     const double* z, int device, swamp_gpu** out);
+int swamp_gpu_destroy(swamp_gpu* g);
+
+/* step_adaptive: one Alg. 3 iteration. No-op when
+ * t >= t_end. Fills `rep` (may be NULL). Synchronises the device. */
+int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep);
+
+/* Advance `n_steps` adaptive steps without host round trips (CUDA graph of
+ * the step's kernels, replayed); stops early (device-side no-op) once
+ * t >= t_end. Synchronises once at the end and checks the error word. */
+int swamp_gpu_advance(swamp_gpu* g, int64_t n_steps, swamp_step_report* rep);
+
+/* run without outputs: step until t >= t_end. */
+int swamp_gpu_run(swamp_gpu* g, swamp_step_report* rep);
+
+/* step_uniform: the GPU-FV1 comparator on all 4^L cells,
+ * no MRA. Only valid on a handle created with swamp_gpu_create_uniform. */
+int swamp_gpu_create_uniform(const swamp_config* cfg, const double* h, const double* qx,
+                             const double* qy, const double* z, int device, swamp_gpu** out);
+int swamp_gpu_step_uniform(swamp_gpu* g, int64_t n_steps, swamp_step_report* rep);
+
+/* Stage timing on/off (per-kernel CUDA events; disables graph replay). */
+int swamp_gpu_set_profiling(swamp_gpu* g, int enabled);
+
+/* State queries / export (SimState). */
+int swamp_gpu_info(const swamp_gpu* g, double* t, double* dt, int64_t* step, int64_t* n_leaves);
+/* Leaves (ascending first-covered Morton) and W,E,N,S descriptors; arrays of
+ * capacity `cap`; *n receives the leaf count. Any pointer may be NULL. */
+int swamp_gpu_copy_leaves(swamp_gpu* g, uint32_t* leaves, uint32_t* nbr_w, uint32_t* nbr_e,
+                          uint32_t* nbr_n, uint32_t* nbr_s, int64_t cap, int64_t* n);
+/* Hierarchy scale coefficients of the CURRENT tree (length hierarchy_cells):
+ * leaves hold post-step values, significant cells their re-encoded / decoded
+ * values; cells off the tree are unspecified. sig: detail_cells bytes, 1 =
+ * significant. Any pointer may be NULL. */
+int swamp_gpu_export_tree(swamp_gpu* g, double* h, double* qx, double* qy, double* z, uint8_t* sig);
+/* Zero-detail expansion to the finest grid: physical
+ * values, row-major south row first, length 4^L each. */
+int swamp_gpu_export_finest(swamp_gpu* g, double* h, double* qx, double* qy);
+
+/* Device error word of the last failure: code, z-index, quantity, stage. */
+int swamp_gpu_last_error(const swamp_gpu* g, int32_t* code, uint32_t* z, int32_t* quantity,
+                         int32_t* stage, char* msg, size_t msg_cap);
+
+/* Per-step counters of the last stepped grid, for roofline bookkeeping:
+ * [0] leaves N, [1] significant tree cells (prev tree, re-encoded),
+ * [2] newly significant cells (decoded), [3] 4^L. */
+int swamp_gpu_counters(swamp_gpu* g, int64_t* out4);
+
+/* Build identification (arch, flags) for logs. */
+const char* swamp_gpu_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWAMP_GPU_H */

@@ -1,0 +1,910 @@
+// hwfv1_kernels.cuh — the sm_100a kernels of one adaptive HWFV1 time step
+// (Alg. 3):
+//
+//   K1 k_encode    zero_details_and_reencode + significance (+ DEM mask at t=0)
+//                  level-fused over a level-R subtree per CTA, 4 lanes per
+//                  parent at the finest level (warp shuffles), shared memory
+//                  above; the last CTA finishes levels < R.
+//   K2 k_band      safety band + ancestor closure per subtree, leaf count per
+//                  subtree; the last CTA closes levels < R and scans the
+//                  per-subtree leaf counts into output offsets.
+//   K3 k_traverse  decode (projection of newly significant cells, D4) +
+//                  parallel tree traversal (Alg. 5) + stream compaction.
+//   K5 k_fv1       neighbour finding by Morton arithmetic + flag walk, FV1
+//                  (HLL, hydrostatic reconstruction, friction), write-back,
+//                  CFL min; the last CTA advances t and computes the next dt.
+//
+// Storage: the hierarchy is an array of double4 cells
+// {h, qx, qy, z} in PHYSICAL units, one Morton-ordered slice per level with
+// every level base 256-B aligned; two copies ping-pong (D15). Significance is
+// one byte per detail cell and per level, two copies ping-pong (previous /
+// current tree). All control state (t, dt, parity, leaf count, error word)
+// lives on the device so a step is a fixed kernel sequence (CUDA-graph
+// capturable); every kernel is a no-op once t >= t_end.
+#pragma once
+#include <cstdint>
+
+#include "hwfv1_physics.cuh"
+#include "swamp/zorder.hpp"
+
+namespace hwfv1 {
+
+namespace zo = swamp::zorder;
+
+constexpr int kThreads = 256;
+constexpr int kMaxL = 13;
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr uint32_t kNoSrc = 0xFFFFFFFFu;
+
+enum Stage : int { kStageImport = 0, kStageEncode = 1, kStageBand = 2, kStageTraverse = 3, kStageFV1 = 5, kStageDt = 6 };
+enum ErrCode : int { kErrNone = 0, kErrNonFinite = -3, kErrDt = -4 };
+
+struct Ctl {
+    double t;        // current simulation time
+    double dt;       // dt of the next step
+    double t_next;   // time after the next step (exact stop time when clipped)
+    double dt_used;  // dt of the last step taken
+    unsigned long long dtmin_bits;  // CFL min accumulator (bits of a positive double)
+    unsigned long long smax_bits[4];
+    long long step;
+    unsigned long long cnt_tree;    // cells re-encoded by the last K1
+    unsigned long long cnt_new;     // newly significant cells decoded by the last K3
+    uint32_t n_leaves;              // leaves of the grid built by the last K2/K3
+    uint32_t n_leaves_used;         // leaves the last FV1 updated
+    int parity;                     // current cell buffer / previous-tree flags
+    int err_code;
+    uint32_t err_z;
+    int err_q;
+    int err_stage;
+    unsigned int done_k1, done_k2, done_k5;
+};
+
+struct Params {
+    int L, R, K, n_tiles;
+    int band_mode;
+    int bc[4];
+    int inflow_mode, inflow_n, n_out;
+    double W, cfl, t_end, dt_fallback;
+    double tau[kMaxL + 1];    // significance threshold per detail level, physical units
+    double dx[kMaxL + 1];     // W * 2^-n
+    double smax[4];
+    PhysParams phys;
+    const double* inflow_t;
+    const double* inflow_v;
+    const double* out_times;
+    unsigned long long base[kMaxL + 2];   // double4 offset of level n
+    unsigned long long fbase[kMaxL + 1];  // flag byte offset of level n
+    double4* cells[2];
+    uint8_t* sig[2];
+    uint8_t* pre;
+    uint8_t* dem;
+    uint32_t* leaves;
+    uint32_t* tile_cnt;
+    uint32_t* tile_off;
+};
+
+// ------------------------------------------------------------------ memory ops
+__device__ __forceinline__ double4 ld4(const double4* p) {
+    double4 v;
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double4 ld4_nc(const double4* p) {
+    double4 v;
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double4 ld4_cg(const double4* p) {
+    double4 v;
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st4(double4* p, double4 v) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+}
+__device__ __forceinline__ uint8_t ldcg_u8(const uint8_t* p) {
+    unsigned short v;
+    asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(v) : "l"(p));
+    return static_cast<uint8_t>(v);
+}
+__device__ __forceinline__ uint32_t ldcg_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t lo(int n, int R) { return ((1u << (2 * (n - R))) - 1u) / 3u; }
+
+__device__ __forceinline__ void report_error(Ctl* c, int code, uint32_t z, int q, int stage) {
+    if (atomicCAS(&c->err_code, 0, code) == 0) {
+        c->err_z = z;
+        c->err_q = q;
+        c->err_stage = stage;
+    }
+}
+
+// ------------------------------------------------------ encode helpers (Eqs. 3)
+struct Red {
+    double par, dmax;
+};
+// 4 consecutive lanes hold children c0..c3 (k = lane & 3); lane k = 0 ends up
+// with parent = 0.25*((c0+c1)+(c2+c3)) and max |detail| in physical units.
+__device__ __forceinline__ Red red4_shfl(double v) {
+    const double x1 = __shfl_xor_sync(kFull, v, 1);
+    const double s01 = v + x1;
+    const double x2 = __shfl_xor_sync(kFull, s01, 2);
+    const double par = 0.25 * (s01 + x2);
+    const double da = s01 - x2;
+    const double y2 = __shfl_xor_sync(kFull, v, 2);
+    const double s02 = v + y2;
+    const double z1 = __shfl_xor_sync(kFull, s02, 1);
+    const double db = s02 - z1;
+    const double y3 = __shfl_xor_sync(kFull, v, 3);
+    const double s03 = v + y3;
+    const double w1 = __shfl_xor_sync(kFull, s03, 1);
+    const double dg = s03 - w1;
+    return {par, max2(max2(absd(da), absd(db)), absd(dg))};
+}
+__device__ __forceinline__ double par_shfl(double v) {
+    const double x1 = __shfl_xor_sync(kFull, v, 1);
+    const double s01 = v + x1;
+    const double x2 = __shfl_xor_sync(kFull, s01, 2);
+    return 0.25 * (s01 + x2);
+}
+__device__ __forceinline__ Red red4(double c0, double c1, double c2, double c3) {
+    const double a = c0 + c1, b = c2 + c3;
+    const double par = 0.25 * (a + b);
+    const double da = a - b;
+    const double db = (c0 + c2) - (c1 + c3);
+    const double dg = (c0 + c3) - (c1 + c2);
+    return {par, max2(max2(absd(da), absd(db)), absd(dg))};
+}
+// significance of one quantity (D6, D7): s_max < 1e-12 -> d_norm 0
+__device__ __forceinline__ bool sig_q(double dmax, double smax, double tau) {
+    const double dn = (smax < 1e-12) ? 0.0 : dmax / smax;
+    return dn >= tau;
+}
+
+struct Enc {
+    double4 par;
+    bool flow, zflag;
+};
+__device__ __forceinline__ Enc encode_children(const double4 c[4], const Params& P, int n) {
+    const Red h = red4(c[0].x, c[1].x, c[2].x, c[3].x);
+    const Red qx = red4(c[0].y, c[1].y, c[2].y, c[3].y);
+    const Red qy = red4(c[0].z, c[1].z, c[2].z, c[3].z);
+    const Red z = red4(c[0].w, c[1].w, c[2].w, c[3].w);
+    const double tau = P.tau[n];
+    Enc e;
+    e.par = make_double4(h.par, qx.par, qy.par, z.par);
+    e.flow = sig_q(h.dmax, P.smax[0], tau) || sig_q(qx.dmax, P.smax[1], tau) || sig_q(qy.dmax, P.smax[2], tau);
+    e.zflag = sig_q(z.dmax, P.smax[3], tau);
+    return e;
+}
+
+__device__ __forceinline__ bool active(const Ctl* c, const Params& P) {
+    return *((volatile const double*)&c->t) < P.t_end;
+}
+
+// Block-wide sum of unsigned values (256 threads).
+__device__ __forceinline__ unsigned block_sum(unsigned v, unsigned* scratch) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) scratch[w] = v;
+    __syncthreads();
+    unsigned s = 0;
+    if (threadIdx.x < 32) {
+        s = (l < kThreads / 32) ? scratch[l] : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+        if (l == 0) scratch[0] = s;
+    }
+    __syncthreads();
+    s = scratch[0];
+    __syncthreads();
+    return s;
+}
+// Block-wide exclusive scan (256 threads); returns prefix, *total = sum.
+__device__ __forceinline__ unsigned block_exscan(unsigned v, unsigned* scratch, unsigned* total) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(kFull, x, o);
+        if (l >= o) x += y;
+    }
+    __syncthreads();
+    if (l == 31) scratch[w] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        unsigned s = (l < kThreads / 32) ? scratch[l] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(kFull, s, o);
+            if (l >= o) s += y;
+        }
+        if (l < kThreads / 32) scratch[l] = s;  // inclusive warp totals
+    }
+    __syncthreads();
+    const unsigned warp_prefix = (w == 0) ? 0u : scratch[w - 1];
+    *total = scratch[kThreads / 32 - 1];
+    __syncthreads();
+    return warp_prefix + x - v;
+}
+
+// last-CTA election: every CTA fences its global writes, then bumps a counter
+__device__ __forceinline__ bool last_block(unsigned int* counter, int* s_flag) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(counter, 1u);
+        *s_flag = (prev == gridDim.x - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    const bool last = *s_flag != 0;
+    if (last) __threadfence();
+    return last;
+}
+
+// =========================================================================== K1
+// zero_details_and_reencode + significance
+// over the level-R subtree `blockIdx.x`; restricted to the previous tree (sig
+// prev), so off-tree cells only cost a flag read. INIT = full encode at t=0
+// (sig prev is all ones) and also derives the static DEM mask.
+template <bool INIT>
+__global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
+    if (!INIT && !active(ctl, P)) return;
+    extern __shared__ double4 sv[];
+    __shared__ unsigned s_red[32];
+    __shared__ int s_last;
+    const int p = ctl->parity;
+    double4* buf = P.cells[p];
+    const uint8_t* sigp = P.sig[p];
+    const int L = P.L, R = P.R, K = P.K;
+    const uint32_t j = blockIdx.x;
+    unsigned tree = 0;
+
+    // ---- finest level: 4 lanes per level-(L-1) parent, one child each
+    {
+        const int n = L - 1;
+        const uint32_t npar = 1u << (2 * (K - 1));
+        const uint32_t nchild = npar << 2;
+        const uint32_t pbase = j * npar;
+        const double tau = P.tau[n];
+        const bool store_smem = n > R;
+        for (uint32_t c0 = 0; c0 < nchild; c0 += kThreads) {
+            const uint32_t ci = c0 + threadIdx.x;
+            const bool valid = ci < nchild;
+            const uint32_t pi = ci >> 2;
+            const uint32_t pm = pbase + pi;
+            const bool sp = valid && (INIT || sigp[P.fbase[n] + pm]);
+            double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+            if (sp) v = ld4_nc(buf + P.base[L] + (static_cast<unsigned long long>(pm) << 2) + (ci & 3u));
+            const Red rh = red4_shfl(v.x);
+            const Red rx = red4_shfl(v.y);
+            const Red ry = red4_shfl(v.z);
+            Red rz;
+            if (INIT) rz = red4_shfl(v.w);
+            else rz.par = par_shfl(v.w), rz.dmax = 0.0;
+            if (valid && (ci & 3u) == 0u) {
+                double4 par = make_double4(0.0, 0.0, 0.0, 0.0);
+                bool flow;
+                if (sp) {
+                    par = make_double4(rh.par, rx.par, ry.par, rz.par);
+                    flow = sig_q(rh.dmax, P.smax[0], tau) || sig_q(rx.dmax, P.smax[1], tau) ||
+                           sig_q(ry.dmax, P.smax[2], tau);
+                    st4(buf + P.base[n] + pm, par);
+                    ++tree;
+                } else {
+                    flow = 0.0 >= tau;
+                    if (store_smem && sigp[P.fbase[n - 1] + (pm >> 2)]) par = ld4(buf + P.base[n] + pm);
+                }
+                uint8_t d;
+                if (INIT) {
+                    d = sig_q(rz.dmax, P.smax[3], tau) ? 1 : 0;
+                    P.dem[P.fbase[n] + pm] = d;
+                } else {
+                    d = P.dem[P.fbase[n] + pm];
+                }
+                P.pre[P.fbase[n] + pm] = (flow || d) ? 1 : 0;
+                if (store_smem) sv[lo(n, R) + pi] = par;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- levels L-2 .. R inside the subtree, children from shared memory
+    for (int n = L - 2; n >= R; --n) {
+        const uint32_t cnt = 1u << (2 * (n - R));
+        const uint32_t pb = j * cnt;
+        const bool store_smem = n > R;
+        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
+            const uint32_t pm = pb + pi;
+            const bool sp = INIT || sigp[P.fbase[n] + pm];
+            double4 par = make_double4(0.0, 0.0, 0.0, 0.0);
+            bool flow, zf = false;
+            if (sp) {
+                const uint32_t c0 = lo(n + 1, R) + 4u * pi;
+                const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
+                const Enc e = encode_children(c, P, n);
+                par = e.par;
+                flow = e.flow;
+                zf = e.zflag;
+                st4(buf + P.base[n] + pm, par);
+                ++tree;
+            } else {
+                flow = 0.0 >= P.tau[n];
+                if (store_smem && sigp[P.fbase[n - 1] + (pm >> 2)]) par = ld4(buf + P.base[n] + pm);
+            }
+            uint8_t d;
+            if (INIT) {
+                d = zf ? 1 : 0;
+                P.dem[P.fbase[n] + pm] = d;
+            } else {
+                d = P.dem[P.fbase[n] + pm];
+            }
+            P.pre[P.fbase[n] + pm] = (flow || d) ? 1 : 0;
+            if (store_smem) sv[lo(n, R) + pi] = par;
+        }
+        __syncthreads();
+    }
+
+    const unsigned tsum = block_sum(tree, s_red);
+    if (threadIdx.x == 0 && tsum) atomicAdd(&ctl->cnt_tree, (unsigned long long)tsum);
+    if (!last_block(&ctl->done_k1, &s_last)) return;
+
+    // ---- last CTA: levels R-1 .. 0, children from global (L2)
+    unsigned ttop = 0;
+    for (int n = R - 1; n >= 0; --n) {
+        const uint32_t cnt = 1u << (2 * n);
+        for (uint32_t pm = threadIdx.x; pm < cnt; pm += kThreads) {
+            const bool sp = INIT || sigp[P.fbase[n] + pm];
+            bool flow, zf = false;
+            if (sp) {
+                const double4* cp = buf + P.base[n + 1] + (static_cast<unsigned long long>(pm) << 2);
+                const double4 c[4] = {ld4_cg(cp), ld4_cg(cp + 1), ld4_cg(cp + 2), ld4_cg(cp + 3)};
+                const Enc e = encode_children(c, P, n);
+                flow = e.flow;
+                zf = e.zflag;
+                st4(buf + P.base[n] + pm, e.par);
+                ++ttop;
+            } else {
+                flow = 0.0 >= P.tau[n];
+            }
+            uint8_t d;
+            if (INIT) {
+                d = zf ? 1 : 0;
+                P.dem[P.fbase[n] + pm] = d;
+            } else {
+                d = P.dem[P.fbase[n] + pm];
+            }
+            P.pre[P.fbase[n] + pm] = (flow || d) ? 1 : 0;
+        }
+        __threadfence_block();
+        __syncthreads();
+    }
+    const unsigned tt = block_sum(ttop, s_red);
+    if (threadIdx.x == 0) {
+        if (tt) atomicAdd(&ctl->cnt_tree, (unsigned long long)tt);
+        ctl->done_k1 = 0;
+    }
+}
+
+// =========================================================================== K2
+// band (D3) of cell (n, m) from the pre-band flags (flow | DEM)
+__device__ __forceinline__ uint8_t band_flag(const Params& P, const uint8_t* pre, int n, uint32_t m) {
+    uint8_t b = pre[P.fbase[n] + m];
+    if (P.band_mode == 2) {
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const uint32_t nb = zo::neighbour_dev(n, m, static_cast<zo::Direction>(d));
+            if (nb != zo::kNone) b |= pre[P.fbase[n] + nb];
+        }
+    } else if (P.band_mode == 1 && n + 1 < P.L) {
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t c = 4u * m + static_cast<uint32_t>(k);
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+                const uint32_t nb = zo::neighbour_dev(n + 1, c, static_cast<zo::Direction>(d));
+                if (nb != zo::kNone) b |= pre[P.fbase[n + 1] + nb];
+            }
+        }
+    }
+    return b ? 1 : 0;
+}
+
+// band + ancestor closure per subtree; per-subtree leaf
+// count; the last CTA closes levels < R and scans subtree counts into the
+// leaf-list offsets (the PTT compaction's global scan, done once on 4^R
+// values instead of per finest cell).
+__global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force) {
+    if (!force && !active(ctl, P)) return;
+    extern __shared__ uint8_t sf[];
+    __shared__ unsigned s_red[32];
+    __shared__ int s_last;
+    const int p = ctl->parity;
+    uint8_t* sigc = P.sig[p ^ 1];
+    const uint8_t* pre = P.pre;
+    const int L = P.L, R = P.R, K = P.K;
+    const uint32_t j = blockIdx.x;
+
+    for (int n = R; n < L; ++n) {
+        const uint32_t cnt = 1u << (2 * (n - R));
+        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) sf[lo(n, R) + pi] = band_flag(P, pre, n, j * cnt + pi);
+    }
+    __syncthreads();
+    for (int n = L - 2; n >= R; --n) {
+        const uint32_t cnt = 1u << (2 * (n - R));
+        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
+            const uint32_t c = lo(n + 1, R) + 4u * pi;
+            if (sf[c] | sf[c + 1] | sf[c + 2] | sf[c + 3]) sf[lo(n, R) + pi] = 1;
+        }
+        __syncthreads();
+    }
+    for (int n = R; n < L; ++n) {
+        const uint32_t cnt = 1u << (2 * (n - R));
+        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) sigc[P.fbase[n] + j * cnt + pi] = sf[lo(n, R) + pi];
+    }
+    // leaves in this subtree assuming its root is reached by the traversal
+    {
+        const uint32_t nc = 1u << (2 * (K - 1));  // level-(L-1) cells in the subtree
+        unsigned cntl = 0;
+        for (uint32_t c = threadIdx.x; c < nc; c += kThreads) {
+            int n = R;
+            while (n < L && sf[lo(n, R) + (c >> (2 * (L - 1 - n)))]) ++n;
+            if (n == L) cntl += 4;
+            else cntl += ((c & ((1u << (2 * (L - 1 - n))) - 1u)) == 0u) ? 1u : 0u;
+        }
+        const unsigned tot = block_sum(cntl, s_red);
+        if (threadIdx.x == 0) P.tile_cnt[j] = tot;
+    }
+    if (!last_block(&ctl->done_k2, &s_last)) return;
+
+    // ---- last CTA: band + closure on levels R-1 .. 0
+    for (int n = R - 1; n >= 0; --n) {
+        const uint32_t cnt = 1u << (2 * n);
+        for (uint32_t m = threadIdx.x; m < cnt; m += kThreads) {
+            uint8_t b = band_flag(P, pre, n, m);
+            const uint8_t* c = sigc + P.fbase[n + 1] + 4u * m;
+            if (n + 1 < L && (ldcg_u8(c) | ldcg_u8(c + 1) | ldcg_u8(c + 2) | ldcg_u8(c + 3))) b = 1;
+            sigc[P.fbase[n] + m] = b;
+        }
+        __threadfence_block();
+        __syncthreads();
+    }
+    // ---- final per-subtree counts and their exclusive scan
+    const uint32_t nt = static_cast<uint32_t>(P.n_tiles);
+    const uint32_t per = (nt + kThreads - 1) / kThreads;
+    const uint32_t a = threadIdx.x * per;
+    const uint32_t b = min(nt, a + per);
+    unsigned local = 0;
+    for (uint32_t t = a; t < b; ++t) {
+        int n = 0;
+        while (n < R && ldcg_u8(sigc + P.fbase[n] + (t >> (2 * (R - n))))) ++n;
+        unsigned c;
+        if (n == R) c = ldcg_u32(P.tile_cnt + t);
+        else c = ((t & ((1u << (2 * (R - n))) - 1u)) == 0u) ? 1u : 0u;
+        P.tile_off[t] = c;  // temporarily the count
+        local += c;
+    }
+    unsigned total;
+    unsigned off = block_exscan(local, s_red, &total);
+    for (uint32_t t = a; t < b; ++t) {
+        const unsigned c = P.tile_off[t];
+        P.tile_off[t] = off;
+        off += c;
+    }
+    if (threadIdx.x == 0) {
+        ctl->n_leaves = total;
+        ctl->done_k2 = 0;
+    }
+}
+
+// =========================================================================== K3
+// decode_tree under D4 + PTT (Alg. 5) +
+// compact_leaves. In physical units a zero-detail decode is
+// a copy of the parent's (h, qx, qy) to its children, so a cell
+// below a chain of newly significant cells takes the value of the chain's top.
+__device__ __forceinline__ void write_projection(double4* buf, const Params& P, int n, uint32_t m, uint32_t src) {
+    const int ns = zo::level_of(src);
+    const double4 v = ld4_cg(buf + P.base[ns] + (src - zo::level_offset(ns)));
+    double4* dst = buf + P.base[n] + m;
+    const double4 old = ld4_cg(dst);
+    st4(dst, make_double4(v.x, v.y, v.z, old.w));
+}
+
+__global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int force) {
+    if (!force && !active(ctl, P)) return;
+    extern __shared__ uint32_t smem3[];
+    __shared__ unsigned s_red[32];
+    __shared__ int s_reached, s_leafn;
+    __shared__ uint32_t s_rootsrc;
+    const int p = ctl->parity;
+    double4* buf = P.cells[p];
+    const uint8_t* sigc = P.sig[p ^ 1];
+    const uint8_t* sigp = P.sig[p];
+    const int L = P.L, R = P.R, K = P.K;
+    const uint32_t j = blockIdx.x;
+    const uint32_t ncell = ((1u << (2 * K)) - 1u) / 3u;  // subtree cells on levels R..L-1
+    uint32_t* src = smem3;                               // [ncell]
+    uint8_t* sc = reinterpret_cast<uint8_t*>(src + ncell);  // [ncell]
+    uint8_t* sp = sc + ncell;                               // [ncell]
+
+    for (int n = R; n < L; ++n) {
+        const uint32_t cnt = 1u << (2 * (n - R));
+        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
+            sc[lo(n, R) + pi] = sigc[P.fbase[n] + j * cnt + pi];
+            sp[lo(n, R) + pi] = sigp[P.fbase[n] + j * cnt + pi];
+        }
+    }
+    if (threadIdx.x == 0) {
+        int reached = 1, leafn = R;
+        uint32_t s = kNoSrc;
+        for (int n = 0; n < R; ++n) {
+            const uint32_t a = j >> (2 * (R - n));
+            if (!sigc[P.fbase[n] + a]) {
+                reached = 0;
+                leafn = n;
+                break;
+            }
+            if (s == kNoSrc && !sigp[P.fbase[n] + a]) s = zo::z_of(n, a);
+        }
+        s_reached = reached;
+        s_leafn = leafn;
+        s_rootsrc = s;
+    }
+    __syncthreads();
+    const bool reached = s_reached != 0;
+    unsigned nnew = 0;
+
+    // ---- top levels 1 .. R-1 are projected by CTA 0 (each cell walks its chain)
+    if (j == 0) {
+        for (int n = 1; n < R; ++n) {
+            const uint32_t cnt = 1u << (2 * n);
+            for (uint32_t m = threadIdx.x; m < cnt; m += kThreads) {
+                uint32_t s = kNoSrc;
+                bool ok = true;
+                for (int k = 0; k < n; ++k) {
+                    const uint32_t a = m >> (2 * (n - k));
+                    if (!sigc[P.fbase[k] + a]) { ok = false; break; }
+                    if (s == kNoSrc && !sigp[P.fbase[k] + a]) s = zo::z_of(k, a);
+                }
+                if (ok && s != kNoSrc) write_projection(buf, P, n, m, s);
+            }
+        }
+        for (int n = 0; n < R; ++n) {
+            const uint32_t cnt = 1u << (2 * n);
+            for (uint32_t m = threadIdx.x; m < cnt; m += kThreads)
+                nnew += (sigc[P.fbase[n] + m] && !sigp[P.fbase[n] + m]) ? 1u : 0u;
+        }
+    }
+
+    if (reached) {
+        // ---- projection inside the subtree, top-down
+        if (threadIdx.x == 0) {
+            src[0] = s_rootsrc;
+            if (s_rootsrc != kNoSrc) write_projection(buf, P, R, j, s_rootsrc);
+        }
+        __syncthreads();
+        for (int n = R; n < L; ++n) {
+            const uint32_t cnt = 1u << (2 * (n - R));
+            for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
+                const uint32_t li = lo(n, R) + pi;
+                const uint32_t pm = j * cnt + pi;
+                const bool isnew = sc[li] && !sp[li];
+                nnew += isnew ? 1u : 0u;
+                uint32_t cs = kNoSrc;
+                if (sc[li]) cs = (src[li] != kNoSrc) ? src[li] : (isnew ? zo::z_of(n, pm) : kNoSrc);
+                if (n + 1 < L) {
+                    const uint32_t lc = lo(n + 1, R) + 4u * pi;
+                    src[lc] = cs; src[lc + 1] = cs; src[lc + 2] = cs; src[lc + 3] = cs;
+                }
+                if (cs != kNoSrc)
+                    for (uint32_t k = 0; k < 4; ++k) write_projection(buf, P, n + 1, 4u * pm + k, cs);
+            }
+            __syncthreads();
+        }
+    }
+    {
+        const unsigned tn = block_sum(nnew, s_red);
+        if (threadIdx.x == 0 && tn) atomicAdd(&ctl->cnt_new, (unsigned long long)tn);
+    }
+
+    // ---- PTT + compaction into leaves[tile_off[j] ...]
+    const uint32_t base_out = P.tile_off[j];
+    if (!reached) {
+        const int n = s_leafn;
+        if (threadIdx.x == 0 && ((j & ((1u << (2 * (R - n))) - 1u)) == 0u))
+            P.leaves[base_out] = zo::z_of(n, j >> (2 * (R - n)));
+        return;
+    }
+    const uint32_t nc = 1u << (2 * (K - 1));  // level-(L-1) cells in the subtree
+    const uint32_t per = (nc + kThreads - 1) / kThreads;
+    const uint32_t a = threadIdx.x * per;
+    const uint32_t b = min(nc, a + per);
+    unsigned cntl = 0;
+    for (uint32_t c = a; c < b; ++c) {
+        int n = R;
+        while (n < L && sc[lo(n, R) + (c >> (2 * (L - 1 - n)))]) ++n;
+        if (n == L) cntl += 4;
+        else cntl += ((c & ((1u << (2 * (L - 1 - n))) - 1u)) == 0u) ? 1u : 0u;
+    }
+    unsigned total;
+    uint32_t o = base_out + block_exscan(cntl, s_red, &total);
+    const uint32_t gbase = j * nc;
+    for (uint32_t c = a; c < b; ++c) {
+        int n = R;
+        while (n < L && sc[lo(n, R) + (c >> (2 * (L - 1 - n)))]) ++n;
+        const uint32_t gm = gbase + c;
+        if (n == L) {
+            const uint32_t z0 = zo::z_of(L, gm << 2);
+            P.leaves[o] = z0; P.leaves[o + 1] = z0 + 1; P.leaves[o + 2] = z0 + 2; P.leaves[o + 3] = z0 + 3;
+            o += 4;
+        } else if ((c & ((1u << (2 * (L - 1 - n))) - 1u)) == 0u) {
+            P.leaves[o++] = zo::z_of(n, gm >> (2 * (L - 1 - n)));
+        }
+    }
+}
+
+// =========================================================================== K5
+__device__ __forceinline__ double series_value(const Params& P, double t) {
+    const int n = P.inflow_n;
+    if (n <= 0) return 0.0;
+    const double* ts = P.inflow_t;
+    const double* vs = P.inflow_v;
+    if (t <= ts[0]) return vs[0];
+    if (t >= ts[n - 1]) return vs[n - 1];
+    int k = 0;
+    while (k + 1 < n && ts[k + 1] <= t) ++k;
+    return vs[k] + ((vs[k + 1] - vs[k]) * ((t - ts[k]) / (ts[k + 1] - ts[k])));
+}
+
+// next dt from the CFL minimum (D13), clipped to the next
+// output time / t_end; `advance` also commits the step (t, parity, counters).
+__device__ void finalize_dt(const Params& P, Ctl* ctl, double mincell, bool advance) {
+    const double t_new = advance ? ctl->t_next : ctl->t;
+    const bool dry = __double_as_longlong(mincell) == 0x7FF0000000000000ll;
+    const double dtc = dry ? P.dt_fallback : P.cfl * mincell;
+    double stop = P.t_end;
+    for (int k = 0; k < P.n_out; ++k) {
+        const double o = P.out_times[k];
+        if (o > t_new && o < stop) stop = o;
+    }
+    double dt, tn;
+    if (t_new + dtc >= stop) {
+        dt = stop - t_new;
+        tn = stop;
+    } else {
+        dt = dtc;
+        tn = t_new + dtc;
+    }
+    if (t_new < P.t_end && !(dt > 0.0 && isfinite(dt))) report_error(ctl, kErrDt, 0, 0, kStageDt);
+    if (advance) {
+        ctl->dt_used = ctl->dt;
+        ctl->t = t_new;
+        ctl->step += 1;
+        ctl->parity ^= 1;
+        ctl->n_leaves_used = ctl->n_leaves;
+    }
+    ctl->dt = dt;
+    ctl->t_next = tn;
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(kFull, v, o);
+        v = y < v ? y : v;
+    }
+    return v;
+}
+
+// reduce the per-thread CFL minima, publish, and let the last CTA finish
+__device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ctl, double mn, bool advance) {
+    __shared__ unsigned long long s_min[kThreads / 32];
+    __shared__ int s_last;
+    unsigned long long b = warp_min_u64(static_cast<unsigned long long>(__double_as_longlong(mn)));
+    if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long m = s_min[0];
+        for (int w = 1; w < kThreads / 32; ++w) m = s_min[w] < m ? s_min[w] : m;
+        atomicMin(&ctl->dtmin_bits, m);
+    }
+    if (!last_block(&ctl->done_k5, &s_last)) return;
+    if (threadIdx.x == 0) {
+        const unsigned long long m = atomicAdd(&ctl->dtmin_bits, 0ull);
+        finalize_dt(P, ctl, __longlong_as_double(static_cast<long long>(m)), advance);
+        ctl->dtmin_bits = 0x7FF0000000000000ull;
+        ctl->done_k5 = 0;
+    }
+}
+
+// covering cell of the same-level neighbour region (n, nb): walk up until the
+// parent is significant (SPEC.md:248 — the level-min(n, covering-leaf) cell)
+__device__ __forceinline__ unsigned long long covering(const Params& P, const uint8_t* sigc, int n, uint32_t nb) {
+    int k = n;
+    uint32_t mm = nb;
+    while (k > 0 && !sigc[P.fbase[k - 1] + (mm >> 2)]) {
+        mm >>= 2;
+        --k;
+    }
+    return P.base[k] + mm;
+}
+
+// FV1 over the leaf list: persistent grid-stride, one thread per
+// leaf; reads the current buffer, writes leaf slots of the other (D15).
+template <bool UNIFORM>
+__global__ void __launch_bounds__(kThreads) k_fv1(Params P, Ctl* ctl) {
+    if (!active(ctl, P)) return;
+    const int p = ctl->parity;
+    const double4* __restrict__ cur = P.cells[p];
+    double4* __restrict__ nxt = P.cells[p ^ 1];
+    const uint8_t* __restrict__ sigc = P.sig[p ^ 1];
+    const uint32_t N = UNIFORM ? (1u << (2 * P.L)) : ctl->n_leaves;
+    const double t = ctl->t, dt = ctl->dt;
+    const double inflow = series_value(P, t);
+    double mn = __longlong_as_double(0x7FF0000000000000ll);
+    for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < N; i += gridDim.x * kThreads) {
+        int n;
+        uint32_t m;
+        if (UNIFORM) {
+            n = P.L;
+            m = i;
+        } else {
+            const uint32_t z = P.leaves[i];
+            n = zo::level_of(z);
+            m = z - zo::level_offset(n);
+        }
+        const double4 own = ld4_nc(cur + P.base[n] + m);
+        double4 nb[4];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const uint32_t nm = zo::neighbour_dev(n, m, static_cast<zo::Direction>(d));
+            if (nm == zo::kNone) {
+                nb[d] = boundary_state(own, P.bc[d], d, inflow, P.inflow_mode, P.phys.hdry);
+            } else {
+                const unsigned long long off = UNIFORM ? (P.base[n] + nm) : covering(P, sigc, n, nm);
+                nb[d] = ld4_nc(cur + off);
+            }
+        }
+        double hn, qxn, qyn;
+        const double dx = P.dx[n];
+        fv1_cell(own, nb, dx, dt, P.phys, hn, qxn, qyn);
+        if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))
+            report_error(ctl, kErrNonFinite, zo::z_of(n, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2), kStageFV1);
+        st4(nxt + P.base[n] + m, make_double4(hn, qxn, qyn, own.w));
+        const double c = cfl_cell(hn, qxn, qyn, dx, P.phys);
+        mn = c < mn ? c : mn;
+    }
+    cfl_reduce_and_finalize(P, ctl, mn, true);
+}
+
+// dt at initialise: CFL over the initial leaves, no update.
+__global__ void __launch_bounds__(kThreads) k_cfl_init(Params P, Ctl* ctl, int uniform) {
+    const int p = ctl->parity;
+    const double4* cur = P.cells[p];
+    const uint32_t N = uniform ? (1u << (2 * P.L)) : ctl->n_leaves;
+    double mn = __longlong_as_double(0x7FF0000000000000ll);
+    for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < N; i += gridDim.x * kThreads) {
+        int n;
+        uint32_t m;
+        if (uniform) {
+            n = P.L;
+            m = i;
+        } else {
+            const uint32_t z = P.leaves[i];
+            n = zo::level_of(z);
+            m = z - zo::level_offset(n);
+        }
+        const double4 v = ld4(cur + P.base[n] + m);
+        const double c = cfl_cell(v.x, v.y, v.z, P.dx[n], P.phys);
+        mn = c < mn ? c : mn;
+    }
+    cfl_reduce_and_finalize(P, ctl, mn, false);
+}
+
+// =========================================================== import / export
+// initial discretisation: row-major (south row first) finest
+// fields -> Morton slots of level L; s_max per quantity.
+__global__ void __launch_bounds__(kThreads) k_import(Params P, Ctl* ctl, const double* h, const double* qx,
+                                                     const double* qy, const double* z, int buffer) {
+    const uint32_t side = 1u << P.L;
+    const uint64_t total = static_cast<uint64_t>(side) * side;
+    double mx[4] = {0.0, 0.0, 0.0, 0.0};
+    for (uint64_t r = blockIdx.x * (uint64_t)kThreads + threadIdx.x; r < total; r += (uint64_t)gridDim.x * kThreads) {
+        const uint32_t i = static_cast<uint32_t>(r & (side - 1)), jj = static_cast<uint32_t>(r >> P.L);
+        const uint32_t m = zo::interleave(i, jj);
+        const double4 v = make_double4(h[r], qx[r], qy[r], z[r]);
+        if (!(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w)))
+            report_error(ctl, kErrNonFinite, zo::z_of(P.L, m), 0, kStageImport);
+        st4(P.cells[buffer] + P.base[P.L] + m, v);
+        mx[0] = max2(mx[0], absd(v.x));
+        mx[1] = max2(mx[1], absd(v.y));
+        mx[2] = max2(mx[2], absd(v.z));
+        mx[3] = max2(mx[3], absd(v.w));
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(mx[q]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(kFull, b, o);
+            b = y > b ? y : b;
+        }
+        if ((threadIdx.x & 31) == 0) atomicMax(&ctl->smax_bits[q], b);
+    }
+}
+
+// hierarchy export in z-index order, s-units (s = p * 2^(L-n)); leaves from
+// the current buffer, significant cells from the other; off-tree cells NaN.
+__global__ void k_export_tree(Params P, const Ctl* ctl, double* h, double* qx, double* qy, double* z, uint8_t* sig) {
+    const int p = ctl->parity;
+    const uint8_t* sigc = P.sig[p];
+    const uint32_t total = zo::level_offset(P.L + 1);
+    for (uint32_t zi = blockIdx.x * kThreads + threadIdx.x; zi < total; zi += gridDim.x * kThreads) {
+        const int n = zo::level_of(zi);
+        const uint32_t m = zi - zo::level_offset(n);
+        if (n < P.L) sig[zi] = sigc[P.fbase[n] + m];
+        const bool in_tree = (n == 0) || sigc[P.fbase[n - 1] + (m >> 2)];
+        const bool is_sig = (n < P.L) && sigc[P.fbase[n] + m];
+        const double nan = __longlong_as_double(0x7FF8000000000000ll);
+        double4 v = make_double4(nan, nan, nan, nan);
+        if (in_tree) v = ld4(P.cells[is_sig ? (p ^ 1) : p] + P.base[n] + m);
+        const double sc = ldexp(1.0, P.L - n);
+        h[zi] = v.x * sc;
+        qx[zi] = v.y * sc;
+        qy[zi] = v.z * sc;
+        z[zi] = v.w * sc;
+    }
+}
+
+// neighbour descriptors of the current leaf list
+__global__ void k_descriptors(Params P, const Ctl* ctl, uint32_t* nbr, uint32_t N) {
+    const int p = ctl->parity;
+    const uint8_t* sigc = P.sig[p];
+    for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < N; i += gridDim.x * kThreads) {
+        const uint32_t z = P.leaves[i];
+        const int n = zo::level_of(z);
+        const uint32_t m = z - zo::level_offset(n);
+        for (int d = 0; d < 4; ++d) {
+            const uint32_t nm = zo::neighbour_dev(n, m, static_cast<zo::Direction>(d));
+            uint32_t desc;
+            if (nm == zo::kNone) {
+                desc = 0xFFFFFFF0u + static_cast<uint32_t>(P.bc[d]);
+            } else {
+                int k = n;
+                uint32_t mm = nm;
+                while (k > 0 && !sigc[P.fbase[k - 1] + (mm >> 2)]) {
+                    mm >>= 2;
+                    --k;
+                }
+                desc = zo::z_of(k, mm);
+            }
+            nbr[static_cast<uint64_t>(d) * N + i] = desc;
+        }
+    }
+}
+
+// zero-detail expansion to the finest grid: physical,
+// row-major south row first
+__global__ void k_export_finest(Params P, const Ctl* ctl, double* h, double* qx, double* qy) {
+    const int p = ctl->parity;
+    const uint8_t* sigc = P.sig[p];
+    const uint32_t side = 1u << P.L;
+    const uint64_t total = static_cast<uint64_t>(side) * side;
+    for (uint64_t r = blockIdx.x * (uint64_t)kThreads + threadIdx.x; r < total; r += (uint64_t)gridDim.x * kThreads) {
+        const uint32_t i = static_cast<uint32_t>(r & (side - 1)), jj = static_cast<uint32_t>(r >> P.L);
+        const uint32_t m = zo::interleave(i, jj);
+        int n = 0;
+        while (n < P.L && sigc[P.fbase[n] + (m >> (2 * (P.L - n)))]) ++n;
+        const double4 v = ld4(P.cells[p] + P.base[n] + (m >> (2 * (P.L - n))));
+        h[r] = v.x;
+        qx[r] = v.y;
+        qy[r] = v.z;
+    }
+}
+
+}  // namespace hwfv1

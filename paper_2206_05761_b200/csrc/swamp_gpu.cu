@@ -1,0 +1,508 @@
+// swamp_gpu.cu — host side of the C-ABI (include/swamp_gpu.h): owns device
+// memory, sequences the sm_100a kernels of hwfv1_kernels.cuh, captures one
+// adaptive step (K1 -> K2 -> K3 -> K5) as a CUDA graph and replays it.
+//
+// Boundary: replaces the reference's engine operations initialise /
+// step_adaptive / step_uniform / run for the adaptive
+// time-step loop. No CPU fallback: every compute path is a CUDA kernel; a
+// missing device is an error.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hwfv1_kernels.cuh"
+#include "swamp_gpu.h"
+
+using hwfv1::Ctl;
+using hwfv1::kThreads;
+using hwfv1::Params;
+
+namespace {
+
+constexpr int kGraphSteps = 8;
+
+struct Mem {
+    void* p = nullptr;
+    ~Mem() {
+        if (p) cudaFree(p);
+    }
+};
+
+}  // namespace
+
+struct swamp_gpu {
+    int device = 0;
+    bool uniform = false;
+    bool profiling = false;
+    cudaStream_t stream = nullptr;
+    Params P{};
+    Ctl* ctl = nullptr;      // device
+    Ctl* ctl_host = nullptr; // pinned mirror
+    std::vector<void*> allocs;
+    cudaGraphExec_t graph1 = nullptr, graphS = nullptr;
+    int fv1_grid = 0;
+    int num_sms = 0;
+    size_t smem_k1 = 0, smem_k2 = 0, smem_k3 = 0;
+    cudaEvent_t ev[6] = {};
+    std::string err;
+    int64_t n_cells = 0;
+
+    ~swamp_gpu() {
+        if (graph1) cudaGraphExecDestroy(graph1);
+        if (graphS) cudaGraphExecDestroy(graphS);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        for (void* a : allocs) cudaFree(a);
+        if (ctl_host) cudaFreeHost(ctl_host);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+#define CK(call)                                                                      \
+    do {                                                                              \
+        cudaError_t e_ = (call);                                                      \
+        if (e_ != cudaSuccess) {                                                      \
+            if (g) g->err = std::string(#call) + ": " + cudaGetErrorString(e_);       \
+            return SWAMP_E_CUDA;                                                      \
+        }                                                                             \
+    } while (0)
+
+namespace {
+
+template <class T>
+int dalloc(swamp_gpu* g, T** out, size_t bytes) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 16));
+    if (e != cudaSuccess) {
+        g->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+        return SWAMP_E_NOMEM;
+    }
+    g->allocs.push_back(p);
+    *out = static_cast<T*>(p);
+    return SWAMP_OK;
+}
+
+int validate(const swamp_config* c) {
+    if (!c) return SWAMP_E_ARG;
+    if (c->L < 1 || c->L > 13) return SWAMP_E_ARG;
+    if (!(c->epsilon >= 0.0) || !(c->width > 0.0) || !(c->cfl > 0.0 && c->cfl <= 1.0)) return SWAMP_E_ARG;
+    if (!(c->h_dry > 0.0) || !(c->g > 0.0) || !(c->manning >= 0.0) || !(c->dt_fallback > 0.0)) return SWAMP_E_ARG;
+    for (int k = 0; k < 4; ++k)
+        if (c->bc[k] < 0 || c->bc[k] > 2) return SWAMP_E_ARG;
+    if (c->band_mode < 0 || c->band_mode > 2) return SWAMP_E_ARG;
+    if (c->inflow_n < 0 || (c->inflow_n > 0 && (!c->inflow_t || !c->inflow_v))) return SWAMP_E_ARG;
+    if (c->n_outputs < 0 || (c->n_outputs > 0 && !c->output_times)) return SWAMP_E_ARG;
+    return SWAMP_OK;
+}
+
+void launch_step_kernels(swamp_gpu* g, bool timed) {
+    Params& P = g->P;
+    cudaStream_t s = g->stream;
+    if (timed) cudaEventRecord(g->ev[0], s);
+    if (g->uniform) {
+        hwfv1::k_fv1<true><<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl);
+        if (timed) for (int k = 1; k < 5; ++k) cudaEventRecord(g->ev[k], s);
+        return;
+    }
+    hwfv1::k_encode<false><<<P.n_tiles, kThreads, g->smem_k1, s>>>(P, g->ctl);
+    if (timed) cudaEventRecord(g->ev[1], s);
+    hwfv1::k_band<<<P.n_tiles, kThreads, g->smem_k2, s>>>(P, g->ctl, 0);
+    if (timed) cudaEventRecord(g->ev[2], s);
+    hwfv1::k_traverse<<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 0);
+    if (timed) cudaEventRecord(g->ev[3], s);
+    hwfv1::k_fv1<false><<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl);
+    if (timed) cudaEventRecord(g->ev[4], s);
+}
+
+int build_graphs(swamp_gpu* g) {
+    for (int which = 0; which < 2; ++which) {
+        const int steps = which == 0 ? 1 : kGraphSteps;
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
+        for (int k = 0; k < steps; ++k) launch_step_kernels(g, false);
+        CK(cudaStreamEndCapture(g->stream, &graph));
+        cudaGraphExec_t exec;
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+        cudaGraphDestroy(graph);
+        (which == 0 ? g->graph1 : g->graphS) = exec;
+    }
+    return SWAMP_OK;
+}
+
+int fetch_ctl(swamp_gpu* g) {
+    CK(cudaMemcpyAsync(g->ctl_host, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    if (g->ctl_host->err_code != 0) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "device error %d at z=%u quantity=%d stage=%d", g->ctl_host->err_code,
+                      g->ctl_host->err_z, g->ctl_host->err_q, g->ctl_host->err_stage);
+        g->err = buf;
+        return g->ctl_host->err_code;
+    }
+    return SWAMP_OK;
+}
+
+void fill_report(const swamp_gpu* g, swamp_step_report* r) {
+    if (!r) return;
+    const Ctl& c = *g->ctl_host;
+    std::memset(r, 0, sizeof(*r));
+    r->step = c.step;
+    r->t = c.t;
+    r->dt = c.dt;
+    r->dt_used = c.dt_used;
+    r->n_leaves = g->uniform ? (int64_t(1) << (2 * g->P.L)) : c.n_leaves_used;
+    r->n_leaves_next = g->uniform ? r->n_leaves : c.n_leaves;
+}
+
+int create_impl(const swamp_config* cfg, const double* h, const double* qx, const double* qy, const double* z,
+                int device, bool uniform, swamp_gpu** out) {
+    if (!out || !h || !qx || !qy || !z) return SWAMP_E_ARG;
+    *out = nullptr;
+    int st = validate(cfg);
+    if (st) return st;
+    auto* g = new swamp_gpu();
+    g->device = device;
+    g->uniform = uniform;
+    auto fail = [&](int code) {
+        delete g;
+        return code;
+    };
+    if (cudaSetDevice(device) != cudaSuccess) return fail(SWAMP_E_CUDA);
+    if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(SWAMP_E_CUDA);
+    for (auto& e : g->ev)
+        if (cudaEventCreate(&e) != cudaSuccess) return fail(SWAMP_E_CUDA);
+    cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
+
+    Params& P = g->P;
+    const int L = cfg->L;
+    P.L = L;
+    P.K = std::min(L, 6);
+    P.R = L - P.K;
+    P.n_tiles = 1 << (2 * P.R);
+    P.band_mode = cfg->band_mode;
+    for (int k = 0; k < 4; ++k) P.bc[k] = cfg->bc[k];
+    P.inflow_mode = cfg->inflow_mode;
+    P.inflow_n = cfg->inflow_n;
+    P.n_out = cfg->n_outputs;
+    P.W = cfg->width;
+    P.cfl = cfg->cfl;
+    P.t_end = cfg->t_end;
+    P.dt_fallback = cfg->dt_fallback;
+    P.phys.g = cfg->g;
+    P.phys.half_g = 0.5 * cfg->g;
+    P.phys.hdry = cfg->h_dry;
+    P.phys.nM = cfg->manning;
+    P.phys.g_nM2 = cfg->g * (cfg->manning * cfg->manning);
+    for (int n = 0; n <= L; ++n) P.dx[n] = std::ldexp(cfg->width, -n);
+    // level layout: each level's slice rounded up to 8 cells (256 B)
+    unsigned long long off = 0, foff = 0;
+    for (int n = 0; n <= L; ++n) {
+        P.base[n] = off;
+        off += ((1ull << (2 * n)) + 7ull) & ~7ull;
+    }
+    for (int n = 0; n < L; ++n) {
+        P.fbase[n] = foff;
+        foff += ((1ull << (2 * n)) + 15ull) & ~15ull;
+    }
+    g->n_cells = static_cast<int64_t>(off);
+    const size_t nf = static_cast<size_t>(1) << (2 * L);
+    if ((st = dalloc(g, &P.cells[0], off * sizeof(double4)))) return fail(st);
+    if ((st = dalloc(g, &P.cells[1], off * sizeof(double4)))) return fail(st);
+    if ((st = dalloc(g, &P.sig[0], foff))) return fail(st);
+    if ((st = dalloc(g, &P.sig[1], foff))) return fail(st);
+    if ((st = dalloc(g, &P.pre, foff))) return fail(st);
+    if ((st = dalloc(g, &P.dem, foff))) return fail(st);
+    if ((st = dalloc(g, &P.leaves, nf * sizeof(uint32_t)))) return fail(st);
+    if ((st = dalloc(g, &P.tile_cnt, P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    if ((st = dalloc(g, &P.tile_off, P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    if ((st = dalloc(g, &g->ctl, sizeof(Ctl)))) return fail(st);
+    if (cudaMallocHost(&g->ctl_host, sizeof(Ctl)) != cudaSuccess) return fail(SWAMP_E_NOMEM);
+    double *d_it = nullptr, *d_iv = nullptr, *d_out = nullptr;
+    if ((st = dalloc(g, &d_it, sizeof(double) * std::max(1, cfg->inflow_n)))) return fail(st);
+    if ((st = dalloc(g, &d_iv, sizeof(double) * std::max(1, cfg->inflow_n)))) return fail(st);
+    if ((st = dalloc(g, &d_out, sizeof(double) * std::max(1, cfg->n_outputs)))) return fail(st);
+    cudaStream_t s = g->stream;
+    if (cfg->inflow_n > 0) {
+        cudaMemcpyAsync(d_it, cfg->inflow_t, sizeof(double) * cfg->inflow_n, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(d_iv, cfg->inflow_v, sizeof(double) * cfg->inflow_n, cudaMemcpyHostToDevice, s);
+    }
+    if (cfg->n_outputs > 0)
+        cudaMemcpyAsync(d_out, cfg->output_times, sizeof(double) * cfg->n_outputs, cudaMemcpyHostToDevice, s);
+    P.inflow_t = d_it;
+    P.inflow_v = d_iv;
+    P.out_times = d_out;
+
+    // control block
+    Ctl c0{};
+    c0.dtmin_bits = 0x7FF0000000000000ull;
+    std::memcpy(g->ctl_host, &c0, sizeof(Ctl));
+    if (cudaMemcpyAsync(g->ctl, g->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return fail(SWAMP_E_CUDA);
+
+    // upload + import (the staging buffer is released right after)
+    {
+        double* stage = nullptr;
+        if (cudaMalloc(&stage, 4 * nf * sizeof(double)) != cudaSuccess) return fail(SWAMP_E_NOMEM);
+        const double* src[4] = {h, qx, qy, z};
+        for (int q = 0; q < 4; ++q)
+            cudaMemcpyAsync(stage + q * nf, src[q], nf * sizeof(double), cudaMemcpyHostToDevice, s);
+        const int grid = std::max(1, std::min<int>(g->num_sms * 8, static_cast<int>((nf + kThreads - 1) / kThreads)));
+        hwfv1::k_import<<<grid, kThreads, 0, s>>>(P, g->ctl, stage, stage + nf, stage + 2 * nf, stage + 3 * nf, 0);
+        cudaError_t e = cudaStreamSynchronize(s);
+        cudaFree(stage);
+        if (e != cudaSuccess) {
+            g->err = cudaGetErrorString(e);
+            return fail(SWAMP_E_CUDA);
+        }
+    }
+    if (cudaMemcpy(g->ctl_host, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost) != cudaSuccess) return fail(SWAMP_E_CUDA);
+    if (g->ctl_host->err_code) return fail(SWAMP_E_NONFINITE);
+    for (int q = 0; q < 4; ++q) {
+        unsigned long long b = g->ctl_host->smax_bits[q];
+        std::memcpy(&P.smax[q], &b, 8);
+    }
+    // significance threshold in physical units: eps * 2^(2n-2L+2) (D7)
+    for (int n = 0; n < L; ++n) P.tau[n] = std::ldexp(cfg->epsilon, 2 * n - 2 * L + 2);
+
+    g->smem_k1 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u) * sizeof(double4);
+    g->smem_k2 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u);
+    g->smem_k3 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u) * 6;
+    {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false>, kThreads, 0);
+        g->fv1_grid = std::max(1, occ) * g->num_sms;
+    }
+
+    if (uniform) {
+        // full tree, no MRA: every detail cell significant
+        cudaMemsetAsync(P.sig[0], 1, foff, s);
+        cudaMemsetAsync(P.sig[1], 1, foff, s);
+        cudaMemsetAsync(P.pre, 1, foff, s);
+        // leaf list = every finest cell in Morton order (for exports)
+        hwfv1::k_band<<<P.n_tiles, kThreads, g->smem_k2, s>>>(P, g->ctl, 1);
+        hwfv1::k_traverse<<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 1);
+        cudaMemcpyAsync(P.cells[1], P.cells[0], off * sizeof(double4), cudaMemcpyDeviceToDevice, s);
+        hwfv1::k_cfl_init<<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl, 1);
+    } else {
+        // initialise: previous tree := everything, full
+        // encode + DEM mask, band + closure, traversal; no decode at t = 0
+        cudaMemsetAsync(P.sig[0], 1, foff, s);
+        hwfv1::k_encode<true><<<P.n_tiles, kThreads, g->smem_k1, s>>>(P, g->ctl);
+        hwfv1::k_band<<<P.n_tiles, kThreads, g->smem_k2, s>>>(P, g->ctl, 1);
+        hwfv1::k_traverse<<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 1);
+        // both buffers hold the full hierarchy; the current tree becomes "previous"
+        cudaMemcpyAsync(P.cells[1], P.cells[0], off * sizeof(double4), cudaMemcpyDeviceToDevice, s);
+        const int one = 1;
+        cudaMemcpyAsync(&g->ctl->parity, &one, sizeof(int), cudaMemcpyHostToDevice, s);
+        hwfv1::k_cfl_init<<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl, 0);
+    }
+    {
+        cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+            g->err = cudaGetErrorString(e);
+            return fail(SWAMP_E_CUDA);
+        }
+        if (cudaGetLastError() != cudaSuccess) return fail(SWAMP_E_CUDA);
+    }
+    if ((st = fetch_ctl(g))) return fail(st);
+    if ((st = build_graphs(g))) return fail(st);
+    *out = g;
+    return SWAMP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int swamp_gpu_create(const swamp_config* cfg, const double* h, const double* qx, const double* qy, const double* z,
+                     int device, swamp_gpu** out) {
+    return create_impl(cfg, h, qx, qy, z, device, false, out);
+}
+
+int swamp_gpu_create_uniform(const swamp_config* cfg, const double* h, const double* qx, const double* qy,
+                             const double* z, int device, swamp_gpu** out) {
+    return create_impl(cfg, h, qx, qy, z, device, true, out);
+}
+
+int swamp_gpu_destroy(swamp_gpu* g) {
+    if (!g) return SWAMP_E_ARG;
+    cudaSetDevice(g->device);
+    delete g;
+    return SWAMP_OK;
+}
+
+int swamp_gpu_set_profiling(swamp_gpu* g, int enabled) {
+    if (!g) return SWAMP_E_ARG;
+    g->profiling = enabled != 0;
+    return SWAMP_OK;
+}
+
+int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep) {
+    if (!g) return SWAMP_E_ARG;
+    cudaSetDevice(g->device);
+    if (g->profiling) {
+        launch_step_kernels(g, true);
+        CK(cudaGetLastError());
+    } else {
+        CK(cudaGraphLaunch(g->graph1, g->stream));
+    }
+    int st = fetch_ctl(g);
+    fill_report(g, rep);
+    if (rep && g->profiling) {
+        float ms[4] = {0, 0, 0, 0};
+        for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&ms[k], g->ev[k], g->ev[k + 1]);
+        rep->ms_encode_flag = ms[0];
+        rep->ms_band_closure = ms[1];
+        rep->ms_decode_traverse = ms[2];
+        rep->ms_neighbours = 0.0;
+        rep->ms_fv1 = ms[3];
+        float tot = 0;
+        cudaEventElapsedTime(&tot, g->ev[0], g->ev[4]);
+        rep->ms_total = tot;
+    }
+    return st;
+}
+
+int swamp_gpu_advance(swamp_gpu* g, int64_t n_steps, swamp_step_report* rep) {
+    if (!g || n_steps < 0) return SWAMP_E_ARG;
+    cudaSetDevice(g->device);
+    int64_t k = 0;
+    for (; k + kGraphSteps <= n_steps; k += kGraphSteps) CK(cudaGraphLaunch(g->graphS, g->stream));
+    for (; k < n_steps; ++k) CK(cudaGraphLaunch(g->graph1, g->stream));
+    int st = fetch_ctl(g);
+    fill_report(g, rep);
+    return st;
+}
+
+int swamp_gpu_step_uniform(swamp_gpu* g, int64_t n_steps, swamp_step_report* rep) {
+    if (!g || !g->uniform) return SWAMP_E_STATE;
+    return swamp_gpu_advance(g, n_steps, rep);
+}
+
+int swamp_gpu_run(swamp_gpu* g, swamp_step_report* rep) {
+    if (!g) return SWAMP_E_ARG;
+    int st = fetch_ctl(g);
+    if (st) return st;
+    while (g->ctl_host->t < g->P.t_end) {
+        st = swamp_gpu_advance(g, 64, rep);
+        if (st) return st;
+    }
+    fill_report(g, rep);
+    return SWAMP_OK;
+}
+
+int swamp_gpu_info(const swamp_gpu* gc, double* t, double* dt, int64_t* step, int64_t* n_leaves) {
+    swamp_gpu* g = const_cast<swamp_gpu*>(gc);
+    if (!g) return SWAMP_E_ARG;
+    cudaSetDevice(g->device);
+    int st = fetch_ctl(g);
+    if (t) *t = g->ctl_host->t;
+    if (dt) *dt = g->ctl_host->dt;
+    if (step) *step = g->ctl_host->step;
+    if (n_leaves) *n_leaves = g->uniform ? (int64_t(1) << (2 * g->P.L)) : g->ctl_host->n_leaves;
+    return st;
+}
+
+int swamp_gpu_copy_leaves(swamp_gpu* g, uint32_t* leaves, uint32_t* nw, uint32_t* ne, uint32_t* nn, uint32_t* ns,
+                          int64_t cap, int64_t* n) {
+    if (!g) return SWAMP_E_ARG;
+    cudaSetDevice(g->device);
+    int st = fetch_ctl(g);
+    if (st) return st;
+    const uint32_t N = g->ctl_host->n_leaves;
+    if (n) *n = N;
+    if (!leaves && !nw && !ne && !nn && !ns) return SWAMP_OK;
+    if (cap < static_cast<int64_t>(N)) return SWAMP_E_ARG;
+    if (leaves) CK(cudaMemcpy(leaves, g->P.leaves, N * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    if (nw || ne || nn || ns) {
+        uint32_t* d = nullptr;
+        CK(cudaMalloc(&d, std::max<size_t>(16, 4ull * N * sizeof(uint32_t))));
+        const int grid = std::max(1, std::min<int>(g->num_sms * 8, (N + kThreads - 1) / kThreads));
+        hwfv1::k_descriptors<<<grid, kThreads, 0, g->stream>>>(g->P, g->ctl, d, N);
+        cudaError_t e = cudaStreamSynchronize(g->stream);
+        uint32_t* outs[4] = {nw, ne, nn, ns};
+        for (int k = 0; k < 4 && e == cudaSuccess; ++k)
+            if (outs[k]) e = cudaMemcpy(outs[k], d + static_cast<size_t>(k) * N, N * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        CK(e);
+    }
+    return SWAMP_OK;
+}
+
+int swamp_gpu_export_tree(swamp_gpu* g, double* h, double* qx, double* qy, double* z, uint8_t* sig) {
+    if (!g) return SWAMP_E_ARG;
+    cudaSetDevice(g->device);
+    const size_t NH = swamp::zorder::hierarchy_cells(g->P.L);
+    const size_t ND = swamp::zorder::detail_cells(g->P.L);
+    double* d = nullptr;
+    uint8_t* ds = nullptr;
+    CK(cudaMalloc(&d, 4 * NH * sizeof(double)));
+    cudaError_t e = cudaMalloc(&ds, std::max<size_t>(ND, 16));
+    if (e == cudaSuccess) {
+        hwfv1::k_export_tree<<<std::max(1, g->num_sms * 8), kThreads, 0, g->stream>>>(g->P, g->ctl, d, d + NH,
+                                                                                       d + 2 * NH, d + 3 * NH, ds);
+        e = cudaStreamSynchronize(g->stream);
+    }
+    double* outs[4] = {h, qx, qy, z};
+    for (int q = 0; q < 4 && e == cudaSuccess; ++q)
+        if (outs[q]) e = cudaMemcpy(outs[q], d + q * NH, NH * sizeof(double), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && sig) e = cudaMemcpy(sig, ds, ND, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (ds) cudaFree(ds);
+    CK(e);
+    return SWAMP_OK;
+}
+
+int swamp_gpu_export_finest(swamp_gpu* g, double* h, double* qx, double* qy) {
+    if (!g) return SWAMP_E_ARG;
+    cudaSetDevice(g->device);
+    const size_t nf = static_cast<size_t>(1) << (2 * g->P.L);
+    double* d = nullptr;
+    CK(cudaMalloc(&d, 3 * nf * sizeof(double)));
+    hwfv1::k_export_finest<<<std::max(1, g->num_sms * 8), kThreads, 0, g->stream>>>(g->P, g->ctl, d, d + nf,
+                                                                                     d + 2 * nf);
+    cudaError_t e = cudaStreamSynchronize(g->stream);
+    double* outs[3] = {h, qx, qy};
+    for (int q = 0; q < 3 && e == cudaSuccess; ++q)
+        if (outs[q]) e = cudaMemcpy(outs[q], d + q * nf, nf * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    CK(e);
+    return SWAMP_OK;
+}
+
+int swamp_gpu_last_error(const swamp_gpu* g, int32_t* code, uint32_t* z, int32_t* quantity, int32_t* stage, char* msg,
+                         size_t msg_cap) {
+    if (!g) return SWAMP_E_ARG;
+    if (code) *code = g->ctl_host ? g->ctl_host->err_code : 0;
+    if (z) *z = g->ctl_host ? g->ctl_host->err_z : 0;
+    if (quantity) *quantity = g->ctl_host ? g->ctl_host->err_q : 0;
+    if (stage) *stage = g->ctl_host ? g->ctl_host->err_stage : 0;
+    if (msg && msg_cap) {
+        std::strncpy(msg, g->err.c_str(), msg_cap - 1);
+        msg[msg_cap - 1] = 0;
+    }
+    return SWAMP_OK;
+}
+
+int swamp_gpu_counters(swamp_gpu* g, int64_t* out4) {
+    if (!g || !out4) return SWAMP_E_ARG;
+    int st = fetch_ctl(g);
+    out4[0] = g->uniform ? (int64_t(1) << (2 * g->P.L)) : g->ctl_host->n_leaves_used;
+    out4[1] = static_cast<int64_t>(g->ctl_host->cnt_tree);
+    out4[2] = static_cast<int64_t>(g->ctl_host->cnt_new);
+    out4[3] = int64_t(1) << (2 * g->P.L);
+    return st;
+}
+
+#define SWAMP_STR2(x) #x
+#define SWAMP_STR(x) SWAMP_STR2(x)
+const char* swamp_gpu_build_info(void) {
+    return "libswamp_gpu: sm_100a, --fmad=false, nvcc " SWAMP_STR(__CUDACC_VER_MAJOR__) "." SWAMP_STR(__CUDACC_VER_MINOR__);
+}
+
+}  // extern "C"

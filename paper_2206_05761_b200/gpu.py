@@ -1,0 +1,172 @@
+"""Python host binding of the C-ABI (include/swamp_gpu.h) via ctypes.
+
+Mirrors the reference engine interface: `initialise`
+returns an `Engine` (SimState owner) with `step_adaptive`, `advance`, `run`,
+and exports of the LeafAssembly / hierarchy / finest-grid expansion.
+`initialise_uniform` gives the GPU-FV1 comparator (`step_uniform`).
+
+There is no CPU fallback: if libswamp_gpu.so or a CUDA device is missing,
+construction raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .abi import STATUS, SimConfig, as_f64, dptr, level_offset, swamp_config, swamp_step_report, u8ptr, u32ptr
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libswamp_gpu.so")
+_LIB = None
+
+
+def lib():
+    """Load the in-tree sm_100a library (fails loudly when missing)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} missing — build it with `python -m paper_2206_05761_b200.build` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        dp = C.POINTER(C.c_double)
+        u32p = C.POINTER(C.c_uint32)
+        i64p = C.POINTER(C.c_int64)
+        rp = C.POINTER(swamp_step_report)
+        L.swamp_gpu_create.argtypes = [C.POINTER(swamp_config), dp, dp, dp, dp, C.c_int, C.POINTER(P)]
+        L.swamp_gpu_create_uniform.argtypes = L.swamp_gpu_create.argtypes
+        L.swamp_gpu_destroy.argtypes = [P]
+        L.swamp_gpu_step.argtypes = [P, rp]
+        L.swamp_gpu_advance.argtypes = [P, C.c_int64, rp]
+        L.swamp_gpu_run.argtypes = [P, rp]
+        L.swamp_gpu_step_uniform.argtypes = [P, C.c_int64, rp]
+        L.swamp_gpu_set_profiling.argtypes = [P, C.c_int]
+        L.swamp_gpu_info.argtypes = [P, dp, dp, i64p, i64p]
+        L.swamp_gpu_copy_leaves.argtypes = [P, u32p, u32p, u32p, u32p, u32p, C.c_int64, i64p]
+        L.swamp_gpu_export_tree.argtypes = [P, dp, dp, dp, dp, C.POINTER(C.c_uint8)]
+        L.swamp_gpu_export_finest.argtypes = [P, dp, dp, dp]
+        L.swamp_gpu_last_error.argtypes = [P, C.POINTER(C.c_int32), u32p, C.POINTER(C.c_int32),
+                                           C.POINTER(C.c_int32), C.c_char_p, C.c_size_t]
+        L.swamp_gpu_counters.argtypes = [P, i64p]
+        L.swamp_gpu_build_info.restype = C.c_char_p
+        _LIB = L
+    return _LIB
+
+
+EXPORTED_SYMBOLS = (
+    "swamp_gpu_create", "swamp_gpu_destroy", "swamp_gpu_step", "swamp_gpu_advance", "swamp_gpu_run",
+    "swamp_gpu_create_uniform", "swamp_gpu_step_uniform", "swamp_gpu_set_profiling", "swamp_gpu_info",
+    "swamp_gpu_copy_leaves", "swamp_gpu_export_tree", "swamp_gpu_export_finest", "swamp_gpu_last_error",
+    "swamp_gpu_counters", "swamp_gpu_build_info",
+)
+
+
+class SwampError(RuntimeError):
+    pass
+
+
+class Engine:
+    """SimState owner on one GPU."""
+
+    def __init__(self, cfg: SimConfig, h, qx, qy, z, device: int = 0, uniform: bool = False):
+        self.cfg = cfg
+        self.L = int(cfg.L)
+        self.uniform = uniform
+        self._c = cfg.to_c()
+        n = cfg.side * cfg.side
+        arrs = [as_f64(a).reshape(-1) for a in (h, qx, qy, z)]
+        if any(a.size != n for a in arrs):
+            raise ValueError(f"fields must be 2^L x 2^L = {cfg.side} x {cfg.side}")
+        self._h = C.c_void_p()
+        f = lib().swamp_gpu_create_uniform if uniform else lib().swamp_gpu_create
+        st = f(C.byref(self._c), *[dptr(a) for a in arrs], int(device), C.byref(self._h))
+        if st != 0:
+            raise SwampError(f"initialise failed: {STATUS.get(st, st)}")
+        self.report = swamp_step_report()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().swamp_gpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st, what):
+        if st != 0:
+            code, z, q, stg = C.c_int32(), C.c_uint32(), C.c_int32(), C.c_int32()
+            buf = C.create_string_buffer(256)
+            lib().swamp_gpu_last_error(self._h, C.byref(code), C.byref(z), C.byref(q), C.byref(stg), buf, 256)
+            raise SwampError(f"{what}: {STATUS.get(st, st)} (z={z.value}, quantity={q.value}, stage={stg.value}; "
+                             f"{buf.value.decode()})")
+
+    # ---- engine operations
+    def step_adaptive(self) -> dict:
+        self._check(lib().swamp_gpu_step(self._h, C.byref(self.report)), "step_adaptive")
+        return self.report.as_dict()
+
+    def step_uniform(self, n: int = 1) -> dict:
+        self._check(lib().swamp_gpu_step_uniform(self._h, int(n), C.byref(self.report)), "step_uniform")
+        return self.report.as_dict()
+
+    def advance(self, n: int) -> dict:
+        self._check(lib().swamp_gpu_advance(self._h, int(n), C.byref(self.report)), "advance")
+        return self.report.as_dict()
+
+    def run(self) -> dict:
+        self._check(lib().swamp_gpu_run(self._h, C.byref(self.report)), "run")
+        return self.report.as_dict()
+
+    def set_profiling(self, on: bool):
+        lib().swamp_gpu_set_profiling(self._h, 1 if on else 0)
+
+    # ---- state
+    def info(self) -> dict:
+        t, dt = C.c_double(), C.c_double()
+        s, nl = C.c_int64(), C.c_int64()
+        self._check(lib().swamp_gpu_info(self._h, C.byref(t), C.byref(dt), C.byref(s), C.byref(nl)), "info")
+        return {"t": t.value, "dt": dt.value, "step": s.value, "n_leaves": nl.value}
+
+    def leaves(self, with_neighbours: bool = True):
+        n = C.c_int64()
+        self._check(lib().swamp_gpu_copy_leaves(self._h, None, None, None, None, None, 0, C.byref(n)), "leaves")
+        N = n.value
+        lv = np.zeros(N, np.uint32)
+        nb = np.zeros((4, N), np.uint32)
+        ptrs = [u32ptr(nb[d]) for d in range(4)] if with_neighbours else [None] * 4
+        self._check(lib().swamp_gpu_copy_leaves(self._h, u32ptr(lv), *ptrs, N, C.byref(n)), "leaves")
+        return lv, nb
+
+    def export_tree(self):
+        NH, ND = level_offset(self.L + 1), level_offset(self.L)
+        out = [np.zeros(NH) for _ in range(4)]
+        sig = np.zeros(ND, np.uint8)
+        self._check(lib().swamp_gpu_export_tree(self._h, *[dptr(a) for a in out], u8ptr(sig)), "export_tree")
+        return out, sig
+
+    def export_finest(self):
+        n = self.cfg.side
+        out = [np.zeros((n, n)) for _ in range(3)]
+        self._check(lib().swamp_gpu_export_finest(self._h, *[dptr(a) for a in out]), "export_finest")
+        return out
+
+    def counters(self):
+        a = (C.c_int64 * 4)()
+        self._check(lib().swamp_gpu_counters(self._h, a), "counters")
+        return list(a)
+
+
+def initialise(cfg: SimConfig, h, qx, qy, z, device: int = 0) -> Engine:
+    """engine.initialise on `device`."""
+    return Engine(cfg, h, qx, qy, z, device=device)
+
+
+def initialise_uniform(cfg: SimConfig, h, qx, qy, z, device: int = 0) -> Engine:
+    """The uniform GPU-FV1 solver state."""
+    return Engine(cfg, h, qx, qy, z, device=device, uniform=True)

@@ -1,0 +1,127 @@
+"""GPU (sm_100a, through the C-ABI) vs the CPU oracle on identical inputs.
+
+The bar: leaf lists, neighbour descriptors, significance flags
+and every scale coefficient on the tree are BIT-identical after initialise and
+after every checked step; t and dt are bit-identical. The oracle is the
+checker only.
+"""
+import numpy as np
+import pytest
+
+from paper_2206_05761_b200 import cases
+from paper_2206_05761_b200.abi import BAND_NONE, BAND_PARENTS
+from tests._parity import compare_states
+
+gpu = pytest.importorskip("paper_2206_05761_b200.gpu")
+from oracle import oracle as O  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    ("pseudo2d_dambreak", dict(L=6)),
+    ("pseudo2d_dambreak", dict(L=8)),
+    ("circular_dambreak", dict(L=7)),
+    ("circular_dambreak", dict(L=8, epsilon=1e-2)),
+    ("quiescent_humps", dict(L=7)),
+    ("hump_dambreak", dict(L=7)),
+    ("monai_runup", dict(L=7)),
+    ("river_flood", dict(L=7)),
+    ("pseudo2d_dambreak", dict(L=3)),
+    ("circular_dambreak", dict(L=1)),
+    ("circular_dambreak", dict(L=2)),
+]
+
+
+@pytest.mark.parametrize("name,kw", CASES, ids=[f"{n}-{'-'.join(f'{k}{v}' for k, v in kw.items())}" for n, kw in CASES])
+def test_step_parity(name, kw):
+    cfg, h, qx, qy, z = cases.CASES[name](**kw)
+    g = gpu.initialise(cfg, h, qx, qy, z)
+    o = O.Oracle(cfg, h, qx, qy, z)
+    compare_states(g, o, f"{name} init")
+    for k in range(1, 41):
+        g.step_adaptive()
+        o.step()
+        if k in (1, 2, 3, 5, 10, 20, 40):
+            compare_states(g, o, f"{name} step {k}")
+
+
+def test_graph_advance_matches_single_steps():
+    cfg, h, qx, qy, z = cases.circular_dambreak(L=8)
+    a = gpu.initialise(cfg, h, qx, qy, z)
+    b = gpu.initialise(cfg, h, qx, qy, z)
+    for _ in range(19):
+        a.step_adaptive()
+    b.advance(19)
+    (ah, *_), asig = a.export_tree()
+    (bh, *_), bsig = b.export_tree()
+    np.testing.assert_array_equal(asig, bsig)
+    assert a.info() == b.info()
+    fa = a.export_finest()[0]
+    fb = b.export_finest()[0]
+    np.testing.assert_array_equal(fa.view(np.uint64), fb.view(np.uint64))
+
+
+@pytest.mark.parametrize("band", [BAND_NONE, BAND_PARENTS])
+def test_band_modes(band):
+    cfg, h, qx, qy, z = cases.pseudo2d_dambreak(L=7, band_mode=band)
+    g = gpu.initialise(cfg, h, qx, qy, z)
+    o = O.Oracle(cfg, h, qx, qy, z)
+    for _ in range(15):
+        g.step_adaptive()
+        o.step()
+    compare_states(g, o, f"band {band}")
+
+
+def test_full_run_to_t_end():
+    """Config 1 to t_end = 2.5 s: whole-run parity, finest expansion equal."""
+    cfg, h, qx, qy, z = cases.pseudo2d_dambreak(L=7, t_end=2.5)
+    g = gpu.initialise(cfg, h, qx, qy, z)
+    o = O.Oracle(cfg, h, qx, qy, z)
+    g.run()
+    o.run()
+    compare_states(g, o, "run")
+    assert g.info()["t"] == 2.5
+    for a, b in zip(g.export_finest(), o.export_finest()):
+        np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def test_output_time_clipping():
+    cfg, h, qx, qy, z = cases.hump_dambreak(L=6, t_end=1.0)
+    cfg.output_times = (0.3, 0.7)
+    g = gpu.initialise(cfg, h, qx, qy, z)
+    o = O.Oracle(cfg, h, qx, qy, z)
+    ts = []
+    while g.info()["t"] < 1.0:
+        g.step_adaptive()
+        o.step()
+        ts.append(g.info()["t"])
+    compare_states(g, o, "clipped")
+    assert 0.3 in ts and 0.7 in ts and ts[-1] == 1.0
+
+
+def test_uniform_parity_and_eps0_equivalence():
+    """step_uniform parity, and adaptive at eps = 0 == uniform (A4) bitwise."""
+    cfg, h, qx, qy, z = cases.circular_dambreak(L=6, epsilon=0.0)
+    u = gpu.initialise_uniform(cfg, h, qx, qy, z)
+    ou = O.Oracle(cfg, h, qx, qy, z, uniform=True)
+    a = gpu.initialise(cfg, h, qx, qy, z)
+    assert a.info()["n_leaves"] == 4 ** 6
+    for _ in range(25):
+        u.step_uniform(1)
+        ou.step(uniform=True)
+        a.step_adaptive()
+    fu = u.export_finest()
+    fo = ou.export_finest()
+    fa = a.export_finest()
+    for x, y, w in zip(fu, fo, fa):
+        np.testing.assert_array_equal(x.view(np.uint64), y.view(np.uint64))
+        np.testing.assert_array_equal(x.view(np.uint64), w.view(np.uint64))
+
+
+def test_profiling_report_has_stage_times():
+    cfg, h, qx, qy, z = cases.circular_dambreak(L=8)
+    g = gpu.initialise(cfg, h, qx, qy, z)
+    g.set_profiling(True)
+    r = g.step_adaptive()
+    assert r["ms_fv1"] > 0 and r["ms_encode_flag"] > 0 and r["ms_total"] >= r["ms_fv1"]
+    assert r["n_leaves"] > 0 and r["step"] == 1
