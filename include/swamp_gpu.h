@@ -117,6 +117,13 @@ int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep);
  * t >= t_end. Synchronises once at the end and checks the error word. */
 int swamp_gpu_advance(swamp_gpu* g, int64_t n_steps, swamp_step_report* rep);
 
+/* Asynchronous form of swamp_gpu_advance: enqueue `n_steps` graph replays on
+ * the handle's stream and return without synchronising or checking errors
+ * (the next synchronising call reports them). */
+int swamp_gpu_enqueue(swamp_gpu* g, int64_t n_steps);
+/* The cudaStream_t (as void*) every kernel of this handle runs on. */
+int swamp_gpu_stream(swamp_gpu* g, void** stream);
+
 /* run without outputs: step until t >= t_end. */
 int swamp_gpu_run(swamp_gpu* g, swamp_step_report* rep);
 

@@ -147,21 +147,21 @@ def monai_runup(L=10, epsilon=1e-3, t_end=22.5, seed=2206, band_mode=BAND_NEIGHB
 
 def river_flood(L=11, epsilon=1e-3, t_end=1e30, seed=5, band_mode=BAND_NEIGHBOURS):
     """Config 5 — synthetic-DEM river flood at L = 11 (2048 x 2048 cells of
-    5 m). A meandering valley sloping east with multi-octave seeded noise;
-    the channel starts filled 2 m above its thalweg; a west depth hydrograph
-    (2 m -> 6 m); east transmissive, N/S walls; n_M = 0.03. Timed with a fixed
-    step count (t_end effectively unbounded)."""
-    side = 1 << L
-    W = side * 5.0 * (2048.0 / side) if L != 11 else 2048 * 5.0
+    5 m, W = 10240 m). A meandering valley (Gaussian cross-section, 10 m
+    walls) sloping 20 m west -> east, plus 3 octaves of seeded value noise
+    (0.3 m); the channel starts filled 3 m above its thalweg; a west depth
+    hydrograph (2 m -> 6 m); east transmissive, N/S walls; n_M = 0.03. Timed
+    with a fixed step count (t_end effectively unbounded). At L < 11 the same
+    geometry is sampled on a coarser grid (same W)."""
+    W = 2048 * 5.0
     cfg = SimConfig(L=L, epsilon=epsilon, width=W, t_end=t_end, manning=0.03, band_mode=band_mode,
                     bc=(BC_INFLOW, BC_TRANSMISSIVE, BC_REFLECTIVE, BC_REFLECTIVE), inflow_mode=INFLOW_DEPTH,
                     dt_fallback=0.1, name="river_flood")
     X, Y = centres(cfg)
     yc = 0.5 * W + 0.06 * W * np.sin(2.0 * np.pi * X / (0.4 * W))
     thalweg = 20.0 * (1.0 - X / W)
-    z = thalweg + 4.0e-4 * (W / 10240.0) ** -1 * (Y - yc) ** 2 / 40.0 + 1.5 * _value_noise(cfg.side, 6, seed)
-    eta0 = thalweg + 2.0
-    h = np.maximum(0.0, eta0 - z)
+    z = thalweg + 10.0 * (1.0 - np.exp(-(((Y - yc) / 600.0) ** 2))) + 0.3 * _value_noise(cfg.side, 3, seed)
+    h = np.maximum(0.0, (thalweg + 3.0) - z)
     t = np.array([0.0, 600.0, 3600.0, 7200.0])
     d = np.array([2.0, 4.0, 6.0, 6.0])
     cfg.inflow_t, cfg.inflow_v = tuple(t), tuple(d)

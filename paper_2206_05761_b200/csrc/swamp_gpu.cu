@@ -44,7 +44,7 @@ struct swamp_gpu {
     Ctl* ctl = nullptr;      // device
     Ctl* ctl_host = nullptr; // pinned mirror
     std::vector<void*> allocs;
-    cudaGraphExec_t graph1 = nullptr, graphS = nullptr;
+    cudaGraphExec_t graph1 = nullptr, graphS = nullptr, graphT = nullptr;
     int fv1_grid = 0;
     int num_sms = 0;
     size_t smem_k1 = 0, smem_k2 = 0, smem_k3 = 0;
@@ -55,6 +55,7 @@ struct swamp_gpu {
     ~swamp_gpu() {
         if (graph1) cudaGraphExecDestroy(graph1);
         if (graphS) cudaGraphExecDestroy(graphS);
+        if (graphT) cudaGraphExecDestroy(graphT);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         for (void* a : allocs) cudaFree(a);
@@ -119,17 +120,19 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     if (timed) cudaEventRecord(g->ev[4], s);
 }
 
+// graph1: one step; graphS: kGraphSteps steps; graphT: one step with event
+// record nodes between the kernels (per-stage device times, StepReport)
 int build_graphs(swamp_gpu* g) {
-    for (int which = 0; which < 2; ++which) {
-        const int steps = which == 0 ? 1 : kGraphSteps;
+    for (int which = 0; which < 3; ++which) {
+        const int steps = which == 1 ? kGraphSteps : 1;
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
-        for (int k = 0; k < steps; ++k) launch_step_kernels(g, false);
+        for (int k = 0; k < steps; ++k) launch_step_kernels(g, which == 2);
         CK(cudaStreamEndCapture(g->stream, &graph));
         cudaGraphExec_t exec;
         CK(cudaGraphInstantiate(&exec, graph, 0));
         cudaGraphDestroy(graph);
-        (which == 0 ? g->graph1 : g->graphS) = exec;
+        (which == 0 ? g->graph1 : which == 1 ? g->graphS : g->graphT) = exec;
     }
     return SWAMP_OK;
 }
@@ -346,8 +349,7 @@ int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep) {
     if (!g) return SWAMP_E_ARG;
     cudaSetDevice(g->device);
     if (g->profiling) {
-        launch_step_kernels(g, true);
-        CK(cudaGetLastError());
+        CK(cudaGraphLaunch(g->graphT, g->stream));
     } else {
         CK(cudaGraphLaunch(g->graph1, g->stream));
     }
@@ -366,6 +368,21 @@ int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep) {
         rep->ms_total = tot;
     }
     return st;
+}
+
+int swamp_gpu_stream(swamp_gpu* g, void** stream) {
+    if (!g || !stream) return SWAMP_E_ARG;
+    *stream = static_cast<void*>(g->stream);
+    return SWAMP_OK;
+}
+
+int swamp_gpu_enqueue(swamp_gpu* g, int64_t n_steps) {
+    if (!g || n_steps < 0) return SWAMP_E_ARG;
+    cudaSetDevice(g->device);
+    int64_t k = 0;
+    for (; k + kGraphSteps <= n_steps; k += kGraphSteps) CK(cudaGraphLaunch(g->graphS, g->stream));
+    for (; k < n_steps; ++k) CK(cudaGraphLaunch(g->graph1, g->stream));
+    return SWAMP_OK;
 }
 
 int swamp_gpu_advance(swamp_gpu* g, int64_t n_steps, swamp_step_report* rep) {

@@ -51,6 +51,8 @@ def lib():
         L.swamp_gpu_last_error.argtypes = [P, C.POINTER(C.c_int32), u32p, C.POINTER(C.c_int32),
                                            C.POINTER(C.c_int32), C.c_char_p, C.c_size_t]
         L.swamp_gpu_counters.argtypes = [P, i64p]
+        L.swamp_gpu_enqueue.argtypes = [P, C.c_int64]
+        L.swamp_gpu_stream.argtypes = [P, C.POINTER(C.c_void_p)]
         L.swamp_gpu_build_info.restype = C.c_char_p
         _LIB = L
     return _LIB
@@ -60,7 +62,7 @@ EXPORTED_SYMBOLS = (
     "swamp_gpu_create", "swamp_gpu_destroy", "swamp_gpu_step", "swamp_gpu_advance", "swamp_gpu_run",
     "swamp_gpu_create_uniform", "swamp_gpu_step_uniform", "swamp_gpu_set_profiling", "swamp_gpu_info",
     "swamp_gpu_copy_leaves", "swamp_gpu_export_tree", "swamp_gpu_export_finest", "swamp_gpu_last_error",
-    "swamp_gpu_counters", "swamp_gpu_build_info",
+    "swamp_gpu_counters", "swamp_gpu_build_info", "swamp_gpu_enqueue", "swamp_gpu_stream",
 )
 
 
@@ -122,6 +124,15 @@ class Engine:
     def run(self) -> dict:
         self._check(lib().swamp_gpu_run(self._h, C.byref(self.report)), "run")
         return self.report.as_dict()
+
+    def enqueue(self, n: int):
+        """Launch n steps asynchronously on the engine's stream (no sync)."""
+        self._check(lib().swamp_gpu_enqueue(self._h, int(n)), "enqueue")
+
+    def stream_ptr(self) -> int:
+        s = C.c_void_p()
+        self._check(lib().swamp_gpu_stream(self._h, C.byref(s)), "stream")
+        return s.value or 0
 
     def set_profiling(self, on: bool):
         lib().swamp_gpu_set_profiling(self._h, 1 if on else 0)
