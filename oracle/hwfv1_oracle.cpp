@@ -171,33 +171,40 @@ void face(const double Lc[4], const double Rc[4], const Phys& p, double F[3], do
     const double uR = vel(Rc[0], Rc[1], p.hdry), vR = vel(Rc[0], Rc[2], p.hdry);
     hll(*hLs, uL, vL, *hRs, uR, vR, p.g, F);
 }
-// Deterministic cube root (D2): bit-level seed + Newton, IEEE ops only, so
-// CPU and GPU agree bit for bit (libm cbrt and libdevice cbrt do not).
-double cbrt_det(double x) {
+// Deterministic inverse cube root (D2): bit-level seed + 4 division-free
+// Newton steps y <- y + y(1 - h y^3)/3, IEEE ops only, so CPU and GPU agree
+// bit for bit (libm cbrt and libdevice cbrt do not).
+double rcbrt_det(double x) {
     uint64_t b;
     std::memcpy(&b, &x, 8);
-    b = b / 3u + 0x2A9F7893782DA1CEull;
+    b = 0x553EF0FF289DD796ull - b / 3u;
     double y;
     std::memcpy(&y, &b, 8);
-    for (int it = 0; it < 5; ++it) y = ((2.0 * y) + (x / (y * y))) / 3.0;
+    const double third = 1.0 / 3.0;
+    for (int it = 0; it < 4; ++it) {
+        const double t = (x * y) * (y * y);
+        y = y + ((y * (1.0 - t)) * third);
+    }
     return y;
 }
-// semi-implicit Manning friction on a wet post-Euler state.
+double cbrt_det(double x) { return 1.0 / rcbrt_det(x); }
+// semi-implicit Manning friction on a wet post-Euler state:
+// q /= 1 + dt * C_f * |q| / h^2 with C_f = g n^2 h^(-1/3) (|u| = |q|/h).
 void friction(double h, double* qx, double* qy, double dt, const Phys& p) {
-    const double u = *qx / h, v = *qy / h;
-    const double sp = std::sqrt((u * u) + (v * v));
-    if (sp > 0.0) {
-        const double Cf = (p.g * (p.nM * p.nM)) / cbrt_det(h);
-        const double den = 1.0 + (((dt * Cf) * sp) / h);
-        *qx = *qx / den;
-        *qy = *qy / den;
+    const double qm = std::sqrt((*qx * *qx) + (*qy * *qy));
+    if (qm > 0.0) {
+        const double Cf = (p.g * (p.nM * p.nM)) * rcbrt_det(h);
+        const double den = 1.0 + (((dt * Cf) * qm) / (h * h));
+        const double r = 1.0 / den;
+        *qx = *qx * r;
+        *qy = *qy * r;
     }
 }
 // CFL bound of one cell: +inf when dry.
 double cfl_cell(double h, double qx, double qy, double dx, double g, double hdry) {
     if (!(h >= hdry)) return std::numeric_limits<double>::infinity();
-    const double au = absd(qx / h), av = absd(qy / h);
-    const double s = ((au > av) ? au : av) + std::sqrt(g * h);
+    const double aq = max2(absd(qx), absd(qy));
+    const double s = (aq / h) + std::sqrt(g * h);
     return dx / s;
 }
 // linear interpolation of the inflow series, last value held
@@ -235,6 +242,7 @@ void boundary_state(const double own[4], int kind, int dir, double t, const doub
 // four W,E,N,S neighbour states are physical (h, qx, qy, z). Writes new
 // (h, qx, qy). Returns false on a non-finite result.
 bool fv1_cell(const double own[4], const double nb[4][4], double dx, double dt, const Phys& p, double out[3]) {
+    const double idx = 1.0 / dx;
     const double h = own[0], qx = own[1], qy = own[2];
     const double hg = 0.5 * p.g;
     double FE[3], FW[3], GN[3], GS[3], hLs, hRs;
@@ -262,10 +270,11 @@ bool fv1_cell(const double own[4], const double nb[4][4], double dx, double dt, 
         face(Lc, Rc, p, GS, &hLs, &hRs);
         GS[1] = GS[1] + (hg * ((h * h) - (hRs * hRs)));
     }
-    // spatial operator L_c: -(F_e - F_w)/dx - (G_n - G_s)/dx
-    const double Lh = (-((FE[0] - FW[0]) / dx)) - ((GN[0] - GS[0]) / dx);
-    const double Lqx = (-((FE[1] - FW[1]) / dx)) - ((GN[2] - GS[2]) / dx);
-    const double Lqy = (-((FE[2] - FW[2]) / dx)) - ((GN[1] - GS[1]) / dx);
+    // spatial operator L_c: -(F_e - F_w)/dx - (G_n - G_s)/dx,
+    // with 1/dx formed once (D2 pin)
+    const double Lh = (-((FE[0] - FW[0]) * idx)) - ((GN[0] - GS[0]) * idx);
+    const double Lqx = (-((FE[1] - FW[1]) * idx)) - ((GN[2] - GS[2]) * idx);
+    const double Lqy = (-((FE[2] - FW[2]) * idx)) - ((GN[1] - GS[1]) * idx);
     // forward Euler (Eq. 2)
     double hn = h + (dt * Lh);
     double qxn = qx + (dt * Lqx);

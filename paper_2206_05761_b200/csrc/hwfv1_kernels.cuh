@@ -67,6 +67,7 @@ struct Params {
     double W, cfl, t_end, dt_fallback;
     double tau[kMaxL + 1];    // significance threshold per detail level, physical units
     double dx[kMaxL + 1];     // W * 2^-n
+    double inv_dx[kMaxL + 1]; // 1.0 / dx[n] (IEEE division, as the oracle)
     double smax[4];
     PhysParams phys;
     const double* inflow_t;
@@ -81,17 +82,19 @@ struct Params {
     uint32_t* leaves;
     uint32_t* tile_cnt;
     uint32_t* tile_off;
+    uint32_t* tile_lvl;   // traversal depth of each level-R subtree root (R = reached)
+    uint32_t* tile_src;   // z of the root's decode source, or kNoSrc
 };
 
 // ------------------------------------------------------------------ memory ops
 __device__ __forceinline__ double4 ld4(const double4* p) {
     double4 v;
-    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+    asm("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
     return v;
 }
 __device__ __forceinline__ double4 ld4_nc(const double4* p) {
     double4 v;
-    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
     return v;
 }
 __device__ __forceinline__ double4 ld4_cg(const double4* p) {
@@ -127,30 +130,7 @@ __device__ __forceinline__ void report_error(Ctl* c, int code, uint32_t z, int q
 struct Red {
     double par, dmax;
 };
-// 4 consecutive lanes hold children c0..c3 (k = lane & 3); lane k = 0 ends up
-// with parent = 0.25*((c0+c1)+(c2+c3)) and max |detail| in physical units.
-__device__ __forceinline__ Red red4_shfl(double v) {
-    const double x1 = __shfl_xor_sync(kFull, v, 1);
-    const double s01 = v + x1;
-    const double x2 = __shfl_xor_sync(kFull, s01, 2);
-    const double par = 0.25 * (s01 + x2);
-    const double da = s01 - x2;
-    const double y2 = __shfl_xor_sync(kFull, v, 2);
-    const double s02 = v + y2;
-    const double z1 = __shfl_xor_sync(kFull, s02, 1);
-    const double db = s02 - z1;
-    const double y3 = __shfl_xor_sync(kFull, v, 3);
-    const double s03 = v + y3;
-    const double w1 = __shfl_xor_sync(kFull, s03, 1);
-    const double dg = s03 - w1;
-    return {par, max2(max2(absd(da), absd(db)), absd(dg))};
-}
-__device__ __forceinline__ double par_shfl(double v) {
-    const double x1 = __shfl_xor_sync(kFull, v, 1);
-    const double s01 = v + x1;
-    const double x2 = __shfl_xor_sync(kFull, s01, 2);
-    return 0.25 * (s01 + x2);
-}
+// parent = 0.25*((c0+c1)+(c2+c3)) and max |detail| of 4 children, physical units
 __device__ __forceinline__ Red red4(double c0, double c1, double c2, double c3) {
     const double a = c0 + c1, b = c2 + c3;
     const double par = 0.25 * (a + b);
@@ -169,16 +149,24 @@ struct Enc {
     double4 par;
     bool flow, zflag;
 };
+// WITH_Z: also threshold z's details (the static DEM mask, t = 0 only)
+template <bool WITH_Z = true>
 __device__ __forceinline__ Enc encode_children(const double4 c[4], const Params& P, int n) {
     const Red h = red4(c[0].x, c[1].x, c[2].x, c[3].x);
     const Red qx = red4(c[0].y, c[1].y, c[2].y, c[3].y);
     const Red qy = red4(c[0].z, c[1].z, c[2].z, c[3].z);
-    const Red z = red4(c[0].w, c[1].w, c[2].w, c[3].w);
     const double tau = P.tau[n];
     Enc e;
-    e.par = make_double4(h.par, qx.par, qy.par, z.par);
     e.flow = sig_q(h.dmax, P.smax[0], tau) || sig_q(qx.dmax, P.smax[1], tau) || sig_q(qy.dmax, P.smax[2], tau);
-    e.zflag = sig_q(z.dmax, P.smax[3], tau);
+    if (WITH_Z) {
+        const Red z = red4(c[0].w, c[1].w, c[2].w, c[3].w);
+        e.par = make_double4(h.par, qx.par, qy.par, z.par);
+        e.zflag = sig_q(z.dmax, P.smax[3], tau);
+    } else {
+        const double a = c[0].w + c[1].w, b = c[2].w + c[3].w;
+        e.par = make_double4(h.par, qx.par, qy.par, 0.25 * (a + b));
+        e.zflag = false;
+    }
     return e;
 }
 
@@ -266,51 +254,42 @@ __global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
     const uint32_t j = blockIdx.x;
     unsigned tree = 0;
 
-    // ---- finest level: 4 lanes per level-(L-1) parent, one child each
+    // ---- finest level: one thread per level-(L-1) parent; its 4 children are
+    //      128 contiguous bytes, read with four 256-bit loads
     {
         const int n = L - 1;
         const uint32_t npar = 1u << (2 * (K - 1));
-        const uint32_t nchild = npar << 2;
         const uint32_t pbase = j * npar;
-        const double tau = P.tau[n];
         const bool store_smem = n > R;
-        for (uint32_t c0 = 0; c0 < nchild; c0 += kThreads) {
-            const uint32_t ci = c0 + threadIdx.x;
-            const bool valid = ci < nchild;
-            const uint32_t pi = ci >> 2;
+#pragma unroll 2
+        for (uint32_t pi = threadIdx.x; pi < npar; pi += kThreads) {
             const uint32_t pm = pbase + pi;
-            const bool sp = valid && (INIT || sigp[P.fbase[n] + pm]);
-            double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
-            if (sp) v = ld4_nc(buf + P.base[L] + (static_cast<unsigned long long>(pm) << 2) + (ci & 3u));
-            const Red rh = red4_shfl(v.x);
-            const Red rx = red4_shfl(v.y);
-            const Red ry = red4_shfl(v.z);
-            Red rz;
-            if (INIT) rz = red4_shfl(v.w);
-            else rz.par = par_shfl(v.w), rz.dmax = 0.0;
-            if (valid && (ci & 3u) == 0u) {
-                double4 par = make_double4(0.0, 0.0, 0.0, 0.0);
-                bool flow;
-                if (sp) {
-                    par = make_double4(rh.par, rx.par, ry.par, rz.par);
-                    flow = sig_q(rh.dmax, P.smax[0], tau) || sig_q(rx.dmax, P.smax[1], tau) ||
-                           sig_q(ry.dmax, P.smax[2], tau);
-                    st4(buf + P.base[n] + pm, par);
-                    ++tree;
-                } else {
-                    flow = 0.0 >= tau;
-                    if (store_smem && sigp[P.fbase[n - 1] + (pm >> 2)]) par = ld4(buf + P.base[n] + pm);
-                }
-                uint8_t d;
-                if (INIT) {
-                    d = sig_q(rz.dmax, P.smax[3], tau) ? 1 : 0;
-                    P.dem[P.fbase[n] + pm] = d;
-                } else {
-                    d = P.dem[P.fbase[n] + pm];
-                }
-                P.pre[P.fbase[n] + pm] = (flow || d) ? 1 : 0;
-                if (store_smem) sv[lo(n, R) + pi] = par;
+            const bool sp = INIT || sigp[P.fbase[n] + pm];
+            const uint8_t d0 = INIT ? 0 : P.dem[P.fbase[n] + pm];
+            double4 par = make_double4(0.0, 0.0, 0.0, 0.0);
+            bool flow, zf = false;
+            if (sp) {
+                const double4* cp = buf + P.base[L] + (static_cast<unsigned long long>(pm) << 2);
+                const double4 c[4] = {ld4_nc(cp), ld4_nc(cp + 1), ld4_nc(cp + 2), ld4_nc(cp + 3)};
+                const Enc e = encode_children<INIT>(c, P, n);
+                par = e.par;
+                flow = e.flow;
+                zf = e.zflag;
+                st4(buf + P.base[n] + pm, par);
+                ++tree;
+            } else {
+                flow = 0.0 >= P.tau[n];
+                if (store_smem && sigp[P.fbase[n - 1] + (pm >> 2)]) par = ld4(buf + P.base[n] + pm);
             }
+            uint8_t d;
+            if (INIT) {
+                d = zf ? 1 : 0;
+                P.dem[P.fbase[n] + pm] = d;
+            } else {
+                d = d0;
+            }
+            P.pre[P.fbase[n] + pm] = (flow || d) ? 1 : 0;
+            if (store_smem) sv[lo(n, R) + pi] = par;
         }
     }
     __syncthreads();
@@ -328,7 +307,7 @@ __global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
             if (sp) {
                 const uint32_t c0 = lo(n + 1, R) + 4u * pi;
                 const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
-                const Enc e = encode_children(c, P, n);
+                const Enc e = encode_children<INIT>(c, P, n);
                 par = e.par;
                 flow = e.flow;
                 zf = e.zflag;
@@ -355,23 +334,35 @@ __global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
     if (threadIdx.x == 0 && tsum) atomicAdd(&ctl->cnt_tree, (unsigned long long)tsum);
     if (!last_block(&ctl->done_k1, &s_last)) return;
 
-    // ---- last CTA: levels R-1 .. 0, children from global (L2)
+    // ---- last CTA: levels R-1 .. 0. Level R children come from global (L2,
+    //      written by every CTA); above that the block keeps its results in
+    //      shared memory when levels 0..R-1 fit (R <= K).
     unsigned ttop = 0;
+    const bool top_smem = ((1u << (2 * R)) - 1u) / 3u <= ((1u << (2 * K)) - 1u) / 3u;
     for (int n = R - 1; n >= 0; --n) {
         const uint32_t cnt = 1u << (2 * n);
+        const bool kids_in_smem = top_smem && n < R - 1;
         for (uint32_t pm = threadIdx.x; pm < cnt; pm += kThreads) {
             const bool sp = INIT || sigp[P.fbase[n] + pm];
             bool flow, zf = false;
             if (sp) {
-                const double4* cp = buf + P.base[n + 1] + (static_cast<unsigned long long>(pm) << 2);
-                const double4 c[4] = {ld4_cg(cp), ld4_cg(cp + 1), ld4_cg(cp + 2), ld4_cg(cp + 3)};
-                const Enc e = encode_children(c, P, n);
+                double4 c[4];
+                if (kids_in_smem) {
+                    const uint32_t c0 = lo(n + 1, 0) + 4u * pm;
+                    c[0] = sv[c0]; c[1] = sv[c0 + 1]; c[2] = sv[c0 + 2]; c[3] = sv[c0 + 3];
+                } else {
+                    const double4* cp = buf + P.base[n + 1] + (static_cast<unsigned long long>(pm) << 2);
+                    c[0] = ld4_cg(cp); c[1] = ld4_cg(cp + 1); c[2] = ld4_cg(cp + 2); c[3] = ld4_cg(cp + 3);
+                }
+                const Enc e = encode_children<INIT>(c, P, n);
                 flow = e.flow;
                 zf = e.zflag;
                 st4(buf + P.base[n] + pm, e.par);
+                if (top_smem) sv[lo(n, 0) + pm] = e.par;
                 ++ttop;
             } else {
                 flow = 0.0 >= P.tau[n];
+                if (top_smem && n > 0 && sigp[P.fbase[n - 1] + (pm >> 2)]) sv[lo(n, 0) + pm] = ld4_cg(buf + P.base[n] + pm);
             }
             uint8_t d;
             if (INIT) {
@@ -390,6 +381,19 @@ __global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
         if (tt) atomicAdd(&ctl->cnt_tree, (unsigned long long)tt);
         ctl->done_k1 = 0;
     }
+}
+
+// ----------------------------------------------------------- decode helper
+// decode_tree (SPEC.md:146-154) under D4 + PTT (SPEC.md:227-235, Alg. 5) +
+// compact_leaves (SPEC.md:236-244). In physical units a zero-detail decode is
+// a copy of the parent's (h, qx, qy) to its children (SPEC.md:153), so a cell
+// below a chain of newly significant cells takes the value of the chain's top.
+__device__ __forceinline__ void write_projection(double4* buf, const Params& P, int n, uint32_t m, uint32_t src) {
+    const int ns = zo::level_of(src);
+    const double4 v = ld4_cg(buf + P.base[ns] + (src - zo::level_offset(ns)));
+    double4* dst = buf + P.base[n] + m;
+    const double4 old = ld4_cg(dst);
+    st4(dst, make_double4(v.x, v.y, v.z, old.w));
 }
 
 // =========================================================================== K2
@@ -462,30 +466,83 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
     }
     if (!last_block(&ctl->done_k2, &s_last)) return;
 
-    // ---- last CTA: band + closure on levels R-1 .. 0
-    for (int n = R - 1; n >= 0; --n) {
+    // ---- last CTA. Shared memory (reusing sf): tsig / tprev = current /
+    //      previous flags of levels 0..R-1, intree = "cell is on the current
+    //      tree" for levels 0..R.
+    uint8_t* tsig = sf;
+    uint8_t* tprev = tsig + lo(R, 0);
+    uint8_t* intree = tprev + lo(R, 0);
+    const uint8_t* sigp = P.sig[p];
+    for (int n = R - 1; n >= 0; --n) {  // band + closure, levels R-1 .. 0
         const uint32_t cnt = 1u << (2 * n);
         for (uint32_t m = threadIdx.x; m < cnt; m += kThreads) {
             uint8_t b = band_flag(P, pre, n, m);
-            const uint8_t* c = sigc + P.fbase[n + 1] + 4u * m;
-            if (n + 1 < L && (ldcg_u8(c) | ldcg_u8(c + 1) | ldcg_u8(c + 2) | ldcg_u8(c + 3))) b = 1;
+            if (n == R - 1) {
+                const uint8_t* c = sigc + P.fbase[n + 1] + 4u * m;
+                if (ldcg_u8(c) | ldcg_u8(c + 1) | ldcg_u8(c + 2) | ldcg_u8(c + 3)) b = 1;
+            } else {
+                const uint8_t* c = tsig + lo(n + 1, 0) + 4u * m;
+                if (c[0] | c[1] | c[2] | c[3]) b = 1;
+            }
             sigc[P.fbase[n] + m] = b;
+            tsig[lo(n, 0) + m] = b;
+            tprev[lo(n, 0) + m] = sigp[P.fbase[n] + m];
         }
-        __threadfence_block();
         __syncthreads();
     }
-    // ---- final per-subtree counts and their exclusive scan
+    if (threadIdx.x == 0) intree[0] = 1;
+    __syncthreads();
+    for (int n = 1; n <= R; ++n) {
+        const uint32_t cnt = 1u << (2 * n);
+        for (uint32_t m = threadIdx.x; m < cnt; m += kThreads)
+            intree[lo(n, 0) + m] = intree[lo(n - 1, 0) + (m >> 2)] & tsig[lo(n - 1, 0) + (m >> 2)];
+        __syncthreads();
+    }
+    // decode (projection, D4) of levels 1..R: a cell on the tree below a newly
+    // significant ancestor takes the value of the topmost such ancestor; the
+    // level-R result is also each subtree's inherited source for K3
+    {
+        double4* buf = P.cells[p];
+        unsigned nnew = 0;
+        for (int n = 0; n < R; ++n) {
+            const uint32_t cnt = 1u << (2 * n);
+            for (uint32_t m = threadIdx.x; m < cnt; m += kThreads)
+                nnew += (tsig[lo(n, 0) + m] && !tprev[lo(n, 0) + m]) ? 1u : 0u;
+        }
+        for (int n = 1; n <= R; ++n) {
+            const uint32_t cnt = 1u << (2 * n);
+            for (uint32_t m = threadIdx.x; m < cnt; m += kThreads) {
+                uint32_t src = kNoSrc;
+                if (intree[lo(n, 0) + m]) {
+                    for (int k = 0; k < n; ++k) {
+                        const uint32_t a = lo(k, 0) + (m >> (2 * (n - k)));
+                        if (tsig[a] && !tprev[a]) {
+                            src = zo::z_of(k, m >> (2 * (n - k)));
+                            break;
+                        }
+                    }
+                    if (src != kNoSrc) write_projection(buf, P, n, m, src);
+                }
+                if (n == R) P.tile_src[m] = src;
+            }
+        }
+        const unsigned tn = block_sum(nnew, s_red);
+        if (threadIdx.x == 0 && tn) atomicAdd(&ctl->cnt_new, (unsigned long long)tn);
+    }
+    // ---- per-subtree leaf counts, their exclusive scan, and each subtree's
+    //      traversal depth (R = reached, else the level of its covering leaf)
     const uint32_t nt = static_cast<uint32_t>(P.n_tiles);
     const uint32_t per = (nt + kThreads - 1) / kThreads;
     const uint32_t a = threadIdx.x * per;
     const uint32_t b = min(nt, a + per);
     unsigned local = 0;
     for (uint32_t t = a; t < b; ++t) {
-        int n = 0;
-        while (n < R && ldcg_u8(sigc + P.fbase[n] + (t >> (2 * (R - n))))) ++n;
+        int n = R;
+        while (!intree[lo(n, 0) + (t >> (2 * (R - n)))]) --n;
         unsigned c;
         if (n == R) c = ldcg_u32(P.tile_cnt + t);
         else c = ((t & ((1u << (2 * (R - n))) - 1u)) == 0u) ? 1u : 0u;
+        P.tile_lvl[t] = static_cast<uint32_t>(n);
         P.tile_off[t] = c;  // temporarily the count
         local += c;
     }
@@ -502,25 +559,10 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
     }
 }
 
-// =========================================================================== K3
-// decode_tree (SPEC.md:146-154) under D4 + PTT (SPEC.md:227-235, Alg. 5) +
-// compact_leaves (SPEC.md:236-244). In physical units a zero-detail decode is
-// a copy of the parent's (h, qx, qy) to its children (SPEC.md:153), so a cell
-// below a chain of newly significant cells takes the value of the chain's top.
-__device__ __forceinline__ void write_projection(double4* buf, const Params& P, int n, uint32_t m, uint32_t src) {
-    const int ns = zo::level_of(src);
-    const double4 v = ld4_cg(buf + P.base[ns] + (src - zo::level_offset(ns)));
-    double4* dst = buf + P.base[n] + m;
-    const double4 old = ld4_cg(dst);
-    st4(dst, make_double4(v.x, v.y, v.z, old.w));
-}
-
 __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int force) {
     if (!force && !active(ctl, P)) return;
     extern __shared__ uint32_t smem3[];
     __shared__ unsigned s_red[32];
-    __shared__ int s_reached, s_leafn;
-    __shared__ uint32_t s_rootsrc;
     const int p = ctl->parity;
     double4* buf = P.cells[p];
     const uint8_t* sigc = P.sig[p ^ 1];
@@ -539,54 +581,15 @@ __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int f
             sp[lo(n, R) + pi] = sigp[P.fbase[n] + j * cnt + pi];
         }
     }
-    if (threadIdx.x == 0) {
-        int reached = 1, leafn = R;
-        uint32_t s = kNoSrc;
-        for (int n = 0; n < R; ++n) {
-            const uint32_t a = j >> (2 * (R - n));
-            if (!sigc[P.fbase[n] + a]) {
-                reached = 0;
-                leafn = n;
-                break;
-            }
-            if (s == kNoSrc && !sigp[P.fbase[n] + a]) s = zo::z_of(n, a);
-        }
-        s_reached = reached;
-        s_leafn = leafn;
-        s_rootsrc = s;
-    }
     __syncthreads();
-    const bool reached = s_reached != 0;
+    const uint32_t leafn = P.tile_lvl[j];
+    const uint32_t rootsrc = P.tile_src[j];
+    const bool reached = leafn == static_cast<uint32_t>(R);
     unsigned nnew = 0;
-
-    // ---- top levels 1 .. R-1 are projected by CTA 0 (each cell walks its chain)
-    if (j == 0) {
-        for (int n = 1; n < R; ++n) {
-            const uint32_t cnt = 1u << (2 * n);
-            for (uint32_t m = threadIdx.x; m < cnt; m += kThreads) {
-                uint32_t s = kNoSrc;
-                bool ok = true;
-                for (int k = 0; k < n; ++k) {
-                    const uint32_t a = m >> (2 * (n - k));
-                    if (!sigc[P.fbase[k] + a]) { ok = false; break; }
-                    if (s == kNoSrc && !sigp[P.fbase[k] + a]) s = zo::z_of(k, a);
-                }
-                if (ok && s != kNoSrc) write_projection(buf, P, n, m, s);
-            }
-        }
-        for (int n = 0; n < R; ++n) {
-            const uint32_t cnt = 1u << (2 * n);
-            for (uint32_t m = threadIdx.x; m < cnt; m += kThreads)
-                nnew += (sigc[P.fbase[n] + m] && !sigp[P.fbase[n] + m]) ? 1u : 0u;
-        }
-    }
 
     if (reached) {
         // ---- projection inside the subtree, top-down
-        if (threadIdx.x == 0) {
-            src[0] = s_rootsrc;
-            if (s_rootsrc != kNoSrc) write_projection(buf, P, R, j, s_rootsrc);
-        }
+        if (threadIdx.x == 0) src[0] = rootsrc;  // the root itself was projected by K2
         __syncthreads();
         for (int n = R; n < L; ++n) {
             const uint32_t cnt = 1u << (2 * (n - R));
@@ -615,7 +618,7 @@ __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int f
     // ---- PTT + compaction into leaves[tile_off[j] ...]
     const uint32_t base_out = P.tile_off[j];
     if (!reached) {
-        const int n = s_leafn;
+        const int n = static_cast<int>(leafn);
         if (threadIdx.x == 0 && ((j & ((1u << (2 * (R - n))) - 1u)) == 0u))
             P.leaves[base_out] = zo::z_of(n, j >> (2 * (R - n)));
         return;
@@ -737,7 +740,7 @@ __device__ __forceinline__ unsigned long long covering(const Params& P, const ui
 // FV1 over the leaf list: persistent grid-stride, one thread per
 // leaf; reads the current buffer, writes leaf slots of the other (D15).
 template <bool UNIFORM>
-__global__ void __launch_bounds__(kThreads) k_fv1(Params P, Ctl* ctl) {
+__global__ void __launch_bounds__(kThreads, 3) k_fv1(Params P, Ctl* ctl) {
     if (!active(ctl, P)) return;
     const int p = ctl->parity;
     const double4* __restrict__ cur = P.cells[p];
@@ -758,24 +761,21 @@ __global__ void __launch_bounds__(kThreads) k_fv1(Params P, Ctl* ctl) {
             n = zo::level_of(z);
             m = z - zo::level_offset(n);
         }
-        const double4 own = ld4_nc(cur + P.base[n] + m);
-        double4 nb[4];
-#pragma unroll
-        for (int d = 0; d < 4; ++d) {
+        const double4 o4 = ld4_nc(cur + P.base[n] + m);
+        const CellV own = make_cell(o4, P.phys);
+        // the W, E, N, S neighbour as seen by its face (ghost on the boundary)
+        auto neighbour = [&](int d) -> CellV {
             const uint32_t nm = zo::neighbour_dev(n, m, static_cast<zo::Direction>(d));
-            if (nm == zo::kNone) {
-                nb[d] = boundary_state(own, P.bc[d], d, inflow, P.inflow_mode, P.phys.hdry);
-            } else {
-                const unsigned long long off = UNIFORM ? (P.base[n] + nm) : covering(P, sigc, n, nm);
-                nb[d] = ld4_nc(cur + off);
-            }
-        }
+            if (nm == zo::kNone) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, P.phys);
+            const unsigned long long off = UNIFORM ? (P.base[n] + nm) : covering(P, sigc, n, nm);
+            return make_cell(ld4_nc(cur + off), P.phys);
+        };
         double hn, qxn, qyn;
         const double dx = P.dx[n];
-        fv1_cell(own, nb, dx, dt, P.phys, hn, qxn, qyn);
+        fv1_cell_seq(own, neighbour, P.inv_dx[n], dt, P.phys, hn, qxn, qyn);
         if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))
             report_error(ctl, kErrNonFinite, zo::z_of(n, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2), kStageFV1);
-        st4(nxt + P.base[n] + m, make_double4(hn, qxn, qyn, own.w));
+        st4(nxt + P.base[n] + m, make_double4(hn, qxn, qyn, o4.w));
         const double c = cfl_cell(hn, qxn, qyn, dx, P.phys);
         mn = c < mn ? c : mn;
     }

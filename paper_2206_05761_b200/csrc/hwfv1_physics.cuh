@@ -35,17 +35,34 @@ __device__ __forceinline__ double recon(double h, double z, double zf, double hd
     return hs;
 }
 
+// A cell as seen by a face: depth, bed, and its velocities / celerity formed
+// once per cell (the per-face recomputation in the oracle gives the same bits:
+// vel() and sqrt() of identical inputs).
+struct CellV {
+    double h, qx, qy, z;  // physical state
+    double ux, uy;        // vel(h, qx), vel(h, qy)
+    double c;             // sqrt(g h)
+};
+__device__ __forceinline__ CellV make_cell(double4 s, const PhysParams& p) {
+    CellV c;
+    c.h = s.x; c.qx = s.y; c.qy = s.z; c.z = s.w;
+    c.ux = vel(s.x, s.y, p.hdry);
+    c.uy = vel(s.x, s.z, p.hdry);
+    c.c = sqrt(p.g * s.x);
+    return c;
+}
+
 // HLL flux in the face-normal frame (h, q_n, q_t); identical expression
-// order to oracle/hwfv1_oracle.cpp hll().
-__device__ __forceinline__ void hll(double hL, double uL, double vL, double hR, double uR, double vR,
-                                    const PhysParams& p, double F[3]) {
+// order to oracle/hwfv1_oracle.cpp hll(). cLc / cRc are sqrt(g h) of the
+// cells, reused when the reconstructed depth equals the cell depth.
+__device__ __forceinline__ void hll(double hL, double uL, double vL, double hR, double uR, double vR, double cL,
+                                    double cR, const PhysParams& p, double F[3]) {
     if (hL == 0.0 && hR == 0.0) {
         F[0] = 0.0; F[1] = 0.0; F[2] = 0.0;
         return;
     }
     const double qL = hL * uL, qR = hR * uR;
     const double tL = hL * vL, tR = hR * vR;
-    const double cL = sqrt(p.g * hL), cR = sqrt(p.g * hR);
     double SL, SR;
     if (hL == 0.0) {
         SL = uR - 2.0 * cR;
@@ -77,97 +94,167 @@ __device__ __forceinline__ void hll(double hL, double uL, double vL, double hR, 
     }
 }
 
-// One face, cells given in the normal frame as (h, q_n, q_t, z).
-__device__ __forceinline__ void face(double Lh, double Ln, double Lt, double Lz, double Rh, double Rn, double Rt,
-                                     double Rz, const PhysParams& p, double F[3], double& hLs, double& hRs) {
-    const double zf = (Lz > Rz) ? Lz : Rz;
-    hLs = recon(Lh, Lz, zf, p.hdry);
-    hRs = recon(Rh, Rz, zf, p.hdry);
-    const double uL = vel(Lh, Ln, p.hdry), vL = vel(Lh, Lt, p.hdry);
-    const double uR = vel(Rh, Rn, p.hdry), vR = vel(Rh, Rt, p.hdry);
-    hll(hLs, uL, vL, hRs, uR, vR, p, F);
+// One face between left cell L and right cell R; xface selects the normal
+// (x: normal qx / tangential qy; y: normal qy / tangential qx). Returns the
+// flux and the reconstructed depths.
+__device__ __forceinline__ void face(const CellV& L, const CellV& R, bool xface, const PhysParams& p, double F[3],
+                                     double& hLs, double& hRs) {
+    const double zf = (L.z > R.z) ? L.z : R.z;
+    hLs = recon(L.h, L.z, zf, p.hdry);
+    hRs = recon(R.h, R.z, zf, p.hdry);
+    if (hLs == 0.0 && hRs == 0.0) {
+        F[0] = 0.0; F[1] = 0.0; F[2] = 0.0;
+        return;
+    }
+    const double cL = (hLs == L.h) ? L.c : sqrt(p.g * hLs);
+    const double cR = (hRs == R.h) ? R.c : sqrt(p.g * hRs);
+    if (xface) hll(hLs, L.ux, L.uy, hRs, R.ux, R.uy, cL, cR, p, F);
+    else hll(hLs, L.uy, L.ux, hRs, R.uy, R.ux, cL, cR, p, F);
 }
 
-// Deterministic cube root (D2): same bit-level seed and Newton
-// iterations as the oracle, IEEE ops only.
-__device__ __forceinline__ double cbrt_det(double x) {
+// Deterministic inverse cube root (D2): same bit-level seed and
+// division-free Newton steps as the oracle, IEEE ops only.
+__device__ __forceinline__ double rcbrt_det(double x) {
     unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
-    b = b / 3ull + 0x2A9F7893782DA1CEull;
+    b = 0x553EF0FF289DD796ull - b / 3ull;
     double y = __longlong_as_double(static_cast<long long>(b));
+    const double third = 1.0 / 3.0;
 #pragma unroll
-    for (int it = 0; it < 5; ++it) y = ((2.0 * y) + (x / (y * y))) / 3.0;
+    for (int it = 0; it < 4; ++it) {
+        const double t = (x * y) * (y * y);
+        y = y + ((y * (1.0 - t)) * third);
+    }
     return y;
 }
 
-// CFL bound of one cell; +inf when dry.
+// CFL bound of one cell; +inf when dry. max(|qx|,|qy|)/h == max(|u|,|v|)
+// exactly (correctly rounded division is monotone).
 __device__ __forceinline__ double cfl_cell(double h, double qx, double qy, double dx, const PhysParams& p) {
     if (!(h >= p.hdry)) return __longlong_as_double(0x7FF0000000000000ll);
-    const double au = absd(qx / h), av = absd(qy / h);
-    const double s = ((au > av) ? au : av) + sqrt(p.g * h);
+    const double aq = max2(absd(qx), absd(qy));
+    const double s = (aq / h) + sqrt(p.g * h);
     return dx / s;
 }
 
-// Boundary ghost state; own = physical (h, qx, qy, z); dir W=0,E=1,N=2,S=3.
-__device__ __forceinline__ double4 boundary_state(double4 own, int kind, int dir, double inflow_value, int mode,
-                                                  double hdry) {
-    double4 o = own;
+// Boundary ghost state (D10); dir W=0,E=1,N=2,S=3. The
+// ghost's velocities follow exactly from the interior's (negation and copy
+// are exact); an inflow ghost gets fresh ones.
+__device__ __forceinline__ CellV boundary_cell(const CellV& own, int kind, int dir, double inflow_value, int mode,
+                                               const PhysParams& p) {
+    CellV o = own;
     const bool xface = (dir == 0 || dir == 1);
-    if (kind == 0) {  // reflective
-        if (xface) o.y = -own.y; else o.z = -own.z;
+    if (kind == 0) {  // reflective: negate the normal discharge
+        // vel(h, -q): -(q/h) when wet (exact), +0 when dry (as the oracle)
+        if (xface) { o.qx = -own.qx; o.ux = (own.h >= p.hdry) ? -own.ux : 0.0; }
+        else { o.qy = -own.qy; o.uy = (own.h >= p.hdry) ? -own.uy : 0.0; }
     } else if (kind == 2) {  // inflow
         double hg;
         if (mode == 1) {
-            const double d = inflow_value - own.w;
+            const double d = inflow_value - own.z;
             hg = (d > 0.0) ? d : 0.0;
         } else {
             hg = inflow_value;
         }
-        const double un = xface ? vel(own.x, own.y, hdry) : vel(own.x, own.z, hdry);
-        o.x = hg;
-        if (xface) { o.y = hg * un; o.z = 0.0; }
-        else { o.y = 0.0; o.z = hg * un; }
+        const double un = xface ? own.ux : own.uy;
+        double4 g4;
+        g4.x = hg;
+        g4.w = own.z;
+        if (xface) { g4.y = hg * un; g4.z = 0.0; }
+        else { g4.y = 0.0; g4.z = hg * un; }
+        o = make_cell(g4, p);
     }
     return o;
 }
 
-// FV1 leaf update (spatial operator + Euler + clamp + friction). nb[d] are
-// the W, E, N, S neighbour states (physical). Returns (h, qx, qy).
-__device__ __forceinline__ void fv1_cell(const double4 own, const double4 nb[4], double dx, double dt,
+// FV1 leaf update (spatial operator + Euler + clamp + friction); nb = W, E,
+// N, S neighbour cells. Returns (h, qx, qy). Same pinned expressions as
+// oracle fv1_cell().
+__device__ __forceinline__ void fv1_cell(const CellV& own, const CellV nb[4], double idx, double dt,
                                          const PhysParams& p, double& hn, double& qxn, double& qyn) {
-    const double h = own.x, qx = own.y, qy = own.z;
+    const double h = own.h;
+    const double hh = h * h;
     double FE[3], FW[3], GN[3], GS[3], hLs, hRs;
-    // east face: own is left, x-frame (h, qx, qy, z)
-    face(own.x, own.y, own.z, own.w, nb[1].x, nb[1].y, nb[1].z, nb[1].w, p, FE, hLs, hRs);
-    FE[1] = FE[1] + (p.half_g * ((h * h) - (hLs * hLs)));
-    // west face: own is right
-    face(nb[0].x, nb[0].y, nb[0].z, nb[0].w, own.x, own.y, own.z, own.w, p, FW, hLs, hRs);
-    FW[1] = FW[1] + (p.half_g * ((h * h) - (hRs * hRs)));
-    // north face: own is left (south cell), y-frame (h, qy, qx, z)
-    face(own.x, own.z, own.y, own.w, nb[2].x, nb[2].z, nb[2].y, nb[2].w, p, GN, hLs, hRs);
-    GN[1] = GN[1] + (p.half_g * ((h * h) - (hLs * hLs)));
-    // south face: own is right
-    face(nb[3].x, nb[3].z, nb[3].y, nb[3].w, own.x, own.z, own.y, own.w, p, GS, hLs, hRs);
-    GS[1] = GS[1] + (p.half_g * ((h * h) - (hRs * hRs)));
+    face(own, nb[1], true, p, FE, hLs, hRs);
+    FE[1] = FE[1] + (p.half_g * (hh - (hLs * hLs)));
+    face(nb[0], own, true, p, FW, hLs, hRs);
+    FW[1] = FW[1] + (p.half_g * (hh - (hRs * hRs)));
+    face(own, nb[2], false, p, GN, hLs, hRs);
+    GN[1] = GN[1] + (p.half_g * (hh - (hLs * hLs)));
+    face(nb[3], own, false, p, GS, hLs, hRs);
+    GS[1] = GS[1] + (p.half_g * (hh - (hRs * hRs)));
 
-    const double Lh = (-((FE[0] - FW[0]) / dx)) - ((GN[0] - GS[0]) / dx);
-    const double Lqx = (-((FE[1] - FW[1]) / dx)) - ((GN[2] - GS[2]) / dx);
-    const double Lqy = (-((FE[2] - FW[2]) / dx)) - ((GN[1] - GS[1]) / dx);
+    const double Lh = (-((FE[0] - FW[0]) * idx)) - ((GN[0] - GS[0]) * idx);
+    const double Lqx = (-((FE[1] - FW[1]) * idx)) - ((GN[2] - GS[2]) * idx);
+    const double Lqy = (-((FE[2] - FW[2]) * idx)) - ((GN[1] - GS[1]) * idx);
 
     hn = h + (dt * Lh);
-    qxn = qx + (dt * Lqx);
-    qyn = qy + (dt * Lqy);
+    qxn = own.qx + (dt * Lqx);
+    qyn = own.qy + (dt * Lqy);
     if (hn < 0.0) hn = 0.0;
     if (hn < p.hdry) {
         qxn = 0.0;
         qyn = 0.0;
     } else if (p.nM > 0.0) {
-        const double u = qxn / hn, v = qyn / hn;
-        const double sp = sqrt((u * u) + (v * v));
-        if (sp > 0.0) {
-            const double Cf = p.g_nM2 / cbrt_det(hn);
-            const double den = 1.0 + (((dt * Cf) * sp) / hn);
-            qxn = qxn / den;
-            qyn = qyn / den;
+        const double qm = sqrt((qxn * qxn) + (qyn * qyn));
+        if (qm > 0.0) {
+            const double Cf = p.g_nM2 * rcbrt_det(hn);
+            const double den = 1.0 + (((dt * Cf) * qm) / (hn * hn));
+            const double r = 1.0 / den;
+            qxn = qxn * r;
+            qyn = qyn * r;
+        }
+    }
+}
+
+// Same update as fv1_cell, with the neighbours produced one face at a time
+// by `get(d)` so only one neighbour is live (register pressure / occupancy).
+template <class GetNb>
+__device__ __forceinline__ void fv1_cell_seq(const CellV& own, GetNb&& get, double idx, double dt,
+                                             const PhysParams& p, double& hn, double& qxn, double& qyn) {
+    const double h = own.h;
+    const double hh = h * h;
+    double hLs, hRs, F[3];
+    double dFx0, dFx1, dFx2, dGy0, dGy1, dGy2;
+    {
+        const CellV e = get(1);
+        face(own, e, true, p, F, hLs, hRs);
+        const double FE0 = F[0], FE1 = F[1] + (p.half_g * (hh - (hLs * hLs))), FE2 = F[2];
+        const CellV w = get(0);
+        face(w, own, true, p, F, hLs, hRs);
+        const double FW1 = F[1] + (p.half_g * (hh - (hRs * hRs)));
+        dFx0 = FE0 - F[0];
+        dFx1 = FE1 - FW1;
+        dFx2 = FE2 - F[2];
+    }
+    {
+        const CellV nn = get(2);
+        face(own, nn, false, p, F, hLs, hRs);
+        const double GN0 = F[0], GN1 = F[1] + (p.half_g * (hh - (hLs * hLs))), GN2 = F[2];
+        const CellV ss = get(3);
+        face(ss, own, false, p, F, hLs, hRs);
+        const double GS1 = F[1] + (p.half_g * (hh - (hRs * hRs)));
+        dGy0 = GN0 - F[0];
+        dGy1 = GN1 - GS1;
+        dGy2 = GN2 - F[2];
+    }
+    const double Lh = (-(dFx0 * idx)) - (dGy0 * idx);
+    const double Lqx = (-(dFx1 * idx)) - (dGy2 * idx);
+    const double Lqy = (-(dFx2 * idx)) - (dGy1 * idx);
+    hn = h + (dt * Lh);
+    qxn = own.qx + (dt * Lqx);
+    qyn = own.qy + (dt * Lqy);
+    if (hn < 0.0) hn = 0.0;
+    if (hn < p.hdry) {
+        qxn = 0.0;
+        qyn = 0.0;
+    } else if (p.nM > 0.0) {
+        const double qm = sqrt((qxn * qxn) + (qyn * qyn));
+        if (qm > 0.0) {
+            const double Cf = p.g_nM2 * rcbrt_det(hn);
+            const double den = 1.0 + (((dt * Cf) * qm) / (hn * hn));
+            const double r = 1.0 / den;
+            qxn = qxn * r;
+            qyn = qyn * r;
         }
     }
 }

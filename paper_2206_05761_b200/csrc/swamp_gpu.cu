@@ -104,20 +104,24 @@ int validate(const swamp_config* c) {
 void launch_step_kernels(swamp_gpu* g, bool timed) {
     Params& P = g->P;
     cudaStream_t s = g->stream;
-    if (timed) cudaEventRecord(g->ev[0], s);
+    // event record NODES inside a captured graph need the External flag
+    auto mark = [&](int k) {
+        if (timed) cudaEventRecordWithFlags(g->ev[k], s, cudaEventRecordExternal);
+    };
+    mark(0);
     if (g->uniform) {
         hwfv1::k_fv1<true><<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl);
-        if (timed) for (int k = 1; k < 5; ++k) cudaEventRecord(g->ev[k], s);
+        for (int k = 1; k < 5; ++k) mark(k);
         return;
     }
     hwfv1::k_encode<false><<<P.n_tiles, kThreads, g->smem_k1, s>>>(P, g->ctl);
-    if (timed) cudaEventRecord(g->ev[1], s);
+    mark(1);
     hwfv1::k_band<<<P.n_tiles, kThreads, g->smem_k2, s>>>(P, g->ctl, 0);
-    if (timed) cudaEventRecord(g->ev[2], s);
+    mark(2);
     hwfv1::k_traverse<<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 0);
-    if (timed) cudaEventRecord(g->ev[3], s);
+    mark(3);
     hwfv1::k_fv1<false><<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl);
-    if (timed) cudaEventRecord(g->ev[4], s);
+    mark(4);
 }
 
 // graph1: one step; graphS: kGraphSteps steps; graphT: one step with event
@@ -201,7 +205,10 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     P.phys.hdry = cfg->h_dry;
     P.phys.nM = cfg->manning;
     P.phys.g_nM2 = cfg->g * (cfg->manning * cfg->manning);
-    for (int n = 0; n <= L; ++n) P.dx[n] = std::ldexp(cfg->width, -n);
+    for (int n = 0; n <= L; ++n) {
+        P.dx[n] = std::ldexp(cfg->width, -n);
+        P.inv_dx[n] = 1.0 / P.dx[n];
+    }
     // level layout: each level's slice rounded up to 8 cells (256 B)
     unsigned long long off = 0, foff = 0;
     for (int n = 0; n <= L; ++n) {
@@ -223,6 +230,8 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     if ((st = dalloc(g, &P.leaves, nf * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.tile_cnt, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.tile_off, P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    if ((st = dalloc(g, &P.tile_lvl, P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    if ((st = dalloc(g, &P.tile_src, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &g->ctl, sizeof(Ctl)))) return fail(st);
     if (cudaMallocHost(&g->ctl_host, sizeof(Ctl)) != cudaSuccess) return fail(SWAMP_E_NOMEM);
     double *d_it = nullptr, *d_iv = nullptr, *d_out = nullptr;
@@ -273,7 +282,8 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     for (int n = 0; n < L; ++n) P.tau[n] = std::ldexp(cfg->epsilon, 2 * n - 2 * L + 2);
 
     g->smem_k1 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u) * sizeof(double4);
-    g->smem_k2 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u);
+    g->smem_k2 = std::max<size_t>(((1u << (2 * P.K)) - 1u) / 3u,
+                                  2 * (((1u << (2 * P.R)) - 1u) / 3u) + ((1u << (2 * (P.R + 1))) - 1u) / 3u);
     g->smem_k3 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u) * 6;
     {
         int occ = 0;
