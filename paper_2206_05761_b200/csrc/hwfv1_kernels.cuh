@@ -224,9 +224,9 @@ __device__ __forceinline__ unsigned block_exscan(unsigned v, unsigned* scratch, 
 
 // last-CTA election: every CTA fences its global writes, then bumps a counter
 __device__ __forceinline__ bool last_block(unsigned int* counter, int* s_flag) {
-    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
+        __threadfence();
         const unsigned prev = atomicAdd(counter, 1u);
         *s_flag = (prev == gridDim.x - 1) ? 1 : 0;
     }
@@ -252,7 +252,28 @@ __global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
     const uint8_t* sigp = P.sig[p];
     const int L = P.L, R = P.R, K = P.K;
     const uint32_t j = blockIdx.x;
+    const uint32_t ncell = ((1u << (2 * K)) - 1u) / 3u;  // subtree cells on levels R..L-1
+    uint8_t* sfl = reinterpret_cast<uint8_t*>(sv + ncell);  // previous-tree flags of the subtree
     unsigned tree = 0;
+
+    // ---- all global reads that do not depend on this step's results are
+    //      issued up front: the subtree's previous-tree flags, then the values
+    //      of previous-tree leaves whose parent gets re-encoded here
+    for (int n = R; n < L; ++n) {
+        const uint32_t cnt = 1u << (2 * (n - R));
+        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads)
+            sfl[lo(n, R) + pi] = INIT ? 1 : sigp[P.fbase[n] + j * cnt + pi];
+    }
+    __syncthreads();
+    if (!INIT) {
+        for (int n = R + 1; n < L; ++n) {
+            const uint32_t cnt = 1u << (2 * (n - R));
+            for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
+                const uint32_t li = lo(n, R) + pi;
+                if (!sfl[li] && sfl[lo(n - 1, R) + (pi >> 2)]) sv[li] = ld4(buf + P.base[n] + j * cnt + pi);
+            }
+        }
+    }
 
     // ---- finest level: one thread per level-(L-1) parent; its 4 children are
     //      128 contiguous bytes, read with four 256-bit loads
@@ -260,72 +281,61 @@ __global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
         const int n = L - 1;
         const uint32_t npar = 1u << (2 * (K - 1));
         const uint32_t pbase = j * npar;
-        const bool store_smem = n > R;
 #pragma unroll 2
         for (uint32_t pi = threadIdx.x; pi < npar; pi += kThreads) {
             const uint32_t pm = pbase + pi;
-            const bool sp = INIT || sigp[P.fbase[n] + pm];
+            const bool sp = sfl[lo(n, R) + pi] != 0;
             const uint8_t d0 = INIT ? 0 : P.dem[P.fbase[n] + pm];
-            double4 par = make_double4(0.0, 0.0, 0.0, 0.0);
             bool flow, zf = false;
             if (sp) {
                 const double4* cp = buf + P.base[L] + (static_cast<unsigned long long>(pm) << 2);
                 const double4 c[4] = {ld4_nc(cp), ld4_nc(cp + 1), ld4_nc(cp + 2), ld4_nc(cp + 3)};
                 const Enc e = encode_children<INIT>(c, P, n);
-                par = e.par;
                 flow = e.flow;
                 zf = e.zflag;
-                st4(buf + P.base[n] + pm, par);
+                st4(buf + P.base[n] + pm, e.par);
+                if (n > R) sv[lo(n, R) + pi] = e.par;
                 ++tree;
             } else {
                 flow = 0.0 >= P.tau[n];
-                if (store_smem && sigp[P.fbase[n - 1] + (pm >> 2)]) par = ld4(buf + P.base[n] + pm);
             }
-            uint8_t d;
+            uint8_t d = d0;
             if (INIT) {
                 d = zf ? 1 : 0;
                 P.dem[P.fbase[n] + pm] = d;
-            } else {
-                d = d0;
             }
             P.pre[P.fbase[n] + pm] = (flow || d) ? 1 : 0;
-            if (store_smem) sv[lo(n, R) + pi] = par;
         }
     }
     __syncthreads();
 
-    // ---- levels L-2 .. R inside the subtree, children from shared memory
+    // ---- levels L-2 .. R inside the subtree: shared memory only
     for (int n = L - 2; n >= R; --n) {
         const uint32_t cnt = 1u << (2 * (n - R));
         const uint32_t pb = j * cnt;
-        const bool store_smem = n > R;
         for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
             const uint32_t pm = pb + pi;
-            const bool sp = INIT || sigp[P.fbase[n] + pm];
-            double4 par = make_double4(0.0, 0.0, 0.0, 0.0);
+            const bool sp = sfl[lo(n, R) + pi] != 0;
+            const uint8_t d0 = INIT ? 0 : P.dem[P.fbase[n] + pm];
             bool flow, zf = false;
             if (sp) {
                 const uint32_t c0 = lo(n + 1, R) + 4u * pi;
                 const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
                 const Enc e = encode_children<INIT>(c, P, n);
-                par = e.par;
                 flow = e.flow;
                 zf = e.zflag;
-                st4(buf + P.base[n] + pm, par);
+                st4(buf + P.base[n] + pm, e.par);
+                if (n > R) sv[lo(n, R) + pi] = e.par;
                 ++tree;
             } else {
                 flow = 0.0 >= P.tau[n];
-                if (store_smem && sigp[P.fbase[n - 1] + (pm >> 2)]) par = ld4(buf + P.base[n] + pm);
             }
-            uint8_t d;
+            uint8_t d = d0;
             if (INIT) {
                 d = zf ? 1 : 0;
                 P.dem[P.fbase[n] + pm] = d;
-            } else {
-                d = P.dem[P.fbase[n] + pm];
             }
             P.pre[P.fbase[n] + pm] = (flow || d) ? 1 : 0;
-            if (store_smem) sv[lo(n, R) + pi] = par;
         }
         __syncthreads();
     }
@@ -397,22 +407,24 @@ __device__ __forceinline__ void write_projection(double4* buf, const Params& P, 
 }
 
 // =========================================================================== K2
-// band (D3) of cell (n, m) from the pre-band flags (flow | DEM)
-__device__ __forceinline__ uint8_t band_flag(const Params& P, const uint8_t* pre, int n, uint32_t m) {
-    uint8_t b = pre[P.fbase[n] + m];
-    if (P.band_mode == 2) {
+// band (D3) of cell (n, m) from the pre-band flags (flow | DEM);
+// `pre_at(level, morton)` reads a pre flag (global or shared memory)
+template <class PreAt>
+__device__ __forceinline__ uint8_t band_flag(int mode, int L, int n, uint32_t m, PreAt&& pre_at) {
+    uint8_t b = pre_at(n, m);
+    if (mode == 2) {
 #pragma unroll
         for (int d = 0; d < 4; ++d) {
             const uint32_t nb = zo::neighbour_dev(n, m, static_cast<zo::Direction>(d));
-            if (nb != zo::kNone) b |= pre[P.fbase[n] + nb];
+            if (nb != zo::kNone) b |= pre_at(n, nb);
         }
-    } else if (P.band_mode == 1 && n + 1 < P.L) {
+    } else if (mode == 1 && n + 1 < L) {
         for (int k = 0; k < 4; ++k) {
             const uint32_t c = 4u * m + static_cast<uint32_t>(k);
 #pragma unroll
             for (int d = 0; d < 4; ++d) {
                 const uint32_t nb = zo::neighbour_dev(n + 1, c, static_cast<zo::Direction>(d));
-                if (nb != zo::kNone) b |= pre[P.fbase[n + 1] + nb];
+                if (nb != zo::kNone) b |= pre_at(n + 1, nb);
             }
         }
     }
@@ -436,7 +448,9 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
 
     for (int n = R; n < L; ++n) {
         const uint32_t cnt = 1u << (2 * (n - R));
-        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) sf[lo(n, R) + pi] = band_flag(P, pre, n, j * cnt + pi);
+        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads)
+            sf[lo(n, R) + pi] = band_flag(P.band_mode, L, n, j * cnt + pi,
+                                          [&](int k, uint32_t mm) { return pre[P.fbase[k] + mm]; });
     }
     __syncthreads();
     for (int n = L - 2; n >= R; --n) {
@@ -466,27 +480,38 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
     }
     if (!last_block(&ctl->done_k2, &s_last)) return;
 
-    // ---- last CTA. Shared memory (reusing sf): tsig / tprev = current /
-    //      previous flags of levels 0..R-1, intree = "cell is on the current
-    //      tree" for levels 0..R.
-    uint8_t* tsig = sf;
-    uint8_t* tprev = tsig + lo(R, 0);
-    uint8_t* intree = tprev + lo(R, 0);
+    // ---- last CTA, all in shared memory (reusing sf): tpre / tprev = pre-band
+    //      and previous flags of levels 0..R, tsig = current flags of levels
+    //      0..R (level R written by every CTA), intree = "on the current tree",
+    //      tcnt = per-subtree counts
+    uint8_t* tsig = sf;                       // lo(R+1)
+    uint8_t* tprev = tsig + lo(R + 1, 0);     // lo(R+1)
+    uint8_t* tpre = tprev + lo(R + 1, 0);     // lo(R+1)
+    uint8_t* intree = tpre + lo(R + 1, 0);    // lo(R+1)
+    uint32_t* tcnt = reinterpret_cast<uint32_t*>(intree + ((lo(R + 1, 0) + 15u) & ~15u));  // 4^R
     const uint8_t* sigp = P.sig[p];
+    for (int n = 0; n <= R; ++n) {
+        const uint32_t cnt = 1u << (2 * n);
+        for (uint32_t m = threadIdx.x; m < cnt; m += kThreads) {
+            if (n < L) {
+                tpre[lo(n, 0) + m] = pre[P.fbase[n] + m];
+                tprev[lo(n, 0) + m] = sigp[P.fbase[n] + m];
+            }
+            if (n == R) {
+                tsig[lo(R, 0) + m] = ldcg_u8(sigc + P.fbase[R] + m);
+                tcnt[m] = ldcg_u32(P.tile_cnt + m);
+            }
+        }
+    }
+    __syncthreads();
     for (int n = R - 1; n >= 0; --n) {  // band + closure, levels R-1 .. 0
         const uint32_t cnt = 1u << (2 * n);
         for (uint32_t m = threadIdx.x; m < cnt; m += kThreads) {
-            uint8_t b = band_flag(P, pre, n, m);
-            if (n == R - 1) {
-                const uint8_t* c = sigc + P.fbase[n + 1] + 4u * m;
-                if (ldcg_u8(c) | ldcg_u8(c + 1) | ldcg_u8(c + 2) | ldcg_u8(c + 3)) b = 1;
-            } else {
-                const uint8_t* c = tsig + lo(n + 1, 0) + 4u * m;
-                if (c[0] | c[1] | c[2] | c[3]) b = 1;
-            }
+            uint8_t b = band_flag(P.band_mode, L, n, m, [&](int k, uint32_t mm) { return tpre[lo(k, 0) + mm]; });
+            const uint8_t* c = tsig + lo(n + 1, 0) + 4u * m;
+            if (c[0] | c[1] | c[2] | c[3]) b = 1;
             sigc[P.fbase[n] + m] = b;
             tsig[lo(n, 0) + m] = b;
-            tprev[lo(n, 0) + m] = sigp[P.fbase[n] + m];
         }
         __syncthreads();
     }
@@ -526,6 +551,7 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
                 if (n == R) P.tile_src[m] = src;
             }
         }
+        if (R == 0 && threadIdx.x == 0) P.tile_src[0] = kNoSrc;  // the root has no ancestor
         const unsigned tn = block_sum(nnew, s_red);
         if (threadIdx.x == 0 && tn) atomicAdd(&ctl->cnt_new, (unsigned long long)tn);
     }
@@ -540,7 +566,7 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
         int n = R;
         while (!intree[lo(n, 0) + (t >> (2 * (R - n)))]) --n;
         unsigned c;
-        if (n == R) c = ldcg_u32(P.tile_cnt + t);
+        if (n == R) c = tcnt[t];
         else c = ((t & ((1u << (2 * (R - n))) - 1u)) == 0u) ? 1u : 0u;
         P.tile_lvl[t] = static_cast<uint32_t>(n);
         P.tile_off[t] = c;  // temporarily the count
@@ -574,20 +600,24 @@ __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int f
     uint8_t* sc = reinterpret_cast<uint8_t*>(src + ncell);  // [ncell]
     uint8_t* sp = sc + ncell;                               // [ncell]
 
-    for (int n = R; n < L; ++n) {
-        const uint32_t cnt = 1u << (2 * (n - R));
-        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
-            sc[lo(n, R) + pi] = sigc[P.fbase[n] + j * cnt + pi];
-            sp[lo(n, R) + pi] = sigp[P.fbase[n] + j * cnt + pi];
-        }
-    }
-    __syncthreads();
     const uint32_t leafn = P.tile_lvl[j];
     const uint32_t rootsrc = P.tile_src[j];
     const bool reached = leafn == static_cast<uint32_t>(R);
+    int any_new = 0;
+    for (int n = R; n < L; ++n) {
+        const uint32_t cnt = 1u << (2 * (n - R));
+        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
+            const uint8_t c = sigc[P.fbase[n] + j * cnt + pi], q = sigp[P.fbase[n] + j * cnt + pi];
+            sc[lo(n, R) + pi] = c;
+            sp[lo(n, R) + pi] = q;
+            any_new |= (c && !q) ? 1 : 0;
+        }
+    }
+    // decode is needed only where something became significant
+    any_new = __syncthreads_or(any_new | (rootsrc != kNoSrc ? 1 : 0));
     unsigned nnew = 0;
 
-    if (reached) {
+    if (reached && any_new) {
         // ---- projection inside the subtree, top-down
         if (threadIdx.x == 0) src[0] = rootsrc;  // the root itself was projected by K2
         __syncthreads();

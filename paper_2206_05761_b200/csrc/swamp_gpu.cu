@@ -281,9 +281,16 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     // significance threshold in physical units: eps * 2^(2n-2L+2) (D7)
     for (int n = 0; n < L; ++n) P.tau[n] = std::ldexp(cfg->epsilon, 2 * n - 2 * L + 2);
 
-    g->smem_k1 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u) * sizeof(double4);
-    g->smem_k2 = std::max<size_t>(((1u << (2 * P.K)) - 1u) / 3u,
-                                  2 * (((1u << (2 * P.R)) - 1u) / 3u) + ((1u << (2 * (P.R + 1))) - 1u) / 3u);
+    g->smem_k1 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u) * (sizeof(double4) + 1);
+    {
+        const size_t top = ((1u << (2 * (P.R + 1))) - 1u) / 3u;  // cells on levels 0..R
+        g->smem_k2 = std::max<size_t>(((1u << (2 * P.K)) - 1u) / 3u,
+                                      3 * top + ((top + 15) & ~size_t(15)) + 4 * (size_t(1) << (2 * P.R)));
+        if (g->smem_k2 > 48 * 1024 &&
+            cudaFuncSetAttribute(hwfv1::k_band, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(g->smem_k2)) != cudaSuccess)
+            return fail(SWAMP_E_CUDA);
+    }
     g->smem_k3 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u) * 6;
     {
         int occ = 0;
