@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
     uint8_t* tprev = tsig + lo(R + 1, 0);     // lo(R+1)
     uint8_t* tpre = tprev + lo(R + 1, 0);     // lo(R+1)
     uint8_t* intree = tpre + lo(R + 1, 0);    // lo(R+1)
-    uint32_t* tcnt = reinterpret_cast<uint32_t*>(intree + ((lo(R + 1, 0) + 15u) & ~15u));  // 4^R
+    uint32_t* tcnt = reinterpret_cast<uint32_t*>(sf + ((4u * lo(R + 1, 0) + 15u) & ~15u));  // 4^R
     const uint8_t* sigp = P.sig[p];
     for (int n = 0; n <= R; ++n) {
         const uint32_t cnt = 1u << (2 * n);

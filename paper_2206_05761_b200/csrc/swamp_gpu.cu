@@ -285,7 +285,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     {
         const size_t top = ((1u << (2 * (P.R + 1))) - 1u) / 3u;  // cells on levels 0..R
         g->smem_k2 = std::max<size_t>(((1u << (2 * P.K)) - 1u) / 3u,
-                                      3 * top + ((top + 15) & ~size_t(15)) + 4 * (size_t(1) << (2 * P.R)));
+                                      ((4 * top + 15) & ~size_t(15)) + 4 * (size_t(1) << (2 * P.R)));
         if (g->smem_k2 > 48 * 1024 &&
             cudaFuncSetAttribute(hwfv1::k_band, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(g->smem_k2)) != cudaSuccess)
