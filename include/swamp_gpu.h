@@ -160,6 +160,11 @@ int swamp_gpu_last_error(const swamp_gpu* g, int32_t* code, uint32_t* z, int32_t
  * [2] newly significant cells (decoded), [3] 4^L. */
 int swamp_gpu_counters(swamp_gpu* g, int64_t* out4);
 
+/* Device timeline of the last profiled step, microseconds from K1's first
+ * CTA: for K1, K2, K3, K5 (k = 0..3): [3k] first CTA start, [3k+1] last CTA
+ * elected (K3: unused, -1), [3k+2] last CTA / kernel done. */
+int swamp_gpu_timeline(swamp_gpu* g, double* out12);
+
 /* Build identification (arch, flags) for logs. */
 const char* swamp_gpu_build_info(void);
 

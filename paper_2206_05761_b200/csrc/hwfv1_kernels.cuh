@@ -57,7 +57,23 @@ struct Ctl {
     int err_q;
     int err_stage;
     unsigned int done_k1, done_k2, done_k5;
+    // stage timeline (globaltimer ns) of the last profiled step: for kernel k
+    // (K1, K2, K3, K5) [3k] = ~(first CTA start), [3k+1] = last CTA elected,
+    // [3k+2] = last CTA done (all via atomicMax; zeroed before the step)
+    unsigned long long tl[12];
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void tl_start(Ctl* c, int k) {
+    if (threadIdx.x == 0) atomicMax(&c->tl[3 * k], ~gtimer());
+}
+__device__ __forceinline__ void tl_mark(Ctl* c, int slot) {
+    if (threadIdx.x == 0) atomicMax(&c->tl[slot], gtimer());
+}
 
 struct Params {
     int L, R, K, n_tiles;
@@ -244,6 +260,7 @@ __device__ __forceinline__ bool last_block(unsigned int* counter, int* s_flag) {
 template <bool INIT>
 __global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
     if (!INIT && !active(ctl, P)) return;
+    tl_start(ctl, 0);
     extern __shared__ double4 sv[];
     __shared__ unsigned s_red[32];
     __shared__ int s_last;
@@ -343,6 +360,7 @@ __global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
     const unsigned tsum = block_sum(tree, s_red);
     if (threadIdx.x == 0 && tsum) atomicAdd(&ctl->cnt_tree, (unsigned long long)tsum);
     if (!last_block(&ctl->done_k1, &s_last)) return;
+    tl_mark(ctl, 1);
 
     // ---- last CTA: levels R-1 .. 0. Level R children come from global (L2,
     //      written by every CTA); above that the block keeps its results in
@@ -391,6 +409,7 @@ __global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
         if (tt) atomicAdd(&ctl->cnt_tree, (unsigned long long)tt);
         ctl->done_k1 = 0;
     }
+    tl_mark(ctl, 2);
 }
 
 // ----------------------------------------------------------- decode helper
@@ -437,6 +456,7 @@ __device__ __forceinline__ uint8_t band_flag(int mode, int L, int n, uint32_t m,
 // values instead of per finest cell).
 __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force) {
     if (!force && !active(ctl, P)) return;
+    tl_start(ctl, 1);
     extern __shared__ uint8_t sf[];
     __shared__ unsigned s_red[32];
     __shared__ int s_last;
@@ -479,6 +499,7 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
         if (threadIdx.x == 0) P.tile_cnt[j] = tot;
     }
     if (!last_block(&ctl->done_k2, &s_last)) return;
+    tl_mark(ctl, 4);
 
     // ---- last CTA, all in shared memory (reusing sf): tpre / tprev = pre-band
     //      and previous flags of levels 0..R, tsig = current flags of levels
@@ -583,10 +604,12 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
         ctl->n_leaves = total;
         ctl->done_k2 = 0;
     }
+    tl_mark(ctl, 5);
 }
 
 __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int force) {
     if (!force && !active(ctl, P)) return;
+    tl_start(ctl, 2);
     extern __shared__ uint32_t smem3[];
     __shared__ unsigned s_red[32];
     const int p = ctl->parity;
@@ -651,6 +674,7 @@ __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int f
         const int n = static_cast<int>(leafn);
         if (threadIdx.x == 0 && ((j & ((1u << (2 * (R - n))) - 1u)) == 0u))
             P.leaves[base_out] = zo::z_of(n, j >> (2 * (R - n)));
+        tl_mark(ctl, 8);
         return;
     }
     const uint32_t nc = 1u << (2 * (K - 1));  // level-(L-1) cells in the subtree
@@ -679,6 +703,8 @@ __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int f
             P.leaves[o++] = zo::z_of(n, gm >> (2 * (L - 1 - n)));
         }
     }
+    __syncthreads();
+    tl_mark(ctl, 8);
 }
 
 // =========================================================================== K5
@@ -747,11 +773,13 @@ __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ct
         atomicMin(&ctl->dtmin_bits, m);
     }
     if (!last_block(&ctl->done_k5, &s_last)) return;
+    tl_mark(ctl, 10);
     if (threadIdx.x == 0) {
         const unsigned long long m = atomicAdd(&ctl->dtmin_bits, 0ull);
         finalize_dt(P, ctl, __longlong_as_double(static_cast<long long>(m)), advance);
         ctl->dtmin_bits = 0x7FF0000000000000ull;
         ctl->done_k5 = 0;
+        ctl->tl[11] = gtimer();
     }
 }
 
@@ -772,6 +800,7 @@ __device__ __forceinline__ unsigned long long covering(const Params& P, const ui
 template <bool UNIFORM>
 __global__ void __launch_bounds__(kThreads, 3) k_fv1(Params P, Ctl* ctl) {
     if (!active(ctl, P)) return;
+    tl_start(ctl, 3);
     const int p = ctl->parity;
     const double4* __restrict__ cur = P.cells[p];
     double4* __restrict__ nxt = P.cells[p ^ 1];

@@ -108,6 +108,7 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     auto mark = [&](int k) {
         if (timed) cudaEventRecordWithFlags(g->ev[k], s, cudaEventRecordExternal);
     };
+    if (timed) cudaMemsetAsync(g->ctl->tl, 0, sizeof(g->ctl->tl), s);
     mark(0);
     if (g->uniform) {
         hwfv1::k_fv1<true><<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl);
@@ -521,6 +522,18 @@ int swamp_gpu_last_error(const swamp_gpu* g, int32_t* code, uint32_t* z, int32_t
         msg[msg_cap - 1] = 0;
     }
     return SWAMP_OK;
+}
+
+int swamp_gpu_timeline(swamp_gpu* g, double* out12) {
+    if (!g || !out12) return SWAMP_E_ARG;
+    int st = fetch_ctl(g);
+    const unsigned long long* tl = g->ctl_host->tl;
+    const unsigned long long t0 = ~tl[0];
+    for (int k = 0; k < 12; ++k) {
+        unsigned long long v = (k % 3 == 0) ? ~tl[k] : tl[k];
+        out12[k] = (tl[k] == 0 || v < t0) ? -1.0 : 1e-3 * static_cast<double>(v - t0);
+    }
+    return st;
 }
 
 int swamp_gpu_counters(swamp_gpu* g, int64_t* out4) {

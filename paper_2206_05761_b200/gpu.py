@@ -52,6 +52,7 @@ def lib():
                                            C.POINTER(C.c_int32), C.c_char_p, C.c_size_t]
         L.swamp_gpu_counters.argtypes = [P, i64p]
         L.swamp_gpu_enqueue.argtypes = [P, C.c_int64]
+        L.swamp_gpu_timeline.argtypes = [P, dp]
         L.swamp_gpu_stream.argtypes = [P, C.POINTER(C.c_void_p)]
         L.swamp_gpu_build_info.restype = C.c_char_p
         _LIB = L
@@ -63,6 +64,7 @@ EXPORTED_SYMBOLS = (
     "swamp_gpu_create_uniform", "swamp_gpu_step_uniform", "swamp_gpu_set_profiling", "swamp_gpu_info",
     "swamp_gpu_copy_leaves", "swamp_gpu_export_tree", "swamp_gpu_export_finest", "swamp_gpu_last_error",
     "swamp_gpu_counters", "swamp_gpu_build_info", "swamp_gpu_enqueue", "swamp_gpu_stream",
+    "swamp_gpu_timeline",
 )
 
 
@@ -166,6 +168,13 @@ class Engine:
         out = [np.zeros((n, n)) for _ in range(3)]
         self._check(lib().swamp_gpu_export_finest(self._h, *[dptr(a) for a in out]), "export_finest")
         return out
+
+    def timeline(self):
+        """Stage timeline (us) of the last profiled step: K1/K2/K3/K5 x
+        (first CTA start, last CTA elected, done)."""
+        a = (C.c_double * 12)()
+        self._check(lib().swamp_gpu_timeline(self._h, a), "timeline")
+        return [round(v, 2) for v in a]
 
     def counters(self):
         a = (C.c_int64 * 4)()
