@@ -783,11 +783,11 @@ __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ct
     }
 }
 
-// covering cell of the same-level neighbour region (n, nb): walk up until the
-// parent is significant (SPEC.md:248 — the level-min(n, covering-leaf) cell)
-__device__ __forceinline__ unsigned long long covering(const Params& P, const uint8_t* sigc, int n, uint32_t nb) {
-    int k = n;
-    uint32_t mm = nb;
+// covering cell of a same-level neighbour region whose parent (k, mm) is NOT
+// significant: walk up until the parent is significant (SPEC.md:248 — the
+// coarser covering leaf); the fast path (parent significant -> the same-level
+// cell itself) is tested by the caller for all four faces at once
+__device__ __forceinline__ unsigned long long covering(const Params& P, const uint8_t* sigc, int k, uint32_t mm) {
     while (k > 0 && !sigc[P.fbase[k - 1] + (mm >> 2)]) {
         mm >>= 2;
         --k;
@@ -797,8 +797,8 @@ __device__ __forceinline__ unsigned long long covering(const Params& P, const ui
 
 // FV1 over the leaf list: persistent grid-stride, one thread per
 // leaf; reads the current buffer, writes leaf slots of the other (D15).
-template <bool UNIFORM>
-__global__ void __launch_bounds__(kThreads, 3) k_fv1(Params P, Ctl* ctl) {
+template <bool UNIFORM, int MINB = 2>
+__global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     if (!active(ctl, P)) return;
     tl_start(ctl, 3);
     const int p = ctl->parity;
@@ -809,25 +809,47 @@ __global__ void __launch_bounds__(kThreads, 3) k_fv1(Params P, Ctl* ctl) {
     const double t = ctl->t, dt = ctl->dt;
     const double inflow = series_value(P, t);
     double mn = __longlong_as_double(0x7FF0000000000000ll);
-    for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < N; i += gridDim.x * kThreads) {
+    const uint32_t stride = gridDim.x * kThreads;
+    uint32_t i = blockIdx.x * kThreads + threadIdx.x;
+    uint32_t z_next = (!UNIFORM && i < N) ? P.leaves[i] : 0u;
+    for (; i < N; i += stride) {
         int n;
         uint32_t m;
         if (UNIFORM) {
             n = P.L;
             m = i;
         } else {
-            const uint32_t z = P.leaves[i];
+            const uint32_t z = z_next;  // leaf ids are prefetched one iteration ahead
+            if (i + stride < N) z_next = P.leaves[i + stride];
             n = zo::level_of(z);
             m = z - zo::level_offset(n);
         }
+        // every global read of this leaf is issued before any arithmetic: own
+        // cell, the four neighbours' parent-level flags, the four neighbours
         const double4 o4 = ld4_nc(cur + P.base[n] + m);
+        uint32_t nm[4];
+        unsigned long long off[4];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) nm[d] = zo::neighbour_dev(n, m, static_cast<zo::Direction>(d));
+        if (UNIFORM) {
+#pragma unroll
+            for (int d = 0; d < 4; ++d) off[d] = P.base[n] + nm[d];
+        } else {
+            uint8_t f[4];
+#pragma unroll
+            for (int d = 0; d < 4; ++d) f[d] = (nm[d] != zo::kNone) ? sigc[P.fbase[n - 1] + (nm[d] >> 2)] : 1;
+#pragma unroll
+            for (int d = 0; d < 4; ++d) off[d] = f[d] ? P.base[n] + nm[d] : covering(P, sigc, n - 1, nm[d] >> 2);
+        }
+        double4 r4[4];
+#pragma unroll
+        for (int d = 0; d < 4; ++d)
+            if (nm[d] != zo::kNone) r4[d] = ld4_nc(cur + off[d]);
         const CellV own = make_cell(o4, P.phys);
         // the W, E, N, S neighbour as seen by its face (ghost on the boundary)
         auto neighbour = [&](int d) -> CellV {
-            const uint32_t nm = zo::neighbour_dev(n, m, static_cast<zo::Direction>(d));
-            if (nm == zo::kNone) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, P.phys);
-            const unsigned long long off = UNIFORM ? (P.base[n] + nm) : covering(P, sigc, n, nm);
-            return make_cell(ld4_nc(cur + off), P.phys);
+            if (nm[d] == zo::kNone) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, P.phys);
+            return make_cell(r4[d], P.phys);
         };
         double hn, qxn, qyn;
         const double dx = P.dx[n];

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -46,6 +47,7 @@ struct swamp_gpu {
     std::vector<void*> allocs;
     cudaGraphExec_t graph1 = nullptr, graphS = nullptr, graphT = nullptr;
     int fv1_grid = 0;
+    int fv1_minb = 2;  // occupancy variant of k_fv1 (SWAMP_FV1_MINB=3 for 3 CTAs/SM)
     int num_sms = 0;
     size_t smem_k1 = 0, smem_k2 = 0, smem_k3 = 0;
     cudaEvent_t ev[6] = {};
@@ -121,7 +123,10 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     mark(2);
     hwfv1::k_traverse<<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 0);
     mark(3);
-    hwfv1::k_fv1<false><<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl);
+    if (g->fv1_minb == 3)
+        hwfv1::k_fv1<false, 3><<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl);
+    else
+        hwfv1::k_fv1<false, 2><<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl);
     mark(4);
 }
 
@@ -294,8 +299,12 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     }
     g->smem_k3 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u) * 6;
     {
+        if (const char* e = std::getenv("SWAMP_FV1_MINB")) g->fv1_minb = std::atoi(e) == 3 ? 3 : 2;
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false>, kThreads, 0);
+        if (g->fv1_minb == 3)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 3>, kThreads, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 2>, kThreads, 0);
         g->fv1_grid = std::max(1, occ) * g->num_sms;
     }
 
