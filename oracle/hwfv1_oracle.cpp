@@ -111,8 +111,9 @@ inline bool significant(double da, double db, double dg, double smax, int n, int
 struct Phys {
     double g, hdry, nM;
 };
-// de-singularised velocity
-inline double vel(double h, double q, double hdry) { return (h >= hdry) ? q / h : 0.0; }
+// de-singularised velocity, pinned as q * (1/h): one reciprocal
+// per cell serves both components (D2)
+inline double vel(double h, double q, double hdry) { return (h >= hdry) ? q * (1.0 / h) : 0.0; }
 // hydrostatic reconstruction of one side (D11): max(0, eta - zf),
 // depths below h_dry are treated as exactly dry.
 inline double recon(double h, double z, double zf, double hdry) {
@@ -194,18 +195,22 @@ void friction(double h, double* qx, double* qy, double dt, const Phys& p) {
     const double qm = std::sqrt((*qx * *qx) + (*qy * *qy));
     if (qm > 0.0) {
         const double Cf = (p.g * (p.nM * p.nM)) * rcbrt_det(h);
-        const double den = 1.0 + (((dt * Cf) * qm) / (h * h));
+        const double rh = 1.0 / h;
+        const double den = 1.0 + (((dt * Cf) * qm) * (rh * rh));
         const double r = 1.0 / den;
         *qx = *qx * r;
         *qy = *qy * r;
     }
 }
-// CFL bound of one cell: +inf when dry.
+// CFL rate of one cell: (max(|u|,|v|) + sqrt(gh)) / dx,
+// 0 when dry; dt = C / max rate (D13 pin: one reciprocal per cell, none per
+// reduction element).
 double cfl_cell(double h, double qx, double qy, double dx, double g, double hdry) {
-    if (!(h >= hdry)) return std::numeric_limits<double>::infinity();
+    if (!(h >= hdry)) return 0.0;
+    const double rh = 1.0 / h;
     const double aq = max2(absd(qx), absd(qy));
-    const double s = (aq / h) + std::sqrt(g * h);
-    return dx / s;
+    const double s = (aq * rh) + std::sqrt(g * h);
+    return s * (1.0 / dx);
 }
 // linear interpolation of the inflow series, last value held
 double series_value(double t, const double* ts, const double* vs, int n) {
@@ -540,8 +545,8 @@ double next_stop(const oracle_state& S, double t) {
 
 // cfl_timestep: C * min over wet leaves, fallback when all
 // dry, clipped to the next output time / t_end. Sets dt and t_next.
-bool set_dt(oracle_state& S, double mincell) {
-    double dtc = (mincell == std::numeric_limits<double>::infinity()) ? S.cfg.dt_fallback : S.cfg.cfl * mincell;
+bool set_dt(oracle_state& S, double maxrate) {
+    double dtc = (maxrate == 0.0) ? S.cfg.dt_fallback : S.cfg.cfl / maxrate;
     const double stop = next_stop(S, S.t);
     if (S.t + dtc >= stop) {
         S.dt = stop - S.t;
@@ -557,16 +562,16 @@ bool set_dt(oracle_state& S, double mincell) {
     return true;
 }
 
-double leaves_min_cfl(const oracle_state& S) {
+double leaves_max_rate(const oracle_state& S) {
     const int64_t N = (int64_t)S.leaves.size();
-    double mn = std::numeric_limits<double>::infinity();
-#pragma omp parallel for schedule(static) reduction(min : mn)
+    double mn = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : mn)
     for (int64_t i = 0; i < N; ++i) {
         double u[4];
         cell_phys(S, S.leaves[i], u);
         const int n = o_level_of(S.leaves[i]);
         const double v = cfl_cell(u[0], u[1], u[2], std::ldexp(S.cfg.width, -n), S.cfg.g, S.cfg.h_dry);
-        mn = v < mn ? v : mn;
+        mn = v > mn ? v : mn;
     }
     return mn;
 }
@@ -574,15 +579,15 @@ double leaves_min_cfl(const oracle_state& S) {
 // FV1 over the leaf assembly, writer-exclusive into U_new, then the write-back
 // (from_physical into each leaf's own slot; D15 semantics: all
 // updates read the pre-update state).
-bool fv1_all(oracle_state& S, double* mincell) {
+bool fv1_all(oracle_state& S, double* maxrate) {
     const int64_t N = (int64_t)S.leaves.size();
     const int L = S.L;
     const Phys p{S.cfg.g, S.cfg.h_dry, S.cfg.manning};
     std::vector<double> U(3 * N);
-    double mn = std::numeric_limits<double>::infinity();
+    double mn = 0.0;
     bool ok = true;
     const double dt = S.dt, t = S.t;
-#pragma omp parallel for schedule(static) reduction(min : mn) reduction(&& : ok)
+#pragma omp parallel for schedule(static) reduction(max : mn) reduction(&& : ok)
     for (int64_t i = 0; i < N; ++i) {
         const uint32_t zl = S.leaves[i];
         const int n = o_level_of(zl);
@@ -603,7 +608,7 @@ bool fv1_all(oracle_state& S, double* mincell) {
         U[3 * i + 1] = out[1];
         U[3 * i + 2] = out[2];
         const double c = cfl_cell(out[0], out[1], out[2], dx, p.g, p.hdry);
-        mn = c < mn ? c : mn;
+        mn = c > mn ? c : mn;
     }
     if (!ok) {
         S.err = "spatial_operator: non-finite state";
@@ -615,7 +620,7 @@ bool fv1_all(oracle_state& S, double* mincell) {
         const int n = o_level_of(zl);
         for (int q = 0; q < 3; ++q) S.s[q][zl] = from_phys(U[3 * i + q], n, L);
     }
-    *mincell = mn;
+    *maxrate = mn;
     return true;
 }
 
@@ -699,7 +704,7 @@ static int create_impl(const swamp_config* cfg, const double* h, const double* q
         delete S;
         return SWAMP_E_STATE;
     }
-    if (!set_dt(*S, leaves_min_cfl(*S))) {
+    if (!set_dt(*S, leaves_max_rate(*S))) {
         delete S;
         return SWAMP_E_DT;
     }

@@ -44,7 +44,7 @@ struct Ctl {
     double dt;       // dt of the next step
     double t_next;   // time after the next step (exact stop time when clipped)
     double dt_used;  // dt of the last step taken
-    unsigned long long dtmin_bits;  // CFL min accumulator (bits of a positive double)
+    unsigned long long rate_bits;   // CFL max-rate accumulator (bits of a non-negative double)
     unsigned long long smax_bits[4];
     long long step;
     unsigned long long cnt_tree;    // cells re-encoded by the last K1
@@ -720,12 +720,11 @@ __device__ __forceinline__ double series_value(const Params& P, double t) {
     return vs[k] + ((vs[k + 1] - vs[k]) * ((t - ts[k]) / (ts[k + 1] - ts[k])));
 }
 
-// next dt from the CFL minimum (D13), clipped to the next
-// output time / t_end; `advance` also commits the step (t, parity, counters).
-__device__ void finalize_dt(const Params& P, Ctl* ctl, double mincell, bool advance) {
+// next dt from the CFL maximum rate (D13), clipped to the
+// next output time / t_end; `advance` also commits the step (t, parity, counters).
+__device__ void finalize_dt(const Params& P, Ctl* ctl, double maxrate, bool advance) {
     const double t_new = advance ? ctl->t_next : ctl->t;
-    const bool dry = __double_as_longlong(mincell) == 0x7FF0000000000000ll;
-    const double dtc = dry ? P.dt_fallback : P.cfl * mincell;
+    const double dtc = (maxrate == 0.0) ? P.dt_fallback : P.cfl / maxrate;
     double stop = P.t_end;
     for (int k = 0; k < P.n_out; ++k) {
         const double o = P.out_times[k];
@@ -751,33 +750,34 @@ __device__ void finalize_dt(const Params& P, Ctl* ctl, double mincell, bool adva
     ctl->t_next = tn;
 }
 
-__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const unsigned long long y = __shfl_xor_sync(kFull, v, o);
-        v = y < v ? y : v;
+        v = y > v ? y : v;
     }
     return v;
 }
 
-// reduce the per-thread CFL minima, publish, and let the last CTA finish
-__device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ctl, double mn, bool advance) {
-    __shared__ unsigned long long s_min[kThreads / 32];
+// reduce the per-thread CFL rates (exact max on the bits of non-negative
+// doubles), publish, and let the last CTA finish the step
+__device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ctl, double rate, bool advance) {
+    __shared__ unsigned long long s_max[kThreads / 32];
     __shared__ int s_last;
-    unsigned long long b = warp_min_u64(static_cast<unsigned long long>(__double_as_longlong(mn)));
-    if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = b;
+    unsigned long long b = warp_max_u64(static_cast<unsigned long long>(__double_as_longlong(rate)));
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = b;
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned long long m = s_min[0];
-        for (int w = 1; w < kThreads / 32; ++w) m = s_min[w] < m ? s_min[w] : m;
-        atomicMin(&ctl->dtmin_bits, m);
+        unsigned long long m = s_max[0];
+        for (int w = 1; w < kThreads / 32; ++w) m = s_max[w] > m ? s_max[w] : m;
+        atomicMax(&ctl->rate_bits, m);
     }
     if (!last_block(&ctl->done_k5, &s_last)) return;
     tl_mark(ctl, 10);
     if (threadIdx.x == 0) {
-        const unsigned long long m = atomicAdd(&ctl->dtmin_bits, 0ull);
+        const unsigned long long m = atomicAdd(&ctl->rate_bits, 0ull);
         finalize_dt(P, ctl, __longlong_as_double(static_cast<long long>(m)), advance);
-        ctl->dtmin_bits = 0x7FF0000000000000ull;
+        ctl->rate_bits = 0ull;
         ctl->done_k5 = 0;
         ctl->tl[11] = gtimer();
     }
@@ -808,7 +808,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     const uint32_t N = UNIFORM ? (1u << (2 * P.L)) : ctl->n_leaves;
     const double t = ctl->t, dt = ctl->dt;
     const double inflow = series_value(P, t);
-    double mn = __longlong_as_double(0x7FF0000000000000ll);
+    double mx = 0.0;
     const uint32_t stride = gridDim.x * kThreads;
     uint32_t i = blockIdx.x * kThreads + threadIdx.x;
     uint32_t z_next = (!UNIFORM && i < N) ? P.leaves[i] : 0u;
@@ -852,15 +852,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             return make_cell(r4[d], P.phys);
         };
         double hn, qxn, qyn;
-        const double dx = P.dx[n];
         fv1_cell_seq(own, neighbour, P.inv_dx[n], dt, P.phys, hn, qxn, qyn);
         if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))
             report_error(ctl, kErrNonFinite, zo::z_of(n, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2), kStageFV1);
         st4(nxt + P.base[n] + m, make_double4(hn, qxn, qyn, o4.w));
-        const double c = cfl_cell(hn, qxn, qyn, dx, P.phys);
-        mn = c < mn ? c : mn;
+        const double c = cfl_rate(hn, qxn, qyn, P.inv_dx[n], P.phys);
+        mx = c > mx ? c : mx;
     }
-    cfl_reduce_and_finalize(P, ctl, mn, true);
+    cfl_reduce_and_finalize(P, ctl, mx, true);
 }
 
 // dt at initialise: CFL over the initial leaves, no update.
@@ -868,7 +867,7 @@ __global__ void __launch_bounds__(kThreads) k_cfl_init(Params P, Ctl* ctl, int u
     const int p = ctl->parity;
     const double4* cur = P.cells[p];
     const uint32_t N = uniform ? (1u << (2 * P.L)) : ctl->n_leaves;
-    double mn = __longlong_as_double(0x7FF0000000000000ll);
+    double mx = 0.0;
     for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < N; i += gridDim.x * kThreads) {
         int n;
         uint32_t m;
@@ -881,10 +880,10 @@ __global__ void __launch_bounds__(kThreads) k_cfl_init(Params P, Ctl* ctl, int u
             m = z - zo::level_offset(n);
         }
         const double4 v = ld4(cur + P.base[n] + m);
-        const double c = cfl_cell(v.x, v.y, v.z, P.dx[n], P.phys);
-        mn = c < mn ? c : mn;
+        const double c = cfl_rate(v.x, v.y, v.z, P.inv_dx[n], P.phys);
+        mx = c > mx ? c : mx;
     }
-    cfl_reduce_and_finalize(P, ctl, mn, false);
+    cfl_reduce_and_finalize(P, ctl, mx, false);
 }
 
 // =========================================================== import / export

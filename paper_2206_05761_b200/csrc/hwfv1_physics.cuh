@@ -24,8 +24,8 @@ struct PhysParams {
 __device__ __forceinline__ double absd(double x) { return x < 0.0 ? -x : x; }
 __device__ __forceinline__ double max2(double a, double b) { return a > b ? a : b; }
 
-// de-singularised velocity
-__device__ __forceinline__ double vel(double h, double q, double hdry) { return (h >= hdry) ? q / h : 0.0; }
+// de-singularised velocity, pinned as q * (1/h) (D2)
+__device__ __forceinline__ double vel(double h, double q, double hdry) { return (h >= hdry) ? q * (1.0 / h) : 0.0; }
 
 // hydrostatic reconstruction of one side: max(0, (h+z)-zf), below h_dry -> 0
 __device__ __forceinline__ double recon(double h, double z, double zf, double hdry) {
@@ -46,8 +46,10 @@ struct CellV {
 __device__ __forceinline__ CellV make_cell(double4 s, const PhysParams& p) {
     CellV c;
     c.h = s.x; c.qx = s.y; c.qy = s.z; c.z = s.w;
-    c.ux = vel(s.x, s.y, p.hdry);
-    c.uy = vel(s.x, s.z, p.hdry);
+    const bool wet = s.x >= p.hdry;
+    const double rh = wet ? 1.0 / s.x : 0.0;  // one reciprocal serves both components
+    c.ux = wet ? s.y * rh : 0.0;
+    c.uy = wet ? s.z * rh : 0.0;
     c.c = sqrt(p.g * s.x);
     return c;
 }
@@ -127,13 +129,14 @@ __device__ __forceinline__ double rcbrt_det(double x) {
     return y;
 }
 
-// CFL bound of one cell; +inf when dry. max(|qx|,|qy|)/h == max(|u|,|v|)
-// exactly (correctly rounded division is monotone).
-__device__ __forceinline__ double cfl_cell(double h, double qx, double qy, double dx, const PhysParams& p) {
-    if (!(h >= p.hdry)) return __longlong_as_double(0x7FF0000000000000ll);
+// CFL rate of one cell, (max(|u|,|v|) + sqrt(gh)) / dx, 0 when dry; the
+// step's dt is C / (max rate) (D13).
+__device__ __forceinline__ double cfl_rate(double h, double qx, double qy, double inv_dx, const PhysParams& p) {
+    if (!(h >= p.hdry)) return 0.0;
+    const double rh = 1.0 / h;
     const double aq = max2(absd(qx), absd(qy));
-    const double s = (aq / h) + sqrt(p.g * h);
-    return dx / s;
+    const double s = (aq * rh) + sqrt(p.g * h);
+    return s * inv_dx;
 }
 
 // Boundary ghost state (D10); dir W=0,E=1,N=2,S=3. The
@@ -198,7 +201,8 @@ __device__ __forceinline__ void fv1_cell(const CellV& own, const CellV nb[4], do
         const double qm = sqrt((qxn * qxn) + (qyn * qyn));
         if (qm > 0.0) {
             const double Cf = p.g_nM2 * rcbrt_det(hn);
-            const double den = 1.0 + (((dt * Cf) * qm) / (hn * hn));
+            const double rh = 1.0 / hn;
+            const double den = 1.0 + (((dt * Cf) * qm) * (rh * rh));
             const double r = 1.0 / den;
             qxn = qxn * r;
             qyn = qyn * r;
@@ -251,7 +255,8 @@ __device__ __forceinline__ void fv1_cell_seq(const CellV& own, GetNb&& get, doub
         const double qm = sqrt((qxn * qxn) + (qyn * qyn));
         if (qm > 0.0) {
             const double Cf = p.g_nM2 * rcbrt_det(hn);
-            const double den = 1.0 + (((dt * Cf) * qm) / (hn * hn));
+            const double rh = 1.0 / hn;
+            const double den = 1.0 + (((dt * Cf) * qm) * (rh * rh));
             const double r = 1.0 / den;
             qxn = qxn * r;
             qyn = qyn * r;

@@ -257,7 +257,6 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
 
     // control block
     Ctl c0{};
-    c0.dtmin_bits = 0x7FF0000000000000ull;
     std::memcpy(g->ctl_host, &c0, sizeof(Ctl));
     if (cudaMemcpyAsync(g->ctl, g->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, s) != cudaSuccess)
         return fail(SWAMP_E_CUDA);

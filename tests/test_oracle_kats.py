@@ -217,10 +217,13 @@ def test_friction_example():
 
 
 def test_cfl_examples():
-    # SPEC.md:337-339
-    assert O.cfl_cell(1.0, 0.0, 0.0, 1.0) * 0.5 == pytest.approx(0.5 / math.sqrt(G), rel=1e-15)
-    assert abs(0.5 * O.cfl_cell(1.0, 0.0, 0.0, 1.0) - 0.15966497839052937) <= 1e-16
-    assert math.isinf(O.cfl_cell(0.0, 0.0, 0.0, 1.0))
+    # SPEC.md:337-339; the oracle returns the CFL rate (max(|u|,|v|)+sqrt(gh))/dx
+    # and dt = C / max rate (D13)
+    assert 0.5 / O.cfl_cell(1.0, 0.0, 0.0, 1.0) == pytest.approx(0.5 / math.sqrt(G), rel=1e-15)
+    assert abs(0.5 / O.cfl_cell(1.0, 0.0, 0.0, 1.0) - 0.15966497839052937) <= 1e-16
+    assert O.cfl_cell(0.0, 0.0, 0.0, 1.0) == 0.0  # dry: no constraint
+    # mixed levels: the level-L cell (smallest dx) dominates when states are equal
+    assert O.cfl_cell(1.0, 0.2, 0.0, 0.25) > O.cfl_cell(1.0, 0.2, 0.0, 0.5)
 
 
 def test_boundary_examples():
