@@ -63,6 +63,14 @@ struct Ctl {
     unsigned long long tl[12];
 };
 
+// Programmatic dependent launch: every kernel of the step is launched with
+// programmatic stream serialisation; it lets its successor be scheduled as
+// soon as all of its CTAs are running (pdl_trigger) and waits for its
+// predecessor's completion + memory flush before touching any state
+// (pdl_wait). Hides the launch gap behind the last-CTA tails.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -259,6 +267,8 @@ __device__ __forceinline__ bool last_block(unsigned int* counter, int* s_flag) {
 // (sig prev is all ones) and also derives the static DEM mask.
 template <bool INIT>
 __global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
+    pdl_wait();
+    pdl_trigger();
     if (!INIT && !active(ctl, P)) return;
     tl_start(ctl, 0);
     extern __shared__ double4 sv[];
@@ -455,6 +465,8 @@ __device__ __forceinline__ uint8_t band_flag(int mode, int L, int n, uint32_t m,
 // leaf-list offsets (the PTT compaction's global scan, done once on 4^R
 // values instead of per finest cell).
 __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force) {
+    pdl_wait();
+    pdl_trigger();
     if (!force && !active(ctl, P)) return;
     tl_start(ctl, 1);
     extern __shared__ uint8_t sf[];
@@ -608,6 +620,8 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
 }
 
 __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int force) {
+    pdl_wait();
+    pdl_trigger();
     if (!force && !active(ctl, P)) return;
     tl_start(ctl, 2);
     extern __shared__ uint32_t smem3[];
@@ -799,6 +813,8 @@ __device__ __forceinline__ unsigned long long covering(const Params& P, const ui
 // leaf; reads the current buffer, writes leaf slots of the other (D15).
 template <bool UNIFORM, int MINB = 2>
 __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
+    pdl_wait();
+    pdl_trigger();
     if (!active(ctl, P)) return;
     tl_start(ctl, 3);
     const int p = ctl->parity;

@@ -47,7 +47,7 @@ struct swamp_gpu {
     std::vector<void*> allocs;
     cudaGraphExec_t graph1 = nullptr, graphS = nullptr, graphT = nullptr;
     int fv1_grid = 0;
-    int fv1_minb = 2;  // occupancy variant of k_fv1 (SWAMP_FV1_MINB=3 for 3 CTAs/SM)
+    int fv1_minb = 3;  // occupancy variant of k_fv1 (SWAMP_FV1_MINB=2 for 2 CTAs/SM, no spills)
     int num_sms = 0;
     size_t smem_k1 = 0, smem_k2 = 0, smem_k3 = 0;
     cudaEvent_t ev[6] = {};
@@ -103,6 +103,22 @@ int validate(const swamp_config* c) {
     return SWAMP_OK;
 }
 
+// launch with programmatic stream serialisation (PDL, see pdl_wait/pdl_trigger)
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kernel)(KArgs...), int grid, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 void launch_step_kernels(swamp_gpu* g, bool timed) {
     Params& P = g->P;
     cudaStream_t s = g->stream;
@@ -113,20 +129,20 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     if (timed) cudaMemsetAsync(g->ctl->tl, 0, sizeof(g->ctl->tl), s);
     mark(0);
     if (g->uniform) {
-        hwfv1::k_fv1<true><<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl);
+        launch_pdl(hwfv1::k_fv1<true, 2>, g->fv1_grid, 0, s, P, g->ctl);
         for (int k = 1; k < 5; ++k) mark(k);
         return;
     }
-    hwfv1::k_encode<false><<<P.n_tiles, kThreads, g->smem_k1, s>>>(P, g->ctl);
+    launch_pdl(hwfv1::k_encode<false>, P.n_tiles, g->smem_k1, s, P, g->ctl);
     mark(1);
-    hwfv1::k_band<<<P.n_tiles, kThreads, g->smem_k2, s>>>(P, g->ctl, 0);
+    launch_pdl(hwfv1::k_band, P.n_tiles, g->smem_k2, s, P, g->ctl, 0);
     mark(2);
-    hwfv1::k_traverse<<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 0);
+    launch_pdl(hwfv1::k_traverse, P.n_tiles, g->smem_k3, s, P, g->ctl, 0);
     mark(3);
     if (g->fv1_minb == 3)
-        hwfv1::k_fv1<false, 3><<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl);
+        launch_pdl(hwfv1::k_fv1<false, 3>, g->fv1_grid, 0, s, P, g->ctl);
     else
-        hwfv1::k_fv1<false, 2><<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl);
+        launch_pdl(hwfv1::k_fv1<false, 2>, g->fv1_grid, 0, s, P, g->ctl);
     mark(4);
 }
 
@@ -298,7 +314,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     }
     g->smem_k3 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u) * 6;
     {
-        if (const char* e = std::getenv("SWAMP_FV1_MINB")) g->fv1_minb = std::atoi(e) == 3 ? 3 : 2;
+        if (const char* e = std::getenv("SWAMP_FV1_MINB")) g->fv1_minb = std::atoi(e) == 2 ? 2 : 3;
         int occ = 0;
         if (g->fv1_minb == 3)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 3>, kThreads, 0);
