@@ -81,9 +81,10 @@ typedef struct swamp_config {
     const double* output_times; /* ascending; dt is clipped to hit them        */
 } swamp_config;
 
-/* StepReport. Stage times are device times in ms measured
- * with CUDA events when the handle was created with profiling enabled
- * (swamp_gpu_set_profiling), otherwise 0. */
+/* StepReport. Stage times are device times in ms of the
+ * step just taken, from the kernels' %globaltimer stamps (first CTA start to
+ * last CTA end of each kernel); with swamp_gpu_set_profiling(1) they come
+ * from CUDA events recorded between the kernels instead. */
 typedef struct swamp_step_report {
     int64_t step;          /* steps taken so far                                */
     double t;              /* simulation time after the step                    */
@@ -133,7 +134,8 @@ int swamp_gpu_create_uniform(const swamp_config* cfg, const double* h, const dou
                              const double* qy, const double* z, int device, swamp_gpu** out);
 int swamp_gpu_step_uniform(swamp_gpu* g, int64_t n_steps, swamp_step_report* rep);
 
-/* Stage timing on/off (per-kernel CUDA events; disables graph replay). */
+/* Stage timing from CUDA event nodes between the kernels (a separate graph
+ * with event record nodes) instead of the device timeline. */
 int swamp_gpu_set_profiling(swamp_gpu* g, int enabled);
 
 /* State queries / export (SimState). */

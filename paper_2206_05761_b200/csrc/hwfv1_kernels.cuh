@@ -57,10 +57,10 @@ struct Ctl {
     int err_q;
     int err_stage;
     unsigned int done_k1, done_k2, done_k5;
-    // stage timeline (globaltimer ns) of the last profiled step: for kernel k
-    // (K1, K2, K3, K5) [3k] = ~(first CTA start), [3k+1] = last CTA elected,
-    // [3k+2] = last CTA done (all via atomicMax; zeroed before the step)
-    unsigned long long tl[12];
+    // stage timeline (globaltimer ns), double-buffered by step parity: for
+    // kernel k (K1, K2, K3, K5) [3k] = ~(first CTA start), [3k+1] = last CTA
+    // elected, [3k+2] = last CTA done (atomicMax; K5 zeroes the next buffer)
+    unsigned long long tl[2][12];
 };
 
 // Programmatic dependent launch: every kernel of the step is launched with
@@ -76,11 +76,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
+__device__ __forceinline__ int tl_buf(const Ctl* c) { return static_cast<int>(c->step & 1); }
 __device__ __forceinline__ void tl_start(Ctl* c, int k) {
-    if (threadIdx.x == 0) atomicMax(&c->tl[3 * k], ~gtimer());
+    if (threadIdx.x == 0) atomicMax(&c->tl[tl_buf(c)][3 * k], ~gtimer());
 }
 __device__ __forceinline__ void tl_mark(Ctl* c, int slot) {
-    if (threadIdx.x == 0) atomicMax(&c->tl[slot], gtimer());
+    if (threadIdx.x == 0) atomicMax(&c->tl[tl_buf(c)][slot], gtimer());
 }
 
 struct Params {
@@ -793,7 +794,10 @@ __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ct
         finalize_dt(P, ctl, __longlong_as_double(static_cast<long long>(m)), advance);
         ctl->rate_bits = 0ull;
         ctl->done_k5 = 0;
-        ctl->tl[11] = gtimer();
+        const int tb = advance ? static_cast<int>((ctl->step - 1) & 1) : tl_buf(ctl);
+        ctl->tl[tb][11] = gtimer();
+        if (advance)
+            for (int k = 0; k < 12; ++k) ctl->tl[tb ^ 1][k] = 0ull;  // next step's buffer
     }
 }
 

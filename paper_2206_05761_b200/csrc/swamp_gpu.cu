@@ -126,7 +126,6 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     auto mark = [&](int k) {
         if (timed) cudaEventRecordWithFlags(g->ev[k], s, cudaEventRecordExternal);
     };
-    if (timed) cudaMemsetAsync(g->ctl->tl, 0, sizeof(g->ctl->tl), s);
     mark(0);
     if (g->uniform) {
         launch_pdl(hwfv1::k_fv1<true, 2>, g->fv1_grid, 0, s, P, g->ctl);
@@ -176,10 +175,34 @@ int fetch_ctl(swamp_gpu* g) {
     return SWAMP_OK;
 }
 
+// stage times of the last completed step from the device timeline (globaltimer)
+void fill_stage_times(const swamp_gpu* g, swamp_step_report* r) {
+    const Ctl& c = *g->ctl_host;
+    if (c.step <= 0) return;
+    const unsigned long long* tl = c.tl[(c.step - 1) & 1];
+    auto span = [&](int a, int b) -> double {
+        const unsigned long long s0 = (a % 3 == 0) ? ~tl[a] : tl[a];
+        const unsigned long long s1 = (b % 3 == 0) ? ~tl[b] : tl[b];
+        return (tl[a] == 0 || tl[b] == 0 || s1 < s0) ? 0.0 : 1e-6 * static_cast<double>(s1 - s0);
+    };
+    if (g->uniform) {
+        r->ms_fv1 = span(9, 11);
+        r->ms_total = r->ms_fv1;
+        return;
+    }
+    r->ms_encode_flag = span(0, 2);
+    r->ms_band_closure = span(3, 5);
+    r->ms_decode_traverse = span(6, 8);
+    r->ms_neighbours = 0.0;
+    r->ms_fv1 = span(9, 11);
+    r->ms_total = span(0, 11);
+}
+
 void fill_report(const swamp_gpu* g, swamp_step_report* r) {
     if (!r) return;
     const Ctl& c = *g->ctl_host;
     std::memset(r, 0, sizeof(*r));
+    fill_stage_times(g, r);
     r->step = c.step;
     r->t = c.t;
     r->dt = c.dt;
@@ -355,6 +378,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
         if (cudaGetLastError() != cudaSuccess) return fail(SWAMP_E_CUDA);
     }
     if ((st = fetch_ctl(g))) return fail(st);
+    cudaMemsetAsync(g->ctl->tl, 0, sizeof(g->ctl->tl), s);
     if ((st = build_graphs(g))) return fail(st);
     *out = g;
     return SWAMP_OK;
@@ -551,7 +575,8 @@ int swamp_gpu_last_error(const swamp_gpu* g, int32_t* code, uint32_t* z, int32_t
 int swamp_gpu_timeline(swamp_gpu* g, double* out12) {
     if (!g || !out12) return SWAMP_E_ARG;
     int st = fetch_ctl(g);
-    const unsigned long long* tl = g->ctl_host->tl;
+    // the last completed step ran with step counter (step - 1)
+    const unsigned long long* tl = g->ctl_host->tl[(g->ctl_host->step - 1) & 1];
     const unsigned long long t0 = ~tl[0];
     for (int k = 0; k < 12; ++k) {
         unsigned long long v = (k % 3 == 0) ? ~tl[k] : tl[k];
