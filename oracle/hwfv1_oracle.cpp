@@ -99,12 +99,12 @@ inline void decode4(double s, double da, double db, double dg, double c[4]) {
 }
 inline double absd(double x) { return x < 0.0 ? -x : x; }
 inline double max2(double a, double b) { return a > b ? a : b; }
-// significance, D6/D7: d_norm = max|d| / s_max, s_max < 1e-12
-// contributes 0; compared with ">=" against 2^(n-L) * eps.
+// significance, D6/D7: d_norm = max|d| / s_max >= 2^(n-L) eps,
+// evaluated division-free as max|d| >= ldexp(eps * s_max, n - L) (pinned);
+// a quantity with s_max < 1e-12 contributes d_norm = 0.
 inline bool significant(double da, double db, double dg, double smax, int n, int L, double eps) {
-    double dn = 0.0;
-    if (!(smax < 1e-12)) dn = max2(max2(absd(da), absd(db)), absd(dg)) / smax;
-    return dn >= std::ldexp(eps, n - L);
+    if (smax < 1e-12) return 0.0 >= std::ldexp(eps, n - L);
+    return max2(max2(absd(da), absd(db)), absd(dg)) >= std::ldexp(eps * smax, n - L);
 }
 
 // ============================================================== swe physics

@@ -90,7 +90,8 @@ struct Params {
     int bc[4];
     int inflow_mode, inflow_n, n_out;
     double W, cfl, t_end, dt_fallback;
-    double tau[kMaxL + 1];    // significance threshold per detail level, physical units
+    double tau[kMaxL + 1];    // 0 >= tau[n]: significance of a zero-detail cell (eps == 0)
+    double thr[4][kMaxL + 1]; // per quantity and level: max |D| >= thr (D7)
     double dx[kMaxL + 1];     // W * 2^-n
     double inv_dx[kMaxL + 1]; // 1.0 / dx[n] (IEEE division, as the oracle)
     double smax[4];
@@ -164,11 +165,10 @@ __device__ __forceinline__ Red red4(double c0, double c1, double c2, double c3) 
     const double dg = (c0 + c3) - (c1 + c2);
     return {par, max2(max2(absd(da), absd(db)), absd(dg))};
 }
-// significance of one quantity (D6, D7): s_max < 1e-12 -> d_norm 0
-__device__ __forceinline__ bool sig_q(double dmax, double smax, double tau) {
-    const double dn = (smax < 1e-12) ? 0.0 : dmax / smax;
-    return dn >= tau;
-}
+// significance of one quantity (D6, D7), division-free:
+// thr = ldexp(eps * s_max, 2n - 2L + 2) in physical units (+inf / 0 when
+// s_max < 1e-12, i.e. d_norm = 0)
+__device__ __forceinline__ bool sig_q(double dmax, double thr) { return dmax >= thr; }
 
 struct Enc {
     double4 par;
@@ -180,13 +180,12 @@ __device__ __forceinline__ Enc encode_children(const double4 c[4], const Params&
     const Red h = red4(c[0].x, c[1].x, c[2].x, c[3].x);
     const Red qx = red4(c[0].y, c[1].y, c[2].y, c[3].y);
     const Red qy = red4(c[0].z, c[1].z, c[2].z, c[3].z);
-    const double tau = P.tau[n];
     Enc e;
-    e.flow = sig_q(h.dmax, P.smax[0], tau) || sig_q(qx.dmax, P.smax[1], tau) || sig_q(qy.dmax, P.smax[2], tau);
+    e.flow = sig_q(h.dmax, P.thr[0][n]) || sig_q(qx.dmax, P.thr[1][n]) || sig_q(qy.dmax, P.thr[2][n]);
     if (WITH_Z) {
         const Red z = red4(c[0].w, c[1].w, c[2].w, c[3].w);
         e.par = make_double4(h.par, qx.par, qy.par, z.par);
-        e.zflag = sig_q(z.dmax, P.smax[3], tau);
+        e.zflag = sig_q(z.dmax, P.thr[3][n]);
     } else {
         const double a = c[0].w + c[1].w, b = c[2].w + c[3].w;
         e.par = make_double4(h.par, qx.par, qy.par, 0.25 * (a + b));
@@ -261,13 +260,160 @@ __device__ __forceinline__ bool last_block(unsigned int* counter, int* s_flag) {
     return last;
 }
 
+// ---------------------------------------------------------------- K1 warp part
+__device__ __forceinline__ double4 shfl4(double4 v, int src) {
+    return make_double4(__shfl_sync(kFull, v.x, src), __shfl_sync(kFull, v.y, src), __shfl_sync(kFull, v.z, src),
+                        __shfl_sync(kFull, v.w, src));
+}
+__device__ __forceinline__ bool byte_of(uint32_t w, int k) { return ((w >> (8 * k)) & 0xFFu) != 0u; }
+
+// Encode of 4 children held by lanes lane, lane+s, lane+2s, lane+3s (result
+// meaningful at the gathering lane); one component at a time to keep few
+// values live. Same arithmetic as encode_children.
+template <bool INIT>
+__device__ __forceinline__ Enc encode_lanes(double4 v, int s, const Params& P, int n) {
+    const int lane = threadIdx.x & 31;
+    auto red = [&](double x) {
+        const double x1 = __shfl_sync(kFull, x, (lane + s) & 31);
+        const double x2 = __shfl_sync(kFull, x, (lane + 2 * s) & 31);
+        const double x3 = __shfl_sync(kFull, x, (lane + 3 * s) & 31);
+        return red4(x, x1, x2, x3);
+    };
+    const Red h = red(v.x);
+    const Red qx = red(v.y);
+    const Red qy = red(v.z);
+    const Red z = red(v.w);
+    Enc e;
+    e.flow = sig_q(h.dmax, P.thr[0][n]) || sig_q(qx.dmax, P.thr[1][n]) || sig_q(qy.dmax, P.thr[2][n]);
+    e.par = make_double4(h.par, qx.par, qy.par, z.par);
+    e.zflag = INIT && sig_q(z.dmax, P.thr[3][n]);
+    return e;
+}
+
+// Re-encode + threshold of levels L-1, L-2, L-3 of subtree j by warps: warp w
+// owns tile-local level-(L-1) cells [128w, 128w+128) (one per lane per
+// iteration, 4 iterations), their level-(L-2) parents (lanes 4k) and
+// level-(L-3) grandparents (lanes 16m); values move up by shuffles, flags are
+// prefetched as words. Level-(L-3) values go to sv3[tile-local index] for the
+// CTA-level part. Returns the number of re-encoded cells of this thread.
+template <bool INIT>
+__device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4* buf, const uint8_t* sigp,
+                                                       double4* sv3, uint32_t j, int L, int K) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t n1 = 1u << (2 * (K - 1)), n2 = n1 >> 2, n3 = n2 >> 2;  // tile cells on L-1, L-2, L-3
+    const uint32_t b1 = 128u * w, b2 = 32u * w, b3 = 8u * w;
+    if (b1 >= n1) return 0;
+    const int L1 = L - 1, L2 = L - 2, L3 = L - 3;
+    const unsigned long long g1 = P.fbase[L1] + static_cast<unsigned long long>(j) * n1;
+    const unsigned long long g2 = P.fbase[L2] + static_cast<unsigned long long>(j) * n2;
+    const unsigned long long g3 = P.fbase[L3] + static_cast<unsigned long long>(j) * n3;
+    // previous-tree / DEM flags: words for L-1 (4 cells per lane), bytes above
+    uint32_t f1w = 0, d1w = 0;
+    if (b1 + 4u * lane < n1) {
+        f1w = INIT ? 0x01010101u : *reinterpret_cast<const uint32_t*>(sigp + g1 + b1 + 4u * lane);
+        d1w = INIT ? 0u : *reinterpret_cast<const uint32_t*>(P.dem + g1 + b1 + 4u * lane);
+    }
+    uint32_t f2 = 0, d2 = 0, f3 = 0, d3 = 0, f4 = 0;
+    if (b2 + lane < n2) {
+        f2 = INIT ? 1u : sigp[g2 + b2 + lane];
+        d2 = INIT ? 0u : P.dem[g2 + b2 + lane];
+    }
+    if (lane < 8 && b3 + lane < n3) {
+        f3 = INIT ? 1u : sigp[g3 + b3 + lane];
+        d3 = INIT ? 0u : P.dem[g3 + b3 + lane];
+        if (K >= 4) f4 = INIT ? 1u : sigp[P.fbase[L3 - 1] + static_cast<unsigned long long>(j) * (n3 >> 2) + ((b3 + lane) >> 2)];
+    }
+    const bool zero1 = 0.0 >= P.tau[L1], zero2 = 0.0 >= P.tau[L2], zero3 = 0.0 >= P.tau[L3];
+    unsigned tree = 0;
+#pragma unroll 1
+    for (int i = 0; i < 4; ++i) {
+        if (b1 + 32u * i >= n1) break;  // warp-uniform
+        const uint32_t c1 = b1 + 32u * i + lane, c2 = b2 + 8u * i + (lane >> 2), c3 = b3 + 2u * i + (lane >> 4);
+        const bool ok1 = c1 < n1, ok2 = (lane & 3) == 0 && c2 < n2, ok3 = (lane & 15) == 0 && c3 < n3;
+        const uint32_t gm1 = j * n1 + c1, gm2 = j * n2 + c2, gm3 = j * n3 + c3;
+        const int src1 = 8 * i + (lane >> 2), src3 = 2 * i + (lane >> 4);
+        const uint32_t w1 = __shfl_sync(kFull, f1w, src1), wd1 = __shfl_sync(kFull, d1w, src1);
+        const bool sp1 = ok1 && byte_of(w1, lane & 3);
+        const bool dm1 = byte_of(wd1, lane & 3);
+        const bool sp2 = __shfl_sync(kFull, f2, src1) != 0;  // my L-2 parent (lanes 4k: my own L-2 cell)
+        const bool dm2 = __shfl_sync(kFull, d2, src1) != 0;
+        const bool sp3 = __shfl_sync(kFull, f3, src3) != 0;  // my L-3 ancestor (lanes 16m: my own)
+        const bool dm3 = __shfl_sync(kFull, d3, src3) != 0;
+        const bool sp4 = __shfl_sync(kFull, f4, src3) != 0;
+        // every global read of the iteration first: children, then the values
+        // of previous-tree leaves whose parent is re-encoded here
+        double4 ch[4];
+        if (sp1) {
+            const double4* cp = buf + P.base[L] + (static_cast<unsigned long long>(gm1) << 2);
+            ch[0] = ld4_nc(cp); ch[1] = ld4_nc(cp + 1); ch[2] = ld4_nc(cp + 2); ch[3] = ld4_nc(cp + 3);
+        }
+        double4 v1 = make_double4(0.0, 0.0, 0.0, 0.0), v2 = v1, v3 = v1;
+        if (ok1 && !sp1 && sp2) v1 = ld4(buf + P.base[L1] + gm1);
+        if (ok2 && !sp2 && sp3) v2 = ld4(buf + P.base[L2] + gm2);
+        if (ok3 && !sp3 && sp4 && K >= 4) v3 = ld4(buf + P.base[L3] + gm3);
+        // level L-1
+        {
+            bool flow = zero1, zf = false;
+            if (sp1) {
+                const Enc e = encode_children<INIT>(ch, P, L1);
+                v1 = e.par;
+                flow = e.flow;
+                zf = e.zflag;
+                st4(buf + P.base[L1] + gm1, v1);
+                ++tree;
+            }
+            if (ok1) {
+                const bool d = INIT ? zf : dm1;
+                if (INIT) P.dem[g1 + c1] = d ? 1 : 0;
+                P.pre[g1 + c1] = (flow || d) ? 1 : 0;
+            }
+        }
+        // level L-2: lane 4k gathers lanes 4k..4k+3
+        {
+            const Enc e = encode_lanes<INIT>(v1, 1, P, L2);
+            if (ok2) {
+                bool flow = zero2, zf = false;
+                if (sp2) {
+                    v2 = e.par;
+                    flow = e.flow;
+                    zf = e.zflag;
+                    st4(buf + P.base[L2] + gm2, v2);
+                    ++tree;
+                }
+                const bool d = INIT ? zf : dm2;
+                if (INIT) P.dem[g2 + c2] = d ? 1 : 0;
+                P.pre[g2 + c2] = (flow || d) ? 1 : 0;
+            }
+        }
+        // level L-3: lane 16m gathers lanes 16m, +4, +8, +12
+        {
+            const Enc e = encode_lanes<INIT>(v2, 4, P, L3);
+            if (ok3) {
+                bool flow = zero3, zf = false;
+                if (sp3) {
+                    v3 = e.par;
+                    flow = e.flow;
+                    zf = e.zflag;
+                    st4(buf + P.base[L3] + gm3, v3);
+                    ++tree;
+                }
+                const bool d = INIT ? zf : dm3;
+                if (INIT) P.dem[g3 + c3] = d ? 1 : 0;
+                P.pre[g3 + c3] = (flow || d) ? 1 : 0;
+                sv3[c3] = v3;
+            }
+        }
+    }
+    return tree;
+}
+
 // =========================================================================== K1
 // zero_details_and_reencode + significance
 // over the level-R subtree `blockIdx.x`; restricted to the previous tree (sig
 // prev), so off-tree cells only cost a flag read. INIT = full encode at t=0
 // (sig prev is all ones) and also derives the static DEM mask.
 template <bool INIT>
-__global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
+__global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
     pdl_wait();
     pdl_trigger();
     if (!INIT && !active(ctl, P)) return;
@@ -284,17 +430,21 @@ __global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
     uint8_t* sfl = reinterpret_cast<uint8_t*>(sv + ncell);  // previous-tree flags of the subtree
     unsigned tree = 0;
 
-    // ---- all global reads that do not depend on this step's results are
-    //      issued up front: the subtree's previous-tree flags, then the values
-    //      of previous-tree leaves whose parent gets re-encoded here
-    for (int n = R; n < L; ++n) {
+    // Levels handled per warp: L-1, L-2, L-3 (when K >= 3) with warp
+    // shuffles and no CTA barrier; the CTA then finishes levels top_n .. R
+    // from shared memory.
+    const int top_n = (K >= 3) ? L - 4 : L - 1;
+
+    // ---- flags of the CTA-level part and the values of previous-tree leaves
+    //      whose parent gets re-encoded there, issued up front
+    for (int n = R; n <= top_n; ++n) {
         const uint32_t cnt = 1u << (2 * (n - R));
         for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads)
             sfl[lo(n, R) + pi] = INIT ? 1 : sigp[P.fbase[n] + j * cnt + pi];
     }
     __syncthreads();
     if (!INIT) {
-        for (int n = R + 1; n < L; ++n) {
+        for (int n = R + 1; n <= top_n; ++n) {
             const uint32_t cnt = 1u << (2 * (n - R));
             for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
                 const uint32_t li = lo(n, R) + pi;
@@ -303,13 +453,13 @@ __global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
         }
     }
 
-    // ---- finest level: one thread per level-(L-1) parent; its 4 children are
-    //      128 contiguous bytes, read with four 256-bit loads
-    {
+    if (K >= 3) {
+        tree += encode_warp_levels<INIT>(P, buf, sigp, sv + lo(L - 3, R), j, L, K);
+    } else {
+        // small trees (L <= 2): one thread per level-(L-1) parent
         const int n = L - 1;
         const uint32_t npar = 1u << (2 * (K - 1));
         const uint32_t pbase = j * npar;
-#pragma unroll 2
         for (uint32_t pi = threadIdx.x; pi < npar; pi += kThreads) {
             const uint32_t pm = pbase + pi;
             const bool sp = sfl[lo(n, R) + pi] != 0;
@@ -337,8 +487,8 @@ __global__ void __launch_bounds__(kThreads) k_encode(Params P, Ctl* ctl) {
     }
     __syncthreads();
 
-    // ---- levels L-2 .. R inside the subtree: shared memory only
-    for (int n = L - 2; n >= R; --n) {
+    // ---- CTA-level part: levels top_n-? .. R from shared memory
+    for (int n = (K >= 3 ? L - 4 : L - 2); n >= R; --n) {
         const uint32_t cnt = 1u << (2 * (n - R));
         const uint32_t pb = j * cnt;
         for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {

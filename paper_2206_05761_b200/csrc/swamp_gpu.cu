@@ -323,7 +323,18 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
         std::memcpy(&P.smax[q], &b, 8);
     }
     // significance threshold in physical units: eps * 2^(2n-2L+2) (D7)
-    for (int n = 0; n < L; ++n) P.tau[n] = std::ldexp(cfg->epsilon, 2 * n - 2 * L + 2);
+    // significance thresholds in physical units (D7): spec form
+    // max|d|/s_max >= eps 2^(n-L) on s = p 2^(L-n) coefficients, evaluated as
+    // max|D| >= ldexp(eps * s_max, 2n - 2L + 2) on physical details D
+    for (int n = 0; n < L; ++n) {
+        P.tau[n] = std::ldexp(cfg->epsilon, 2 * n - 2 * L + 2);
+        for (int q = 0; q < 4; ++q) {
+            if (P.smax[q] < 1e-12)
+                P.thr[q][n] = (0.0 >= P.tau[n]) ? 0.0 : HUGE_VAL;
+            else
+                P.thr[q][n] = std::ldexp(cfg->epsilon * P.smax[q], 2 * n - 2 * L + 2);
+        }
+    }
 
     g->smem_k1 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u) * (sizeof(double4) + 1);
     {

@@ -18,7 +18,7 @@ import numpy as np
 from .abi import STATUS, SimConfig, as_f64, dptr, level_offset, swamp_config, swamp_step_report, u8ptr, u32ptr
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libswamp_gpu.so")
+LIB_PATH = os.environ.get("SWAMP_GPU_LIB") or os.path.join(_HERE, "libswamp_gpu.so")
 _LIB = None
 
 
