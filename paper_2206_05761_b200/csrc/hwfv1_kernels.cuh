@@ -50,6 +50,7 @@ struct Ctl {
     unsigned long long cnt_tree;    // cells re-encoded by the last K1
     unsigned long long cnt_new;     // newly significant cells decoded by the last K3
     uint32_t n_leaves;              // leaves of the grid built by the last K2/K3
+    uint32_t n_leaves_A;            // of which level-L leaves (listed first, in sibling quadruples)
     uint32_t n_leaves_used;         // leaves the last FV1 updated
     int parity;                     // current cell buffer / previous-tree flags
     int err_code;
@@ -105,7 +106,8 @@ struct Params {
     uint8_t* sig[2];
     uint8_t* pre;
     uint8_t* dem;
-    uint32_t* leaves;
+    uint32_t* leaves;     // hot-path leaf list: level-L leaves, then the coarser ones
+    uint32_t* leaves_x;   // Morton-ordered leaf list for exports
     uint32_t* tile_cnt;
     uint32_t* tile_off;
     uint32_t* tile_lvl;   // traversal depth of each level-R subtree root (R = reached)
@@ -290,43 +292,45 @@ __device__ __forceinline__ Enc encode_lanes(double4 v, int s, const Params& P, i
     return e;
 }
 
-// Re-encode + threshold of levels L-1, L-2, L-3 of subtree j by warps: warp w
-// owns tile-local level-(L-1) cells [128w, 128w+128) (one per lane per
-// iteration, 4 iterations), their level-(L-2) parents (lanes 4k) and
-// level-(L-3) grandparents (lanes 16m); values move up by shuffles, flags are
-// prefetched as words. Level-(L-3) values go to sv3[tile-local index] for the
-// CTA-level part. Returns the number of re-encoded cells of this thread.
+// Re-encode + threshold of levels T, T-1, T-2 of subtree j by warps (T = L-1
+// at t = 0, else L-2: level L-1 was re-encoded by the previous FV1). Warp w
+// owns a contiguous block of 32*ipw tile-local level-T cells (one per lane per
+// iteration), their level-(T-1) parents (lanes 4k) and level-(T-2)
+// grandparents (lanes 16m); values move up by shuffles, flags are prefetched
+// as words. Level-(T-2) values go to sv3[tile-local index] for the CTA-level
+// part. Returns the number of re-encoded cells of this thread.
 template <bool INIT>
 __device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4* buf, const uint8_t* sigp,
-                                                       double4* sv3, uint32_t j, int L, int K) {
+                                                       double4* sv3, uint32_t j, int T, int R) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint32_t n1 = 1u << (2 * (K - 1)), n2 = n1 >> 2, n3 = n2 >> 2;  // tile cells on L-1, L-2, L-3
-    const uint32_t b1 = 128u * w, b2 = 32u * w, b3 = 8u * w;
+    const uint32_t n1 = 1u << (2 * (T - R)), n2 = n1 >> 2, n3 = n2 >> 2;  // tile cells on T, T-1, T-2
+    const int ipw = (n1 >= 32u * (kThreads / 32)) ? static_cast<int>(n1 / (32u * (kThreads / 32))) : 1;
+    const uint32_t b1 = 32u * ipw * w, b2 = 8u * ipw * w, b3 = 2u * ipw * w;
     if (b1 >= n1) return 0;
-    const int L1 = L - 1, L2 = L - 2, L3 = L - 3;
+    const int L1 = T, L2 = T - 1, L3 = T - 2;
     const unsigned long long g1 = P.fbase[L1] + static_cast<unsigned long long>(j) * n1;
     const unsigned long long g2 = P.fbase[L2] + static_cast<unsigned long long>(j) * n2;
     const unsigned long long g3 = P.fbase[L3] + static_cast<unsigned long long>(j) * n3;
-    // previous-tree / DEM flags: words for L-1 (4 cells per lane), bytes above
+    // previous-tree / DEM flags: words for level T (4 cells per lane), bytes above
     uint32_t f1w = 0, d1w = 0;
-    if (b1 + 4u * lane < n1) {
+    if (b1 + 4u * lane < n1 && lane < 8 * ipw) {
         f1w = INIT ? 0x01010101u : *reinterpret_cast<const uint32_t*>(sigp + g1 + b1 + 4u * lane);
         d1w = INIT ? 0u : *reinterpret_cast<const uint32_t*>(P.dem + g1 + b1 + 4u * lane);
     }
     uint32_t f2 = 0, d2 = 0, f3 = 0, d3 = 0, f4 = 0;
-    if (b2 + lane < n2) {
+    if (lane < 8 * ipw && b2 + lane < n2) {
         f2 = INIT ? 1u : sigp[g2 + b2 + lane];
         d2 = INIT ? 0u : P.dem[g2 + b2 + lane];
     }
-    if (lane < 8 && b3 + lane < n3) {
+    if (lane < 2 * ipw && b3 + lane < n3) {
         f3 = INIT ? 1u : sigp[g3 + b3 + lane];
         d3 = INIT ? 0u : P.dem[g3 + b3 + lane];
-        if (K >= 4) f4 = INIT ? 1u : sigp[P.fbase[L3 - 1] + static_cast<unsigned long long>(j) * (n3 >> 2) + ((b3 + lane) >> 2)];
+        if (L3 > R) f4 = INIT ? 1u : sigp[P.fbase[L3 - 1] + static_cast<unsigned long long>(j) * (n3 >> 2) + ((b3 + lane) >> 2)];
     }
     const bool zero1 = 0.0 >= P.tau[L1], zero2 = 0.0 >= P.tau[L2], zero3 = 0.0 >= P.tau[L3];
     unsigned tree = 0;
 #pragma unroll 1
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < ipw; ++i) {
         if (b1 + 32u * i >= n1) break;  // warp-uniform
         const uint32_t c1 = b1 + 32u * i + lane, c2 = b2 + 8u * i + (lane >> 2), c3 = b3 + 2u * i + (lane >> 4);
         const bool ok1 = c1 < n1, ok2 = (lane & 3) == 0 && c2 < n2, ok3 = (lane & 15) == 0 && c3 < n3;
@@ -335,23 +339,23 @@ __device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4*
         const uint32_t w1 = __shfl_sync(kFull, f1w, src1), wd1 = __shfl_sync(kFull, d1w, src1);
         const bool sp1 = ok1 && byte_of(w1, lane & 3);
         const bool dm1 = byte_of(wd1, lane & 3);
-        const bool sp2 = __shfl_sync(kFull, f2, src1) != 0;  // my L-2 parent (lanes 4k: my own L-2 cell)
+        const bool sp2 = __shfl_sync(kFull, f2, src1) != 0;  // my T-1 parent (lanes 4k: my own T-1 cell)
         const bool dm2 = __shfl_sync(kFull, d2, src1) != 0;
-        const bool sp3 = __shfl_sync(kFull, f3, src3) != 0;  // my L-3 ancestor (lanes 16m: my own)
+        const bool sp3 = __shfl_sync(kFull, f3, src3) != 0;  // my T-2 ancestor (lanes 16m: my own)
         const bool dm3 = __shfl_sync(kFull, d3, src3) != 0;
         const bool sp4 = __shfl_sync(kFull, f4, src3) != 0;
         // every global read of the iteration first: children, then the values
         // of previous-tree leaves whose parent is re-encoded here
         double4 ch[4];
         if (sp1) {
-            const double4* cp = buf + P.base[L] + (static_cast<unsigned long long>(gm1) << 2);
+            const double4* cp = buf + P.base[L1 + 1] + (static_cast<unsigned long long>(gm1) << 2);
             ch[0] = ld4_nc(cp); ch[1] = ld4_nc(cp + 1); ch[2] = ld4_nc(cp + 2); ch[3] = ld4_nc(cp + 3);
         }
         double4 v1 = make_double4(0.0, 0.0, 0.0, 0.0), v2 = v1, v3 = v1;
         if (ok1 && !sp1 && sp2) v1 = ld4(buf + P.base[L1] + gm1);
         if (ok2 && !sp2 && sp3) v2 = ld4(buf + P.base[L2] + gm2);
-        if (ok3 && !sp3 && sp4 && K >= 4) v3 = ld4(buf + P.base[L3] + gm3);
-        // level L-1
+        if (ok3 && !sp3 && sp4 && L3 > R) v3 = ld4(buf + P.base[L3] + gm3);
+        // level T
         {
             bool flow = zero1, zf = false;
             if (sp1) {
@@ -368,7 +372,7 @@ __device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4*
                 P.pre[g1 + c1] = (flow || d) ? 1 : 0;
             }
         }
-        // level L-2: lane 4k gathers lanes 4k..4k+3
+        // level T-1: lane 4k gathers lanes 4k..4k+3
         {
             const Enc e = encode_lanes<INIT>(v1, 1, P, L2);
             if (ok2) {
@@ -385,7 +389,7 @@ __device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4*
                 P.pre[g2 + c2] = (flow || d) ? 1 : 0;
             }
         }
-        // level L-3: lane 16m gathers lanes 16m, +4, +8, +12
+        // level T-2: lane 16m gathers lanes 16m, +4, +8, +12
         {
             const Enc e = encode_lanes<INIT>(v2, 4, P, L3);
             if (ok3) {
@@ -430,21 +434,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
     uint8_t* sfl = reinterpret_cast<uint8_t*>(sv + ncell);  // previous-tree flags of the subtree
     unsigned tree = 0;
 
-    // Levels handled per warp: L-1, L-2, L-3 (when K >= 3) with warp
-    // shuffles and no CTA barrier; the CTA then finishes levels top_n .. R
-    // from shared memory.
-    const int top_n = (K >= 3) ? L - 4 : L - 1;
+    // Warp part: levels T, T-1, T-2 with shuffles and no CTA barrier, where
+    // T = L-1 at t = 0 and T = L-2 afterwards (the previous step's FV1 already
+    // re-encoded level L-1 of the previous tree, see k_fv1). The CTA then
+    // finishes levels top_n .. R from shared memory. Small trees use the
+    // per-thread path for level L-1 (re-encoding it again is bit-identical).
+    const int T = INIT ? L - 1 : L - 2;
+    const bool warp_path = T - 2 >= R;
+    const int top_n = warp_path ? T - 3 : L - 2;
 
     // ---- flags of the CTA-level part and the values of previous-tree leaves
     //      whose parent gets re-encoded there, issued up front
-    for (int n = R; n <= top_n; ++n) {
+    for (int n = R; n <= top_n + (warp_path ? 0 : 1); ++n) {
         const uint32_t cnt = 1u << (2 * (n - R));
         for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads)
             sfl[lo(n, R) + pi] = INIT ? 1 : sigp[P.fbase[n] + j * cnt + pi];
     }
     __syncthreads();
     if (!INIT) {
-        for (int n = R + 1; n <= top_n; ++n) {
+        for (int n = R + 1; n <= top_n + (warp_path ? 0 : 1); ++n) {
             const uint32_t cnt = 1u << (2 * (n - R));
             for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
                 const uint32_t li = lo(n, R) + pi;
@@ -453,10 +461,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
         }
     }
 
-    if (K >= 3) {
-        tree += encode_warp_levels<INIT>(P, buf, sigp, sv + lo(L - 3, R), j, L, K);
+    if (warp_path) {
+        if (!INIT) {
+            // level L-1: previous-tree cells were re-encoded (and flagged) by
+            // the previous FV1; the others only get pre = DEM | (eps == 0)
+            const int n = L - 1;
+            const uint32_t cnt = 1u << (2 * (n - R));
+            const bool zero = 0.0 >= P.tau[n];
+            const unsigned long long g = P.fbase[n] + static_cast<unsigned long long>(j) * cnt;
+            for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads) {
+                const uint32_t f = *reinterpret_cast<const uint32_t*>(sigp + g + q);
+                const uint32_t d = *reinterpret_cast<const uint32_t*>(P.dem + g + q);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (!byte_of(f, k)) P.pre[g + q + k] = (zero || byte_of(d, k)) ? 1 : 0;
+            }
+        }
+        tree += encode_warp_levels<INIT>(P, buf, sigp, sv + lo(T - 2, R), j, T, R);
     } else {
-        // small trees (L <= 2): one thread per level-(L-1) parent
+        // small trees: one thread per level-(L-1) parent
         const int n = L - 1;
         const uint32_t npar = 1u << (2 * (K - 1));
         const uint32_t pbase = j * npar;
@@ -487,8 +510,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
     }
     __syncthreads();
 
-    // ---- CTA-level part: levels top_n-? .. R from shared memory
-    for (int n = (K >= 3 ? L - 4 : L - 2); n >= R; --n) {
+    // ---- CTA-level part: levels top_n .. R from shared memory
+    for (int n = top_n; n >= R; --n) {
         const uint32_t cnt = 1u << (2 * (n - R));
         const uint32_t pb = j * cnt;
         for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
@@ -648,18 +671,23 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
         const uint32_t cnt = 1u << (2 * (n - R));
         for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) sigc[P.fbase[n] + j * cnt + pi] = sf[lo(n, R) + pi];
     }
-    // leaves in this subtree assuming its root is reached by the traversal
+    // leaves in this subtree assuming its root is reached by the traversal:
+    // level-L leaves (A) and coarser leaves (B)
     {
         const uint32_t nc = 1u << (2 * (K - 1));  // level-(L-1) cells in the subtree
-        unsigned cntl = 0;
+        unsigned ca = 0, cb = 0;
         for (uint32_t c = threadIdx.x; c < nc; c += kThreads) {
             int n = R;
             while (n < L && sf[lo(n, R) + (c >> (2 * (L - 1 - n)))]) ++n;
-            if (n == L) cntl += 4;
-            else cntl += ((c & ((1u << (2 * (L - 1 - n))) - 1u)) == 0u) ? 1u : 0u;
+            if (n == L) ca += 4;
+            else cb += ((c & ((1u << (2 * (L - 1 - n))) - 1u)) == 0u) ? 1u : 0u;
         }
-        const unsigned tot = block_sum(cntl, s_red);
-        if (threadIdx.x == 0) P.tile_cnt[j] = tot;
+        const unsigned ta = block_sum(ca, s_red);
+        const unsigned tb = block_sum(cb, s_red);
+        if (threadIdx.x == 0) {
+            P.tile_cnt[j] = ta;
+            P.tile_cnt[P.n_tiles + j] = tb;
+        }
     }
     if (!last_block(&ctl->done_k2, &s_last)) return;
     tl_mark(ctl, 4);
@@ -684,6 +712,7 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
             if (n == R) {
                 tsig[lo(R, 0) + m] = ldcg_u8(sigc + P.fbase[R] + m);
                 tcnt[m] = ldcg_u32(P.tile_cnt + m);
+                tcnt[P.n_tiles + m] = ldcg_u32(P.tile_cnt + P.n_tiles + m);
             }
         }
     }
@@ -739,48 +768,66 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
         const unsigned tn = block_sum(nnew, s_red);
         if (threadIdx.x == 0 && tn) atomicAdd(&ctl->cnt_new, (unsigned long long)tn);
     }
-    // ---- per-subtree leaf counts, their exclusive scan, and each subtree's
-    //      traversal depth (R = reached, else the level of its covering leaf)
+    // ---- per-subtree leaf counts, their exclusive scans, and each subtree's
+    //      traversal depth (R = reached, else the level of its covering leaf).
+    //      Hot-path list: all level-L leaves (A) first, then the coarser ones
+    //      (B); export list: Morton order (A and B interleaved per subtree).
     const uint32_t nt = static_cast<uint32_t>(P.n_tiles);
     const uint32_t per = (nt + kThreads - 1) / kThreads;
     const uint32_t a = threadIdx.x * per;
     const uint32_t b = min(nt, a + per);
-    unsigned local = 0;
+    unsigned la = 0, lb = 0;
     for (uint32_t t = a; t < b; ++t) {
         int n = R;
         while (!intree[lo(n, 0) + (t >> (2 * (R - n)))]) --n;
-        unsigned c;
-        if (n == R) c = tcnt[t];
-        else c = ((t & ((1u << (2 * (R - n))) - 1u)) == 0u) ? 1u : 0u;
+        unsigned ca = 0, cb;
+        if (n == R) {
+            ca = tcnt[t];
+            cb = tcnt[nt + t];
+        } else {
+            cb = ((t & ((1u << (2 * (R - n))) - 1u)) == 0u) ? 1u : 0u;
+        }
         P.tile_lvl[t] = static_cast<uint32_t>(n);
-        P.tile_off[t] = c;  // temporarily the count
-        local += c;
+        P.tile_off[t] = ca;       // temporarily the counts
+        P.tile_off[nt + t] = cb;
+        la += ca;
+        lb += cb;
     }
-    unsigned total;
-    unsigned off = block_exscan(local, s_red, &total);
+    unsigned ta, tb;
+    unsigned oa = block_exscan(la, s_red, &ta);
+    unsigned ob = block_exscan(lb, s_red, &tb);
+    unsigned om = oa + ob;
     for (uint32_t t = a; t < b; ++t) {
-        const unsigned c = P.tile_off[t];
-        P.tile_off[t] = off;
-        off += c;
+        const unsigned ca = P.tile_off[t], cb = P.tile_off[nt + t];
+        P.tile_off[t] = oa;               // A: level-L leaves
+        P.tile_off[nt + t] = ta + ob;     // B: after all of A
+        P.tile_off[2 * nt + t] = om;      // Morton-ordered export list
+        oa += ca;
+        ob += cb;
+        om += ca + cb;
     }
     if (threadIdx.x == 0) {
-        ctl->n_leaves = total;
+        ctl->n_leaves = ta + tb;
+        ctl->n_leaves_A = ta;
         ctl->done_k2 = 0;
     }
     tl_mark(ctl, 5);
 }
 
+// EXPORT = re-run the traversal of the current tree (after a step) into the
+// Morton-ordered export list, with no side effects (no decode, no timeline).
+template <bool EXPORT>
 __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int force) {
     pdl_wait();
     pdl_trigger();
-    if (!force && !active(ctl, P)) return;
-    tl_start(ctl, 2);
+    if (!EXPORT && !force && !active(ctl, P)) return;
+    if (!EXPORT) tl_start(ctl, 2);
     extern __shared__ uint32_t smem3[];
     __shared__ unsigned s_red[32];
     const int p = ctl->parity;
     double4* buf = P.cells[p];
-    const uint8_t* sigc = P.sig[p ^ 1];
-    const uint8_t* sigp = P.sig[p];
+    const uint8_t* sigc = EXPORT ? P.sig[p] : P.sig[p ^ 1];
+    const uint8_t* sigp = EXPORT ? P.sig[p ^ 1] : P.sig[p];
     const int L = P.L, R = P.R, K = P.K;
     const uint32_t j = blockIdx.x;
     const uint32_t ncell = ((1u << (2 * K)) - 1u) / 3u;  // subtree cells on levels R..L-1
@@ -803,6 +850,7 @@ __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int f
     }
     // decode is needed only where something became significant
     any_new = __syncthreads_or(any_new | (rootsrc != kNoSrc ? 1 : 0));
+    if (EXPORT) any_new = 0;
     unsigned nnew = 0;
 
     if (reached && any_new) {
@@ -828,33 +876,43 @@ __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int f
             __syncthreads();
         }
     }
-    {
+    if (!EXPORT) {
         const unsigned tn = block_sum(nnew, s_red);
         if (threadIdx.x == 0 && tn) atomicAdd(&ctl->cnt_new, (unsigned long long)tn);
     }
 
-    // ---- PTT + compaction into leaves[tile_off[j] ...]
-    const uint32_t base_out = P.tile_off[j];
+    // ---- PTT + compaction. Hot path: level-L leaves to list A at
+    //      tile_off[j], coarser leaves to list B at tile_off[nt + j]; export:
+    //      one Morton-ordered list at tile_off[2 nt + j].
+    const uint32_t nt = static_cast<uint32_t>(P.n_tiles);
+    uint32_t* outA = EXPORT ? P.leaves_x : P.leaves;
+    uint32_t oa = EXPORT ? P.tile_off[2 * nt + j] : P.tile_off[j];
+    uint32_t ob = EXPORT ? 0u : P.tile_off[nt + j];
     if (!reached) {
         const int n = static_cast<int>(leafn);
         if (threadIdx.x == 0 && ((j & ((1u << (2 * (R - n))) - 1u)) == 0u))
-            P.leaves[base_out] = zo::z_of(n, j >> (2 * (R - n)));
-        tl_mark(ctl, 8);
+            (EXPORT ? outA[oa] : P.leaves[ob]) = zo::z_of(n, j >> (2 * (R - n)));
+        if (!EXPORT) tl_mark(ctl, 8);
         return;
     }
     const uint32_t nc = 1u << (2 * (K - 1));  // level-(L-1) cells in the subtree
     const uint32_t per = (nc + kThreads - 1) / kThreads;
     const uint32_t a = threadIdx.x * per;
     const uint32_t b = min(nc, a + per);
-    unsigned cntl = 0;
+    unsigned ca = 0, cb = 0;
     for (uint32_t c = a; c < b; ++c) {
         int n = R;
         while (n < L && sc[lo(n, R) + (c >> (2 * (L - 1 - n)))]) ++n;
-        if (n == L) cntl += 4;
-        else cntl += ((c & ((1u << (2 * (L - 1 - n))) - 1u)) == 0u) ? 1u : 0u;
+        if (n == L) ca += 4;
+        else cb += ((c & ((1u << (2 * (L - 1 - n))) - 1u)) == 0u) ? 1u : 0u;
     }
     unsigned total;
-    uint32_t o = base_out + block_exscan(cntl, s_red, &total);
+    if (EXPORT) {
+        oa += block_exscan(ca + cb, s_red, &total);
+    } else {
+        oa += block_exscan(ca, s_red, &total);
+        ob += block_exscan(cb, s_red, &total);
+    }
     const uint32_t gbase = j * nc;
     for (uint32_t c = a; c < b; ++c) {
         int n = R;
@@ -862,14 +920,17 @@ __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int f
         const uint32_t gm = gbase + c;
         if (n == L) {
             const uint32_t z0 = zo::z_of(L, gm << 2);
-            P.leaves[o] = z0; P.leaves[o + 1] = z0 + 1; P.leaves[o + 2] = z0 + 2; P.leaves[o + 3] = z0 + 3;
-            o += 4;
+            outA[oa] = z0; outA[oa + 1] = z0 + 1; outA[oa + 2] = z0 + 2; outA[oa + 3] = z0 + 3;
+            oa += 4;
         } else if ((c & ((1u << (2 * (L - 1 - n))) - 1u)) == 0u) {
-            P.leaves[o++] = zo::z_of(n, gm >> (2 * (L - 1 - n)));
+            if (EXPORT) outA[oa++] = zo::z_of(n, gm >> (2 * (L - 1 - n)));
+            else P.leaves[ob++] = zo::z_of(n, gm >> (2 * (L - 1 - n)));
         }
     }
-    __syncthreads();
-    tl_mark(ctl, 8);
+    if (!EXPORT) {
+        __syncthreads();
+        tl_mark(ctl, 8);
+    }
 }
 
 // =========================================================================== K5
@@ -976,58 +1037,89 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     double4* __restrict__ nxt = P.cells[p ^ 1];
     const uint8_t* __restrict__ sigc = P.sig[p ^ 1];
     const uint32_t N = UNIFORM ? (1u << (2 * P.L)) : ctl->n_leaves;
+    // the leaf list starts with the level-L leaves (sibling quadruples at
+    // indices 4g..4g+3), then the coarser leaves
+    const uint32_t NA = UNIFORM ? 0u : ctl->n_leaves_A;
     const double t = ctl->t, dt = ctl->dt;
     const double inflow = series_value(P, t);
+    const int lane = threadIdx.x & 31;
     double mx = 0.0;
+    unsigned tree = 0;
     const uint32_t stride = gridDim.x * kThreads;
-    uint32_t i = blockIdx.x * kThreads + threadIdx.x;
-    uint32_t z_next = (!UNIFORM && i < N) ? P.leaves[i] : 0u;
-    for (; i < N; i += stride) {
+    // warp-uniform trip count: every lane runs every iteration (shuffles below)
+    uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
+    uint32_t z_next = (!UNIFORM && wbase + lane < N) ? P.leaves[wbase + lane] : 0u;
+    for (; wbase < N; wbase += stride) {
+        const uint32_t i = wbase + lane;
+        const bool valid = i < N;
         int n;
         uint32_t m;
         if (UNIFORM) {
             n = P.L;
-            m = i;
+            m = valid ? i : 0u;
         } else {
-            const uint32_t z = z_next;  // leaf ids are prefetched one iteration ahead
+            const uint32_t z = valid ? z_next : zo::level_offset(P.L);  // leaf ids prefetched one iteration ahead
             if (i + stride < N) z_next = P.leaves[i + stride];
             n = zo::level_of(z);
             m = z - zo::level_offset(n);
         }
-        // every global read of this leaf is issued before any arithmetic: own
-        // cell, the four neighbours' parent-level flags, the four neighbours
-        const double4 o4 = ld4_nc(cur + P.base[n] + m);
-        uint32_t nm[4];
-        unsigned long long off[4];
+        double hn = 0.0, qxn = 0.0, qyn = 0.0, zown = 0.0;
+        if (valid) {
+            // every global read of this leaf is issued before any arithmetic:
+            // own cell, the neighbours' parent-level flags, the neighbours
+            const double4 o4 = ld4_nc(cur + P.base[n] + m);
+            uint32_t nm[4];
+            unsigned long long off[4];
 #pragma unroll
-        for (int d = 0; d < 4; ++d) nm[d] = zo::neighbour_dev(n, m, static_cast<zo::Direction>(d));
-        if (UNIFORM) {
+            for (int d = 0; d < 4; ++d) nm[d] = zo::neighbour_dev(n, m, static_cast<zo::Direction>(d));
+            if (UNIFORM) {
 #pragma unroll
-            for (int d = 0; d < 4; ++d) off[d] = P.base[n] + nm[d];
-        } else {
-            uint8_t f[4];
+                for (int d = 0; d < 4; ++d) off[d] = P.base[n] + nm[d];
+            } else {
+                uint8_t f[4];
 #pragma unroll
-            for (int d = 0; d < 4; ++d) f[d] = (nm[d] != zo::kNone) ? sigc[P.fbase[n - 1] + (nm[d] >> 2)] : 1;
+                for (int d = 0; d < 4; ++d) f[d] = (nm[d] != zo::kNone) ? sigc[P.fbase[n - 1] + (nm[d] >> 2)] : 1;
 #pragma unroll
-            for (int d = 0; d < 4; ++d) off[d] = f[d] ? P.base[n] + nm[d] : covering(P, sigc, n - 1, nm[d] >> 2);
+                for (int d = 0; d < 4; ++d) off[d] = f[d] ? P.base[n] + nm[d] : covering(P, sigc, n - 1, nm[d] >> 2);
+            }
+            double4 r4[4];
+#pragma unroll
+            for (int d = 0; d < 4; ++d)
+                if (nm[d] != zo::kNone) r4[d] = ld4_nc(cur + off[d]);
+            const CellV own = make_cell(o4, P.phys);
+            // the W, E, N, S neighbour as seen by its face (ghost on the boundary)
+            auto neighbour = [&](int d) -> CellV {
+                if (nm[d] == zo::kNone) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, P.phys);
+                return make_cell(r4[d], P.phys);
+            };
+            fv1_cell_seq(own, neighbour, P.inv_dx[n], dt, P.phys, hn, qxn, qyn);
+            zown = o4.w;
+            if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))
+                report_error(ctl, kErrNonFinite, zo::z_of(n, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2),
+                             kStageFV1);
+            st4(nxt + P.base[n] + m, make_double4(hn, qxn, qyn, zown));
+            const double c = cfl_rate(hn, qxn, qyn, P.inv_dx[n], P.phys);
+            mx = c > mx ? c : mx;
         }
-        double4 r4[4];
-#pragma unroll
-        for (int d = 0; d < 4; ++d)
-            if (nm[d] != zo::kNone) r4[d] = ld4_nc(cur + off[d]);
-        const CellV own = make_cell(o4, P.phys);
-        // the W, E, N, S neighbour as seen by its face (ghost on the boundary)
-        auto neighbour = [&](int d) -> CellV {
-            if (nm[d] == zo::kNone) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, P.phys);
-            return make_cell(r4[d], P.phys);
-        };
-        double hn, qxn, qyn;
-        fv1_cell_seq(own, neighbour, P.inv_dx[n], dt, P.phys, hn, qxn, qyn);
-        if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))
-            report_error(ctl, kErrNonFinite, zo::z_of(n, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2), kStageFV1);
-        st4(nxt + P.base[n] + m, make_double4(hn, qxn, qyn, o4.w));
-        const double c = cfl_rate(hn, qxn, qyn, P.inv_dx[n], P.phys);
-        mx = c > mx ? c : mx;
+        // Next step's zero_details_and_reencode of level L-1, fused here: the
+        // four updated children of a previous-tree level-(L-1) cell sit in
+        // lanes 4k..4k+3; lane 4k forms the parent and its significance
+        // (identical arithmetic to k_encode; the next K1 starts at L-2).
+        if (!UNIFORM && wbase < NA) {
+            const Enc e = encode_lanes<false>(make_double4(hn, qxn, qyn, zown), 1, P, P.L - 1);
+            if ((lane & 3) == 0 && i < NA) {
+                const uint32_t pm = m >> 2;
+                st4(nxt + P.base[P.L - 1] + pm, e.par);
+                const unsigned long long fi = P.fbase[P.L - 1] + pm;
+                P.pre[fi] = (e.flow || P.dem[fi]) ? 1 : 0;
+                ++tree;
+            }
+        }
+    }
+    if (!UNIFORM) {
+        __shared__ unsigned s_red5[32];
+        const unsigned tt = block_sum(tree, s_red5);
+        if (threadIdx.x == 0 && tt) atomicAdd(&ctl->cnt_tree, (unsigned long long)tt);
     }
     cfl_reduce_and_finalize(P, ctl, mx, true);
 }
@@ -1116,7 +1208,7 @@ __global__ void k_descriptors(Params P, const Ctl* ctl, uint32_t* nbr, uint32_t 
     const int p = ctl->parity;
     const uint8_t* sigc = P.sig[p];
     for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < N; i += gridDim.x * kThreads) {
-        const uint32_t z = P.leaves[i];
+        const uint32_t z = P.leaves_x[i];
         const int n = zo::level_of(z);
         const uint32_t m = z - zo::level_offset(n);
         for (int d = 0; d < 4; ++d) {

@@ -136,7 +136,7 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     mark(1);
     launch_pdl(hwfv1::k_band, P.n_tiles, g->smem_k2, s, P, g->ctl, 0);
     mark(2);
-    launch_pdl(hwfv1::k_traverse, P.n_tiles, g->smem_k3, s, P, g->ctl, 0);
+    launch_pdl(hwfv1::k_traverse<false>, P.n_tiles, g->smem_k3, s, P, g->ctl, 0);
     mark(3);
     if (g->fv1_minb == 3)
         launch_pdl(hwfv1::k_fv1<false, 3>, g->fv1_grid, 0, s, P, g->ctl);
@@ -273,8 +273,9 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     if ((st = dalloc(g, &P.pre, foff))) return fail(st);
     if ((st = dalloc(g, &P.dem, foff))) return fail(st);
     if ((st = dalloc(g, &P.leaves, nf * sizeof(uint32_t)))) return fail(st);
-    if ((st = dalloc(g, &P.tile_cnt, P.n_tiles * sizeof(uint32_t)))) return fail(st);
-    if ((st = dalloc(g, &P.tile_off, P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    if ((st = dalloc(g, &P.leaves_x, nf * sizeof(uint32_t)))) return fail(st);
+    if ((st = dalloc(g, &P.tile_cnt, 2 * P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    if ((st = dalloc(g, &P.tile_off, 3 * P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.tile_lvl, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.tile_src, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &g->ctl, sizeof(Ctl)))) return fail(st);
@@ -340,7 +341,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     {
         const size_t top = ((1u << (2 * (P.R + 1))) - 1u) / 3u;  // cells on levels 0..R
         g->smem_k2 = std::max<size_t>(((1u << (2 * P.K)) - 1u) / 3u,
-                                      ((4 * top + 15) & ~size_t(15)) + 4 * (size_t(1) << (2 * P.R)));
+                                      ((4 * top + 15) & ~size_t(15)) + 8 * (size_t(1) << (2 * P.R)));
         if (g->smem_k2 > 48 * 1024 &&
             cudaFuncSetAttribute(hwfv1::k_band, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(g->smem_k2)) != cudaSuccess)
@@ -364,7 +365,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
         cudaMemsetAsync(P.pre, 1, foff, s);
         // leaf list = every finest cell in Morton order (for exports)
         hwfv1::k_band<<<P.n_tiles, kThreads, g->smem_k2, s>>>(P, g->ctl, 1);
-        hwfv1::k_traverse<<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 1);
+        hwfv1::k_traverse<false><<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 1);
         cudaMemcpyAsync(P.cells[1], P.cells[0], off * sizeof(double4), cudaMemcpyDeviceToDevice, s);
         hwfv1::k_cfl_init<<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl, 1);
     } else {
@@ -373,7 +374,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
         cudaMemsetAsync(P.sig[0], 1, foff, s);
         hwfv1::k_encode<true><<<P.n_tiles, kThreads, g->smem_k1, s>>>(P, g->ctl);
         hwfv1::k_band<<<P.n_tiles, kThreads, g->smem_k2, s>>>(P, g->ctl, 1);
-        hwfv1::k_traverse<<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 1);
+        hwfv1::k_traverse<false><<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 1);
         // both buffers hold the full hierarchy; the current tree becomes "previous"
         cudaMemcpyAsync(P.cells[1], P.cells[0], off * sizeof(double4), cudaMemcpyDeviceToDevice, s);
         const int one = 1;
@@ -512,7 +513,11 @@ int swamp_gpu_copy_leaves(swamp_gpu* g, uint32_t* leaves, uint32_t* nw, uint32_t
     if (n) *n = N;
     if (!leaves && !nw && !ne && !nn && !ns) return SWAMP_OK;
     if (cap < static_cast<int64_t>(N)) return SWAMP_E_ARG;
-    if (leaves) CK(cudaMemcpy(leaves, g->P.leaves, N * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    // Morton-ordered LeafAssembly of the current tree (the hot path keeps the
+    // level-L leaves first)
+    hwfv1::k_traverse<true><<<g->P.n_tiles, kThreads, g->smem_k3, g->stream>>>(g->P, g->ctl, 1);
+    CK(cudaStreamSynchronize(g->stream));
+    if (leaves) CK(cudaMemcpy(leaves, g->P.leaves_x, N * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     if (nw || ne || nn || ns) {
         uint32_t* d = nullptr;
         CK(cudaMalloc(&d, std::max<size_t>(16, 4ull * N * sizeof(uint32_t))));
