@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
     pdl_trigger();
     if (!force && !active(ctl, P)) return;
     tl_start(ctl, 1);
-    extern __shared__ uint8_t sf[];
+    extern __shared__ __align__(16) uint8_t smem2[];
     __shared__ unsigned s_red[32];
     __shared__ int s_last;
     const int p = ctl->parity;
@@ -651,44 +651,79 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
     const uint8_t* pre = P.pre;
     const int L = P.L, R = P.R, K = P.K;
     const uint32_t j = blockIdx.x;
+    const uint32_t ncell = ((1u << (2 * K)) - 1u) / 3u;     // subtree cells on levels R..L-1
+    uint16_t* cA = reinterpret_cast<uint16_t*>(smem2);      // level-L leaves under the cell
+    uint16_t* cB = cA + ncell;                              // coarser leaves under the cell
+    uint8_t* sf = reinterpret_cast<uint8_t*>(cB + ncell);   // band, then final flags
+    uint8_t* spre = sf + ncell;                             // pre-band flags of the subtree
 
+    // ---- the subtree's pre-band flags, word loads where a level has >= 4 cells
+    for (int n = R; n < L; ++n) {
+        const uint32_t cnt = 1u << (2 * (n - R));
+        const unsigned long long g = P.fbase[n] + static_cast<unsigned long long>(j) * cnt;
+        if (cnt >= 4) {
+            for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads) {
+                const uint32_t w = *reinterpret_cast<const uint32_t*>(pre + g + q);
+                uint8_t* d = spre + lo(n, R) + q;
+                d[0] = w & 0xFFu; d[1] = (w >> 8) & 0xFFu; d[2] = (w >> 16) & 0xFFu; d[3] = w >> 24;
+            }
+        } else if (threadIdx.x < cnt) {
+            spre[lo(n, R) + threadIdx.x] = pre[g + threadIdx.x];
+        }
+    }
+    __syncthreads();
+    // ---- band (D3): neighbours inside the subtree from shared memory
     for (int n = R; n < L; ++n) {
         const uint32_t cnt = 1u << (2 * (n - R));
         for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads)
-            sf[lo(n, R) + pi] = band_flag(P.band_mode, L, n, j * cnt + pi,
-                                          [&](int k, uint32_t mm) { return pre[P.fbase[k] + mm]; });
+            sf[lo(n, R) + pi] = band_flag(P.band_mode, L, n, j * cnt + pi, [&](int k, uint32_t mm) -> uint8_t {
+                const uint32_t kc = 1u << (2 * (k - R));
+                const uint32_t t = mm >> (2 * (k - R));
+                return (t == j) ? spre[lo(k, R) + (mm - j * kc)] : pre[P.fbase[k] + mm];
+            });
+    }
+    __syncthreads();
+    // ---- ancestor closure bottom-up, with the leaf counts of every subtree
+    //      cell assuming it is reached (level L-1: 4 level-L leaves or itself)
+    {
+        const uint32_t cnt = 1u << (2 * (L - 1 - R));
+        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
+            const bool sg = sf[lo(L - 1, R) + pi] != 0;
+            cA[lo(L - 1, R) + pi] = sg ? 4 : 0;
+            cB[lo(L - 1, R) + pi] = sg ? 0 : 1;
+        }
     }
     __syncthreads();
     for (int n = L - 2; n >= R; --n) {
         const uint32_t cnt = 1u << (2 * (n - R));
         for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
             const uint32_t c = lo(n + 1, R) + 4u * pi;
-            if (sf[c] | sf[c + 1] | sf[c + 2] | sf[c + 3]) sf[lo(n, R) + pi] = 1;
+            const bool sg = sf[lo(n, R) + pi] || sf[c] || sf[c + 1] || sf[c + 2] || sf[c + 3];
+            sf[lo(n, R) + pi] = sg ? 1 : 0;
+            cA[lo(n, R) + pi] = sg ? static_cast<uint16_t>(cA[c] + cA[c + 1] + cA[c + 2] + cA[c + 3]) : 0;
+            cB[lo(n, R) + pi] = sg ? static_cast<uint16_t>(cB[c] + cB[c + 1] + cB[c + 2] + cB[c + 3]) : 1;
         }
         __syncthreads();
     }
+    // ---- final flags of the subtree, word stores where a level has >= 4 cells
     for (int n = R; n < L; ++n) {
         const uint32_t cnt = 1u << (2 * (n - R));
-        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) sigc[P.fbase[n] + j * cnt + pi] = sf[lo(n, R) + pi];
-    }
-    // leaves in this subtree assuming its root is reached by the traversal:
-    // level-L leaves (A) and coarser leaves (B)
-    {
-        const uint32_t nc = 1u << (2 * (K - 1));  // level-(L-1) cells in the subtree
-        unsigned ca = 0, cb = 0;
-        for (uint32_t c = threadIdx.x; c < nc; c += kThreads) {
-            int n = R;
-            while (n < L && sf[lo(n, R) + (c >> (2 * (L - 1 - n)))]) ++n;
-            if (n == L) ca += 4;
-            else cb += ((c & ((1u << (2 * (L - 1 - n))) - 1u)) == 0u) ? 1u : 0u;
-        }
-        const unsigned ta = block_sum(ca, s_red);
-        const unsigned tb = block_sum(cb, s_red);
-        if (threadIdx.x == 0) {
-            P.tile_cnt[j] = ta;
-            P.tile_cnt[P.n_tiles + j] = tb;
+        const unsigned long long g = P.fbase[n] + static_cast<unsigned long long>(j) * cnt;
+        if (cnt >= 4) {
+            for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads) {
+                const uint8_t* d = sf + lo(n, R) + q;
+                *reinterpret_cast<uint32_t*>(sigc + g + q) =
+                    uint32_t(d[0]) | (uint32_t(d[1]) << 8) | (uint32_t(d[2]) << 16) | (uint32_t(d[3]) << 24);
+            }
+        } else if (threadIdx.x < cnt) {
+            sigc[g + threadIdx.x] = sf[lo(n, R) + threadIdx.x];
         }
     }
+    if (threadIdx.x == 0) {
+        P.tile_cnt[j] = cA[0];
+        P.tile_cnt[P.n_tiles + j] = cB[0];
+    }
+    uint8_t* sfl_top = smem2;  // the last CTA reuses the dynamic shared memory
     if (!last_block(&ctl->done_k2, &s_last)) return;
     tl_mark(ctl, 4);
 
@@ -696,11 +731,11 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
     //      and previous flags of levels 0..R, tsig = current flags of levels
     //      0..R (level R written by every CTA), intree = "on the current tree",
     //      tcnt = per-subtree counts
-    uint8_t* tsig = sf;                       // lo(R+1)
+    uint8_t* tsig = sfl_top;                  // lo(R+1)
     uint8_t* tprev = tsig + lo(R + 1, 0);     // lo(R+1)
     uint8_t* tpre = tprev + lo(R + 1, 0);     // lo(R+1)
     uint8_t* intree = tpre + lo(R + 1, 0);    // lo(R+1)
-    uint32_t* tcnt = reinterpret_cast<uint32_t*>(sf + ((4u * lo(R + 1, 0) + 15u) & ~15u));  // 4^R
+    uint32_t* tcnt = reinterpret_cast<uint32_t*>(sfl_top + ((4u * lo(R + 1, 0) + 15u) & ~15u));  // 2 x 4^R
     const uint8_t* sigp = P.sig[p];
     for (int n = 0; n <= R; ++n) {
         const uint32_t cnt = 1u << (2 * n);
@@ -839,12 +874,26 @@ __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int f
     const uint32_t rootsrc = P.tile_src[j];
     const bool reached = leafn == static_cast<uint32_t>(R);
     int any_new = 0;
-    for (int n = R; n < L; ++n) {
+    for (int n = R; n < L; ++n) {  // current / previous flags of the subtree, word loads
         const uint32_t cnt = 1u << (2 * (n - R));
-        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
-            const uint8_t c = sigc[P.fbase[n] + j * cnt + pi], q = sigp[P.fbase[n] + j * cnt + pi];
-            sc[lo(n, R) + pi] = c;
-            sp[lo(n, R) + pi] = q;
+        const unsigned long long g = P.fbase[n] + static_cast<unsigned long long>(j) * cnt;
+        if (cnt >= 4) {
+            for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads) {
+                const uint32_t wc = *reinterpret_cast<const uint32_t*>(sigc + g + q);
+                const uint32_t wp = *reinterpret_cast<const uint32_t*>(sigp + g + q);
+                uint8_t* dc = sc + lo(n, R) + q;
+                uint8_t* dp = sp + lo(n, R) + q;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    dc[k] = (wc >> (8 * k)) & 0xFFu;
+                    dp[k] = (wp >> (8 * k)) & 0xFFu;
+                }
+                any_new |= (wc & ~wp) ? 1 : 0;
+            }
+        } else if (threadIdx.x < cnt) {
+            const uint8_t c = sigc[g + threadIdx.x], q = sigp[g + threadIdx.x];
+            sc[lo(n, R) + threadIdx.x] = c;
+            sp[lo(n, R) + threadIdx.x] = q;
             any_new |= (c && !q) ? 1 : 0;
         }
     }
@@ -895,16 +944,38 @@ __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int f
         if (!EXPORT) tl_mark(ctl, 8);
         return;
     }
-    const uint32_t nc = 1u << (2 * (K - 1));  // level-(L-1) cells in the subtree
-    const uint32_t per = (nc + kThreads - 1) / kThreads;
+    // one walk per level-(L-2) cell (its 4 level-(L-1) children share the
+    // path); K = 1 (L = 1) walks the level-(L-1) cells directly
+    const int G = (K >= 2) ? L - 2 : L - 1;              // walked level
+    const uint32_t ng = 1u << (2 * (G - R));               // walked cells in the subtree
+    const uint32_t per = (ng + kThreads - 1) / kThreads;
     const uint32_t a = threadIdx.x * per;
-    const uint32_t b = min(nc, a + per);
-    unsigned ca = 0, cb = 0;
-    for (uint32_t c = a; c < b; ++c) {
+    const uint32_t b = min(ng, a + per);
+    const uint32_t loL1 = lo(L - 1, R);
+    // depth of the walk: first level <= G whose cell is not significant, or G + 1
+    auto walk = [&](uint32_t t) -> int {
         int n = R;
-        while (n < L && sc[lo(n, R) + (c >> (2 * (L - 1 - n)))]) ++n;
-        if (n == L) ca += 4;
-        else cb += ((c & ((1u << (2 * (L - 1 - n))) - 1u)) == 0u) ? 1u : 0u;
+        uint32_t off = 0, span = 1;
+        while (n <= G && sc[off + (t >> (2 * (G - n)))]) {
+            off += span;
+            span <<= 2;
+            ++n;
+        }
+        return n;
+    };
+    unsigned ca = 0, cb = 0;
+    for (uint32_t t = a; t < b; ++t) {
+        const int n = walk(t);
+        if (n <= G) {
+            cb += ((t & ((1u << (2 * (G - n))) - 1u)) == 0u) ? 1u : 0u;
+        } else if (G == L - 1) {
+            ca += 4;
+        } else {
+            for (uint32_t k = 0; k < 4; ++k) {
+                if (sc[loL1 + 4u * t + k]) ca += 4;
+                else cb += 1;
+            }
+        }
     }
     unsigned total;
     if (EXPORT) {
@@ -913,18 +984,29 @@ __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int f
         oa += block_exscan(ca, s_red, &total);
         ob += block_exscan(cb, s_red, &total);
     }
-    const uint32_t gbase = j * nc;
-    for (uint32_t c = a; c < b; ++c) {
-        int n = R;
-        while (n < L && sc[lo(n, R) + (c >> (2 * (L - 1 - n)))]) ++n;
-        const uint32_t gm = gbase + c;
-        if (n == L) {
-            const uint32_t z0 = zo::z_of(L, gm << 2);
-            outA[oa] = z0; outA[oa + 1] = z0 + 1; outA[oa + 2] = z0 + 2; outA[oa + 3] = z0 + 3;
-            oa += 4;
-        } else if ((c & ((1u << (2 * (L - 1 - n))) - 1u)) == 0u) {
-            if (EXPORT) outA[oa++] = zo::z_of(n, gm >> (2 * (L - 1 - n)));
-            else P.leaves[ob++] = zo::z_of(n, gm >> (2 * (L - 1 - n)));
+    auto emitA = [&](uint32_t m1) {  // the 4 level-L children of level-(L-1) cell m1
+        const uint32_t z0 = zo::z_of(L, m1 << 2);
+        outA[oa] = z0; outA[oa + 1] = z0 + 1; outA[oa + 2] = z0 + 2; outA[oa + 3] = z0 + 3;
+        oa += 4;
+    };
+    auto emitB = [&](uint32_t z) {
+        if (EXPORT) outA[oa++] = z;
+        else P.leaves[ob++] = z;
+    };
+    const uint32_t gbase = j * ng;
+    for (uint32_t t = a; t < b; ++t) {
+        const int n = walk(t);
+        const uint32_t gm = gbase + t;
+        if (n <= G) {
+            if ((t & ((1u << (2 * (G - n))) - 1u)) == 0u) emitB(zo::z_of(n, gm >> (2 * (G - n))));
+        } else if (G == L - 1) {
+            emitA(gm);
+        } else {
+            for (uint32_t k = 0; k < 4; ++k) {
+                const uint32_t m1 = 4u * gm + k;
+                if (sc[loL1 + 4u * t + k]) emitA(m1);
+                else emitB(zo::z_of(L - 1, m1));
+            }
         }
     }
     if (!EXPORT) {

@@ -340,7 +340,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     g->smem_k1 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u) * (sizeof(double4) + 1);
     {
         const size_t top = ((1u << (2 * (P.R + 1))) - 1u) / 3u;  // cells on levels 0..R
-        g->smem_k2 = std::max<size_t>(((1u << (2 * P.K)) - 1u) / 3u,
+        g->smem_k2 = std::max<size_t>(6 * (((1u << (2 * P.K)) - 1u) / 3u),
                                       ((4 * top + 15) & ~size_t(15)) + 8 * (size_t(1) << (2 * P.R)));
         if (g->smem_k2 > 48 * 1024 &&
             cudaFuncSetAttribute(hwfv1::k_band, cudaFuncAttributeMaxDynamicSharedMemorySize,
