@@ -138,7 +138,9 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     mark(2);
     launch_pdl(hwfv1::k_traverse<false>, P.n_tiles, g->smem_k3, s, P, g->ctl, 0);
     mark(3);
-    if (g->fv1_minb == 3)
+    if (g->fv1_minb == 4)
+        launch_pdl(hwfv1::k_fv1<false, 4>, g->fv1_grid, 0, s, P, g->ctl);
+    else if (g->fv1_minb == 3)
         launch_pdl(hwfv1::k_fv1<false, 3>, g->fv1_grid, 0, s, P, g->ctl);
     else
         launch_pdl(hwfv1::k_fv1<false, 2>, g->fv1_grid, 0, s, P, g->ctl);
@@ -349,9 +351,11 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     }
     g->smem_k3 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u) * 6;
     {
-        if (const char* e = std::getenv("SWAMP_FV1_MINB")) g->fv1_minb = std::atoi(e) == 2 ? 2 : 3;
+        if (const char* e = std::getenv("SWAMP_FV1_MINB")) g->fv1_minb = std::max(2, std::min(4, std::atoi(e)));
         int occ = 0;
-        if (g->fv1_minb == 3)
+        if (g->fv1_minb == 4)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 4>, kThreads, 0);
+        else if (g->fv1_minb == 3)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 3>, kThreads, 0);
         else
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 2>, kThreads, 0);
