@@ -1168,13 +1168,29 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
 #pragma unroll
             for (int d = 0; d < 4; ++d)
                 if (nm[d] != zo::kNone) r4[d] = ld4_nc(cur + off[d]);
-            const CellV own = make_cell(o4, P.phys);
-            // the W, E, N, S neighbour as seen by its face (ghost on the boundary)
-            auto neighbour = [&](int d) -> CellV {
-                if (nm[d] == zo::kNone) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, P.phys);
-                return make_cell(r4[d], P.phys);
-            };
-            fv1_cell_seq(own, neighbour, P.inv_dx[n], dt, P.phys, hn, qxn, qyn);
+            // dry neighbourhood: own cell and every neighbour / ghost below
+            // h_dry => every reconstructed depth is 0, every flux 0, the bed
+            // corrections cancel pairwise: h stays, q = 0 (the general path
+            // gives the same bits)
+            bool all_dry = o4.x < P.phys.hdry;
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+                if (nm[d] != zo::kNone) all_dry = all_dry && r4[d].x < P.phys.hdry;
+                else if (P.bc[d] == 2) all_dry = false;  // inflow ghosts can be wet
+            }
+            if (all_dry) {
+                hn = (o4.x < 0.0) ? 0.0 : o4.x;
+                qxn = 0.0;
+                qyn = 0.0;
+            } else {
+                const CellV own = make_cell(o4, P.phys);
+                // the W, E, N, S neighbour as seen by its face (ghost on the boundary)
+                auto neighbour = [&](int d) -> CellV {
+                    if (nm[d] == zo::kNone) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, P.phys);
+                    return make_cell(r4[d], P.phys);
+                };
+                fv1_cell_seq(own, neighbour, P.inv_dx[n], dt, P.phys, hn, qxn, qyn);
+            }
             zown = o4.w;
             if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))
                 report_error(ctl, kErrNonFinite, zo::z_of(n, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2),

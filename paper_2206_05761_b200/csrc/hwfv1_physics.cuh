@@ -46,11 +46,15 @@ struct CellV {
 __device__ __forceinline__ CellV make_cell(double4 s, const PhysParams& p) {
     CellV c;
     c.h = s.x; c.qx = s.y; c.qy = s.z; c.z = s.w;
-    const bool wet = s.x >= p.hdry;
-    const double rh = wet ? 1.0 / s.x : 0.0;  // one reciprocal serves both components
-    c.ux = wet ? s.y * rh : 0.0;
-    c.uy = wet ? s.z * rh : 0.0;
-    c.c = sqrt(p.g * s.x);
+    c.ux = 0.0;
+    c.uy = 0.0;
+    c.c = 0.0;  // only read when the reconstructed depth equals a wet h (face())
+    if (s.x >= p.hdry) {  // dry cells need no reciprocal / square root
+        const double rh = 1.0 / s.x;  // one reciprocal serves both components
+        c.ux = s.y * rh;
+        c.uy = s.z * rh;
+        c.c = sqrt(p.g * s.x);
+    }
     return c;
 }
 
@@ -108,8 +112,10 @@ __device__ __forceinline__ void face(const CellV& L, const CellV& R, bool xface,
         F[0] = 0.0; F[1] = 0.0; F[2] = 0.0;
         return;
     }
-    const double cL = (hLs == L.h) ? L.c : sqrt(p.g * hLs);
-    const double cR = (hRs == R.h) ? R.c : sqrt(p.g * hRs);
+    // sqrt(g h*) (= the cell's c when the reconstruction kept its depth; a
+    // reconstructed depth is 0 or >= h_dry, so a dry cell's c is never read)
+    const double cL = (hLs == 0.0) ? 0.0 : ((hLs == L.h) ? L.c : sqrt(p.g * hLs));
+    const double cR = (hRs == 0.0) ? 0.0 : ((hRs == R.h) ? R.c : sqrt(p.g * hRs));
     if (xface) hll(hLs, L.ux, L.uy, hRs, R.ux, R.uy, cL, cR, p, F);
     else hll(hLs, L.uy, L.ux, hRs, R.uy, R.ux, cL, cR, p, F);
 }
