@@ -47,7 +47,7 @@ struct swamp_gpu {
     std::vector<void*> allocs;
     cudaGraphExec_t graph1 = nullptr, graphS = nullptr, graphT = nullptr;
     int fv1_grid = 0;
-    int fv1_minb = 3;  // occupancy variant of k_fv1 (SWAMP_FV1_MINB=2 for 2 CTAs/SM, no spills)
+    int fv1_minb = 2;  // occupancy variant of k_fv1 (SWAMP_FV1_MINB=3|4 for more CTAs/SM, with spills)
     int num_sms = 0;
     size_t smem_k1 = 0, smem_k2 = 0, smem_k3 = 0;
     cudaEvent_t ev[6] = {};
