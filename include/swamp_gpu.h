@@ -109,6 +109,18 @@ int swamp_gpu_create(const swamp_config* cfg, const double* h, const double* qx,
                      const double* z, int device, swamp_gpu** out);
 int swamp_gpu_destroy(swamp_gpu* g);
 
+/* Morton-subtree partitioned engine (BASELINE north star):
+ * n_parts (1, 2, 4 or 8; must divide the number of level-R subtrees 4^R)
+ * contiguous ranges of level-R subtrees, partition k on CUDA device
+ * devices[k] (devices may repeat: several partitions on one GPU run as
+ * virtual partitions with identical results). Cross-partition data (band
+ * flags, flux neighbours, level-R encode inputs, subtree counts, the CFL max)
+ * is read in place through peer pointers (NVLink peer access between distinct
+ * devices); results are bitwise equal to the single-partition engine. All
+ * other entry points accept the returned handle (no uniform / profiling). */
+int swamp_gpu_create_partitioned(const swamp_config* cfg, const double* h, const double* qx, const double* qy,
+                                 const double* z, int n_parts, const int* devices, swamp_gpu** out);
+
 /* step_adaptive: one Alg. 3 iteration. No-op when
  * t >= t_end. Fills `rep` (may be NULL). Synchronises the device. */
 int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep);

@@ -35,6 +35,7 @@ constexpr int kThreads = 256;
 constexpr int kMaxL = 13;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr uint32_t kNoSrc = 0xFFFFFFFFu;
+constexpr int kMaxParts = 8;
 
 enum Stage : int { kStageImport = 0, kStageEncode = 1, kStageBand = 2, kStageTraverse = 3, kStageFV1 = 5, kStageDt = 6 };
 enum ErrCode : int { kErrNone = 0, kErrNonFinite = -3, kErrDt = -4 };
@@ -44,13 +45,14 @@ struct Ctl {
     double dt;       // dt of the next step
     double t_next;   // time after the next step (exact stop time when clipped)
     double dt_used;  // dt of the last step taken
-    unsigned long long rate_bits;   // CFL max-rate accumulator (bits of a non-negative double)
+    unsigned long long rate_bits[2];  // CFL max-rate accumulators (bits of a non-negative double), by step parity
     unsigned long long smax_bits[4];
     long long step;
     unsigned long long cnt_tree;    // cells re-encoded by the last K1
     unsigned long long cnt_new;     // newly significant cells decoded by the last K3
     uint32_t n_leaves;              // leaves of the grid built by the last K2/K3
     uint32_t n_leaves_A;            // of which level-L leaves (listed first, in sibling quadruples)
+    uint32_t a_lo, a_hi, b_lo, b_hi; // this partition's slices of the A (level-L) and B lists
     uint32_t n_leaves_used;         // leaves the last FV1 updated
     int parity;                     // current cell buffer / previous-tree flags
     int err_code;
@@ -112,6 +114,19 @@ struct Params {
     uint32_t* tile_off;
     uint32_t* tile_lvl;   // traversal depth of each level-R subtree root (R = reached)
     uint32_t* tile_src;   // z of the root's decode source, or kNoSrc
+    // Morton-subtree partitions: this partition owns level-R
+    // subtrees [tile_lo, tile_hi); cells on levels >= R belong to their
+    // subtree's partition, cells above R are replicated except that a leaf's
+    // value is current only in the partition of its first subtree. pcells /
+    // psig / ppre / ptile_cnt / pctl are every partition's arrays (peer
+    // pointers across GPUs; index 0 = self when G = 1).
+    int G, part;
+    uint32_t tile_lo, tile_hi, tiles_per_part;
+    double4* pcells[kMaxParts][2];
+    uint8_t* psig[kMaxParts][2];
+    uint8_t* ppre[kMaxParts];
+    uint32_t* ptile_cnt[kMaxParts];
+    Ctl* pctl[kMaxParts];
 };
 
 // ------------------------------------------------------------------ memory ops
@@ -145,6 +160,21 @@ __device__ __forceinline__ uint32_t ldcg_u32(const uint32_t* p) {
 }
 
 __device__ __forceinline__ uint32_t lo(int n, int R) { return ((1u << (2 * (n - R))) - 1u) / 3u; }
+
+// partition owning cell (n, m): the one holding its (first) level-R subtree
+__device__ __forceinline__ int owner_of(const Params& P, int n, uint32_t m) {
+    if (P.G == 1) return 0;
+    const uint32_t t = (n >= P.R) ? (m >> (2 * (n - P.R))) : (m << (2 * (P.R - n)));
+    return static_cast<int>(t / P.tiles_per_part);
+}
+__device__ __forceinline__ double4* cell_ptr(const Params& P, int buf, int n, uint32_t m) {
+    return P.pcells[owner_of(P, n, m)][buf] + P.base[n] + m;
+}
+// significance byte of (n, m) in copy `which`; levels above R are replicated
+__device__ __forceinline__ uint8_t sig_at(const Params& P, int which, int n, uint32_t m) {
+    const int g = (n < P.R) ? P.part : owner_of(P, n, m);
+    return P.psig[g][which][P.fbase[n] + m];
+}
 
 __device__ __forceinline__ void report_error(Ctl* c, int code, uint32_t z, int q, int stage) {
     if (atomicCAS(&c->err_code, 0, code) == 0) {
@@ -429,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
     double4* buf = P.cells[p];
     const uint8_t* sigp = P.sig[p];
     const int L = P.L, R = P.R, K = P.K;
-    const uint32_t j = blockIdx.x;
+    const uint32_t j = P.tile_lo + blockIdx.x;
     const uint32_t ncell = ((1u << (2 * K)) - 1u) / 3u;  // subtree cells on levels R..L-1
     uint8_t* sfl = reinterpret_cast<uint8_t*>(sv + ncell);  // previous-tree flags of the subtree
     unsigned tree = 0;
@@ -543,12 +573,32 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
 
     const unsigned tsum = block_sum(tree, s_red);
     if (threadIdx.x == 0 && tsum) atomicAdd(&ctl->cnt_tree, (unsigned long long)tsum);
+    if (P.G > 1) return;  // partitioned: k_encode_top runs after all partitions' subtrees
     if (!last_block(&ctl->done_k1, &s_last)) return;
     tl_mark(ctl, 1);
+    encode_top<INIT>(P, ctl, sv, s_red);
+    tl_mark(ctl, 2);
+}
 
-    // ---- last CTA: levels R-1 .. 0. Level R children come from global (L2,
-    //      written by every CTA); above that the block keeps its results in
-    //      shared memory when levels 0..R-1 fit (R <= K).
+template <bool INIT>
+__global__ void __launch_bounds__(kThreads) k_encode_top(Params P, Ctl* ctl) {
+    pdl_wait();
+    if (!INIT && !active(ctl, P)) return;
+    extern __shared__ double4 sv_top[];
+    __shared__ unsigned s_red[32];
+    encode_top<INIT>(P, ctl, sv_top, s_red);
+}
+
+// Levels R-1 .. 0 of the re-encode (one CTA). Level-R children come from
+// global memory (every subtree's CTA / partition wrote them); above that the
+// block keeps its results in shared memory when levels 0..R-1 fit (R <= K).
+template <bool INIT>
+__device__ void encode_top(const Params& P, Ctl* ctl, double4* sv, unsigned* s_red) {
+    const int p = ctl->parity;
+    double4* buf = P.cells[p];
+    const uint8_t* sigp = P.sig[p];
+    const int R = P.R, K = P.K;
+
     unsigned ttop = 0;
     const bool top_smem = ((1u << (2 * R)) - 1u) / 3u <= ((1u << (2 * K)) - 1u) / 3u;
     for (int n = R - 1; n >= 0; --n) {
@@ -563,8 +613,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
                     const uint32_t c0 = lo(n + 1, 0) + 4u * pm;
                     c[0] = sv[c0]; c[1] = sv[c0 + 1]; c[2] = sv[c0 + 2]; c[3] = sv[c0 + 3];
                 } else {
-                    const double4* cp = buf + P.base[n + 1] + (static_cast<unsigned long long>(pm) << 2);
-                    c[0] = ld4_cg(cp); c[1] = ld4_cg(cp + 1); c[2] = ld4_cg(cp + 2); c[3] = ld4_cg(cp + 3);
+                    const uint32_t c0 = pm << 2;  // the children's partition(s) hold them
+                    c[0] = ld4_cg(cell_ptr(P, p, n + 1, c0)); c[1] = ld4_cg(cell_ptr(P, p, n + 1, c0 + 1));
+                    c[2] = ld4_cg(cell_ptr(P, p, n + 1, c0 + 2)); c[3] = ld4_cg(cell_ptr(P, p, n + 1, c0 + 3));
                 }
                 const Enc e = encode_children<INIT>(c, P, n);
                 flow = e.flow;
@@ -574,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
                 ++ttop;
             } else {
                 flow = 0.0 >= P.tau[n];
-                if (top_smem && n > 0 && sigp[P.fbase[n - 1] + (pm >> 2)]) sv[lo(n, 0) + pm] = ld4_cg(buf + P.base[n] + pm);
+                if (top_smem && n > 0 && sigp[P.fbase[n - 1] + (pm >> 2)]) sv[lo(n, 0) + pm] = ld4_cg(cell_ptr(P, p, n, pm));
             }
             uint8_t d;
             if (INIT) {
@@ -593,8 +644,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
         if (tt) atomicAdd(&ctl->cnt_tree, (unsigned long long)tt);
         ctl->done_k1 = 0;
     }
-    tl_mark(ctl, 2);
 }
+
 
 // ----------------------------------------------------------- decode helper
 // decode_tree under D4 + PTT (Alg. 5) +
@@ -603,7 +654,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
 // below a chain of newly significant cells takes the value of the chain's top.
 __device__ __forceinline__ void write_projection(double4* buf, const Params& P, int n, uint32_t m, uint32_t src) {
     const int ns = zo::level_of(src);
-    const double4 v = ld4_cg(buf + P.base[ns] + (src - zo::level_offset(ns)));
+    const int p = static_cast<int>(buf == P.cells[1]);
+    const double4 v = ld4_cg(cell_ptr(P, p, ns, src - zo::level_offset(ns)));
     double4* dst = buf + P.base[n] + m;
     const double4 old = ld4_cg(dst);
     st4(dst, make_double4(v.x, v.y, v.z, old.w));
@@ -638,6 +690,8 @@ __device__ __forceinline__ uint8_t band_flag(int mode, int L, int n, uint32_t m,
 // count; the last CTA closes levels < R and scans subtree counts into the
 // leaf-list offsets (the PTT compaction's global scan, done once on 4^R
 // values instead of per finest cell).
+__device__ void band_top(const Params& P, Ctl* ctl, uint8_t* sfl_top, unsigned* s_red);
+
 __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force) {
     pdl_wait();
     pdl_trigger();
@@ -650,7 +704,7 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
     uint8_t* sigc = P.sig[p ^ 1];
     const uint8_t* pre = P.pre;
     const int L = P.L, R = P.R, K = P.K;
-    const uint32_t j = blockIdx.x;
+    const uint32_t j = P.tile_lo + blockIdx.x;
     const uint32_t ncell = ((1u << (2 * K)) - 1u) / 3u;     // subtree cells on levels R..L-1
     uint16_t* cA = reinterpret_cast<uint16_t*>(smem2);      // level-L leaves under the cell
     uint16_t* cB = cA + ncell;                              // coarser leaves under the cell
@@ -679,7 +733,7 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
             sf[lo(n, R) + pi] = band_flag(P.band_mode, L, n, j * cnt + pi, [&](int k, uint32_t mm) -> uint8_t {
                 const uint32_t kc = 1u << (2 * (k - R));
                 const uint32_t t = mm >> (2 * (k - R));
-                return (t == j) ? spre[lo(k, R) + (mm - j * kc)] : pre[P.fbase[k] + mm];
+                return (t == j) ? spre[lo(k, R) + (mm - j * kc)] : P.ppre[owner_of(P, k, mm)][P.fbase[k] + mm];
             });
     }
     __syncthreads();
@@ -723,14 +777,32 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
         P.tile_cnt[j] = cA[0];
         P.tile_cnt[P.n_tiles + j] = cB[0];
     }
-    uint8_t* sfl_top = smem2;  // the last CTA reuses the dynamic shared memory
+    if (P.G > 1) return;  // partitioned: k_band_top runs after all partitions' subtrees
     if (!last_block(&ctl->done_k2, &s_last)) return;
     tl_mark(ctl, 4);
+    band_top(P, ctl, smem2, s_red);
+    tl_mark(ctl, 5);
+}
 
-    // ---- last CTA, all in shared memory (reusing sf): tpre / tprev = pre-band
-    //      and previous flags of levels 0..R, tsig = current flags of levels
-    //      0..R (level R written by every CTA), intree = "on the current tree",
-    //      tcnt = per-subtree counts
+__global__ void __launch_bounds__(kThreads) k_band_top(Params P, Ctl* ctl, int force) {
+    pdl_wait();
+    if (!force && !active(ctl, P)) return;
+    extern __shared__ __align__(16) uint8_t smem2t[];
+    __shared__ unsigned s_red[32];
+    band_top(P, ctl, smem2t, s_red);
+}
+
+// Top of K2 (one CTA), all in shared memory: tpre / tprev = pre-band and
+// previous flags of levels 0..R (replicated), tsig = current flags of levels
+// 0..R (level R from every subtree's partition), intree = "on the current
+// tree", tcnt = per-subtree counts. Band + closure of levels R-1..0, decode of
+// levels 1..R, per-subtree traversal depth and the leaf-list scans.
+__device__ void band_top(const Params& P, Ctl* ctl, uint8_t* sfl_top, unsigned* s_red) {
+    const int p = ctl->parity;
+    uint8_t* sigc = P.sig[p ^ 1];
+    const uint8_t* pre = P.pre;
+    const int L = P.L, R = P.R;
+
     uint8_t* tsig = sfl_top;                  // lo(R+1)
     uint8_t* tprev = tsig + lo(R + 1, 0);     // lo(R+1)
     uint8_t* tpre = tprev + lo(R + 1, 0);     // lo(R+1)
@@ -745,9 +817,10 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
                 tprev[lo(n, 0) + m] = sigp[P.fbase[n] + m];
             }
             if (n == R) {
-                tsig[lo(R, 0) + m] = ldcg_u8(sigc + P.fbase[R] + m);
-                tcnt[m] = ldcg_u32(P.tile_cnt + m);
-                tcnt[P.n_tiles + m] = ldcg_u32(P.tile_cnt + P.n_tiles + m);
+                const int g = owner_of(P, R, m);  // subtree m's partition
+                tsig[lo(R, 0) + m] = ldcg_u8(P.psig[g][p ^ 1] + P.fbase[R] + m);
+                tcnt[m] = ldcg_u32(P.ptile_cnt[g] + m);
+                tcnt[P.n_tiles + m] = ldcg_u32(P.ptile_cnt[g] + P.n_tiles + m);
             }
         }
     }
@@ -841,13 +914,19 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
         ob += cb;
         om += ca + cb;
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
         ctl->n_leaves = ta + tb;
         ctl->n_leaves_A = ta;
+        // this partition's slices of the A and B lists
+        ctl->a_lo = P.tile_off[P.tile_lo];
+        ctl->a_hi = (P.tile_hi < nt) ? P.tile_off[P.tile_hi] : ta;
+        ctl->b_lo = P.tile_off[nt + P.tile_lo];
+        ctl->b_hi = (P.tile_hi < nt) ? P.tile_off[nt + P.tile_hi] : ta + tb;
         ctl->done_k2 = 0;
     }
-    tl_mark(ctl, 5);
 }
+
 
 // EXPORT = re-run the traversal of the current tree (after a step) into the
 // Morton-ordered export list, with no side effects (no decode, no timeline).
@@ -864,7 +943,7 @@ __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int f
     const uint8_t* sigc = EXPORT ? P.sig[p] : P.sig[p ^ 1];
     const uint8_t* sigp = EXPORT ? P.sig[p ^ 1] : P.sig[p];
     const int L = P.L, R = P.R, K = P.K;
-    const uint32_t j = blockIdx.x;
+    const uint32_t j = P.tile_lo + blockIdx.x;
     const uint32_t ncell = ((1u << (2 * K)) - 1u) / 3u;  // subtree cells on levels R..L-1
     uint32_t* src = smem3;                               // [ncell]
     uint8_t* sc = reinterpret_cast<uint8_t*>(src + ncell);  // [ncell]
@@ -1068,24 +1147,27 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 }
 
 // reduce the per-thread CFL rates (exact max on the bits of non-negative
-// doubles), publish, and let the last CTA finish the step
+// doubles) into this step's slot; with one partition the last CTA finishes
+// the step, with several k_finalize does (after every partition's FV1)
 __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ctl, double rate, bool advance) {
     __shared__ unsigned long long s_max[kThreads / 32];
     __shared__ int s_last;
+    const int slot = static_cast<int>(ctl->step & 1);
     unsigned long long b = warp_max_u64(static_cast<unsigned long long>(__double_as_longlong(rate)));
     if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = b;
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long m = s_max[0];
         for (int w = 1; w < kThreads / 32; ++w) m = s_max[w] > m ? s_max[w] : m;
-        atomicMax(&ctl->rate_bits, m);
+        atomicMax(&ctl->rate_bits[slot], m);
     }
+    if (P.G > 1) return;  // partitioned: k_finalize combines every partition's slot
     if (!last_block(&ctl->done_k5, &s_last)) return;
     tl_mark(ctl, 10);
     if (threadIdx.x == 0) {
-        const unsigned long long m = atomicAdd(&ctl->rate_bits, 0ull);
+        const unsigned long long m = atomicAdd(&ctl->rate_bits[slot], 0ull);
         finalize_dt(P, ctl, __longlong_as_double(static_cast<long long>(m)), advance);
-        ctl->rate_bits = 0ull;
+        ctl->rate_bits[slot] = 0ull;
         ctl->done_k5 = 0;
         const int tb = advance ? static_cast<int>((ctl->step - 1) & 1) : tl_buf(ctl);
         ctl->tl[tb][11] = gtimer();
@@ -1094,16 +1176,38 @@ __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ct
     }
 }
 
+// partitioned step end: global max of every partition's CFL rate (exact, so
+// every partition computes the same dt), then commit the step locally. The
+// slot of the next step is cleared; this step's slot stays readable by the
+// other partitions until the next step's barrier chain has passed.
+__global__ void k_finalize(Params P, Ctl* ctl, int advance) {
+    pdl_wait();
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (advance && !active(ctl, P)) return;
+    const int slot = static_cast<int>(ctl->step & 1);
+    unsigned long long m = 0ull;
+    for (int g = 0; g < P.G; ++g) {
+        const unsigned long long v = *((volatile const unsigned long long*)&P.pctl[g]->rate_bits[slot]);
+        m = v > m ? v : m;
+    }
+    const int tb = tl_buf(ctl);
+    finalize_dt(P, ctl, __longlong_as_double(static_cast<long long>(m)), advance != 0);
+    if (!advance) return;  // initialise: the host clears the slots afterwards
+    ctl->rate_bits[slot ^ 1] = 0ull;
+    ctl->tl[tb][11] = gtimer();
+    for (int k = 0; k < 12; ++k) ctl->tl[tb ^ 1][k] = 0ull;
+}
+
 // covering cell of a same-level neighbour region whose parent (k, mm) is NOT
 // significant: walk up until the parent is significant (SPEC.md:248 — the
 // coarser covering leaf); the fast path (parent significant -> the same-level
 // cell itself) is tested by the caller for all four faces at once
-__device__ __forceinline__ unsigned long long covering(const Params& P, const uint8_t* sigc, int k, uint32_t mm) {
-    while (k > 0 && !sigc[P.fbase[k - 1] + (mm >> 2)]) {
+__device__ __forceinline__ double4* covering(const Params& P, int cur, int k, uint32_t mm) {
+    while (k > 0 && !sig_at(P, cur ^ 1, k - 1, mm >> 2)) {
         mm >>= 2;
         --k;
     }
-    return P.base[k] + mm;
+    return cell_ptr(P, cur, k, mm);
 }
 
 // FV1 over the leaf list: persistent grid-stride, one thread per
@@ -1118,10 +1222,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     const double4* __restrict__ cur = P.cells[p];
     double4* __restrict__ nxt = P.cells[p ^ 1];
     const uint8_t* __restrict__ sigc = P.sig[p ^ 1];
-    const uint32_t N = UNIFORM ? (1u << (2 * P.L)) : ctl->n_leaves;
-    // the leaf list starts with the level-L leaves (sibling quadruples at
-    // indices 4g..4g+3), then the coarser leaves
-    const uint32_t NA = UNIFORM ? 0u : ctl->n_leaves_A;
+    // this partition's leaves: its slice of the level-L list A (sibling
+    // quadruples at indices 4g..4g+3) followed by its slice of list B
+    const uint32_t a_lo = UNIFORM ? 0u : ctl->a_lo, b_lo = UNIFORM ? 0u : ctl->b_lo;
+    const uint32_t NA = UNIFORM ? 0u : ctl->a_hi - a_lo;
+    const uint32_t N = UNIFORM ? (1u << (2 * P.L)) : NA + (ctl->b_hi - b_lo);
+    auto leaf_at = [&](uint32_t k) { return P.leaves[k < NA ? a_lo + k : b_lo + (k - NA)]; };
     const double t = ctl->t, dt = ctl->dt;
     const double inflow = series_value(P, t);
     const int lane = threadIdx.x & 31;
@@ -1130,7 +1236,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     const uint32_t stride = gridDim.x * kThreads;
     // warp-uniform trip count: every lane runs every iteration (shuffles below)
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
-    uint32_t z_next = (!UNIFORM && wbase + lane < N) ? P.leaves[wbase + lane] : 0u;
+    uint32_t z_next = (!UNIFORM && wbase + lane < N) ? leaf_at(wbase + lane) : 0u;
     for (; wbase < N; wbase += stride) {
         const uint32_t i = wbase + lane;
         const bool valid = i < N;
@@ -1141,7 +1247,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             m = valid ? i : 0u;
         } else {
             const uint32_t z = valid ? z_next : zo::level_offset(P.L);  // leaf ids prefetched one iteration ahead
-            if (i + stride < N) z_next = P.leaves[i + stride];
+            if (i + stride < N) z_next = leaf_at(i + stride);
             n = zo::level_of(z);
             m = z - zo::level_offset(n);
         }
@@ -1151,23 +1257,24 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             // own cell, the neighbours' parent-level flags, the neighbours
             const double4 o4 = ld4_nc(cur + P.base[n] + m);
             uint32_t nm[4];
-            unsigned long long off[4];
+            const double4* src[4];
 #pragma unroll
             for (int d = 0; d < 4; ++d) nm[d] = zo::neighbour_dev(n, m, static_cast<zo::Direction>(d));
             if (UNIFORM) {
 #pragma unroll
-                for (int d = 0; d < 4; ++d) off[d] = P.base[n] + nm[d];
+                for (int d = 0; d < 4; ++d) src[d] = cur + P.base[n] + nm[d];
             } else {
                 uint8_t f[4];
 #pragma unroll
-                for (int d = 0; d < 4; ++d) f[d] = (nm[d] != zo::kNone) ? sigc[P.fbase[n - 1] + (nm[d] >> 2)] : 1;
+                for (int d = 0; d < 4; ++d) f[d] = (nm[d] != zo::kNone) ? sig_at(P, p ^ 1, n - 1, nm[d] >> 2) : 1;
 #pragma unroll
-                for (int d = 0; d < 4; ++d) off[d] = f[d] ? P.base[n] + nm[d] : covering(P, sigc, n - 1, nm[d] >> 2);
+                for (int d = 0; d < 4; ++d)
+                    src[d] = f[d] ? cell_ptr(P, p, n, nm[d]) : covering(P, p, n - 1, nm[d] >> 2);
             }
             double4 r4[4];
 #pragma unroll
             for (int d = 0; d < 4; ++d)
-                if (nm[d] != zo::kNone) r4[d] = ld4_nc(cur + off[d]);
+                if (nm[d] != zo::kNone) r4[d] = ld4_nc(src[d]);
             // dry neighbourhood: own cell and every neighbour / ghost below
             // h_dry => every reconstructed depth is 0, every flux 0, the bed
             // corrections cancel pairwise: h stays, q = 0 (the general path
@@ -1226,7 +1333,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
 __global__ void __launch_bounds__(kThreads) k_cfl_init(Params P, Ctl* ctl, int uniform) {
     const int p = ctl->parity;
     const double4* cur = P.cells[p];
-    const uint32_t N = uniform ? (1u << (2 * P.L)) : ctl->n_leaves;
+    const uint32_t a_lo = uniform ? 0u : ctl->a_lo, b_lo = uniform ? 0u : ctl->b_lo;
+    const uint32_t NA = uniform ? 0u : ctl->a_hi - a_lo;
+    const uint32_t N = uniform ? (1u << (2 * P.L)) : NA + (ctl->b_hi - b_lo);
     double mx = 0.0;
     for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < N; i += gridDim.x * kThreads) {
         int n;
@@ -1235,7 +1344,7 @@ __global__ void __launch_bounds__(kThreads) k_cfl_init(Params P, Ctl* ctl, int u
             n = P.L;
             m = i;
         } else {
-            const uint32_t z = P.leaves[i];
+            const uint32_t z = P.leaves[i < NA ? a_lo + i : b_lo + (i - NA)];
             n = zo::level_of(z);
             m = z - zo::level_offset(n);
         }
@@ -1287,12 +1396,12 @@ __global__ void k_export_tree(Params P, const Ctl* ctl, double* h, double* qx, d
     for (uint32_t zi = blockIdx.x * kThreads + threadIdx.x; zi < total; zi += gridDim.x * kThreads) {
         const int n = zo::level_of(zi);
         const uint32_t m = zi - zo::level_offset(n);
-        if (n < P.L) sig[zi] = sigc[P.fbase[n] + m];
-        const bool in_tree = (n == 0) || sigc[P.fbase[n - 1] + (m >> 2)];
-        const bool is_sig = (n < P.L) && sigc[P.fbase[n] + m];
+        if (n < P.L) sig[zi] = sig_at(P, p, n, m);
+        const bool in_tree = (n == 0) || sig_at(P, p, n - 1, m >> 2);
+        const bool is_sig = (n < P.L) && sig_at(P, p, n, m);
         const double nan = __longlong_as_double(0x7FF8000000000000ll);
         double4 v = make_double4(nan, nan, nan, nan);
-        if (in_tree) v = ld4(P.cells[is_sig ? (p ^ 1) : p] + P.base[n] + m);
+        if (in_tree) v = ld4(cell_ptr(P, is_sig ? (p ^ 1) : p, n, m));
         const double sc = ldexp(1.0, P.L - n);
         h[zi] = v.x * sc;
         qx[zi] = v.y * sc;
@@ -1317,7 +1426,7 @@ __global__ void k_descriptors(Params P, const Ctl* ctl, uint32_t* nbr, uint32_t 
             } else {
                 int k = n;
                 uint32_t mm = nm;
-                while (k > 0 && !sigc[P.fbase[k - 1] + (mm >> 2)]) {
+                while (k > 0 && !sig_at(P, p, k - 1, mm >> 2)) {
                     mm >>= 2;
                     --k;
                 }
@@ -1339,8 +1448,8 @@ __global__ void k_export_finest(Params P, const Ctl* ctl, double* h, double* qx,
         const uint32_t i = static_cast<uint32_t>(r & (side - 1)), jj = static_cast<uint32_t>(r >> P.L);
         const uint32_t m = zo::interleave(i, jj);
         int n = 0;
-        while (n < P.L && sigc[P.fbase[n] + (m >> (2 * (P.L - n)))]) ++n;
-        const double4 v = ld4(P.cells[p] + P.base[n] + (m >> (2 * (P.L - n))));
+        while (n < P.L && sig_at(P, p, n, m >> (2 * (P.L - n)))) ++n;
+        const double4 v = ld4(cell_ptr(P, p, n, m >> (2 * (P.L - n))));
         h[r] = v.x;
         qx[r] = v.y;
         qy[r] = v.z;

@@ -53,8 +53,19 @@ struct swamp_gpu {
     cudaEvent_t ev[6] = {};
     std::string err;
     int64_t n_cells = 0;
+    // partitioned group: the shell owns one sub-engine per
+    // partition (each with full-size arrays on its device); empty otherwise
+    std::vector<swamp_gpu*> parts;
+    cudaEvent_t phase_ev[2] = {};  // per sub-engine: end of the last two phases
+    int phase = 0;
 
     ~swamp_gpu() {
+        for (swamp_gpu* q : parts) {
+            cudaSetDevice(q->device);
+            delete q;
+        }
+        for (auto& e : phase_ev)
+            if (e) cudaEventDestroy(e);
         if (graph1) cudaGraphExecDestroy(graph1);
         if (graphS) cudaGraphExecDestroy(graphS);
         if (graphT) cudaGraphExecDestroy(graphT);
@@ -213,19 +224,14 @@ void fill_report(const swamp_gpu* g, swamp_step_report* r) {
     r->n_leaves_next = g->uniform ? r->n_leaves : c.n_leaves;
 }
 
-int create_impl(const swamp_config* cfg, const double* h, const double* qx, const double* qy, const double* z,
-                int device, bool uniform, swamp_gpu** out) {
-    if (!out || !h || !qx || !qy || !z) return SWAMP_E_ARG;
-    *out = nullptr;
-    int st = validate(cfg);
-    if (st) return st;
-    auto* g = new swamp_gpu();
+// allocate + upload + import one (sub-)engine: everything before the
+// initialise pipeline. Partition `part` of `G` owns level-R subtrees
+// [part, part+1) * 4^R / G.
+int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const double* qx, const double* qy,
+               const double* z, int device, int G, int part) {
+    int st = SWAMP_OK;
+    auto fail = [&](int code) { return code; };
     g->device = device;
-    g->uniform = uniform;
-    auto fail = [&](int code) {
-        delete g;
-        return code;
-    };
     if (cudaSetDevice(device) != cudaSuccess) return fail(SWAMP_E_CUDA);
     if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(SWAMP_E_CUDA);
     for (auto& e : g->ev)
@@ -238,6 +244,12 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     P.K = std::min(L, 6);
     P.R = L - P.K;
     P.n_tiles = 1 << (2 * P.R);
+    if (G < 1 || G > hwfv1::kMaxParts || P.n_tiles % G != 0) return SWAMP_E_ARG;
+    P.G = G;
+    P.part = part;
+    P.tiles_per_part = static_cast<uint32_t>(P.n_tiles / G);
+    P.tile_lo = static_cast<uint32_t>(part) * P.tiles_per_part;
+    P.tile_hi = P.tile_lo + P.tiles_per_part;
     P.band_mode = cfg->band_mode;
     for (int k = 0; k < 4; ++k) P.bc[k] = cfg->bc[k];
     P.inflow_mode = cfg->inflow_mode;
@@ -281,6 +293,14 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     if ((st = dalloc(g, &P.tile_lvl, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.tile_src, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &g->ctl, sizeof(Ctl)))) return fail(st);
+    // peer tables: self only (a partitioned group fills in every partition)
+    for (int b = 0; b < 2; ++b) {
+        P.pcells[0][b] = P.cells[b];
+        P.psig[0][b] = P.sig[b];
+    }
+    P.ppre[0] = P.pre;
+    P.ptile_cnt[0] = P.tile_cnt;
+    P.pctl[0] = g->ctl;
     if (cudaMallocHost(&g->ctl_host, sizeof(Ctl)) != cudaSuccess) return fail(SWAMP_E_NOMEM);
     double *d_it = nullptr, *d_iv = nullptr, *d_out = nullptr;
     if ((st = dalloc(g, &d_it, sizeof(double) * std::max(1, cfg->inflow_n)))) return fail(st);
@@ -361,6 +381,27 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 2>, kThreads, 0);
         g->fv1_grid = std::max(1, occ) * g->num_sms;
     }
+    g->n_cells = static_cast<int64_t>(off);
+    return SWAMP_OK;
+}
+
+int create_impl(const swamp_config* cfg, const double* h, const double* qx, const double* qy, const double* z,
+                int device, bool uniform, swamp_gpu** out) {
+    if (!out || !h || !qx || !qy || !z) return SWAMP_E_ARG;
+    *out = nullptr;
+    int st = validate(cfg);
+    if (st) return st;
+    auto* g = new swamp_gpu();
+    g->uniform = uniform;
+    auto fail = [&](int code) {
+        delete g;
+        return code;
+    };
+    if ((st = setup_part(g, cfg, h, qx, qy, z, device, 1, 0))) return fail(st);
+    Params& P = g->P;
+    cudaStream_t s = g->stream;
+    const unsigned long long off = static_cast<unsigned long long>(g->n_cells);
+    const unsigned long long foff = P.fbase[P.L - 1] + (((1ull << (2 * (P.L - 1))) + 15ull) & ~15ull);
 
     if (uniform) {
         // full tree, no MRA: every detail cell significant
@@ -400,6 +441,219 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     return SWAMP_OK;
 }
 
+
+// ============================================================ partitioned
+// A group of G sub-engines (one per partition / GPU). Every phase of a step
+// runs on every partition, then a cross-partition barrier (events; peers'
+// arrays are read in place through the peer tables).
+template <class F>
+void group_phase(swamp_gpu* grp, F&& launch) {
+    const int G = static_cast<int>(grp->parts.size());
+    const int cur = grp->phase & 1, prev = cur ^ 1;
+    for (int g = 0; g < G; ++g) {
+        swamp_gpu* q = grp->parts[g];
+        cudaSetDevice(q->device);
+        if (grp->phase > 0)
+            for (int h = 0; h < G; ++h)
+                if (h != g) cudaStreamWaitEvent(q->stream, grp->parts[h]->phase_ev[prev], 0);
+        launch(q);
+        cudaEventRecord(q->phase_ev[cur], q->stream);
+    }
+    grp->phase++;
+}
+
+int group_sync(swamp_gpu* grp) {
+    for (swamp_gpu* q : grp->parts) {
+        cudaSetDevice(q->device);
+        cudaError_t e = cudaStreamSynchronize(q->stream);
+        if (e != cudaSuccess) {
+            grp->err = cudaGetErrorString(e);
+            return SWAMP_E_CUDA;
+        }
+    }
+    for (swamp_gpu* q : grp->parts) {
+        int st = fetch_ctl(q);
+        if (st) {
+            grp->err = q->err;
+            return st;
+        }
+    }
+    return SWAMP_OK;
+}
+
+void group_enqueue_step(swamp_gpu* grp) {
+    group_phase(grp, [](swamp_gpu* q) {
+        hwfv1::k_encode<false><<<q->P.tiles_per_part, kThreads, q->smem_k1, q->stream>>>(q->P, q->ctl);
+    });
+    group_phase(grp, [](swamp_gpu* q) {
+        hwfv1::k_encode_top<false><<<1, kThreads, q->smem_k1, q->stream>>>(q->P, q->ctl);
+    });
+    group_phase(grp, [](swamp_gpu* q) {
+        hwfv1::k_band<<<q->P.tiles_per_part, kThreads, q->smem_k2, q->stream>>>(q->P, q->ctl, 0);
+    });
+    group_phase(grp, [](swamp_gpu* q) {
+        hwfv1::k_band_top<<<1, kThreads, q->smem_k2, q->stream>>>(q->P, q->ctl, 0);
+    });
+    group_phase(grp, [](swamp_gpu* q) {
+        hwfv1::k_traverse<false><<<q->P.tiles_per_part, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 0);
+    });
+    group_phase(grp, [](swamp_gpu* q) {
+        if (q->fv1_minb == 4) hwfv1::k_fv1<false, 4><<<q->fv1_grid, kThreads, 0, q->stream>>>(q->P, q->ctl);
+        else if (q->fv1_minb == 3) hwfv1::k_fv1<false, 3><<<q->fv1_grid, kThreads, 0, q->stream>>>(q->P, q->ctl);
+        else hwfv1::k_fv1<false, 2><<<q->fv1_grid, kThreads, 0, q->stream>>>(q->P, q->ctl);
+    });
+    group_phase(grp, [](swamp_gpu* q) { hwfv1::k_finalize<<<1, 32, 0, q->stream>>>(q->P, q->ctl, 1); });
+}
+
+int create_group(const swamp_config* cfg, const double* h, const double* qx, const double* qy, const double* z,
+                 int G, const int* devices, swamp_gpu** out) {
+    if (!out || !h || !qx || !qy || !z || G < 1 || G > hwfv1::kMaxParts) return SWAMP_E_ARG;
+    *out = nullptr;
+    int st = validate(cfg);
+    if (st) return st;
+    auto* grp = new swamp_gpu();
+    auto fail = [&](int code) {
+        delete grp;
+        return code;
+    };
+    grp->device = devices ? devices[0] : 0;
+    for (int g = 0; g < G; ++g) {
+        auto* q = new swamp_gpu();
+        grp->parts.push_back(q);
+        if ((st = setup_part(q, cfg, h, qx, qy, z, devices ? devices[g] : 0, G, g))) {
+            grp->err = q->err;
+            return fail(st);
+        }
+        for (auto& e : q->phase_ev)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return fail(SWAMP_E_CUDA);
+    }
+    // peer access between distinct devices (NVLink / NVSwitch)
+    for (int a = 0; a < G; ++a)
+        for (int b = 0; b < G; ++b) {
+            const int da = grp->parts[a]->device, db = grp->parts[b]->device;
+            if (da == db) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, da, db);
+            if (!can) return fail(SWAMP_E_CUDA);
+            cudaSetDevice(da);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return fail(SWAMP_E_CUDA);
+            cudaGetLastError();
+        }
+    for (swamp_gpu* q : grp->parts)
+        for (int k = 0; k < G; ++k) {
+            swamp_gpu* r = grp->parts[k];
+            for (int b = 0; b < 2; ++b) {
+                q->P.pcells[k][b] = r->P.cells[b];
+                q->P.psig[k][b] = r->P.sig[b];
+            }
+            q->P.ppre[k] = r->P.pre;
+            q->P.ptile_cnt[k] = r->P.tile_cnt;
+            q->P.pctl[k] = r->ctl;
+        }
+    for (swamp_gpu* q : grp->parts) {
+        cudaSetDevice(q->device);
+        if (q->smem_k2 > 48 * 1024)
+            cudaFuncSetAttribute(hwfv1::k_band_top, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(q->smem_k2));
+    }
+    // initialise, phase by phase across the partitions
+    static const int kOne = 1;
+    group_phase(grp, [](swamp_gpu* q) {
+        const Params& P = q->P;
+        const size_t foff = P.fbase[P.L - 1] + (((size_t(1) << (2 * (P.L - 1))) + 15) & ~size_t(15));
+        cudaMemsetAsync(P.sig[0], 1, foff, q->stream);
+        hwfv1::k_encode<true><<<P.tiles_per_part, kThreads, q->smem_k1, q->stream>>>(P, q->ctl);
+    });
+    group_phase(grp, [](swamp_gpu* q) {
+        hwfv1::k_encode_top<true><<<1, kThreads, q->smem_k1, q->stream>>>(q->P, q->ctl);
+    });
+    group_phase(grp, [](swamp_gpu* q) {
+        hwfv1::k_band<<<q->P.tiles_per_part, kThreads, q->smem_k2, q->stream>>>(q->P, q->ctl, 1);
+    });
+    group_phase(grp, [](swamp_gpu* q) {
+        hwfv1::k_band_top<<<1, kThreads, q->smem_k2, q->stream>>>(q->P, q->ctl, 1);
+    });
+    group_phase(grp, [](swamp_gpu* q) {
+        hwfv1::k_traverse<false><<<q->P.tiles_per_part, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 1);
+    });
+    group_phase(grp, [](swamp_gpu* q) {
+        cudaMemcpyAsync(q->P.cells[1], q->P.cells[0], static_cast<size_t>(q->n_cells) * sizeof(double4),
+                        cudaMemcpyDeviceToDevice, q->stream);
+        cudaMemcpyAsync(&q->ctl->parity, &kOne, sizeof(int), cudaMemcpyHostToDevice, q->stream);
+        hwfv1::k_cfl_init<<<q->fv1_grid, kThreads, 0, q->stream>>>(q->P, q->ctl, 0);
+    });
+    group_phase(grp, [](swamp_gpu* q) { hwfv1::k_finalize<<<1, 32, 0, q->stream>>>(q->P, q->ctl, 0); });
+    if ((st = group_sync(grp))) return fail(st);
+    for (swamp_gpu* q : grp->parts) {
+        cudaSetDevice(q->device);
+        cudaMemsetAsync(q->ctl->rate_bits, 0, sizeof(q->ctl->rate_bits), q->stream);
+        cudaMemsetAsync(q->ctl->tl, 0, sizeof(q->ctl->tl), q->stream);
+    }
+    if ((st = group_sync(grp))) return fail(st);
+    *out = grp;
+    return SWAMP_OK;
+}
+
+// leaves_x (Morton order, already built) -> host leaves + W/E/N/S descriptors
+int copy_leaves_x(swamp_gpu* g, uint32_t N, uint32_t* leaves, uint32_t* nw, uint32_t* ne, uint32_t* nn,
+                  uint32_t* ns) {
+    cudaSetDevice(g->device);
+    if (leaves) CK(cudaMemcpy(leaves, g->P.leaves_x, N * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    if (nw || ne || nn || ns) {
+        uint32_t* d = nullptr;
+        CK(cudaMalloc(&d, std::max<size_t>(16, 4ull * N * sizeof(uint32_t))));
+        const int grid = std::max(1, std::min<int>(g->num_sms * 8, (N + kThreads - 1) / kThreads));
+        hwfv1::k_descriptors<<<grid, kThreads, 0, g->stream>>>(g->P, g->ctl, d, N);
+        cudaError_t e = cudaStreamSynchronize(g->stream);
+        uint32_t* outs[4] = {nw, ne, nn, ns};
+        for (int k = 0; k < 4 && e == cudaSuccess; ++k)
+            if (outs[k]) e = cudaMemcpy(outs[k], d + static_cast<size_t>(k) * N, N * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        CK(e);
+    }
+    return SWAMP_OK;
+}
+
+int group_copy_leaves(swamp_gpu* grp, uint32_t* leaves, uint32_t* nw, uint32_t* ne, uint32_t* nn, uint32_t* ns,
+                      int64_t cap, int64_t* n) {
+    int st = group_sync(grp);
+    if (st) return st;
+    swamp_gpu* p0 = grp->parts[0];
+    const uint32_t N = p0->ctl_host->n_leaves;
+    if (n) *n = N;
+    if (!leaves && !nw && !ne && !nn && !ns) return SWAMP_OK;
+    if (cap < static_cast<int64_t>(N)) return SWAMP_E_ARG;
+    for (swamp_gpu* q : grp->parts) {
+        cudaSetDevice(q->device);
+        hwfv1::k_traverse<true><<<q->P.tiles_per_part, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 1);
+    }
+    if ((st = group_sync(grp))) return st;
+    const uint32_t nt = static_cast<uint32_t>(p0->P.n_tiles);
+    std::vector<uint32_t> toff(3 * static_cast<size_t>(nt));
+    cudaSetDevice(p0->device);
+    if (cudaMemcpy(toff.data(), p0->P.tile_off, toff.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return SWAMP_E_CUDA;
+    for (size_t k = 1; k < grp->parts.size(); ++k) {  // gather the Morton-ordered slices into partition 0
+        swamp_gpu* q = grp->parts[k];
+        const uint32_t lo = toff[2 * nt + q->P.tile_lo];
+        const uint32_t hi = (q->P.tile_hi < nt) ? toff[2 * nt + q->P.tile_hi] : N;
+        if (hi > lo &&
+            cudaMemcpyPeer(p0->P.leaves_x + lo, p0->device, q->P.leaves_x + lo, q->device,
+                           (hi - lo) * sizeof(uint32_t)) != cudaSuccess)
+            return SWAMP_E_CUDA;
+    }
+    return copy_leaves_x(p0, N, leaves, nw, ne, nn, ns);
+}
+
+int group_advance(swamp_gpu* grp, int64_t n_steps, bool sync, swamp_step_report* rep) {
+    for (int64_t k = 0; k < n_steps; ++k) group_enqueue_step(grp);
+    if (!sync) return SWAMP_OK;
+    int st = group_sync(grp);
+    fill_report(grp->parts[0], rep);
+    return st;
+}
+
 }  // namespace
 
 extern "C" {
@@ -427,8 +681,14 @@ int swamp_gpu_set_profiling(swamp_gpu* g, int enabled) {
     return SWAMP_OK;
 }
 
+int swamp_gpu_create_partitioned(const swamp_config* cfg, const double* h, const double* qx, const double* qy,
+                                 const double* z, int n_parts, const int* devices, swamp_gpu** out) {
+    return create_group(cfg, h, qx, qy, z, n_parts, devices, out);
+}
+
 int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep) {
     if (!g) return SWAMP_E_ARG;
+    if (!g->parts.empty()) return group_advance(g, 1, true, rep);
     cudaSetDevice(g->device);
     if (g->profiling) {
         CK(cudaGraphLaunch(g->graphT, g->stream));
@@ -454,12 +714,14 @@ int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep) {
 
 int swamp_gpu_stream(swamp_gpu* g, void** stream) {
     if (!g || !stream) return SWAMP_E_ARG;
+    if (!g->parts.empty()) g = g->parts[0];
     *stream = static_cast<void*>(g->stream);
     return SWAMP_OK;
 }
 
 int swamp_gpu_enqueue(swamp_gpu* g, int64_t n_steps) {
     if (!g || n_steps < 0) return SWAMP_E_ARG;
+    if (!g->parts.empty()) return group_advance(g, n_steps, false, nullptr);
     cudaSetDevice(g->device);
     int64_t k = 0;
     for (; k + kGraphSteps <= n_steps; k += kGraphSteps) CK(cudaGraphLaunch(g->graphS, g->stream));
@@ -469,6 +731,7 @@ int swamp_gpu_enqueue(swamp_gpu* g, int64_t n_steps) {
 
 int swamp_gpu_advance(swamp_gpu* g, int64_t n_steps, swamp_step_report* rep) {
     if (!g || n_steps < 0) return SWAMP_E_ARG;
+    if (!g->parts.empty()) return group_advance(g, n_steps, true, rep);
     cudaSetDevice(g->device);
     int64_t k = 0;
     for (; k + kGraphSteps <= n_steps; k += kGraphSteps) CK(cudaGraphLaunch(g->graphS, g->stream));
@@ -485,6 +748,14 @@ int swamp_gpu_step_uniform(swamp_gpu* g, int64_t n_steps, swamp_step_report* rep
 
 int swamp_gpu_run(swamp_gpu* g, swamp_step_report* rep) {
     if (!g) return SWAMP_E_ARG;
+    if (!g->parts.empty()) {
+        int st = group_sync(g);
+        if (st) return st;
+        while (g->parts[0]->ctl_host->t < g->parts[0]->P.t_end)
+            if ((st = group_advance(g, 16, true, rep))) return st;
+        fill_report(g->parts[0], rep);
+        return SWAMP_OK;
+    }
     int st = fetch_ctl(g);
     if (st) return st;
     while (g->ctl_host->t < g->P.t_end) {
@@ -498,6 +769,11 @@ int swamp_gpu_run(swamp_gpu* g, swamp_step_report* rep) {
 int swamp_gpu_info(const swamp_gpu* gc, double* t, double* dt, int64_t* step, int64_t* n_leaves) {
     swamp_gpu* g = const_cast<swamp_gpu*>(gc);
     if (!g) return SWAMP_E_ARG;
+    if (!g->parts.empty()) {
+        const int st = group_sync(g);
+        if (st) return st;
+        g = g->parts[0];
+    }
     cudaSetDevice(g->device);
     int st = fetch_ctl(g);
     if (t) *t = g->ctl_host->t;
@@ -510,6 +786,7 @@ int swamp_gpu_info(const swamp_gpu* gc, double* t, double* dt, int64_t* step, in
 int swamp_gpu_copy_leaves(swamp_gpu* g, uint32_t* leaves, uint32_t* nw, uint32_t* ne, uint32_t* nn, uint32_t* ns,
                           int64_t cap, int64_t* n) {
     if (!g) return SWAMP_E_ARG;
+    if (!g->parts.empty()) return group_copy_leaves(g, leaves, nw, ne, nn, ns, cap, n);
     cudaSetDevice(g->device);
     int st = fetch_ctl(g);
     if (st) return st;
@@ -521,24 +798,16 @@ int swamp_gpu_copy_leaves(swamp_gpu* g, uint32_t* leaves, uint32_t* nw, uint32_t
     // level-L leaves first)
     hwfv1::k_traverse<true><<<g->P.n_tiles, kThreads, g->smem_k3, g->stream>>>(g->P, g->ctl, 1);
     CK(cudaStreamSynchronize(g->stream));
-    if (leaves) CK(cudaMemcpy(leaves, g->P.leaves_x, N * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-    if (nw || ne || nn || ns) {
-        uint32_t* d = nullptr;
-        CK(cudaMalloc(&d, std::max<size_t>(16, 4ull * N * sizeof(uint32_t))));
-        const int grid = std::max(1, std::min<int>(g->num_sms * 8, (N + kThreads - 1) / kThreads));
-        hwfv1::k_descriptors<<<grid, kThreads, 0, g->stream>>>(g->P, g->ctl, d, N);
-        cudaError_t e = cudaStreamSynchronize(g->stream);
-        uint32_t* outs[4] = {nw, ne, nn, ns};
-        for (int k = 0; k < 4 && e == cudaSuccess; ++k)
-            if (outs[k]) e = cudaMemcpy(outs[k], d + static_cast<size_t>(k) * N, N * sizeof(uint32_t), cudaMemcpyDeviceToHost);
-        cudaFree(d);
-        CK(e);
-    }
-    return SWAMP_OK;
+    return copy_leaves_x(g, N, leaves, nw, ne, nn, ns);
 }
 
 int swamp_gpu_export_tree(swamp_gpu* g, double* h, double* qx, double* qy, double* z, uint8_t* sig) {
     if (!g) return SWAMP_E_ARG;
+    if (!g->parts.empty()) {  // owner-aware export from partition 0
+        const int st = group_sync(g);
+        if (st) return st;
+        g = g->parts[0];
+    }
     cudaSetDevice(g->device);
     const size_t NH = swamp::zorder::hierarchy_cells(g->P.L);
     const size_t ND = swamp::zorder::detail_cells(g->P.L);
@@ -563,6 +832,11 @@ int swamp_gpu_export_tree(swamp_gpu* g, double* h, double* qx, double* qy, doubl
 
 int swamp_gpu_export_finest(swamp_gpu* g, double* h, double* qx, double* qy) {
     if (!g) return SWAMP_E_ARG;
+    if (!g->parts.empty()) {
+        const int st = group_sync(g);
+        if (st) return st;
+        g = g->parts[0];
+    }
     cudaSetDevice(g->device);
     const size_t nf = static_cast<size_t>(1) << (2 * g->P.L);
     double* d = nullptr;
@@ -581,6 +855,16 @@ int swamp_gpu_export_finest(swamp_gpu* g, double* h, double* qx, double* qy) {
 int swamp_gpu_last_error(const swamp_gpu* g, int32_t* code, uint32_t* z, int32_t* quantity, int32_t* stage, char* msg,
                          size_t msg_cap) {
     if (!g) return SWAMP_E_ARG;
+    if (!g->parts.empty()) {
+        for (const swamp_gpu* q : g->parts)
+            if (q->ctl_host && q->ctl_host->err_code) return swamp_gpu_last_error(q, code, z, quantity, stage, msg, msg_cap);
+        if (msg && msg_cap) {
+            std::strncpy(msg, g->err.c_str(), msg_cap - 1);
+            msg[msg_cap - 1] = 0;
+        }
+        if (code) *code = 0;
+        return SWAMP_OK;
+    }
     if (code) *code = g->ctl_host ? g->ctl_host->err_code : 0;
     if (z) *z = g->ctl_host ? g->ctl_host->err_z : 0;
     if (quantity) *quantity = g->ctl_host ? g->ctl_host->err_q : 0;
@@ -594,6 +878,7 @@ int swamp_gpu_last_error(const swamp_gpu* g, int32_t* code, uint32_t* z, int32_t
 
 int swamp_gpu_timeline(swamp_gpu* g, double* out12) {
     if (!g || !out12) return SWAMP_E_ARG;
+    if (!g->parts.empty()) g = g->parts[0];
     int st = fetch_ctl(g);
     // the last completed step ran with step counter (step - 1)
     const unsigned long long* tl = g->ctl_host->tl[(g->ctl_host->step - 1) & 1];
@@ -607,6 +892,19 @@ int swamp_gpu_timeline(swamp_gpu* g, double* out12) {
 
 int swamp_gpu_counters(swamp_gpu* g, int64_t* out4) {
     if (!g || !out4) return SWAMP_E_ARG;
+    if (!g->parts.empty()) {
+        int64_t acc[4] = {0, 0, 0, 0};
+        for (swamp_gpu* q : g->parts) {
+            int64_t c[4];
+            const int st = swamp_gpu_counters(q, c);
+            if (st) return st;
+            for (int k = 1; k < 3; ++k) acc[k] += c[k];
+            acc[0] = c[0];
+            acc[3] = c[3];
+        }
+        std::memcpy(out4, acc, sizeof(acc));
+        return SWAMP_OK;
+    }
     int st = fetch_ctl(g);
     out4[0] = g->uniform ? (int64_t(1) << (2 * g->P.L)) : g->ctl_host->n_leaves_used;
     out4[1] = static_cast<int64_t>(g->ctl_host->cnt_tree);

@@ -38,6 +38,8 @@ def lib():
         rp = C.POINTER(swamp_step_report)
         L.swamp_gpu_create.argtypes = [C.POINTER(swamp_config), dp, dp, dp, dp, C.c_int, C.POINTER(P)]
         L.swamp_gpu_create_uniform.argtypes = L.swamp_gpu_create.argtypes
+        L.swamp_gpu_create_partitioned.argtypes = [C.POINTER(swamp_config), dp, dp, dp, dp, C.c_int,
+                                                   C.POINTER(C.c_int), C.POINTER(P)]
         L.swamp_gpu_destroy.argtypes = [P]
         L.swamp_gpu_step.argtypes = [P, rp]
         L.swamp_gpu_advance.argtypes = [P, C.c_int64, rp]
@@ -64,7 +66,7 @@ EXPORTED_SYMBOLS = (
     "swamp_gpu_create_uniform", "swamp_gpu_step_uniform", "swamp_gpu_set_profiling", "swamp_gpu_info",
     "swamp_gpu_copy_leaves", "swamp_gpu_export_tree", "swamp_gpu_export_finest", "swamp_gpu_last_error",
     "swamp_gpu_counters", "swamp_gpu_build_info", "swamp_gpu_enqueue", "swamp_gpu_stream",
-    "swamp_gpu_timeline",
+    "swamp_gpu_timeline", "swamp_gpu_create_partitioned",
 )
 
 
@@ -75,7 +77,7 @@ class SwampError(RuntimeError):
 class Engine:
     """SimState owner on one GPU."""
 
-    def __init__(self, cfg: SimConfig, h, qx, qy, z, device: int = 0, uniform: bool = False):
+    def __init__(self, cfg: SimConfig, h, qx, qy, z, device: int = 0, uniform: bool = False, parts=None):
         self.cfg = cfg
         self.L = int(cfg.L)
         self.uniform = uniform
@@ -85,8 +87,13 @@ class Engine:
         if any(a.size != n for a in arrs):
             raise ValueError(f"fields must be 2^L x 2^L = {cfg.side} x {cfg.side}")
         self._h = C.c_void_p()
-        f = lib().swamp_gpu_create_uniform if uniform else lib().swamp_gpu_create
-        st = f(C.byref(self._c), *[dptr(a) for a in arrs], int(device), C.byref(self._h))
+        if parts is not None:  # Morton-subtree partitions: list of CUDA devices, one per partition
+            devs = (C.c_int * len(parts))(*[int(d) for d in parts])
+            st = lib().swamp_gpu_create_partitioned(C.byref(self._c), *[dptr(a) for a in arrs], len(parts), devs,
+                                                     C.byref(self._h))
+        else:
+            f = lib().swamp_gpu_create_uniform if uniform else lib().swamp_gpu_create
+            st = f(C.byref(self._c), *[dptr(a) for a in arrs], int(device), C.byref(self._h))
         if st != 0:
             raise SwampError(f"initialise failed: {STATUS.get(st, st)}")
         self.report = swamp_step_report()
@@ -185,6 +192,12 @@ class Engine:
 def initialise(cfg: SimConfig, h, qx, qy, z, device: int = 0) -> Engine:
     """engine.initialise (SPEC.md:390-398) on `device`."""
     return Engine(cfg, h, qx, qy, z, device=device)
+
+
+def initialise_partitioned(cfg: SimConfig, h, qx, qy, z, devices) -> Engine:
+    """Morton-subtree partitioned engine: partition k on CUDA device devices[k]
+    (repeat a device to run virtual partitions on one GPU)."""
+    return Engine(cfg, h, qx, qy, z, parts=list(devices))
 
 
 def initialise_uniform(cfg: SimConfig, h, qx, qy, z, device: int = 0) -> Engine:

@@ -125,3 +125,28 @@ def test_profiling_report_has_stage_times():
     r = g.step_adaptive()
     assert r["ms_fv1"] > 0 and r["ms_encode_flag"] > 0 and r["ms_total"] >= r["ms_fv1"]
     assert r["n_leaves"] > 0 and r["step"] == 1
+
+
+@pytest.mark.parametrize("parts,name,kw", [
+    (2, "river_flood", dict(L=8)),
+    (4, "circular_dambreak", dict(L=8)),
+    (8, "monai_runup", dict(L=8)),
+    (4, "pseudo2d_dambreak", dict(L=9)),
+    (2, "quiescent_humps", dict(L=7)),
+])
+def test_partitioned_equals_single(parts, name, kw):
+    """Morton-subtree partitions (virtual, on one GPU) == one partition, bitwise."""
+    cfg, h, qx, qy, z = cases.CASES[name](**kw)
+    one = gpu.initialise(cfg, h, qx, qy, z)
+    many = gpu.initialise_partitioned(cfg, h, qx, qy, z, [0] * parts)
+    compare_states(many, one, f"{name} x{parts} init")
+    for k in range(1, 31):
+        one.step_adaptive()
+        many.step_adaptive()
+        if k in (1, 2, 5, 30):
+            compare_states(many, one, f"{name} x{parts} step {k}")
+    many.advance(10)
+    one.advance(10)
+    compare_states(many, one, f"{name} x{parts} advance")
+    for a, b in zip(many.export_finest(), one.export_finest()):
+        np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))
