@@ -11,9 +11,11 @@ export). L2 is flushed (256 MiB write) before every timed step.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun (N > 1) every rank runs an independent replica of the L = 11
-case on its own GPU (weak scaling, replicas only this round; the Morton-
-subtree partition is DESIGN.md §8); value = all ranks' updates / max time.
+Under torchrun (N > 1) the same L = 11 problem is split into N Morton-subtree
+partitions, one per GPU (strong scaling): rank 0 drives the partitioned
+engine over all N devices (cross-partition reads go through peer pointers over
+NVLink), the other ranks only join the barriers; the step time is partition
+0's device time, which waits for every partition at each phase.
 
 `--impl reference` times the CPU-HWFV1 oracle (oracle/, the spec
 restatement — the reference ships no engine to build) on this host's cores,
@@ -182,6 +184,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-sims", action="store_true", help="skip the configs 1-4 runtime table")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--virtual-parts", type=int, default=1,
+                    help="N=1 only: run the partitioned engine with this many partitions on one GPU (testing)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -192,18 +196,38 @@ def main():
 
     ws, rank, local = dist_env()
     if ws > 1:
+        # one process per GPU is launched; the partitioned engine is driven by
+        # rank 0 over all N GPUs (peer access across NVLink / NVSwitch) and the
+        # other ranks only join the coordination barriers (gloo, CPU)
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = local
+        dist.init_process_group("gloo")
+        if rank != 0:
+            dist.barrier()
+            dist.destroy_process_group()
+            return 0
+    dev = 0 if ws > 1 else local
     torch.cuda.set_device(dev)
     from paper_2206_05761_b200 import gpu
 
     cfg, h, qx, qy, z = cases.river_flood(L=args.L, epsilon=args.eps)
-    eng = gpu.initialise(cfg, h, qx, qy, z, device=dev)
+    parallelism = "single"
+    if ws > 1:
+        try:
+            eng = gpu.initialise_partitioned(cfg, h, qx, qy, z, list(range(ws)))
+            parallelism = f"morton-subtree x{ws} (one engine over {ws} GPUs, peer reads)"
+        except Exception as e:  # pragma: no cover - depends on the box
+            print(f"partitioned engine unavailable ({e}); running replicas", file=sys.stderr)
+            eng = gpu.initialise(cfg, h, qx, qy, z, device=dev)
+            parallelism = "replica (partitioned engine unavailable)"
+    elif args.virtual_parts > 1:
+        eng = gpu.initialise_partitioned(cfg, h, qx, qy, z, [dev] * args.virtual_parts)
+        parallelism = f"morton-subtree x{args.virtual_parts} virtual partitions on one GPU"
+    else:
+        eng = gpu.initialise(cfg, h, qx, qy, z, device=dev)
     stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=torch.device("cuda", dev))
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+    n_flush = ws if ws > 1 else 1
+    flush = [torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{d if ws > 1 else dev}") for d in range(n_flush)]
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
 
@@ -216,19 +240,19 @@ def main():
     updates = 0
     dev_ms = 0.0
     leaves = []
-    if ws > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize(dev)
+    for d in range(n_flush):
+        torch.cuda.synchronize(d if ws > 1 else dev)
     with ClockSampler(dev) as clk:
         wall0 = time.perf_counter()
         for _ in range(args.steps):
-            flush.fill_(1)  # L2 flush (256 MiB > 126 MB L2) before each timed step ...
-            stream.wait_stream(torch.cuda.current_stream(dev))
+            for d in range(n_flush):  # L2 flush (256 MiB > 126 MB L2) of every GPU ...
+                flush[d].fill_(1)
+                torch.cuda.synchronize(d if ws > 1 else dev)
             ev0.record(stream)  # ... outside the timed interval
-            eng.enqueue(1)      # one adaptive step: CUDA-graph replay of the 4 kernels
+            eng.enqueue(1)      # one adaptive step (graph replay; partitioned: every phase on every GPU)
             ev1.record(stream)
             ev1.synchronize()
-            dev_ms += ev0.elapsed_time(ev1)
+            dev_ms += ev0.elapsed_time(ev1)  # partition 0's stream waits for every partition at each phase
             r = eng.advance(0)  # StepReport of that step (leaf count, device stage timeline)
             updates += r["n_leaves"]
             leaves.append(r["n_leaves"])
@@ -237,14 +261,7 @@ def main():
         torch.cuda.synchronize(dev)
         wall = time.perf_counter() - wall0
     c1 = eng.counters()
-    if ws > 1:
-        t = torch.tensor([dev_ms, float(updates)], dtype=torch.float64, device=f"cuda:{dev}")
-        tmax = t.clone()
-        torch.distributed.all_reduce(tmax[:1], op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(t[1:], op=torch.distributed.ReduceOp.SUM)
-        dev_ms_max, updates_all = float(tmax[0]), float(t[1])
-    else:
-        dev_ms_max, updates_all = dev_ms, float(updates)
+    dev_ms_max, updates_all = dev_ms, float(updates)
 
     K = args.steps
     n_mean = updates / K
@@ -279,11 +296,12 @@ def main():
 
     # ---- e2e through the public API with host buffers
     e2e = None
-    if rank == 0 or ws > 1:
+    if rank == 0:
         del eng
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        e = gpu.initialise(cfg, h, qx, qy, z, device=dev)
+        e = (gpu.initialise_partitioned(cfg, h, qx, qy, z, list(range(ws))) if ws > 1 and "morton" in parallelism
+             else gpu.initialise(cfg, h, qx, qy, z, device=dev))
         up = 0
         for _ in range(K):
             r = e.step_adaptive()  # each step reads its StepReport back
@@ -309,17 +327,14 @@ def main():
     if rank == 0 and ws == 1 and not args.no_sims:
         sims = sim_runtimes(gpu, dev)
 
-    if ws > 1:
-        torch.distributed.barrier()
-    if rank != 0:
-        return 0
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
-        "ms_per_step": dev_ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": dev_ms_max / K, "higher_is_better": True,
+        "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"river_flood_L{args.L}_eps{args.eps:g}", "L": args.L, "epsilon": args.eps,
                    "finest_cells": 4 ** args.L, "leaves_mean": n_mean, "leaves_min": min(leaves),
-                   "leaves_max": max(leaves), "parallelism": "replicas" if ws > 1 else "single",
+                   "leaves_max": max(leaves), "parallelism": parallelism,
                    "l2": "flushed (256 MiB write) before every timed step"},
         "mra_ms_per_step": kern["ms_encode_flag"] + kern["ms_band_closure"] + kern["ms_decode_traverse"],
         "stage_ms_per_step": kern,
@@ -338,6 +353,7 @@ def main():
     }
     print(json.dumps(line), flush=True)
     if ws > 1:
+        torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     return 0
 

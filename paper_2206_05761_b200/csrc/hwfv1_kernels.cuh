@@ -1202,6 +1202,14 @@ __global__ void k_finalize(Params P, Ctl* ctl, int advance) {
 // significant: walk up until the parent is significant (SPEC.md:248 — the
 // coarser covering leaf); the fast path (parent significant -> the same-level
 // cell itself) is tested by the caller for all four faces at once
+__device__ __forceinline__ const double4* covering_local(const Params& P, const double4* cur, const uint8_t* sigc, int k,
+                                                        uint32_t mm) {
+    while (k > 0 && !sigc[P.fbase[k - 1] + (mm >> 2)]) {
+        mm >>= 2;
+        --k;
+    }
+    return cur + P.base[k] + mm;
+}
 __device__ __forceinline__ double4* covering(const Params& P, int cur, int k, uint32_t mm) {
     while (k > 0 && !sig_at(P, cur ^ 1, k - 1, mm >> 2)) {
         mm >>= 2;
@@ -1212,7 +1220,7 @@ __device__ __forceinline__ double4* covering(const Params& P, int cur, int k, ui
 
 // FV1 over the leaf list: persistent grid-stride, one thread per
 // leaf; reads the current buffer, writes leaf slots of the other (D15).
-template <bool UNIFORM, int MINB = 2>
+template <bool UNIFORM, int MINB = 2, bool PART = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     pdl_wait();
     pdl_trigger();
@@ -1265,11 +1273,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                 for (int d = 0; d < 4; ++d) src[d] = cur + P.base[n] + nm[d];
             } else {
                 uint8_t f[4];
+                if (PART) {  // cross-partition reads through the peer tables
 #pragma unroll
-                for (int d = 0; d < 4; ++d) f[d] = (nm[d] != zo::kNone) ? sig_at(P, p ^ 1, n - 1, nm[d] >> 2) : 1;
+                    for (int d = 0; d < 4; ++d) f[d] = (nm[d] != zo::kNone) ? sig_at(P, p ^ 1, n - 1, nm[d] >> 2) : 1;
 #pragma unroll
-                for (int d = 0; d < 4; ++d)
-                    src[d] = f[d] ? cell_ptr(P, p, n, nm[d]) : covering(P, p, n - 1, nm[d] >> 2);
+                    for (int d = 0; d < 4; ++d)
+                        src[d] = f[d] ? cell_ptr(P, p, n, nm[d]) : covering(P, p, n - 1, nm[d] >> 2);
+                } else {
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) f[d] = (nm[d] != zo::kNone) ? sigc[P.fbase[n - 1] + (nm[d] >> 2)] : 1;
+#pragma unroll
+                    for (int d = 0; d < 4; ++d)
+                        src[d] = f[d] ? cur + P.base[n] + nm[d] : covering_local(P, cur, sigc, n - 1, nm[d] >> 2);
+                }
             }
             double4 r4[4];
 #pragma unroll

@@ -498,9 +498,7 @@ void group_enqueue_step(swamp_gpu* grp) {
         hwfv1::k_traverse<false><<<q->P.tiles_per_part, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 0);
     });
     group_phase(grp, [](swamp_gpu* q) {
-        if (q->fv1_minb == 4) hwfv1::k_fv1<false, 4><<<q->fv1_grid, kThreads, 0, q->stream>>>(q->P, q->ctl);
-        else if (q->fv1_minb == 3) hwfv1::k_fv1<false, 3><<<q->fv1_grid, kThreads, 0, q->stream>>>(q->P, q->ctl);
-        else hwfv1::k_fv1<false, 2><<<q->fv1_grid, kThreads, 0, q->stream>>>(q->P, q->ctl);
+        hwfv1::k_fv1<false, 2, true><<<q->fv1_grid, kThreads, 0, q->stream>>>(q->P, q->ctl);
     });
     group_phase(grp, [](swamp_gpu* q) { hwfv1::k_finalize<<<1, 32, 0, q->stream>>>(q->P, q->ctl, 1); });
 }
