@@ -60,6 +60,7 @@ struct Ctl {
     int err_q;
     int err_stage;
     unsigned int done_k1, done_k2, done_k5;
+    unsigned long long k2_ready;    // step + 1 once K2's last CTA published the traversal offsets
     // stage timeline (globaltimer ns), double-buffered by step parity: for
     // kernel k (K1, K2, K3, K5) [3k] = ~(first CTA start), [3k+1] = last CTA
     // elected, [3k+2] = last CTA done (atomicMax; K5 zeroes the next buffer)
@@ -121,6 +122,7 @@ struct Params {
     // psig / ppre / ptile_cnt / pctl are every partition's arrays (peer
     // pointers across GPUs; index 0 = self when G = 1).
     int G, part;
+    int fuse_k3;          // K3 runs inside K2 (every K2 CTA is resident; host-checked)
     uint32_t tile_lo, tile_hi, tiles_per_part;
     double4* pcells[kMaxParts][2];
     uint8_t* psig[kMaxParts][2];
@@ -152,6 +154,14 @@ __device__ __forceinline__ uint8_t ldcg_u8(const uint8_t* p) {
     unsigned short v;
     asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(v) : "l"(p));
     return static_cast<uint8_t>(v);
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t ldcg_u32(const uint32_t* p) {
     uint32_t v;
@@ -691,6 +701,8 @@ __device__ __forceinline__ uint8_t band_flag(int mode, int L, int n, uint32_t m,
 // leaf-list offsets (the PTT compaction's global scan, done once on 4^R
 // values instead of per finest cell).
 __device__ void band_top(const Params& P, Ctl* ctl, uint8_t* sfl_top, unsigned* s_red);
+template <bool EXPORT>
+__device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint32_t* smem3, unsigned* s_red);
 
 __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force) {
     pdl_wait();
@@ -726,15 +738,46 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
         }
     }
     __syncthreads();
-    // ---- band (D3): neighbours inside the subtree from shared memory
+    // ---- band (D3). The subtree is aligned, so a neighbour inside it is the
+    //      neighbour of the subtree-local Morton code on the local grid (level
+    //      n - R); only edge cells look outside (global / other partitions).
     for (int n = R; n < L; ++n) {
         const uint32_t cnt = 1u << (2 * (n - R));
-        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads)
-            sf[lo(n, R) + pi] = band_flag(P.band_mode, L, n, j * cnt + pi, [&](int k, uint32_t mm) -> uint8_t {
-                const uint32_t kc = 1u << (2 * (k - R));
-                const uint32_t t = mm >> (2 * (k - R));
-                return (t == j) ? spre[lo(k, R) + (mm - j * kc)] : P.ppre[owner_of(P, k, mm)][P.fbase[k] + mm];
-            });
+        const uint32_t loN = lo(n, R), jb = j * cnt;
+        auto pre_out = [&](int k, uint32_t mm) -> uint8_t {  // (k, mm) outside the subtree
+            return P.ppre[owner_of(P, k, mm)][P.fbase[k] + mm];
+        };
+        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
+            uint8_t b = spre[loN + pi];
+            if (P.band_mode == 2) {
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const uint32_t ln = zo::neighbour_dev(n - R, pi, static_cast<zo::Direction>(d));
+                    if (ln != zo::kNone) {
+                        b |= spre[loN + ln];
+                    } else {
+                        const uint32_t nb = zo::neighbour_dev(n, jb + pi, static_cast<zo::Direction>(d));
+                        if (nb != zo::kNone) b |= pre_out(n, nb);
+                    }
+                }
+            } else if (P.band_mode == 1 && n + 1 < L) {
+                const uint32_t loC = lo(n + 1, R), jc = jb << 2;
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t lc = 4u * pi + static_cast<uint32_t>(k);
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) {
+                        const uint32_t ln = zo::neighbour_dev(n + 1 - R, lc, static_cast<zo::Direction>(d));
+                        if (ln != zo::kNone) {
+                            b |= spre[loC + ln];
+                        } else {
+                            const uint32_t nb = zo::neighbour_dev(n + 1, jc + lc, static_cast<zo::Direction>(d));
+                            if (nb != zo::kNone) b |= pre_out(n + 1, nb);
+                        }
+                    }
+                }
+            }
+            sf[loN + pi] = b ? 1 : 0;
+        }
     }
     __syncthreads();
     // ---- ancestor closure bottom-up, with the leaf counts of every subtree
@@ -778,10 +821,36 @@ __global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force
         P.tile_cnt[P.n_tiles + j] = cB[0];
     }
     if (P.G > 1) return;  // partitioned: k_band_top runs after all partitions' subtrees
-    if (!last_block(&ctl->done_k2, &s_last)) return;
-    tl_mark(ctl, 4);
-    band_top(P, ctl, smem2, s_red);
-    tl_mark(ctl, 5);
+    const bool fuse = P.fuse_k3 && !force;
+    const unsigned long long target = static_cast<unsigned long long>(ctl->step) + 1ull;
+    const bool last = last_block(&ctl->done_k2, &s_last);
+    if (last) {
+        tl_mark(ctl, 4);
+        band_top(P, ctl, smem2, s_red);
+        tl_mark(ctl, 5);
+    }
+    if (!fuse) return;
+    // ---- K3 fused: every CTA is resident (host-checked), so the others wait
+    //      for the last CTA's offsets instead of a new launch
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (last) {
+            __threadfence();
+            st_release_u64(&ctl->k2_ready, target);
+        } else {
+            const unsigned long long t0 = gtimer();
+            while (ld_acquire_u64(&ctl->k2_ready) != target) {
+                __nanosleep(200);
+                if (gtimer() - t0 > 2000000000ull) {  // 2 s: never expected; fail instead of hanging
+                    report_error(ctl, kErrDt, j, 0, kStageTraverse);
+                    break;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    tl_start(ctl, 2);
+    traverse_tile<false>(P, ctl, j, reinterpret_cast<uint32_t*>(smem2), s_red);
 }
 
 __global__ void __launch_bounds__(kThreads) k_band_top(Params P, Ctl* ctl, int force) {
@@ -928,29 +997,23 @@ __device__ void band_top(const Params& P, Ctl* ctl, uint8_t* sfl_top, unsigned* 
 }
 
 
-// EXPORT = re-run the traversal of the current tree (after a step) into the
-// Morton-ordered export list, with no side effects (no decode, no timeline).
+// decode + PTT + compaction of subtree j (K3). EXPORT = re-run the traversal
+// of the current tree (after a step) into the Morton-ordered export list, with
+// no side effects (no decode, no timeline).
 template <bool EXPORT>
-__global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int force) {
-    pdl_wait();
-    pdl_trigger();
-    if (!EXPORT && !force && !active(ctl, P)) return;
-    if (!EXPORT) tl_start(ctl, 2);
-    extern __shared__ uint32_t smem3[];
-    __shared__ unsigned s_red[32];
+__device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint32_t* smem3, unsigned* s_red) {
     const int p = ctl->parity;
     double4* buf = P.cells[p];
     const uint8_t* sigc = EXPORT ? P.sig[p] : P.sig[p ^ 1];
     const uint8_t* sigp = EXPORT ? P.sig[p ^ 1] : P.sig[p];
     const int L = P.L, R = P.R, K = P.K;
-    const uint32_t j = P.tile_lo + blockIdx.x;
     const uint32_t ncell = ((1u << (2 * K)) - 1u) / 3u;  // subtree cells on levels R..L-1
     uint32_t* src = smem3;                               // [ncell]
     uint8_t* sc = reinterpret_cast<uint8_t*>(src + ncell);  // [ncell]
     uint8_t* sp = sc + ncell;                               // [ncell]
 
-    const uint32_t leafn = P.tile_lvl[j];
-    const uint32_t rootsrc = P.tile_src[j];
+    const uint32_t leafn = ldcg_u32(P.tile_lvl + j);  // written by K2's last CTA
+    const uint32_t rootsrc = ldcg_u32(P.tile_src + j);
     const bool reached = leafn == static_cast<uint32_t>(R);
     int any_new = 0;
     for (int n = R; n < L; ++n) {  // current / previous flags of the subtree, word loads
@@ -1014,8 +1077,8 @@ __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int f
     //      one Morton-ordered list at tile_off[2 nt + j].
     const uint32_t nt = static_cast<uint32_t>(P.n_tiles);
     uint32_t* outA = EXPORT ? P.leaves_x : P.leaves;
-    uint32_t oa = EXPORT ? P.tile_off[2 * nt + j] : P.tile_off[j];
-    uint32_t ob = EXPORT ? 0u : P.tile_off[nt + j];
+    uint32_t oa = ldcg_u32(P.tile_off + (EXPORT ? 2 * nt + j : j));
+    uint32_t ob = EXPORT ? 0u : ldcg_u32(P.tile_off + nt + j);
     if (!reached) {
         const int n = static_cast<int>(leafn);
         if (threadIdx.x == 0 && ((j & ((1u << (2 * (R - n))) - 1u)) == 0u))
@@ -1092,6 +1155,17 @@ __global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int f
         __syncthreads();
         tl_mark(ctl, 8);
     }
+}
+
+template <bool EXPORT>
+__global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int force) {
+    pdl_wait();
+    pdl_trigger();
+    if (!EXPORT && !force && !active(ctl, P)) return;
+    if (!EXPORT) tl_start(ctl, 2);
+    extern __shared__ uint32_t smem3[];
+    __shared__ unsigned s_red[32];
+    traverse_tile<EXPORT>(P, ctl, P.tile_lo + blockIdx.x, smem3, s_red);
 }
 
 // =========================================================================== K5

@@ -147,7 +147,7 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     mark(1);
     launch_pdl(hwfv1::k_band, P.n_tiles, g->smem_k2, s, P, g->ctl, 0);
     mark(2);
-    launch_pdl(hwfv1::k_traverse<false>, P.n_tiles, g->smem_k3, s, P, g->ctl, 0);
+    if (!P.fuse_k3) launch_pdl(hwfv1::k_traverse<false>, P.n_tiles, g->smem_k3, s, P, g->ctl, 0);
     mark(3);
     if (g->fv1_minb == 4)
         launch_pdl(hwfv1::k_fv1<false, 4>, g->fv1_grid, 0, s, P, g->ctl);
@@ -382,6 +382,14 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         g->fv1_grid = std::max(1, occ) * g->num_sms;
     }
     g->n_cells = static_cast<int64_t>(off);
+    // K3 fused into K2 when every K2 CTA can be resident at once (its CTAs
+    // wait for the last CTA); SWAMP_FUSE_K3=0 disables
+    {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_band, kThreads, g->smem_k2);
+        const char* e = std::getenv("SWAMP_FUSE_K3");
+        P.fuse_k3 = (G == 1 && P.n_tiles <= occ * g->num_sms && !(e && e[0] == '0')) ? 1 : 0;
+    }
     return SWAMP_OK;
 }
 
