@@ -382,13 +382,14 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         g->fv1_grid = std::max(1, occ) * g->num_sms;
     }
     g->n_cells = static_cast<int64_t>(off);
-    // K3 fused into K2 when every K2 CTA can be resident at once (its CTAs
-    // wait for the last CTA); SWAMP_FUSE_K3=0 disables
+    // K3 fused into K2 (its CTAs wait for the last CTA instead of a new
+    // launch) is possible when every K2 CTA can be resident at once;
+    // SWAMP_FUSE_K3=1 enables it
     {
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_band, kThreads, g->smem_k2);
-        const char* e = std::getenv("SWAMP_FUSE_K3");
-        P.fuse_k3 = (G == 1 && P.n_tiles <= occ * g->num_sms && !(e && e[0] == '0')) ? 1 : 0;
+        const char* e = std::getenv("SWAMP_FUSE_K3");  // opt-in: measured slower on B200 (L=11)
+        P.fuse_k3 = (G == 1 && P.n_tiles <= occ * g->num_sms && e && e[0] == '1') ? 1 : 0;
     }
     return SWAMP_OK;
 }
