@@ -302,6 +302,38 @@ __device__ __forceinline__ bool last_block(unsigned int* counter, int* s_flag) {
     return last;
 }
 
+
+// ------------------------------------------------------- TMA bulk copies (1D)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* mbar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* mbar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+}
+// global -> shared bulk copy through the TMA unit (cp.async.bulk, SASS UBLKCP)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mbar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(mbar)),
+        "r"(parity)
+        : "memory");
+}
+
 // ---------------------------------------------------------------- K1 warp part
 __device__ __forceinline__ double4 shfl4(double4 v, int src) {
     return make_double4(__shfl_sync(kFull, v.x, src), __shfl_sync(kFull, v.y, src), __shfl_sync(kFull, v.z, src),
@@ -654,6 +686,100 @@ __device__ void encode_top(const Params& P, Ctl* ctl, double4* sv, unsigned* s_r
         if (tt) atomicAdd(&ctl->cnt_tree, (unsigned long long)tt);
         ctl->done_k1 = 0;
     }
+}
+
+
+
+// K1 after t = 0 (level L-1 was re-encoded by the previous FV1): the
+// subtree's level slices R..L-1 (contiguous, 32 B per cell) are brought into
+// shared memory by TMA bulk copies (one per level, one mbarrier), the flags
+// by word loads in parallel; levels L-2..R are then re-encoded from shared
+// memory. One global round trip per CTA instead of one per level.
+__global__ void __launch_bounds__(kThreads) k_encode_tma(Params P, Ctl* ctl) {
+    pdl_wait();
+    pdl_trigger();
+    if (!active(ctl, P)) return;
+    tl_start(ctl, 0);
+    extern __shared__ __align__(128) double4 sv[];
+    __shared__ unsigned s_red[32];
+    __shared__ int s_last;
+    __shared__ __align__(8) unsigned long long mbar;
+    const int p = ctl->parity;
+    double4* buf = P.cells[p];
+    const uint8_t* sigp = P.sig[p];
+    const int L = P.L, R = P.R, K = P.K;
+    const uint32_t j = P.tile_lo + blockIdx.x;
+    const uint32_t ncell = ((1u << (2 * K)) - 1u) / 3u;
+    uint8_t* sfl = reinterpret_cast<uint8_t*>(sv + ncell);  // previous-tree flags
+    uint8_t* sdm = sfl + ncell;                             // DEM flags
+    if (threadIdx.x == 0) mbar_init(&mbar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(&mbar, ncell * static_cast<unsigned>(sizeof(double4)));
+        for (int n = R; n < L; ++n) {
+            const uint32_t cnt = 1u << (2 * (n - R));
+            bulk_g2s(sv + lo(n, R), buf + P.base[n] + static_cast<unsigned long long>(j) * cnt,
+                     cnt * static_cast<unsigned>(sizeof(double4)), &mbar);
+        }
+    }
+    for (int n = R; n < L; ++n) {  // flags while the bulk copies fly
+        const uint32_t cnt = 1u << (2 * (n - R));
+        const unsigned long long g = P.fbase[n] + static_cast<unsigned long long>(j) * cnt;
+        if (cnt >= 4) {
+            for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads) {
+                const uint32_t wf = *reinterpret_cast<const uint32_t*>(sigp + g + q);
+                const uint32_t wd = *reinterpret_cast<const uint32_t*>(P.dem + g + q);
+                uint8_t* df = sfl + lo(n, R) + q;
+                uint8_t* dd = sdm + lo(n, R) + q;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    df[k] = (wf >> (8 * k)) & 0xFFu;
+                    dd[k] = (wd >> (8 * k)) & 0xFFu;
+                }
+                if (n == L - 1) {  // level L-1: the previous FV1 flagged the tree cells
+                    const bool zero = 0.0 >= P.tau[n];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (!byte_of(wf, k)) P.pre[g + q + k] = (zero || byte_of(wd, k)) ? 1 : 0;
+                }
+            }
+        } else if (threadIdx.x < cnt) {
+            const uint8_t f = sigp[g + threadIdx.x], d = P.dem[g + threadIdx.x];
+            sfl[lo(n, R) + threadIdx.x] = f;
+            sdm[lo(n, R) + threadIdx.x] = d;
+            if (n == L - 1 && !f) P.pre[g + threadIdx.x] = ((0.0 >= P.tau[n]) || d) ? 1 : 0;
+        }
+    }
+    __syncthreads();
+    mbar_wait(&mbar, 0);
+    unsigned tree = 0;
+    for (int n = L - 2; n >= R; --n) {
+        const uint32_t cnt = 1u << (2 * (n - R));
+        const uint32_t pb = j * cnt;
+        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
+            const uint32_t pm = pb + pi;
+            const uint32_t li = lo(n, R) + pi;
+            bool flow = 0.0 >= P.tau[n];
+            if (sfl[li]) {
+                const uint32_t c0 = lo(n + 1, R) + 4u * pi;
+                const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
+                const Enc e = encode_children<false>(c, P, n);
+                flow = e.flow;
+                st4(buf + P.base[n] + pm, e.par);
+                sv[li] = e.par;
+                ++tree;
+            }
+            P.pre[P.fbase[n] + pm] = (flow || sdm[li]) ? 1 : 0;
+        }
+        __syncthreads();
+    }
+    const unsigned tsum = block_sum(tree, s_red);
+    if (threadIdx.x == 0 && tsum) atomicAdd(&ctl->cnt_tree, (unsigned long long)tsum);
+    if (P.G > 1) return;
+    if (!last_block(&ctl->done_k1, &s_last)) return;
+    tl_mark(ctl, 1);
+    encode_top<false>(P, ctl, sv, s_red);
+    tl_mark(ctl, 2);
 }
 
 

@@ -143,7 +143,7 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
         for (int k = 1; k < 5; ++k) mark(k);
         return;
     }
-    launch_pdl(hwfv1::k_encode<false>, P.n_tiles, g->smem_k1, s, P, g->ctl);
+    launch_pdl(hwfv1::k_encode_tma, P.n_tiles, g->smem_k1 + g->smem_k1 / 33, s, P, g->ctl);
     mark(1);
     launch_pdl(hwfv1::k_band, P.n_tiles, g->smem_k2, s, P, g->ctl, 0);
     mark(2);
@@ -492,7 +492,7 @@ int group_sync(swamp_gpu* grp) {
 
 void group_enqueue_step(swamp_gpu* grp) {
     group_phase(grp, [](swamp_gpu* q) {
-        hwfv1::k_encode<false><<<q->P.tiles_per_part, kThreads, q->smem_k1, q->stream>>>(q->P, q->ctl);
+        hwfv1::k_encode_tma<<<q->P.tiles_per_part, kThreads, q->smem_k1 + q->smem_k1 / 33, q->stream>>>(q->P, q->ctl);
     });
     group_phase(grp, [](swamp_gpu* q) {
         hwfv1::k_encode_top<false><<<1, kThreads, q->smem_k1, q->stream>>>(q->P, q->ctl);
