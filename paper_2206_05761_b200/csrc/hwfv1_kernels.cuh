@@ -61,6 +61,7 @@ struct Ctl {
     int err_stage;
     unsigned int done_k1, done_k2, done_k5;
     unsigned long long k2_ready;    // step + 1 once K2's last CTA published the traversal offsets
+    unsigned long long dbg[16];     // per-phase globaltimer stamps of probe CTAs (diagnostics)
     // stage timeline (globaltimer ns), double-buffered by step parity: for
     // kernel k (K1, K2, K3, K5) [3k] = ~(first CTA start), [3k+1] = last CTA
     // elected, [3k+2] = last CTA done (atomicMax; K5 zeroes the next buffer)
@@ -698,8 +699,15 @@ __device__ void encode_top(const Params& P, Ctl* ctl, double4* sv, unsigned* s_r
 __global__ void __launch_bounds__(kThreads) k_encode_tma(Params P, Ctl* ctl) {
     pdl_wait();
     pdl_trigger();
+    const unsigned long long t_entry = gtimer();
     if (!active(ctl, P)) return;
     tl_start(ctl, 0);
+    const int probe = (blockIdx.x == 0) ? 0 : ((blockIdx.x == gridDim.x / 2) ? 8 : -1);
+    auto stamp = [&](int k) {
+        if (probe >= 0 && threadIdx.x == 0) ctl->dbg[probe + k] = gtimer();
+    };
+    stamp(0);
+    if (probe >= 0 && threadIdx.x == 0) ctl->dbg[probe + 7] = t_entry;
     extern __shared__ __align__(128) double4 sv[];
     __shared__ unsigned s_red[32];
     __shared__ int s_last;
@@ -751,7 +759,9 @@ __global__ void __launch_bounds__(kThreads) k_encode_tma(Params P, Ctl* ctl) {
         }
     }
     __syncthreads();
+    stamp(1);
     mbar_wait(&mbar, 0);
+    stamp(2);
     unsigned tree = 0;
     for (int n = L - 2; n >= R; --n) {
         const uint32_t cnt = 1u << (2 * (n - R));
@@ -773,10 +783,14 @@ __global__ void __launch_bounds__(kThreads) k_encode_tma(Params P, Ctl* ctl) {
         }
         __syncthreads();
     }
+    stamp(3);
     const unsigned tsum = block_sum(tree, s_red);
     if (threadIdx.x == 0 && tsum) atomicAdd(&ctl->cnt_tree, (unsigned long long)tsum);
+    stamp(4);
     if (P.G > 1) return;
-    if (!last_block(&ctl->done_k1, &s_last)) return;
+    const bool lastb = last_block(&ctl->done_k1, &s_last);
+    stamp(5);
+    if (!lastb) return;
     tl_mark(ctl, 1);
     encode_top<false>(P, ctl, sv, s_red);
     tl_mark(ctl, 2);

@@ -897,6 +897,14 @@ int swamp_gpu_timeline(swamp_gpu* g, double* out12) {
     return st;
 }
 
+int swamp_gpu_debug(swamp_gpu* g, uint64_t* out16) {
+    if (!g || !out16) return SWAMP_E_ARG;
+    if (!g->parts.empty()) g = g->parts[0];
+    int st = fetch_ctl(g);
+    std::memcpy(out16, g->ctl_host->dbg, sizeof(g->ctl_host->dbg));
+    return st;
+}
+
 int swamp_gpu_counters(swamp_gpu* g, int64_t* out4) {
     if (!g || !out4) return SWAMP_E_ARG;
     if (!g->parts.empty()) {

@@ -1,0 +1,13 @@
+import os, sys, ctypes as C
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2206_05761_b200 import cases, gpu
+cfg, h, qx, qy, z = cases.river_flood(L=11)
+e = gpu.initialise(cfg, h, qx, qy, z)
+lib = gpu.lib(); lib.swamp_gpu_debug.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
+for k in range(5):
+    e.step_adaptive()
+    a = (C.c_uint64 * 16)(); lib.swamp_gpu_debug(e._h, a)
+    tl = e.timeline()
+    for base in (0, 8):
+        t0 = a[base + 7]
+        print(base, "entry->", [round((a[base + i] - t0) / 1e3, 2) if a[base + i] else None for i in range(6)], "K1 tl", tl[0:3])
