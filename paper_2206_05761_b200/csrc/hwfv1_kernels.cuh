@@ -59,8 +59,7 @@ struct Ctl {
     uint32_t err_z;
     int err_q;
     int err_stage;
-    unsigned int done_k1, done_k2, done_k5;
-    unsigned long long k2_ready;    // step + 1 once K2's last CTA published the traversal offsets
+    unsigned int done_k1, done_k5;
     unsigned long long dbg[16];     // per-phase globaltimer stamps of probe CTAs (diagnostics)
     // stage timeline (globaltimer ns), double-buffered by step parity: for
     // kernel k (K1, K2, K3, K5) [3k] = ~(first CTA start), [3k+1] = last CTA
@@ -114,8 +113,6 @@ struct Params {
     uint32_t* leaves_x;   // Morton-ordered leaf list for exports
     uint32_t* tile_cnt;
     uint32_t* tile_off;
-    uint32_t* tile_lvl;   // traversal depth of each level-R subtree root (R = reached)
-    uint32_t* tile_src;   // z of the root's decode source, or kNoSrc
     // Morton-subtree partitions: this partition owns level-R
     // subtrees [tile_lo, tile_hi); cells on levels >= R belong to their
     // subtree's partition, cells above R are replicated except that a leaf's
@@ -123,7 +120,7 @@ struct Params {
     // psig / ppre / ptile_cnt / pctl are every partition's arrays (peer
     // pointers across GPUs; index 0 = self when G = 1).
     int G, part;
-    int fuse_k3;          // K3 runs inside K2 (every K2 CTA is resident; host-checked)
+    int top_mode;         // levels < R after t = 0: 0 none (R = 0), 1 extra CTA of K2, 2 k_encode_top
     uint32_t tile_lo, tile_hi, tiles_per_part;
     double4* pcells[kMaxParts][2];
     uint8_t* psig[kMaxParts][2];
@@ -333,6 +330,47 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* mbar, unsigned par
         "}\n" ::"r"(smem_u32(mbar)),
         "r"(parity)
         : "memory");
+}
+
+// ------------------------------------------------ cp.async staging (LDGSTS)
+// Every MRA kernel stages what it reads into shared memory with asynchronous
+// copies issued up front, so a CTA pays ONE global round trip instead of one
+// per level loop iteration (the loads of a runtime-bounded level loop are
+// otherwise serialised behind the stores that consume them). cp.async takes
+// any global address, including NVLink peer pointers of other partitions.
+__device__ __forceinline__ void cp_async4(void* s, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// shared-memory offset of tile level k (k = n - R) in a per-tile flag slice,
+// every level 16-B aligned: 0, 16, 32, 48, 112, 368, 1392, ... ; slo(K) = size
+__host__ __device__ __forceinline__ uint32_t slo(int k) {
+    return k <= 3 ? 16u * static_cast<uint32_t>(k) : 48u + ((1u << (2 * k)) - 64u) / 3u;
+}
+
+// stage `bytes` (a multiple of 16, both ends 16-B aligned) into shared memory
+__device__ __forceinline__ void stage16(void* s, const void* g, uint32_t bytes) {
+    for (uint32_t q = 16u * threadIdx.x; q < bytes; q += 16u * kThreads)
+        cp_async16(static_cast<uint8_t*>(s) + q, static_cast<const uint8_t*>(g) + q);
+}
+
+// stage the flag bytes of tile j, levels R..L-1, into the slo layout. Level R
+// (one byte) cannot be copied asynchronously: it is returned (thread 0 only)
+// and must be stored by the caller after cp_async_wait_all.
+__device__ __forceinline__ uint8_t stage_tile_flags(uint8_t* s, const uint8_t* base, const Params& P, uint32_t j) {
+    const int K = P.K, R = P.R;
+    uint8_t v0 = 0;
+    if (threadIdx.x == 0) v0 = base[P.fbase[R] + j];
+    if (K > 1 && threadIdx.x == 32) cp_async4(s + slo(1), base + P.fbase[R + 1] + 4ull * j);
+    for (int k = 2; k < K; ++k) {
+        const uint32_t cnt = 1u << (2 * k);
+        stage16(s + slo(k), base + P.fbase[R + k] + static_cast<unsigned long long>(j) * cnt, cnt);
+    }
+    return v0;
 }
 
 // ---------------------------------------------------------------- K1 warp part
@@ -691,109 +729,204 @@ __device__ void encode_top(const Params& P, Ctl* ctl, double4* sv, unsigned* s_r
 
 
 
-// K1 after t = 0 (level L-1 was re-encoded by the previous FV1): the
-// subtree's level slices R..L-1 (contiguous, 32 B per cell) are brought into
-// shared memory by TMA bulk copies (one per level, one mbarrier), the flags
-// by word loads in parallel; levels L-2..R are then re-encoded from shared
-// memory. One global round trip per CTA instead of one per level.
-__global__ void __launch_bounds__(kThreads) k_encode_tma(Params P, Ctl* ctl) {
+// K1 after t = 0 (level L-1 was re-encoded and flagged by the previous
+// FV1): re-encode + threshold of levels L-2 .. R of subtree j. Everything the
+// CTA reads is issued at once: the previous-tree and DEM flags of levels
+// R..L-1 and the values of levels R+1..L-2 (inputs where a previous-tree
+// leaf's parent is re-encoded) are staged into shared memory by cp.async;
+// thread t loads the four level-(L-1) children of level-(L-2) cell t straight
+// into registers when that cell is on the previous tree. Levels L-3..R are
+// then encoded from shared memory. No last-CTA tail: levels < R are encoded
+// by an extra CTA of K2 (encode_top_staged).
+template <int KT>
+__global__ void __launch_bounds__(kThreads) k_encode_step(Params P, Ctl* ctl) {
     pdl_wait();
     pdl_trigger();
-    const unsigned long long t_entry = gtimer();
     if (!active(ctl, P)) return;
     tl_start(ctl, 0);
-    const int probe = (blockIdx.x == 0) ? 0 : ((blockIdx.x == gridDim.x / 2) ? 8 : -1);
-    auto stamp = [&](int k) {
-        if (probe >= 0 && threadIdx.x == 0) ctl->dbg[probe + k] = gtimer();
-    };
-    stamp(0);
-    if (probe >= 0 && threadIdx.x == 0) ctl->dbg[probe + 7] = t_entry;
-    extern __shared__ __align__(128) double4 sv[];
+    extern __shared__ __align__(16) uint8_t sm1[];
     __shared__ unsigned s_red[32];
-    __shared__ int s_last;
-    __shared__ __align__(8) unsigned long long mbar;
     const int p = ctl->parity;
     double4* buf = P.cells[p];
     const uint8_t* sigp = P.sig[p];
-    const int L = P.L, R = P.R, K = P.K;
+    const int L = P.L, R = P.R;
+    const int K = KT ? KT : P.K;
     const uint32_t j = P.tile_lo + blockIdx.x;
-    const uint32_t ncell = ((1u << (2 * K)) - 1u) / 3u;
-    uint8_t* sfl = reinterpret_cast<uint8_t*>(sv + ncell);  // previous-tree flags
-    uint8_t* sdm = sfl + ncell;                             // DEM flags
-    if (threadIdx.x == 0) mbar_init(&mbar, 1);
-    __syncthreads();
+    const uint32_t nv = lo(K - 1, 0);  // cells on levels R..L-2
+    double4* sv = reinterpret_cast<double4*>(sm1);
+    uint8_t* sf = sm1 + 32u * nv;      // previous-tree flags, slo layout
+    uint8_t* sd = sf + slo(K);         // DEM flags, slo layout
+
+    // ---- one round trip: flags + inputs (async), own level-(L-2) children
+    const uint8_t f0 = stage_tile_flags(sf, sigp, P, j);
+    const uint8_t d0 = stage_tile_flags(sd, P.dem, P, j);
+#pragma unroll
+    for (int k = 1; k < (KT ? KT - 1 : kMaxL); ++k) {
+        if (!KT && k > K - 2) break;
+        const uint32_t cnt = 1u << (2 * k);
+        stage16(sv + lo(k, 0), buf + P.base[R + k] + static_cast<unsigned long long>(j) * cnt, 32u * cnt);
+    }
+    const int k2 = K - 2;                 // tile level of L-2
+    const uint32_t c2 = (k2 >= 0) ? (1u << (2 * k2)) : 0u;
+    const bool has2 = threadIdx.x < c2;
+    const uint32_t m2 = j * c2 + threadIdx.x;
+    bool sp2 = false;
+    double4 ch[4];
+    if (has2) {
+        sp2 = sigp[P.fbase[L - 2] + m2] != 0;
+        if (sp2) {
+            const double4* cp = buf + P.base[L - 1] + (static_cast<unsigned long long>(m2) << 2);
+            ch[0] = ld4_nc(cp); ch[1] = ld4_nc(cp + 1); ch[2] = ld4_nc(cp + 2); ch[3] = ld4_nc(cp + 3);
+        }
+    }
+    cp_async_wait_all();
     if (threadIdx.x == 0) {
-        mbar_expect_tx(&mbar, ncell * static_cast<unsigned>(sizeof(double4)));
-        for (int n = R; n < L; ++n) {
-            const uint32_t cnt = 1u << (2 * (n - R));
-            bulk_g2s(sv + lo(n, R), buf + P.base[n] + static_cast<unsigned long long>(j) * cnt,
-                     cnt * static_cast<unsigned>(sizeof(double4)), &mbar);
-        }
-    }
-    for (int n = R; n < L; ++n) {  // flags while the bulk copies fly
-        const uint32_t cnt = 1u << (2 * (n - R));
-        const unsigned long long g = P.fbase[n] + static_cast<unsigned long long>(j) * cnt;
-        if (cnt >= 4) {
-            for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads) {
-                const uint32_t wf = *reinterpret_cast<const uint32_t*>(sigp + g + q);
-                const uint32_t wd = *reinterpret_cast<const uint32_t*>(P.dem + g + q);
-                uint8_t* df = sfl + lo(n, R) + q;
-                uint8_t* dd = sdm + lo(n, R) + q;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    df[k] = (wf >> (8 * k)) & 0xFFu;
-                    dd[k] = (wd >> (8 * k)) & 0xFFu;
-                }
-                if (n == L - 1) {  // level L-1: the previous FV1 flagged the tree cells
-                    const bool zero = 0.0 >= P.tau[n];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (!byte_of(wf, k)) P.pre[g + q + k] = (zero || byte_of(wd, k)) ? 1 : 0;
-                }
-            }
-        } else if (threadIdx.x < cnt) {
-            const uint8_t f = sigp[g + threadIdx.x], d = P.dem[g + threadIdx.x];
-            sfl[lo(n, R) + threadIdx.x] = f;
-            sdm[lo(n, R) + threadIdx.x] = d;
-            if (n == L - 1 && !f) P.pre[g + threadIdx.x] = ((0.0 >= P.tau[n]) || d) ? 1 : 0;
-        }
+        sf[0] = f0;
+        sd[0] = d0;
     }
     __syncthreads();
-    stamp(1);
-    mbar_wait(&mbar, 0);
-    stamp(2);
+
+    // ---- level L-1: cells off the previous tree only get pre = DEM | (eps == 0)
+    {
+        const int k = K - 1;
+        const uint32_t cnt = 1u << (2 * k);
+        const uint32_t zero = (0.0 >= P.tau[L - 1]) ? 0x01010101u : 0u;
+        const unsigned long long g = P.fbase[L - 1] + static_cast<unsigned long long>(j) * cnt;
+        if (cnt >= 4) {
+            for (uint32_t c = 4u * threadIdx.x; c < cnt; c += 4u * kThreads) {
+                const uint32_t f = *reinterpret_cast<const uint32_t*>(sf + slo(k) + c);
+                if (f == 0x01010101u) continue;
+                const uint32_t v = zero | *reinterpret_cast<const uint32_t*>(sd + slo(k) + c);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (!byte_of(f, q)) P.pre[g + c + q] = byte_of(v, q) ? 1 : 0;
+            }
+        } else if (threadIdx.x == 0 && !sf[0]) {
+            P.pre[g] = (zero || sd[0]) ? 1 : 0;
+        }
+    }
     unsigned tree = 0;
-    for (int n = L - 2; n >= R; --n) {
-        const uint32_t cnt = 1u << (2 * (n - R));
-        const uint32_t pb = j * cnt;
+    // ---- level L-2 from the registers
+    if (has2) {
+        bool flow = 0.0 >= P.tau[L - 2];
+        if (sp2) {
+            const Enc e = encode_children<false>(ch, P, L - 2);
+            flow = e.flow;
+            st4(buf + P.base[L - 2] + m2, e.par);
+            sv[lo(k2, 0) + threadIdx.x] = e.par;
+            ++tree;
+        }
+        P.pre[P.fbase[L - 2] + m2] = (flow || sd[slo(k2) + threadIdx.x]) ? 1 : 0;
+    }
+    __syncthreads();
+    // ---- levels L-3 .. R from shared memory
+#pragma unroll
+    for (int k = (KT ? KT : kMaxL) - 3; k >= 0; --k) {
+        if (!KT && k > K - 3) continue;
+        const int n = R + k;
+        const uint32_t cnt = 1u << (2 * k);
         for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
-            const uint32_t pm = pb + pi;
-            const uint32_t li = lo(n, R) + pi;
+            const uint32_t pm = j * cnt + pi;
             bool flow = 0.0 >= P.tau[n];
-            if (sfl[li]) {
-                const uint32_t c0 = lo(n + 1, R) + 4u * pi;
+            if (sf[slo(k) + pi]) {
+                const uint32_t c0 = lo(k + 1, 0) + 4u * pi;
                 const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
                 const Enc e = encode_children<false>(c, P, n);
                 flow = e.flow;
                 st4(buf + P.base[n] + pm, e.par);
-                sv[li] = e.par;
+                sv[lo(k, 0) + pi] = e.par;
                 ++tree;
             }
-            P.pre[P.fbase[n] + pm] = (flow || sdm[li]) ? 1 : 0;
+            P.pre[P.fbase[n] + pm] = (flow || sd[slo(k) + pi]) ? 1 : 0;
         }
         __syncthreads();
     }
-    stamp(3);
     const unsigned tsum = block_sum(tree, s_red);
     if (threadIdx.x == 0 && tsum) atomicAdd(&ctl->cnt_tree, (unsigned long long)tsum);
-    stamp(4);
-    if (P.G > 1) return;
-    const bool lastb = last_block(&ctl->done_k1, &s_last);
-    stamp(5);
-    if (!lastb) return;
-    tl_mark(ctl, 1);
-    encode_top<false>(P, ctl, sv, s_red);
     tl_mark(ctl, 2);
+}
+
+// Levels R-1 .. 0 of the re-encode after t = 0, one CTA (run as the extra
+// CTA of K2, concurrently with the subtree CTAs). Round trip 1 stages the
+// previous-tree and DEM flags of levels 0..R-1; round trip 2 loads the
+// level-R children of re-encoded level-(R-1) cells into registers and stages
+// the values of previous-tree leaves whose parent is re-encoded. Needs
+// 32 * lo(R, 0) + 2 * fbase[R] bytes of shared memory (host: R <= 6).
+__device__ void encode_top_staged(const Params& P, Ctl* ctl, uint8_t* sm) {
+    const int p = ctl->parity;
+    double4* buf = P.cells[p];
+    const uint8_t* sigp = P.sig[p];
+    const int R = P.R;
+    if (R == 0) return;
+    __shared__ unsigned s_red[32];
+    const uint32_t fb = static_cast<uint32_t>(P.fbase[R]);  // flag bytes of levels 0..R-1 (fbase[0] = 0)
+    double4* sv = reinterpret_cast<double4*>(sm);          // levels 0..R-1, compact lo(n, 0)
+    uint8_t* sf = sm + 32u * lo(R, 0);                     // previous-tree flags at fbase[n]
+    uint8_t* sd = sf + fb;                                 // DEM flags at fbase[n]
+    stage16(sf, sigp, fb);
+    stage16(sd, P.dem, fb);
+    cp_async_wait_all();
+    __syncthreads();
+    // values of previous-tree leaves (levels 1..R-2) under a re-encoded parent
+    for (int n = 1; n <= R - 2; ++n) {
+        const uint32_t cnt = 1u << (2 * n);
+        for (uint32_t m = threadIdx.x; m < cnt; m += kThreads)
+            if (!sf[P.fbase[n] + m] && sf[P.fbase[n - 1] + (m >> 2)]) {
+                const double4* g = cell_ptr(P, p, n, m);
+                cp_async16(sv + lo(n, 0) + m, g);
+                cp_async16(reinterpret_cast<uint8_t*>(sv + lo(n, 0) + m) + 16, reinterpret_cast<const uint8_t*>(g) + 16);
+            }
+    }
+    unsigned tree = 0;
+    {
+        // level R-1: children from every subtree's partition
+        const int n = R - 1;
+        const uint32_t cnt = 1u << (2 * n);
+        for (uint32_t m0 = 0; m0 < cnt; m0 += kThreads) {
+            const uint32_t m = m0 + threadIdx.x;
+            if (m >= cnt) break;
+            const bool sp = sf[P.fbase[n] + m] != 0;
+            const bool need = !sp && n > 0 && sf[P.fbase[n - 1] + (m >> 2)];
+            double4 c[4], v = make_double4(0.0, 0.0, 0.0, 0.0);
+            if (sp) {
+                c[0] = ld4_cg(cell_ptr(P, p, n + 1, 4u * m)); c[1] = ld4_cg(cell_ptr(P, p, n + 1, 4u * m + 1));
+                c[2] = ld4_cg(cell_ptr(P, p, n + 1, 4u * m + 2)); c[3] = ld4_cg(cell_ptr(P, p, n + 1, 4u * m + 3));
+            } else if (need) {
+                v = ld4_cg(cell_ptr(P, p, n, m));
+            }
+            bool flow = 0.0 >= P.tau[n];
+            if (sp) {
+                const Enc e = encode_children<false>(c, P, n);
+                flow = e.flow;
+                v = e.par;
+                st4(buf + P.base[n] + m, v);
+                ++tree;
+            }
+            if (sp || need) sv[lo(n, 0) + m] = v;
+            P.pre[P.fbase[n] + m] = (flow || sd[P.fbase[n] + m]) ? 1 : 0;
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    for (int n = R - 2; n >= 0; --n) {
+        const uint32_t cnt = 1u << (2 * n);
+        for (uint32_t m = threadIdx.x; m < cnt; m += kThreads) {
+            bool flow = 0.0 >= P.tau[n];
+            if (sf[P.fbase[n] + m]) {
+                const uint32_t c0 = lo(n + 1, 0) + 4u * m;
+                const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
+                const Enc e = encode_children<false>(c, P, n);
+                flow = e.flow;
+                st4(buf + P.base[n] + m, e.par);
+                sv[lo(n, 0) + m] = e.par;
+                ++tree;
+            }
+            P.pre[P.fbase[n] + m] = (flow || sd[P.fbase[n] + m]) ? 1 : 0;
+        }
+        __syncthreads();
+    }
+    const unsigned tt = block_sum(tree, s_red);
+    if (threadIdx.x == 0 && tt) atomicAdd(&ctl->cnt_tree, (unsigned long long)tt);
 }
 
 
@@ -836,373 +969,446 @@ __device__ __forceinline__ uint8_t band_flag(int mode, int L, int n, uint32_t m,
     return b ? 1 : 0;
 }
 
-// band + ancestor closure per subtree; per-subtree leaf
-// count; the last CTA closes levels < R and scans subtree counts into the
-// leaf-list offsets (the PTT compaction's global scan, done once on 4^R
-// values instead of per finest cell).
-__device__ void band_top(const Params& P, Ctl* ctl, uint8_t* sfl_top, unsigned* s_red);
-template <bool EXPORT>
-__device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint32_t* smem3, unsigned* s_red);
-
-__global__ void __launch_bounds__(kThreads) k_band(Params P, Ctl* ctl, int force) {
+// band + ancestor closure of subtree j and its leaf
+// counts, on 32-bit words: the word at slo(k) + 4b holds the flag bytes of
+// the 2x2 block b of tile level k (Morton children 0..3 = SW, SE, NW, NE), so
+// same-level face neighbours inside a block are byte swaps and the ones
+// outside come from the four neighbouring blocks (neighbour_dev on the block
+// index, or the halo word of the adjacent subtree). The subtree's pre-band
+// flags and the halo (edge blocks of the four adjacent subtrees at every
+// level, read from the owning partition) are staged up front. Counts follow
+// from popcounts: a reached subtree with S significant cells (S_{L-1} on
+// level L-1) has 4 S_{L-1} level-L leaves and 1 + 3 S - 4 S_{L-1} coarser
+// ones. No last-CTA tail: levels < R are closed by every K3 CTA
+// (traverse_tile); with do_top, block 0 is an extra CTA that re-encodes
+// levels R-1..0 (encode_top_staged) concurrently.
+//
+// halo: direction d (W, E, N, S), level k >= 1, block position pos < 2^(k-1)
+// along the edge at word hw(d, k, pos) = d (2^(K-1) - 1) + 2^(k-1) - 1 + pos;
+// the adjacent subtrees' roots (level R) are bytes hr[d].
+template <int KT>
+__global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int force, int do_top) {
     pdl_wait();
     pdl_trigger();
     if (!force && !active(ctl, P)) return;
-    tl_start(ctl, 1);
     extern __shared__ __align__(16) uint8_t smem2[];
+    if (do_top && blockIdx.x == 0) {
+        encode_top_staged(P, ctl, smem2);
+        return;
+    }
+    tl_start(ctl, 1);
     __shared__ unsigned s_red[32];
-    __shared__ int s_last;
+    __shared__ uint8_t hr[4];
     const int p = ctl->parity;
     uint8_t* sigc = P.sig[p ^ 1];
-    const uint8_t* pre = P.pre;
-    const int L = P.L, R = P.R, K = P.K;
-    const uint32_t j = P.tile_lo + blockIdx.x;
-    const uint32_t ncell = ((1u << (2 * K)) - 1u) / 3u;     // subtree cells on levels R..L-1
-    uint16_t* cA = reinterpret_cast<uint16_t*>(smem2);      // level-L leaves under the cell
-    uint16_t* cB = cA + ncell;                              // coarser leaves under the cell
-    uint8_t* sf = reinterpret_cast<uint8_t*>(cB + ncell);   // band, then final flags
-    uint8_t* spre = sf + ncell;                             // pre-band flags of the subtree
+    const int R = P.R;
+    const int K = KT ? KT : P.K;
+    const uint32_t j = P.tile_lo + blockIdx.x - (do_top ? 1u : 0u);
+    const uint32_t hwd = (1u << (K - 1)) - 1u;          // halo words per direction
+    uint8_t* spre = smem2;                              // pre-band flags, slo layout
+    uint8_t* sf = spre + slo(K);                        // band, then final flags, slo layout
+    __shared__ uint32_t halo[4 * 31];                   // 4 * hwd words (K <= 6)
+    const int mode = P.band_mode;
 
-    // ---- the subtree's pre-band flags, word loads where a level has >= 4 cells
-    for (int n = R; n < L; ++n) {
-        const uint32_t cnt = 1u << (2 * (n - R));
-        const unsigned long long g = P.fbase[n] + static_cast<unsigned long long>(j) * cnt;
-        if (cnt >= 4) {
-            for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads) {
-                const uint32_t w = *reinterpret_cast<const uint32_t*>(pre + g + q);
-                uint8_t* d = spre + lo(n, R) + q;
-                d[0] = w & 0xFFu; d[1] = (w >> 8) & 0xFFu; d[2] = (w >> 16) & 0xFFu; d[3] = w >> 24;
-            }
-        } else if (threadIdx.x < cnt) {
-            spre[lo(n, R) + threadIdx.x] = pre[g + threadIdx.x];
+    // ---- one round trip: own pre flags (async) + halo words (one per thread)
+    const uint8_t f0 = stage_tile_flags(spre, P.pre, P, j);
+    const uint32_t hi = threadIdx.x;
+    uint32_t hv = 0;
+    if (mode != 0 && hi < 4u * hwd) {
+        const int d = static_cast<int>(hi / hwd);
+        const uint32_t r = hi - static_cast<uint32_t>(d) * hwd;
+        const int k = 32 - __clz(r + 1u);               // level k >= 1 of this halo word
+        const uint32_t pos = r + 1u - (1u << (k - 1)), sb = 1u << (k - 1);
+        const uint32_t jn = zo::neighbour_dev(R, j, static_cast<zo::Direction>(d));
+        if (jn != zo::kNone) {
+            // the adjacent subtree's edge blocks: W -> its east column, E -> its
+            // west column, N -> its south row, S -> its north row
+            const uint32_t bx = (d == 0) ? sb - 1u : (d == 1) ? 0u : pos;
+            const uint32_t by = (d == 2) ? 0u : (d == 3) ? sb - 1u : pos;
+            const unsigned long long g =
+                P.fbase[R + k] + (static_cast<unsigned long long>(jn) << (2 * k)) + 4ull * zo::interleave(bx, by);
+            hv = *reinterpret_cast<const uint32_t*>(P.ppre[owner_of(P, R, jn)] + g);
         }
+    } else if (mode != 0 && hi >= 128 && hi < 132) {
+        const int d = static_cast<int>(hi - 128);
+        const uint32_t jn = zo::neighbour_dev(R, j, static_cast<zo::Direction>(d));
+        hv = (jn != zo::kNone) ? P.ppre[owner_of(P, R, jn)][P.fbase[R] + jn] : 0u;
     }
+    cp_async_wait_all();
+    if (threadIdx.x == 0) spre[0] = f0;
+    if (mode != 0 && hi < 4u * hwd) halo[hi] = hv;
+    if (mode != 0 && hi >= 128 && hi < 132) hr[hi - 128] = static_cast<uint8_t>(hv);
     __syncthreads();
-    // ---- band (D3). The subtree is aligned, so a neighbour inside it is the
-    //      neighbour of the subtree-local Morton code on the local grid (level
-    //      n - R); only edge cells look outside (global / other partitions).
-    for (int n = R; n < L; ++n) {
-        const uint32_t cnt = 1u << (2 * (n - R));
-        const uint32_t loN = lo(n, R), jb = j * cnt;
-        auto pre_out = [&](int k, uint32_t mm) -> uint8_t {  // (k, mm) outside the subtree
-            return P.ppre[owner_of(P, k, mm)][P.fbase[k] + mm];
-        };
-        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
-            uint8_t b = spre[loN + pi];
-            if (P.band_mode == 2) {
+
+    // pre flag of the level-k cell at local (x, y) (possibly one step outside)
+    auto pre_cell = [&](int k, int x, int y) -> uint32_t {
+        const int s = 1 << k;
+        int d = -1;
+        if (x < 0) d = 0; else if (x >= s) d = 1; else if (y >= s) d = 2; else if (y < 0) d = 3;
+        if (d < 0) return spre[slo(k) + zo::interleave(x, y)];
+        if (k == 0) return hr[d];
+        const int xo = (x + s) & (s - 1), yo = (y + s) & (s - 1);  // cell inside the adjacent subtree
+        const uint32_t pos = (d < 2) ? static_cast<uint32_t>(yo >> 1) : static_cast<uint32_t>(xo >> 1);
+        const uint32_t w = halo[static_cast<uint32_t>(d) * hwd + (1u << (k - 1)) - 1u + pos];
+        return (w >> (8 * (((yo & 1) << 1) | (xo & 1)))) & 0xFFu;
+    };
+
+    // ---- band (D3)
+    if (mode == 2) {
+        if (threadIdx.x == 0) sf[0] = (spre[0] | hr[0] | hr[1] | hr[2] | hr[3]) ? 1 : 0;
 #pragma unroll
-                for (int d = 0; d < 4; ++d) {
-                    const uint32_t ln = zo::neighbour_dev(n - R, pi, static_cast<zo::Direction>(d));
-                    if (ln != zo::kNone) {
-                        b |= spre[loN + ln];
-                    } else {
-                        const uint32_t nb = zo::neighbour_dev(n, jb + pi, static_cast<zo::Direction>(d));
-                        if (nb != zo::kNone) b |= pre_out(n, nb);
+        for (int k = 1; k < (KT ? KT : kMaxL); ++k) {
+            if (!KT && k >= K) break;
+            const uint32_t nw = 1u << (2 * (k - 1));
+            const uint32_t sb = 1u << (k - 1);                        // blocks per side
+            const uint32_t* wk = reinterpret_cast<const uint32_t*>(spre + slo(k));
+            const uint32_t* hk = halo + (sb - 1u);                    // + d * hwd + pos
+            for (uint32_t b = threadIdx.x; b < nw; b += kThreads) {
+                const uint32_t w = wk[b];
+                const uint32_t bx = zo::compact_bits(b), by = zo::compact_bits(b >> 1);
+                const uint32_t ww = bx > 0u ? wk[zo::interleave(bx - 1u, by)] : hk[by];
+                const uint32_t we = bx + 1u < sb ? wk[zo::interleave(bx + 1u, by)] : hk[hwd + by];
+                const uint32_t wn = by + 1u < sb ? wk[zo::interleave(bx, by + 1u)] : hk[2u * hwd + bx];
+                const uint32_t ws = by > 0u ? wk[zo::interleave(bx, by - 1u)] : hk[3u * hwd + bx];
+                uint32_t o = w | ((w >> 8) & 0x00FF00FFu) | ((w << 8) & 0xFF00FF00u) | (w >> 16) | (w << 16);
+                o |= (ww >> 8) & 0x00FF00FFu;   // W block: its SE, NE
+                o |= (we << 8) & 0xFF00FF00u;   // E block: its SW, NW
+                o |= wn << 16;                  // N block: its SW, SE
+                o |= ws >> 16;                  // S block: its NW, NE
+                *reinterpret_cast<uint32_t*>(sf + slo(k) + 4u * b) = o;
+            }
+        }
+    } else {
+        for (int k = 0; k < K; ++k) {
+            const uint32_t cnt = 1u << (2 * k);
+            for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
+                uint32_t b = spre[slo(k) + pi];
+                if (mode == 1 && k + 1 < K) {
+                    const int x = static_cast<int>(zo::compact_bits(pi)), y = static_cast<int>(zo::compact_bits(pi >> 1));
+                    for (int q = 0; q < 4; ++q) {
+                        const int cx = 2 * x + (q & 1), cy = 2 * y + (q >> 1);
+                        b |= pre_cell(k + 1, cx - 1, cy) | pre_cell(k + 1, cx + 1, cy) | pre_cell(k + 1, cx, cy + 1) |
+                             pre_cell(k + 1, cx, cy - 1);
                     }
                 }
-            } else if (P.band_mode == 1 && n + 1 < L) {
-                const uint32_t loC = lo(n + 1, R), jc = jb << 2;
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t lc = 4u * pi + static_cast<uint32_t>(k);
-#pragma unroll
-                    for (int d = 0; d < 4; ++d) {
-                        const uint32_t ln = zo::neighbour_dev(n + 1 - R, lc, static_cast<zo::Direction>(d));
-                        if (ln != zo::kNone) {
-                            b |= spre[loC + ln];
-                        } else {
-                            const uint32_t nb = zo::neighbour_dev(n + 1, jc + lc, static_cast<zo::Direction>(d));
-                            if (nb != zo::kNone) b |= pre_out(n + 1, nb);
-                        }
-                    }
-                }
+                sf[slo(k) + pi] = b ? 1 : 0;
             }
-            sf[loN + pi] = b ? 1 : 0;
         }
     }
     __syncthreads();
-    // ---- ancestor closure bottom-up, with the leaf counts of every subtree
-    //      cell assuming it is reached (level L-1: 4 level-L leaves or itself)
-    {
-        const uint32_t cnt = 1u << (2 * (L - 1 - R));
-        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
-            const bool sg = sf[lo(L - 1, R) + pi] != 0;
-            cA[lo(L - 1, R) + pi] = sg ? 4 : 0;
-            cB[lo(L - 1, R) + pi] = sg ? 0 : 1;
-        }
-    }
-    __syncthreads();
-    for (int n = L - 2; n >= R; --n) {
-        const uint32_t cnt = 1u << (2 * (n - R));
-        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
-            const uint32_t c = lo(n + 1, R) + 4u * pi;
-            const bool sg = sf[lo(n, R) + pi] || sf[c] || sf[c + 1] || sf[c + 2] || sf[c + 3];
-            sf[lo(n, R) + pi] = sg ? 1 : 0;
-            cA[lo(n, R) + pi] = sg ? static_cast<uint16_t>(cA[c] + cA[c + 1] + cA[c + 2] + cA[c + 3]) : 0;
-            cB[lo(n, R) + pi] = sg ? static_cast<uint16_t>(cB[c] + cB[c + 1] + cB[c + 2] + cB[c + 3]) : 1;
+    // ---- ancestor closure bottom-up: a cell is significant if its band flag
+    //      or any child is; byte-per-cell words of level k from level k + 1
+    auto nz = [](uint32_t w) -> uint32_t { return w ? 1u : 0u; };
+#pragma unroll
+    for (int k = (KT ? KT : kMaxL) - 2; k >= 0; --k) {
+        if (!KT && k > K - 2) continue;
+        if (k == 0) {
+            if (threadIdx.x == 0) sf[0] = (sf[0] | nz(*reinterpret_cast<const uint32_t*>(sf + slo(1)))) ? 1 : 0;
+        } else {
+            const uint32_t nw = 1u << (2 * (k - 1));
+            for (uint32_t b = threadIdx.x; b < nw; b += kThreads) {
+                const uint4 c = *reinterpret_cast<const uint4*>(sf + slo(k + 1) + 16u * b);
+                uint32_t* w = reinterpret_cast<uint32_t*>(sf + slo(k) + 4u * b);
+                *w |= nz(c.x) | (nz(c.y) << 8) | (nz(c.z) << 16) | (nz(c.w) << 24);
+            }
         }
         __syncthreads();
     }
-    // ---- final flags of the subtree, word stores where a level has >= 4 cells
-    for (int n = R; n < L; ++n) {
-        const uint32_t cnt = 1u << (2 * (n - R));
-        const unsigned long long g = P.fbase[n] + static_cast<unsigned long long>(j) * cnt;
-        if (cnt >= 4) {
-            for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads) {
-                const uint8_t* d = sf + lo(n, R) + q;
-                *reinterpret_cast<uint32_t*>(sigc + g + q) =
-                    uint32_t(d[0]) | (uint32_t(d[1]) << 8) | (uint32_t(d[2]) << 16) | (uint32_t(d[3]) << 24);
-            }
-        } else if (threadIdx.x < cnt) {
-            sigc[g + threadIdx.x] = sf[lo(n, R) + threadIdx.x];
+    // ---- final flags (word stores), leaf counts from popcounts
+    unsigned S = 0, S1 = 0;
+    if (threadIdx.x == 0) {
+        sigc[P.fbase[R] + j] = sf[0];
+        S = sf[0];
+        if (K == 1) S1 = sf[0];
+    }
+#pragma unroll
+    for (int k = 1; k < (KT ? KT : kMaxL); ++k) {
+        if (!KT && k >= K) break;
+        const uint32_t nw = 1u << (2 * (k - 1));
+        const unsigned long long g = P.fbase[R + k] + (static_cast<unsigned long long>(j) << (2 * k));
+        for (uint32_t b = threadIdx.x; b < nw; b += kThreads) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(sf + slo(k) + 4u * b);
+            *reinterpret_cast<uint32_t*>(sigc + g + 4u * b) = w;
+            const unsigned c = __popc(w);
+            S += c;
+            if (k == K - 1) S1 += c;
         }
     }
+    const unsigned St = block_sum(S, s_red);
+    const unsigned S1t = block_sum(S1, s_red);
     if (threadIdx.x == 0) {
-        P.tile_cnt[j] = cA[0];
-        P.tile_cnt[P.n_tiles + j] = cB[0];
+        P.tile_cnt[j] = 4u * S1t;
+        P.tile_cnt[P.n_tiles + j] = 1u + 3u * St - 4u * S1t;
     }
-    if (P.G > 1) return;  // partitioned: k_band_top runs after all partitions' subtrees
-    const bool fuse = P.fuse_k3 && !force;
-    const unsigned long long target = static_cast<unsigned long long>(ctl->step) + 1ull;
-    const bool last = last_block(&ctl->done_k2, &s_last);
-    if (last) {
-        tl_mark(ctl, 4);
-        band_top(P, ctl, smem2, s_red);
-        tl_mark(ctl, 5);
-    }
-    if (!fuse) return;
-    // ---- K3 fused: every CTA is resident (host-checked), so the others wait
-    //      for the last CTA's offsets instead of a new launch
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (last) {
-            __threadfence();
-            st_release_u64(&ctl->k2_ready, target);
-        } else {
-            const unsigned long long t0 = gtimer();
-            while (ld_acquire_u64(&ctl->k2_ready) != target) {
-                __nanosleep(200);
-                if (gtimer() - t0 > 2000000000ull) {  // 2 s: never expected; fail instead of hanging
-                    report_error(ctl, kErrDt, j, 0, kStageTraverse);
-                    break;
-                }
-            }
-        }
-    }
-    __syncthreads();
-    tl_start(ctl, 2);
-    traverse_tile<false>(P, ctl, j, reinterpret_cast<uint32_t*>(smem2), s_red);
+    tl_mark(ctl, 5);
 }
 
-__global__ void __launch_bounds__(kThreads) k_band_top(Params P, Ctl* ctl, int force) {
-    pdl_wait();
-    if (!force && !active(ctl, P)) return;
-    extern __shared__ __align__(16) uint8_t smem2t[];
+// The top of the tree (levels 0..R) as every K3 CTA sees it, in shared memory
+// at the padded flag offsets fbase[n] (fbase[0] = 0): ts = flags of levels
+// 0..R (level R = every subtree root, from K2). Hot path: band (D3) + closure
+// of levels R-1..0 from the pre-band flags tp; export: the stored flags.
+// Closure makes significance upward-closed, so a cell is on the tree iff its
+// parent is significant, and a subtree's depth is the first non-significant
+// ancestor level.
+struct Top {
+    uint8_t* ts;
+    uint8_t* tp;  // pre-band flags (hot path)
+    uint8_t* tv;  // previous-tree flags (hot path)
+};
+
+// level of the leaf covering subtree t (R: the subtree root is reached)
+__device__ __forceinline__ int tile_depth(const Params& P, const uint8_t* ts, uint32_t t) {
+    const int R = P.R;
+    int n = 0;
+    while (n < R && ts[P.fbase[n] + (t >> (2 * (R - n)))]) ++n;
+    return n;
+}
+
+// leaf counts (A: level L, B: coarser) that subtree t contributes: reached
+// subtrees from K2's counts, else one B leaf for the first subtree under the
+// covering leaf
+__device__ __forceinline__ void tile_counts(const Params& P, const uint8_t* ts, const uint32_t* cnt, uint32_t t,
+                                            unsigned& ca, unsigned& cb) {
+    const int R = P.R;
+    const int n = tile_depth(P, ts, t);
+    if (n == R) {
+        ca = cnt[t];
+        cb = cnt[P.n_tiles + t];
+    } else {
+        ca = 0;
+        cb = ((t & ((1u << (2 * (R - n))) - 1u)) == 0u) ? 1u : 0u;
+    }
+}
+
+// decode (projection, D4) + PTT (Alg. 5) + compaction
+// of subtree j (K3). Every CTA first rebuilds the top of the
+// tree (band/closure of levels < R, per-subtree leaf counts and their scan up
+// to j) from staged copies — instead of a serial last CTA in K2. EXPORT = the
+// traversal of the current tree (after a step) into the Morton-ordered export
+// list, with no side effects on the state.
+template <bool EXPORT, int KT>
+__device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint8_t* sm) {
     __shared__ unsigned s_red[32];
-    band_top(P, ctl, smem2t, s_red);
-}
-
-// Top of K2 (one CTA), all in shared memory: tpre / tprev = pre-band and
-// previous flags of levels 0..R (replicated), tsig = current flags of levels
-// 0..R (level R from every subtree's partition), intree = "on the current
-// tree", tcnt = per-subtree counts. Band + closure of levels R-1..0, decode of
-// levels 1..R, per-subtree traversal depth and the leaf-list scans.
-__device__ void band_top(const Params& P, Ctl* ctl, uint8_t* sfl_top, unsigned* s_red) {
-    const int p = ctl->parity;
-    uint8_t* sigc = P.sig[p ^ 1];
-    const uint8_t* pre = P.pre;
-    const int L = P.L, R = P.R;
-
-    uint8_t* tsig = sfl_top;                  // lo(R+1)
-    uint8_t* tprev = tsig + lo(R + 1, 0);     // lo(R+1)
-    uint8_t* tpre = tprev + lo(R + 1, 0);     // lo(R+1)
-    uint8_t* intree = tpre + lo(R + 1, 0);    // lo(R+1)
-    uint32_t* tcnt = reinterpret_cast<uint32_t*>(sfl_top + ((4u * lo(R + 1, 0) + 15u) & ~15u));  // 2 x 4^R
-    const uint8_t* sigp = P.sig[p];
-    for (int n = 0; n <= R; ++n) {
-        const uint32_t cnt = 1u << (2 * n);
-        for (uint32_t m = threadIdx.x; m < cnt; m += kThreads) {
-            if (n < L) {
-                tpre[lo(n, 0) + m] = pre[P.fbase[n] + m];
-                tprev[lo(n, 0) + m] = sigp[P.fbase[n] + m];
-            }
-            if (n == R) {
-                const int g = owner_of(P, R, m);  // subtree m's partition
-                tsig[lo(R, 0) + m] = ldcg_u8(P.psig[g][p ^ 1] + P.fbase[R] + m);
-                tcnt[m] = ldcg_u32(P.ptile_cnt[g] + m);
-                tcnt[P.n_tiles + m] = ldcg_u32(P.ptile_cnt[g] + P.n_tiles + m);
-            }
-        }
-    }
-    __syncthreads();
-    for (int n = R - 1; n >= 0; --n) {  // band + closure, levels R-1 .. 0
-        const uint32_t cnt = 1u << (2 * n);
-        for (uint32_t m = threadIdx.x; m < cnt; m += kThreads) {
-            uint8_t b = band_flag(P.band_mode, L, n, m, [&](int k, uint32_t mm) { return tpre[lo(k, 0) + mm]; });
-            const uint8_t* c = tsig + lo(n + 1, 0) + 4u * m;
-            if (c[0] | c[1] | c[2] | c[3]) b = 1;
-            sigc[P.fbase[n] + m] = b;
-            tsig[lo(n, 0) + m] = b;
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) intree[0] = 1;
-    __syncthreads();
-    for (int n = 1; n <= R; ++n) {
-        const uint32_t cnt = 1u << (2 * n);
-        for (uint32_t m = threadIdx.x; m < cnt; m += kThreads)
-            intree[lo(n, 0) + m] = intree[lo(n - 1, 0) + (m >> 2)] & tsig[lo(n - 1, 0) + (m >> 2)];
-        __syncthreads();
-    }
-    // decode (projection, D4) of levels 1..R: a cell on the tree below a newly
-    // significant ancestor takes the value of the topmost such ancestor; the
-    // level-R result is also each subtree's inherited source for K3
-    {
-        double4* buf = P.cells[p];
-        unsigned nnew = 0;
-        for (int n = 0; n < R; ++n) {
-            const uint32_t cnt = 1u << (2 * n);
-            for (uint32_t m = threadIdx.x; m < cnt; m += kThreads)
-                nnew += (tsig[lo(n, 0) + m] && !tprev[lo(n, 0) + m]) ? 1u : 0u;
-        }
-        for (int n = 1; n <= R; ++n) {
-            const uint32_t cnt = 1u << (2 * n);
-            for (uint32_t m = threadIdx.x; m < cnt; m += kThreads) {
-                uint32_t src = kNoSrc;
-                if (intree[lo(n, 0) + m]) {
-                    for (int k = 0; k < n; ++k) {
-                        const uint32_t a = lo(k, 0) + (m >> (2 * (n - k)));
-                        if (tsig[a] && !tprev[a]) {
-                            src = zo::z_of(k, m >> (2 * (n - k)));
-                            break;
-                        }
-                    }
-                    if (src != kNoSrc) write_projection(buf, P, n, m, src);
-                }
-                if (n == R) P.tile_src[m] = src;
-            }
-        }
-        if (R == 0 && threadIdx.x == 0) P.tile_src[0] = kNoSrc;  // the root has no ancestor
-        const unsigned tn = block_sum(nnew, s_red);
-        if (threadIdx.x == 0 && tn) atomicAdd(&ctl->cnt_new, (unsigned long long)tn);
-    }
-    // ---- per-subtree leaf counts, their exclusive scans, and each subtree's
-    //      traversal depth (R = reached, else the level of its covering leaf).
-    //      Hot-path list: all level-L leaves (A) first, then the coarser ones
-    //      (B); export list: Morton order (A and B interleaved per subtree).
-    const uint32_t nt = static_cast<uint32_t>(P.n_tiles);
-    const uint32_t per = (nt + kThreads - 1) / kThreads;
-    const uint32_t a = threadIdx.x * per;
-    const uint32_t b = min(nt, a + per);
-    unsigned la = 0, lb = 0;
-    for (uint32_t t = a; t < b; ++t) {
-        int n = R;
-        while (!intree[lo(n, 0) + (t >> (2 * (R - n)))]) --n;
-        unsigned ca = 0, cb;
-        if (n == R) {
-            ca = tcnt[t];
-            cb = tcnt[nt + t];
-        } else {
-            cb = ((t & ((1u << (2 * (R - n))) - 1u)) == 0u) ? 1u : 0u;
-        }
-        P.tile_lvl[t] = static_cast<uint32_t>(n);
-        P.tile_off[t] = ca;       // temporarily the counts
-        P.tile_off[nt + t] = cb;
-        la += ca;
-        lb += cb;
-    }
-    unsigned ta, tb;
-    unsigned oa = block_exscan(la, s_red, &ta);
-    unsigned ob = block_exscan(lb, s_red, &tb);
-    unsigned om = oa + ob;
-    for (uint32_t t = a; t < b; ++t) {
-        const unsigned ca = P.tile_off[t], cb = P.tile_off[nt + t];
-        P.tile_off[t] = oa;               // A: level-L leaves
-        P.tile_off[nt + t] = ta + ob;     // B: after all of A
-        P.tile_off[2 * nt + t] = om;      // Morton-ordered export list
-        oa += ca;
-        ob += cb;
-        om += ca + cb;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        ctl->n_leaves = ta + tb;
-        ctl->n_leaves_A = ta;
-        // this partition's slices of the A and B lists
-        ctl->a_lo = P.tile_off[P.tile_lo];
-        ctl->a_hi = (P.tile_hi < nt) ? P.tile_off[P.tile_hi] : ta;
-        ctl->b_lo = P.tile_off[nt + P.tile_lo];
-        ctl->b_hi = (P.tile_hi < nt) ? P.tile_off[nt + P.tile_hi] : ta + tb;
-        ctl->done_k2 = 0;
-    }
-}
-
-
-// decode + PTT + compaction of subtree j (K3). EXPORT = re-run the traversal
-// of the current tree (after a step) into the Morton-ordered export list, with
-// no side effects (no decode, no timeline).
-template <bool EXPORT>
-__device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint32_t* smem3, unsigned* s_red) {
+    __shared__ unsigned s_off[4];
     const int p = ctl->parity;
     double4* buf = P.cells[p];
     const uint8_t* sigc = EXPORT ? P.sig[p] : P.sig[p ^ 1];
     const uint8_t* sigp = EXPORT ? P.sig[p ^ 1] : P.sig[p];
-    const int L = P.L, R = P.R, K = P.K;
-    const uint32_t ncell = ((1u << (2 * K)) - 1u) / 3u;  // subtree cells on levels R..L-1
-    uint32_t* src = smem3;                               // [ncell]
-    uint8_t* sc = reinterpret_cast<uint8_t*>(src + ncell);  // [ncell]
-    uint8_t* sp = sc + ncell;                               // [ncell]
+    const int L = P.L, R = P.R;
+    const int K = KT ? KT : P.K;
+    const uint32_t nt = static_cast<uint32_t>(P.n_tiles);
+    const uint32_t ncell = lo(L, R);
+    const uint32_t fb = static_cast<uint32_t>(P.fbase[R]);  // top flag bytes of levels 0..R-1
+    const uint32_t ftop = (fb + nt + 15u) & ~15u;
+    // shared memory
+    uint8_t* sc = sm;                                          // own current flags, slo layout
+    uint8_t* sp = sc + slo(K);                                 // own previous flags
+    Top T;
+    T.ts = sp + slo(K);
+    T.tp = T.ts + ftop;
+    T.tv = T.tp + fb;
+    uint32_t* scnt = reinterpret_cast<uint32_t*>(T.tv + fb);  // [2 nt] subtree counts when nt <= 1024
+    const bool cnt_smem = nt <= 1024u;
+    uint32_t* src = scnt + (cnt_smem ? 2u * nt : 0u);          // [ncell] projection sources
+    const uint32_t* cnt = cnt_smem ? scnt : P.tile_cnt;
 
-    const uint32_t leafn = ldcg_u32(P.tile_lvl + j);  // written by K2's last CTA
-    const uint32_t rootsrc = ldcg_u32(P.tile_src + j);
-    const bool reached = leafn == static_cast<uint32_t>(R);
-    int any_new = 0;
-    for (int n = R; n < L; ++n) {  // current / previous flags of the subtree, word loads
-        const uint32_t cnt = 1u << (2 * (n - R));
-        const unsigned long long g = P.fbase[n] + static_cast<unsigned long long>(j) * cnt;
-        if (cnt >= 4) {
-            for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads) {
-                const uint32_t wc = *reinterpret_cast<const uint32_t*>(sigc + g + q);
-                const uint32_t wp = *reinterpret_cast<const uint32_t*>(sigp + g + q);
-                uint8_t* dc = sc + lo(n, R) + q;
-                uint8_t* dp = sp + lo(n, R) + q;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    dc[k] = (wc >> (8 * k)) & 0xFFu;
-                    dp[k] = (wp >> (8 * k)) & 0xFFu;
-                }
-                any_new |= (wc & ~wp) ? 1 : 0;
+    // ---- one round trip: own flags, top flags, subtree roots and counts
+    const uint8_t c0 = stage_tile_flags(sc, sigc, P, j);
+    const uint8_t q0 = EXPORT ? 0 : stage_tile_flags(sp, sigp, P, j);
+    if (EXPORT) {
+        stage16(T.ts, sigc, fb);
+    } else {
+        stage16(T.tp, P.pre, fb);
+        stage16(T.tv, sigp, fb);
+    }
+    // subtree roots (level R) and counts from each subtree's partition
+    const uint32_t tpp = P.tiles_per_part;
+    const int rb = EXPORT ? p : p ^ 1;
+    uint8_t r0 = 0;
+    if (nt == 1u) {
+        if (threadIdx.x == 64) r0 = P.psig[0][rb][P.fbase[R]];
+    } else if (P.G == 1 || (tpp & 15u) == 0u) {
+        for (uint32_t q = 16u * threadIdx.x; q < nt; q += 16u * kThreads)
+            cp_async16(T.ts + fb + q, P.psig[owner_of(P, R, q)][rb] + P.fbase[R] + q);
+    } else if ((tpp & 3u) == 0u) {
+        for (uint32_t q = 4u * threadIdx.x; q < nt; q += 4u * kThreads)
+            cp_async4(T.ts + fb + q, P.psig[owner_of(P, R, q)][rb] + P.fbase[R] + q);
+    } else {  // small partitioned grids (tests): plain byte copies
+        for (uint32_t q = threadIdx.x; q < nt; q += kThreads)
+            T.ts[fb + q] = P.psig[owner_of(P, R, q)][rb][P.fbase[R] + q];
+    }
+    if (cnt_smem) {
+        if (P.G == 1 && (nt & 3u) == 0u) {
+            for (uint32_t q = 4u * threadIdx.x; q < 2u * nt; q += 4u * kThreads) cp_async16(scnt + q, P.tile_cnt + q);
+        } else {
+            for (uint32_t q = threadIdx.x; q < 2u * nt; q += kThreads) {
+                const uint32_t t = q < nt ? q : q - nt;
+                cp_async4(scnt + q, P.ptile_cnt[owner_of(P, R, t)] + q);
             }
-        } else if (threadIdx.x < cnt) {
-            const uint8_t c = sigc[g + threadIdx.x], q = sigp[g + threadIdx.x];
-            sc[lo(n, R) + threadIdx.x] = c;
-            sp[lo(n, R) + threadIdx.x] = q;
-            any_new |= (c && !q) ? 1 : 0;
         }
     }
-    // decode is needed only where something became significant
-    any_new = __syncthreads_or(any_new | (rootsrc != kNoSrc ? 1 : 0));
-    if (EXPORT) any_new = 0;
-    unsigned nnew = 0;
+    cp_async_wait_all();
+    if (threadIdx.x == 0) {
+        sc[0] = c0;
+        if (!EXPORT) sp[0] = q0;
+    }
+    if (threadIdx.x == 64 && nt == 1u) T.ts[fb] = r0;
+    __syncthreads();
 
-    if (reached && any_new) {
+    // ---- top: band + closure of levels R-1 .. 0 (hot path)
+    if (!EXPORT) {
+        for (int n = R - 1; n >= 0; --n) {
+            const uint32_t cnt_n = 1u << (2 * n);
+            for (uint32_t m = threadIdx.x; m < cnt_n; m += kThreads) {
+                uint8_t b = band_flag(P.band_mode, L, n, m, [&](int k, uint32_t mm) -> uint8_t {
+                    return k < R ? T.tp[P.fbase[k] + mm] : P.ppre[owner_of(P, k, mm)][P.fbase[k] + mm];
+                });
+                const uint8_t* c = T.ts + P.fbase[n + 1] + 4u * m;
+                if (c[0] | c[1] | c[2] | c[3]) b = 1;
+                T.ts[P.fbase[n] + m] = b;
+            }
+            __syncthreads();
+        }
+    }
+
+    // ---- subtree leaf counts and their exclusive scan up to j (and, for the
+    //      partition's first CTA, up to tile_hi and the totals). Hot path:
+    //      all level-L leaves (list A) first, then the coarser ones (list B);
+    //      export: one Morton-ordered list.
+    const bool first = blockIdx.x == 0;
+    unsigned tot_a = 0;  // leaves in list A (all partitions)
+    {
+        const uint32_t per = (nt + kThreads - 1) / kThreads;
+        const uint32_t a = threadIdx.x * per;
+        const uint32_t b = min(nt, a + per);
+        unsigned la = 0, lb = 0;
+        for (uint32_t t = a; t < b; ++t) {
+            unsigned ca, cb;
+            tile_counts(P, T.ts, cnt, t, ca, cb);
+            la += ca;
+            lb += cb;
+        }
+        unsigned ta, tb;
+        const unsigned oa = block_exscan(la, s_red, &ta);
+        const unsigned ob = block_exscan(lb, s_red, &tb);
+        tot_a = ta;
+        auto offsets_at = [&](uint32_t x, int slot) {  // exclusive prefix at subtree x (x < nt)
+            if (x < a || x >= b) return;
+            unsigned xa = oa, xb = ob;
+            for (uint32_t t = a; t < x; ++t) {
+                unsigned ca, cb;
+                tile_counts(P, T.ts, cnt, t, ca, cb);
+                xa += ca;
+                xb += cb;
+            }
+            s_off[slot] = xa;
+            s_off[slot + 1] = xb;
+        };
+        offsets_at(j, 0);
+        if (!EXPORT && first) {
+            if (P.tile_hi < nt) {
+                offsets_at(P.tile_hi, 2);
+            } else if (threadIdx.x == 0) {
+                s_off[2] = ta;
+                s_off[3] = tb;
+            }
+        }
+        __syncthreads();
+        if (!EXPORT && first && threadIdx.x == 0) {
+            ctl->n_leaves = ta + tb;
+            ctl->n_leaves_A = ta;
+            // this partition's slices of the A and B lists
+            ctl->a_lo = s_off[0];
+            ctl->a_hi = s_off[2];
+            ctl->b_lo = ta + s_off[1];
+            ctl->b_hi = ta + s_off[3];
+        }
+    }
+    uint32_t oa, ob;
+    if (EXPORT) {
+        oa = s_off[0] + s_off[1];
+        ob = 0;
+        if (threadIdx.x == 0) P.tile_off[2 * nt + j] = oa;
+    } else {
+        oa = s_off[0];
+        ob = tot_a + s_off[1];  // list B follows all of list A
+    }
+
+    // ---- this CTA's share of the top: final flags of levels < R (the
+    //      partition's first CTA), projection (D4) of the top cells whose
+    //      first subtree is j, the root's decode source, new-cell count
+    const int leafn = tile_depth(P, T.ts, j);
+    uint32_t rootsrc = kNoSrc;
+    unsigned nnew = 0;
+    if (!EXPORT) {
+        for (int k = 0; k < R; ++k) {
+            const uint32_t a = P.fbase[k] + (j >> (2 * (R - k)));
+            if (T.ts[a] && !T.tv[a]) {
+                rootsrc = zo::z_of(k, j >> (2 * (R - k)));
+                break;
+            }
+        }
+        if (first) {
+            for (int n = 0; n < R; ++n)
+                for (uint32_t m = threadIdx.x; m < (1u << (2 * n)); m += kThreads) {
+                    const uint32_t a = P.fbase[n] + m;
+                    P.sig[p ^ 1][a] = T.ts[a];
+                    if (P.part == 0) nnew += (T.ts[a] && !T.tv[a]) ? 1u : 0u;
+                }
+        }
+        // top cells (levels 1..R) on the tree whose first subtree is j
+        const int n = static_cast<int>(threadIdx.x) + 1;
+        if (n <= R && n <= leafn && (j & ((1u << (2 * (R - n))) - 1u)) == 0u) {
+            const uint32_t m = j >> (2 * (R - n));
+            uint32_t s = kNoSrc;
+            for (int k = 0; k < n; ++k) {
+                const uint32_t a = P.fbase[k] + (m >> (2 * (n - k)));
+                if (T.ts[a] && !T.tv[a]) {
+                    s = zo::z_of(k, m >> (2 * (n - k)));
+                    break;
+                }
+            }
+            if (s != kNoSrc) write_projection(buf, P, n, m, s);
+        }
+    }
+
+    const bool reached = leafn == R;
+    int any_new = 0;
+    if (!EXPORT && reached) {
+        if (sc[0] && !sp[0]) any_new = 1;
+#pragma unroll
+        for (int k = 1; k < (KT ? KT : kMaxL); ++k) {
+            if (!KT && k >= K) break;
+            for (uint32_t q = 4u * threadIdx.x; q < (1u << (2 * k)); q += 4u * kThreads)
+                any_new |= (*reinterpret_cast<const uint32_t*>(sc + slo(k) + q) &
+                            ~*reinterpret_cast<const uint32_t*>(sp + slo(k) + q))
+                               ? 1
+                               : 0;
+        }
+    }
+    any_new = __syncthreads_or(any_new | (rootsrc != kNoSrc ? 1 : 0));
+    if (EXPORT || !reached) any_new = 0;
+
+    if (any_new) {
         // ---- projection inside the subtree, top-down
-        if (threadIdx.x == 0) src[0] = rootsrc;  // the root itself was projected by K2
+        if (threadIdx.x == 0) src[0] = rootsrc;  // the root itself was projected above
         __syncthreads();
         for (int n = R; n < L; ++n) {
-            const uint32_t cnt = 1u << (2 * (n - R));
-            for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
+            const int k = n - R;
+            const uint32_t cnt_k = 1u << (2 * k);
+            for (uint32_t pi = threadIdx.x; pi < cnt_k; pi += kThreads) {
                 const uint32_t li = lo(n, R) + pi;
-                const uint32_t pm = j * cnt + pi;
-                const bool isnew = sc[li] && !sp[li];
+                const uint32_t pm = j * cnt_k + pi;
+                const bool isnew = sc[slo(k) + pi] && !sp[slo(k) + pi];
                 nnew += isnew ? 1u : 0u;
                 uint32_t cs = kNoSrc;
-                if (sc[li]) cs = (src[li] != kNoSrc) ? src[li] : (isnew ? zo::z_of(n, pm) : kNoSrc);
+                if (sc[slo(k) + pi]) cs = (src[li] != kNoSrc) ? src[li] : (isnew ? zo::z_of(n, pm) : kNoSrc);
                 if (n + 1 < L) {
                     const uint32_t lc = lo(n + 1, R) + 4u * pi;
                     src[lc] = cs; src[lc + 1] = cs; src[lc + 2] = cs; src[lc + 3] = cs;
                 }
                 if (cs != kNoSrc)
-                    for (uint32_t k = 0; k < 4; ++k) write_projection(buf, P, n + 1, 4u * pm + k, cs);
+                    for (uint32_t q = 0; q < 4; ++q) write_projection(buf, P, n + 1, 4u * pm + q, cs);
             }
             __syncthreads();
         }
@@ -1210,17 +1416,15 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint32_t* s
     if (!EXPORT) {
         const unsigned tn = block_sum(nnew, s_red);
         if (threadIdx.x == 0 && tn) atomicAdd(&ctl->cnt_new, (unsigned long long)tn);
+    } else {
+        __syncthreads();  // s_off consumed before s_red is reused
     }
 
-    // ---- PTT + compaction. Hot path: level-L leaves to list A at
-    //      tile_off[j], coarser leaves to list B at tile_off[nt + j]; export:
-    //      one Morton-ordered list at tile_off[2 nt + j].
-    const uint32_t nt = static_cast<uint32_t>(P.n_tiles);
+    // ---- PTT + compaction. Hot path: level-L leaves to list A at oa,
+    //      coarser leaves to list B at ob; export: one Morton-ordered list.
     uint32_t* outA = EXPORT ? P.leaves_x : P.leaves;
-    uint32_t oa = ldcg_u32(P.tile_off + (EXPORT ? 2 * nt + j : j));
-    uint32_t ob = EXPORT ? 0u : ldcg_u32(P.tile_off + nt + j);
     if (!reached) {
-        const int n = static_cast<int>(leafn);
+        const int n = leafn;
         if (threadIdx.x == 0 && ((j & ((1u << (2 * (R - n))) - 1u)) == 0u))
             (EXPORT ? outA[oa] : P.leaves[ob]) = zo::z_of(n, j >> (2 * (R - n)));
         if (!EXPORT) tl_mark(ctl, 8);
@@ -1228,35 +1432,35 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint32_t* s
     }
     // one walk per level-(L-2) cell (its 4 level-(L-1) children share the
     // path); K = 1 (L = 1) walks the level-(L-1) cells directly
-    const int G = (K >= 2) ? L - 2 : L - 1;              // walked level
-    const uint32_t ng = 1u << (2 * (G - R));               // walked cells in the subtree
+    const int Gk = (K >= 2) ? K - 2 : K - 1;               // walked tile level
+    const int G = R + Gk;
+    const uint32_t ng = 1u << (2 * Gk);                    // walked cells in the subtree
     const uint32_t per = (ng + kThreads - 1) / kThreads;
     const uint32_t a = threadIdx.x * per;
     const uint32_t b = min(ng, a + per);
-    const uint32_t loL1 = lo(L - 1, R);
-    // depth of the walk: first level <= G whose cell is not significant, or G + 1
+    const uint8_t* sL1 = sc + slo(K - 1);
+    // depth of the walk: first tile level <= Gk whose cell is not significant, or Gk + 1
     auto walk = [&](uint32_t t) -> int {
-        int n = R;
-        uint32_t off = 0, span = 1;
-        while (n <= G && sc[off + (t >> (2 * (G - n)))]) {
-            off += span;
-            span <<= 2;
-            ++n;
+        int k = 0;
+#pragma unroll
+        for (int kk = 0; kk < (KT ? KT : kMaxL); ++kk) {
+            if (kk > Gk || !sc[slo(kk) + (t >> (2 * (Gk - kk)))]) break;
+            k = kk + 1;
         }
-        return n;
+        return k;
     };
     unsigned ca = 0, cb = 0;
     for (uint32_t t = a; t < b; ++t) {
-        const int n = walk(t);
-        if (n <= G) {
-            cb += ((t & ((1u << (2 * (G - n))) - 1u)) == 0u) ? 1u : 0u;
+        const int k = walk(t);
+        if (k <= Gk) {
+            cb += ((t & ((1u << (2 * (Gk - k))) - 1u)) == 0u) ? 1u : 0u;
         } else if (G == L - 1) {
             ca += 4;
         } else {
-            for (uint32_t k = 0; k < 4; ++k) {
-                if (sc[loL1 + 4u * t + k]) ca += 4;
-                else cb += 1;
-            }
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(sL1 + 4u * t);
+            const unsigned s4 = __popc(w);
+            ca += 4 * s4;
+            cb += 4 - s4;
         }
     }
     unsigned total;
@@ -1268,7 +1472,11 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint32_t* s
     }
     auto emitA = [&](uint32_t m1) {  // the 4 level-L children of level-(L-1) cell m1
         const uint32_t z0 = zo::z_of(L, m1 << 2);
-        outA[oa] = z0; outA[oa + 1] = z0 + 1; outA[oa + 2] = z0 + 2; outA[oa + 3] = z0 + 3;
+        if (EXPORT) {
+            outA[oa] = z0; outA[oa + 1] = z0 + 1; outA[oa + 2] = z0 + 2; outA[oa + 3] = z0 + 3;
+        } else {  // list A offsets are multiples of 4
+            *reinterpret_cast<uint4*>(outA + oa) = make_uint4(z0, z0 + 1, z0 + 2, z0 + 3);
+        }
         oa += 4;
     };
     auto emitB = [&](uint32_t z) {
@@ -1277,35 +1485,31 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint32_t* s
     };
     const uint32_t gbase = j * ng;
     for (uint32_t t = a; t < b; ++t) {
-        const int n = walk(t);
+        const int k = walk(t);
         const uint32_t gm = gbase + t;
-        if (n <= G) {
-            if ((t & ((1u << (2 * (G - n))) - 1u)) == 0u) emitB(zo::z_of(n, gm >> (2 * (G - n))));
+        if (k <= Gk) {
+            if ((t & ((1u << (2 * (Gk - k))) - 1u)) == 0u) emitB(zo::z_of(R + k, gm >> (2 * (Gk - k))));
         } else if (G == L - 1) {
             emitA(gm);
         } else {
-            for (uint32_t k = 0; k < 4; ++k) {
-                const uint32_t m1 = 4u * gm + k;
-                if (sc[loL1 + 4u * t + k]) emitA(m1);
+            for (uint32_t q = 0; q < 4; ++q) {
+                const uint32_t m1 = 4u * gm + q;
+                if (sL1[4u * t + q]) emitA(m1);
                 else emitB(zo::z_of(L - 1, m1));
             }
         }
     }
-    if (!EXPORT) {
-        __syncthreads();
-        tl_mark(ctl, 8);
-    }
+    if (!EXPORT) tl_mark(ctl, 8);
 }
 
-template <bool EXPORT>
-__global__ void __launch_bounds__(kThreads) k_traverse(Params P, Ctl* ctl, int force) {
+template <bool EXPORT, int KT>
+__global__ void __launch_bounds__(kThreads, 8) k_traverse(Params P, Ctl* ctl, int force) {
     pdl_wait();
     pdl_trigger();
     if (!EXPORT && !force && !active(ctl, P)) return;
     if (!EXPORT) tl_start(ctl, 2);
-    extern __shared__ uint32_t smem3[];
-    __shared__ unsigned s_red[32];
-    traverse_tile<EXPORT>(P, ctl, P.tile_lo + blockIdx.x, smem3, s_red);
+    extern __shared__ __align__(16) uint8_t smem3[];
+    traverse_tile<EXPORT, KT>(P, ctl, P.tile_lo + blockIdx.x, smem3);
 }
 
 // =========================================================================== K5

@@ -49,7 +49,12 @@ struct swamp_gpu {
     int fv1_grid = 0;
     int fv1_minb = 2;  // occupancy variant of k_fv1 (SWAMP_FV1_MINB=3|4 for more CTAs/SM, with spills)
     int num_sms = 0;
-    size_t smem_k1 = 0, smem_k2 = 0, smem_k3 = 0;
+    size_t smem_k1 = 0, smem_k1s = 0, smem_k2 = 0, smem_k3 = 0;
+    // tile kernels, specialised for K = 6 (every L >= 6) or generic
+    void (*k1)(Params, Ctl*) = nullptr;
+    void (*k2)(Params, Ctl*, int, int) = nullptr;
+    void (*k3)(Params, Ctl*, int) = nullptr;
+    void (*k3x)(Params, Ctl*, int) = nullptr;
     cudaEvent_t ev[6] = {};
     std::string err;
     int64_t n_cells = 0;
@@ -143,11 +148,13 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
         for (int k = 1; k < 5; ++k) mark(k);
         return;
     }
-    launch_pdl(hwfv1::k_encode_tma, P.n_tiles, g->smem_k1 + g->smem_k1 / 33, s, P, g->ctl);
+    launch_pdl(g->k1, P.n_tiles, g->smem_k1s, s, P, g->ctl);
+    if (P.top_mode == 2) launch_pdl(hwfv1::k_encode_top<false>, 1, g->smem_k1, s, P, g->ctl);
     mark(1);
-    launch_pdl(hwfv1::k_band, P.n_tiles, g->smem_k2, s, P, g->ctl, 0);
+    const int do_top = P.top_mode == 1 ? 1 : 0;
+    launch_pdl(g->k2, P.n_tiles + do_top, g->smem_k2, s, P, g->ctl, 0, do_top);
     mark(2);
-    if (!P.fuse_k3) launch_pdl(hwfv1::k_traverse<false>, P.n_tiles, g->smem_k3, s, P, g->ctl, 0);
+    launch_pdl(g->k3, P.n_tiles, g->smem_k3, s, P, g->ctl, 0);
     mark(3);
     if (g->fv1_minb == 4)
         launch_pdl(hwfv1::k_fv1<false, 4>, g->fv1_grid, 0, s, P, g->ctl);
@@ -290,8 +297,6 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     if ((st = dalloc(g, &P.leaves_x, nf * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.tile_cnt, 2 * P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.tile_off, 3 * P.n_tiles * sizeof(uint32_t)))) return fail(st);
-    if ((st = dalloc(g, &P.tile_lvl, P.n_tiles * sizeof(uint32_t)))) return fail(st);
-    if ((st = dalloc(g, &P.tile_src, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &g->ctl, sizeof(Ctl)))) return fail(st);
     // peer tables: self only (a partitioned group fills in every partition)
     for (int b = 0; b < 2; ++b) {
@@ -359,17 +364,49 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         }
     }
 
-    g->smem_k1 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u) * (sizeof(double4) + 1);
+    // shared memory per kernel (hwfv1_kernels.cuh layouts)
     {
-        const size_t top = ((1u << (2 * (P.R + 1))) - 1u) / 3u;  // cells on levels 0..R
-        g->smem_k2 = std::max<size_t>(6 * (((1u << (2 * P.K)) - 1u) / 3u),
-                                      ((4 * top + 15) & ~size_t(15)) + 8 * (size_t(1) << (2 * P.R)));
-        if (g->smem_k2 > 48 * 1024 &&
-            cudaFuncSetAttribute(hwfv1::k_band, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(g->smem_k2)) != cudaSuccess)
-            return fail(SWAMP_E_CUDA);
+        const int Ki = P.K;
+        const size_t K = P.K, R = P.R, nt = P.n_tiles;
+        const size_t ncell = ((size_t(1) << (2 * K)) - 1) / 3;      // subtree cells, levels R..L-1
+        const size_t fb = P.fbase[R];                                // top flag bytes (levels < R)
+        const size_t ltop = ((size_t(1) << (2 * R)) - 1) / 3;        // top cells (levels < R)
+        const size_t sl = hwfv1::slo(Ki);
+        if (Ki == 6) {
+            g->k1 = hwfv1::k_encode_step<6>;
+            g->k2 = hwfv1::k_band<6>;
+            g->k3 = hwfv1::k_traverse<false, 6>;
+            g->k3x = hwfv1::k_traverse<true, 6>;
+        } else {
+            g->k1 = hwfv1::k_encode_step<0>;
+            g->k2 = hwfv1::k_band<0>;
+            g->k3 = hwfv1::k_traverse<false, 0>;
+            g->k3x = hwfv1::k_traverse<true, 0>;
+        }
+        g->smem_k1 = ncell * (sizeof(double4) + 1);                  // k_encode<true> / k_encode_top
+        g->smem_k1s = 32 * (((size_t(1) << (2 * (K - 1))) - 1) / 3) + 2 * sl;
+        P.top_mode = (R == 0) ? 0 : (R <= 6 ? 1 : 2);
+        const size_t k2_tile = 2 * sl;
+        const size_t k2_top = P.top_mode == 1 ? 32 * ltop + 2 * fb : 0;
+        g->smem_k2 = std::max(k2_tile, k2_top);
+        const size_t ftop = (fb + nt + 15) & ~size_t(15);
+        g->smem_k3 = 2 * sl + ftop + 2 * fb + (nt <= 1024 ? 8 * nt : 0) + 4 * ncell;
+        struct {
+            const void* f;
+            size_t bytes;
+        } attrs[] = {{reinterpret_cast<const void*>(g->k1), g->smem_k1s},
+                     {reinterpret_cast<const void*>(hwfv1::k_encode<true>), g->smem_k1},
+                     {reinterpret_cast<const void*>(hwfv1::k_encode_top<true>), g->smem_k1},
+                     {reinterpret_cast<const void*>(hwfv1::k_encode_top<false>), g->smem_k1},
+                     {reinterpret_cast<const void*>(g->k2), g->smem_k2},
+                     {reinterpret_cast<const void*>(g->k3), g->smem_k3},
+                     {reinterpret_cast<const void*>(g->k3x), g->smem_k3}};
+        for (auto& a : attrs)
+            if (a.bytes > 48 * 1024 &&
+                cudaFuncSetAttribute(a.f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(a.bytes)) !=
+                    cudaSuccess)
+                return fail(SWAMP_E_CUDA);
     }
-    g->smem_k3 = static_cast<size_t>(((1u << (2 * P.K)) - 1u) / 3u) * 6;
     {
         if (const char* e = std::getenv("SWAMP_FV1_MINB")) g->fv1_minb = std::max(2, std::min(4, std::atoi(e)));
         int occ = 0;
@@ -382,15 +419,6 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         g->fv1_grid = std::max(1, occ) * g->num_sms;
     }
     g->n_cells = static_cast<int64_t>(off);
-    // K3 fused into K2 (its CTAs wait for the last CTA instead of a new
-    // launch) is possible when every K2 CTA can be resident at once;
-    // SWAMP_FUSE_K3=1 enables it
-    {
-        int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_band, kThreads, g->smem_k2);
-        const char* e = std::getenv("SWAMP_FUSE_K3");  // opt-in: measured slower on B200 (L=11)
-        P.fuse_k3 = (G == 1 && P.n_tiles <= occ * g->num_sms && e && e[0] == '1') ? 1 : 0;
-    }
     return SWAMP_OK;
 }
 
@@ -418,8 +446,8 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
         cudaMemsetAsync(P.sig[1], 1, foff, s);
         cudaMemsetAsync(P.pre, 1, foff, s);
         // leaf list = every finest cell in Morton order (for exports)
-        hwfv1::k_band<<<P.n_tiles, kThreads, g->smem_k2, s>>>(P, g->ctl, 1);
-        hwfv1::k_traverse<false><<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 1);
+        g->k2<<<P.n_tiles, kThreads, g->smem_k2, s>>>(P, g->ctl, 1, 0);
+        g->k3<<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 1);
         cudaMemcpyAsync(P.cells[1], P.cells[0], off * sizeof(double4), cudaMemcpyDeviceToDevice, s);
         hwfv1::k_cfl_init<<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl, 1);
     } else {
@@ -427,8 +455,8 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
         // encode + DEM mask, band + closure, traversal; no decode at t = 0
         cudaMemsetAsync(P.sig[0], 1, foff, s);
         hwfv1::k_encode<true><<<P.n_tiles, kThreads, g->smem_k1, s>>>(P, g->ctl);
-        hwfv1::k_band<<<P.n_tiles, kThreads, g->smem_k2, s>>>(P, g->ctl, 1);
-        hwfv1::k_traverse<false><<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 1);
+        g->k2<<<P.n_tiles, kThreads, g->smem_k2, s>>>(P, g->ctl, 1, 0);
+        g->k3<<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 1);
         // both buffers hold the full hierarchy; the current tree becomes "previous"
         cudaMemcpyAsync(P.cells[1], P.cells[0], off * sizeof(double4), cudaMemcpyDeviceToDevice, s);
         const int one = 1;
@@ -492,19 +520,18 @@ int group_sync(swamp_gpu* grp) {
 
 void group_enqueue_step(swamp_gpu* grp) {
     group_phase(grp, [](swamp_gpu* q) {
-        hwfv1::k_encode_tma<<<q->P.tiles_per_part, kThreads, q->smem_k1 + q->smem_k1 / 33, q->stream>>>(q->P, q->ctl);
+        q->k1<<<q->P.tiles_per_part, kThreads, q->smem_k1s, q->stream>>>(q->P, q->ctl);
+    });
+    if (grp->parts[0]->P.top_mode == 2)
+        group_phase(grp, [](swamp_gpu* q) {
+            hwfv1::k_encode_top<false><<<1, kThreads, q->smem_k1, q->stream>>>(q->P, q->ctl);
+        });
+    group_phase(grp, [](swamp_gpu* q) {
+        const int do_top = q->P.top_mode == 1 ? 1 : 0;
+        q->k2<<<q->P.tiles_per_part + do_top, kThreads, q->smem_k2, q->stream>>>(q->P, q->ctl, 0, do_top);
     });
     group_phase(grp, [](swamp_gpu* q) {
-        hwfv1::k_encode_top<false><<<1, kThreads, q->smem_k1, q->stream>>>(q->P, q->ctl);
-    });
-    group_phase(grp, [](swamp_gpu* q) {
-        hwfv1::k_band<<<q->P.tiles_per_part, kThreads, q->smem_k2, q->stream>>>(q->P, q->ctl, 0);
-    });
-    group_phase(grp, [](swamp_gpu* q) {
-        hwfv1::k_band_top<<<1, kThreads, q->smem_k2, q->stream>>>(q->P, q->ctl, 0);
-    });
-    group_phase(grp, [](swamp_gpu* q) {
-        hwfv1::k_traverse<false><<<q->P.tiles_per_part, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 0);
+        q->k3<<<q->P.tiles_per_part, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 0);
     });
     group_phase(grp, [](swamp_gpu* q) {
         hwfv1::k_fv1<false, 2, true><<<q->fv1_grid, kThreads, 0, q->stream>>>(q->P, q->ctl);
@@ -558,12 +585,6 @@ int create_group(const swamp_config* cfg, const double* h, const double* qx, con
             q->P.ptile_cnt[k] = r->P.tile_cnt;
             q->P.pctl[k] = r->ctl;
         }
-    for (swamp_gpu* q : grp->parts) {
-        cudaSetDevice(q->device);
-        if (q->smem_k2 > 48 * 1024)
-            cudaFuncSetAttribute(hwfv1::k_band_top, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(q->smem_k2));
-    }
     // initialise, phase by phase across the partitions
     static const int kOne = 1;
     group_phase(grp, [](swamp_gpu* q) {
@@ -576,13 +597,10 @@ int create_group(const swamp_config* cfg, const double* h, const double* qx, con
         hwfv1::k_encode_top<true><<<1, kThreads, q->smem_k1, q->stream>>>(q->P, q->ctl);
     });
     group_phase(grp, [](swamp_gpu* q) {
-        hwfv1::k_band<<<q->P.tiles_per_part, kThreads, q->smem_k2, q->stream>>>(q->P, q->ctl, 1);
+        q->k2<<<q->P.tiles_per_part, kThreads, q->smem_k2, q->stream>>>(q->P, q->ctl, 1, 0);
     });
     group_phase(grp, [](swamp_gpu* q) {
-        hwfv1::k_band_top<<<1, kThreads, q->smem_k2, q->stream>>>(q->P, q->ctl, 1);
-    });
-    group_phase(grp, [](swamp_gpu* q) {
-        hwfv1::k_traverse<false><<<q->P.tiles_per_part, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 1);
+        q->k3<<<q->P.tiles_per_part, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 1);
     });
     group_phase(grp, [](swamp_gpu* q) {
         cudaMemcpyAsync(q->P.cells[1], q->P.cells[0], static_cast<size_t>(q->n_cells) * sizeof(double4),
@@ -633,23 +651,29 @@ int group_copy_leaves(swamp_gpu* grp, uint32_t* leaves, uint32_t* nw, uint32_t* 
     if (cap < static_cast<int64_t>(N)) return SWAMP_E_ARG;
     for (swamp_gpu* q : grp->parts) {
         cudaSetDevice(q->device);
-        hwfv1::k_traverse<true><<<q->P.tiles_per_part, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 1);
+        q->k3x<<<q->P.tiles_per_part, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 1);
     }
     if ((st = group_sync(grp))) return st;
     const uint32_t nt = static_cast<uint32_t>(p0->P.n_tiles);
-    std::vector<uint32_t> toff(3 * static_cast<size_t>(nt));
-    cudaSetDevice(p0->device);
-    if (cudaMemcpy(toff.data(), p0->P.tile_off, toff.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
-        return SWAMP_E_CUDA;
-    for (size_t k = 1; k < grp->parts.size(); ++k) {  // gather the Morton-ordered slices into partition 0
+    // each partition's K3 recorded its first subtree's export offset at tile_off[2 nt + tile_lo]
+    const size_t G = grp->parts.size();
+    std::vector<uint32_t> lo(G + 1, N);
+    for (size_t k = 0; k < G; ++k) {
         swamp_gpu* q = grp->parts[k];
-        const uint32_t lo = toff[2 * nt + q->P.tile_lo];
-        const uint32_t hi = (q->P.tile_hi < nt) ? toff[2 * nt + q->P.tile_hi] : N;
-        if (hi > lo &&
-            cudaMemcpyPeer(p0->P.leaves_x + lo, p0->device, q->P.leaves_x + lo, q->device,
-                           (hi - lo) * sizeof(uint32_t)) != cudaSuccess)
+        cudaSetDevice(q->device);
+        if (cudaMemcpy(&lo[k], q->P.tile_off + 2 * nt + q->P.tile_lo, sizeof(uint32_t), cudaMemcpyDeviceToHost) !=
+            cudaSuccess)
             return SWAMP_E_CUDA;
     }
+    for (size_t k = 1; k < G; ++k) {  // gather the Morton-ordered slices into partition 0
+        swamp_gpu* q = grp->parts[k];
+        const uint32_t a = lo[k], b = lo[k + 1];
+        if (b > a &&
+            cudaMemcpyPeer(p0->P.leaves_x + a, p0->device, q->P.leaves_x + a, q->device, (b - a) * sizeof(uint32_t)) !=
+                cudaSuccess)
+            return SWAMP_E_CUDA;
+    }
+    cudaSetDevice(p0->device);
     return copy_leaves_x(p0, N, leaves, nw, ne, nn, ns);
 }
 
@@ -803,7 +827,7 @@ int swamp_gpu_copy_leaves(swamp_gpu* g, uint32_t* leaves, uint32_t* nw, uint32_t
     if (cap < static_cast<int64_t>(N)) return SWAMP_E_ARG;
     // Morton-ordered LeafAssembly of the current tree (the hot path keeps the
     // level-L leaves first)
-    hwfv1::k_traverse<true><<<g->P.n_tiles, kThreads, g->smem_k3, g->stream>>>(g->P, g->ctl, 1);
+    g->k3x<<<g->P.n_tiles, kThreads, g->smem_k3, g->stream>>>(g->P, g->ctl, 1);
     CK(cudaStreamSynchronize(g->stream));
     return copy_leaves_x(g, N, leaves, nw, ne, nn, ns);
 }
