@@ -41,30 +41,33 @@ enum Stage : int { kStageImport = 0, kStageEncode = 1, kStageBand = 2, kStageTra
 enum ErrCode : int { kErrNone = 0, kErrNonFinite = -3, kErrDt = -4 };
 
 struct Ctl {
+    // ---- line 0: read once per CTA (cta_head) by every kernel of a step
     double t;        // current simulation time
     double dt;       // dt of the next step
     double t_next;   // time after the next step (exact stop time when clipped)
     double dt_used;  // dt of the last step taken
-    unsigned long long rate_bits[2];  // CFL max-rate accumulators (bits of a non-negative double), by step parity
-    unsigned long long smax_bits[4];
     long long step;
-    unsigned long long cnt_tree;    // cells re-encoded by the last K1
-    unsigned long long cnt_new;     // newly significant cells decoded by the last K3
+    int parity;                     // current cell buffer / previous-tree flags
     uint32_t n_leaves;              // leaves of the grid built by the last K2/K3
     uint32_t n_leaves_A;            // of which level-L leaves (listed first, in sibling quadruples)
     uint32_t a_lo, a_hi, b_lo, b_hi; // this partition's slices of the A (level-L) and B lists
     uint32_t n_leaves_used;         // leaves the last FV1 updated
-    int parity;                     // current cell buffer / previous-tree flags
+    // ---- atomically updated fields, each on its own 128-B line so that the
+    //      per-CTA atomics do not queue in front of the line-0 reads
+    alignas(128) unsigned long long rate_bits[2];  // CFL max-rate accumulators (bits of a non-negative double), by step parity
+    unsigned int done_k1, done_k5;
+    alignas(128) unsigned long long cnt_tree;    // cells re-encoded by the last K1
+    alignas(128) unsigned long long cnt_new;     // newly significant cells decoded by the last K3
+    alignas(128) unsigned long long smax_bits[4];
     int err_code;
     uint32_t err_z;
     int err_q;
     int err_stage;
-    unsigned int done_k1, done_k5;
-    unsigned long long dbg[16];     // per-phase globaltimer stamps of probe CTAs (diagnostics)
-    // stage timeline (globaltimer ns), double-buffered by step parity: for
-    // kernel k (K1, K2, K3, K5) [3k] = ~(first CTA start), [3k+1] = last CTA
-    // elected, [3k+2] = last CTA done (atomicMax; K5 zeroes the next buffer)
-    unsigned long long tl[2][12];
+    alignas(128) unsigned long long dbg[16];     // per-phase globaltimer stamps of probe CTAs (diagnostics)
+    // stage timeline (globaltimer ns), double-buffered by step parity, one
+    // line per kernel k (K1, K2, K3, K5): [0] = ~(first CTA start), [2] = last
+    // CTA done (atomicMax); K5 zeroes the next buffer
+    alignas(128) unsigned long long tl[2][4][16];
 };
 
 // Programmatic dependent launch: every kernel of the step is launched with
@@ -80,12 +83,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-__device__ __forceinline__ int tl_buf(const Ctl* c) { return static_cast<int>(c->step & 1); }
-__device__ __forceinline__ void tl_start(Ctl* c, int k) {
-    if (threadIdx.x == 0) atomicMax(&c->tl[tl_buf(c)][3 * k], ~gtimer());
+__device__ __forceinline__ void tl_start(Ctl* c, int buf, int k) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) atomicMax(&c->tl[buf][k][0], ~gtimer());
 }
-__device__ __forceinline__ void tl_mark(Ctl* c, int slot) {
-    if (threadIdx.x == 0) atomicMax(&c->tl[tl_buf(c)][slot], gtimer());
+__device__ __forceinline__ void tl_end(Ctl* c, int buf, int k) {
+    if (threadIdx.x == 0) atomicMax(&c->tl[buf][k][2], gtimer());
 }
 
 struct Params {
@@ -128,6 +130,24 @@ struct Params {
     uint32_t* ptile_cnt[kMaxParts];
     Ctl* pctl[kMaxParts];
 };
+
+// offset of level k in a padded flag layout (every level 16-B aligned): the
+// global flag arrays (== Params::fbase, host-checked) and the per-tile
+// shared-memory slices (k = n - R) use the same one,
+// every level 16-B aligned: 0, 16, 32, 48, 112, 368, 1392, ... ; slo(K) = size
+__host__ __device__ __forceinline__ uint32_t slo(int k) {
+    return k < 3 ? 16u * static_cast<uint32_t>(k) : 27u + (0x55555555u >> (32 - 2 * k));  // 48 + (4^k - 64) / 3
+}
+
+// double4 offset of level n in a cell buffer: every level slice rounded up
+// to 8 cells (256 B): 0, 8, 16, 32, 96, 352, ... (host-checked == Params::base)
+__host__ __device__ __forceinline__ unsigned long long cbase(int n) {
+    return n < 2 ? 8ull * static_cast<unsigned>(n) : 11ull + (0x55555555u >> (32 - 2 * n));  // 16 + (4^n - 16) / 3
+}
+// 1 / dx_n = 2^n / W exactly: the exponent of 1/W plus n (host-checked == Params::inv_dx)
+__device__ __forceinline__ double inv_dx_of(const Params& P, int n) {
+    return __longlong_as_double(__double_as_longlong(P.inv_dx[0]) + (static_cast<long long>(n) << 52));
+}
 
 // ------------------------------------------------------------------ memory ops
 __device__ __forceinline__ double4 ld4(const double4* p) {
@@ -176,12 +196,12 @@ __device__ __forceinline__ int owner_of(const Params& P, int n, uint32_t m) {
     return static_cast<int>(t / P.tiles_per_part);
 }
 __device__ __forceinline__ double4* cell_ptr(const Params& P, int buf, int n, uint32_t m) {
-    return P.pcells[owner_of(P, n, m)][buf] + P.base[n] + m;
+    return P.pcells[owner_of(P, n, m)][buf] + cbase(n) + m;
 }
 // significance byte of (n, m) in copy `which`; levels above R are replicated
 __device__ __forceinline__ uint8_t sig_at(const Params& P, int which, int n, uint32_t m) {
     const int g = (n < P.R) ? P.part : owner_of(P, n, m);
-    return P.psig[g][which][P.fbase[n] + m];
+    return P.psig[g][which][slo(n) + m];
 }
 
 __device__ __forceinline__ void report_error(Ctl* c, int code, uint32_t z, int q, int stage) {
@@ -234,8 +254,50 @@ __device__ __forceinline__ Enc encode_children(const double4 c[4], const Params&
     return e;
 }
 
+// encode + flow significance with the level's thresholds from a staged table
+// thr4 = {thr[0][n], thr[1][n], thr[2][n], tau[n]} (same arithmetic as
+// encode_children<false>)
+__device__ __forceinline__ Enc encode_children_t(const double4 c[4], const double* thr4) {
+    const Red h = red4(c[0].x, c[1].x, c[2].x, c[3].x);
+    const Red qx = red4(c[0].y, c[1].y, c[2].y, c[3].y);
+    const Red qy = red4(c[0].z, c[1].z, c[2].z, c[3].z);
+    const double a = c[0].w + c[1].w, b = c[2].w + c[3].w;
+    Enc e;
+    e.flow = sig_q(h.dmax, thr4[0]) || sig_q(qx.dmax, thr4[1]) || sig_q(qy.dmax, thr4[2]);
+    e.par = make_double4(h.par, qx.par, qy.par, 0.25 * (a + b));
+    e.zflag = false;
+    return e;
+}
+// per-level thresholds staged in shared memory (indexed constant-bank loads
+// with a runtime level miss the constant cache on the critical path)
+__device__ __forceinline__ void stage_thresholds(const Params& P, double (*s_thr)[4]) {
+    const int t = static_cast<int>(threadIdx.x);
+    if (t < 4 * P.L) {
+        const int n = t >> 2, q = t & 3;
+        s_thr[n][q] = q < 3 ? P.thr[q][n] : P.tau[n];
+    }
+}
+
 __device__ __forceinline__ bool active(const Ctl* c, const Params& P) {
     return *((volatile const double*)&c->t) < P.t_end;
+}
+
+// Per-CTA view of the control block: thread 0 reads t / parity / step once
+// and broadcasts them through shared memory, so a grid of 1000+ CTAs makes
+// one request per CTA to the control line instead of one per warp.
+struct Head {
+    int active, parity, buf;  // buf = timeline buffer (step parity)
+};
+__device__ __forceinline__ Head cta_head(const Ctl* c, const Params& P, bool force) {
+    __shared__ int s_h[3];
+    if (threadIdx.x == 0) {
+        const double t = *((volatile const double*)&c->t);
+        s_h[0] = (force || t < P.t_end) ? 1 : 0;
+        s_h[1] = *((volatile const int*)&c->parity);
+        s_h[2] = static_cast<int>(*((volatile const long long*)&c->step) & 1);
+    }
+    __syncthreads();
+    return {s_h[0], s_h[1], s_h[2]};
 }
 
 // Block-wide sum of unsigned values (256 threads).
@@ -346,11 +408,7 @@ __device__ __forceinline__ void cp_async16(void* s, const void* g) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// shared-memory offset of tile level k (k = n - R) in a per-tile flag slice,
-// every level 16-B aligned: 0, 16, 32, 48, 112, 368, 1392, ... ; slo(K) = size
-__host__ __device__ __forceinline__ uint32_t slo(int k) {
-    return k <= 3 ? 16u * static_cast<uint32_t>(k) : 48u + ((1u << (2 * k)) - 64u) / 3u;
-}
+
 
 // stage `bytes` (a multiple of 16, both ends 16-B aligned) into shared memory
 __device__ __forceinline__ void stage16(void* s, const void* g, uint32_t bytes) {
@@ -364,11 +422,11 @@ __device__ __forceinline__ void stage16(void* s, const void* g, uint32_t bytes) 
 __device__ __forceinline__ uint8_t stage_tile_flags(uint8_t* s, const uint8_t* base, const Params& P, uint32_t j) {
     const int K = P.K, R = P.R;
     uint8_t v0 = 0;
-    if (threadIdx.x == 0) v0 = base[P.fbase[R] + j];
-    if (K > 1 && threadIdx.x == 32) cp_async4(s + slo(1), base + P.fbase[R + 1] + 4ull * j);
+    if (threadIdx.x == 0) v0 = base[slo(R) + j];
+    if (K > 1 && threadIdx.x == 32) cp_async4(s + slo(1), base + slo(R + 1) + 4ull * j);
     for (int k = 2; k < K; ++k) {
         const uint32_t cnt = 1u << (2 * k);
-        stage16(s + slo(k), base + P.fbase[R + k] + static_cast<unsigned long long>(j) * cnt, cnt);
+        stage16(s + slo(k), base + slo(R + k) + static_cast<unsigned long long>(j) * cnt, cnt);
     }
     return v0;
 }
@@ -419,9 +477,9 @@ __device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4*
     const uint32_t b1 = 32u * ipw * w, b2 = 8u * ipw * w, b3 = 2u * ipw * w;
     if (b1 >= n1) return 0;
     const int L1 = T, L2 = T - 1, L3 = T - 2;
-    const unsigned long long g1 = P.fbase[L1] + static_cast<unsigned long long>(j) * n1;
-    const unsigned long long g2 = P.fbase[L2] + static_cast<unsigned long long>(j) * n2;
-    const unsigned long long g3 = P.fbase[L3] + static_cast<unsigned long long>(j) * n3;
+    const unsigned long long g1 = slo(L1) + static_cast<unsigned long long>(j) * n1;
+    const unsigned long long g2 = slo(L2) + static_cast<unsigned long long>(j) * n2;
+    const unsigned long long g3 = slo(L3) + static_cast<unsigned long long>(j) * n3;
     // previous-tree / DEM flags: words for level T (4 cells per lane), bytes above
     uint32_t f1w = 0, d1w = 0;
     if (b1 + 4u * lane < n1 && lane < 8 * ipw) {
@@ -436,7 +494,7 @@ __device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4*
     if (lane < 2 * ipw && b3 + lane < n3) {
         f3 = INIT ? 1u : sigp[g3 + b3 + lane];
         d3 = INIT ? 0u : P.dem[g3 + b3 + lane];
-        if (L3 > R) f4 = INIT ? 1u : sigp[P.fbase[L3 - 1] + static_cast<unsigned long long>(j) * (n3 >> 2) + ((b3 + lane) >> 2)];
+        if (L3 > R) f4 = INIT ? 1u : sigp[slo(L3 - 1) + static_cast<unsigned long long>(j) * (n3 >> 2) + ((b3 + lane) >> 2)];
     }
     const bool zero1 = 0.0 >= P.tau[L1], zero2 = 0.0 >= P.tau[L2], zero3 = 0.0 >= P.tau[L3];
     unsigned tree = 0;
@@ -459,13 +517,13 @@ __device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4*
         // of previous-tree leaves whose parent is re-encoded here
         double4 ch[4];
         if (sp1) {
-            const double4* cp = buf + P.base[L1 + 1] + (static_cast<unsigned long long>(gm1) << 2);
+            const double4* cp = buf + cbase(L1 + 1) + (static_cast<unsigned long long>(gm1) << 2);
             ch[0] = ld4_nc(cp); ch[1] = ld4_nc(cp + 1); ch[2] = ld4_nc(cp + 2); ch[3] = ld4_nc(cp + 3);
         }
         double4 v1 = make_double4(0.0, 0.0, 0.0, 0.0), v2 = v1, v3 = v1;
-        if (ok1 && !sp1 && sp2) v1 = ld4(buf + P.base[L1] + gm1);
-        if (ok2 && !sp2 && sp3) v2 = ld4(buf + P.base[L2] + gm2);
-        if (ok3 && !sp3 && sp4 && L3 > R) v3 = ld4(buf + P.base[L3] + gm3);
+        if (ok1 && !sp1 && sp2) v1 = ld4(buf + cbase(L1) + gm1);
+        if (ok2 && !sp2 && sp3) v2 = ld4(buf + cbase(L2) + gm2);
+        if (ok3 && !sp3 && sp4 && L3 > R) v3 = ld4(buf + cbase(L3) + gm3);
         // level T
         {
             bool flow = zero1, zf = false;
@@ -474,7 +532,7 @@ __device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4*
                 v1 = e.par;
                 flow = e.flow;
                 zf = e.zflag;
-                st4(buf + P.base[L1] + gm1, v1);
+                st4(buf + cbase(L1) + gm1, v1);
                 ++tree;
             }
             if (ok1) {
@@ -492,7 +550,7 @@ __device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4*
                     v2 = e.par;
                     flow = e.flow;
                     zf = e.zflag;
-                    st4(buf + P.base[L2] + gm2, v2);
+                    st4(buf + cbase(L2) + gm2, v2);
                     ++tree;
                 }
                 const bool d = INIT ? zf : dm2;
@@ -509,7 +567,7 @@ __device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4*
                     v3 = e.par;
                     flow = e.flow;
                     zf = e.zflag;
-                    st4(buf + P.base[L3] + gm3, v3);
+                    st4(buf + cbase(L3) + gm3, v3);
                     ++tree;
                 }
                 const bool d = INIT ? zf : dm3;
@@ -531,12 +589,13 @@ template <bool INIT>
 __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
     pdl_wait();
     pdl_trigger();
-    if (!INIT && !active(ctl, P)) return;
-    tl_start(ctl, 0);
+    const Head hd = cta_head(ctl, P, INIT);
+    if (!hd.active) return;
+    tl_start(ctl, hd.buf, 0);
     extern __shared__ double4 sv[];
     __shared__ unsigned s_red[32];
     __shared__ int s_last;
-    const int p = ctl->parity;
+    const int p = hd.parity;
     double4* buf = P.cells[p];
     const uint8_t* sigp = P.sig[p];
     const int L = P.L, R = P.R, K = P.K;
@@ -559,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
     for (int n = R; n <= top_n + (warp_path ? 0 : 1); ++n) {
         const uint32_t cnt = 1u << (2 * (n - R));
         for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads)
-            sfl[lo(n, R) + pi] = INIT ? 1 : sigp[P.fbase[n] + j * cnt + pi];
+            sfl[lo(n, R) + pi] = INIT ? 1 : sigp[slo(n) + j * cnt + pi];
     }
     __syncthreads();
     if (!INIT) {
@@ -567,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
             const uint32_t cnt = 1u << (2 * (n - R));
             for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
                 const uint32_t li = lo(n, R) + pi;
-                if (!sfl[li] && sfl[lo(n - 1, R) + (pi >> 2)]) sv[li] = ld4(buf + P.base[n] + j * cnt + pi);
+                if (!sfl[li] && sfl[lo(n - 1, R) + (pi >> 2)]) sv[li] = ld4(buf + cbase(n) + j * cnt + pi);
             }
         }
     }
@@ -579,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
             const int n = L - 1;
             const uint32_t cnt = 1u << (2 * (n - R));
             const bool zero = 0.0 >= P.tau[n];
-            const unsigned long long g = P.fbase[n] + static_cast<unsigned long long>(j) * cnt;
+            const unsigned long long g = slo(n) + static_cast<unsigned long long>(j) * cnt;
             for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads) {
                 const uint32_t f = *reinterpret_cast<const uint32_t*>(sigp + g + q);
                 const uint32_t d = *reinterpret_cast<const uint32_t*>(P.dem + g + q);
@@ -597,15 +656,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
         for (uint32_t pi = threadIdx.x; pi < npar; pi += kThreads) {
             const uint32_t pm = pbase + pi;
             const bool sp = sfl[lo(n, R) + pi] != 0;
-            const uint8_t d0 = INIT ? 0 : P.dem[P.fbase[n] + pm];
+            const uint8_t d0 = INIT ? 0 : P.dem[slo(n) + pm];
             bool flow, zf = false;
             if (sp) {
-                const double4* cp = buf + P.base[L] + (static_cast<unsigned long long>(pm) << 2);
+                const double4* cp = buf + cbase(L) + (static_cast<unsigned long long>(pm) << 2);
                 const double4 c[4] = {ld4_nc(cp), ld4_nc(cp + 1), ld4_nc(cp + 2), ld4_nc(cp + 3)};
                 const Enc e = encode_children<INIT>(c, P, n);
                 flow = e.flow;
                 zf = e.zflag;
-                st4(buf + P.base[n] + pm, e.par);
+                st4(buf + cbase(n) + pm, e.par);
                 if (n > R) sv[lo(n, R) + pi] = e.par;
                 ++tree;
             } else {
@@ -614,9 +673,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
             uint8_t d = d0;
             if (INIT) {
                 d = zf ? 1 : 0;
-                P.dem[P.fbase[n] + pm] = d;
+                P.dem[slo(n) + pm] = d;
             }
-            P.pre[P.fbase[n] + pm] = (flow || d) ? 1 : 0;
+            P.pre[slo(n) + pm] = (flow || d) ? 1 : 0;
         }
     }
     __syncthreads();
@@ -628,7 +687,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
         for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
             const uint32_t pm = pb + pi;
             const bool sp = sfl[lo(n, R) + pi] != 0;
-            const uint8_t d0 = INIT ? 0 : P.dem[P.fbase[n] + pm];
+            const uint8_t d0 = INIT ? 0 : P.dem[slo(n) + pm];
             bool flow, zf = false;
             if (sp) {
                 const uint32_t c0 = lo(n + 1, R) + 4u * pi;
@@ -636,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
                 const Enc e = encode_children<INIT>(c, P, n);
                 flow = e.flow;
                 zf = e.zflag;
-                st4(buf + P.base[n] + pm, e.par);
+                st4(buf + cbase(n) + pm, e.par);
                 if (n > R) sv[lo(n, R) + pi] = e.par;
                 ++tree;
             } else {
@@ -645,9 +704,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
             uint8_t d = d0;
             if (INIT) {
                 d = zf ? 1 : 0;
-                P.dem[P.fbase[n] + pm] = d;
+                P.dem[slo(n) + pm] = d;
             }
-            P.pre[P.fbase[n] + pm] = (flow || d) ? 1 : 0;
+            P.pre[slo(n) + pm] = (flow || d) ? 1 : 0;
         }
         __syncthreads();
     }
@@ -656,9 +715,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
     if (threadIdx.x == 0 && tsum) atomicAdd(&ctl->cnt_tree, (unsigned long long)tsum);
     if (P.G > 1) return;  // partitioned: k_encode_top runs after all partitions' subtrees
     if (!last_block(&ctl->done_k1, &s_last)) return;
-    tl_mark(ctl, 1);
     encode_top<INIT>(P, ctl, sv, s_red);
-    tl_mark(ctl, 2);
+    tl_end(ctl, hd.buf, 0);
 }
 
 template <bool INIT>
@@ -686,7 +744,7 @@ __device__ void encode_top(const Params& P, Ctl* ctl, double4* sv, unsigned* s_r
         const uint32_t cnt = 1u << (2 * n);
         const bool kids_in_smem = top_smem && n < R - 1;
         for (uint32_t pm = threadIdx.x; pm < cnt; pm += kThreads) {
-            const bool sp = INIT || sigp[P.fbase[n] + pm];
+            const bool sp = INIT || sigp[slo(n) + pm];
             bool flow, zf = false;
             if (sp) {
                 double4 c[4];
@@ -701,21 +759,21 @@ __device__ void encode_top(const Params& P, Ctl* ctl, double4* sv, unsigned* s_r
                 const Enc e = encode_children<INIT>(c, P, n);
                 flow = e.flow;
                 zf = e.zflag;
-                st4(buf + P.base[n] + pm, e.par);
+                st4(buf + cbase(n) + pm, e.par);
                 if (top_smem) sv[lo(n, 0) + pm] = e.par;
                 ++ttop;
             } else {
                 flow = 0.0 >= P.tau[n];
-                if (top_smem && n > 0 && sigp[P.fbase[n - 1] + (pm >> 2)]) sv[lo(n, 0) + pm] = ld4_cg(cell_ptr(P, p, n, pm));
+                if (top_smem && n > 0 && sigp[slo(n - 1) + (pm >> 2)]) sv[lo(n, 0) + pm] = ld4_cg(cell_ptr(P, p, n, pm));
             }
             uint8_t d;
             if (INIT) {
                 d = zf ? 1 : 0;
-                P.dem[P.fbase[n] + pm] = d;
+                P.dem[slo(n) + pm] = d;
             } else {
-                d = P.dem[P.fbase[n] + pm];
+                d = P.dem[slo(n) + pm];
             }
-            P.pre[P.fbase[n] + pm] = (flow || d) ? 1 : 0;
+            P.pre[slo(n) + pm] = (flow || d) ? 1 : 0;
         }
         __threadfence_block();
         __syncthreads();
@@ -739,14 +797,24 @@ __device__ void encode_top(const Params& P, Ctl* ctl, double4* sv, unsigned* s_r
 // then encoded from shared memory. No last-CTA tail: levels < R are encoded
 // by an extra CTA of K2 (encode_top_staged).
 template <int KT>
-__global__ void __launch_bounds__(kThreads) k_encode_step(Params P, Ctl* ctl) {
+__global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl) {
     pdl_wait();
     pdl_trigger();
-    if (!active(ctl, P)) return;
-    tl_start(ctl, 0);
+    const unsigned long long t_entry = gtimer();
+    __shared__ __align__(8) unsigned long long mbar;
+    if (threadIdx.x == 0) mbar_init(&mbar, 1);
+    const Head hd = cta_head(ctl, P, false);  // (its barrier also publishes the mbarrier init)
+    if (!hd.active) return;
+    tl_start(ctl, hd.buf, 0);
+    const int probe = (blockIdx.x == 0) ? 0 : ((blockIdx.x == gridDim.x - 1) ? 8 : -1);
+    auto stamp = [&](int k) {
+        if (probe >= 0 && threadIdx.x == 0) ctl->dbg[probe + k] = (k == 7) ? t_entry : gtimer();
+    };
+    stamp(7);
     extern __shared__ __align__(16) uint8_t sm1[];
     __shared__ unsigned s_red[32];
-    const int p = ctl->parity;
+    __shared__ double s_thr[kMaxL][4];
+    const int p = hd.parity;
     double4* buf = P.cells[p];
     const uint8_t* sigp = P.sig[p];
     const int L = P.L, R = P.R;
@@ -756,42 +824,68 @@ __global__ void __launch_bounds__(kThreads) k_encode_step(Params P, Ctl* ctl) {
     double4* sv = reinterpret_cast<double4*>(sm1);
     uint8_t* sf = sm1 + 32u * nv;      // previous-tree flags, slo layout
     uint8_t* sd = sf + slo(K);         // DEM flags, slo layout
+    uint8_t* so = sd + slo(K);         // new pre flags of levels R..L-2, slo layout
 
-    // ---- one round trip: flags + inputs (async), own level-(L-2) children
-    const uint8_t f0 = stage_tile_flags(sf, sigp, P, j);
-    const uint8_t d0 = stage_tile_flags(sd, P.dem, P, j);
-#pragma unroll
-    for (int k = 1; k < (KT ? KT - 1 : kMaxL); ++k) {
-        if (!KT && k > K - 2) break;
-        const uint32_t cnt = 1u << (2 * k);
-        stage16(sv + lo(k, 0), buf + P.base[R + k] + static_cast<unsigned long long>(j) * cnt, 32u * cnt);
-    }
-    const int k2 = K - 2;                 // tile level of L-2
+    // ---- the critical-path load first: this thread's level-(L-2) flag
+    const int k2 = K - 2;              // tile level of L-2
     const uint32_t c2 = (k2 >= 0) ? (1u << (2 * k2)) : 0u;
     const bool has2 = threadIdx.x < c2;
     const uint32_t m2 = j * c2 + threadIdx.x;
     bool sp2 = false;
-    double4 ch[4];
-    if (has2) {
-        sp2 = sigp[P.fbase[L - 2] + m2] != 0;
-        if (sp2) {
-            const double4* cp = buf + P.base[L - 1] + (static_cast<unsigned long long>(m2) << 2);
-            ch[0] = ld4_nc(cp); ch[1] = ld4_nc(cp + 1); ch[2] = ld4_nc(cp + 2); ch[3] = ld4_nc(cp + 3);
+    if (has2) sp2 = sigp[slo(L - 2) + m2] != 0;
+    // ---- bulk copies (TMA, one thread): flags of levels R+2..L-1, values of
+    //      levels R+1..L-2; the two smallest flag levels by plain loads
+    if (threadIdx.x == 0) {
+        unsigned bytes = 0;
+        for (int k = 2; k < K; ++k) bytes += 2u << (2 * k);
+        for (int k = 1; k <= K - 2; ++k) bytes += 32u << (2 * k);
+        mbar_expect_tx(&mbar, bytes);
+        for (int k = 2; k < K; ++k) {
+            const uint32_t cnt = 1u << (2 * k);
+            const unsigned long long g = slo(R + k) + static_cast<unsigned long long>(j) * cnt;
+            bulk_g2s(sf + slo(k), sigp + g, cnt, &mbar);
+            bulk_g2s(sd + slo(k), P.dem + g, cnt, &mbar);
+        }
+        for (int k = 1; k <= K - 2; ++k) {
+            const uint32_t cnt = 1u << (2 * k);
+            bulk_g2s(sv + lo(k, 0), buf + cbase(R + k) + static_cast<unsigned long long>(j) * cnt, 32u * cnt, &mbar);
         }
     }
-    cp_async_wait_all();
-    if (threadIdx.x == 0) {
+    uint32_t fsmall = 0, dsmall = 0;
+    if (threadIdx.x == 32 && K > 1) {
+        fsmall = *reinterpret_cast<const uint32_t*>(sigp + slo(R + 1) + 4ull * j);
+        dsmall = *reinterpret_cast<const uint32_t*>(P.dem + slo(R + 1) + 4ull * j);
+    }
+    uint8_t f0 = 0, d0 = 0;
+    if (threadIdx.x == 64) {
+        f0 = sigp[slo(R) + j];
+        d0 = P.dem[slo(R) + j];
+    }
+    stage_thresholds(P, s_thr);
+    double4 ch[4];
+    if (sp2) {
+        const double4* cp = buf + cbase(L - 1) + (static_cast<unsigned long long>(m2) << 2);
+        ch[0] = ld4_nc(cp); ch[1] = ld4_nc(cp + 1); ch[2] = ld4_nc(cp + 2); ch[3] = ld4_nc(cp + 3);
+    }
+    stamp(0);
+    if (threadIdx.x == 32 && K > 1) {
+        *reinterpret_cast<uint32_t*>(sf + slo(1)) = fsmall;
+        *reinterpret_cast<uint32_t*>(sd + slo(1)) = dsmall;
+    }
+    if (threadIdx.x == 64) {
         sf[0] = f0;
         sd[0] = d0;
     }
+    mbar_wait(&mbar, 0);
     __syncthreads();
+    stamp(1);
 
     // ---- level L-1: cells off the previous tree only get pre = DEM | (eps == 0)
     {
         const int k = K - 1;
         const uint32_t cnt = 1u << (2 * k);
-        const uint32_t zero = (0.0 >= P.tau[L - 1]) ? 0x01010101u : 0u;
-        const unsigned long long g = P.fbase[L - 1] + static_cast<unsigned long long>(j) * cnt;
+        const uint32_t zero = (0.0 >= s_thr[L - 1][3]) ? 0x01010101u : 0u;
+        const unsigned long long g = slo(L - 1) + static_cast<unsigned long long>(j) * cnt;
         if (cnt >= 4) {
             for (uint32_t c = 4u * threadIdx.x; c < cnt; c += 4u * kThreads) {
                 const uint32_t f = *reinterpret_cast<const uint32_t*>(sf + slo(k) + c);
@@ -806,44 +900,59 @@ __global__ void __launch_bounds__(kThreads) k_encode_step(Params P, Ctl* ctl) {
         }
     }
     unsigned tree = 0;
+    stamp(2);
     // ---- level L-2 from the registers
     if (has2) {
-        bool flow = 0.0 >= P.tau[L - 2];
+        bool flow = 0.0 >= s_thr[L - 2][3];
         if (sp2) {
-            const Enc e = encode_children<false>(ch, P, L - 2);
+            const Enc e = encode_children_t(ch, s_thr[L - 2]);
             flow = e.flow;
-            st4(buf + P.base[L - 2] + m2, e.par);
             sv[lo(k2, 0) + threadIdx.x] = e.par;
             ++tree;
         }
-        P.pre[P.fbase[L - 2] + m2] = (flow || sd[slo(k2) + threadIdx.x]) ? 1 : 0;
+        so[slo(k2) + threadIdx.x] = (flow || sd[slo(k2) + threadIdx.x]) ? 1 : 0;
     }
     __syncthreads();
-    // ---- levels L-3 .. R from shared memory
+    stamp(3);
+    // ---- levels L-3 .. R in shared memory
 #pragma unroll
     for (int k = (KT ? KT : kMaxL) - 3; k >= 0; --k) {
         if (!KT && k > K - 3) continue;
         const int n = R + k;
         const uint32_t cnt = 1u << (2 * k);
         for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
-            const uint32_t pm = j * cnt + pi;
-            bool flow = 0.0 >= P.tau[n];
+            bool flow = 0.0 >= s_thr[n][3];
             if (sf[slo(k) + pi]) {
                 const uint32_t c0 = lo(k + 1, 0) + 4u * pi;
                 const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
-                const Enc e = encode_children<false>(c, P, n);
+                const Enc e = encode_children_t(c, s_thr[n]);
                 flow = e.flow;
-                st4(buf + P.base[n] + pm, e.par);
                 sv[lo(k, 0) + pi] = e.par;
                 ++tree;
             }
-            P.pre[P.fbase[n] + pm] = (flow || sd[slo(k) + pi]) ? 1 : 0;
+            so[slo(k) + pi] = (flow || sd[slo(k) + pi]) ? 1 : 0;
         }
         __syncthreads();
     }
+    stamp(4);
+    // ---- one burst of stores: re-encoded values (previous-tree cells) and
+    //      the pre-band flags of levels R..L-2 (words where a level has >= 4)
+    for (int k = 0; k <= K - 2; ++k) {
+        const uint32_t cnt = 1u << (2 * k);
+        const unsigned long long jb = static_cast<unsigned long long>(j) * cnt;
+        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads)
+            if (sf[slo(k) + pi]) st4(buf + cbase(R + k) + jb + pi, sv[lo(k, 0) + pi]);
+        if (cnt >= 4) {
+            for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads)
+                *reinterpret_cast<uint32_t*>(P.pre + slo(R + k) + jb + q) = *reinterpret_cast<const uint32_t*>(so + slo(k) + q);
+        } else if (threadIdx.x == 0) {
+            P.pre[slo(R) + jb] = so[0];
+        }
+    }
     const unsigned tsum = block_sum(tree, s_red);
     if (threadIdx.x == 0 && tsum) atomicAdd(&ctl->cnt_tree, (unsigned long long)tsum);
-    tl_mark(ctl, 2);
+    tl_end(ctl, hd.buf, 0);
+    stamp(5);
 }
 
 // Levels R-1 .. 0 of the re-encode after t = 0, one CTA (run as the extra
@@ -852,14 +961,15 @@ __global__ void __launch_bounds__(kThreads) k_encode_step(Params P, Ctl* ctl) {
 // level-R children of re-encoded level-(R-1) cells into registers and stages
 // the values of previous-tree leaves whose parent is re-encoded. Needs
 // 32 * lo(R, 0) + 2 * fbase[R] bytes of shared memory (host: R <= 6).
-__device__ void encode_top_staged(const Params& P, Ctl* ctl, uint8_t* sm) {
-    const int p = ctl->parity;
+__device__ void encode_top_staged(const Params& P, Ctl* ctl, int p, uint8_t* sm) {
     double4* buf = P.cells[p];
     const uint8_t* sigp = P.sig[p];
     const int R = P.R;
     if (R == 0) return;
     __shared__ unsigned s_red[32];
-    const uint32_t fb = static_cast<uint32_t>(P.fbase[R]);  // flag bytes of levels 0..R-1 (fbase[0] = 0)
+    __shared__ double s_thr[kMaxL][4];
+    stage_thresholds(P, s_thr);
+    const uint32_t fb = static_cast<uint32_t>(slo(R));  // flag bytes of levels 0..R-1 (fbase[0] = 0)
     double4* sv = reinterpret_cast<double4*>(sm);          // levels 0..R-1, compact lo(n, 0)
     uint8_t* sf = sm + 32u * lo(R, 0);                     // previous-tree flags at fbase[n]
     uint8_t* sd = sf + fb;                                 // DEM flags at fbase[n]
@@ -871,7 +981,7 @@ __device__ void encode_top_staged(const Params& P, Ctl* ctl, uint8_t* sm) {
     for (int n = 1; n <= R - 2; ++n) {
         const uint32_t cnt = 1u << (2 * n);
         for (uint32_t m = threadIdx.x; m < cnt; m += kThreads)
-            if (!sf[P.fbase[n] + m] && sf[P.fbase[n - 1] + (m >> 2)]) {
+            if (!sf[slo(n) + m] && sf[slo(n - 1) + (m >> 2)]) {
                 const double4* g = cell_ptr(P, p, n, m);
                 cp_async16(sv + lo(n, 0) + m, g);
                 cp_async16(reinterpret_cast<uint8_t*>(sv + lo(n, 0) + m) + 16, reinterpret_cast<const uint8_t*>(g) + 16);
@@ -885,8 +995,8 @@ __device__ void encode_top_staged(const Params& P, Ctl* ctl, uint8_t* sm) {
         for (uint32_t m0 = 0; m0 < cnt; m0 += kThreads) {
             const uint32_t m = m0 + threadIdx.x;
             if (m >= cnt) break;
-            const bool sp = sf[P.fbase[n] + m] != 0;
-            const bool need = !sp && n > 0 && sf[P.fbase[n - 1] + (m >> 2)];
+            const bool sp = sf[slo(n) + m] != 0;
+            const bool need = !sp && n > 0 && sf[slo(n - 1) + (m >> 2)];
             double4 c[4], v = make_double4(0.0, 0.0, 0.0, 0.0);
             if (sp) {
                 c[0] = ld4_cg(cell_ptr(P, p, n + 1, 4u * m)); c[1] = ld4_cg(cell_ptr(P, p, n + 1, 4u * m + 1));
@@ -894,16 +1004,16 @@ __device__ void encode_top_staged(const Params& P, Ctl* ctl, uint8_t* sm) {
             } else if (need) {
                 v = ld4_cg(cell_ptr(P, p, n, m));
             }
-            bool flow = 0.0 >= P.tau[n];
+            bool flow = 0.0 >= s_thr[n][3];
             if (sp) {
-                const Enc e = encode_children<false>(c, P, n);
+                const Enc e = encode_children_t(c, s_thr[n]);
                 flow = e.flow;
                 v = e.par;
-                st4(buf + P.base[n] + m, v);
+                st4(buf + cbase(n) + m, v);
                 ++tree;
             }
             if (sp || need) sv[lo(n, 0) + m] = v;
-            P.pre[P.fbase[n] + m] = (flow || sd[P.fbase[n] + m]) ? 1 : 0;
+            P.pre[slo(n) + m] = (flow || sd[slo(n) + m]) ? 1 : 0;
         }
     }
     cp_async_wait_all();
@@ -911,17 +1021,17 @@ __device__ void encode_top_staged(const Params& P, Ctl* ctl, uint8_t* sm) {
     for (int n = R - 2; n >= 0; --n) {
         const uint32_t cnt = 1u << (2 * n);
         for (uint32_t m = threadIdx.x; m < cnt; m += kThreads) {
-            bool flow = 0.0 >= P.tau[n];
-            if (sf[P.fbase[n] + m]) {
+            bool flow = 0.0 >= s_thr[n][3];
+            if (sf[slo(n) + m]) {
                 const uint32_t c0 = lo(n + 1, 0) + 4u * m;
                 const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
-                const Enc e = encode_children<false>(c, P, n);
+                const Enc e = encode_children_t(c, s_thr[n]);
                 flow = e.flow;
-                st4(buf + P.base[n] + m, e.par);
+                st4(buf + cbase(n) + m, e.par);
                 sv[lo(n, 0) + m] = e.par;
                 ++tree;
             }
-            P.pre[P.fbase[n] + m] = (flow || sd[P.fbase[n] + m]) ? 1 : 0;
+            P.pre[slo(n) + m] = (flow || sd[slo(n) + m]) ? 1 : 0;
         }
         __syncthreads();
     }
@@ -939,7 +1049,7 @@ __device__ __forceinline__ void write_projection(double4* buf, const Params& P, 
     const int ns = zo::level_of(src);
     const int p = static_cast<int>(buf == P.cells[1]);
     const double4 v = ld4_cg(cell_ptr(P, p, ns, src - zo::level_offset(ns)));
-    double4* dst = buf + P.base[n] + m;
+    double4* dst = buf + cbase(n) + m;
     const double4 old = ld4_cg(dst);
     st4(dst, make_double4(v.x, v.y, v.z, old.w));
 }
@@ -990,16 +1100,17 @@ template <int KT>
 __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int force, int do_top) {
     pdl_wait();
     pdl_trigger();
-    if (!force && !active(ctl, P)) return;
+    const Head hd = cta_head(ctl, P, force != 0);
+    if (!hd.active) return;
     extern __shared__ __align__(16) uint8_t smem2[];
     if (do_top && blockIdx.x == 0) {
-        encode_top_staged(P, ctl, smem2);
+        encode_top_staged(P, ctl, hd.parity, smem2);
         return;
     }
-    tl_start(ctl, 1);
+    tl_start(ctl, hd.buf, 1);
     __shared__ unsigned s_red[32];
     __shared__ uint8_t hr[4];
-    const int p = ctl->parity;
+    const int p = hd.parity;
     uint8_t* sigc = P.sig[p ^ 1];
     const int R = P.R;
     const int K = KT ? KT : P.K;
@@ -1026,13 +1137,13 @@ __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int fo
             const uint32_t bx = (d == 0) ? sb - 1u : (d == 1) ? 0u : pos;
             const uint32_t by = (d == 2) ? 0u : (d == 3) ? sb - 1u : pos;
             const unsigned long long g =
-                P.fbase[R + k] + (static_cast<unsigned long long>(jn) << (2 * k)) + 4ull * zo::interleave(bx, by);
+                slo(R + k) + (static_cast<unsigned long long>(jn) << (2 * k)) + 4ull * zo::interleave(bx, by);
             hv = *reinterpret_cast<const uint32_t*>(P.ppre[owner_of(P, R, jn)] + g);
         }
     } else if (mode != 0 && hi >= 128 && hi < 132) {
         const int d = static_cast<int>(hi - 128);
         const uint32_t jn = zo::neighbour_dev(R, j, static_cast<zo::Direction>(d));
-        hv = (jn != zo::kNone) ? P.ppre[owner_of(P, R, jn)][P.fbase[R] + jn] : 0u;
+        hv = (jn != zo::kNone) ? P.ppre[owner_of(P, R, jn)][slo(R) + jn] : 0u;
     }
     cp_async_wait_all();
     if (threadIdx.x == 0) spre[0] = f0;
@@ -1117,7 +1228,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int fo
     // ---- final flags (word stores), leaf counts from popcounts
     unsigned S = 0, S1 = 0;
     if (threadIdx.x == 0) {
-        sigc[P.fbase[R] + j] = sf[0];
+        sigc[slo(R) + j] = sf[0];
         S = sf[0];
         if (K == 1) S1 = sf[0];
     }
@@ -1125,7 +1236,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int fo
     for (int k = 1; k < (KT ? KT : kMaxL); ++k) {
         if (!KT && k >= K) break;
         const uint32_t nw = 1u << (2 * (k - 1));
-        const unsigned long long g = P.fbase[R + k] + (static_cast<unsigned long long>(j) << (2 * k));
+        const unsigned long long g = slo(R + k) + (static_cast<unsigned long long>(j) << (2 * k));
         for (uint32_t b = threadIdx.x; b < nw; b += kThreads) {
             const uint32_t w = *reinterpret_cast<const uint32_t*>(sf + slo(k) + 4u * b);
             *reinterpret_cast<uint32_t*>(sigc + g + 4u * b) = w;
@@ -1140,7 +1251,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int fo
         P.tile_cnt[j] = 4u * S1t;
         P.tile_cnt[P.n_tiles + j] = 1u + 3u * St - 4u * S1t;
     }
-    tl_mark(ctl, 5);
+    tl_end(ctl, hd.buf, 1);
 }
 
 // The top of the tree (levels 0..R) as every K3 CTA sees it, in shared memory
@@ -1152,33 +1263,11 @@ __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int fo
 // ancestor level.
 struct Top {
     uint8_t* ts;
-    uint8_t* tp;  // pre-band flags (hot path)
-    uint8_t* tv;  // previous-tree flags (hot path)
+    uint8_t* ti;   // on the tree (top-down), levels 0..R
+    uint8_t* cbf;  // 1 at the first subtree under each top-level leaf
+    uint8_t* tp;   // pre-band flags (hot path)
+    uint8_t* tv;   // previous-tree flags (hot path)
 };
-
-// level of the leaf covering subtree t (R: the subtree root is reached)
-__device__ __forceinline__ int tile_depth(const Params& P, const uint8_t* ts, uint32_t t) {
-    const int R = P.R;
-    int n = 0;
-    while (n < R && ts[P.fbase[n] + (t >> (2 * (R - n)))]) ++n;
-    return n;
-}
-
-// leaf counts (A: level L, B: coarser) that subtree t contributes: reached
-// subtrees from K2's counts, else one B leaf for the first subtree under the
-// covering leaf
-__device__ __forceinline__ void tile_counts(const Params& P, const uint8_t* ts, const uint32_t* cnt, uint32_t t,
-                                            unsigned& ca, unsigned& cb) {
-    const int R = P.R;
-    const int n = tile_depth(P, ts, t);
-    if (n == R) {
-        ca = cnt[t];
-        cb = cnt[P.n_tiles + t];
-    } else {
-        ca = 0;
-        cb = ((t & ((1u << (2 * (R - n))) - 1u)) == 0u) ? 1u : 0u;
-    }
-}
 
 // decode (projection, D4) + PTT (Alg. 5) + compaction
 // of subtree j (K3). Every CTA first rebuilds the top of the
@@ -1187,10 +1276,9 @@ __device__ __forceinline__ void tile_counts(const Params& P, const uint8_t* ts, 
 // traversal of the current tree (after a step) into the Morton-ordered export
 // list, with no side effects on the state.
 template <bool EXPORT, int KT>
-__device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint8_t* sm) {
+__device__ void traverse_tile(const Params& P, Ctl* ctl, int p, int tbuf, uint32_t j, uint8_t* sm) {
     __shared__ unsigned s_red[32];
     __shared__ unsigned s_off[4];
-    const int p = ctl->parity;
     double4* buf = P.cells[p];
     const uint8_t* sigc = EXPORT ? P.sig[p] : P.sig[p ^ 1];
     const uint8_t* sigp = EXPORT ? P.sig[p ^ 1] : P.sig[p];
@@ -1198,14 +1286,16 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint8_t* sm
     const int K = KT ? KT : P.K;
     const uint32_t nt = static_cast<uint32_t>(P.n_tiles);
     const uint32_t ncell = lo(L, R);
-    const uint32_t fb = static_cast<uint32_t>(P.fbase[R]);  // top flag bytes of levels 0..R-1
+    const uint32_t fb = static_cast<uint32_t>(slo(R));  // top flag bytes of levels 0..R-1
     const uint32_t ftop = (fb + nt + 15u) & ~15u;
     // shared memory
     uint8_t* sc = sm;                                          // own current flags, slo layout
     uint8_t* sp = sc + slo(K);                                 // own previous flags
     Top T;
     T.ts = sp + slo(K);
-    T.tp = T.ts + ftop;
+    T.ti = T.ts + ftop;
+    T.cbf = T.ti + ftop;
+    T.tp = T.cbf + ((nt + 15u) & ~15u);
     T.tv = T.tp + fb;
     uint32_t* scnt = reinterpret_cast<uint32_t*>(T.tv + fb);  // [2 nt] subtree counts when nt <= 1024
     const bool cnt_smem = nt <= 1024u;
@@ -1226,16 +1316,16 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint8_t* sm
     const int rb = EXPORT ? p : p ^ 1;
     uint8_t r0 = 0;
     if (nt == 1u) {
-        if (threadIdx.x == 64) r0 = P.psig[0][rb][P.fbase[R]];
+        if (threadIdx.x == 64) r0 = P.psig[0][rb][slo(R)];
     } else if (P.G == 1 || (tpp & 15u) == 0u) {
         for (uint32_t q = 16u * threadIdx.x; q < nt; q += 16u * kThreads)
-            cp_async16(T.ts + fb + q, P.psig[owner_of(P, R, q)][rb] + P.fbase[R] + q);
+            cp_async16(T.ts + fb + q, P.psig[owner_of(P, R, q)][rb] + slo(R) + q);
     } else if ((tpp & 3u) == 0u) {
         for (uint32_t q = 4u * threadIdx.x; q < nt; q += 4u * kThreads)
-            cp_async4(T.ts + fb + q, P.psig[owner_of(P, R, q)][rb] + P.fbase[R] + q);
+            cp_async4(T.ts + fb + q, P.psig[owner_of(P, R, q)][rb] + slo(R) + q);
     } else {  // small partitioned grids (tests): plain byte copies
         for (uint32_t q = threadIdx.x; q < nt; q += kThreads)
-            T.ts[fb + q] = P.psig[owner_of(P, R, q)][rb][P.fbase[R] + q];
+            T.ts[fb + q] = P.psig[owner_of(P, R, q)][rb][slo(R) + q];
     }
     if (cnt_smem) {
         if (P.G == 1 && (nt & 3u) == 0u) {
@@ -1253,6 +1343,7 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint8_t* sm
         if (!EXPORT) sp[0] = q0;
     }
     if (threadIdx.x == 64 && nt == 1u) T.ts[fb] = r0;
+    for (uint32_t q = threadIdx.x; q < nt; q += kThreads) T.cbf[q] = 0;
     __syncthreads();
 
     // ---- top: band + closure of levels R-1 .. 0 (hot path)
@@ -1261,15 +1352,29 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint8_t* sm
             const uint32_t cnt_n = 1u << (2 * n);
             for (uint32_t m = threadIdx.x; m < cnt_n; m += kThreads) {
                 uint8_t b = band_flag(P.band_mode, L, n, m, [&](int k, uint32_t mm) -> uint8_t {
-                    return k < R ? T.tp[P.fbase[k] + mm] : P.ppre[owner_of(P, k, mm)][P.fbase[k] + mm];
+                    return k < R ? T.tp[slo(k) + mm] : P.ppre[owner_of(P, k, mm)][slo(k) + mm];
                 });
-                const uint8_t* c = T.ts + P.fbase[n + 1] + 4u * m;
-                if (c[0] | c[1] | c[2] | c[3]) b = 1;
-                T.ts[P.fbase[n] + m] = b;
+                if (*reinterpret_cast<const uint32_t*>(T.ts + slo(n + 1) + 4u * m)) b = 1;
+                T.ts[slo(n) + m] = b;
             }
             __syncthreads();
         }
     }
+
+    // ---- on-tree flags top-down (a cell is on the tree iff its parent is
+    //      significant and on it); the first subtree under each top-level leaf
+    if (threadIdx.x == 0) T.ti[0] = 1;
+    __syncthreads();
+    for (int n = 0; n < R; ++n) {
+        const uint32_t cnt_n = 1u << (2 * n);
+        for (uint32_t m = threadIdx.x; m < cnt_n; m += kThreads) {
+            const bool in = T.ti[slo(n) + m] != 0, sg = T.ts[slo(n) + m] != 0;
+            *reinterpret_cast<uint32_t*>(T.ti + slo(n + 1) + 4u * m) = (in && sg) ? 0x01010101u : 0u;
+            if (in && !sg) T.cbf[m << (2 * (R - n))] = 1;
+        }
+        __syncthreads();
+    }
+    const uint8_t* reach = T.ti + fb;  // level R: subtree root on the tree
 
     // ---- subtree leaf counts and their exclusive scan up to j (and, for the
     //      partition's first CTA, up to tile_hi and the totals). Hot path:
@@ -1281,10 +1386,15 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint8_t* sm
         const uint32_t per = (nt + kThreads - 1) / kThreads;
         const uint32_t a = threadIdx.x * per;
         const uint32_t b = min(nt, a + per);
+        auto counts = [&](uint32_t t, unsigned& ca, unsigned& cb) {
+            const bool r = reach[t] != 0;
+            ca = r ? cnt[t] : 0u;
+            cb = r ? cnt[nt + t] : T.cbf[t];
+        };
         unsigned la = 0, lb = 0;
         for (uint32_t t = a; t < b; ++t) {
             unsigned ca, cb;
-            tile_counts(P, T.ts, cnt, t, ca, cb);
+            counts(t, ca, cb);
             la += ca;
             lb += cb;
         }
@@ -1297,7 +1407,7 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint8_t* sm
             unsigned xa = oa, xb = ob;
             for (uint32_t t = a; t < x; ++t) {
                 unsigned ca, cb;
-                tile_counts(P, T.ts, cnt, t, ca, cb);
+                counts(t, ca, cb);
                 xa += ca;
                 xb += cb;
             }
@@ -1337,12 +1447,11 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint8_t* sm
     // ---- this CTA's share of the top: final flags of levels < R (the
     //      partition's first CTA), projection (D4) of the top cells whose
     //      first subtree is j, the root's decode source, new-cell count
-    const int leafn = tile_depth(P, T.ts, j);
     uint32_t rootsrc = kNoSrc;
     unsigned nnew = 0;
     if (!EXPORT) {
         for (int k = 0; k < R; ++k) {
-            const uint32_t a = P.fbase[k] + (j >> (2 * (R - k)));
+            const uint32_t a = slo(k) + (j >> (2 * (R - k)));
             if (T.ts[a] && !T.tv[a]) {
                 rootsrc = zo::z_of(k, j >> (2 * (R - k)));
                 break;
@@ -1351,28 +1460,30 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint8_t* sm
         if (first) {
             for (int n = 0; n < R; ++n)
                 for (uint32_t m = threadIdx.x; m < (1u << (2 * n)); m += kThreads) {
-                    const uint32_t a = P.fbase[n] + m;
-                    P.sig[p ^ 1][a] = T.ts[a];
+                    const uint32_t a = slo(n) + m;
+                    P.sig[p ^ 1][a] = T.ts[a];  // fbase[n] == slo(n)
                     if (P.part == 0) nnew += (T.ts[a] && !T.tv[a]) ? 1u : 0u;
                 }
         }
         // top cells (levels 1..R) on the tree whose first subtree is j
         const int n = static_cast<int>(threadIdx.x) + 1;
-        if (n <= R && n <= leafn && (j & ((1u << (2 * (R - n))) - 1u)) == 0u) {
+        if (n <= R && (j & ((1u << (2 * (R - n))) - 1u)) == 0u) {
             const uint32_t m = j >> (2 * (R - n));
-            uint32_t s = kNoSrc;
-            for (int k = 0; k < n; ++k) {
-                const uint32_t a = P.fbase[k] + (m >> (2 * (n - k)));
-                if (T.ts[a] && !T.tv[a]) {
-                    s = zo::z_of(k, m >> (2 * (n - k)));
-                    break;
+            if (T.ti[slo(n) + m]) {
+                uint32_t s = kNoSrc;
+                for (int k = 0; k < n; ++k) {
+                    const uint32_t a = slo(k) + (m >> (2 * (n - k)));
+                    if (T.ts[a] && !T.tv[a]) {
+                        s = zo::z_of(k, m >> (2 * (n - k)));
+                        break;
+                    }
                 }
+                if (s != kNoSrc) write_projection(buf, P, n, m, s);
             }
-            if (s != kNoSrc) write_projection(buf, P, n, m, s);
         }
     }
 
-    const bool reached = leafn == R;
+    const bool reached = reach[j] != 0;
     int any_new = 0;
     if (!EXPORT && reached) {
         if (sc[0] && !sp[0]) any_new = 1;
@@ -1424,10 +1535,12 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint8_t* sm
     //      coarser leaves to list B at ob; export: one Morton-ordered list.
     uint32_t* outA = EXPORT ? P.leaves_x : P.leaves;
     if (!reached) {
-        const int n = leafn;
-        if (threadIdx.x == 0 && ((j & ((1u << (2 * (R - n))) - 1u)) == 0u))
+        if (threadIdx.x == 0 && T.cbf[j]) {  // the covering top-level leaf: first non-significant ancestor
+            int n = 0;
+            while (T.ts[slo(n) + (j >> (2 * (R - n)))]) ++n;
             (EXPORT ? outA[oa] : P.leaves[ob]) = zo::z_of(n, j >> (2 * (R - n)));
-        if (!EXPORT) tl_mark(ctl, 8);
+        }
+        if (!EXPORT) tl_end(ctl, tbuf, 2);
         return;
     }
     // one walk per level-(L-2) cell (its 4 level-(L-1) children share the
@@ -1499,17 +1612,18 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, uint32_t j, uint8_t* sm
             }
         }
     }
-    if (!EXPORT) tl_mark(ctl, 8);
+    if (!EXPORT) tl_end(ctl, tbuf, 2);
 }
 
 template <bool EXPORT, int KT>
 __global__ void __launch_bounds__(kThreads, 8) k_traverse(Params P, Ctl* ctl, int force) {
     pdl_wait();
     pdl_trigger();
-    if (!EXPORT && !force && !active(ctl, P)) return;
-    if (!EXPORT) tl_start(ctl, 2);
+    const Head hd = cta_head(ctl, P, EXPORT || force);
+    if (!hd.active) return;
+    if (!EXPORT) tl_start(ctl, hd.buf, 2);
     extern __shared__ __align__(16) uint8_t smem3[];
-    traverse_tile<EXPORT, KT>(P, ctl, P.tile_lo + blockIdx.x, smem3);
+    traverse_tile<EXPORT, KT>(P, ctl, hd.parity, hd.buf, P.tile_lo + blockIdx.x, smem3);
 }
 
 // =========================================================================== K5
@@ -1567,10 +1681,10 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 // reduce the per-thread CFL rates (exact max on the bits of non-negative
 // doubles) into this step's slot; with one partition the last CTA finishes
 // the step, with several k_finalize does (after every partition's FV1)
-__device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ctl, double rate, bool advance) {
+__device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ctl, double rate, bool advance,
+                                                        int slot) {
     __shared__ unsigned long long s_max[kThreads / 32];
     __shared__ int s_last;
-    const int slot = static_cast<int>(ctl->step & 1);
     unsigned long long b = warp_max_u64(static_cast<unsigned long long>(__double_as_longlong(rate)));
     if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = b;
     __syncthreads();
@@ -1581,16 +1695,14 @@ __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ct
     }
     if (P.G > 1) return;  // partitioned: k_finalize combines every partition's slot
     if (!last_block(&ctl->done_k5, &s_last)) return;
-    tl_mark(ctl, 10);
     if (threadIdx.x == 0) {
         const unsigned long long m = atomicAdd(&ctl->rate_bits[slot], 0ull);
         finalize_dt(P, ctl, __longlong_as_double(static_cast<long long>(m)), advance);
         ctl->rate_bits[slot] = 0ull;
         ctl->done_k5 = 0;
-        const int tb = advance ? static_cast<int>((ctl->step - 1) & 1) : tl_buf(ctl);
-        ctl->tl[tb][11] = gtimer();
-        if (advance)
-            for (int k = 0; k < 12; ++k) ctl->tl[tb ^ 1][k] = 0ull;  // next step's buffer
+        ctl->tl[slot][3][2] = gtimer();
+        if (advance)  // next step's buffer
+            for (int k = 0; k < 4; ++k) ctl->tl[slot ^ 1][k][0] = ctl->tl[slot ^ 1][k][2] = 0ull;
     }
 }
 
@@ -1608,12 +1720,11 @@ __global__ void k_finalize(Params P, Ctl* ctl, int advance) {
         const unsigned long long v = *((volatile const unsigned long long*)&P.pctl[g]->rate_bits[slot]);
         m = v > m ? v : m;
     }
-    const int tb = tl_buf(ctl);
     finalize_dt(P, ctl, __longlong_as_double(static_cast<long long>(m)), advance != 0);
     if (!advance) return;  // initialise: the host clears the slots afterwards
     ctl->rate_bits[slot ^ 1] = 0ull;
-    ctl->tl[tb][11] = gtimer();
-    for (int k = 0; k < 12; ++k) ctl->tl[tb ^ 1][k] = 0ull;
+    ctl->tl[slot][3][2] = gtimer();
+    for (int k = 0; k < 4; ++k) ctl->tl[slot ^ 1][k][0] = ctl->tl[slot ^ 1][k][2] = 0ull;
 }
 
 // covering cell of a same-level neighbour region whose parent (k, mm) is NOT
@@ -1622,11 +1733,11 @@ __global__ void k_finalize(Params P, Ctl* ctl, int advance) {
 // cell itself) is tested by the caller for all four faces at once
 __device__ __forceinline__ const double4* covering_local(const Params& P, const double4* cur, const uint8_t* sigc, int k,
                                                         uint32_t mm) {
-    while (k > 0 && !sigc[P.fbase[k - 1] + (mm >> 2)]) {
+    while (k > 0 && !sigc[slo(k - 1) + (mm >> 2)]) {
         mm >>= 2;
         --k;
     }
-    return cur + P.base[k] + mm;
+    return cur + cbase(k) + mm;
 }
 __device__ __forceinline__ double4* covering(const Params& P, int cur, int k, uint32_t mm) {
     while (k > 0 && !sig_at(P, cur ^ 1, k - 1, mm >> 2)) {
@@ -1642,19 +1753,32 @@ template <bool UNIFORM, int MINB = 2, bool PART = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     pdl_wait();
     pdl_trigger();
-    if (!active(ctl, P)) return;
-    tl_start(ctl, 3);
-    const int p = ctl->parity;
+    // control words, read once per CTA (line 0 of Ctl)
+    __shared__ double s_td[2];
+    __shared__ uint32_t s_u[7];
+    if (threadIdx.x == 0) {
+        const volatile Ctl* vc = ctl;
+        s_td[0] = vc->t;
+        s_td[1] = vc->dt;
+        s_u[0] = static_cast<uint32_t>(vc->parity);
+        s_u[1] = static_cast<uint32_t>(vc->step & 1);
+        s_u[2] = vc->a_lo; s_u[3] = vc->a_hi; s_u[4] = vc->b_lo; s_u[5] = vc->b_hi;
+    }
+    __syncthreads();
+    const double t = s_td[0], dt = s_td[1];
+    if (!(t < P.t_end)) return;
+    const int tbuf = static_cast<int>(s_u[1]);
+    tl_start(ctl, tbuf, 3);
+    const int p = static_cast<int>(s_u[0]);
     const double4* __restrict__ cur = P.cells[p];
     double4* __restrict__ nxt = P.cells[p ^ 1];
     const uint8_t* __restrict__ sigc = P.sig[p ^ 1];
     // this partition's leaves: its slice of the level-L list A (sibling
     // quadruples at indices 4g..4g+3) followed by its slice of list B
-    const uint32_t a_lo = UNIFORM ? 0u : ctl->a_lo, b_lo = UNIFORM ? 0u : ctl->b_lo;
-    const uint32_t NA = UNIFORM ? 0u : ctl->a_hi - a_lo;
-    const uint32_t N = UNIFORM ? (1u << (2 * P.L)) : NA + (ctl->b_hi - b_lo);
+    const uint32_t a_lo = UNIFORM ? 0u : s_u[2], b_lo = UNIFORM ? 0u : s_u[4];
+    const uint32_t NA = UNIFORM ? 0u : s_u[3] - a_lo;
+    const uint32_t N = UNIFORM ? (1u << (2 * P.L)) : NA + (s_u[5] - b_lo);
     auto leaf_at = [&](uint32_t k) { return P.leaves[k < NA ? a_lo + k : b_lo + (k - NA)]; };
-    const double t = ctl->t, dt = ctl->dt;
     const double inflow = series_value(P, t);
     const int lane = threadIdx.x & 31;
     double mx = 0.0;
@@ -1681,14 +1805,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
         if (valid) {
             // every global read of this leaf is issued before any arithmetic:
             // own cell, the neighbours' parent-level flags, the neighbours
-            const double4 o4 = ld4_nc(cur + P.base[n] + m);
+            const double4 o4 = ld4_nc(cur + cbase(n) + m);
             uint32_t nm[4];
             const double4* src[4];
 #pragma unroll
             for (int d = 0; d < 4; ++d) nm[d] = zo::neighbour_dev(n, m, static_cast<zo::Direction>(d));
             if (UNIFORM) {
 #pragma unroll
-                for (int d = 0; d < 4; ++d) src[d] = cur + P.base[n] + nm[d];
+                for (int d = 0; d < 4; ++d) src[d] = cur + cbase(n) + nm[d];
             } else {
                 uint8_t f[4];
                 if (PART) {  // cross-partition reads through the peer tables
@@ -1699,10 +1823,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                         src[d] = f[d] ? cell_ptr(P, p, n, nm[d]) : covering(P, p, n - 1, nm[d] >> 2);
                 } else {
 #pragma unroll
-                    for (int d = 0; d < 4; ++d) f[d] = (nm[d] != zo::kNone) ? sigc[P.fbase[n - 1] + (nm[d] >> 2)] : 1;
+                    for (int d = 0; d < 4; ++d) f[d] = (nm[d] != zo::kNone) ? sigc[slo(n - 1) + (nm[d] >> 2)] : 1;
 #pragma unroll
                     for (int d = 0; d < 4; ++d)
-                        src[d] = f[d] ? cur + P.base[n] + nm[d] : covering_local(P, cur, sigc, n - 1, nm[d] >> 2);
+                        src[d] = f[d] ? cur + cbase(n) + nm[d] : covering_local(P, cur, sigc, n - 1, nm[d] >> 2);
                 }
             }
             double4 r4[4];
@@ -1730,14 +1854,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                     if (nm[d] == zo::kNone) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, P.phys);
                     return make_cell(r4[d], P.phys);
                 };
-                fv1_cell_seq(own, neighbour, P.inv_dx[n], dt, P.phys, hn, qxn, qyn);
+                fv1_cell_seq(own, neighbour, inv_dx_of(P, n), dt, P.phys, hn, qxn, qyn);
             }
             zown = o4.w;
             if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))
                 report_error(ctl, kErrNonFinite, zo::z_of(n, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2),
                              kStageFV1);
-            st4(nxt + P.base[n] + m, make_double4(hn, qxn, qyn, zown));
-            const double c = cfl_rate(hn, qxn, qyn, P.inv_dx[n], P.phys);
+            st4(nxt + cbase(n) + m, make_double4(hn, qxn, qyn, zown));
+            const double c = cfl_rate(hn, qxn, qyn, inv_dx_of(P, n), P.phys);
             mx = c > mx ? c : mx;
         }
         // Next step's zero_details_and_reencode of level L-1, fused here: the
@@ -1748,8 +1872,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             const Enc e = encode_lanes<false>(make_double4(hn, qxn, qyn, zown), 1, P, P.L - 1);
             if ((lane & 3) == 0 && i < NA) {
                 const uint32_t pm = m >> 2;
-                st4(nxt + P.base[P.L - 1] + pm, e.par);
-                const unsigned long long fi = P.fbase[P.L - 1] + pm;
+                st4(nxt + cbase(P.L - 1) + pm, e.par);
+                const unsigned long long fi = slo(P.L - 1) + pm;
                 P.pre[fi] = (e.flow || P.dem[fi]) ? 1 : 0;
                 ++tree;
             }
@@ -1760,7 +1884,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
         const unsigned tt = block_sum(tree, s_red5);
         if (threadIdx.x == 0 && tt) atomicAdd(&ctl->cnt_tree, (unsigned long long)tt);
     }
-    cfl_reduce_and_finalize(P, ctl, mx, true);
+    cfl_reduce_and_finalize(P, ctl, mx, true, tbuf);
 }
 
 // dt at initialise: CFL over the initial leaves, no update.
@@ -1782,11 +1906,11 @@ __global__ void __launch_bounds__(kThreads) k_cfl_init(Params P, Ctl* ctl, int u
             n = zo::level_of(z);
             m = z - zo::level_offset(n);
         }
-        const double4 v = ld4(cur + P.base[n] + m);
-        const double c = cfl_rate(v.x, v.y, v.z, P.inv_dx[n], P.phys);
+        const double4 v = ld4(cur + cbase(n) + m);
+        const double c = cfl_rate(v.x, v.y, v.z, inv_dx_of(P, n), P.phys);
         mx = c > mx ? c : mx;
     }
-    cfl_reduce_and_finalize(P, ctl, mx, false);
+    cfl_reduce_and_finalize(P, ctl, mx, false, static_cast<int>(ctl->step & 1));
 }
 
 // =========================================================== import / export
@@ -1803,7 +1927,7 @@ __global__ void __launch_bounds__(kThreads) k_import(Params P, Ctl* ctl, const d
         const double4 v = make_double4(h[r], qx[r], qy[r], z[r]);
         if (!(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w)))
             report_error(ctl, kErrNonFinite, zo::z_of(P.L, m), 0, kStageImport);
-        st4(P.cells[buffer] + P.base[P.L] + m, v);
+        st4(P.cells[buffer] + cbase(P.L) + m, v);
         mx[0] = max2(mx[0], absd(v.x));
         mx[1] = max2(mx[1], absd(v.y));
         mx[2] = max2(mx[2], absd(v.z));

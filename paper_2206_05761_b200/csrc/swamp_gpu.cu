@@ -199,23 +199,24 @@ int fetch_ctl(swamp_gpu* g) {
 void fill_stage_times(const swamp_gpu* g, swamp_step_report* r) {
     const Ctl& c = *g->ctl_host;
     if (c.step <= 0) return;
-    const unsigned long long* tl = c.tl[(c.step - 1) & 1];
-    auto span = [&](int a, int b) -> double {
-        const unsigned long long s0 = (a % 3 == 0) ? ~tl[a] : tl[a];
-        const unsigned long long s1 = (b % 3 == 0) ? ~tl[b] : tl[b];
-        return (tl[a] == 0 || tl[b] == 0 || s1 < s0) ? 0.0 : 1e-6 * static_cast<double>(s1 - s0);
+    const auto& tl = c.tl[(c.step - 1) & 1];
+    // kernel k: from its first CTA's start to its last CTA's end
+    auto start = [&](int k) { return tl[k][0] ? ~tl[k][0] : 0ull; };
+    auto span = [&](int ka, int kb) -> double {
+        const unsigned long long s0 = start(ka), s1 = tl[kb][2];
+        return (s0 == 0 || s1 == 0 || s1 < s0) ? 0.0 : 1e-6 * static_cast<double>(s1 - s0);
     };
     if (g->uniform) {
-        r->ms_fv1 = span(9, 11);
+        r->ms_fv1 = span(3, 3);
         r->ms_total = r->ms_fv1;
         return;
     }
-    r->ms_encode_flag = span(0, 2);
-    r->ms_band_closure = span(3, 5);
-    r->ms_decode_traverse = span(6, 8);
+    r->ms_encode_flag = span(0, 0);
+    r->ms_band_closure = span(1, 1);
+    r->ms_decode_traverse = span(2, 2);
     r->ms_neighbours = 0.0;
-    r->ms_fv1 = span(9, 11);
-    r->ms_total = span(0, 11);
+    r->ms_fv1 = span(3, 3);
+    r->ms_total = span(0, 3);
 }
 
 void fill_report(const swamp_gpu* g, swamp_step_report* r) {
@@ -284,6 +285,16 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     for (int n = 0; n < L; ++n) {
         P.fbase[n] = foff;
         foff += ((1ull << (2 * n)) + 15ull) & ~15ull;
+    }
+    // the kernels use closed forms of the level tables (hwfv1_kernels.cuh)
+    for (int n = 0; n < L; ++n)
+        if (P.fbase[n] != hwfv1::slo(n)) return fail(SWAMP_E_ARG);
+    for (int n = 0; n <= L; ++n) {
+        if (P.base[n] != hwfv1::cbase(n)) return fail(SWAMP_E_ARG);
+        long long b0, bn;
+        std::memcpy(&b0, &P.inv_dx[0], 8);
+        std::memcpy(&bn, &P.inv_dx[n], 8);
+        if (bn != b0 + (static_cast<long long>(n) << 52)) return fail(SWAMP_E_ARG);
     }
     g->n_cells = static_cast<int64_t>(off);
     const size_t nf = static_cast<size_t>(1) << (2 * L);
@@ -384,13 +395,13 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             g->k3x = hwfv1::k_traverse<true, 0>;
         }
         g->smem_k1 = ncell * (sizeof(double4) + 1);                  // k_encode<true> / k_encode_top
-        g->smem_k1s = 32 * (((size_t(1) << (2 * (K - 1))) - 1) / 3) + 2 * sl;
+        g->smem_k1s = 32 * (((size_t(1) << (2 * (K - 1))) - 1) / 3) + 3 * sl;
         P.top_mode = (R == 0) ? 0 : (R <= 6 ? 1 : 2);
         const size_t k2_tile = 2 * sl;
         const size_t k2_top = P.top_mode == 1 ? 32 * ltop + 2 * fb : 0;
         g->smem_k2 = std::max(k2_tile, k2_top);
         const size_t ftop = (fb + nt + 15) & ~size_t(15);
-        g->smem_k3 = 2 * sl + ftop + 2 * fb + (nt <= 1024 ? 8 * nt : 0) + 4 * ncell;
+        g->smem_k3 = 2 * sl + 2 * ftop + ((nt + 15) & ~size_t(15)) + 2 * fb + (nt <= 1024 ? 8 * nt : 0) + 4 * ncell;
         struct {
             const void* f;
             size_t bytes;
@@ -912,11 +923,12 @@ int swamp_gpu_timeline(swamp_gpu* g, double* out12) {
     if (!g->parts.empty()) g = g->parts[0];
     int st = fetch_ctl(g);
     // the last completed step ran with step counter (step - 1)
-    const unsigned long long* tl = g->ctl_host->tl[(g->ctl_host->step - 1) & 1];
-    const unsigned long long t0 = ~tl[0];
+    const auto& tl = g->ctl_host->tl[(g->ctl_host->step - 1) & 1];
+    const unsigned long long t0 = ~tl[0][0];
     for (int k = 0; k < 12; ++k) {
-        unsigned long long v = (k % 3 == 0) ? ~tl[k] : tl[k];
-        out12[k] = (tl[k] == 0 || v < t0) ? -1.0 : 1e-3 * static_cast<double>(v - t0);
+        const unsigned long long raw = tl[k / 3][k % 3];
+        const unsigned long long v = (k % 3 == 0) ? ~raw : raw;
+        out12[k] = (raw == 0 || v < t0) ? -1.0 : 1e-3 * static_cast<double>(v - t0);
     }
     return st;
 }
