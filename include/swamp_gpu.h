@@ -174,10 +174,14 @@ int swamp_gpu_last_error(const swamp_gpu* g, int32_t* code, uint32_t* z, int32_t
  * [2] newly significant cells (decoded), [3] 4^L. */
 int swamp_gpu_counters(swamp_gpu* g, int64_t* out4);
 
-/* Device timeline of the last profiled step, microseconds from K1's first
- * CTA: for K1, K2, K3, K5 (k = 0..3): [3k] first CTA start, [3k+1] last CTA
- * elected (K3: unused, -1), [3k+2] last CTA / kernel done. */
+/* Device timeline of the last step, microseconds from K1's first CTA: for
+ * K1, K2, K3, K5 (k = 0..3): [3k] first CTA start, [3k+1] unused (-1),
+ * [3k+2] last CTA done. */
 int swamp_gpu_timeline(swamp_gpu* g, double* out12);
+
+/* Diagnostics: raw %globaltimer phase stamps (ns) of the first and last CTA
+ * of K1 ([0, 16)) and K3 ([16, 32)) of the last step; [8 * c + 7] = entry. */
+int swamp_gpu_debug(swamp_gpu* g, uint64_t* out64);
 
 /* Build identification (arch, flags) for logs. */
 const char* swamp_gpu_build_info(void);

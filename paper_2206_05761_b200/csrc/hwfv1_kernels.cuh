@@ -58,12 +58,13 @@ struct Ctl {
     unsigned int done_k1, done_k5;
     alignas(128) unsigned long long cnt_tree;    // cells re-encoded by the last K1
     alignas(128) unsigned long long cnt_new;     // newly significant cells decoded by the last K3
+    alignas(128) unsigned long long k3_ready;    // K3's top CTA published its results (epoch)
     alignas(128) unsigned long long smax_bits[4];
     int err_code;
     uint32_t err_z;
     int err_q;
     int err_stage;
-    alignas(128) unsigned long long dbg[16];     // per-phase globaltimer stamps of probe CTAs (diagnostics)
+    alignas(128) unsigned long long dbg[64];     // per-phase globaltimer stamps of probe CTAs (diagnostics)
     // stage timeline (globaltimer ns), double-buffered by step parity, one
     // line per kernel k (K1, K2, K3, K5): [0] = ~(first CTA start), [2] = last
     // CTA done (atomicMax); K5 zeroes the next buffer
@@ -83,6 +84,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
+// diagnostics: phase stamps of the first and last CTA of a kernel into
+// dbg[base + 8 * (last) + k] (k = 7: entry)
+struct Probe {
+    Ctl* c;
+    int slot;
+    __device__ __forceinline__ Probe(Ctl* ctl, int base) : c(ctl), slot(-1) {
+        if (blockIdx.x == 0) slot = base;
+        else if (blockIdx.x == gridDim.x - 1) slot = base + 8;
+    }
+    __device__ __forceinline__ void operator()(int k, unsigned long long t = 0) const {
+        if (slot >= 0 && threadIdx.x == 0) c->dbg[slot + k] = t ? t : gtimer();
+    }
+};
+
 __device__ __forceinline__ void tl_start(Ctl* c, int buf, int k) {
     if (threadIdx.x == 0 && blockIdx.x == 0) atomicMax(&c->tl[buf][k][0], ~gtimer());
 }
@@ -115,6 +130,8 @@ struct Params {
     uint32_t* leaves_x;   // Morton-ordered leaf list for exports
     uint32_t* tile_cnt;
     uint32_t* tile_off;
+    uint32_t* tile_lvl;   // traversal depth of each subtree (R = reached) | kEmit
+    uint32_t* tile_src;   // decode source of a reached subtree root, or kNoSrc
     // Morton-subtree partitions: this partition owns level-R
     // subtrees [tile_lo, tile_hi); cells on levels >= R belong to their
     // subtree's partition, cells above R are replicated except that a leaf's
@@ -287,17 +304,20 @@ __device__ __forceinline__ bool active(const Ctl* c, const Params& P) {
 // one request per CTA to the control line instead of one per warp.
 struct Head {
     int active, parity, buf;  // buf = timeline buffer (step parity)
+    long long step;
 };
 __device__ __forceinline__ Head cta_head(const Ctl* c, const Params& P, bool force) {
     __shared__ int s_h[3];
+    __shared__ long long s_step;
     if (threadIdx.x == 0) {
         const double t = *((volatile const double*)&c->t);
         s_h[0] = (force || t < P.t_end) ? 1 : 0;
         s_h[1] = *((volatile const int*)&c->parity);
-        s_h[2] = static_cast<int>(*((volatile const long long*)&c->step) & 1);
+        s_step = *((volatile const long long*)&c->step);
+        s_h[2] = static_cast<int>(s_step & 1);
     }
     __syncthreads();
-    return {s_h[0], s_h[1], s_h[2]};
+    return {s_h[0], s_h[1], s_h[2], s_step};
 }
 
 // Block-wide sum of unsigned values (256 threads).
@@ -806,11 +826,8 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
     const Head hd = cta_head(ctl, P, false);  // (its barrier also publishes the mbarrier init)
     if (!hd.active) return;
     tl_start(ctl, hd.buf, 0);
-    const int probe = (blockIdx.x == 0) ? 0 : ((blockIdx.x == gridDim.x - 1) ? 8 : -1);
-    auto stamp = [&](int k) {
-        if (probe >= 0 && threadIdx.x == 0) ctl->dbg[probe + k] = (k == 7) ? t_entry : gtimer();
-    };
-    stamp(7);
+    const Probe stamp(ctl, 0);
+    stamp(7, t_entry);
     extern __shared__ __align__(16) uint8_t sm1[];
     __shared__ unsigned s_red[32];
     __shared__ double s_thr[kMaxL][4];
@@ -1103,11 +1120,11 @@ __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int fo
     const Head hd = cta_head(ctl, P, force != 0);
     if (!hd.active) return;
     extern __shared__ __align__(16) uint8_t smem2[];
+    tl_start(ctl, hd.buf, 1);
     if (do_top && blockIdx.x == 0) {
         encode_top_staged(P, ctl, hd.parity, smem2);
         return;
     }
-    tl_start(ctl, hd.buf, 1);
     __shared__ unsigned s_red[32];
     __shared__ uint8_t hr[4];
     const int p = hd.parity;
@@ -1254,78 +1271,76 @@ __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int fo
     tl_end(ctl, hd.buf, 1);
 }
 
-// The top of the tree (levels 0..R) as every K3 CTA sees it, in shared memory
-// at the padded flag offsets fbase[n] (fbase[0] = 0): ts = flags of levels
-// 0..R (level R = every subtree root, from K2). Hot path: band (D3) + closure
-// of levels R-1..0 from the pre-band flags tp; export: the stored flags.
-// Closure makes significance upward-closed, so a cell is on the tree iff its
-// parent is significant, and a subtree's depth is the first non-significant
-// ancestor level.
-struct Top {
-    uint8_t* ts;
-    uint8_t* ti;   // on the tree (top-down), levels 0..R
-    uint8_t* cbf;  // 1 at the first subtree under each top-level leaf
-    uint8_t* tp;   // pre-band flags (hot path)
-    uint8_t* tv;   // previous-tree flags (hot path)
-};
+// K3 = decode (projection, D4) + PTT (Alg. 5) + compaction
+// (SPEC.md:236-244). Block 0 is the top CTA: it builds the top of the tree
+// once (band + closure of levels < R from the pre-band flags, on-tree flags,
+// every subtree's leaf counts, their scans into list offsets, each
+// subtree's traversal depth and decode source, the projection of top
+// cells) and publishes it with a release flag. The subtree CTAs meanwhile
+// stage their own flags and count their leaves, then wait only for their
+// offsets. Block 0 is dispatched first, so the wait cannot deadlock.
+//
+// Per-subtree results: tile_off[t] / [nt + t] = list A / B offsets (hot path),
+// [2 nt + t] = Morton export offset; tile_lvl[t] = depth (R: reached) | 0x100
+// if t is the first subtree under its covering top-level leaf; tile_src[t] =
+// decode source of a reached root (kNoSrc: none).
+constexpr uint32_t kEmit = 0x100u;
 
-// decode (projection, D4) + PTT (Alg. 5) + compaction
-// of subtree j (K3). Every CTA first rebuilds the top of the
-// tree (band/closure of levels < R, per-subtree leaf counts and their scan up
-// to j) from staged copies — instead of a serial last CTA in K2. EXPORT = the
-// traversal of the current tree (after a step) into the Morton-ordered export
-// list, with no side effects on the state.
-template <bool EXPORT, int KT>
-__device__ void traverse_tile(const Params& P, Ctl* ctl, int p, int tbuf, uint32_t j, uint8_t* sm) {
+__device__ __forceinline__ void k3_publish(Ctl* ctl, unsigned long long epoch) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        st_release_u64(&ctl->k3_ready, epoch);
+    }
+}
+__device__ __forceinline__ void k3_wait(const Ctl* ctl, unsigned long long epoch) {
+    if (threadIdx.x == 0) {
+        while (ld_acquire_u64(&ctl->k3_ready) != epoch) __nanosleep(64);
+    }
+    __syncthreads();
+}
+
+// top of the tree (block 0 of K3); top flags at the padded offsets slo(n)
+template <bool EXPORT>
+__device__ void k3_top(const Params& P, Ctl* ctl, int p, unsigned long long epoch, uint8_t* sm, const Probe& stamp) {
     __shared__ unsigned s_red[32];
-    __shared__ unsigned s_off[4];
-    double4* buf = P.cells[p];
+    __shared__ unsigned s_off[6];
     const uint8_t* sigc = EXPORT ? P.sig[p] : P.sig[p ^ 1];
     const uint8_t* sigp = EXPORT ? P.sig[p ^ 1] : P.sig[p];
     const int L = P.L, R = P.R;
-    const int K = KT ? KT : P.K;
     const uint32_t nt = static_cast<uint32_t>(P.n_tiles);
-    const uint32_t ncell = lo(L, R);
-    const uint32_t fb = static_cast<uint32_t>(slo(R));  // top flag bytes of levels 0..R-1
+    const uint32_t fb = slo(R);  // top flag bytes of levels 0..R-1
     const uint32_t ftop = (fb + nt + 15u) & ~15u;
-    // shared memory
-    uint8_t* sc = sm;                                          // own current flags, slo layout
-    uint8_t* sp = sc + slo(K);                                 // own previous flags
-    Top T;
-    T.ts = sp + slo(K);
-    T.ti = T.ts + ftop;
-    T.cbf = T.ti + ftop;
-    T.tp = T.cbf + ((nt + 15u) & ~15u);
-    T.tv = T.tp + fb;
-    uint32_t* scnt = reinterpret_cast<uint32_t*>(T.tv + fb);  // [2 nt] subtree counts when nt <= 1024
+    uint8_t* ts = sm;             // flags of levels 0..R
+    uint8_t* ti = ts + ftop;      // on the tree, levels 0..R
+    uint8_t* cbf = ti + ftop;     // first subtree under a top-level leaf
+    uint8_t* tp = cbf + ((nt + 15u) & ~15u);
+    uint8_t* tv = tp + fb;
+    uint32_t* scnt = reinterpret_cast<uint32_t*>(tv + fb);
     const bool cnt_smem = nt <= 1024u;
-    uint32_t* src = scnt + (cnt_smem ? 2u * nt : 0u);          // [ncell] projection sources
     const uint32_t* cnt = cnt_smem ? scnt : P.tile_cnt;
-
-    // ---- one round trip: own flags, top flags, subtree roots and counts
-    const uint8_t c0 = stage_tile_flags(sc, sigc, P, j);
-    const uint8_t q0 = EXPORT ? 0 : stage_tile_flags(sp, sigp, P, j);
-    if (EXPORT) {
-        stage16(T.ts, sigc, fb);
-    } else {
-        stage16(T.tp, P.pre, fb);
-        stage16(T.tv, sigp, fb);
-    }
-    // subtree roots (level R) and counts from each subtree's partition
     const uint32_t tpp = P.tiles_per_part;
     const int rb = EXPORT ? p : p ^ 1;
+
+    // ---- stage (one round trip)
+    if (EXPORT) {
+        stage16(ts, sigc, fb);
+    } else {
+        stage16(tp, P.pre, fb);
+        stage16(tv, sigp, fb);
+    }
     uint8_t r0 = 0;
     if (nt == 1u) {
         if (threadIdx.x == 64) r0 = P.psig[0][rb][slo(R)];
     } else if (P.G == 1 || (tpp & 15u) == 0u) {
         for (uint32_t q = 16u * threadIdx.x; q < nt; q += 16u * kThreads)
-            cp_async16(T.ts + fb + q, P.psig[owner_of(P, R, q)][rb] + slo(R) + q);
+            cp_async16(ts + fb + q, P.psig[owner_of(P, R, q)][rb] + slo(R) + q);
     } else if ((tpp & 3u) == 0u) {
         for (uint32_t q = 4u * threadIdx.x; q < nt; q += 4u * kThreads)
-            cp_async4(T.ts + fb + q, P.psig[owner_of(P, R, q)][rb] + slo(R) + q);
+            cp_async4(ts + fb + q, P.psig[owner_of(P, R, q)][rb] + slo(R) + q);
     } else {  // small partitioned grids (tests): plain byte copies
         for (uint32_t q = threadIdx.x; q < nt; q += kThreads)
-            T.ts[fb + q] = P.psig[owner_of(P, R, q)][rb][slo(R) + q];
+            ts[fb + q] = P.psig[owner_of(P, R, q)][rb][slo(R) + q];
     }
     if (cnt_smem) {
         if (P.G == 1 && (nt & 3u) == 0u) {
@@ -1337,155 +1352,179 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, int p, int tbuf, uint32
             }
         }
     }
+    for (uint32_t q = threadIdx.x; q < nt; q += kThreads) cbf[q] = 0;
     cp_async_wait_all();
-    if (threadIdx.x == 0) {
-        sc[0] = c0;
-        if (!EXPORT) sp[0] = q0;
-    }
-    if (threadIdx.x == 64 && nt == 1u) T.ts[fb] = r0;
-    for (uint32_t q = threadIdx.x; q < nt; q += kThreads) T.cbf[q] = 0;
+    if (threadIdx.x == 64 && nt == 1u) ts[fb] = r0;
     __syncthreads();
+    stamp(0);
 
-    // ---- top: band + closure of levels R-1 .. 0 (hot path)
+    // ---- band + closure of levels R-1 .. 0 (hot path)
     if (!EXPORT) {
         for (int n = R - 1; n >= 0; --n) {
             const uint32_t cnt_n = 1u << (2 * n);
             for (uint32_t m = threadIdx.x; m < cnt_n; m += kThreads) {
                 uint8_t b = band_flag(P.band_mode, L, n, m, [&](int k, uint32_t mm) -> uint8_t {
-                    return k < R ? T.tp[slo(k) + mm] : P.ppre[owner_of(P, k, mm)][slo(k) + mm];
+                    return k < R ? tp[slo(k) + mm] : P.ppre[owner_of(P, k, mm)][slo(k) + mm];
                 });
-                if (*reinterpret_cast<const uint32_t*>(T.ts + slo(n + 1) + 4u * m)) b = 1;
-                T.ts[slo(n) + m] = b;
+                if (*reinterpret_cast<const uint32_t*>(ts + slo(n + 1) + 4u * m)) b = 1;
+                ts[slo(n) + m] = b;
             }
             __syncthreads();
         }
     }
-
-    // ---- on-tree flags top-down (a cell is on the tree iff its parent is
-    //      significant and on it); the first subtree under each top-level leaf
-    if (threadIdx.x == 0) T.ti[0] = 1;
+    stamp(1);
+    // ---- on-tree flags top-down (closure makes significance upward-closed:
+    //      a cell is on the tree iff its parent is significant and on it) and
+    //      the first subtree under each top-level leaf
+    if (threadIdx.x == 0) ti[0] = 1;
     __syncthreads();
     for (int n = 0; n < R; ++n) {
         const uint32_t cnt_n = 1u << (2 * n);
         for (uint32_t m = threadIdx.x; m < cnt_n; m += kThreads) {
-            const bool in = T.ti[slo(n) + m] != 0, sg = T.ts[slo(n) + m] != 0;
-            *reinterpret_cast<uint32_t*>(T.ti + slo(n + 1) + 4u * m) = (in && sg) ? 0x01010101u : 0u;
-            if (in && !sg) T.cbf[m << (2 * (R - n))] = 1;
+            const bool in = ti[slo(n) + m] != 0, sg = ts[slo(n) + m] != 0;
+            *reinterpret_cast<uint32_t*>(ti + slo(n + 1) + 4u * m) = (in && sg) ? 0x01010101u : 0u;
+            if (in && !sg) cbf[m << (2 * (R - n))] = 1;
         }
         __syncthreads();
     }
-    const uint8_t* reach = T.ti + fb;  // level R: subtree root on the tree
+    const uint8_t* reach = ti + fb;
+    stamp(2);
 
-    // ---- subtree leaf counts and their exclusive scan up to j (and, for the
-    //      partition's first CTA, up to tile_hi and the totals). Hot path:
-    //      all level-L leaves (list A) first, then the coarser ones (list B);
-    //      export: one Morton-ordered list.
-    const bool first = blockIdx.x == 0;
-    unsigned tot_a = 0;  // leaves in list A (all partitions)
-    {
-        const uint32_t per = (nt + kThreads - 1) / kThreads;
-        const uint32_t a = threadIdx.x * per;
-        const uint32_t b = min(nt, a + per);
-        auto counts = [&](uint32_t t, unsigned& ca, unsigned& cb) {
-            const bool r = reach[t] != 0;
-            ca = r ? cnt[t] : 0u;
-            cb = r ? cnt[nt + t] : T.cbf[t];
-        };
-        unsigned la = 0, lb = 0;
-        for (uint32_t t = a; t < b; ++t) {
-            unsigned ca, cb;
-            counts(t, ca, cb);
-            la += ca;
-            lb += cb;
-        }
-        unsigned ta, tb;
-        const unsigned oa = block_exscan(la, s_red, &ta);
-        const unsigned ob = block_exscan(lb, s_red, &tb);
-        tot_a = ta;
-        auto offsets_at = [&](uint32_t x, int slot) {  // exclusive prefix at subtree x (x < nt)
-            if (x < a || x >= b) return;
-            unsigned xa = oa, xb = ob;
-            for (uint32_t t = a; t < x; ++t) {
-                unsigned ca, cb;
-                counts(t, ca, cb);
-                xa += ca;
-                xb += cb;
-            }
-            s_off[slot] = xa;
-            s_off[slot + 1] = xb;
-        };
-        offsets_at(j, 0);
-        if (!EXPORT && first) {
-            if (P.tile_hi < nt) {
-                offsets_at(P.tile_hi, 2);
-            } else if (threadIdx.x == 0) {
-                s_off[2] = ta;
-                s_off[3] = tb;
-            }
-        }
-        __syncthreads();
-        if (!EXPORT && first && threadIdx.x == 0) {
-            ctl->n_leaves = ta + tb;
-            ctl->n_leaves_A = ta;
-            // this partition's slices of the A and B lists
-            ctl->a_lo = s_off[0];
-            ctl->a_hi = s_off[2];
-            ctl->b_lo = ta + s_off[1];
-            ctl->b_hi = ta + s_off[3];
-        }
+    // ---- per-subtree counts, scans, depth and decode source
+    const uint32_t per = (nt + kThreads - 1) / kThreads;
+    const uint32_t a = threadIdx.x * per;
+    const uint32_t b = min(nt, a + per);
+    auto counts = [&](uint32_t t, unsigned& ca, unsigned& cb) {
+        const bool r = reach[t] != 0;
+        ca = r ? cnt[t] : 0u;
+        cb = r ? cnt[nt + t] : cbf[t];
+    };
+    unsigned la = 0, lb = 0;
+    for (uint32_t t = a; t < b; ++t) {
+        unsigned ca, cb;
+        counts(t, ca, cb);
+        la += ca;
+        lb += cb;
     }
-    uint32_t oa, ob;
-    if (EXPORT) {
-        oa = s_off[0] + s_off[1];
-        ob = 0;
-        if (threadIdx.x == 0) P.tile_off[2 * nt + j] = oa;
-    } else {
-        oa = s_off[0];
-        ob = tot_a + s_off[1];  // list B follows all of list A
-    }
-
-    // ---- this CTA's share of the top: final flags of levels < R (the
-    //      partition's first CTA), projection (D4) of the top cells whose
-    //      first subtree is j, the root's decode source, new-cell count
-    uint32_t rootsrc = kNoSrc;
-    unsigned nnew = 0;
-    if (!EXPORT) {
-        for (int k = 0; k < R; ++k) {
-            const uint32_t a = slo(k) + (j >> (2 * (R - k)));
-            if (T.ts[a] && !T.tv[a]) {
-                rootsrc = zo::z_of(k, j >> (2 * (R - k)));
-                break;
+    unsigned ta, tb;
+    unsigned oa = block_exscan(la, s_red, &ta);
+    unsigned ob = block_exscan(lb, s_red, &tb);
+    stamp(3);
+    for (uint32_t t = a; t < b; ++t) {
+        unsigned ca, cb;
+        counts(t, ca, cb);
+        if (!EXPORT) {
+            P.tile_off[t] = oa;
+            P.tile_off[nt + t] = ta + ob;
+            if (t == P.tile_lo) {
+                s_off[0] = oa;
+                s_off[1] = ta + ob;
+            }
+            if (t == P.tile_hi) {
+                s_off[2] = oa;
+                s_off[3] = ta + ob;
             }
         }
-        if (first) {
-            for (int n = 0; n < R; ++n)
-                for (uint32_t m = threadIdx.x; m < (1u << (2 * n)); m += kThreads) {
-                    const uint32_t a = slo(n) + m;
-                    P.sig[p ^ 1][a] = T.ts[a];  // fbase[n] == slo(n)
-                    if (P.part == 0) nnew += (T.ts[a] && !T.tv[a]) ? 1u : 0u;
+        P.tile_off[2 * nt + t] = oa + ob;
+        int n = R;
+        uint32_t src = kNoSrc;
+        if (!reach[t]) {
+            n = 0;
+            while (ts[slo(n) + (t >> (2 * (R - n)))]) ++n;
+        } else if (!EXPORT) {
+            for (int k = 0; k < R; ++k) {
+                const uint32_t q = slo(k) + (t >> (2 * (R - k)));
+                if (ts[q] && !tv[q]) {
+                    src = zo::z_of(k, t >> (2 * (R - k)));
+                    break;
                 }
+            }
         }
-        // top cells (levels 1..R) on the tree whose first subtree is j
-        const int n = static_cast<int>(threadIdx.x) + 1;
-        if (n <= R && (j & ((1u << (2 * (R - n))) - 1u)) == 0u) {
-            const uint32_t m = j >> (2 * (R - n));
-            if (T.ti[slo(n) + m]) {
-                uint32_t s = kNoSrc;
+        P.tile_lvl[t] = static_cast<uint32_t>(n) | (cbf[t] ? kEmit : 0u);
+        if (!EXPORT) P.tile_src[t] = src;
+        oa += ca;
+        ob += cb;
+    }
+    stamp(4);
+    if (EXPORT) {
+        k3_publish(ctl, epoch);
+        return;
+    }
+    if (threadIdx.x == 0 && P.tile_hi >= nt) {
+        s_off[2] = ta;
+        s_off[3] = ta + tb;
+    }
+    // ---- final flags of levels < R, newly significant top cells, projection
+    //      (D4) of top cells on the tree below a newly significant ancestor
+    unsigned nnew = 0;
+    for (int n = 0; n < R; ++n)
+        for (uint32_t m = threadIdx.x; m < (1u << (2 * n)); m += kThreads) {
+            const uint32_t q = slo(n) + m;
+            P.sig[p ^ 1][q] = ts[q];
+            nnew += (ts[q] && !tv[q]) ? 1u : 0u;
+        }
+    const unsigned tn = block_sum(nnew, s_red);  // (barrier: s_off complete)
+    if (threadIdx.x == 0) {
+        if (tn && P.part == 0) atomicAdd(&ctl->cnt_new, (unsigned long long)tn);
+        ctl->n_leaves = ta + tb;
+        ctl->n_leaves_A = ta;
+        // this partition's slices of the A and B lists
+        ctl->a_lo = s_off[0];
+        ctl->a_hi = s_off[2];
+        ctl->b_lo = s_off[1];
+        ctl->b_hi = s_off[3];
+    }
+    stamp(5);
+    if (tn) {
+        double4* buf = P.cells[p];
+        for (int n = 1; n <= R; ++n)
+            for (uint32_t m = threadIdx.x; m < (1u << (2 * n)); m += kThreads) {
+                if (!ti[slo(n) + m] || owner_of(P, n, m) != P.part) continue;
                 for (int k = 0; k < n; ++k) {
-                    const uint32_t a = slo(k) + (m >> (2 * (n - k)));
-                    if (T.ts[a] && !T.tv[a]) {
-                        s = zo::z_of(k, m >> (2 * (n - k)));
+                    const uint32_t q = slo(k) + (m >> (2 * (n - k)));
+                    if (ts[q] && !tv[q]) {
+                        write_projection(buf, P, n, m, zo::z_of(k, m >> (2 * (n - k))));
                         break;
                     }
                 }
-                if (s != kNoSrc) write_projection(buf, P, n, m, s);
             }
-        }
     }
+    k3_publish(ctl, epoch);
+    stamp(6);
+}
 
-    const bool reached = reach[j] != 0;
+// subtree CTA of K3: stage own flags, count own leaves (independent of the
+// top), wait for the top's offsets, then decode and emit
+template <bool EXPORT, int KT>
+__device__ void k3_tile(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long long epoch, uint32_t j, uint8_t* sm,
+                        const Probe& stamp) {
+    __shared__ unsigned s_red[32];
+    __shared__ uint32_t s_top[4];
+    double4* buf = P.cells[p];
+    const uint8_t* sigc = EXPORT ? P.sig[p] : P.sig[p ^ 1];
+    const uint8_t* sigp = EXPORT ? P.sig[p ^ 1] : P.sig[p];
+    const int L = P.L, R = P.R;
+    const int K = KT ? KT : P.K;
+    const uint32_t nt = static_cast<uint32_t>(P.n_tiles);
+    const uint32_t ncell = lo(L, R);
+    uint8_t* sc = sm;                                      // own current flags, slo layout
+    uint8_t* sp = sc + slo(K);                             // own previous flags
+    uint32_t* src = reinterpret_cast<uint32_t*>(sp + slo(K));  // [ncell] projection sources
+    (void)ncell;
+
+    const uint8_t c0 = stage_tile_flags(sc, sigc, P, j);
+    const uint8_t q0 = EXPORT ? 0 : stage_tile_flags(sp, sigp, P, j);
+    cp_async_wait_all();
+    if (threadIdx.x == 0) {
+        sc[0] = c0;
+        if (!EXPORT) sp[0] = q0;
+    }
+    __syncthreads();
+    stamp(0);
+
+    // ---- anything newly significant inside the subtree (hot path)
     int any_new = 0;
-    if (!EXPORT && reached) {
+    if (!EXPORT) {
         if (sc[0] && !sp[0]) any_new = 1;
 #pragma unroll
         for (int k = 1; k < (KT ? KT : kMaxL); ++k) {
@@ -1497,12 +1536,80 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, int p, int tbuf, uint32
                                : 0;
         }
     }
-    any_new = __syncthreads_or(any_new | (rootsrc != kNoSrc ? 1 : 0));
-    if (EXPORT || !reached) any_new = 0;
+    // ---- PTT counts of the subtree, assuming its root is reached: one walk
+    //      per level-(L-2) cell (its 4 level-(L-1) children share the path);
+    //      K = 1 (L = 1) walks the level-(L-1) cells directly
+    const int Gk = (K >= 2) ? K - 2 : K - 1;               // walked tile level
+    const int G = R + Gk;
+    const uint32_t ng = 1u << (2 * Gk);
+    const uint32_t per = (ng + kThreads - 1) / kThreads;
+    const uint32_t a = threadIdx.x * per;
+    const uint32_t b = min(ng, a + per);
+    const uint8_t* sL1 = sc + slo(K - 1);
+    auto walk = [&](uint32_t t) -> int {  // first tile level <= Gk whose cell is not significant, or Gk + 1
+        int k = 0;
+#pragma unroll
+        for (int kk = 0; kk < (KT ? KT : kMaxL); ++kk) {
+            if (kk > Gk || !sc[slo(kk) + (t >> (2 * (Gk - kk)))]) break;
+            k = kk + 1;
+        }
+        return k;
+    };
+    unsigned ca = 0, cb = 0;
+    for (uint32_t t = a; t < b; ++t) {
+        const int k = walk(t);
+        if (k <= Gk) {
+            cb += ((t & ((1u << (2 * (Gk - k))) - 1u)) == 0u) ? 1u : 0u;
+        } else if (G == L - 1) {
+            ca += 4;
+        } else {
+            const unsigned s4 = __popc(*reinterpret_cast<const uint32_t*>(sL1 + 4u * t));
+            ca += 4 * s4;
+            cb += 4 - s4;
+        }
+    }
+    unsigned total;
+    unsigned xa, xb;
+    if (EXPORT) {
+        xa = block_exscan(ca + cb, s_red, &total);
+        xb = 0;
+    } else {
+        xa = block_exscan(ca, s_red, &total);
+        xb = block_exscan(cb, s_red, &total);
+    }
+    any_new = __syncthreads_or(any_new);
+    stamp(1);
 
-    if (any_new) {
-        // ---- projection inside the subtree, top-down
-        if (threadIdx.x == 0) src[0] = rootsrc;  // the root itself was projected above
+    // ---- the top's results for this subtree
+    k3_wait(ctl, epoch);
+    stamp(2);
+    if (threadIdx.x == 0) {
+        s_top[0] = ldcg_u32(P.tile_off + (EXPORT ? 2 * nt + j : j));
+        s_top[1] = EXPORT ? 0u : ldcg_u32(P.tile_off + nt + j);
+        s_top[2] = ldcg_u32(P.tile_lvl + j);
+        s_top[3] = EXPORT ? kNoSrc : ldcg_u32(P.tile_src + j);
+    }
+    __syncthreads();
+    stamp(3);
+    uint32_t oa = s_top[0], ob = s_top[1];
+    const uint32_t lvl = s_top[2], rootsrc = s_top[3];
+    uint32_t* outA = EXPORT ? P.leaves_x : P.leaves;
+    const bool reached = (lvl & 0xFFu) == static_cast<uint32_t>(R);
+    if (!reached) {
+        if (threadIdx.x == 0 && (lvl & kEmit)) {
+            const int n = static_cast<int>(lvl & 0xFFu);
+            (EXPORT ? outA[oa] : P.leaves[ob]) = zo::z_of(n, j >> (2 * (R - n)));
+        }
+        if (!EXPORT) tl_end(ctl, tbuf, 2);
+        stamp(6);
+        return;
+    }
+
+    // ---- projection inside the subtree, top-down (the root itself was
+    //      projected by the top CTA)
+    unsigned nnew = 0;
+    if (!EXPORT && (any_new || rootsrc != kNoSrc)) {
+        if (threadIdx.x == 0) src[0] = rootsrc;
         __syncthreads();
         for (int n = R; n < L; ++n) {
             const int k = n - R;
@@ -1523,66 +1630,15 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, int p, int tbuf, uint32
             }
             __syncthreads();
         }
-    }
-    if (!EXPORT) {
         const unsigned tn = block_sum(nnew, s_red);
         if (threadIdx.x == 0 && tn) atomicAdd(&ctl->cnt_new, (unsigned long long)tn);
-    } else {
-        __syncthreads();  // s_off consumed before s_red is reused
     }
+    stamp(4);
 
-    // ---- PTT + compaction. Hot path: level-L leaves to list A at oa,
-    //      coarser leaves to list B at ob; export: one Morton-ordered list.
-    uint32_t* outA = EXPORT ? P.leaves_x : P.leaves;
-    if (!reached) {
-        if (threadIdx.x == 0 && T.cbf[j]) {  // the covering top-level leaf: first non-significant ancestor
-            int n = 0;
-            while (T.ts[slo(n) + (j >> (2 * (R - n)))]) ++n;
-            (EXPORT ? outA[oa] : P.leaves[ob]) = zo::z_of(n, j >> (2 * (R - n)));
-        }
-        if (!EXPORT) tl_end(ctl, tbuf, 2);
-        return;
-    }
-    // one walk per level-(L-2) cell (its 4 level-(L-1) children share the
-    // path); K = 1 (L = 1) walks the level-(L-1) cells directly
-    const int Gk = (K >= 2) ? K - 2 : K - 1;               // walked tile level
-    const int G = R + Gk;
-    const uint32_t ng = 1u << (2 * Gk);                    // walked cells in the subtree
-    const uint32_t per = (ng + kThreads - 1) / kThreads;
-    const uint32_t a = threadIdx.x * per;
-    const uint32_t b = min(ng, a + per);
-    const uint8_t* sL1 = sc + slo(K - 1);
-    // depth of the walk: first tile level <= Gk whose cell is not significant, or Gk + 1
-    auto walk = [&](uint32_t t) -> int {
-        int k = 0;
-#pragma unroll
-        for (int kk = 0; kk < (KT ? KT : kMaxL); ++kk) {
-            if (kk > Gk || !sc[slo(kk) + (t >> (2 * (Gk - kk)))]) break;
-            k = kk + 1;
-        }
-        return k;
-    };
-    unsigned ca = 0, cb = 0;
-    for (uint32_t t = a; t < b; ++t) {
-        const int k = walk(t);
-        if (k <= Gk) {
-            cb += ((t & ((1u << (2 * (Gk - k))) - 1u)) == 0u) ? 1u : 0u;
-        } else if (G == L - 1) {
-            ca += 4;
-        } else {
-            const uint32_t w = *reinterpret_cast<const uint32_t*>(sL1 + 4u * t);
-            const unsigned s4 = __popc(w);
-            ca += 4 * s4;
-            cb += 4 - s4;
-        }
-    }
-    unsigned total;
-    if (EXPORT) {
-        oa += block_exscan(ca + cb, s_red, &total);
-    } else {
-        oa += block_exscan(ca, s_red, &total);
-        ob += block_exscan(cb, s_red, &total);
-    }
+    // ---- emit: hot path level-L leaves to list A, coarser ones to list B;
+    //      export one Morton-ordered list
+    oa += xa;
+    ob += xb;
     auto emitA = [&](uint32_t m1) {  // the 4 level-L children of level-(L-1) cell m1
         const uint32_t z0 = zo::z_of(L, m1 << 2);
         if (EXPORT) {
@@ -1613,17 +1669,28 @@ __device__ void traverse_tile(const Params& P, Ctl* ctl, int p, int tbuf, uint32
         }
     }
     if (!EXPORT) tl_end(ctl, tbuf, 2);
+    stamp(6);
 }
 
+// epoch: 0 = hot path (2 step + 2, unique per step; the host clears the flag
+// after initialise), else the host's export sequence number
 template <bool EXPORT, int KT>
-__global__ void __launch_bounds__(kThreads, 8) k_traverse(Params P, Ctl* ctl, int force) {
+__global__ void __launch_bounds__(kThreads, 8) k_traverse(Params P, Ctl* ctl, int force, unsigned long long epoch) {
     pdl_wait();
     pdl_trigger();
+    const unsigned long long t_entry = gtimer();
     const Head hd = cta_head(ctl, P, EXPORT || force);
     if (!hd.active) return;
-    if (!EXPORT) tl_start(ctl, hd.buf, 2);
+    const unsigned long long ep = epoch ? epoch : 2ull * static_cast<unsigned long long>(hd.step) + 2ull;
     extern __shared__ __align__(16) uint8_t smem3[];
-    traverse_tile<EXPORT, KT>(P, ctl, hd.parity, hd.buf, P.tile_lo + blockIdx.x, smem3);
+    if (!EXPORT) tl_start(ctl, hd.buf, 2);
+    const Probe stamp(ctl, EXPORT ? -1000 : 16);
+    stamp(7, t_entry);
+    if (blockIdx.x == 0) {
+        k3_top<EXPORT>(P, ctl, hd.parity, ep, smem3, stamp);
+        return;
+    }
+    k3_tile<EXPORT, KT>(P, ctl, hd.parity, hd.buf, ep, P.tile_lo + blockIdx.x - 1, smem3, stamp);
 }
 
 // =========================================================================== K5

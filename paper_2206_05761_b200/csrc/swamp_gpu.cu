@@ -53,8 +53,9 @@ struct swamp_gpu {
     // tile kernels, specialised for K = 6 (every L >= 6) or generic
     void (*k1)(Params, Ctl*) = nullptr;
     void (*k2)(Params, Ctl*, int, int) = nullptr;
-    void (*k3)(Params, Ctl*, int) = nullptr;
-    void (*k3x)(Params, Ctl*, int) = nullptr;
+    void (*k3)(Params, Ctl*, int, unsigned long long) = nullptr;
+    void (*k3x)(Params, Ctl*, int, unsigned long long) = nullptr;
+    unsigned long long export_epoch = 1ull << 62;  // K3 export launches (hot-path epochs are 2 step + 2)
     cudaEvent_t ev[6] = {};
     std::string err;
     int64_t n_cells = 0;
@@ -154,7 +155,7 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     const int do_top = P.top_mode == 1 ? 1 : 0;
     launch_pdl(g->k2, P.n_tiles + do_top, g->smem_k2, s, P, g->ctl, 0, do_top);
     mark(2);
-    launch_pdl(g->k3, P.n_tiles, g->smem_k3, s, P, g->ctl, 0);
+    launch_pdl(g->k3, P.n_tiles + 1, g->smem_k3, s, P, g->ctl, 0, 0ull);
     mark(3);
     if (g->fv1_minb == 4)
         launch_pdl(hwfv1::k_fv1<false, 4>, g->fv1_grid, 0, s, P, g->ctl);
@@ -308,6 +309,8 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     if ((st = dalloc(g, &P.leaves_x, nf * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.tile_cnt, 2 * P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.tile_off, 3 * P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    if ((st = dalloc(g, &P.tile_lvl, P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    if ((st = dalloc(g, &P.tile_src, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &g->ctl, sizeof(Ctl)))) return fail(st);
     // peer tables: self only (a partitioned group fills in every partition)
     for (int b = 0; b < 2; ++b) {
@@ -401,7 +404,8 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         const size_t k2_top = P.top_mode == 1 ? 32 * ltop + 2 * fb : 0;
         g->smem_k2 = std::max(k2_tile, k2_top);
         const size_t ftop = (fb + nt + 15) & ~size_t(15);
-        g->smem_k3 = 2 * sl + 2 * ftop + ((nt + 15) & ~size_t(15)) + 2 * fb + (nt <= 1024 ? 8 * nt : 0) + 4 * ncell;
+        g->smem_k3 = std::max(2 * sl + 4 * ncell,                                                        // subtree CTA
+                              2 * ftop + ((nt + 15) & ~size_t(15)) + 2 * fb + (nt <= 1024 ? 8 * nt : 0));  // top CTA
         struct {
             const void* f;
             size_t bytes;
@@ -458,7 +462,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
         cudaMemsetAsync(P.pre, 1, foff, s);
         // leaf list = every finest cell in Morton order (for exports)
         g->k2<<<P.n_tiles, kThreads, g->smem_k2, s>>>(P, g->ctl, 1, 0);
-        g->k3<<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 1);
+        g->k3<<<P.n_tiles + 1, kThreads, g->smem_k3, s>>>(P, g->ctl, 1, 0ull);
         cudaMemcpyAsync(P.cells[1], P.cells[0], off * sizeof(double4), cudaMemcpyDeviceToDevice, s);
         hwfv1::k_cfl_init<<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl, 1);
     } else {
@@ -467,7 +471,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
         cudaMemsetAsync(P.sig[0], 1, foff, s);
         hwfv1::k_encode<true><<<P.n_tiles, kThreads, g->smem_k1, s>>>(P, g->ctl);
         g->k2<<<P.n_tiles, kThreads, g->smem_k2, s>>>(P, g->ctl, 1, 0);
-        g->k3<<<P.n_tiles, kThreads, g->smem_k3, s>>>(P, g->ctl, 1);
+        g->k3<<<P.n_tiles + 1, kThreads, g->smem_k3, s>>>(P, g->ctl, 1, 0ull);
         // both buffers hold the full hierarchy; the current tree becomes "previous"
         cudaMemcpyAsync(P.cells[1], P.cells[0], off * sizeof(double4), cudaMemcpyDeviceToDevice, s);
         const int one = 1;
@@ -484,6 +488,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     }
     if ((st = fetch_ctl(g))) return fail(st);
     cudaMemsetAsync(g->ctl->tl, 0, sizeof(g->ctl->tl), s);
+    cudaMemsetAsync(&g->ctl->k3_ready, 0, sizeof(g->ctl->k3_ready), s);  // hot-path epochs restart at step 0
     if ((st = build_graphs(g))) return fail(st);
     *out = g;
     return SWAMP_OK;
@@ -542,7 +547,7 @@ void group_enqueue_step(swamp_gpu* grp) {
         q->k2<<<q->P.tiles_per_part + do_top, kThreads, q->smem_k2, q->stream>>>(q->P, q->ctl, 0, do_top);
     });
     group_phase(grp, [](swamp_gpu* q) {
-        q->k3<<<q->P.tiles_per_part, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 0);
+        q->k3<<<q->P.tiles_per_part + 1, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 0, 0ull);
     });
     group_phase(grp, [](swamp_gpu* q) {
         hwfv1::k_fv1<false, 2, true><<<q->fv1_grid, kThreads, 0, q->stream>>>(q->P, q->ctl);
@@ -611,7 +616,7 @@ int create_group(const swamp_config* cfg, const double* h, const double* qx, con
         q->k2<<<q->P.tiles_per_part, kThreads, q->smem_k2, q->stream>>>(q->P, q->ctl, 1, 0);
     });
     group_phase(grp, [](swamp_gpu* q) {
-        q->k3<<<q->P.tiles_per_part, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 1);
+        q->k3<<<q->P.tiles_per_part + 1, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 1, 0ull);
     });
     group_phase(grp, [](swamp_gpu* q) {
         cudaMemcpyAsync(q->P.cells[1], q->P.cells[0], static_cast<size_t>(q->n_cells) * sizeof(double4),
@@ -625,6 +630,7 @@ int create_group(const swamp_config* cfg, const double* h, const double* qx, con
         cudaSetDevice(q->device);
         cudaMemsetAsync(q->ctl->rate_bits, 0, sizeof(q->ctl->rate_bits), q->stream);
         cudaMemsetAsync(q->ctl->tl, 0, sizeof(q->ctl->tl), q->stream);
+        cudaMemsetAsync(&q->ctl->k3_ready, 0, sizeof(q->ctl->k3_ready), q->stream);
     }
     if ((st = group_sync(grp))) return fail(st);
     *out = grp;
@@ -662,7 +668,7 @@ int group_copy_leaves(swamp_gpu* grp, uint32_t* leaves, uint32_t* nw, uint32_t* 
     if (cap < static_cast<int64_t>(N)) return SWAMP_E_ARG;
     for (swamp_gpu* q : grp->parts) {
         cudaSetDevice(q->device);
-        q->k3x<<<q->P.tiles_per_part, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 1);
+        q->k3x<<<q->P.tiles_per_part + 1, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 1, ++q->export_epoch);
     }
     if ((st = group_sync(grp))) return st;
     const uint32_t nt = static_cast<uint32_t>(p0->P.n_tiles);
@@ -838,7 +844,7 @@ int swamp_gpu_copy_leaves(swamp_gpu* g, uint32_t* leaves, uint32_t* nw, uint32_t
     if (cap < static_cast<int64_t>(N)) return SWAMP_E_ARG;
     // Morton-ordered LeafAssembly of the current tree (the hot path keeps the
     // level-L leaves first)
-    g->k3x<<<g->P.n_tiles, kThreads, g->smem_k3, g->stream>>>(g->P, g->ctl, 1);
+    g->k3x<<<g->P.n_tiles + 1, kThreads, g->smem_k3, g->stream>>>(g->P, g->ctl, 1, ++g->export_epoch);
     CK(cudaStreamSynchronize(g->stream));
     return copy_leaves_x(g, N, leaves, nw, ne, nn, ns);
 }
@@ -933,11 +939,11 @@ int swamp_gpu_timeline(swamp_gpu* g, double* out12) {
     return st;
 }
 
-int swamp_gpu_debug(swamp_gpu* g, uint64_t* out16) {
-    if (!g || !out16) return SWAMP_E_ARG;
+int swamp_gpu_debug(swamp_gpu* g, uint64_t* out64) {
+    if (!g || !out64) return SWAMP_E_ARG;
     if (!g->parts.empty()) g = g->parts[0];
     int st = fetch_ctl(g);
-    std::memcpy(out16, g->ctl_host->dbg, sizeof(g->ctl_host->dbg));
+    std::memcpy(out64, g->ctl_host->dbg, sizeof(g->ctl_host->dbg));
     return st;
 }
 

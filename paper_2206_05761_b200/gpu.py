@@ -55,6 +55,7 @@ def lib():
         L.swamp_gpu_counters.argtypes = [P, i64p]
         L.swamp_gpu_enqueue.argtypes = [P, C.c_int64]
         L.swamp_gpu_timeline.argtypes = [P, dp]
+        L.swamp_gpu_debug.argtypes = [P, C.POINTER(C.c_uint64)]
         L.swamp_gpu_stream.argtypes = [P, C.POINTER(C.c_void_p)]
         L.swamp_gpu_build_info.restype = C.c_char_p
         _LIB = L
@@ -66,7 +67,7 @@ EXPORTED_SYMBOLS = (
     "swamp_gpu_create_uniform", "swamp_gpu_step_uniform", "swamp_gpu_set_profiling", "swamp_gpu_info",
     "swamp_gpu_copy_leaves", "swamp_gpu_export_tree", "swamp_gpu_export_finest", "swamp_gpu_last_error",
     "swamp_gpu_counters", "swamp_gpu_build_info", "swamp_gpu_enqueue", "swamp_gpu_stream",
-    "swamp_gpu_timeline", "swamp_gpu_create_partitioned",
+    "swamp_gpu_timeline", "swamp_gpu_create_partitioned", "swamp_gpu_debug",
 )
 
 
@@ -182,6 +183,12 @@ class Engine:
         a = (C.c_double * 12)()
         self._check(lib().swamp_gpu_timeline(self._h, a), "timeline")
         return [round(v, 2) for v in a]
+
+    def debug(self):
+        """Raw phase stamps (ns) of probe CTAs (swamp_gpu_debug)."""
+        a = (C.c_uint64 * 64)()
+        self._check(lib().swamp_gpu_debug(self._h, a), "debug")
+        return list(a)
 
     def counters(self):
         a = (C.c_int64 * 4)()
