@@ -132,6 +132,11 @@ struct Params {
     uint32_t* tile_off;
     uint32_t* tile_lvl;   // traversal depth of each subtree (R = reached) | kEmit
     uint32_t* tile_src;   // decode source of a reached subtree root, or kNoSrc
+    // FV1 dry shortcut (one partition): wet[b][t] = some leaf of subtree t
+    // ended the step with h >= h_dry (b = step parity); tact[t] = subtree t or
+    // a face-adjacent one is wet, or t touches an inflow edge
+    uint8_t* wet[2];
+    uint8_t* tact;
     // Morton-subtree partitions: this partition owns level-R
     // subtrees [tile_lo, tile_hi); cells on levels >= R belong to their
     // subtree's partition, cells above R are replicated except that a leaf's
@@ -1302,7 +1307,8 @@ __device__ __forceinline__ void k3_wait(const Ctl* ctl, unsigned long long epoch
 
 // top of the tree (block 0 of K3); top flags at the padded offsets slo(n)
 template <bool EXPORT>
-__device__ void k3_top(const Params& P, Ctl* ctl, int p, unsigned long long epoch, uint8_t* sm, const Probe& stamp) {
+__device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long long epoch, uint8_t* sm,
+                       const Probe& stamp) {
     __shared__ unsigned s_red[32];
     __shared__ unsigned s_off[6];
     const uint8_t* sigc = EXPORT ? P.sig[p] : P.sig[p ^ 1];
@@ -1316,7 +1322,8 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, unsigned long long epoc
     uint8_t* cbf = ti + ftop;     // first subtree under a top-level leaf
     uint8_t* tp = cbf + ((nt + 15u) & ~15u);
     uint8_t* tv = tp + fb;
-    uint32_t* scnt = reinterpret_cast<uint32_t*>(tv + fb);
+    uint8_t* swet = tv + fb;      // wet subtrees after the previous FV1
+    uint32_t* scnt = reinterpret_cast<uint32_t*>(swet + ((nt + 15u) & ~15u));
     const bool cnt_smem = nt <= 1024u;
     const uint32_t* cnt = cnt_smem ? scnt : P.tile_cnt;
     const uint32_t tpp = P.tiles_per_part;
@@ -1328,6 +1335,8 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, unsigned long long epoc
     } else {
         stage16(tp, P.pre, fb);
         stage16(tv, sigp, fb);
+        if (nt >= 16u) stage16(swet, P.wet[tbuf], nt);
+        else if (threadIdx.x < nt) swet[threadIdx.x] = P.wet[tbuf][threadIdx.x];
     }
     uint8_t r0 = 0;
     if (nt == 1u) {
@@ -1453,6 +1462,18 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, unsigned long long epoc
     if (threadIdx.x == 0 && P.tile_hi >= nt) {
         s_off[2] = ta;
         s_off[3] = ta + tb;
+    }
+    // ---- FV1 dry shortcut: active subtrees, and clear the flags FV1 sets next
+    for (uint32_t t = threadIdx.x; t < nt; t += kThreads) {
+        uint8_t act = swet[t];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const uint32_t nb = zo::neighbour_dev(R, t, static_cast<zo::Direction>(d));
+            if (nb == zo::kNone) act |= (P.bc[d] == 2) ? 1 : 0;
+            else act |= swet[nb];
+        }
+        P.tact[t] = act;
+        P.wet[tbuf ^ 1][t] = 0;
     }
     // ---- final flags of levels < R, newly significant top cells, projection
     //      (D4) of top cells on the tree below a newly significant ancestor
@@ -1687,7 +1708,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_traverse(Params P, Ctl* ctl, in
     const Probe stamp(ctl, EXPORT ? -1000 : 16);
     stamp(7, t_entry);
     if (blockIdx.x == 0) {
-        k3_top<EXPORT>(P, ctl, hd.parity, ep, smem3, stamp);
+        k3_top<EXPORT>(P, ctl, hd.parity, hd.buf, ep, smem3, stamp);
         return;
     }
     k3_tile<EXPORT, KT>(P, ctl, hd.parity, hd.buf, ep, P.tile_lo + blockIdx.x - 1, smem3, stamp);
@@ -1873,6 +1894,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             // every global read of this leaf is issued before any arithmetic:
             // own cell, the neighbours' parent-level flags, the neighbours
             const double4 o4 = ld4_nc(cur + cbase(n) + m);
+            // dry shortcut: in a subtree whose neighbourhood holds no wet cell
+            // (K3's tact) the leaf and all its neighbours are dry, so the
+            // dry-neighbourhood result below follows without the gathers
+            const bool quiet = !UNIFORM && !PART && n >= P.R && !P.tact[m >> (2 * (n - P.R))];
+            if (quiet) {
+                hn = (o4.x < 0.0) ? 0.0 : o4.x;
+                qxn = 0.0;
+                qyn = 0.0;
+            } else {
             uint32_t nm[4];
             const double4* src[4];
 #pragma unroll
@@ -1923,7 +1953,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                 };
                 fv1_cell_seq(own, neighbour, inv_dx_of(P, n), dt, P.phys, hn, qxn, qyn);
             }
+            }  // !quiet
             zown = o4.w;
+            // mark the subtree(s) of a leaf that ends wet (a leaf above level R
+            // marks every subtree under it)
+            if (!UNIFORM && !PART && !(hn < P.phys.hdry)) {
+                uint8_t* wn = P.wet[tbuf ^ 1];
+                if (n >= P.R) {
+                    wn[m >> (2 * (n - P.R))] = 1;
+                } else {
+                    const uint32_t t0 = m << (2 * (P.R - n)), t1 = (m + 1u) << (2 * (P.R - n));
+                    for (uint32_t t = t0; t < t1; ++t) wn[t] = 1;
+                }
+            }
             if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))
                 report_error(ctl, kErrNonFinite, zo::z_of(n, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2),
                              kStageFV1);

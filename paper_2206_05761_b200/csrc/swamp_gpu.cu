@@ -310,6 +310,13 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     if ((st = dalloc(g, &P.tile_cnt, 2 * P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.tile_off, 3 * P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.tile_lvl, P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    if ((st = dalloc(g, &P.wet[0], P.n_tiles))) return fail(st);
+    if ((st = dalloc(g, &P.wet[1], P.n_tiles))) return fail(st);
+    if ((st = dalloc(g, &P.tact, P.n_tiles))) return fail(st);
+    // every subtree counts as wet until FV1 has run once
+    cudaMemset(P.wet[0], 1, P.n_tiles);
+    cudaMemset(P.wet[1], 1, P.n_tiles);
+    cudaMemset(P.tact, 1, P.n_tiles);
     if ((st = dalloc(g, &P.tile_src, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &g->ctl, sizeof(Ctl)))) return fail(st);
     // peer tables: self only (a partitioned group fills in every partition)
@@ -405,7 +412,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         g->smem_k2 = std::max(k2_tile, k2_top);
         const size_t ftop = (fb + nt + 15) & ~size_t(15);
         g->smem_k3 = std::max(2 * sl + 4 * ncell,                                                        // subtree CTA
-                              2 * ftop + ((nt + 15) & ~size_t(15)) + 2 * fb + (nt <= 1024 ? 8 * nt : 0));  // top CTA
+                              2 * ftop + 2 * ((nt + 15) & ~size_t(15)) + 2 * fb + (nt <= 1024 ? 8 * nt : 0));  // top CTA
         struct {
             const void* f;
             size_t bytes;
