@@ -59,6 +59,7 @@ struct Ctl {
     alignas(128) unsigned long long cnt_tree;    // cells re-encoded by the last K1
     alignas(128) unsigned long long cnt_new;     // newly significant cells decoded by the last K3
     alignas(128) unsigned long long k3_ready;    // K3's top CTA published its results (epoch)
+    uint32_t n_stile;                            // subtrees on FV1's strip path this step
     alignas(128) unsigned long long smax_bits[4];
     int err_code;
     uint32_t err_z;
@@ -137,6 +138,12 @@ struct Params {
     // a face-adjacent one is wet, or t touches an inflow edge
     uint8_t* wet[2];
     uint8_t* tact;
+    // FV1 strip path: subtrees that are active, reached and fully refined to
+    // level L (every level-L cell a leaf) are updated by warps marching
+    // 32 x 8 strips (k_fv1 fv1_strip); tsten[t] marks them, stile lists them
+    uint8_t* tsten;
+    uint32_t* stile;
+    int strips;           // strip path enabled (SWAMP_FV1_STRIPS=1; measured slower on B200)
     // Morton-subtree partitions: this partition owns level-R
     // subtrees [tile_lo, tile_hi); cells on levels >= R belong to their
     // subtree's partition, cells above R are replicated except that a leaf's
@@ -1419,9 +1426,29 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     unsigned oa = block_exscan(la, s_red, &ta);
     unsigned ob = block_exscan(lb, s_red, &tb);
     stamp(3);
+    const uint32_t full = 1u << (2 * P.K);  // level-L leaves of a fully refined subtree
+    const bool strips = !EXPORT && P.strips && P.G == 1 && P.K == 6;
+    unsigned nst = 0;                       // this thread's strip-path subtrees
     for (uint32_t t = a; t < b; ++t) {
         unsigned ca, cb;
         counts(t, ca, cb);
+        if (!EXPORT) {
+            // FV1 dry shortcut: subtree t is active if it or a face-adjacent
+            // subtree holds a wet cell, or it touches an inflow edge; clear
+            // the flags FV1 sets next
+            uint8_t act = swet[t];
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+                const uint32_t nb = zo::neighbour_dev(R, t, static_cast<zo::Direction>(d));
+                if (nb == zo::kNone) act |= (P.bc[d] == 2) ? 1 : 0;
+                else act |= swet[nb];
+            }
+            P.tact[t] = act;
+            P.wet[tbuf ^ 1][t] = 0;
+            const uint8_t st = (strips && act && ca == full) ? 1 : 0;
+            P.tsten[t] = st;
+            nst += st;
+        }
         if (!EXPORT) {
             P.tile_off[t] = oa;
             P.tile_off[nt + t] = ta + ob;
@@ -1463,17 +1490,16 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         s_off[2] = ta;
         s_off[3] = ta + tb;
     }
-    // ---- FV1 dry shortcut: active subtrees, and clear the flags FV1 sets next
-    for (uint32_t t = threadIdx.x; t < nt; t += kThreads) {
-        uint8_t act = swet[t];
-#pragma unroll
-        for (int d = 0; d < 4; ++d) {
-            const uint32_t nb = zo::neighbour_dev(R, t, static_cast<zo::Direction>(d));
-            if (nb == zo::kNone) act |= (P.bc[d] == 2) ? 1 : 0;
-            else act |= swet[nb];
+    // ---- the strip-path subtree list (Morton order)
+    {
+        unsigned tot;
+        unsigned os = block_exscan(nst, s_red, &tot);
+        for (uint32_t t = a; t < b; ++t)
+            if (P.tsten[t]) P.stile[os++] = t;  // (own writes of this thread: ordered)
+        if (threadIdx.x == 0) {
+            ctl->n_stile = tot;
+            ctl->dbg[40] += tot;  // diagnostics: strip-path subtrees so far
         }
-        P.tact[t] = act;
-        P.wet[tbuf ^ 1][t] = 0;
     }
     // ---- final flags of levels < R, newly significant top cells, projection
     //      (D4) of top cells on the tree below a newly significant ancestor
@@ -1835,6 +1861,168 @@ __device__ __forceinline__ double4* covering(const Params& P, int cur, int k, ui
     return cell_ptr(P, cur, k, mm);
 }
 
+__device__ __forceinline__ CellV shfl_cell(const CellV& c, int src) {
+    CellV o;
+    o.h = __shfl_sync(kFull, c.h, src);
+    o.qx = __shfl_sync(kFull, c.qx, src);
+    o.qy = __shfl_sync(kFull, c.qy, src);
+    o.z = __shfl_sync(kFull, c.z, src);
+    o.ux = __shfl_sync(kFull, c.ux, src);
+    o.uy = __shfl_sync(kFull, c.uy, src);
+    o.c = __shfl_sync(kFull, c.c, src);
+    return o;
+}
+
+// Strip path of FV1 (one warp): strip q (0..15) of a fully refined 64 x 64
+// subtree `tile` = 32 columns (one per lane) x 8 rows of level-L leaves,
+// marched south to north. Every cell's velocities / celerity are formed once
+// (make_cell) and every face flux once: the x-face between lanes x-1 and x is
+// computed by lane x and handed to lane x-1 by a shuffle, the y-face above row
+// r is the y-face below row r+1. face() and fv1_finish() are the per-leaf
+// path's, with the same (left, right) arguments, so the bits are the same.
+// The strip's outside neighbours (its W and E columns, the rows below and
+// above: the same-level cell, the coarser covering leaf of SPEC.md:248, or a
+// boundary ghost) are fetched once into the warp's shared slots `bsm`; the
+// strip's own rows need no flags (every level-L cell of the subtree is a
+// leaf) and are prefetched two rows ahead. Also the fused level-(L-1)
+// re-encode of the next step (quads = lane pairs x row pairs), the CFL rate,
+// the wet marks.
+constexpr int kStripSlots = 80;  // 8 W + 8 E + 32 S + 32 N neighbours
+__device__ void fv1_strip(const Params& P, Ctl* ctl, const double4* __restrict__ cur, double4* __restrict__ nxt,
+                          const uint8_t* __restrict__ sigc, const double (*thr)[4], uint32_t tile, int q, double dt,
+                          double inflow, int tbuf, double4* bsm, double& mx, unsigned& tree) {
+    const int L = P.L;
+    const int lane = threadIdx.x & 31;
+    const PhysParams& ph = P.phys;
+    const double idx = inv_dx_of(P, L);
+    const uint32_t Xs = (zo::compact_bits(tile) << 6) + (static_cast<uint32_t>(q & 1) << 5);
+    const uint32_t X = Xs + lane;
+    const uint32_t Y0 = (zo::compact_bits(tile >> 1) << 6) + (static_cast<uint32_t>(q >> 1) << 3);
+    const double4* base = cur + cbase(L);
+    // ---- prologue: the strip's outside neighbours (slot k: 0..7 W of row k,
+    //      8..15 E of row k-8, 16..47 S of column k-16, 48..79 N of column
+    //      k-48); a ghost is marked by one NaN bit pattern in h (its state needs
+    //      the cell)
+    {
+        uint32_t nmk[3];
+        int dk[3];
+        uint8_t f[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const int k = lane + 32 * i;
+            uint32_t cx, cy;
+            int d;
+            if (k < 8) { cx = Xs; cy = Y0 + k; d = 0; }
+            else if (k < 16) { cx = Xs + 31u; cy = Y0 + (k - 8); d = 1; }
+            else if (k < 48) { cx = Xs + (k - 16); cy = Y0; d = 3; }
+            else { cx = Xs + (k - 48); cy = Y0 + 7u; d = 2; }
+            dk[i] = d;
+            nmk[i] = (k < kStripSlots) ? zo::neighbour_dev(L, zo::interleave(cx, cy), static_cast<zo::Direction>(d))
+                                       : zo::kNone;
+            f[i] = (nmk[i] != zo::kNone) ? sigc[slo(L - 1) + (nmk[i] >> 2)] : 1;
+        }
+        double4 v[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            if (nmk[i] != zo::kNone) {
+                const double4* src = f[i] ? base + nmk[i] : covering_local(P, cur, sigc, L - 1, nmk[i] >> 2);
+                v[i] = ld4_nc(src);
+            } else {
+                v[i] = make_double4(__longlong_as_double(0x7FF8DEAD00000000ll), 0.0, 0.0, 0.0);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            if (lane + 32 * i < kStripSlots) bsm[lane + 32 * i] = v[i];
+        (void)dk;
+    }
+    __syncwarp();
+    // outside neighbour in direction d of `own` from slot k
+    auto outside = [&](int k, int d, const CellV& own) -> CellV {
+        const double4 v = bsm[k];
+        if (__double_as_longlong(v.x) == 0x7FF8DEAD00000000ll) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, ph);
+        return make_cell(v, ph);
+    };
+    uint32_t m = zo::interleave(X, Y0);
+    double4 raw1 = ld4_nc(base + zo::interleave(X, Y0 + 1u));
+    CellV own = make_cell(ld4_nc(base + m), ph);
+    double FS[3], hRsS;  // the face below the current row (own on its north side)
+    {
+        const CellV sc = outside(16 + lane, 3, own);
+        double hL;
+        face(sc, own, false, ph, FS, hL, hRsS);
+    }
+    bool wet = false;
+    double4 prev = make_double4(0.0, 0.0, 0.0, 0.0);  // this lane's updated cell of the row below
+#pragma unroll 1
+    for (int r = 0; r < 8; ++r) {
+        double4 raw2 = raw1;
+        if (r + 2 <= 7) raw2 = ld4_nc(base + zo::interleave(X, Y0 + static_cast<uint32_t>(r) + 2u));
+        const CellV north = (r < 7) ? make_cell(raw1, ph) : outside(48 + lane, 2, own);
+        CellV w = shfl_cell(own, (lane + 31) & 31);
+        if (lane == 0) w = outside(r, 0, own);
+        const double h = own.h, hh = h * h;
+        double FW[3], hLsW, hRsW;
+        face(w, own, true, ph, FW, hLsW, hRsW);
+        double FE[3], hLsE;
+        FE[0] = __shfl_sync(kFull, FW[0], (lane + 1) & 31);
+        FE[1] = __shfl_sync(kFull, FW[1], (lane + 1) & 31);
+        FE[2] = __shfl_sync(kFull, FW[2], (lane + 1) & 31);
+        hLsE = __shfl_sync(kFull, hLsW, (lane + 1) & 31);
+        if (lane == 31) {
+            const CellV e = outside(8 + r, 1, own);
+            double hR;
+            face(own, e, true, ph, FE, hLsE, hR);
+        }
+        double FN[3], hLsN, hRsN;
+        face(own, north, false, ph, FN, hLsN, hRsN);
+        // the per-leaf path's differences (fv1_cell_seq)
+        const double FE1 = FE[1] + (ph.half_g * (hh - (hLsE * hLsE)));
+        const double FW1 = FW[1] + (ph.half_g * (hh - (hRsW * hRsW)));
+        const double GN1 = FN[1] + (ph.half_g * (hh - (hLsN * hLsN)));
+        const double GS1 = FS[1] + (ph.half_g * (hh - (hRsS * hRsS)));
+        double hn, qxn, qyn;
+        fv1_finish(own, FE[0] - FW[0], FE1 - FW1, FE[2] - FW[2], FN[0] - FS[0], GN1 - GS1, FN[2] - FS[2], idx, dt,
+                   ph, hn, qxn, qyn);
+        if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))
+            report_error(ctl, kErrNonFinite, zo::z_of(L, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2), kStageFV1);
+        const double4 o = make_double4(hn, qxn, qyn, own.z);
+        st4(nxt + cbase(L) + m, o);
+        const double c = cfl_rate(hn, qxn, qyn, idx, ph);
+        mx = c > mx ? c : mx;
+        wet = wet || !(hn < ph.hdry);
+        // next step's re-encode of level L-1: lane pair (x even, x + 1) x rows (r - 1, r)
+        if (r & 1) {
+            double4 ch[4];
+            ch[0] = prev;
+            ch[1] = make_double4(__shfl_sync(kFull, prev.x, (lane + 1) & 31), __shfl_sync(kFull, prev.y, (lane + 1) & 31),
+                                 __shfl_sync(kFull, prev.z, (lane + 1) & 31), __shfl_sync(kFull, prev.w, (lane + 1) & 31));
+            ch[2] = o;
+            ch[3] = make_double4(__shfl_sync(kFull, o.x, (lane + 1) & 31), __shfl_sync(kFull, o.y, (lane + 1) & 31),
+                                 __shfl_sync(kFull, o.z, (lane + 1) & 31), __shfl_sync(kFull, o.w, (lane + 1) & 31));
+            if ((lane & 1) == 0) {
+                const Enc e2 = encode_children_t(ch, thr[L - 1]);
+                const uint32_t pm = m >> 2;
+                st4(nxt + cbase(L - 1) + pm, e2.par);
+                const unsigned long long fi = slo(L - 1) + pm;
+                P.pre[fi] = (e2.flow || P.dem[fi]) ? 1 : 0;
+                ++tree;
+            }
+        }
+        prev = o;
+        // the face above is the next row's face below
+        FS[0] = FN[0];
+        FS[1] = FN[1];
+        FS[2] = FN[2];
+        hRsS = hRsN;
+        own = north;
+        raw1 = raw2;
+        m = zo::interleave(X, Y0 + static_cast<uint32_t>(r) + 1u);
+    }
+    if (__any_sync(kFull, wet) && lane == 0) P.wet[tbuf ^ 1][tile] = 1;
+    __syncwarp();  // bsm reused by the warp's next strip
+}
+
 // FV1 over the leaf list: persistent grid-stride, one thread per
 // leaf; reads the current buffer, writes leaf slots of the other (D15).
 template <bool UNIFORM, int MINB = 2, bool PART = false>
@@ -1844,6 +2032,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     // control words, read once per CTA (line 0 of Ctl)
     __shared__ double s_td[2];
     __shared__ uint32_t s_u[7];
+    __shared__ double s_thr[kMaxL][4];
     if (threadIdx.x == 0) {
         const volatile Ctl* vc = ctl;
         s_td[0] = vc->t;
@@ -1851,7 +2040,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
         s_u[0] = static_cast<uint32_t>(vc->parity);
         s_u[1] = static_cast<uint32_t>(vc->step & 1);
         s_u[2] = vc->a_lo; s_u[3] = vc->a_hi; s_u[4] = vc->b_lo; s_u[5] = vc->b_hi;
+        s_u[6] = (UNIFORM || PART) ? 0u : vc->n_stile;
     }
+    if (!UNIFORM && !PART) stage_thresholds(P, s_thr);
     __syncthreads();
     const double t = s_td[0], dt = s_td[1];
     if (!(t < P.t_end)) return;
@@ -1873,11 +2064,20 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     unsigned tree = 0;
     const uint32_t stride = gridDim.x * kThreads;
     // warp-uniform trip count: every lane runs every iteration (shuffles below)
+    // strip path first: 16 strips per fully refined active subtree
+    if (!UNIFORM && !PART) {
+        const uint32_t nwarps = gridDim.x * (kThreads / 32);
+        const uint32_t ns = 16u * s_u[6];
+        extern __shared__ double4 s_bnd[];  // kThreads / 32 x kStripSlots when P.strips (launch smem)
+        for (uint32_t s = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); s < ns; s += nwarps)
+            fv1_strip(P, ctl, cur, nxt, sigc, s_thr, P.stile[s >> 4], static_cast<int>(s & 15u), dt, inflow, tbuf,
+                      s_bnd + (threadIdx.x >> 5) * kStripSlots, mx, tree);
+    }
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
     uint32_t z_next = (!UNIFORM && wbase + lane < N) ? leaf_at(wbase + lane) : 0u;
     for (; wbase < N; wbase += stride) {
         const uint32_t i = wbase + lane;
-        const bool valid = i < N;
+        bool valid = i < N;
         int n;
         uint32_t m;
         if (UNIFORM) {
@@ -1888,6 +2088,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             if (i + stride < N) z_next = leaf_at(i + stride);
             n = zo::level_of(z);
             m = z - zo::level_offset(n);
+            // leaves of strip-path subtrees were updated above
+            if (!PART && valid && n >= P.R && P.tsten[m >> (2 * (n - P.R))]) valid = false;
         }
         double hn = 0.0, qxn = 0.0, qyn = 0.0, zown = 0.0;
         if (valid) {
@@ -1979,7 +2181,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
         // (identical arithmetic to k_encode; the next K1 starts at L-2).
         if (!UNIFORM && wbase < NA) {
             const Enc e = encode_lanes<false>(make_double4(hn, qxn, qyn, zown), 1, P, P.L - 1);
-            if ((lane & 3) == 0 && i < NA) {
+            if ((lane & 3) == 0 && i < NA && valid) {
                 const uint32_t pm = m >> 2;
                 st4(nxt + cbase(P.L - 1) + pm, e.par);
                 const unsigned long long fi = slo(P.L - 1) + pm;

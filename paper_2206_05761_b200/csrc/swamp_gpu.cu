@@ -157,12 +157,13 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     mark(2);
     launch_pdl(g->k3, P.n_tiles + 1, g->smem_k3, s, P, g->ctl, 0, 0ull);
     mark(3);
+    const size_t sm5 = P.strips ? sizeof(double4) * (kThreads / 32) * hwfv1::kStripSlots : 0;
     if (g->fv1_minb == 4)
-        launch_pdl(hwfv1::k_fv1<false, 4>, g->fv1_grid, 0, s, P, g->ctl);
+        launch_pdl(hwfv1::k_fv1<false, 4>, g->fv1_grid, sm5, s, P, g->ctl);
     else if (g->fv1_minb == 3)
-        launch_pdl(hwfv1::k_fv1<false, 3>, g->fv1_grid, 0, s, P, g->ctl);
+        launch_pdl(hwfv1::k_fv1<false, 3>, g->fv1_grid, sm5, s, P, g->ctl);
     else
-        launch_pdl(hwfv1::k_fv1<false, 2>, g->fv1_grid, 0, s, P, g->ctl);
+        launch_pdl(hwfv1::k_fv1<false, 2>, g->fv1_grid, sm5, s, P, g->ctl);
     mark(4);
 }
 
@@ -313,6 +314,9 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     if ((st = dalloc(g, &P.wet[0], P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.wet[1], P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.tact, P.n_tiles))) return fail(st);
+    if ((st = dalloc(g, &P.tsten, P.n_tiles))) return fail(st);
+    if ((st = dalloc(g, &P.stile, P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    cudaMemset(P.tsten, 0, P.n_tiles);
     // every subtree counts as wet until FV1 has run once
     cudaMemset(P.wet[0], 1, P.n_tiles);
     cudaMemset(P.wet[1], 1, P.n_tiles);
@@ -431,6 +435,8 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     }
     {
         if (const char* e = std::getenv("SWAMP_FV1_MINB")) g->fv1_minb = std::max(2, std::min(4, std::atoi(e)));
+        const char* es = std::getenv("SWAMP_FV1_STRIPS");
+        P.strips = (es && es[0] == '1') ? 1 : 0;
         int occ = 0;
         if (g->fv1_minb == 4)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 4>, kThreads, 0);

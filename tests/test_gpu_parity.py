@@ -150,3 +150,21 @@ def test_partitioned_equals_single(parts, name, kw):
     compare_states(many, one, f"{name} x{parts} advance")
     for a, b in zip(many.export_finest(), one.export_finest()):
         np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+@pytest.mark.parametrize("strips", [False, True], ids=["per-leaf", "strips"])
+@pytest.mark.parametrize("name,kw", [("river_flood", dict(L=9)), ("monai_runup", dict(L=9))])
+def test_active_subtree_paths(monkeypatch, strips, name, kw):
+    """L = 9 (64 subtrees of 64 x 64): FV1's dry-subtree shortcut and, opt-in,
+    the strip path for fully refined active subtrees == the oracle, bitwise."""
+    monkeypatch.setenv("SWAMP_FV1_STRIPS", "1" if strips else "0")
+    cfg, h, qx, qy, z = cases.CASES[name](**kw)
+    g = gpu.initialise(cfg, h, qx, qy, z)
+    o = O.Oracle(cfg, h, qx, qy, z)
+    for k in range(1, 31):
+        g.step_adaptive()
+        o.step()
+        if k in (1, 10, 30):
+            compare_states(g, o, f"{name} strips={strips} step {k}")
+    if strips:
+        assert g.debug()[40] > 0, "no subtree took the strip path"
