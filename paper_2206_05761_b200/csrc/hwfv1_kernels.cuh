@@ -134,14 +134,13 @@ struct Params {
     uint32_t* tile_lvl;   // traversal depth of each subtree (R = reached) | kEmit
     uint32_t* tile_src;   // decode source of a reached subtree root, or kNoSrc
     // FV1 dry shortcut (one partition): wet[b][t] = some leaf of subtree t
-    // ended the step with h >= h_dry (b = step parity); tact[t] = subtree t or
-    // a face-adjacent one is wet, or t touches an inflow edge
+    // ended the step with h >= h_dry (b = step parity); tact[t] bit 0 =
+    // subtree t or a face-adjacent one is wet, or t touches an inflow edge
     uint8_t* wet[2];
     uint8_t* tact;
     // FV1 strip path: subtrees that are active, reached and fully refined to
     // level L (every level-L cell a leaf) are updated by warps marching
-    // 32 x 8 strips (k_fv1 fv1_strip); tsten[t] marks them, stile lists them
-    uint8_t* tsten;
+    // 32 x 8 strips (k_fv1 fv1_strip); tact bit 1 marks them, stile lists them
     uint32_t* stile;
     int strips;           // strip path enabled (SWAMP_FV1_STRIPS=1; measured slower on B200)
     // Morton-subtree partitions: this partition owns level-R
@@ -1443,10 +1442,9 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
                 if (nb == zo::kNone) act |= (P.bc[d] == 2) ? 1 : 0;
                 else act |= swet[nb];
             }
-            P.tact[t] = act;
-            P.wet[tbuf ^ 1][t] = 0;
             const uint8_t st = (strips && act && ca == full) ? 1 : 0;
-            P.tsten[t] = st;
+            P.tact[t] = act | (st << 1);
+            P.wet[tbuf ^ 1][t] = 0;
             nst += st;
         }
         if (!EXPORT) {
@@ -1495,7 +1493,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         unsigned tot;
         unsigned os = block_exscan(nst, s_red, &tot);
         for (uint32_t t = a; t < b; ++t)
-            if (P.tsten[t]) P.stile[os++] = t;  // (own writes of this thread: ordered)
+            if (P.tact[t] & 2u) P.stile[os++] = t;  // (this thread's own writes: ordered)
         if (threadIdx.x == 0) {
             ctl->n_stile = tot;
             ctl->dbg[40] += tot;  // diagnostics: strip-path subtrees so far
@@ -2025,7 +2023,7 @@ __device__ void fv1_strip(const Params& P, Ctl* ctl, const double4* __restrict__
 
 // FV1 over the leaf list: persistent grid-stride, one thread per
 // leaf; reads the current buffer, writes leaf slots of the other (D15).
-template <bool UNIFORM, int MINB = 2, bool PART = false>
+template <bool UNIFORM, int MINB = 2, bool PART = false, bool STRIPS = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     pdl_wait();
     pdl_trigger();
@@ -2040,9 +2038,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
         s_u[0] = static_cast<uint32_t>(vc->parity);
         s_u[1] = static_cast<uint32_t>(vc->step & 1);
         s_u[2] = vc->a_lo; s_u[3] = vc->a_hi; s_u[4] = vc->b_lo; s_u[5] = vc->b_hi;
-        s_u[6] = (UNIFORM || PART) ? 0u : vc->n_stile;
+        s_u[6] = STRIPS ? vc->n_stile : 0u;
     }
-    if (!UNIFORM && !PART) stage_thresholds(P, s_thr);
+    if (STRIPS) stage_thresholds(P, s_thr);
     __syncthreads();
     const double t = s_td[0], dt = s_td[1];
     if (!(t < P.t_end)) return;
@@ -2065,7 +2063,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     const uint32_t stride = gridDim.x * kThreads;
     // warp-uniform trip count: every lane runs every iteration (shuffles below)
     // strip path first: 16 strips per fully refined active subtree
-    if (!UNIFORM && !PART) {
+    if (STRIPS && !UNIFORM && !PART) {
         const uint32_t nwarps = gridDim.x * (kThreads / 32);
         const uint32_t ns = 16u * s_u[6];
         extern __shared__ double4 s_bnd[];  // kThreads / 32 x kStripSlots when P.strips (launch smem)
@@ -2088,9 +2086,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             if (i + stride < N) z_next = leaf_at(i + stride);
             n = zo::level_of(z);
             m = z - zo::level_offset(n);
-            // leaves of strip-path subtrees were updated above
-            if (!PART && valid && n >= P.R && P.tsten[m >> (2 * (n - P.R))]) valid = false;
         }
+        // subtree activity (bit 0: wet neighbourhood, bit 1: strip path)
+        const uint8_t ta = (!UNIFORM && !PART && valid && n >= P.R) ? P.tact[m >> (2 * (n - P.R))] : 1;
+        if (STRIPS && (ta & 2u)) valid = false;  // updated by the strip path above
         double hn = 0.0, qxn = 0.0, qyn = 0.0, zown = 0.0;
         if (valid) {
             // every global read of this leaf is issued before any arithmetic:
@@ -2099,7 +2098,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             // dry shortcut: in a subtree whose neighbourhood holds no wet cell
             // (K3's tact) the leaf and all its neighbours are dry, so the
             // dry-neighbourhood result below follows without the gathers
-            const bool quiet = !UNIFORM && !PART && n >= P.R && !P.tact[m >> (2 * (n - P.R))];
+            const bool quiet = ta == 0;
             if (quiet) {
                 hn = (o4.x < 0.0) ? 0.0 : o4.x;
                 qxn = 0.0;

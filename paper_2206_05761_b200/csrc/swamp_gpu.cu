@@ -158,7 +158,9 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     launch_pdl(g->k3, P.n_tiles + 1, g->smem_k3, s, P, g->ctl, 0, 0ull);
     mark(3);
     const size_t sm5 = P.strips ? sizeof(double4) * (kThreads / 32) * hwfv1::kStripSlots : 0;
-    if (g->fv1_minb == 4)
+    if (P.strips)
+        launch_pdl(hwfv1::k_fv1<false, 2, false, true>, g->fv1_grid, sm5, s, P, g->ctl);
+    else if (g->fv1_minb == 4)
         launch_pdl(hwfv1::k_fv1<false, 4>, g->fv1_grid, sm5, s, P, g->ctl);
     else if (g->fv1_minb == 3)
         launch_pdl(hwfv1::k_fv1<false, 3>, g->fv1_grid, sm5, s, P, g->ctl);
@@ -314,9 +316,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     if ((st = dalloc(g, &P.wet[0], P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.wet[1], P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.tact, P.n_tiles))) return fail(st);
-    if ((st = dalloc(g, &P.tsten, P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.stile, P.n_tiles * sizeof(uint32_t)))) return fail(st);
-    cudaMemset(P.tsten, 0, P.n_tiles);
     // every subtree counts as wet until FV1 has run once
     cudaMemset(P.wet[0], 1, P.n_tiles);
     cudaMemset(P.wet[1], 1, P.n_tiles);
