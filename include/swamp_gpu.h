@@ -42,6 +42,7 @@ extern "C" {
 #define SWAMP_E_DT (-4)       /* dt <= 0 or non-finite             */
 #define SWAMP_E_STATE (-5)    /* call not valid in the current state             */
 #define SWAMP_E_NOMEM (-6)    /* device allocation failed                        */
+#define SWAMP_E_PEER (-7)     /* a partition / rank never reached a barrier (10 s) */
 
 /* boundary kinds */
 #define SWAMP_BC_REFLECTIVE 0
@@ -120,6 +121,25 @@ int swamp_gpu_destroy(swamp_gpu* g);
  * other entry points accept the returned handle (no uniform / profiling). */
 int swamp_gpu_create_partitioned(const swamp_config* cfg, const double* h, const double* qx, const double* qy,
                                  const double* z, int n_parts, const int* devices, swamp_gpu** out);
+
+/* One Morton-subtree partition per process (torchrun: one rank per GPU).
+ * Three calls, in this order on every rank:
+ *   swamp_gpu_rank_create  — allocate and import partition `rank` of `world`
+ *     on CUDA `device`; writes this rank's SWAMP_RANK_BLOB_BYTES blob (CUDA
+ *     IPC handles of the arrays peers read in place);
+ *   (the caller all-gathers the blobs, rank order, e.g. torch.distributed)
+ *   swamp_gpu_rank_connect — map every peer's arrays (IPC; a rank handle of
+ *     the same process is used directly) and enqueue initialise; it
+ *     completes once every rank has connected (device-side barriers);
+ *   swamp_gpu_rank_ready   — wait for initialise, build the step graphs.
+ * Then step / advance / enqueue / run / info / export_finest / export_tree
+ * work as for one engine; every rank must step the same number of times
+ * (the ranks synchronise on the device). copy_leaves returns the count only. */
+#define SWAMP_RANK_BLOB_BYTES 1024
+int swamp_gpu_rank_create(const swamp_config* cfg, const double* h, const double* qx, const double* qy,
+                          const double* z, int rank, int world, int device, swamp_gpu** out, uint8_t* blob);
+int swamp_gpu_rank_connect(swamp_gpu* g, const uint8_t* blobs);
+int swamp_gpu_rank_ready(swamp_gpu* g);
 
 /* step_adaptive: one Alg. 3 iteration. No-op when
  * t >= t_end. Fills `rep` (may be NULL). Synchronises the device. */

@@ -25,6 +25,7 @@ STATUS = {
     -4: "dt <= 0 or non-finite",
     -5: "invalid state",
     -6: "device allocation failed",
+    -7: "a partition never reached a barrier",
 }
 
 _dp = C.POINTER(C.c_double)

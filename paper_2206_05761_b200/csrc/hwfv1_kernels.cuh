@@ -38,7 +38,8 @@ constexpr uint32_t kNoSrc = 0xFFFFFFFFu;
 constexpr int kMaxParts = 8;
 
 enum Stage : int { kStageImport = 0, kStageEncode = 1, kStageBand = 2, kStageTraverse = 3, kStageFV1 = 5, kStageDt = 6 };
-enum ErrCode : int { kErrNone = 0, kErrNonFinite = -3, kErrDt = -4 };
+enum ErrCode : int { kErrNone = 0, kErrNonFinite = -3, kErrDt = -4, kErrBarrier = -7 };
+enum : int { kStageBarrier = 7 };
 
 struct Ctl {
     // ---- line 0: read once per CTA (cta_head) by every kernel of a step
@@ -65,6 +66,7 @@ struct Ctl {
     uint32_t err_z;
     int err_q;
     int err_stage;
+    alignas(128) unsigned long long bar_seq;     // cross-partition barriers passed (k_part_barrier; peers read it)
     alignas(128) unsigned long long dbg[64];     // per-phase globaltimer stamps of probe CTAs (diagnostics)
     // stage timeline (globaltimer ns), double-buffered by step parity, one
     // line per kernel k (K1, K2, K3, K5): [0] = ~(first CTA start), [2] = last
@@ -1815,6 +1817,42 @@ __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ct
         ctl->tl[slot][3][2] = gtimer();
         if (advance)  // next step's buffer
             for (int k = 0; k < 4; ++k) ctl->tl[slot ^ 1][k][0] = ctl->tl[slot ^ 1][k][2] = 0ull;
+    }
+}
+
+// ctl->parity = v on the stream (a pageable host copy would block the host
+// until the stream drains — fatal in front of a cross-partition barrier)
+__global__ void k_set_parity(Ctl* ctl, int v) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) ctl->parity = v;
+}
+
+// Cross-partition barrier on the device (one thread per partition, launched
+// between the phases of a partitioned step on every partition's stream): the
+// kernel before it on this stream has completed, so its writes are in this
+// GPU's memory; publish this partition's barrier count with a system-scope
+// release (peers read it over NVLink, or from other processes through CUDA
+// IPC mappings), then acquire every peer's count. Every partition runs the
+// same phase sequence, so counts match. A peer that never arrives (10 s) is
+// reported instead of hanging the GPU.
+__global__ void k_part_barrier(Params P, Ctl* ctl) {
+    if (threadIdx.x != 0) return;
+    const unsigned long long seq = ctl->bar_seq + 1ull;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&ctl->bar_seq), "l"(seq) : "memory");
+    const unsigned long long t0 = gtimer();
+    for (int g = 0; g < P.G; ++g) {
+        if (g == P.part) continue;
+        const unsigned long long* peer = &P.pctl[g]->bar_seq;
+        for (;;) {
+            unsigned long long v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(peer) : "memory");
+            if (v >= seq) break;
+            if (gtimer() - t0 > 10000000000ull) {
+                report_error(ctl, kErrBarrier, static_cast<uint32_t>(g), 0, kStageBarrier);
+                return;
+            }
+            __nanosleep(100);
+        }
     }
 }
 

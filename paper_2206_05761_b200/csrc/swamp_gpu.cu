@@ -7,6 +7,7 @@
 // time-step loop. No CPU fallback: every compute path is a CUDA kernel; a
 // missing device is an error.
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
@@ -62,16 +63,18 @@ struct swamp_gpu {
     // partitioned group: the shell owns one sub-engine per
     // partition (each with full-size arrays on its device); empty otherwise
     std::vector<swamp_gpu*> parts;
-    cudaEvent_t phase_ev[2] = {};  // per sub-engine: end of the last two phases
-    int phase = 0;
+    // one partition of a multi-process (rank) engine: peer mappings opened
+    // from other processes' CUDA IPC handles, closed on destruction
+    int rank_world = 0;
+    std::vector<void*> ipc_opened;
+    bool serial = false;  // group on one device: all partitions on parts[0]'s stream
 
     ~swamp_gpu() {
         for (swamp_gpu* q : parts) {
             cudaSetDevice(q->device);
             delete q;
         }
-        for (auto& e : phase_ev)
-            if (e) cudaEventDestroy(e);
+        for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
         if (graph1) cudaGraphExecDestroy(graph1);
         if (graphS) cudaGraphExecDestroy(graphS);
         if (graphT) cudaGraphExecDestroy(graphT);
@@ -487,8 +490,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
         g->k3<<<P.n_tiles + 1, kThreads, g->smem_k3, s>>>(P, g->ctl, 1, 0ull);
         // both buffers hold the full hierarchy; the current tree becomes "previous"
         cudaMemcpyAsync(P.cells[1], P.cells[0], off * sizeof(double4), cudaMemcpyDeviceToDevice, s);
-        const int one = 1;
-        cudaMemcpyAsync(&g->ctl->parity, &one, sizeof(int), cudaMemcpyHostToDevice, s);
+        hwfv1::k_set_parity<<<1, 32, 0, s>>>(g->ctl, 1);
         hwfv1::k_cfl_init<<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl, 0);
     }
     {
@@ -509,23 +511,122 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
 
 
 // ============================================================ partitioned
-// A group of G sub-engines (one per partition / GPU). Every phase of a step
-// runs on every partition, then a cross-partition barrier (events; peers'
-// arrays are read in place through the peer tables).
-template <class F>
-void group_phase(swamp_gpu* grp, F&& launch) {
-    const int G = static_cast<int>(grp->parts.size());
-    const int cur = grp->phase & 1, prev = cur ^ 1;
-    for (int g = 0; g < G; ++g) {
-        swamp_gpu* q = grp->parts[g];
-        cudaSetDevice(q->device);
-        if (grp->phase > 0)
-            for (int h = 0; h < G; ++h)
-                if (h != g) cudaStreamWaitEvent(q->stream, grp->parts[h]->phase_ev[prev], 0);
-        launch(q);
-        cudaEventRecord(q->phase_ev[cur], q->stream);
+// Morton-subtree partitions. Partition `part` of G owns level-R
+// subtrees [part, part + 1) * 4^R / G; peers' arrays are read in place through
+// the peer tables (NVLink peer access between devices, CUDA IPC mappings
+// between processes). Every partition runs the same kernel sequence on its
+// own stream with a device-side barrier (k_part_barrier) between phases, so a
+// partition's step is a fixed sequence that is captured as a CUDA graph and
+// replayed independently of the others: a group of partitions in one process
+// (swamp_gpu_create_partitioned) and one partition per process
+// (swamp_gpu_rank_*) share this code.
+void part_barrier(swamp_gpu* q, cudaStream_t s) { hwfv1::k_part_barrier<<<1, 32, 0, s>>>(q->P, q->ctl); }
+
+// phase k of a partitioned step on stream s (k = 0..5: K1, top encode, K2,
+// K3, FV1, finalize); false when the phase does not apply
+bool part_step_phase(swamp_gpu* q, int k, cudaStream_t s) {
+    const Params& P = q->P;
+    switch (k) {
+        case 0: q->k1<<<P.tiles_per_part, kThreads, q->smem_k1s, s>>>(P, q->ctl); return true;
+        case 1:
+            if (P.top_mode != 2) return false;
+            hwfv1::k_encode_top<false><<<1, kThreads, q->smem_k1, s>>>(P, q->ctl);
+            return true;
+        case 2: {
+            const int do_top = P.top_mode == 1 ? 1 : 0;
+            q->k2<<<P.tiles_per_part + do_top, kThreads, q->smem_k2, s>>>(P, q->ctl, 0, do_top);
+            return true;
+        }
+        case 3: q->k3<<<P.tiles_per_part + 1, kThreads, q->smem_k3, s>>>(P, q->ctl, 0, 0ull); return true;
+        case 4: hwfv1::k_fv1<false, 2, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl); return true;
+        default: hwfv1::k_finalize<<<1, 32, 0, s>>>(P, q->ctl, 1); return true;
     }
-    grp->phase++;
+}
+constexpr int kStepPhases = 6;
+
+// phase k of initialise on stream s (k = 0..5)
+bool part_init_phase(swamp_gpu* q, int k, cudaStream_t s) {
+    const Params& P = q->P;
+    switch (k) {
+        case 0: {
+            const size_t foff = P.fbase[P.L - 1] + (((size_t(1) << (2 * (P.L - 1))) + 15) & ~size_t(15));
+            cudaMemsetAsync(P.sig[0], 1, foff, s);
+            hwfv1::k_encode<true><<<P.tiles_per_part, kThreads, q->smem_k1, s>>>(P, q->ctl);
+            return true;
+        }
+        case 1: hwfv1::k_encode_top<true><<<1, kThreads, q->smem_k1, s>>>(P, q->ctl); return true;
+        case 2: q->k2<<<P.tiles_per_part, kThreads, q->smem_k2, s>>>(P, q->ctl, 1, 0); return true;
+        case 3: q->k3<<<P.tiles_per_part + 1, kThreads, q->smem_k3, s>>>(P, q->ctl, 1, 0ull); return true;
+        case 4:
+            cudaMemcpyAsync(P.cells[1], P.cells[0], static_cast<size_t>(q->n_cells) * sizeof(double4),
+                            cudaMemcpyDeviceToDevice, s);
+            hwfv1::k_set_parity<<<1, 32, 0, s>>>(q->ctl, 1);
+            hwfv1::k_cfl_init<<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl, 0);
+            return true;
+        default: hwfv1::k_finalize<<<1, 32, 0, s>>>(P, q->ctl, 0); return true;
+    }
+}
+constexpr int kInitPhases = 6;
+
+// one partition on its own stream, device barriers between the phases
+// (distinct devices / processes)
+void part_enqueue_step(swamp_gpu* q) {
+    for (int k = 0; k < kStepPhases; ++k)
+        if (part_step_phase(q, k, q->stream)) part_barrier(q, q->stream);
+}
+void part_enqueue_init(swamp_gpu* q) {
+    for (int k = 0; k < kInitPhases; ++k)
+        if (part_init_phase(q, k, q->stream)) part_barrier(q, q->stream);
+}
+// all partitions of a group that share one device: every partition's phase k
+// on one stream before phase k + 1 (stream order is the barrier; two streams
+// of one context may share a hardware queue, so spinning barriers could
+// serialise behind each other)
+void serial_enqueue_step(swamp_gpu* grp) {
+    for (int k = 0; k < kStepPhases; ++k)
+        for (swamp_gpu* q : grp->parts) part_step_phase(q, k, grp->parts[0]->stream);
+}
+void serial_enqueue_init(swamp_gpu* grp) {
+    for (int k = 0; k < kInitPhases; ++k)
+        for (swamp_gpu* q : grp->parts) part_init_phase(q, k, grp->parts[0]->stream);
+}
+
+// after initialise: clear the CFL slots / timeline / K3 epochs (the trailing
+// barrier guarantees every peer has read this partition's slot)
+void part_after_init(swamp_gpu* q) {
+    cudaMemsetAsync(q->ctl->rate_bits, 0, sizeof(q->ctl->rate_bits), q->stream);
+    cudaMemsetAsync(q->ctl->tl, 0, sizeof(q->ctl->tl), q->stream);
+    cudaMemsetAsync(&q->ctl->k3_ready, 0, sizeof(q->ctl->k3_ready), q->stream);
+}
+
+// step graphs (graph1 = 1 step, graphS = kGraphSteps) of `g`, captured on
+// stream s from `enqueue_step`
+template <class F>
+int capture_step_graphs(swamp_gpu* g, cudaStream_t s, F&& enqueue_step) {
+    for (int which = 0; which < 2; ++which) {
+        const int steps = which == 1 ? kGraphSteps : 1;
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        for (int k = 0; k < steps; ++k) enqueue_step();
+        CK(cudaStreamEndCapture(s, &graph));
+        cudaGraphExec_t exec;
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+        cudaGraphDestroy(graph);
+        (which == 0 ? g->graph1 : g->graphS) = exec;
+    }
+    return SWAMP_OK;
+}
+int part_build_graphs(swamp_gpu* q) {
+    return capture_step_graphs(q, q->stream, [&] { part_enqueue_step(q); });
+}
+
+int part_enqueue(swamp_gpu* q, int64_t n_steps) {
+    swamp_gpu* g = q;
+    cudaSetDevice(q->device);
+    int64_t k = 0;
+    for (; k + kGraphSteps <= n_steps; k += kGraphSteps) CK(cudaGraphLaunch(q->graphS, q->stream));
+    for (; k < n_steps; ++k) CK(cudaGraphLaunch(q->graph1, q->stream));
+    return SWAMP_OK;
 }
 
 int group_sync(swamp_gpu* grp) {
@@ -547,25 +648,18 @@ int group_sync(swamp_gpu* grp) {
     return SWAMP_OK;
 }
 
-void group_enqueue_step(swamp_gpu* grp) {
-    group_phase(grp, [](swamp_gpu* q) {
-        q->k1<<<q->P.tiles_per_part, kThreads, q->smem_k1s, q->stream>>>(q->P, q->ctl);
-    });
-    if (grp->parts[0]->P.top_mode == 2)
-        group_phase(grp, [](swamp_gpu* q) {
-            hwfv1::k_encode_top<false><<<1, kThreads, q->smem_k1, q->stream>>>(q->P, q->ctl);
-        });
-    group_phase(grp, [](swamp_gpu* q) {
-        const int do_top = q->P.top_mode == 1 ? 1 : 0;
-        q->k2<<<q->P.tiles_per_part + do_top, kThreads, q->smem_k2, q->stream>>>(q->P, q->ctl, 0, do_top);
-    });
-    group_phase(grp, [](swamp_gpu* q) {
-        q->k3<<<q->P.tiles_per_part + 1, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 0, 0ull);
-    });
-    group_phase(grp, [](swamp_gpu* q) {
-        hwfv1::k_fv1<false, 2, true><<<q->fv1_grid, kThreads, 0, q->stream>>>(q->P, q->ctl);
-    });
-    group_phase(grp, [](swamp_gpu* q) { hwfv1::k_finalize<<<1, 32, 0, q->stream>>>(q->P, q->ctl, 1); });
+// peer tables of partition q from the partitions' own arrays (one process)
+void fill_peer_tables(swamp_gpu* q, const std::vector<swamp_gpu*>& parts) {
+    for (size_t k = 0; k < parts.size(); ++k) {
+        swamp_gpu* r = parts[k];
+        for (int b = 0; b < 2; ++b) {
+            q->P.pcells[k][b] = r->P.cells[b];
+            q->P.psig[k][b] = r->P.sig[b];
+        }
+        q->P.ppre[k] = r->P.pre;
+        q->P.ptile_cnt[k] = r->P.tile_cnt;
+        q->P.pctl[k] = r->ctl;
+    }
 }
 
 int create_group(const swamp_config* cfg, const double* h, const double* qx, const double* qy, const double* z,
@@ -587,8 +681,6 @@ int create_group(const swamp_config* cfg, const double* h, const double* qx, con
             grp->err = q->err;
             return fail(st);
         }
-        for (auto& e : q->phase_ev)
-            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return fail(SWAMP_E_CUDA);
     }
     // peer access between distinct devices (NVLink / NVSwitch)
     for (int a = 0; a < G; ++a)
@@ -603,49 +695,40 @@ int create_group(const swamp_config* cfg, const double* h, const double* qx, con
             if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return fail(SWAMP_E_CUDA);
             cudaGetLastError();
         }
-    for (swamp_gpu* q : grp->parts)
-        for (int k = 0; k < G; ++k) {
-            swamp_gpu* r = grp->parts[k];
-            for (int b = 0; b < 2; ++b) {
-                q->P.pcells[k][b] = r->P.cells[b];
-                q->P.psig[k][b] = r->P.sig[b];
-            }
-            q->P.ppre[k] = r->P.pre;
-            q->P.ptile_cnt[k] = r->P.tile_cnt;
-            q->P.pctl[k] = r->ctl;
+    for (swamp_gpu* q : grp->parts) fill_peer_tables(q, grp->parts);
+    // one device for all partitions (virtual partitions): one stream, phase
+    // order; distinct devices: a stream each, device barriers
+    bool same = true, distinct = true;
+    for (int a = 0; a < G; ++a)
+        for (int b = a + 1; b < G; ++b) {
+            same = same && grp->parts[a]->device == grp->parts[b]->device;
+            distinct = distinct && grp->parts[a]->device != grp->parts[b]->device;
         }
-    // initialise, phase by phase across the partitions
-    static const int kOne = 1;
-    group_phase(grp, [](swamp_gpu* q) {
-        const Params& P = q->P;
-        const size_t foff = P.fbase[P.L - 1] + (((size_t(1) << (2 * (P.L - 1))) + 15) & ~size_t(15));
-        cudaMemsetAsync(P.sig[0], 1, foff, q->stream);
-        hwfv1::k_encode<true><<<P.tiles_per_part, kThreads, q->smem_k1, q->stream>>>(P, q->ctl);
-    });
-    group_phase(grp, [](swamp_gpu* q) {
-        hwfv1::k_encode_top<true><<<1, kThreads, q->smem_k1, q->stream>>>(q->P, q->ctl);
-    });
-    group_phase(grp, [](swamp_gpu* q) {
-        q->k2<<<q->P.tiles_per_part, kThreads, q->smem_k2, q->stream>>>(q->P, q->ctl, 1, 0);
-    });
-    group_phase(grp, [](swamp_gpu* q) {
-        q->k3<<<q->P.tiles_per_part + 1, kThreads, q->smem_k3, q->stream>>>(q->P, q->ctl, 1, 0ull);
-    });
-    group_phase(grp, [](swamp_gpu* q) {
-        cudaMemcpyAsync(q->P.cells[1], q->P.cells[0], static_cast<size_t>(q->n_cells) * sizeof(double4),
-                        cudaMemcpyDeviceToDevice, q->stream);
-        cudaMemcpyAsync(&q->ctl->parity, &kOne, sizeof(int), cudaMemcpyHostToDevice, q->stream);
-        hwfv1::k_cfl_init<<<q->fv1_grid, kThreads, 0, q->stream>>>(q->P, q->ctl, 0);
-    });
-    group_phase(grp, [](swamp_gpu* q) { hwfv1::k_finalize<<<1, 32, 0, q->stream>>>(q->P, q->ctl, 0); });
+    if (!same && !distinct) return fail(SWAMP_E_ARG);
+    grp->serial = same && G > 1;
+    if (grp->serial) {
+        cudaSetDevice(grp->parts[0]->device);
+        serial_enqueue_init(grp);
+    } else {
+        for (swamp_gpu* q : grp->parts) {
+            cudaSetDevice(q->device);
+            part_enqueue_init(q);
+        }
+    }
     if ((st = group_sync(grp))) return fail(st);
     for (swamp_gpu* q : grp->parts) {
         cudaSetDevice(q->device);
-        cudaMemsetAsync(q->ctl->rate_bits, 0, sizeof(q->ctl->rate_bits), q->stream);
-        cudaMemsetAsync(q->ctl->tl, 0, sizeof(q->ctl->tl), q->stream);
-        cudaMemsetAsync(&q->ctl->k3_ready, 0, sizeof(q->ctl->k3_ready), q->stream);
+        part_after_init(q);
+        if (!grp->serial && (st = part_build_graphs(q))) {
+            grp->err = q->err;
+            return fail(st);
+        }
     }
     if ((st = group_sync(grp))) return fail(st);
+    if (grp->serial) {
+        cudaSetDevice(grp->parts[0]->device);
+        if ((st = capture_step_graphs(grp, grp->parts[0]->stream, [&] { serial_enqueue_step(grp); }))) return fail(st);
+    }
     *out = grp;
     return SWAMP_OK;
 }
@@ -708,11 +791,48 @@ int group_copy_leaves(swamp_gpu* grp, uint32_t* leaves, uint32_t* nw, uint32_t* 
 }
 
 int group_advance(swamp_gpu* grp, int64_t n_steps, bool sync, swamp_step_report* rep) {
-    for (int64_t k = 0; k < n_steps; ++k) group_enqueue_step(grp);
+    if (grp->serial) {
+        swamp_gpu* g = grp;
+        cudaStream_t s0 = grp->parts[0]->stream;
+        cudaSetDevice(grp->parts[0]->device);
+        int64_t k = 0;
+        for (; k + kGraphSteps <= n_steps; k += kGraphSteps) CK(cudaGraphLaunch(grp->graphS, s0));
+        for (; k < n_steps; ++k) CK(cudaGraphLaunch(grp->graph1, s0));
+    } else
+    for (swamp_gpu* q : grp->parts) {
+        const int st = part_enqueue(q, n_steps);
+        if (st) {
+            grp->err = q->err;
+            return st;
+        }
+    }
     if (!sync) return SWAMP_OK;
     int st = group_sync(grp);
     fill_report(grp->parts[0], rep);
     return st;
+}
+
+// ---- one partition per process (rank engines)
+struct RankBlob {  // exchanged between the ranks (swamp_gpu_rank_create / _connect)
+    uint32_t magic;
+    int32_t rank, world, device;
+    uint64_t pid;
+    uint64_t ptr[7];              // cells[0], cells[1], sig[0], sig[1], pre, tile_cnt, ctl
+    cudaIpcMemHandle_t ipc[7];
+};
+static_assert(sizeof(RankBlob) <= SWAMP_RANK_BLOB_BYTES, "rank blob too large");
+constexpr uint32_t kRankMagic = 0x53574D52u;  // "SWMR"
+
+void* rank_ptr(const swamp_gpu* q, int k) {
+    switch (k) {
+        case 0: return q->P.cells[0];
+        case 1: return q->P.cells[1];
+        case 2: return q->P.sig[0];
+        case 3: return q->P.sig[1];
+        case 4: return q->P.pre;
+        case 5: return q->P.tile_cnt;
+        default: return q->ctl;
+    }
 }
 
 }  // namespace
@@ -751,7 +871,7 @@ int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep) {
     if (!g) return SWAMP_E_ARG;
     if (!g->parts.empty()) return group_advance(g, 1, true, rep);
     cudaSetDevice(g->device);
-    if (g->profiling) {
+    if (g->profiling && g->graphT) {
         CK(cudaGraphLaunch(g->graphT, g->stream));
     } else {
         CK(cudaGraphLaunch(g->graph1, g->stream));
@@ -854,6 +974,7 @@ int swamp_gpu_copy_leaves(swamp_gpu* g, uint32_t* leaves, uint32_t* nw, uint32_t
     const uint32_t N = g->ctl_host->n_leaves;
     if (n) *n = N;
     if (!leaves && !nw && !ne && !nn && !ns) return SWAMP_OK;
+    if (g->rank_world > 1) return SWAMP_E_STATE;  // a rank holds only its own slice: count only
     if (cap < static_cast<int64_t>(N)) return SWAMP_E_ARG;
     // Morton-ordered LeafAssembly of the current tree (the hot path keeps the
     // level-L leaves first)
@@ -981,6 +1102,89 @@ int swamp_gpu_counters(swamp_gpu* g, int64_t* out4) {
     out4[2] = static_cast<int64_t>(g->ctl_host->cnt_new);
     out4[3] = int64_t(1) << (2 * g->P.L);
     return st;
+}
+
+int swamp_gpu_rank_create(const swamp_config* cfg, const double* h, const double* qx, const double* qy,
+                          const double* z, int rank, int world, int device, swamp_gpu** out, uint8_t* blob) {
+    if (!out || !blob || !h || !qx || !qy || !z || world < 1 || world > hwfv1::kMaxParts || rank < 0 || rank >= world)
+        return SWAMP_E_ARG;
+    *out = nullptr;
+    int st = validate(cfg);
+    if (st) return st;
+    auto* g = new swamp_gpu();
+    if ((st = setup_part(g, cfg, h, qx, qy, z, device, world, rank))) {
+        delete g;
+        return st;
+    }
+    g->rank_world = world;
+    RankBlob b{};
+    b.magic = kRankMagic;
+    b.rank = rank;
+    b.world = world;
+    b.device = device;
+    b.pid = static_cast<uint64_t>(getpid());
+    for (int k = 0; k < 7; ++k) {
+        void* p = rank_ptr(g, k);
+        b.ptr[k] = reinterpret_cast<uint64_t>(p);
+        if (cudaIpcGetMemHandle(&b.ipc[k], p) != cudaSuccess) {
+            delete g;
+            return SWAMP_E_CUDA;
+        }
+    }
+    std::memset(blob, 0, SWAMP_RANK_BLOB_BYTES);
+    std::memcpy(blob, &b, sizeof(b));
+    *out = g;
+    return SWAMP_OK;
+}
+
+int swamp_gpu_rank_connect(swamp_gpu* g, const uint8_t* blobs) {
+    if (!g || !blobs || g->rank_world < 1) return SWAMP_E_ARG;
+    cudaSetDevice(g->device);
+    const int W = g->rank_world, me = g->P.part;
+    const uint64_t pid = static_cast<uint64_t>(getpid());
+    for (int r = 0; r < W; ++r) {
+        RankBlob b;
+        std::memcpy(&b, blobs + static_cast<size_t>(r) * SWAMP_RANK_BLOB_BYTES, sizeof(b));
+        if (b.magic != kRankMagic || b.rank != r || b.world != W) return SWAMP_E_ARG;
+        void* p[7];
+        if (r == me) {
+            for (int k = 0; k < 7; ++k) p[k] = rank_ptr(g, k);
+        } else if (b.pid == pid) {  // another rank handle of this process: its pointers directly
+            if (b.device != g->device) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return SWAMP_E_CUDA;
+                cudaGetLastError();
+            }
+            for (int k = 0; k < 7; ++k) p[k] = reinterpret_cast<void*>(b.ptr[k]);
+        } else {  // another process: open its CUDA IPC handles (NVLink peer mapping)
+            for (int k = 0; k < 7; ++k) {
+                if (cudaIpcOpenMemHandle(&p[k], b.ipc[k], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    g->err = "cudaIpcOpenMemHandle failed";
+                    return SWAMP_E_CUDA;
+                }
+                g->ipc_opened.push_back(p[k]);
+            }
+        }
+        g->P.pcells[r][0] = static_cast<double4*>(p[0]);
+        g->P.pcells[r][1] = static_cast<double4*>(p[1]);
+        g->P.psig[r][0] = static_cast<uint8_t*>(p[2]);
+        g->P.psig[r][1] = static_cast<uint8_t*>(p[3]);
+        g->P.ppre[r] = static_cast<uint8_t*>(p[4]);
+        g->P.ptile_cnt[r] = static_cast<uint32_t*>(p[5]);
+        g->P.pctl[r] = static_cast<Ctl*>(p[6]);
+    }
+    part_enqueue_init(g);  // completes once every rank has connected (device barriers)
+    return cudaGetLastError() == cudaSuccess ? SWAMP_OK : SWAMP_E_CUDA;
+}
+
+int swamp_gpu_rank_ready(swamp_gpu* g) {
+    if (!g || g->rank_world < 1) return SWAMP_E_ARG;
+    cudaSetDevice(g->device);
+    int st = fetch_ctl(g);
+    if (st) return st;
+    part_after_init(g);
+    if ((st = part_build_graphs(g))) return st;
+    return fetch_ctl(g);
 }
 
 #define SWAMP_STR2(x) #x

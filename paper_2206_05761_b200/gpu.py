@@ -18,6 +18,7 @@ import numpy as np
 from .abi import STATUS, SimConfig, as_f64, dptr, level_offset, swamp_config, swamp_step_report, u8ptr, u32ptr
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
+RANK_BLOB_BYTES = 1024  # SWAMP_RANK_BLOB_BYTES (include/swamp_gpu.h)
 LIB_PATH = os.environ.get("SWAMP_GPU_LIB") or os.path.join(_HERE, "libswamp_gpu.so")
 _LIB = None
 
@@ -40,6 +41,10 @@ def lib():
         L.swamp_gpu_create_uniform.argtypes = L.swamp_gpu_create.argtypes
         L.swamp_gpu_create_partitioned.argtypes = [C.POINTER(swamp_config), dp, dp, dp, dp, C.c_int,
                                                    C.POINTER(C.c_int), C.POINTER(P)]
+        L.swamp_gpu_rank_create.argtypes = [C.POINTER(swamp_config), dp, dp, dp, dp, C.c_int, C.c_int, C.c_int,
+                                            C.POINTER(P), C.POINTER(C.c_uint8)]
+        L.swamp_gpu_rank_connect.argtypes = [P, C.POINTER(C.c_uint8)]
+        L.swamp_gpu_rank_ready.argtypes = [P]
         L.swamp_gpu_destroy.argtypes = [P]
         L.swamp_gpu_step.argtypes = [P, rp]
         L.swamp_gpu_advance.argtypes = [P, C.c_int64, rp]
@@ -68,6 +73,7 @@ EXPORTED_SYMBOLS = (
     "swamp_gpu_copy_leaves", "swamp_gpu_export_tree", "swamp_gpu_export_finest", "swamp_gpu_last_error",
     "swamp_gpu_counters", "swamp_gpu_build_info", "swamp_gpu_enqueue", "swamp_gpu_stream",
     "swamp_gpu_timeline", "swamp_gpu_create_partitioned", "swamp_gpu_debug",
+    "swamp_gpu_rank_create", "swamp_gpu_rank_connect", "swamp_gpu_rank_ready",
 )
 
 
@@ -78,7 +84,8 @@ class SwampError(RuntimeError):
 class Engine:
     """SimState owner on one GPU."""
 
-    def __init__(self, cfg: SimConfig, h, qx, qy, z, device: int = 0, uniform: bool = False, parts=None):
+    def __init__(self, cfg: SimConfig, h, qx, qy, z, device: int = 0, uniform: bool = False, parts=None,
+                 rank=None):
         self.cfg = cfg
         self.L = int(cfg.L)
         self.uniform = uniform
@@ -88,7 +95,13 @@ class Engine:
         if any(a.size != n for a in arrs):
             raise ValueError(f"fields must be 2^L x 2^L = {cfg.side} x {cfg.side}")
         self._h = C.c_void_p()
-        if parts is not None:  # Morton-subtree partitions: list of CUDA devices, one per partition
+        self.blob = None
+        if rank is not None:  # one partition of a multi-process engine: (rank, world); connect() follows
+            r, w = rank
+            self.blob = (C.c_uint8 * RANK_BLOB_BYTES)()
+            st = lib().swamp_gpu_rank_create(C.byref(self._c), *[dptr(a) for a in arrs], int(r), int(w), int(device),
+                                              C.byref(self._h), self.blob)
+        elif parts is not None:  # Morton-subtree partitions: list of CUDA devices, one per partition
             devs = (C.c_int * len(parts))(*[int(d) for d in parts])
             st = lib().swamp_gpu_create_partitioned(C.byref(self._c), *[dptr(a) for a in arrs], len(parts), devs,
                                                      C.byref(self._h))
@@ -98,6 +111,15 @@ class Engine:
         if st != 0:
             raise SwampError(f"initialise failed: {STATUS.get(st, st)}")
         self.report = swamp_step_report()
+
+    def connect(self, blobs):
+        """Rank engines: map the peers (all ranks' blobs, rank order) and enqueue initialise."""
+        buf = (C.c_uint8 * (RANK_BLOB_BYTES * len(blobs))).from_buffer_copy(b"".join(bytes(b) for b in blobs))
+        self._check(lib().swamp_gpu_rank_connect(self._h, buf), "rank_connect")
+
+    def ready(self):
+        """Rank engines: wait for initialise (every rank connected) and build the step graphs."""
+        self._check(lib().swamp_gpu_rank_ready(self._h), "rank_ready")
 
     def close(self):
         if getattr(self, "_h", None):
@@ -205,6 +227,17 @@ def initialise_partitioned(cfg: SimConfig, h, qx, qy, z, devices) -> Engine:
     """Morton-subtree partitioned engine: partition k on CUDA device devices[k]
     (repeat a device to run virtual partitions on one GPU)."""
     return Engine(cfg, h, qx, qy, z, parts=list(devices))
+
+
+def initialise_rank(cfg: SimConfig, h, qx, qy, z, rank: int, world: int, device: int, allgather) -> Engine:
+    """One Morton-subtree partition per process (torchrun rank): partition
+    `rank` of `world` on CUDA `device`. `allgather(bytes) -> list[bytes]`
+    exchanges the ranks' CUDA IPC blobs (rank order), e.g.
+    paper_2206_05761_b200.ranks.torch_allgather."""
+    e = Engine(cfg, h, qx, qy, z, device=device, rank=(rank, world))
+    e.connect(allgather(bytes(e.blob)))
+    e.ready()
+    return e
 
 
 def initialise_uniform(cfg: SimConfig, h, qx, qy, z, device: int = 0) -> Engine:

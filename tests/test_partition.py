@@ -85,3 +85,37 @@ def test_gloo_two_partitions_concatenate_to_global_leaf_list(L):
     assert r0[1] == r1[0]              # contiguous subtree ranges
     assert l0 + l1 == full             # Morton-order concatenation
     assert len(l0) > 0 and len(l1) > 0
+
+
+def _blob_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2206_05761_b200.ranks import max_over_ranks, torch_allgather
+
+    # a stand-in for this rank's CUDA IPC blob: fixed size, rank-specific bytes
+    blob = bytes([rank]) * 7 + bytes(range(256)) * 4
+    got = torch_allgather(blob[:1024])
+    slowest = max_over_ranks(0.5 + rank)
+    out.put((rank, [g[:8] for g in got], len(got[0]), slowest))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_rank_blob_exchange():
+    """The one-process-per-GPU engine's host plumbing (ranks.py) on CPU:
+    every rank receives every rank's IPC blob in rank order, and timings
+    reduce to the max over ranks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_blob_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(), q.get()])
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    for rank, heads, size, slowest in res:
+        assert heads == [bytes([0]) * 7 + b"\x00", bytes([1]) * 7 + b"\x00"]
+        assert size == 1024 and slowest == 1.5
