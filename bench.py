@@ -12,10 +12,11 @@ export). L2 is flushed (256 MiB write) before every timed step.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Under torchrun (N > 1) the same L = 11 problem is split into N Morton-subtree
-partitions, one per GPU (strong scaling): rank 0 drives the partitioned
-engine over all N devices (cross-partition reads go through peer pointers over
-NVLink), the other ranks only join the barriers; the step time is partition
-0's device time, which waits for every partition at each phase.
+partitions, one per GPU and per process (strong scaling): each rank creates
+its partition on its GPU, the ranks exchange CUDA IPC handles over gloo and
+then read each other's arrays in place over NVLink, synchronising on the
+device between phases. Each rank times its own stream with CUDA events; the
+reported step time is the max over ranks.
 
 `--impl reference` times the CPU-HWFV1 oracle (oracle/, the spec
 restatement — the reference ships no engine to build) on this host's cores,
@@ -196,38 +197,29 @@ def main():
 
     ws, rank, local = dist_env()
     if ws > 1:
-        # one process per GPU is launched; the partitioned engine is driven by
-        # rank 0 over all N GPUs (peer access across NVLink / NVSwitch) and the
-        # other ranks only join the coordination barriers (gloo, CPU)
         import torch.distributed as dist
 
-        dist.init_process_group("gloo")
-        if rank != 0:
-            dist.barrier()
-            dist.destroy_process_group()
-            return 0
-    dev = 0 if ws > 1 else local
+        dist.init_process_group("gloo")  # host plumbing only: IPC blobs, barriers, max over ranks
+    ndev = torch.cuda.device_count()
+    dev = local % ndev  # more ranks than GPUs only when testing the multi-process path on a small box
     torch.cuda.set_device(dev)
     from paper_2206_05761_b200 import gpu
+    from paper_2206_05761_b200.ranks import max_over_ranks, torch_allgather
 
     cfg, h, qx, qy, z = cases.river_flood(L=args.L, epsilon=args.eps)
     parallelism = "single"
     if ws > 1:
-        try:
-            eng = gpu.initialise_partitioned(cfg, h, qx, qy, z, list(range(ws)))
-            parallelism = f"morton-subtree x{ws} (one engine over {ws} GPUs, peer reads)"
-        except Exception as e:  # pragma: no cover - depends on the box
-            print(f"partitioned engine unavailable ({e}); running replicas", file=sys.stderr)
-            eng = gpu.initialise(cfg, h, qx, qy, z, device=dev)
-            parallelism = "replica (partitioned engine unavailable)"
+        eng = gpu.initialise_rank(cfg, h, qx, qy, z, rank, ws, dev, torch_allgather)
+        parallelism = f"morton-subtree x{ws} (one process per GPU, CUDA IPC peer reads, device barriers)"
+        if ws > ndev:
+            parallelism += f" [oversubscribed: {ws} ranks on {ndev} GPU(s), time-sliced — not a scaling number]"
     elif args.virtual_parts > 1:
         eng = gpu.initialise_partitioned(cfg, h, qx, qy, z, [dev] * args.virtual_parts)
         parallelism = f"morton-subtree x{args.virtual_parts} virtual partitions on one GPU"
     else:
         eng = gpu.initialise(cfg, h, qx, qy, z, device=dev)
     stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=torch.device("cuda", dev))
-    n_flush = ws if ws > 1 else 1
-    flush = [torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{d if ws > 1 else dev}") for d in range(n_flush)]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
 
@@ -240,19 +232,19 @@ def main():
     updates = 0
     dev_ms = 0.0
     leaves = []
-    for d in range(n_flush):
-        torch.cuda.synchronize(d if ws > 1 else dev)
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
     with ClockSampler(dev) as clk:
         wall0 = time.perf_counter()
         for _ in range(args.steps):
-            for d in range(n_flush):  # L2 flush (256 MiB > 126 MB L2) of every GPU ...
-                flush[d].fill_(1)
-                torch.cuda.synchronize(d if ws > 1 else dev)
+            flush.fill_(1)  # L2 flush (256 MiB > 126 MB L2) ...
+            torch.cuda.synchronize(dev)
             ev0.record(stream)  # ... outside the timed interval
-            eng.enqueue(1)      # one adaptive step (graph replay; partitioned: every phase on every GPU)
+            eng.enqueue(1)      # one adaptive step (graph replay; ranks meet on the device between phases)
             ev1.record(stream)
             ev1.synchronize()
-            dev_ms += ev0.elapsed_time(ev1)  # partition 0's stream waits for every partition at each phase
+            dev_ms += ev0.elapsed_time(ev1)
             r = eng.advance(0)  # StepReport of that step (leaf count, device stage timeline)
             updates += r["n_leaves"]
             leaves.append(r["n_leaves"])
@@ -261,7 +253,10 @@ def main():
         torch.cuda.synchronize(dev)
         wall = time.perf_counter() - wall0
     c1 = eng.counters()
-    dev_ms_max, updates_all = dev_ms, float(updates)
+    # every rank updates the same global leaf set (n_leaves is global); the
+    # slowest rank bounds the step
+    dev_ms_max = max_over_ranks(dev_ms) if ws > 1 else dev_ms
+    updates_all = float(updates)
 
     K = args.steps
     n_mean = updates / K
@@ -296,25 +291,33 @@ def main():
 
     # ---- e2e through the public API with host buffers
     e2e = None
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()  # every rank done before any rank frees memory its peers map
+    del eng
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    e = (gpu.initialise_rank(cfg, h, qx, qy, z, rank, ws, dev, torch_allgather) if ws > 1
+         else gpu.initialise(cfg, h, qx, qy, z, device=dev))
+    up = 0
+    for _ in range(K):
+        r = e.step_adaptive()  # each step reads its StepReport back
+        up += r["n_leaves"]
+    fh, fqx, fqy = e.export_finest()  # (rank 0's copy is the whole grid: peer reads)
+    e2e_s = time.perf_counter() - t0
+    if ws > 1:
+        e2e_s = max_over_ranks(e2e_s)
+        dist.barrier()
+    del e
     if rank == 0:
-        del eng
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        e = (gpu.initialise_partitioned(cfg, h, qx, qy, z, list(range(ws))) if ws > 1 and "morton" in parallelism
-             else gpu.initialise(cfg, h, qx, qy, z, device=dev))
-        up = 0
-        for _ in range(K):
-            r = e.step_adaptive()  # each step reads its StepReport back
-            up += r["n_leaves"]
-        fh, fqx, fqy = e.export_finest()
-        e2e_s = time.perf_counter() - t0
         nf = 4 ** args.L
         h2d = 4 * nf * 8
         d2h = 3 * nf * 8 + K * 96
         e2e = {"value": up / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d // K, "d2h_bytes_per_step": d2h // K,
                "seconds": e2e_s,
                "note": "initialise from host rasters + K steps (StepReport read-back each) + finest export"}
-        del e
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -351,7 +354,8 @@ def main():
         "clocks": clk.summary(),
         "sim_runtimes_s": sims,
     }
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
