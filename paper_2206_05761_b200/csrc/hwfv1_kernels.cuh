@@ -381,6 +381,36 @@ __device__ __forceinline__ unsigned block_exscan(unsigned v, unsigned* scratch, 
     return warp_prefix + x - v;
 }
 
+// Block-wide exclusive scan of 64-bit values (two 32-bit counts packed as
+// hi:lo, neither total reaching 2^32); returns the prefix, *total = sum.
+__device__ __forceinline__ unsigned long long block_exscan64(unsigned long long v, unsigned long long* scratch,
+                                                             unsigned long long* total) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(kFull, x, o);
+        if (l >= o) x += y;
+    }
+    __syncthreads();
+    if (l == 31) scratch[w] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        unsigned long long s = (l < kThreads / 32) ? scratch[l] : 0ull;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(kFull, s, o);
+            if (l >= o) s += y;
+        }
+        if (l < kThreads / 32) scratch[l] = s;
+    }
+    __syncthreads();
+    const unsigned long long warp_prefix = (w == 0) ? 0ull : scratch[w - 1];
+    *total = scratch[kThreads / 32 - 1];
+    __syncthreads();
+    return warp_prefix + x - v;
+}
+
 // last-CTA election: every CTA fences its global writes, then bumps a counter
 __device__ __forceinline__ bool last_block(unsigned int* counter, int* s_flag) {
     __syncthreads();
@@ -1375,36 +1405,67 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     __syncthreads();
     stamp(0);
 
-    // ---- band + closure of levels R-1 .. 0 (hot path)
+    // ---- band (D3) of every top cell at once (band depends on pre flags only)
     if (!EXPORT) {
-        for (int n = R - 1; n >= 0; --n) {
-            const uint32_t cnt_n = 1u << (2 * n);
-            for (uint32_t m = threadIdx.x; m < cnt_n; m += kThreads) {
-                uint8_t b = band_flag(P.band_mode, L, n, m, [&](int k, uint32_t mm) -> uint8_t {
-                    return k < R ? tp[slo(k) + mm] : P.ppre[owner_of(P, k, mm)][slo(k) + mm];
-                });
-                if (*reinterpret_cast<const uint32_t*>(ts + slo(n + 1) + 4u * m)) b = 1;
-                ts[slo(n) + m] = b;
-            }
-            __syncthreads();
+        for (uint32_t q = threadIdx.x; q < lo(R, 0); q += kThreads) {
+            const int n = (31 - __clz(3u * q + 1u)) >> 1;  // level of compact index q
+            const uint32_t m = q - lo(n, 0);
+            ts[slo(n) + m] = band_flag(P.band_mode, L, n, m, [&](int k, uint32_t mm) -> uint8_t {
+                return k < R ? tp[slo(k) + mm] : P.ppre[owner_of(P, k, mm)][slo(k) + mm];
+            });
         }
     }
-    stamp(1);
-    // ---- on-tree flags top-down (closure makes significance upward-closed:
-    //      a cell is on the tree iff its parent is significant and on it) and
-    //      the first subtree under each top-level leaf
-    if (threadIdx.x == 0) ti[0] = 1;
     __syncthreads();
-    for (int n = 0; n < R; ++n) {
-        const uint32_t cnt_n = 1u << (2 * n);
-        for (uint32_t m = threadIdx.x; m < cnt_n; m += kThreads) {
-            const bool in = ti[slo(n) + m] != 0, sg = ts[slo(n) + m] != 0;
-            *reinterpret_cast<uint32_t*>(ti + slo(n + 1) + 4u * m) = (in && sg) ? 0x01010101u : 0u;
-            if (in && !sg) cbf[m << (2 * (R - n))] = 1;
-        }
+    stamp(1);
+    // ---- one warp: closure bottom-up (hot path), then the on-tree flags
+    //      top-down and the first subtree under each top-level leaf (closure
+    //      makes significance upward-closed: a cell is on the tree iff its
+    //      parent is significant and on it); the other warps clear cbf
+    // closure of level R-1 (the largest) by every thread, the rest by warp 0
+    if (!EXPORT && R >= 1) {
+        for (uint32_t m = threadIdx.x; m < (1u << (2 * (R - 1))); m += kThreads)
+            if (*reinterpret_cast<const uint32_t*>(ts + slo(R) + 4u * m)) ts[slo(R - 1) + m] = 1;
         __syncthreads();
     }
+    auto ontree = [&](int n, uint32_t m) {
+        const bool in = ti[slo(n) + m] != 0, sg = ts[slo(n) + m] != 0;
+        *reinterpret_cast<uint32_t*>(ti + slo(n + 1) + 4u * m) = (in && sg) ? 0x01010101u : 0u;
+        if (in && !sg) cbf[m << (2 * (R - n))] = 1;
+    };
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        if (!EXPORT)
+            for (int n = R - 2; n >= 0; --n) {
+                for (uint32_t m = lane; m < (1u << (2 * n)); m += 32)
+                    if (*reinterpret_cast<const uint32_t*>(ts + slo(n + 1) + 4u * m)) ts[slo(n) + m] = 1;
+                __syncwarp();
+            }
+        if (lane == 0) ti[0] = 1;
+        __syncwarp();
+        for (int n = 0; n < R - 1; ++n) {
+            for (uint32_t m = lane; m < (1u << (2 * n)); m += 32) ontree(n, m);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    // on-tree flags of level R (subtree roots) from level R-1, every thread
+    if (R >= 1) {
+        for (uint32_t m = threadIdx.x; m < (1u << (2 * (R - 1))); m += kThreads) ontree(R - 1, m);
+        __syncthreads();
+    } else if (threadIdx.x == 0) {
+        ti[0] = 1;
+    }
+    if (R == 0) __syncthreads();
     const uint8_t* reach = ti + fb;
+    // newly significant top cells (decode sources exist only below them)
+    unsigned nnew = 0;
+    if (!EXPORT)
+        for (uint32_t q = threadIdx.x; q < lo(R, 0); q += kThreads) {
+            const int n = (31 - __clz(3u * q + 1u)) >> 1;
+            const uint32_t a = slo(n) + (q - lo(n, 0));
+            nnew += (ts[a] && !tv[a]) ? 1u : 0u;
+        }
+    const unsigned tn = EXPORT ? 0u : block_sum(nnew, s_red);
     stamp(2);
 
     // ---- per-subtree counts, scans, depth and decode source
@@ -1423,9 +1484,12 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         la += ca;
         lb += cb;
     }
-    unsigned ta, tb;
-    unsigned oa = block_exscan(la, s_red, &ta);
-    unsigned ob = block_exscan(lb, s_red, &tb);
+    __shared__ unsigned long long s_red64[kThreads / 32];
+    unsigned long long tot64;
+    const unsigned long long o64 =
+        block_exscan64((static_cast<unsigned long long>(la) << 32) | lb, s_red64, &tot64);
+    const unsigned ta = static_cast<unsigned>(tot64 >> 32), tb = static_cast<unsigned>(tot64);
+    unsigned oa = static_cast<unsigned>(o64 >> 32), ob = static_cast<unsigned>(o64);
     stamp(3);
     const uint32_t full = 1u << (2 * P.K);  // level-L leaves of a fully refined subtree
     const bool strips = !EXPORT && P.strips && P.G == 1 && P.K == 6;
@@ -1433,7 +1497,34 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     for (uint32_t t = a; t < b; ++t) {
         unsigned ca, cb;
         counts(t, ca, cb);
+        uint32_t src = kNoSrc;
+        int n = R;
+        if (!reach[t]) {
+            n = 0;
+            while (ts[slo(n) + (t >> (2 * (R - n)))]) ++n;
+        } else if (!EXPORT && tn) {
+            for (int k = 0; k < R; ++k) {
+                const uint32_t q = slo(k) + (t >> (2 * (R - k)));
+                if (ts[q] && !tv[q]) {
+                    src = zo::z_of(k, t >> (2 * (R - k)));
+                    break;
+                }
+            }
+        }
+        P.tile_lvl[t] = static_cast<uint32_t>(n) | (cbf[t] ? kEmit : 0u);
+        P.tile_off[2 * nt + t] = oa + ob;
         if (!EXPORT) {
+            P.tile_off[t] = oa;
+            P.tile_off[nt + t] = ta + ob;
+            P.tile_src[t] = src;
+            if (t == P.tile_lo) {
+                s_off[0] = oa;
+                s_off[1] = ta + ob;
+            }
+            if (t == P.tile_hi) {
+                s_off[2] = oa;
+                s_off[3] = ta + ob;
+            }
             // FV1 dry shortcut: subtree t is active if it or a face-adjacent
             // subtree holds a wet cell, or it touches an inflow edge; clear
             // the flags FV1 sets next
@@ -1449,35 +1540,6 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
             P.wet[tbuf ^ 1][t] = 0;
             nst += st;
         }
-        if (!EXPORT) {
-            P.tile_off[t] = oa;
-            P.tile_off[nt + t] = ta + ob;
-            if (t == P.tile_lo) {
-                s_off[0] = oa;
-                s_off[1] = ta + ob;
-            }
-            if (t == P.tile_hi) {
-                s_off[2] = oa;
-                s_off[3] = ta + ob;
-            }
-        }
-        P.tile_off[2 * nt + t] = oa + ob;
-        int n = R;
-        uint32_t src = kNoSrc;
-        if (!reach[t]) {
-            n = 0;
-            while (ts[slo(n) + (t >> (2 * (R - n)))]) ++n;
-        } else if (!EXPORT) {
-            for (int k = 0; k < R; ++k) {
-                const uint32_t q = slo(k) + (t >> (2 * (R - k)));
-                if (ts[q] && !tv[q]) {
-                    src = zo::z_of(k, t >> (2 * (R - k)));
-                    break;
-                }
-            }
-        }
-        P.tile_lvl[t] = static_cast<uint32_t>(n) | (cbf[t] ? kEmit : 0u);
-        if (!EXPORT) P.tile_src[t] = src;
         oa += ca;
         ob += cb;
     }
@@ -1491,27 +1553,28 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         s_off[3] = ta + tb;
     }
     // ---- the strip-path subtree list (Morton order)
-    {
+    if (strips) {
         unsigned tot;
         unsigned os = block_exscan(nst, s_red, &tot);
-        for (uint32_t t = a; t < b; ++t)
-            if (P.tact[t] & 2u) P.stile[os++] = t;  // (this thread's own writes: ordered)
+        if (nst)
+            for (uint32_t t = a; t < b; ++t)
+                if (P.tact[t] & 2u) P.stile[os++] = t;  // (this thread's own writes: ordered)
         if (threadIdx.x == 0) {
             ctl->n_stile = tot;
             ctl->dbg[40] += tot;  // diagnostics: strip-path subtrees so far
         }
+    } else if (threadIdx.x == 0) {
+        ctl->n_stile = 0;
     }
-    // ---- final flags of levels < R, newly significant top cells, projection
-    //      (D4) of top cells on the tree below a newly significant ancestor
-    unsigned nnew = 0;
-    for (int n = 0; n < R; ++n)
-        for (uint32_t m = threadIdx.x; m < (1u << (2 * n)); m += kThreads) {
-            const uint32_t q = slo(n) + m;
-            P.sig[p ^ 1][q] = ts[q];
-            nnew += (ts[q] && !tv[q]) ? 1u : 0u;
-        }
-    const unsigned tn = block_sum(nnew, s_red);  // (barrier: s_off complete)
-    if (threadIdx.x == 0) {
+    __syncthreads();  // s_off complete
+    // ---- final flags of levels < R, projection (D4) of top cells on the tree
+    //      below a newly significant ancestor
+    for (uint32_t q = threadIdx.x; q < lo(R, 0); q += kThreads) {
+        const int n = (31 - __clz(3u * q + 1u)) >> 1;
+        const uint32_t a2 = slo(n) + (q - lo(n, 0));
+        P.sig[p ^ 1][a2] = ts[a2];
+    }
+    if (threadIdx.x == 0) {  // (block_exscan above: s_off complete)
         if (tn && P.part == 0) atomicAdd(&ctl->cnt_new, (unsigned long long)tn);
         ctl->n_leaves = ta + tb;
         ctl->n_leaves_A = ta;
