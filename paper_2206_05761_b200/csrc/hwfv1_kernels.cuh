@@ -1015,6 +1015,218 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
     stamp(5);
 }
 
+// K1, persistent and double-buffered: ~2 CTAs per SM loop over the
+// subtrees; while subtree j is encoded, subtree j + stride's flags and
+// values arrive by TMA bulk copies and, as soon as its level-(L-2) flags are
+// in, its level-(L-1) children by per-thread cp.async (only under
+// previous-tree parents). Level L-2 is encoded thread-per-child (conflict-
+// free shared-memory reads) with quad shuffles, levels L-3..R as in
+// k_encode_step. Same arithmetic as k_encode_step.
+constexpr int kK1Stages = 2;
+__device__ __forceinline__ void cp_async_wait_group0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+__device__ __forceinline__ Enc encode_lanes_t(double4 v, const double* thr4) {
+    const int lane = threadIdx.x & 31;
+    auto red = [&](double x) {
+        const double x1 = __shfl_sync(kFull, x, (lane + 1) & 31);
+        const double x2 = __shfl_sync(kFull, x, (lane + 2) & 31);
+        const double x3 = __shfl_sync(kFull, x, (lane + 3) & 31);
+        return red4(x, x1, x2, x3);
+    };
+    const Red h = red(v.x);
+    const Red qx = red(v.y);
+    const Red qy = red(v.z);
+    const Red z = red(v.w);
+    Enc e;
+    e.flow = sig_q(h.dmax, thr4[0]) || sig_q(qx.dmax, thr4[1]) || sig_q(qy.dmax, thr4[2]);
+    e.par = make_double4(h.par, qx.par, qy.par, z.par);
+    e.zflag = false;
+    return e;
+}
+
+template <int KT>
+__global__ void __launch_bounds__(kThreads, 2) k_encode_pipe(Params P, Ctl* ctl) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ __align__(8) unsigned long long mbar[kK1Stages];
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+    }
+    const Head hd = cta_head(ctl, P, false);  // (its barrier also publishes the mbarrier inits)
+    if (!hd.active) return;
+    tl_start(ctl, hd.buf, 0);
+    extern __shared__ __align__(128) uint8_t sm1[];
+    __shared__ unsigned s_red[32];
+    __shared__ double s_thr[kMaxL][4];
+    stage_thresholds(P, s_thr);
+    const int p = hd.parity;
+    double4* buf = P.cells[p];
+    const uint8_t* sigp = P.sig[p];
+    const int L = P.L, R = P.R;
+    const int K = KT ? KT : P.K;
+    const int k2 = K - 2;                               // tile level of L-2 (K >= 2 here)
+    const uint32_t c2 = 1u << (2 * k2);                 // level-(L-2) cells of a subtree
+    const uint32_t nch = 4u * c2;                       // level-(L-1) children
+    const uint32_t nv = lo(K - 1, 0);                   // cells on levels R..L-2
+    const uint32_t sl = slo(K);
+    const size_t stage_bytes = 32u * (nch + nv) + 3u * sl + 16u;
+    auto st_ch = [&](int s) { return reinterpret_cast<double4*>(sm1 + s * stage_bytes); };
+    auto st_sv = [&](int s) { return reinterpret_cast<double4*>(sm1 + s * stage_bytes + 32u * nch); };
+    auto st_sf = [&](int s) { return sm1 + s * stage_bytes + 32u * (nch + nv); };
+    auto st_sd = [&](int s) { return st_sf(s) + sl; };
+    auto st_so = [&](int s) { return st_sf(s) + 2u * sl; };
+    auto st_small = [&](int s) { return reinterpret_cast<uint32_t*>(st_sf(s) + 3u * sl); };  // level-R words
+
+    // bulk copies of subtree j into stage s: flags of levels R+2..L-1, values
+    // of levels R+1..L-2 (one thread); the level-R / R+1 flag words by cp.async
+    auto issue_bulk = [&](uint32_t j, int s) {
+        if (threadIdx.x == 0) {
+            unsigned bytes = 0;
+            for (int k = 2; k < K; ++k) bytes += 2u << (2 * k);
+            for (int k = 1; k <= K - 2; ++k) bytes += 32u << (2 * k);
+            mbar_expect_tx(&mbar[s], bytes);
+            for (int k = 2; k < K; ++k) {
+                const uint32_t cnt = 1u << (2 * k);
+                const unsigned long long g = slo(R + k) + static_cast<unsigned long long>(j) * cnt;
+                bulk_g2s(st_sf(s) + slo(k), sigp + g, cnt, &mbar[s]);
+                bulk_g2s(st_sd(s) + slo(k), P.dem + g, cnt, &mbar[s]);
+            }
+            for (int k = 1; k <= K - 2; ++k) {
+                const uint32_t cnt = 1u << (2 * k);
+                bulk_g2s(st_sv(s) + lo(k, 0), buf + cbase(R + k) + static_cast<unsigned long long>(j) * cnt,
+                         32u * cnt, &mbar[s]);
+            }
+        }
+        if (threadIdx.x == 32) {
+            cp_async4(st_sf(s) + slo(1), sigp + slo(R + 1) + 4ull * j);
+            cp_async4(st_sd(s) + slo(1), P.dem + slo(R + 1) + 4ull * j);
+            cp_async4(st_small(s), sigp + slo(R) + (j & ~3u));
+            cp_async4(st_small(s) + 1, P.dem + slo(R) + (j & ~3u));
+        }
+    };
+    // children of subtree j's previous-tree level-(L-2) cells (after its flags)
+    auto issue_children = [&](uint32_t j, int s) {
+        const uint8_t* f2 = st_sf(s) + slo(k2);
+        for (uint32_t t = threadIdx.x; t < c2; t += kThreads)
+            if (f2[t]) {
+                const uint8_t* g = reinterpret_cast<const uint8_t*>(buf + cbase(L - 1) + ((j * c2 + t) << 2));
+                uint8_t* d = reinterpret_cast<uint8_t*>(st_ch(s) + 4u * t);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) cp_async16(d + 16 * q, g + 16 * q);
+            }
+        cp_async_commit();
+    };
+
+    unsigned tree = 0;
+    const uint32_t stride = gridDim.x;
+    uint32_t j = P.tile_lo + blockIdx.x;
+    unsigned ph[kK1Stages] = {0u, 0u};
+    int s = 0;
+    if (j < P.tile_hi) {
+        issue_bulk(j, 0);
+        mbar_wait(&mbar[0], 0);
+        ph[0] ^= 1u;
+        issue_children(j, 0);
+    }
+    for (; j < P.tile_hi; j += stride, s ^= 1) {
+        const uint32_t jn = j + stride;
+        const bool more = jn < P.tile_hi;
+        if (more) issue_bulk(jn, s ^ 1);
+        cp_async_wait_group0();  // this subtree's children and small flag words
+        __syncthreads();
+        double4* sv = st_sv(s);
+        uint8_t* sf = st_sf(s);
+        uint8_t* sd = st_sd(s);
+        uint8_t* so = st_so(s);
+        if (threadIdx.x == 0) {
+            const uint32_t* w = st_small(s);
+            sf[0] = (w[0] >> (8 * (j & 3u))) & 0xFFu;
+            sd[0] = (w[1] >> (8 * (j & 3u))) & 0xFFu;
+        }
+        // ---- level L-1: cells off the previous tree only get pre = DEM | (eps == 0)
+        {
+            const int k = K - 1;
+            const uint32_t cnt = 1u << (2 * k);
+            const uint32_t zero = (0.0 >= s_thr[L - 1][3]) ? 0x01010101u : 0u;
+            const unsigned long long g = slo(L - 1) + static_cast<unsigned long long>(j) * cnt;
+            for (uint32_t c = 4u * threadIdx.x; c < cnt; c += 4u * kThreads) {
+                const uint32_t f = *reinterpret_cast<const uint32_t*>(sf + slo(k) + c);
+                if (f == 0x01010101u) continue;
+                const uint32_t v = zero | *reinterpret_cast<const uint32_t*>(sd + slo(k) + c);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (!byte_of(f, q)) P.pre[g + c + q] = byte_of(v, q) ? 1 : 0;
+            }
+        }
+        // ---- level L-2: thread per child, quads reduce by shuffles
+        {
+            const double4* ch = st_ch(s);
+            const int lane = threadIdx.x & 31;
+            const double* thr = s_thr[L - 2];
+            const bool zero2 = 0.0 >= thr[3];
+            for (uint32_t c = threadIdx.x; c < nch; c += kThreads) {  // warp-uniform trip count (nch % 32 == 0 or < 32)
+                const uint32_t t = c >> 2;
+                const Enc e = encode_lanes_t(ch[c], thr);
+                if ((lane & 3) == 0) {
+                    bool flow = zero2;
+                    if (sf[slo(k2) + t]) {
+                        flow = e.flow;
+                        sv[lo(k2, 0) + t] = e.par;
+                        ++tree;
+                    }
+                    so[slo(k2) + t] = (flow || sd[slo(k2) + t]) ? 1 : 0;
+                }
+            }
+        }
+        __syncthreads();  // children of stage s consumed; level L-2 results visible
+        if (more) {       // the next subtree's children fly while levels L-3..R are encoded
+            mbar_wait(&mbar[s ^ 1], ph[s ^ 1]);
+            ph[s ^ 1] ^= 1u;
+            issue_children(jn, s ^ 1);
+        }
+        // ---- levels L-3 .. R in shared memory
+#pragma unroll
+        for (int k = (KT ? KT : kMaxL) - 3; k >= 0; --k) {
+            if (!KT && k > K - 3) continue;
+            const int n = R + k;
+            const uint32_t cnt = 1u << (2 * k);
+            for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
+                bool flow = 0.0 >= s_thr[n][3];
+                if (sf[slo(k) + pi]) {
+                    const uint32_t c0 = lo(k + 1, 0) + 4u * pi;
+                    const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
+                    const Enc e = encode_children_t(c, s_thr[n]);
+                    flow = e.flow;
+                    sv[lo(k, 0) + pi] = e.par;
+                    ++tree;
+                }
+                so[slo(k) + pi] = (flow || sd[slo(k) + pi]) ? 1 : 0;
+            }
+            __syncthreads();
+        }
+        // ---- stores: re-encoded values (previous-tree cells), pre-band flags of levels R..L-2
+        for (int k = 0; k <= K - 2; ++k) {
+            const uint32_t cnt = 1u << (2 * k);
+            const unsigned long long jb = static_cast<unsigned long long>(j) * cnt;
+            for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads)
+                if (sf[slo(k) + pi]) st4(buf + cbase(R + k) + jb + pi, sv[lo(k, 0) + pi]);
+            if (cnt >= 4) {
+                for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads)
+                    *reinterpret_cast<uint32_t*>(P.pre + slo(R + k) + jb + q) =
+                        *reinterpret_cast<const uint32_t*>(so + slo(k) + q);
+            } else if (threadIdx.x == 0) {
+                P.pre[slo(R) + jb] = so[0];
+            }
+        }
+        __syncthreads();  // stage s free for subtree j + 2 stride
+    }
+    const unsigned tsum = block_sum(tree, s_red);
+    if (threadIdx.x == 0 && tsum) atomicAdd(&ctl->cnt_tree, (unsigned long long)tsum);
+    tl_end(ctl, hd.buf, 0);
+}
+
 // Levels R-1 .. 0 of the re-encode after t = 0, one CTA (run as the extra
 // CTA of K2, concurrently with the subtree CTAs). Round trip 1 stages the
 // previous-tree and DEM flags of levels 0..R-1; round trip 2 loads the

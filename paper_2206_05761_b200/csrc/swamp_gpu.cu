@@ -50,7 +50,8 @@ struct swamp_gpu {
     int fv1_grid = 0;
     int fv1_minb = 2;  // occupancy variant of k_fv1 (SWAMP_FV1_MINB=3|4 for more CTAs/SM, with spills)
     int num_sms = 0;
-    size_t smem_k1 = 0, smem_k1s = 0, smem_k2 = 0, smem_k3 = 0;
+    size_t smem_k1 = 0, smem_k1s = 0, smem_k1p = 0, smem_k2 = 0, smem_k3 = 0;
+    int k1p_grid = 0;     // persistent K1 (K = 6): CTAs
     // tile kernels, specialised for K = 6 (every L >= 6) or generic
     void (*k1)(Params, Ctl*) = nullptr;
     void (*k2)(Params, Ctl*, int, int) = nullptr;
@@ -152,7 +153,10 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
         for (int k = 1; k < 5; ++k) mark(k);
         return;
     }
-    launch_pdl(g->k1, P.n_tiles, g->smem_k1s, s, P, g->ctl);
+    if (g->k1p_grid)
+        launch_pdl(hwfv1::k_encode_pipe<6>, g->k1p_grid, g->smem_k1p, s, P, g->ctl);
+    else
+        launch_pdl(g->k1, P.n_tiles, g->smem_k1s, s, P, g->ctl);
     if (P.top_mode == 2) launch_pdl(hwfv1::k_encode_top<false>, 1, g->smem_k1, s, P, g->ctl);
     mark(1);
     const int do_top = P.top_mode == 1 ? 1 : 0;
@@ -413,6 +417,8 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         }
         g->smem_k1 = ncell * (sizeof(double4) + 1);                  // k_encode<true> / k_encode_top
         g->smem_k1s = 32 * (((size_t(1) << (2 * (K - 1))) - 1) / 3) + 3 * sl;
+        // persistent K1: 2 stages of (children + values + 3 flag slices + small words)
+        g->smem_k1p = 2 * (32 * ((size_t(1) << (2 * (K - 1))) + ((size_t(1) << (2 * (K - 1))) - 1) / 3) + 3 * sl + 16);
         P.top_mode = (R == 0) ? 0 : (R <= 6 ? 1 : 2);
         const size_t k2_tile = 2 * sl;
         const size_t k2_top = P.top_mode == 1 ? 32 * ltop + 2 * fb : 0;
@@ -427,6 +433,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
                      {reinterpret_cast<const void*>(hwfv1::k_encode<true>), g->smem_k1},
                      {reinterpret_cast<const void*>(hwfv1::k_encode_top<true>), g->smem_k1},
                      {reinterpret_cast<const void*>(hwfv1::k_encode_top<false>), g->smem_k1},
+                     {reinterpret_cast<const void*>(hwfv1::k_encode_pipe<6>), g->smem_k1p},
                      {reinterpret_cast<const void*>(g->k2), g->smem_k2},
                      {reinterpret_cast<const void*>(g->k3), g->smem_k3},
                      {reinterpret_cast<const void*>(g->k3x), g->smem_k3}};
@@ -440,6 +447,14 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         if (const char* e = std::getenv("SWAMP_FV1_MINB")) g->fv1_minb = std::max(2, std::min(4, std::atoi(e)));
         const char* es = std::getenv("SWAMP_FV1_STRIPS");
         P.strips = (es && es[0] == '1') ? 1 : 0;
+        // persistent double-buffered K1 for K = 6, opt-in (SWAMP_K1_PIPE=1): measured
+        // slower than one CTA per subtree (latency chains, fewer CTAs in flight)
+        const char* ep = std::getenv("SWAMP_K1_PIPE");
+        if (P.K == 6 && ep && ep[0] == '1') {
+            int occ1 = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, hwfv1::k_encode_pipe<6>, kThreads, g->smem_k1p);
+            g->k1p_grid = std::max(1, std::min<int>(static_cast<int>(P.tiles_per_part), std::max(1, occ1) * g->num_sms));
+        }
         int occ = 0;
         if (g->fv1_minb == 4)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 4>, kThreads, 0);
@@ -527,7 +542,10 @@ void part_barrier(swamp_gpu* q, cudaStream_t s) { hwfv1::k_part_barrier<<<1, 32,
 bool part_step_phase(swamp_gpu* q, int k, cudaStream_t s) {
     const Params& P = q->P;
     switch (k) {
-        case 0: q->k1<<<P.tiles_per_part, kThreads, q->smem_k1s, s>>>(P, q->ctl); return true;
+        case 0:
+            if (q->k1p_grid) hwfv1::k_encode_pipe<6><<<q->k1p_grid, kThreads, q->smem_k1p, s>>>(P, q->ctl);
+            else q->k1<<<P.tiles_per_part, kThreads, q->smem_k1s, s>>>(P, q->ctl);
+            return true;
         case 1:
             if (P.top_mode != 2) return false;
             hwfv1::k_encode_top<false><<<1, kThreads, q->smem_k1, s>>>(P, q->ctl);

@@ -168,3 +168,16 @@ def test_active_subtree_paths(monkeypatch, strips, name, kw):
             compare_states(g, o, f"{name} strips={strips} step {k}")
     if strips:
         assert g.debug()[40] > 0, "no subtree took the strip path"
+
+
+def test_persistent_k1_variant(monkeypatch):
+    """Opt-in persistent double-buffered K1 (SWAMP_K1_PIPE=1) == the oracle."""
+    monkeypatch.setenv("SWAMP_K1_PIPE", "1")
+    cfg, h, qx, qy, z = cases.river_flood(L=9)
+    g = gpu.initialise(cfg, h, qx, qy, z)
+    o = O.Oracle(cfg, h, qx, qy, z)
+    for k in range(1, 21):
+        g.step_adaptive()
+        o.step()
+        if k in (1, 20):
+            compare_states(g, o, f"K1 pipe step {k}")
