@@ -145,6 +145,7 @@ struct Params {
     // 32 x 8 strips (k_fv1 fv1_strip); tact bit 1 marks them, stile lists them
     uint32_t* stile;
     int strips;           // strip path enabled (SWAMP_FV1_STRIPS=1; measured slower on B200)
+    int quad;             // sibling-quad path (SWAMP_FV1_QUAD=1; measured slower on B200)
     // Morton-subtree partitions: this partition owns level-R
     // subtrees [tile_lo, tile_hi); cells on levels >= R belong to their
     // subtree's partition, cells above R are replicated except that a leaf's
@@ -2334,9 +2335,98 @@ __device__ void fv1_strip(const Params& P, Ctl* ctl, const double4* __restrict__
     __syncwarp();  // bsm reused by the warp's next strip
 }
 
+// FV1 of one level-L leaf whose sibling quadruple sits in lanes 4k..4k+3
+// (child c = lane & 3 at (c & 1, c >> 1)): the two siblings' cell states
+// come by shuffles, only the two outside neighbours are gathered, and each
+// lane computes one of the quad's four inner faces (c0: c0|c1, c3: c2|c3 in
+// x; c1: c1|c3, c2: c0|c2 in y) and receives the other from its partner —
+// 3 faces, 3 make_cell and 2 gathers per leaf instead of 4, 5, 4. face() and
+// fv1_finish() with the per-leaf path's (left, right) arguments: same bits.
+// Every lane of the warp must call it (shuffles); `skip` lanes (dry subtree,
+// strip path) only take part in the exchange.
+__device__ __forceinline__ void fv1_quad(const Params& P, const double4* __restrict__ cur,
+                                         const uint8_t* __restrict__ sigc, uint32_t m, const double4 o4, bool skip,
+                                         double dt, double inflow, double& hn, double& qxn, double& qyn) {
+    const int L = P.L;
+    const int lane = threadIdx.x & 31;
+    const int c = lane & 3;
+    const PhysParams& ph = P.phys;
+    // outside neighbours: W or E, S or N
+    const int dx = (c & 1) ? 1 : 0, dy = (c & 2) ? 2 : 3;
+    uint32_t nmx = zo::kNone, nmy = zo::kNone;
+    double4 rx = make_double4(0.0, 0.0, 0.0, 0.0), ry = rx;
+    if (!skip) {
+        nmx = zo::neighbour_dev(L, m, static_cast<zo::Direction>(dx));
+        nmy = zo::neighbour_dev(L, m, static_cast<zo::Direction>(dy));
+        const uint8_t fx = (nmx != zo::kNone) ? sigc[slo(L - 1) + (nmx >> 2)] : 1;
+        const uint8_t fy = (nmy != zo::kNone) ? sigc[slo(L - 1) + (nmy >> 2)] : 1;
+        const double4* sx = fx ? cur + cbase(L) + nmx : covering_local(P, cur, sigc, L - 1, nmx >> 2);
+        const double4* sy = fy ? cur + cbase(L) + nmy : covering_local(P, cur, sigc, L - 1, nmy >> 2);
+        if (nmx != zo::kNone) rx = ld4_nc(sx);
+        if (nmy != zo::kNone) ry = ld4_nc(sy);
+    }
+    const CellV own = make_cell(o4, ph);
+    const CellV px = shfl_cell(own, lane ^ 1), py = shfl_cell(own, lane ^ 2);
+    // this lane's inner face
+    const bool ix = (c == 0 || c == 3);        // x pair (c0|c1 or c2|c3), else y pair
+    const bool own_left = (c == 0 || c == 1);  // own on the west / south side
+    double Fi[3], hLi, hRi;
+    {
+        const CellV& q = ix ? px : py;
+        if (own_left) face(own, q, ix, ph, Fi, hLi, hRi);
+        else face(q, own, ix, ph, Fi, hLi, hRi);
+    }
+    // the other inner face from its owner (c0 <- c2, c1 <- c0, c2 <- c3, c3 <- c1)
+    const int src = ix ? (lane ^ 2) : (lane ^ 1);
+    double Fr[3];
+    Fr[0] = __shfl_sync(kFull, Fi[0], src);
+    Fr[1] = __shfl_sync(kFull, Fi[1], src);
+    Fr[2] = __shfl_sync(kFull, Fi[2], src);
+    const double hLr = __shfl_sync(kFull, hLi, src), hRr = __shfl_sync(kFull, hRi, src);
+    if (skip) return;
+    bool all_dry = own.h < ph.hdry && px.h < ph.hdry && py.h < ph.hdry;
+    all_dry = all_dry && ((nmx != zo::kNone) ? rx.x < ph.hdry : P.bc[dx] != 2);
+    all_dry = all_dry && ((nmy != zo::kNone) ? ry.x < ph.hdry : P.bc[dy] != 2);
+    if (all_dry) {  // the dry-neighbourhood result (same bits as the general path)
+        hn = (o4.x < 0.0) ? 0.0 : o4.x;
+        qxn = 0.0;
+        qyn = 0.0;
+        return;
+    }
+    const CellV ex = (nmx != zo::kNone) ? make_cell(rx, ph) : boundary_cell(own, P.bc[dx], dx, inflow, P.inflow_mode, ph);
+    const CellV ey = (nmy != zo::kNone) ? make_cell(ry, ph) : boundary_cell(own, P.bc[dy], dy, inflow, P.inflow_mode, ph);
+    double Fox[3], Foy[3], hL, hR, hox, hoy;  // outside faces and own side's reconstructed depth
+    if (dx == 1) { face(own, ex, true, ph, Fox, hL, hR); hox = hL; }   // E: own left
+    else { face(ex, own, true, ph, Fox, hL, hR); hox = hR; }          // W: own right
+    if (dy == 2) { face(own, ey, false, ph, Foy, hL, hR); hoy = hL; }  // N: own south
+    else { face(ey, own, false, ph, Foy, hL, hR); hoy = hR; }         // S: own north
+    // inner faces as seen by this lane: x inner (c0: E = own, c1: W = recv,
+    // c2: E = recv, c3: W = own), y inner (c0: N = recv, c1: N = own,
+    // c2: S = own, c3: S = recv); own side depth hL when own is west/south
+    // (scalar selects: no pointers into register arrays, no local memory)
+    const double Fx0 = ix ? Fi[0] : Fr[0], Fx1 = ix ? Fi[1] : Fr[1], Fx2 = ix ? Fi[2] : Fr[2];
+    const double Fy0 = ix ? Fr[0] : Fi[0], Fy1 = ix ? Fr[1] : Fi[1], Fy2 = ix ? Fr[2] : Fi[2];
+    const double hxi = (c & 1) ? (ix ? hRi : hRr) : (ix ? hLi : hLr);  // c1, c3 right of the x face
+    const double hyi = (c & 2) ? (ix ? hRr : hRi) : (ix ? hLr : hLi);  // c2, c3 north of the y face
+    const bool ce = (c & 1) != 0, cn = (c & 2) != 0;
+    const double FE[3] = {ce ? Fox[0] : Fx0, ce ? Fox[1] : Fx1, ce ? Fox[2] : Fx2};
+    const double FW[3] = {ce ? Fx0 : Fox[0], ce ? Fx1 : Fox[1], ce ? Fx2 : Fox[2]};
+    const double FN[3] = {cn ? Foy[0] : Fy0, cn ? Foy[1] : Fy1, cn ? Foy[2] : Fy2};
+    const double FS[3] = {cn ? Fy0 : Foy[0], cn ? Fy1 : Foy[1], cn ? Fy2 : Foy[2]};
+    const double hE = ce ? hox : hxi, hW = ce ? hxi : hox;
+    const double hN = cn ? hoy : hyi, hS = cn ? hyi : hoy;
+    const double h = own.h, hh = h * h;
+    const double FE1 = FE[1] + (ph.half_g * (hh - (hE * hE)));
+    const double FW1 = FW[1] + (ph.half_g * (hh - (hW * hW)));
+    const double GN1 = FN[1] + (ph.half_g * (hh - (hN * hN)));
+    const double GS1 = FS[1] + (ph.half_g * (hh - (hS * hS)));
+    fv1_finish(own, FE[0] - FW[0], FE1 - FW1, FE[2] - FW[2], FN[0] - FS[0], GN1 - GS1, FN[2] - FS[2],
+               inv_dx_of(P, L), dt, ph, hn, qxn, qyn);
+}
+
 // FV1 over the leaf list: persistent grid-stride, one thread per
 // leaf; reads the current buffer, writes leaf slots of the other (D15).
-template <bool UNIFORM, int MINB = 2, bool PART = false, bool STRIPS = false>
+template <bool UNIFORM, int MINB = 2, bool PART = false, bool STRIPS = false, bool QUAD = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     pdl_wait();
     pdl_trigger();
@@ -2404,7 +2494,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
         const uint8_t ta = (!UNIFORM && !PART && valid && n >= P.R) ? P.tact[m >> (2 * (n - P.R))] : 1;
         if (STRIPS && (ta & 2u)) valid = false;  // updated by the strip path above
         double hn = 0.0, qxn = 0.0, qyn = 0.0, zown = 0.0;
-        if (valid) {
+        // a warp of whole sibling quadruples of level-L leaves: the quad path
+        const bool quadw = QUAD && !UNIFORM && !PART && wbase + 32u <= NA;
+        if (quadw) {
+            const double4 o4 = ld4_nc(cur + cbase(n) + m);
+            fv1_quad(P, cur, sigc, m, o4, !valid || ta == 0, dt, inflow, hn, qxn, qyn);
+            if (valid && ta == 0) {  // dry subtree
+                hn = (o4.x < 0.0) ? 0.0 : o4.x;
+                qxn = 0.0;
+                qyn = 0.0;
+            }
+            zown = o4.w;
+        }
+        if (valid && !quadw) {
             // every global read of this leaf is issued before any arithmetic:
             // own cell, the neighbours' parent-level flags, the neighbours
             const double4 o4 = ld4_nc(cur + cbase(n) + m);
@@ -2469,6 +2571,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             }
             }  // !quiet
             zown = o4.w;
+        }
+        if (valid) {
             // mark the subtree(s) of a leaf that ends wet (a leaf above level R
             // marks every subtree under it)
             if (!UNIFORM && !PART && !(hn < P.phys.hdry)) {

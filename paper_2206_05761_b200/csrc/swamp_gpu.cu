@@ -167,6 +167,8 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     const size_t sm5 = P.strips ? sizeof(double4) * (kThreads / 32) * hwfv1::kStripSlots : 0;
     if (P.strips)
         launch_pdl(hwfv1::k_fv1<false, 2, false, true>, g->fv1_grid, sm5, s, P, g->ctl);
+    else if (P.quad)
+        launch_pdl(hwfv1::k_fv1<false, 2, false, false, true>, g->fv1_grid, 0, s, P, g->ctl);
     else if (g->fv1_minb == 4)
         launch_pdl(hwfv1::k_fv1<false, 4>, g->fv1_grid, sm5, s, P, g->ctl);
     else if (g->fv1_minb == 3)
@@ -447,6 +449,8 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         if (const char* e = std::getenv("SWAMP_FV1_MINB")) g->fv1_minb = std::max(2, std::min(4, std::atoi(e)));
         const char* es = std::getenv("SWAMP_FV1_STRIPS");
         P.strips = (es && es[0] == '1') ? 1 : 0;
+        const char* eq = std::getenv("SWAMP_FV1_QUAD");
+        P.quad = (eq && eq[0] == '1') ? 1 : 0;
         // persistent double-buffered K1 for K = 6, opt-in (SWAMP_K1_PIPE=1): measured
         // slower than one CTA per subtree (latency chains, fewer CTAs in flight)
         const char* ep = std::getenv("SWAMP_K1_PIPE");
