@@ -203,6 +203,12 @@ int swamp_gpu_timeline(swamp_gpu* g, double* out12);
  * of K1 ([0, 16)) and K3 ([16, 32)) of the last step; [8 * c + 7] = entry. */
 int swamp_gpu_debug(swamp_gpu* g, uint64_t* out64);
 
+/* compare: L1 = sum |h_A - h_B| dx^2 / area and L-infinity
+ * of the depths of two engines on the same device and grid (finest-grid
+ * expansions, both at their current times). SWAMP_E_ARG on mismatched
+ * grids. Deterministic. */
+int swamp_gpu_compare(swamp_gpu* a, swamp_gpu* b, double* l1, double* linf);
+
 /* Build identification (arch, flags) for logs. */
 const char* swamp_gpu_build_info(void);
 

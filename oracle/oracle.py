@@ -272,3 +272,60 @@ def morton_decode(m):
 def neighbour(n, m, d):
     r = lib().oracle_neighbour(n, m, d)
     return None if r < 0 else r
+
+
+# ---------------------------------------------------------------- io
+def load_dem_ref(values, xll, yll, cs, nodata, L, x0, y0, W, wall_z):
+    """numpy restatement of load_dem, the checker of
+    swamp_io_load_dem: finest-cell centres sampled nearest-cell when the raster
+    cellsize equals W / 2^L, bilinear between raster cell centres otherwise
+    (edge cells clamped); outside / nodata -> inactive with z = wall_z.
+    values[row, col] with row 0 the TOP row; returns (z, inactive) with row 0
+    the SOUTH row. Same IEEE operations, same order as the C++."""
+    vals = np.asarray(values, dtype=np.float64)
+    nr, nc = vals.shape
+    side = 1 << L
+    dx = W / side
+    z = np.full((side, side), wall_z)
+    ina = np.ones((side, side), dtype=bool)
+
+    def val(ci, rj):
+        return vals[nr - 1 - rj, ci]
+
+    def nod(v):
+        return v == nodata or not np.isfinite(v)
+
+    for j in range(side):
+        for i in range(side):
+            x = x0 + (i + 0.5) * dx
+            y = y0 + (j + 0.5) * dx
+            if dx == cs:
+                fi, fj = np.floor((x - xll) / cs), np.floor((y - yll) / cs)
+                if 0 <= fi < nc and 0 <= fj < nr:
+                    v = val(int(fi), int(fj))
+                    if not nod(v):
+                        z[j, i], ina[j, i] = v, False
+            else:
+                u = (x - xll) / cs - 0.5
+                w = (y - yll) / cs - 0.5
+                if -0.5 <= u <= nc - 0.5 and -0.5 <= w <= nr - 0.5:
+                    i0, j0 = int(np.floor(u)), int(np.floor(w))
+                    a, b = u - i0, w - j0
+                    if i0 < 0:
+                        i0, a = 0, 0.0
+                    if j0 < 0:
+                        j0, b = 0, 0.0
+                    if i0 >= nc - 1:
+                        i0, a = nc - 1, 0.0
+                    if j0 >= nr - 1:
+                        j0, b = nr - 1, 0.0
+                    i1 = i0 + 1 if i0 + 1 < nc else i0
+                    j1 = j0 + 1 if j0 + 1 < nr else j0
+                    v00, v10, v01, v11 = val(i0, j0), val(i1, j0), val(i0, j1), val(i1, j1)
+                    bad = nod(v00) or (a > 0 and nod(v10)) or (b > 0 and nod(v01)) or (a > 0 and b > 0 and nod(v11))
+                    if not bad:
+                        s0 = v00 + a * (v10 - v00) if a > 0 else v00
+                        s1 = v01 + a * (v11 - v01) if a > 0 else v01
+                        z[j, i] = s0 + b * (s1 - s0) if b > 0 else s0
+                        ina[j, i] = False
+    return z, ina

@@ -14,11 +14,12 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libswamp_gpu.so")
-SOURCES = [os.path.join(HERE, "csrc", "swamp_gpu.cu")]
+SOURCES = [os.path.join(HERE, "csrc", "swamp_gpu.cu"), os.path.join(HERE, "csrc", "swamp_io.cpp")]
 DEPS = SOURCES + [
     os.path.join(HERE, "csrc", "hwfv1_kernels.cuh"),
     os.path.join(HERE, "csrc", "hwfv1_physics.cuh"),
     os.path.join(ROOT, "include", "swamp_gpu.h"),
+    os.path.join(ROOT, "include", "swamp_io.h"),
     os.path.join(ROOT, "include", "swamp", "zorder.hpp"),
 ]
 

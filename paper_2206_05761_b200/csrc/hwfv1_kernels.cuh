@@ -2741,4 +2741,36 @@ __global__ void k_export_finest(Params P, const Ctl* ctl, double* h, double* qx,
     }
 }
 
+// compare: per-block partial sums and maxima of |hA - hB|
+// over the finest expansions (fixed grid, so the host's in-order sum of the
+// partials is deterministic)
+__global__ void k_compare(const double* a, const double* b, uint64_t n, double* part_sum, double* part_max) {
+    __shared__ double ss[kThreads / 32], sm[kThreads / 32];
+    double s = 0.0, mx = 0.0;
+    for (uint64_t k = blockIdx.x * (uint64_t)kThreads + threadIdx.x; k < n; k += (uint64_t)gridDim.x * kThreads) {
+        const double d = absd(a[k] - b[k]);
+        s += d;
+        mx = max2(mx, d);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(kFull, s, o);
+        mx = max2(mx, __shfl_xor_sync(kFull, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        ss[threadIdx.x >> 5] = s;
+        sm[threadIdx.x >> 5] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0, m = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) {
+            t += ss[w];
+            m = max2(m, sm[w]);
+        }
+        part_sum[blockIdx.x] = t;
+        part_max[blockIdx.x] = m;
+    }
+}
+
 }  // namespace hwfv1

@@ -1209,6 +1209,41 @@ int swamp_gpu_rank_ready(swamp_gpu* g) {
     return fetch_ctl(g);
 }
 
+int swamp_gpu_compare(swamp_gpu* a, swamp_gpu* b, double* l1, double* linf) {
+    if (!a || !b || !l1 || !linf) return SWAMP_E_ARG;
+    swamp_gpu* ga = a->parts.empty() ? a : a->parts[0];
+    swamp_gpu* gb = b->parts.empty() ? b : b->parts[0];
+    if (ga->P.L != gb->P.L || ga->P.W != gb->P.W) return SWAMP_E_ARG;  // mismatched grids
+    if (ga->device != gb->device) return SWAMP_E_ARG;
+    if (!a->parts.empty() && group_sync(a)) return SWAMP_E_CUDA;
+    if (!b->parts.empty() && group_sync(b)) return SWAMP_E_CUDA;
+    swamp_gpu* g = ga;
+    cudaSetDevice(ga->device);
+    const size_t nf = static_cast<size_t>(1) << (2 * ga->P.L);
+    const int blocks = std::max(1, std::min<int>(ga->num_sms * 4, static_cast<int>((nf + kThreads - 1) / kThreads)));
+    double* d = nullptr;
+    CK(cudaMalloc(&d, (6 * nf + 2 * blocks) * sizeof(double)));
+    cudaStreamSynchronize(gb->stream);
+    hwfv1::k_export_finest<<<std::max(1, ga->num_sms * 8), kThreads, 0, ga->stream>>>(ga->P, ga->ctl, d, d + nf, d + 2 * nf);
+    hwfv1::k_export_finest<<<std::max(1, ga->num_sms * 8), kThreads, 0, ga->stream>>>(gb->P, gb->ctl, d + 3 * nf,
+                                                                                       d + 4 * nf, d + 5 * nf);
+    hwfv1::k_compare<<<blocks, kThreads, 0, ga->stream>>>(d, d + 3 * nf, nf, d + 6 * nf, d + 6 * nf + blocks);
+    std::vector<double> part(2 * static_cast<size_t>(blocks));
+    cudaError_t e = cudaMemcpyAsync(part.data(), d + 6 * nf, part.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                    ga->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ga->stream);
+    cudaFree(d);
+    CK(e);
+    double s = 0.0, m = 0.0;
+    for (int k = 0; k < blocks; ++k) {
+        s += part[k];
+        m = std::max(m, part[blocks + k]);
+    }
+    *l1 = s / static_cast<double>(nf);  // sum |dh| dx^2 / area over the square: the mean
+    *linf = m;
+    return SWAMP_OK;
+}
+
 #define SWAMP_STR2(x) #x
 #define SWAMP_STR(x) SWAMP_STR2(x)
 const char* swamp_gpu_build_info(void) {

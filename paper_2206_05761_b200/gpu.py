@@ -45,6 +45,7 @@ def lib():
                                             C.POINTER(P), C.POINTER(C.c_uint8)]
         L.swamp_gpu_rank_connect.argtypes = [P, C.POINTER(C.c_uint8)]
         L.swamp_gpu_rank_ready.argtypes = [P]
+        L.swamp_gpu_compare.argtypes = [P, P, dp, dp]
         L.swamp_gpu_destroy.argtypes = [P]
         L.swamp_gpu_step.argtypes = [P, rp]
         L.swamp_gpu_advance.argtypes = [P, C.c_int64, rp]
@@ -73,7 +74,8 @@ EXPORTED_SYMBOLS = (
     "swamp_gpu_copy_leaves", "swamp_gpu_export_tree", "swamp_gpu_export_finest", "swamp_gpu_last_error",
     "swamp_gpu_counters", "swamp_gpu_build_info", "swamp_gpu_enqueue", "swamp_gpu_stream",
     "swamp_gpu_timeline", "swamp_gpu_create_partitioned", "swamp_gpu_debug",
-    "swamp_gpu_rank_create", "swamp_gpu_rank_connect", "swamp_gpu_rank_ready",
+    "swamp_gpu_rank_create", "swamp_gpu_rank_connect", "swamp_gpu_rank_ready", "swamp_gpu_compare",
+    "swamp_io_read_esri", "swamp_io_write_esri", "swamp_io_free_raster", "swamp_io_load_dem", "swamp_io_write_finest",
 )
 
 
@@ -211,6 +213,13 @@ class Engine:
         a = (C.c_uint64 * 64)()
         self._check(lib().swamp_gpu_debug(self._h, a), "debug")
         return list(a)
+
+    def compare(self, other) -> dict:
+        """compare: L1 and L-infinity of the depth against
+        another engine on the same device and grid."""
+        l1, li = C.c_double(), C.c_double()
+        self._check(lib().swamp_gpu_compare(self._h, other._h, C.byref(l1), C.byref(li)), "compare")
+        return {"L1": l1.value, "Linf": li.value}
 
     def counters(self):
         a = (C.c_int64 * 4)()

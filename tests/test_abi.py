@@ -13,13 +13,13 @@ import pytest
 from paper_2206_05761_b200 import abi, gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HDR = os.path.join(ROOT, "include", "swamp_gpu.h")
+HDRS = [os.path.join(ROOT, "include", "swamp_gpu.h"), os.path.join(ROOT, "include", "swamp_io.h")]
 BUILD = os.path.join(ROOT, "tests", "cpp", "_build")
 
 
 def declared_functions():
-    src = open(HDR).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(swamp_gpu_\w+)\s*\(", src, re.M)))
+    src = "".join(open(h).read() for h in HDRS)
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(swamp_(?:gpu|io)_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
