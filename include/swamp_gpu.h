@@ -189,10 +189,11 @@ int swamp_gpu_export_finest(swamp_gpu* g, double* h, double* qx, double* qy);
 int swamp_gpu_last_error(const swamp_gpu* g, int32_t* code, uint32_t* z, int32_t* quantity,
                          int32_t* stage, char* msg, size_t msg_cap);
 
-/* Per-step counters of the last stepped grid, for roofline bookkeeping:
- * [0] leaves N, [1] significant tree cells (prev tree, re-encoded),
- * [2] newly significant cells (decoded), [3] 4^L. */
-int swamp_gpu_counters(swamp_gpu* g, int64_t* out4);
+/* Counters for roofline bookkeeping: [0] leaves N of the last step, [1]
+ * significant tree cells re-encoded (cumulative), [2] newly significant cells
+ * decoded (cumulative), [3] 4^L, [4] leaf updates of all steps (sum of N,
+ * cumulative), [5..7] reserved (0). */
+int swamp_gpu_counters(swamp_gpu* g, int64_t* out8);
 
 /* Device timeline of the last step, microseconds from K1's first CTA: for
  * K1, K2, K3, K5 (k = 0..3): [3k] first CTA start, [3k+1] unused (-1),

@@ -59,6 +59,7 @@ struct Ctl {
     unsigned int done_k1, done_k5;
     alignas(128) unsigned long long cnt_tree;    // cells re-encoded by the last K1
     alignas(128) unsigned long long cnt_new;     // newly significant cells decoded by the last K3
+    unsigned long long cnt_updates;              // leaf updates of all steps so far (sum of N)
     alignas(128) unsigned long long k3_ready;    // K3's top CTA published its results (epoch)
     uint32_t n_stile;                            // subtrees on FV1's strip path this step
     alignas(128) unsigned long long smax_bits[4];
@@ -2054,6 +2055,7 @@ __device__ void finalize_dt(const Params& P, Ctl* ctl, double maxrate, bool adva
         ctl->step += 1;
         ctl->parity ^= 1;
         ctl->n_leaves_used = ctl->n_leaves;
+        ctl->cnt_updates += ctl->n_leaves;
     }
     ctl->dt = dt;
     ctl->t_next = tn;

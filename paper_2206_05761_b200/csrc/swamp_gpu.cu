@@ -1103,26 +1103,29 @@ int swamp_gpu_debug(swamp_gpu* g, uint64_t* out64) {
     return st;
 }
 
-int swamp_gpu_counters(swamp_gpu* g, int64_t* out4) {
-    if (!g || !out4) return SWAMP_E_ARG;
+int swamp_gpu_counters(swamp_gpu* g, int64_t* out8) {
+    if (!g || !out8) return SWAMP_E_ARG;
     if (!g->parts.empty()) {
-        int64_t acc[4] = {0, 0, 0, 0};
+        int64_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (swamp_gpu* q : g->parts) {
-            int64_t c[4];
+            int64_t c[8];
             const int st = swamp_gpu_counters(q, c);
             if (st) return st;
             for (int k = 1; k < 3; ++k) acc[k] += c[k];
             acc[0] = c[0];
             acc[3] = c[3];
+            acc[4] = c[4];  // global leaf counts: every partition holds the same sum
         }
-        std::memcpy(out4, acc, sizeof(acc));
+        std::memcpy(out8, acc, sizeof(acc));
         return SWAMP_OK;
     }
     int st = fetch_ctl(g);
-    out4[0] = g->uniform ? (int64_t(1) << (2 * g->P.L)) : g->ctl_host->n_leaves_used;
-    out4[1] = static_cast<int64_t>(g->ctl_host->cnt_tree);
-    out4[2] = static_cast<int64_t>(g->ctl_host->cnt_new);
-    out4[3] = int64_t(1) << (2 * g->P.L);
+    out8[0] = g->uniform ? (int64_t(1) << (2 * g->P.L)) : g->ctl_host->n_leaves_used;
+    out8[1] = static_cast<int64_t>(g->ctl_host->cnt_tree);
+    out8[2] = static_cast<int64_t>(g->ctl_host->cnt_new);
+    out8[3] = int64_t(1) << (2 * g->P.L);
+    out8[4] = static_cast<int64_t>(g->ctl_host->cnt_updates);
+    out8[5] = out8[6] = out8[7] = 0;
     return st;
 }
 

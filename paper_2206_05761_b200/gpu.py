@@ -222,9 +222,10 @@ class Engine:
         return {"L1": l1.value, "Linf": li.value}
 
     def counters(self):
-        a = (C.c_int64 * 4)()
+        """[N last step, re-encoded cells (cum.), decoded cells (cum.), 4^L, leaf updates (cum.)]"""
+        a = (C.c_int64 * 8)()
         self._check(lib().swamp_gpu_counters(self._h, a), "counters")
-        return list(a)
+        return list(a)[:5]
 
 
 def initialise(cfg: SimConfig, h, qx, qy, z, device: int = 0) -> Engine:
