@@ -42,6 +42,7 @@ struct SimConfig {
     Band band = Band::Neighbours;
     bool inflow_is_eta = false;
     std::vector<double> inflow_t, inflow_v, output_times;
+    std::vector<uint8_t> inactive;  // 4^L finest cells (south row first), empty = all active (D16)
 
     void validate() const {
         if (L < 1 || L > zorder::kMaxLevel) throw std::invalid_argument("SimConfig: L outside [1, 13]");
@@ -74,6 +75,7 @@ struct SimConfig {
         c.inflow_v = inflow_v.empty() ? nullptr : inflow_v.data();
         c.n_outputs = static_cast<int32_t>(output_times.size());
         c.output_times = output_times.empty() ? nullptr : output_times.data();
+        c.inactive = inactive.empty() ? nullptr : inactive.data();
         return c;
     }
 };

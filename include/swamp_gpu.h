@@ -80,6 +80,11 @@ typedef struct swamp_config {
     const double* inflow_t; /* inflow series times, ascending                   */
     const double* inflow_v; /* inflow series values                             */
     const double* output_times; /* ascending; dt is clipped to hit them        */
+    /* inactive finest cells (D16): 4^L bytes,
+     * row-major south row first, nonzero = inactive (a reflective wall,
+     * excluded from CFL and s_max; its state is kept); NULL = all active.
+     * swamp_io_load_dem produces it from a DEM's nodata / outside cells. */
+    const uint8_t* inactive;
 } swamp_config;
 
 /* StepReport. Stage times are device times in ms of the

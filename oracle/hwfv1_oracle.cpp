@@ -309,6 +309,8 @@ struct oracle_state {
     bool uniform = false;
     std::vector<double> s[4];                  // HierarchyField per quantity (h, qx, qy, z), s-units
     std::vector<uint8_t> sig, sig_prev, dem;   // over detail cells (levels 0..L-1)
+    std::vector<uint8_t> ina;                  // over all cells: every finest descendant inactive (D16)
+    bool has_ina = false;
     std::vector<double> det[3][3];             // DetailField (dα,dβ,dγ) of h, qx, qy
     double smax[4] = {0, 0, 0, 0};
     std::vector<uint32_t> recorded;            // RecordedGrid
@@ -567,6 +569,7 @@ double leaves_max_rate(const oracle_state& S) {
     double mn = 0.0;
 #pragma omp parallel for schedule(static) reduction(max : mn)
     for (int64_t i = 0; i < N; ++i) {
+        if (S.has_ina && S.ina[S.leaves[i]]) continue;  // D16
         double u[4];
         cell_phys(S, S.leaves[i], u);
         const int n = o_level_of(S.leaves[i]);
@@ -593,16 +596,24 @@ bool fv1_all(oracle_state& S, double* maxrate) {
         const int n = o_level_of(zl);
         double own[4], nb[4][4];
         cell_phys(S, zl, own);
+        const double dx = std::ldexp(S.cfg.width, -n);
+        double out[3];
+        if (S.has_ina && S.ina[zl]) {  // D16: an inactive leaf keeps its state, no CFL
+            U[3 * i + 0] = own[0];
+            U[3 * i + 1] = own[1];
+            U[3 * i + 2] = own[2];
+            continue;
+        }
         for (int d = 0; d < 4; ++d) {
             const uint32_t desc = S.nbr[d][i];
             if (desc >= kBoundaryBase)
                 boundary_state(own, (int)(desc - kBoundaryBase), d, t, S.inflow_t.data(), S.inflow_v.data(),
                                (int)S.inflow_t.size(), S.cfg.inflow_mode, p.hdry, nb[d]);
+            else if (S.has_ina && S.ina[desc])  // D16: an inactive neighbour is a reflective wall
+                boundary_state(own, SWAMP_BC_REFLECTIVE, d, t, nullptr, nullptr, 0, S.cfg.inflow_mode, p.hdry, nb[d]);
             else
                 cell_phys(S, desc, nb[d]);
         }
-        const double dx = std::ldexp(S.cfg.width, -n);
-        double out[3];
         if (!fv1_cell(own, nb, dx, dt, p, out)) ok = false;
         U[3 * i + 0] = out[0];
         U[3 * i + 1] = out[1];
@@ -663,10 +674,30 @@ static int create_impl(const swamp_config* cfg, const double* h, const double* q
             const uint32_t zi = Z(L, o_interleave(i, j));
             for (int q = 0; q < 4; ++q) S->s[q][zi] = src[q][(size_t)j * side + i];
         }
-    // s_max per quantity from |s^(L)|
+    // D16: inactive finest cells; a cell is inactive when every finest
+    // descendant is, "mixed" when some but not all are
+    std::vector<uint8_t> any;
+    if (cfg->inactive) {
+        S->has_ina = true;
+        S->ina.assign(NH, 0);
+        any.assign(NH, 0);
+        for (uint32_t j = 0; j < side; ++j)
+            for (uint32_t i = 0; i < side; ++i) {
+                const uint32_t zi = Z(L, o_interleave(i, j));
+                S->ina[zi] = any[zi] = cfg->inactive[(size_t)j * side + i] ? 1 : 0;
+            }
+        for (int n = L - 1; n >= 0; --n)
+            for (uint32_t m = 0; m < (1u << (2 * n)); ++m) {
+                const uint32_t zi = Z(n, m), c0 = Z(n + 1, 4u * m);
+                S->ina[zi] = S->ina[c0] & S->ina[c0 + 1] & S->ina[c0 + 2] & S->ina[c0 + 3];
+                any[zi] = any[c0] | any[c0 + 1] | any[c0 + 2] | any[c0 + 3];
+            }
+    }
+    // s_max per quantity from |s^(L)| over the active cells
     for (int q = 0; q < 4; ++q) {
         double mx = 0.0;
-        for (uint32_t m = 0; m < side * side; ++m) mx = max2(mx, absd(S->s[q][Z(L, m)]));
+        for (uint32_t m = 0; m < side * side; ++m)
+            if (!S->has_ina || !S->ina[Z(L, m)]) mx = max2(mx, absd(S->s[q][Z(L, m)]));
         S->smax[q] = mx;
     }
     for (int q = 0; q < 4; ++q)
@@ -694,6 +725,9 @@ static int create_impl(const swamp_config* cfg, const double* h, const double* q
                     double s, a, b, g;
                     encode4(S->s[3][c0], S->s[3][c0 + 1], S->s[3][c0 + 2], S->s[3][c0 + 3], &s, &a, &b, &g);
                     S->dem[zi] = significant(a, b, g, S->smax[3], n, L, cfg->epsilon) ? 1 : 0;
+                    // D16: mixed active / inactive cells are always refined, so
+                    // every leaf is wholly active or wholly inactive
+                    if (S->has_ina && any[zi] && !S->ina[zi]) S->dem[zi] = 1;
                 }
         }
         flag_tree(*S);

@@ -52,6 +52,7 @@ class swamp_config(C.Structure):
         ("inflow_t", _dp),
         ("inflow_v", _dp),
         ("output_times", _dp),
+        ("inactive", C.POINTER(C.c_uint8)),
     ]
 
 
@@ -96,6 +97,7 @@ class SimConfig:
     inflow_t: Sequence[float] = ()
     inflow_v: Sequence[float] = ()
     output_times: Sequence[float] = ()
+    inactive: object = None  # 2^L x 2^L bool/uint8 (south row first) or None (D16)
     name: str = ""
     _keep: list = field(default_factory=list, repr=False)
 
@@ -139,6 +141,12 @@ class SimConfig:
         c.inflow_v = arr(self.inflow_v)
         c.n_outputs = len(self.output_times)
         c.output_times = arr(self.output_times)
+        if self.inactive is not None:
+            m = np.ascontiguousarray(np.asarray(self.inactive).reshape(-1) != 0, dtype=np.uint8)
+            if m.size != self.side * self.side:
+                raise ValueError("inactive mask must be 2^L x 2^L")
+            self._keep.append(m)
+            c.inactive = m.ctypes.data_as(C.POINTER(C.c_uint8))
         return c
 
     @property

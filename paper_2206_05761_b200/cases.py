@@ -168,6 +168,32 @@ def river_flood(L=11, epsilon=1e-3, t_end=1e30, seed=5, band_mode=BAND_NEIGHBOUR
     return _fields(cfg, h, z)
 
 
+def rect_domain(case, height_fraction=3.0 / 7.0, wall_z=10.0, **kw):
+    """a rectangular domain (e.g. the 70 m x 30 m humps box)
+    embedded in the enclosing 2^L square; finest cells above the rectangle
+    are inactive (reflective walls, D16) with a wall bed and no water."""
+    cfg, h, qx, qy, z = case(**kw)
+    X, Y = centres(cfg)
+    ina = Y >= cfg.y0 + height_fraction * cfg.width
+    h = np.where(ina, 0.0, h)
+    z = np.where(ina, wall_z, z)
+    cfg.inactive = ina
+    cfg.name += "_rect"
+    return cfg, h, np.zeros_like(h), np.zeros_like(h), z
+
+
+def with_nodata_block(case, frac=(0.35, 0.55, 0.3, 0.5), wall_z=200.0, **kw):
+    """A DEM with a nodata block: the block's finest cells are
+    inactive (D16) — an island the flow goes around."""
+    cfg, h, qx, qy, z = case(**kw)
+    X, Y = centres(cfg)
+    x0, x1, y0, y1 = (cfg.x0 + f * cfg.width for f in frac)
+    ina = (X >= x0) & (X < x1) & (Y >= y0) & (Y < y1)
+    cfg.inactive = ina
+    cfg.name += "_nodata"
+    return cfg, np.where(ina, 0.0, h), np.where(ina, 0.0, qx), np.where(ina, 0.0, qy), np.where(ina, wall_z, z)
+
+
 CASES = {
     "pseudo2d_dambreak": pseudo2d_dambreak,
     "quiescent_humps": quiescent_humps,

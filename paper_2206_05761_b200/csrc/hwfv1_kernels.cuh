@@ -141,6 +141,11 @@ struct Params {
     // subtree t or a face-adjacent one is wet, or t touches an inflow edge
     uint8_t* wet[2];
     uint8_t* tact;
+    // inactive cells (D16), levels 0..L at slo(n): bit 0 = every finest
+    // descendant inactive, bit 1 = some are; static, every partition holds
+    // the whole array
+    uint8_t* ina;
+    int has_ina;
     // FV1 strip path: subtrees that are active, reached and fully refined to
     // level L (every level-L cell a leaf) are updated by warps marching
     // 32 x 8 strips (k_fv1 fv1_strip); tact bit 1 marks them, stile lists them
@@ -2167,6 +2172,15 @@ __device__ __forceinline__ const double4* covering_local(const Params& P, const 
     }
     return cur + cbase(k) + mm;
 }
+// covering_local that also reports the covering cell (level k, code mm)
+__device__ __forceinline__ const double4* covering_at(const Params& P, const double4* cur, const uint8_t* sigc, int& k,
+                                                     uint32_t& mm) {
+    while (k > 0 && !sigc[slo(k - 1) + (mm >> 2)]) {
+        mm >>= 2;
+        --k;
+    }
+    return cur + cbase(k) + mm;
+}
 __device__ __forceinline__ double4* covering(const Params& P, int cur, int k, uint32_t mm) {
     while (k > 0 && !sig_at(P, cur ^ 1, k - 1, mm >> 2)) {
         mm >>= 2;
@@ -2428,7 +2442,7 @@ __device__ __forceinline__ void fv1_quad(const Params& P, const double4* __restr
 
 // FV1 over the leaf list: persistent grid-stride, one thread per
 // leaf; reads the current buffer, writes leaf slots of the other (D15).
-template <bool UNIFORM, int MINB = 2, bool PART = false, bool STRIPS = false, bool QUAD = false>
+template <bool UNIFORM, int MINB = 2, bool PART = false, bool STRIPS = false, bool QUAD = false, bool INA = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     pdl_wait();
     pdl_trigger();
@@ -2516,26 +2530,71 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             // (K3's tact) the leaf and all its neighbours are dry, so the
             // dry-neighbourhood result below follows without the gathers
             const bool quiet = ta == 0;
-            if (quiet) {
+            const bool dead = INA && (P.ina[slo(n) + m] & 1u);  // D16: an inactive leaf keeps its state
+            if (dead) {
+                hn = o4.x;
+                qxn = o4.y;
+                qyn = o4.z;
+            } else if (quiet) {
                 hn = (o4.x < 0.0) ? 0.0 : o4.x;
                 qxn = 0.0;
                 qyn = 0.0;
             } else {
             uint32_t nm[4];
             const double4* src[4];
+            bool wall[4] = {false, false, false, false};  // D16: inactive neighbour = reflective wall
 #pragma unroll
             for (int d = 0; d < 4; ++d) nm[d] = zo::neighbour_dev(n, m, static_cast<zo::Direction>(d));
             if (UNIFORM) {
 #pragma unroll
-                for (int d = 0; d < 4; ++d) src[d] = cur + cbase(n) + nm[d];
+                for (int d = 0; d < 4; ++d) {
+                    src[d] = cur + cbase(n) + nm[d];
+                    if (INA && nm[d] != zo::kNone) wall[d] = (P.ina[slo(n) + nm[d]] & 1u) != 0;
+                }
+            } else if (!PART && INA) {
+                uint8_t f[4];
+#pragma unroll
+                for (int d = 0; d < 4; ++d) f[d] = (nm[d] != zo::kNone) ? sigc[slo(n - 1) + (nm[d] >> 2)] : 1;
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    int k = n;
+                    uint32_t mm = nm[d];
+                    if (nm[d] == zo::kNone) {
+                        src[d] = cur;
+                        continue;
+                    }
+                    if (f[d]) src[d] = cur + cbase(n) + nm[d];
+                    else {
+                        k = n - 1;
+                        mm = nm[d] >> 2;
+                        src[d] = covering_at(P, cur, sigc, k, mm);
+                    }
+                    wall[d] = (P.ina[slo(k) + mm] & 1u) != 0;
+                }
             } else {
                 uint8_t f[4];
                 if (PART) {  // cross-partition reads through the peer tables
 #pragma unroll
                     for (int d = 0; d < 4; ++d) f[d] = (nm[d] != zo::kNone) ? sig_at(P, p ^ 1, n - 1, nm[d] >> 2) : 1;
 #pragma unroll
-                    for (int d = 0; d < 4; ++d)
-                        src[d] = f[d] ? cell_ptr(P, p, n, nm[d]) : covering(P, p, n - 1, nm[d] >> 2);
+                    for (int d = 0; d < 4; ++d) {
+                        if (nm[d] == zo::kNone) {
+                            src[d] = cur;
+                            continue;
+                        }
+                        int k = n;
+                        uint32_t mm = nm[d];
+                        if (!f[d]) {  // the coarser covering leaf
+                            k = n - 1;
+                            mm = nm[d] >> 2;
+                            while (k > 0 && !sig_at(P, p ^ 1, k - 1, mm >> 2)) {
+                                mm >>= 2;
+                                --k;
+                            }
+                        }
+                        src[d] = cell_ptr(P, p, k, mm);
+                        if (INA) wall[d] = (P.ina[slo(k) + mm] & 1u) != 0;  // replicated (static)
+                    }
                 } else {
 #pragma unroll
                     for (int d = 0; d < 4; ++d) f[d] = (nm[d] != zo::kNone) ? sigc[slo(n - 1) + (nm[d] >> 2)] : 1;
@@ -2555,7 +2614,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             bool all_dry = o4.x < P.phys.hdry;
 #pragma unroll
             for (int d = 0; d < 4; ++d) {
-                if (nm[d] != zo::kNone) all_dry = all_dry && r4[d].x < P.phys.hdry;
+                if (nm[d] != zo::kNone) all_dry = all_dry && (wall[d] || r4[d].x < P.phys.hdry);
                 else if (P.bc[d] == 2) all_dry = false;  // inflow ghosts can be wet
             }
             if (all_dry) {
@@ -2567,6 +2626,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                 // the W, E, N, S neighbour as seen by its face (ghost on the boundary)
                 auto neighbour = [&](int d) -> CellV {
                     if (nm[d] == zo::kNone) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, P.phys);
+                    if (wall[d]) return boundary_cell(own, 0, d, inflow, P.inflow_mode, P.phys);
                     return make_cell(r4[d], P.phys);
                 };
                 fv1_cell_seq(own, neighbour, inv_dx_of(P, n), dt, P.phys, hn, qxn, qyn);
@@ -2590,7 +2650,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                 report_error(ctl, kErrNonFinite, zo::z_of(n, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2),
                              kStageFV1);
             st4(nxt + cbase(n) + m, make_double4(hn, qxn, qyn, zown));
-            const double c = cfl_rate(hn, qxn, qyn, inv_dx_of(P, n), P.phys);
+            const double c = (INA && (P.ina[slo(n) + m] & 1u)) ? 0.0 : cfl_rate(hn, qxn, qyn, inv_dx_of(P, n), P.phys);
             mx = c > mx ? c : mx;
         }
         // Next step's zero_details_and_reencode of level L-1, fused here: the
@@ -2636,7 +2696,7 @@ __global__ void __launch_bounds__(kThreads) k_cfl_init(Params P, Ctl* ctl, int u
             m = z - zo::level_offset(n);
         }
         const double4 v = ld4(cur + cbase(n) + m);
-        const double c = cfl_rate(v.x, v.y, v.z, inv_dx_of(P, n), P.phys);
+        const double c = (P.has_ina && (P.ina[slo(n) + m] & 1u)) ? 0.0 : cfl_rate(v.x, v.y, v.z, inv_dx_of(P, n), P.phys);
         mx = c > mx ? c : mx;
     }
     cfl_reduce_and_finalize(P, ctl, mx, false, static_cast<int>(ctl->step & 1));
@@ -2646,7 +2706,8 @@ __global__ void __launch_bounds__(kThreads) k_cfl_init(Params P, Ctl* ctl, int u
 // initial discretisation: row-major (south row first) finest
 // fields -> Morton slots of level L; s_max per quantity.
 __global__ void __launch_bounds__(kThreads) k_import(Params P, Ctl* ctl, const double* h, const double* qx,
-                                                     const double* qy, const double* z, int buffer) {
+                                                     const double* qy, const double* z, const uint8_t* mask,
+                                                     int buffer) {
     const uint32_t side = 1u << P.L;
     const uint64_t total = static_cast<uint64_t>(side) * side;
     double mx[4] = {0.0, 0.0, 0.0, 0.0};
@@ -2657,6 +2718,11 @@ __global__ void __launch_bounds__(kThreads) k_import(Params P, Ctl* ctl, const d
         if (!(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w)))
             report_error(ctl, kErrNonFinite, zo::z_of(P.L, m), 0, kStageImport);
         st4(P.cells[buffer] + cbase(P.L) + m, v);
+        if (mask) {  // D16: finest inactive flags (bits 0 and 1), excluded from s_max
+            const uint8_t b = mask[r] ? 3 : 0;
+            P.ina[slo(P.L) + m] = b;
+            if (b) continue;
+        }
         mx[0] = max2(mx[0], absd(v.x));
         mx[1] = max2(mx[1], absd(v.y));
         mx[2] = max2(mx[2], absd(v.z));
@@ -2740,6 +2806,30 @@ __global__ void k_export_finest(Params P, const Ctl* ctl, double* h, double* qx,
         h[r] = v.x;
         qx[r] = v.y;
         qy[r] = v.z;
+    }
+}
+
+// D16: inactive flags of level n from level n + 1 (bit 0 = all, bit 1 = any)
+__global__ void k_ina_level(Params P, int n) {
+    const uint32_t cnt = 1u << (2 * n);
+    for (uint32_t m = blockIdx.x * kThreads + threadIdx.x; m < cnt; m += gridDim.x * kThreads) {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(P.ina + slo(n + 1) + 4u * m);
+        const uint32_t all = (w & 0x01010101u) == 0x01010101u ? 1u : 0u;
+        const uint32_t any = (w & 0x02020202u) ? 2u : 0u;
+        P.ina[slo(n) + m] = static_cast<uint8_t>(all | any);
+    }
+}
+// D16: mixed active / inactive cells join the static DEM mask (and the
+// pre-band flags of initialise), so every leaf is wholly active or inactive
+__global__ void k_ina_mix(Params P) {
+    const uint32_t nd = lo(P.L, 0);
+    for (uint32_t q = blockIdx.x * kThreads + threadIdx.x; q < nd; q += gridDim.x * kThreads) {
+        const int n = (31 - __clz(3u * q + 1u)) >> 1;
+        const uint32_t a = slo(n) + (q - lo(n, 0));
+        if (P.ina[a] == 2u) {
+            P.dem[a] = 1;
+            P.pre[a] = 1;
+        }
     }
 }
 

@@ -149,7 +149,10 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     };
     mark(0);
     if (g->uniform) {
-        launch_pdl(hwfv1::k_fv1<true, 2>, g->fv1_grid, 0, s, P, g->ctl);
+        if (P.has_ina)
+            launch_pdl(hwfv1::k_fv1<true, 2, false, false, false, true>, g->fv1_grid, 0, s, P, g->ctl);
+        else
+            launch_pdl(hwfv1::k_fv1<true, 2>, g->fv1_grid, 0, s, P, g->ctl);
         for (int k = 1; k < 5; ++k) mark(k);
         return;
     }
@@ -165,7 +168,9 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     launch_pdl(g->k3, P.n_tiles + 1, g->smem_k3, s, P, g->ctl, 0, 0ull);
     mark(3);
     const size_t sm5 = P.strips ? sizeof(double4) * (kThreads / 32) * hwfv1::kStripSlots : 0;
-    if (P.strips)
+    if (P.has_ina)  // D16 variant (strips / quad / MINB variants do not handle inactive cells)
+        launch_pdl(hwfv1::k_fv1<false, 2, false, false, false, true>, g->fv1_grid, 0, s, P, g->ctl);
+    else if (P.strips)
         launch_pdl(hwfv1::k_fv1<false, 2, false, true>, g->fv1_grid, sm5, s, P, g->ctl);
     else if (P.quad)
         launch_pdl(hwfv1::k_fv1<false, 2, false, false, true>, g->fv1_grid, 0, s, P, g->ctl);
@@ -326,6 +331,8 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     if ((st = dalloc(g, &P.wet[1], P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.tact, P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.stile, P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    P.has_ina = cfg->inactive ? 1 : 0;
+    if (P.has_ina && (st = dalloc(g, &P.ina, hwfv1::slo(L + 1) + 16))) return fail(st);
     // every subtree counts as wet until FV1 has run once
     cudaMemset(P.wet[0], 1, P.n_tiles);
     cudaMemset(P.wet[1], 1, P.n_tiles);
@@ -365,12 +372,21 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     // upload + import (the staging buffer is released right after)
     {
         double* stage = nullptr;
-        if (cudaMalloc(&stage, 4 * nf * sizeof(double)) != cudaSuccess) return fail(SWAMP_E_NOMEM);
+        if (cudaMalloc(&stage, 4 * nf * sizeof(double) + (P.has_ina ? nf : 0)) != cudaSuccess) return fail(SWAMP_E_NOMEM);
         const double* src[4] = {h, qx, qy, z};
         for (int q = 0; q < 4; ++q)
             cudaMemcpyAsync(stage + q * nf, src[q], nf * sizeof(double), cudaMemcpyHostToDevice, s);
+        uint8_t* mask = nullptr;
+        if (P.has_ina) {
+            mask = reinterpret_cast<uint8_t*>(stage + 4 * nf);
+            cudaMemcpyAsync(mask, cfg->inactive, nf, cudaMemcpyHostToDevice, s);
+        }
         const int grid = std::max(1, std::min<int>(g->num_sms * 8, static_cast<int>((nf + kThreads - 1) / kThreads)));
-        hwfv1::k_import<<<grid, kThreads, 0, s>>>(P, g->ctl, stage, stage + nf, stage + 2 * nf, stage + 3 * nf, 0);
+        hwfv1::k_import<<<grid, kThreads, 0, s>>>(P, g->ctl, stage, stage + nf, stage + 2 * nf, stage + 3 * nf, mask, 0);
+        for (int n = L - 1; P.has_ina && n >= 0; --n) {
+            const int gl = std::max(1, std::min<int>(g->num_sms * 4, static_cast<int>(((1u << (2 * n)) + kThreads - 1) / kThreads)));
+            hwfv1::k_ina_level<<<gl, kThreads, 0, s>>>(P, n);
+        }
         cudaError_t e = cudaStreamSynchronize(s);
         cudaFree(stage);
         if (e != cudaSuccess) {
@@ -451,6 +467,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         P.strips = (es && es[0] == '1') ? 1 : 0;
         const char* eq = std::getenv("SWAMP_FV1_QUAD");
         P.quad = (eq && eq[0] == '1') ? 1 : 0;
+        if (P.has_ina) P.strips = P.quad = 0;  // those paths do not handle inactive cells
         // persistent double-buffered K1 for K = 6, opt-in (SWAMP_K1_PIPE=1): measured
         // slower than one CTA per subtree (latency chains, fewer CTAs in flight)
         const char* ep = std::getenv("SWAMP_K1_PIPE");
@@ -505,6 +522,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
         // encode + DEM mask, band + closure, traversal; no decode at t = 0
         cudaMemsetAsync(P.sig[0], 1, foff, s);
         hwfv1::k_encode<true><<<P.n_tiles, kThreads, g->smem_k1, s>>>(P, g->ctl);
+        if (P.has_ina) hwfv1::k_ina_mix<<<std::max(1, g->num_sms * 4), kThreads, 0, s>>>(P);
         g->k2<<<P.n_tiles, kThreads, g->smem_k2, s>>>(P, g->ctl, 1, 0);
         g->k3<<<P.n_tiles + 1, kThreads, g->smem_k3, s>>>(P, g->ctl, 1, 0ull);
         // both buffers hold the full hierarchy; the current tree becomes "previous"
@@ -560,7 +578,10 @@ bool part_step_phase(swamp_gpu* q, int k, cudaStream_t s) {
             return true;
         }
         case 3: q->k3<<<P.tiles_per_part + 1, kThreads, q->smem_k3, s>>>(P, q->ctl, 0, 0ull); return true;
-        case 4: hwfv1::k_fv1<false, 2, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl); return true;
+        case 4:
+            if (P.has_ina) hwfv1::k_fv1<false, 2, true, false, false, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
+            else hwfv1::k_fv1<false, 2, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
+            return true;
         default: hwfv1::k_finalize<<<1, 32, 0, s>>>(P, q->ctl, 1); return true;
     }
 }
@@ -576,7 +597,10 @@ bool part_init_phase(swamp_gpu* q, int k, cudaStream_t s) {
             hwfv1::k_encode<true><<<P.tiles_per_part, kThreads, q->smem_k1, s>>>(P, q->ctl);
             return true;
         }
-        case 1: hwfv1::k_encode_top<true><<<1, kThreads, q->smem_k1, s>>>(P, q->ctl); return true;
+        case 1:
+            hwfv1::k_encode_top<true><<<1, kThreads, q->smem_k1, s>>>(P, q->ctl);
+            if (P.has_ina) hwfv1::k_ina_mix<<<std::max(1, q->num_sms * 4), kThreads, 0, s>>>(P);
+            return true;
         case 2: q->k2<<<P.tiles_per_part, kThreads, q->smem_k2, s>>>(P, q->ctl, 1, 0); return true;
         case 3: q->k3<<<P.tiles_per_part + 1, kThreads, q->smem_k3, s>>>(P, q->ctl, 1, 0ull); return true;
         case 4:

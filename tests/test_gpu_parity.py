@@ -184,3 +184,41 @@ def test_persistent_k1_variant(monkeypatch):
         o.step()
         if k in (1, 20):
             compare_states(g, o, f"K1 pipe step {k}")
+
+
+MASKED = [
+    ("rect humps dambreak L7", lambda: cases.rect_domain(cases.hump_dambreak, L=7)),
+    ("rect quiescent humps L7", lambda: cases.rect_domain(cases.quiescent_humps, L=7)),
+    ("nodata river L8", lambda: cases.with_nodata_block(cases.river_flood, L=8)),
+    ("nodata monai L7", lambda: cases.with_nodata_block(cases.monai_runup, L=7)),
+]
+
+
+@pytest.mark.parametrize("name,make", MASKED, ids=[m[0] for m in MASKED])
+def test_inactive_cells_parity(name, make):
+    """D16 inactive cells == the oracle, bitwise."""
+    cfg, h, qx, qy, z = make()
+    g = gpu.initialise(cfg, h, qx, qy, z)
+    o = O.Oracle(cfg, h, qx, qy, z)
+    compare_states(g, o, f"{name} init")
+    for k in range(1, 31):
+        g.step_adaptive()
+        o.step()
+        if k in (1, 10, 30):
+            compare_states(g, o, f"{name} step {k}")
+
+
+def test_inactive_cells_uniform_and_partitioned():
+    cfg, h, qx, qy, z = cases.with_nodata_block(cases.river_flood, L=8)
+    u = gpu.initialise_uniform(cfg, h, qx, qy, z)
+    ou = O.Oracle(cfg, h, qx, qy, z, uniform=True)
+    one = gpu.initialise(cfg, h, qx, qy, z)
+    many = gpu.initialise_partitioned(cfg, h, qx, qy, z, [0] * 4)
+    for _ in range(20):
+        u.step_uniform(1)
+        ou.step(uniform=True)
+        one.step_adaptive()
+        many.step_adaptive()
+    for a, b in zip(u.export_finest(), ou.export_finest()):
+        np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))
+    compare_states(many, one, "nodata river x4")
