@@ -2442,7 +2442,8 @@ __device__ __forceinline__ void fv1_quad(const Params& P, const double4* __restr
 
 // FV1 over the leaf list: persistent grid-stride, one thread per
 // leaf; reads the current buffer, writes leaf slots of the other (D15).
-template <bool UNIFORM, int MINB = 2, bool PART = false, bool STRIPS = false, bool QUAD = false, bool INA = false>
+template <bool UNIFORM, int MINB = 2, bool PART = false, bool STRIPS = false, bool QUAD = false, bool INA = false,
+          bool STAGE = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     pdl_wait();
     pdl_trigger();
@@ -2603,10 +2604,28 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                         src[d] = f[d] ? cur + cbase(n) + nm[d] : covering_local(P, cur, sigc, n - 1, nm[d] >> 2);
                 }
             }
-            double4 r4[4];
+            // STAGE: the neighbours land in shared memory by cp.async (no
+            // registers held across the load; slot [warp][d][lane])
+            __shared__ __align__(16) double4 s_nb[STAGE ? kThreads / 32 * 4 * 32 : 1];
+            double4 r4s[STAGE ? 1 : 4];
+            auto nbv = [&](int d) -> double4 {
+                if (STAGE) return s_nb[((threadIdx.x >> 5) * 4 + d) * 32 + lane];
+                return r4s[STAGE ? 0 : d];
+            };
+            if (STAGE) {
 #pragma unroll
-            for (int d = 0; d < 4; ++d)
-                if (nm[d] != zo::kNone) r4[d] = ld4_nc(src[d]);
+                for (int d = 0; d < 4; ++d)
+                    if (nm[d] != zo::kNone) {
+                        double4* sl = &s_nb[((threadIdx.x >> 5) * 4 + d) * 32 + lane];
+                        cp_async16(sl, src[d]);
+                        cp_async16(reinterpret_cast<uint8_t*>(sl) + 16, reinterpret_cast<const uint8_t*>(src[d]) + 16);
+                    }
+                cp_async_wait_all();
+            } else {
+#pragma unroll
+                for (int d = 0; d < 4; ++d)
+                    if (nm[d] != zo::kNone) r4s[STAGE ? 0 : d] = ld4_nc(src[d]);
+            }
             // dry neighbourhood: own cell and every neighbour / ghost below
             // h_dry => every reconstructed depth is 0, every flux 0, the bed
             // corrections cancel pairwise: h stays, q = 0 (the general path
@@ -2614,7 +2633,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             bool all_dry = o4.x < P.phys.hdry;
 #pragma unroll
             for (int d = 0; d < 4; ++d) {
-                if (nm[d] != zo::kNone) all_dry = all_dry && (wall[d] || r4[d].x < P.phys.hdry);
+                if (nm[d] != zo::kNone) all_dry = all_dry && (wall[d] || nbv(d).x < P.phys.hdry);
                 else if (P.bc[d] == 2) all_dry = false;  // inflow ghosts can be wet
             }
             if (all_dry) {
@@ -2627,7 +2646,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                 auto neighbour = [&](int d) -> CellV {
                     if (nm[d] == zo::kNone) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, P.phys);
                     if (wall[d]) return boundary_cell(own, 0, d, inflow, P.inflow_mode, P.phys);
-                    return make_cell(r4[d], P.phys);
+                    return make_cell(nbv(d), P.phys);
                 };
                 fv1_cell_seq(own, neighbour, inv_dx_of(P, n), dt, P.phys, hn, qxn, qyn);
             }
