@@ -146,6 +146,15 @@ int swamp_gpu_rank_create(const swamp_config* cfg, const double* h, const double
 int swamp_gpu_rank_connect(swamp_gpu* g, const uint8_t* blobs);
 int swamp_gpu_rank_ready(swamp_gpu* g);
 
+/* Dynamic repartitioning: move the partition boundaries
+ * so that every partition holds about the same number of leaves (contiguous
+ * Morton subtree ranges from the current leaf-list offsets) and pull the
+ * subtrees a partition gains from their old owner (peer reads). Between
+ * steps; rank engines: every rank calls it at the same step (the ranks meet
+ * on the device). *changed = 1 when boundaries moved. Results are unchanged
+ * (bitwise). No-op for a single partition. */
+int swamp_gpu_rebalance(swamp_gpu* g, int32_t* changed);
+
 /* step_adaptive: one Alg. 3 iteration. No-op when
  * t >= t_end. Fills `rep` (may be NULL). Synchronises the device. */
 int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep);

@@ -160,10 +160,14 @@ struct Params {
     // pointers across GPUs; index 0 = self when G = 1).
     int G, part;
     int top_mode;         // levels < R after t = 0: 0 none (R = 0), 1 extra CTA of K2, 2 k_encode_top
-    uint32_t tile_lo, tile_hi, tiles_per_part;
+    uint32_t tile_lo, tile_hi, tiles_per_part;  // this partition's subtrees [tile_lo, tile_hi), their count
+    uint32_t pbound[kMaxParts + 1];             // partition g owns [pbound[g], pbound[g + 1]) (rebalanced)
+    uint32_t pb_align;                          // largest of 16 / 4 / 1 dividing every boundary
     double4* pcells[kMaxParts][2];
     uint8_t* psig[kMaxParts][2];
     uint8_t* ppre[kMaxParts];
+    uint8_t* pdem[kMaxParts];   // (repartitioning only)
+    uint8_t* pwet[kMaxParts][2];
     uint32_t* ptile_cnt[kMaxParts];
     Ctl* pctl[kMaxParts];
 };
@@ -230,7 +234,9 @@ __device__ __forceinline__ uint32_t lo(int n, int R) { return ((1u << (2 * (n - 
 __device__ __forceinline__ int owner_of(const Params& P, int n, uint32_t m) {
     if (P.G == 1) return 0;
     const uint32_t t = (n >= P.R) ? (m >> (2 * (n - P.R))) : (m << (2 * (P.R - n)));
-    return static_cast<int>(t / P.tiles_per_part);
+    int g = 0;
+    while (g + 1 < P.G && t >= P.pbound[g + 1]) ++g;
+    return g;
 }
 __device__ __forceinline__ double4* cell_ptr(const Params& P, int buf, int n, uint32_t m) {
     return P.pcells[owner_of(P, n, m)][buf] + cbase(n) + m;
@@ -1583,7 +1589,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     uint32_t* scnt = reinterpret_cast<uint32_t*>(swet + ((nt + 15u) & ~15u));
     const bool cnt_smem = nt <= 1024u;
     const uint32_t* cnt = cnt_smem ? scnt : P.tile_cnt;
-    const uint32_t tpp = P.tiles_per_part;
+    const uint32_t al = P.G == 1 ? 16u : P.pb_align;
     const int rb = EXPORT ? p : p ^ 1;
 
     // ---- stage (one round trip)
@@ -1598,10 +1604,10 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     uint8_t r0 = 0;
     if (nt == 1u) {
         if (threadIdx.x == 64) r0 = P.psig[0][rb][slo(R)];
-    } else if (P.G == 1 || (tpp & 15u) == 0u) {
+    } else if (al >= 16u) {
         for (uint32_t q = 16u * threadIdx.x; q < nt; q += 16u * kThreads)
             cp_async16(ts + fb + q, P.psig[owner_of(P, R, q)][rb] + slo(R) + q);
-    } else if ((tpp & 3u) == 0u) {
+    } else if (al >= 4u) {
         for (uint32_t q = 4u * threadIdx.x; q < nt; q += 4u * kThreads)
             cp_async4(ts + fb + q, P.psig[owner_of(P, R, q)][rb] + slo(R) + q);
     } else {  // small partitioned grids (tests): plain byte copies
@@ -2849,6 +2855,50 @@ __global__ void k_ina_mix(Params P) {
             P.dem[a] = 1;
             P.pre[a] = 1;
         }
+    }
+}
+
+// Dynamic repartitioning: with the NEW boundaries in P and
+// the old ones in `old`, CTA b of the new range pulls subtree tile_lo + b
+// from its old owner when that owner is another partition: the subtree's
+// cells of levels R..L (both buffers), its flags of levels R..L-1 (both
+// copies, pre-band, DEM), its leaf counts and wet marks. Block 0 also pulls
+// the top cells (levels < R) whose first subtree changed owner. Peers are
+// idle (between steps); every partition pulls only what it gains.
+__global__ void __launch_bounds__(kThreads) k_rebalance_pull(Params P, Params old) {
+    const int R = P.R, L = P.L;
+    const uint32_t t = P.tile_lo + blockIdx.x;
+    const int from = owner_of(old, R, t);
+    if (blockIdx.x == 0) {  // top cells: their value lives in the partition of their first subtree
+        for (uint32_t q = threadIdx.x; q < lo(R, 0); q += kThreads) {
+            const int n = (31 - __clz(3u * q + 1u)) >> 1;
+            const uint32_t m = q - lo(n, 0);
+            const int src = owner_of(old, n, m);
+            if (owner_of(P, n, m) != P.part || src == P.part) continue;
+            for (int b = 0; b < 2; ++b) P.cells[b][cbase(n) + m] = old.pcells[src][b][cbase(n) + m];
+        }
+    }
+    if (from == P.part) return;
+    for (int n = R; n <= L; ++n) {
+        const uint32_t cnt = 1u << (2 * (n - R));
+        const unsigned long long base = cbase(n) + static_cast<unsigned long long>(t) * cnt;
+        for (uint32_t c = threadIdx.x; c < cnt; c += kThreads)
+            for (int b = 0; b < 2; ++b) P.cells[b][base + c] = old.pcells[from][b][base + c];
+        if (n < L) {
+            const unsigned long long fb = slo(n) + static_cast<unsigned long long>(t) * cnt;
+            for (uint32_t c = threadIdx.x; c < cnt; c += kThreads) {
+                P.sig[0][fb + c] = old.psig[from][0][fb + c];
+                P.sig[1][fb + c] = old.psig[from][1][fb + c];
+                P.pre[fb + c] = old.ppre[from][fb + c];
+                P.dem[fb + c] = old.pdem[from][fb + c];
+            }
+        }
+    }
+    if (threadIdx.x == 0) {
+        P.tile_cnt[t] = old.ptile_cnt[from][t];
+        P.tile_cnt[P.n_tiles + t] = old.ptile_cnt[from][P.n_tiles + t];
+        P.wet[0][t] = old.pwet[from][0][t];
+        P.wet[1][t] = old.pwet[from][1][t];
     }
 }
 

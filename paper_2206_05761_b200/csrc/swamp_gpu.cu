@@ -279,6 +279,9 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     P.tiles_per_part = static_cast<uint32_t>(P.n_tiles / G);
     P.tile_lo = static_cast<uint32_t>(part) * P.tiles_per_part;
     P.tile_hi = P.tile_lo + P.tiles_per_part;
+    for (int k = 0; k <= hwfv1::kMaxParts; ++k)
+        P.pbound[k] = static_cast<uint32_t>(std::min(k, G)) * P.tiles_per_part;
+    P.pb_align = (P.tiles_per_part % 16 == 0) ? 16u : (P.tiles_per_part % 4 == 0) ? 4u : 1u;
     P.band_mode = cfg->band_mode;
     for (int k = 0; k < 4; ++k) P.bc[k] = cfg->bc[k];
     P.inflow_mode = cfg->inflow_mode;
@@ -334,6 +337,9 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     if ((st = dalloc(g, &P.wet[1], P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.tact, P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.stile, P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    P.pdem[0] = P.dem;
+    P.pwet[0][0] = P.wet[0];
+    P.pwet[0][1] = P.wet[1];
     P.has_ina = cfg->inactive ? 1 : 0;
     if (P.has_ina && (st = dalloc(g, &P.ina, hwfv1::slo(L + 1) + 16))) return fail(st);
     // every subtree counts as wet until FV1 has run once
@@ -710,6 +716,9 @@ void fill_peer_tables(swamp_gpu* q, const std::vector<swamp_gpu*>& parts) {
             q->P.psig[k][b] = r->P.sig[b];
         }
         q->P.ppre[k] = r->P.pre;
+        q->P.pdem[k] = r->P.dem;
+        q->P.pwet[k][0] = r->P.wet[0];
+        q->P.pwet[k][1] = r->P.wet[1];
         q->P.ptile_cnt[k] = r->P.tile_cnt;
         q->P.pctl[k] = r->ctl;
     }
@@ -865,13 +874,52 @@ int group_advance(swamp_gpu* grp, int64_t n_steps, bool sync, swamp_step_report*
     return st;
 }
 
+// ---- dynamic repartitioning: contiguous subtree ranges
+// that equalise the leaf counts, from the per-subtree list offsets K3's top
+// CTA wrote (every partition holds them for all subtrees)
+bool plan_bounds(swamp_gpu* q, int G, uint32_t* nb) {
+    const uint32_t nt = static_cast<uint32_t>(q->P.n_tiles);
+    std::vector<uint32_t> off(2 * static_cast<size_t>(nt));
+    if (cudaMemcpy(off.data(), q->P.tile_off, off.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return false;
+    const uint64_t ta = q->ctl_host->n_leaves_A, N = q->ctl_host->n_leaves;
+    auto before = [&](uint32_t t) -> uint64_t {  // leaves of subtrees [0, t)
+        return t >= nt ? N : static_cast<uint64_t>(off[t]) + off[nt + t] - ta;
+    };
+    // boundary granularity: 16 subtrees when there are plenty (keeps K3's
+    // 16-byte staging), finer for small grids
+    const uint32_t al = (nt >= 64u * G) ? 16u : (nt >= 16u * G) ? 4u : 1u;
+    nb[0] = 0;
+    for (int g = 1; g < G; ++g) {
+        const uint64_t target = N * static_cast<uint64_t>(g) / G;
+        uint32_t t = nb[g - 1] + al;  // every partition keeps at least `al` subtrees
+        while (t + al * static_cast<uint32_t>(G - g) <= nt && before(t) < target) t += al;
+        if (t + al * static_cast<uint32_t>(G - g) > nt) t = nt - al * static_cast<uint32_t>(G - g);
+        nb[g] = t;
+    }
+    for (int g = G; g <= hwfv1::kMaxParts; ++g) nb[g] = nt;
+    return true;
+}
+
+void apply_bounds(Params& P, const uint32_t* nb) {
+    for (int k = 0; k <= hwfv1::kMaxParts; ++k) P.pbound[k] = nb[k];
+    P.tile_lo = nb[P.part];
+    P.tile_hi = nb[P.part + 1];
+    P.tiles_per_part = P.tile_hi - P.tile_lo;
+    uint32_t a = 16;
+    for (int k = 0; k <= P.G; ++k) {
+        while (a > 1 && nb[k] % a) a = (a == 16) ? 4 : 1;
+    }
+    P.pb_align = a;
+}
+
 // ---- one partition per process (rank engines)
 struct RankBlob {  // exchanged between the ranks (swamp_gpu_rank_create / _connect)
     uint32_t magic;
     int32_t rank, world, device;
     uint64_t pid;
-    uint64_t ptr[7];              // cells[0], cells[1], sig[0], sig[1], pre, tile_cnt, ctl
-    cudaIpcMemHandle_t ipc[7];
+    uint64_t ptr[10];             // cells[0], cells[1], sig[0], sig[1], pre, tile_cnt, ctl, dem, wet[0], wet[1]
+    cudaIpcMemHandle_t ipc[10];
 };
 static_assert(sizeof(RankBlob) <= SWAMP_RANK_BLOB_BYTES, "rank blob too large");
 constexpr uint32_t kRankMagic = 0x53574D52u;  // "SWMR"
@@ -884,7 +932,10 @@ void* rank_ptr(const swamp_gpu* q, int k) {
         case 3: return q->P.sig[1];
         case 4: return q->P.pre;
         case 5: return q->P.tile_cnt;
-        default: return q->ctl;
+        case 6: return q->ctl;
+        case 7: return q->P.dem;
+        case 8: return q->P.wet[0];
+        default: return q->P.wet[1];
     }
 }
 
@@ -1179,7 +1230,7 @@ int swamp_gpu_rank_create(const swamp_config* cfg, const double* h, const double
     b.world = world;
     b.device = device;
     b.pid = static_cast<uint64_t>(getpid());
-    for (int k = 0; k < 7; ++k) {
+    for (int k = 0; k < 10; ++k) {
         void* p = rank_ptr(g, k);
         b.ptr[k] = reinterpret_cast<uint64_t>(p);
         if (cudaIpcGetMemHandle(&b.ipc[k], p) != cudaSuccess) {
@@ -1202,18 +1253,18 @@ int swamp_gpu_rank_connect(swamp_gpu* g, const uint8_t* blobs) {
         RankBlob b;
         std::memcpy(&b, blobs + static_cast<size_t>(r) * SWAMP_RANK_BLOB_BYTES, sizeof(b));
         if (b.magic != kRankMagic || b.rank != r || b.world != W) return SWAMP_E_ARG;
-        void* p[7];
+        void* p[10];
         if (r == me) {
-            for (int k = 0; k < 7; ++k) p[k] = rank_ptr(g, k);
+            for (int k = 0; k < 10; ++k) p[k] = rank_ptr(g, k);
         } else if (b.pid == pid) {  // another rank handle of this process: its pointers directly
             if (b.device != g->device) {
                 const cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
                 if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return SWAMP_E_CUDA;
                 cudaGetLastError();
             }
-            for (int k = 0; k < 7; ++k) p[k] = reinterpret_cast<void*>(b.ptr[k]);
+            for (int k = 0; k < 10; ++k) p[k] = reinterpret_cast<void*>(b.ptr[k]);
         } else {  // another process: open its CUDA IPC handles (NVLink peer mapping)
-            for (int k = 0; k < 7; ++k) {
+            for (int k = 0; k < 10; ++k) {
                 if (cudaIpcOpenMemHandle(&p[k], b.ipc[k], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
                     g->err = "cudaIpcOpenMemHandle failed";
                     return SWAMP_E_CUDA;
@@ -1228,6 +1279,9 @@ int swamp_gpu_rank_connect(swamp_gpu* g, const uint8_t* blobs) {
         g->P.ppre[r] = static_cast<uint8_t*>(p[4]);
         g->P.ptile_cnt[r] = static_cast<uint32_t*>(p[5]);
         g->P.pctl[r] = static_cast<Ctl*>(p[6]);
+        g->P.pdem[r] = static_cast<uint8_t*>(p[7]);
+        g->P.pwet[r][0] = static_cast<uint8_t*>(p[8]);
+        g->P.pwet[r][1] = static_cast<uint8_t*>(p[9]);
     }
     part_enqueue_init(g);  // completes once every rank has connected (device barriers)
     return cudaGetLastError() == cudaSuccess ? SWAMP_OK : SWAMP_E_CUDA;
@@ -1276,6 +1330,67 @@ int swamp_gpu_compare(swamp_gpu* a, swamp_gpu* b, double* l1, double* linf) {
     *l1 = s / static_cast<double>(nf);  // sum |dh| dx^2 / area over the square: the mean
     *linf = m;
     return SWAMP_OK;
+}
+
+int swamp_gpu_rebalance(swamp_gpu* g, int32_t* changed) {
+    if (!g) return SWAMP_E_ARG;
+    if (changed) *changed = 0;
+    const bool group = !g->parts.empty();
+    if (!group && g->rank_world < 2) return SWAMP_OK;  // one partition: nothing to balance
+    int st = group ? group_sync(g) : fetch_ctl(g);
+    if (st) return st;
+    std::vector<swamp_gpu*> mine = group ? g->parts : std::vector<swamp_gpu*>{g};
+    swamp_gpu* q0 = mine[0];
+    const int G = q0->P.G;
+    uint32_t nb[hwfv1::kMaxParts + 1];
+    cudaSetDevice(q0->device);
+    if (!plan_bounds(q0, G, nb)) return SWAMP_E_CUDA;
+    bool same = true;
+    for (int k = 0; k <= G; ++k) same = same && nb[k] == q0->P.pbound[k];
+    if (same) return SWAMP_OK;
+    // every partition pulls what it gains from the old owners (peers idle: a
+    // rank engine first meets its peers on the device)
+    std::vector<Params> old;
+    for (swamp_gpu* q : mine) old.push_back(q->P);
+    for (size_t k = 0; k < mine.size(); ++k) {
+        swamp_gpu* q = mine[k];
+        cudaSetDevice(q->device);
+        if (!group) part_barrier(q, q->stream);
+        Params np = q->P;
+        apply_bounds(np, nb);
+        cudaStream_t s = (group && g->serial) ? q0->stream : q->stream;
+        if (np.tiles_per_part > 0) hwfv1::k_rebalance_pull<<<np.tiles_per_part, kThreads, 0, s>>>(np, old[k]);
+        if (!group) part_barrier(q, q->stream);  // nobody steps until every rank has pulled
+    }
+    if ((st = group ? group_sync(g) : fetch_ctl(g))) return st;
+    if (cudaGetLastError() != cudaSuccess) return SWAMP_E_CUDA;
+    for (swamp_gpu* q : mine) {
+        cudaSetDevice(q->device);
+        apply_bounds(q->P, nb);
+        if (q->k1p_grid)
+            q->k1p_grid = std::max(1, std::min<int>(static_cast<int>(q->P.tiles_per_part), q->k1p_grid));
+        for (cudaGraphExec_t* e : {&q->graph1, &q->graphS})
+            if (*e) {
+                cudaGraphExecDestroy(*e);
+                *e = nullptr;
+            }
+    }
+    if (group && g->serial) {
+        for (cudaGraphExec_t* e : {&g->graph1, &g->graphS})
+            if (*e) {
+                cudaGraphExecDestroy(*e);
+                *e = nullptr;
+            }
+        cudaSetDevice(q0->device);
+        if ((st = capture_step_graphs(g, q0->stream, [&] { serial_enqueue_step(g); }))) return st;
+    } else {
+        for (swamp_gpu* q : mine) {
+            cudaSetDevice(q->device);
+            if ((st = part_build_graphs(q))) return st;
+        }
+    }
+    if (changed) *changed = 1;
+    return group ? group_sync(g) : fetch_ctl(g);
 }
 
 #define SWAMP_STR2(x) #x

@@ -46,6 +46,7 @@ def lib():
         L.swamp_gpu_rank_connect.argtypes = [P, C.POINTER(C.c_uint8)]
         L.swamp_gpu_rank_ready.argtypes = [P]
         L.swamp_gpu_compare.argtypes = [P, P, dp, dp]
+        L.swamp_gpu_rebalance.argtypes = [P, C.POINTER(C.c_int32)]
         L.swamp_gpu_destroy.argtypes = [P]
         L.swamp_gpu_step.argtypes = [P, rp]
         L.swamp_gpu_advance.argtypes = [P, C.c_int64, rp]
@@ -75,6 +76,7 @@ EXPORTED_SYMBOLS = (
     "swamp_gpu_counters", "swamp_gpu_build_info", "swamp_gpu_enqueue", "swamp_gpu_stream",
     "swamp_gpu_timeline", "swamp_gpu_create_partitioned", "swamp_gpu_debug",
     "swamp_gpu_rank_create", "swamp_gpu_rank_connect", "swamp_gpu_rank_ready", "swamp_gpu_compare",
+    "swamp_gpu_rebalance",
     "swamp_io_read_esri", "swamp_io_write_esri", "swamp_io_free_raster", "swamp_io_load_dem", "swamp_io_write_finest",
 )
 
@@ -213,6 +215,12 @@ class Engine:
         a = (C.c_uint64 * 64)()
         self._check(lib().swamp_gpu_debug(self._h, a), "debug")
         return list(a)
+
+    def rebalance(self) -> bool:
+        """Dynamic repartitioning: equalise the partitions' leaf counts; True when boundaries moved."""
+        ch = C.c_int32()
+        self._check(lib().swamp_gpu_rebalance(self._h, C.byref(ch)), "rebalance")
+        return bool(ch.value)
 
     def compare(self, other) -> dict:
         """compare: L1 and L-infinity of the depth against

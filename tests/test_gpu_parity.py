@@ -223,3 +223,25 @@ def test_inactive_cells_uniform_and_partitioned():
     for a, b in zip(u.export_finest(), ou.export_finest()):
         np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))
     compare_states(many, one, "nodata river x4")
+
+
+@pytest.mark.parametrize("parts,name,kw", [(4, "pseudo2d_dambreak", dict(L=8)), (4, "monai_runup", dict(L=8)),
+                                            (8, "monai_runup", dict(L=9))])
+def test_rebalance_keeps_results(parts, name, kw):
+    """Dynamic repartitioning: boundaries move to equalise
+    the leaf counts, subtrees are pulled from their old owners, and the run
+    stays bitwise equal to one partition."""
+    cfg, h, qx, qy, z = cases.CASES[name](**kw)
+    one = gpu.initialise(cfg, h, qx, qy, z)
+    many = gpu.initialise_partitioned(cfg, h, qx, qy, z, [0] * parts)
+    moved = 0
+    for k in range(1, 31):
+        one.step_adaptive()
+        many.step_adaptive()
+        if k % 5 == 0:
+            moved += many.rebalance()
+            compare_states(many, one, f"{name} x{parts} after rebalance at step {k}")
+    assert moved > 0, "the leaf distribution never moved a boundary"
+    many.advance(10)
+    one.advance(10)
+    compare_states(many, one, f"{name} x{parts} end")
