@@ -70,6 +70,7 @@ struct swamp_gpu {
     int rank_world = 0;
     std::vector<void*> ipc_opened;
     bool serial = false;  // group on one device: all partitions on parts[0]'s stream
+    void* scratch = nullptr;  // device scratch of export_finest (3 x 4^L doubles), lazily allocated
 
     ~swamp_gpu() {
         for (swamp_gpu* q : parts) {
@@ -77,6 +78,7 @@ struct swamp_gpu {
             delete q;
         }
         for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+        if (scratch) cudaFree(scratch);
         if (graph1) cudaGraphExecDestroy(graph1);
         if (graphS) cudaGraphExecDestroy(graphS);
         if (graphT) cudaGraphExecDestroy(graphT);
@@ -188,8 +190,10 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
 
 // graph1: one step; graphS: kGraphSteps steps; graphT: one step with event
 // record nodes between the kernels (per-stage device times, StepReport)
-int build_graphs(swamp_gpu* g) {
-    for (int which = 0; which < 3; ++which) {
+// `which`: 0 = graph1, 1 = graphS, 2 = graphT; built on first use (each
+// instantiation costs ~1 ms of host time at creation otherwise)
+int build_graph(swamp_gpu* g, int which) {
+    {
         const int steps = which == 1 ? kGraphSteps : 1;
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
@@ -201,6 +205,13 @@ int build_graphs(swamp_gpu* g) {
         (which == 0 ? g->graph1 : which == 1 ? g->graphS : g->graphT) = exec;
     }
     return SWAMP_OK;
+}
+int build_graphs(swamp_gpu* g) { return build_graph(g, 0); }
+// single engines: the 8-step graph / the profiling graph on demand
+int ensure_graph(swamp_gpu* g, int which) {
+    cudaGraphExec_t e = which == 1 ? g->graphS : which == 2 ? g->graphT : g->graph1;
+    if (e || !g->parts.empty() || g->rank_world > 0) return SWAMP_OK;
+    return build_graph(g, which);
 }
 
 int fetch_ctl(swamp_gpu* g) {
@@ -380,24 +391,28 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
 
     // upload + import (the staging buffer is released right after)
     {
-        double* stage = nullptr;
-        if (cudaMalloc(&stage, 4 * nf * sizeof(double) + (P.has_ina ? nf : 0)) != cudaSuccess) return fail(SWAMP_E_NOMEM);
+        // DMA the host rasters (full speed from page-locked memory) into the
+        // second cell buffer, free until initialise copies buffer 0 into it
         const double* src[4] = {h, qx, qy, z};
-        for (int q = 0; q < 4; ++q)
+        double* stage = reinterpret_cast<double*>(P.cells[1]);
+        static_assert(sizeof(double4) == 4 * sizeof(double), "layout");
+        const double* dsrc[4];
+        for (int q = 0; q < 4; ++q) {
             cudaMemcpyAsync(stage + q * nf, src[q], nf * sizeof(double), cudaMemcpyHostToDevice, s);
+            dsrc[q] = stage + q * nf;
+        }
         uint8_t* mask = nullptr;
         if (P.has_ina) {
-            mask = reinterpret_cast<uint8_t*>(stage + 4 * nf);
+            mask = reinterpret_cast<uint8_t*>(stage + 4 * nf);  // (cells[1] holds 4 nf doubles + 1/8 more)
             cudaMemcpyAsync(mask, cfg->inactive, nf, cudaMemcpyHostToDevice, s);
         }
         const int grid = std::max(1, std::min<int>(g->num_sms * 8, static_cast<int>((nf + kThreads - 1) / kThreads)));
-        hwfv1::k_import<<<grid, kThreads, 0, s>>>(P, g->ctl, stage, stage + nf, stage + 2 * nf, stage + 3 * nf, mask, 0);
+        hwfv1::k_import<<<grid, kThreads, 0, s>>>(P, g->ctl, dsrc[0], dsrc[1], dsrc[2], dsrc[3], mask, 0);
         for (int n = L - 1; P.has_ina && n >= 0; --n) {
             const int gl = std::max(1, std::min<int>(g->num_sms * 4, static_cast<int>(((1u << (2 * n)) + kThreads - 1) / kThreads)));
             hwfv1::k_ina_level<<<gl, kThreads, 0, s>>>(P, n);
         }
         cudaError_t e = cudaStreamSynchronize(s);
-        cudaFree(stage);
         if (e != cudaSuccess) {
             g->err = cudaGetErrorString(e);
             return fail(SWAMP_E_CUDA);
@@ -975,7 +990,7 @@ int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep) {
     if (!g) return SWAMP_E_ARG;
     if (!g->parts.empty()) return group_advance(g, 1, true, rep);
     cudaSetDevice(g->device);
-    if (g->profiling && g->graphT) {
+    if (g->profiling && g->rank_world == 0 && ensure_graph(g, 2) == SWAMP_OK && g->graphT) {
         CK(cudaGraphLaunch(g->graphT, g->stream));
     } else {
         CK(cudaGraphLaunch(g->graph1, g->stream));
@@ -1009,6 +1024,10 @@ int swamp_gpu_enqueue(swamp_gpu* g, int64_t n_steps) {
     if (!g->parts.empty()) return group_advance(g, n_steps, false, nullptr);
     cudaSetDevice(g->device);
     int64_t k = 0;
+    if (n_steps >= kGraphSteps) {
+        const int st = ensure_graph(g, 1);
+        if (st) return st;
+    }
     for (; k + kGraphSteps <= n_steps; k += kGraphSteps) CK(cudaGraphLaunch(g->graphS, g->stream));
     for (; k < n_steps; ++k) CK(cudaGraphLaunch(g->graph1, g->stream));
     return SWAMP_OK;
@@ -1019,6 +1038,10 @@ int swamp_gpu_advance(swamp_gpu* g, int64_t n_steps, swamp_step_report* rep) {
     if (!g->parts.empty()) return group_advance(g, n_steps, true, rep);
     cudaSetDevice(g->device);
     int64_t k = 0;
+    if (n_steps >= kGraphSteps) {
+        const int st = ensure_graph(g, 1);
+        if (st) return st;
+    }
     for (; k + kGraphSteps <= n_steps; k += kGraphSteps) CK(cudaGraphLaunch(g->graphS, g->stream));
     for (; k < n_steps; ++k) CK(cudaGraphLaunch(g->graph1, g->stream));
     int st = fetch_ctl(g);
@@ -1125,16 +1148,15 @@ int swamp_gpu_export_finest(swamp_gpu* g, double* h, double* qx, double* qy) {
     }
     cudaSetDevice(g->device);
     const size_t nf = static_cast<size_t>(1) << (2 * g->P.L);
-    double* d = nullptr;
-    CK(cudaMalloc(&d, 3 * nf * sizeof(double)));
+    if (!g->scratch) CK(cudaMalloc(&g->scratch, 3 * nf * sizeof(double)));  // kept for later exports
+    double* d = static_cast<double*>(g->scratch);
     hwfv1::k_export_finest<<<std::max(1, g->num_sms * 8), kThreads, 0, g->stream>>>(g->P, g->ctl, d, d + nf,
                                                                                      d + 2 * nf);
-    cudaError_t e = cudaStreamSynchronize(g->stream);
+    // async copies on the engine stream: full speed into pinned host buffers
     double* outs[3] = {h, qx, qy};
-    for (int q = 0; q < 3 && e == cudaSuccess; ++q)
-        if (outs[q]) e = cudaMemcpy(outs[q], d + q * nf, nf * sizeof(double), cudaMemcpyDeviceToHost);
-    cudaFree(d);
-    CK(e);
+    for (int q = 0; q < 3; ++q)
+        if (outs[q]) CK(cudaMemcpyAsync(outs[q], d + q * nf, nf * sizeof(double), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
     return SWAMP_OK;
 }
 

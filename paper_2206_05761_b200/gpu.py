@@ -197,9 +197,16 @@ class Engine:
         self._check(lib().swamp_gpu_export_tree(self._h, *[dptr(a) for a in out], u8ptr(sig)), "export_tree")
         return out, sig
 
-    def export_finest(self):
+    def export_finest(self, out=None):
+        """Finest-grid expansion (h, qx, qy), row 0 = south. `out`: three
+        C-contiguous float64 (2^L, 2^L) arrays to fill (e.g. pinned_empty:
+        device-to-host copies at full speed)."""
         n = self.cfg.side
-        out = [np.zeros((n, n)) for _ in range(3)]
+        if out is None:
+            out = [np.zeros((n, n)) for _ in range(3)]
+        for a in out:
+            if a.dtype != np.float64 or not a.flags.c_contiguous or a.size != n * n:
+                raise ValueError("export_finest: out arrays must be C-contiguous float64 2^L x 2^L")
         self._check(lib().swamp_gpu_export_finest(self._h, *[dptr(a) for a in out]), "export_finest")
         return out
 
@@ -234,6 +241,22 @@ class Engine:
         a = (C.c_int64 * 8)()
         self._check(lib().swamp_gpu_counters(self._h, a), "counters")
         return list(a)[:5]
+
+
+def pinned_empty(shape, dtype=np.float64):
+    """A numpy array in page-locked host memory (torch's pinned allocator):
+    host <-> device copies through the C-ABI run at full PCIe speed."""
+    import torch
+
+    t = torch.empty(int(np.prod(shape)), dtype=torch.from_numpy(np.empty(0, dtype)).dtype, pin_memory=True)
+    return t.numpy().reshape(shape)
+
+
+def pinned_copy(a):
+    """A pinned-memory copy of array `a`."""
+    p = pinned_empty(np.shape(a), np.asarray(a).dtype)
+    p[...] = a
+    return p
 
 
 def initialise(cfg: SimConfig, h, qx, qy, z, device: int = 0) -> Engine:
