@@ -61,6 +61,7 @@ struct Ctl {
     alignas(128) unsigned long long cnt_new;     // newly significant cells decoded by the last K3
     unsigned long long cnt_updates;              // leaf updates of all steps so far (sum of N)
     alignas(128) unsigned long long k3_ready;    // K3's top CTA published its results (epoch)
+    alignas(128) unsigned long long k2_done;     // fused K2+K3: subtree CTAs done with K2 (reset by the top CTA)
     uint32_t n_stile;                            // subtrees on FV1's strip path this step
     alignas(128) unsigned long long smax_bits[4];
     int err_code;
@@ -1382,6 +1383,9 @@ __device__ __forceinline__ uint8_t band_flag(int mode, int L, int n, uint32_t m,
 // along the edge at word hw(d, k, pos) = d (2^(K-1) - 1) + 2^(k-1) - 1 + pos;
 // the adjacent subtrees' roots (level R) are bytes hr[d].
 template <int KT>
+__device__ void k2_tile(const Params& P, Ctl* ctl, const Head& hd, uint32_t j, uint8_t* smem2);
+
+template <int KT>
 __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int force, int do_top) {
     pdl_wait();
     pdl_trigger();
@@ -1393,13 +1397,19 @@ __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int fo
         encode_top_staged(P, ctl, hd.parity, smem2);
         return;
     }
+    k2_tile<KT>(P, ctl, hd, P.tile_lo + blockIdx.x - (do_top ? 1u : 0u), smem2);
+}
+
+// the subtree part of K2 (band, closure, counts, stores); leaves the final
+// flags of the subtree in smem2 + slo(K) (slo layout)
+template <int KT>
+__device__ void k2_tile(const Params& P, Ctl* ctl, const Head& hd, uint32_t j, uint8_t* smem2) {
     __shared__ unsigned s_red[32];
     __shared__ uint8_t hr[4];
     const int p = hd.parity;
     uint8_t* sigc = P.sig[p ^ 1];
     const int R = P.R;
     const int K = KT ? KT : P.K;
-    const uint32_t j = P.tile_lo + blockIdx.x - (do_top ? 1u : 0u);
     const uint32_t hwd = (1u << (K - 1)) - 1u;          // halo words per direction
     uint8_t* spre = smem2;                              // pre-band flags, slo layout
     uint8_t* sf = spre + slo(K);                        // band, then final flags, slo layout
@@ -1832,7 +1842,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
 // top), wait for the top's offsets, then decode and emit
 template <bool EXPORT, int KT>
 __device__ void k3_tile(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long long epoch, uint32_t j, uint8_t* sm,
-                        const Probe& stamp) {
+                        const Probe& stamp, bool staged = false, uint8_t q0_staged = 0) {
     __shared__ unsigned s_red[32];
     __shared__ uint32_t s_top[4];
     double4* buf = P.cells[p];
@@ -1847,12 +1857,16 @@ __device__ void k3_tile(const Params& P, Ctl* ctl, int p, int tbuf, unsigned lon
     uint32_t* src = reinterpret_cast<uint32_t*>(sp + slo(K));  // [ncell] projection sources
     (void)ncell;
 
-    const uint8_t c0 = stage_tile_flags(sc, sigc, P, j);
-    const uint8_t q0 = EXPORT ? 0 : stage_tile_flags(sp, sigp, P, j);
-    cp_async_wait_all();
-    if (threadIdx.x == 0) {
-        sc[0] = c0;
-        if (!EXPORT) sp[0] = q0;
+    if (staged) {  // fused K2+K3: current flags left by k2_tile, previous ones prefetched
+        if (threadIdx.x == 0) sp[0] = q0_staged;
+    } else {
+        const uint8_t c0 = stage_tile_flags(sc, sigc, P, j);
+        const uint8_t q0 = EXPORT ? 0 : stage_tile_flags(sp, sigp, P, j);
+        cp_async_wait_all();
+        if (threadIdx.x == 0) {
+            sc[0] = c0;
+            if (!EXPORT) sp[0] = q0;
+        }
     }
     __syncthreads();
     stamp(0);
@@ -2005,6 +2019,55 @@ __device__ void k3_tile(const Params& P, Ctl* ctl, int p, int tbuf, unsigned lon
     }
     if (!EXPORT) tl_end(ctl, tbuf, 2);
     stamp(6);
+}
+
+// K2 and K3 fused (one partition, every CTA resident — host-checked): block
+// 0 re-encodes levels < R, waits until every subtree CTA has finished its K2
+// part (counter), then does K3's top work and publishes; a subtree CTA runs
+// K2 and goes straight on with K3, its final flags still in shared memory and
+// its previous-tree flags prefetched during K2. One launch and one staging
+// round trip less.
+template <int KT>
+__global__ void __launch_bounds__(kThreads, 7) k_band_traverse(Params P, Ctl* ctl) {
+    pdl_wait();
+    pdl_trigger();
+    const unsigned long long t_entry = gtimer();
+    const Head hd = cta_head(ctl, P, false);
+    if (!hd.active) return;
+    extern __shared__ __align__(16) uint8_t smf[];
+    tl_start(ctl, hd.buf, 1);
+    const unsigned long long ep = 2ull * static_cast<unsigned long long>(hd.step) + 2ull;
+    const Probe stamp(ctl, 16);
+    stamp(7, t_entry);
+    if (blockIdx.x == 0) {
+        if (P.top_mode == 1) encode_top_staged(P, ctl, hd.parity, smf);
+        if (threadIdx.x == 0) {
+            const unsigned long long t0 = gtimer();
+            while (ld_acquire_u64(&ctl->k2_done) < P.tiles_per_part) {
+                __nanosleep(64);
+                if (gtimer() - t0 > 2000000000ull) {  // never expected: fail instead of hanging
+                    report_error(ctl, kErrBarrier, 0, 0, kStageBand);
+                    break;
+                }
+            }
+            ctl->k2_done = 0ull;  // every subtree has counted; none counts again in this launch
+        }
+        __syncthreads();
+        tl_start(ctl, hd.buf, 2);
+        k3_top<false>(P, ctl, hd.parity, hd.buf, ep, smf, stamp);
+        return;
+    }
+    const int K = KT ? KT : P.K;
+    const uint32_t j = P.tile_lo + blockIdx.x - 1u;
+    uint8_t* sp = smf + 2u * slo(K);
+    const uint8_t q0 = stage_tile_flags(sp, P.sig[hd.parity], P, j);  // completes with k2_tile's wait
+    k2_tile<KT>(P, ctl, hd, j, smf);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(&ctl->k2_done, 1ull);
+    }
+    k3_tile<false, KT>(P, ctl, hd.parity, hd.buf, ep, j, smf + slo(K), stamp, true, q0);
 }
 
 // epoch: 0 = hot path (2 step + 2, unique per step; the host clears the flag

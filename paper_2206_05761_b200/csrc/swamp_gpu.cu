@@ -58,6 +58,8 @@ struct swamp_gpu {
     void (*k2)(Params, Ctl*, int, int) = nullptr;
     void (*k3)(Params, Ctl*, int, unsigned long long) = nullptr;
     void (*k3x)(Params, Ctl*, int, unsigned long long) = nullptr;
+    void (*k23)(Params, Ctl*) = nullptr;  // fused K2+K3 (one partition, every CTA resident), else null
+    size_t smem_k23 = 0;
     unsigned long long export_epoch = 1ull << 62;  // K3 export launches (hot-path epochs are 2 step + 2)
     cudaEvent_t ev[6] = {};
     std::string err;
@@ -165,11 +167,17 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
         launch_pdl(g->k1, P.n_tiles, g->smem_k1s, s, P, g->ctl);
     if (P.top_mode == 2) launch_pdl(hwfv1::k_encode_top<false>, 1, g->smem_k1, s, P, g->ctl);
     mark(1);
-    const int do_top = P.top_mode == 1 ? 1 : 0;
-    launch_pdl(g->k2, P.n_tiles + do_top, g->smem_k2, s, P, g->ctl, 0, do_top);
-    mark(2);
-    launch_pdl(g->k3, P.n_tiles + 1, g->smem_k3, s, P, g->ctl, 0, 0ull);
-    mark(3);
+    if (g->k23) {
+        launch_pdl(g->k23, P.n_tiles + 1, g->smem_k23, s, P, g->ctl);
+        mark(2);
+        mark(3);
+    } else {
+        const int do_top = P.top_mode == 1 ? 1 : 0;
+        launch_pdl(g->k2, P.n_tiles + do_top, g->smem_k2, s, P, g->ctl, 0, do_top);
+        mark(2);
+        launch_pdl(g->k3, P.n_tiles + 1, g->smem_k3, s, P, g->ctl, 0, 0ull);
+        mark(3);
+    }
     const size_t sm5 = P.strips ? sizeof(double4) * (kThreads / 32) * hwfv1::kStripSlots : 0;
     if (P.has_ina)  // D16 variant (strips / quad / MINB variants do not handle inactive cells)
         launch_pdl(hwfv1::k_fv1<false, 2, false, false, false, true>, g->fv1_grid, 0, s, P, g->ctl);
@@ -490,6 +498,21 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         if (const char* e = std::getenv("SWAMP_FV1_STAGE")) g->fv1_stage = e[0] == '1';
         const char* es = std::getenv("SWAMP_FV1_STRIPS");
         P.strips = (es && es[0] == '1') ? 1 : 0;
+        // fused K2+K3 (opt-in SWAMP_FUSE_K23=1: measured slower on B200 — full
+        // residency caps it at 32 registers and it spills): one partition and
+        // every CTA resident at once (block 0 waits for all subtree CTAs)
+        const char* ef = std::getenv("SWAMP_FUSE_K23");
+        if (G == 1 && ef && ef[0] == '1') {
+            void (*f)(Params, Ctl*) = (P.K == 6) ? hwfv1::k_band_traverse<6> : hwfv1::k_band_traverse<0>;
+            const size_t ncell = ((size_t(1) << (2 * P.K)) - 1) / 3;
+            g->smem_k23 = std::max({3 * static_cast<size_t>(hwfv1::slo(P.K)) + 4 * ncell, g->smem_k2, g->smem_k3});
+            int occ = 0;
+            if (g->smem_k23 > 48 * 1024)
+                cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(g->smem_k23));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kThreads, g->smem_k23);
+            if (static_cast<int64_t>(occ) * g->num_sms >= static_cast<int64_t>(P.n_tiles) + 1) g->k23 = f;
+        }
         const char* eq = std::getenv("SWAMP_FV1_QUAD");
         P.quad = (eq && eq[0] == '1') ? 1 : 0;
         if (P.has_ina) P.strips = P.quad = 0;  // those paths do not handle inactive cells
