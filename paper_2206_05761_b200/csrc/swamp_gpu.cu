@@ -198,8 +198,8 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
 
 // graph1: one step; graphS: kGraphSteps steps; graphT: one step with event
 // record nodes between the kernels (per-stage device times, StepReport)
-// `which`: 0 = graph1, 1 = graphS, 2 = graphT; built on first use (each
-// instantiation costs ~1 ms of host time at creation otherwise)
+// `which`: 0 = graph1, 1 = graphS, 2 = graphT (the profiling graph is built
+// on first use)
 int build_graph(swamp_gpu* g, int which) {
     {
         const int steps = which == 1 ? kGraphSteps : 1;
@@ -214,7 +214,10 @@ int build_graph(swamp_gpu* g, int which) {
     }
     return SWAMP_OK;
 }
-int build_graphs(swamp_gpu* g) { return build_graph(g, 0); }
+int build_graphs(swamp_gpu* g) {  // graph1 and the 8-step graph now (timed loops replay it), graphT on demand
+    const int st = build_graph(g, 0);
+    return st ? st : build_graph(g, 1);
+}
 // single engines: the 8-step graph / the profiling graph on demand
 int ensure_graph(swamp_gpu* g, int which) {
     cudaGraphExec_t e = which == 1 ? g->graphS : which == 2 ? g->graphT : g->graph1;
