@@ -153,6 +153,7 @@ struct Params {
     uint32_t* stile;
     int strips;           // strip path enabled (SWAMP_FV1_STRIPS=1; measured slower on B200)
     int quad;             // sibling-quad path (SWAMP_FV1_QUAD=1; measured slower on B200)
+    int fv1_pf;           // FV1 prefetch of the next iteration's own cells: 0 off, 1 L2, 2 L1
     // Morton-subtree partitions: this partition owns level-R
     // subtrees [tile_lo, tile_hi); cells on levels >= R belong to their
     // subtree's partition, cells above R are replicated except that a leaf's
@@ -202,6 +203,8 @@ __device__ __forceinline__ double4 ld4_nc(const double4* p) {
     asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
     return v;
 }
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 __device__ __forceinline__ double4 ld4_cg(const double4* p) {
     double4 v;
     asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
@@ -2561,7 +2564,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                       s_bnd + (threadIdx.x >> 5) * kStripSlots, mx, tree);
     }
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
+    const int pf = P.fv1_pf;
+    // leaf ids two iterations ahead; the next iteration's own cell is
+    // prefetched (no registers held) while this one computes: the leaf
+    // cells were written a step ago and come from DRAM
     uint32_t z_next = (!UNIFORM && wbase + lane < N) ? leaf_at(wbase + lane) : 0u;
+    uint32_t z_nn = (!UNIFORM && pf && wbase + stride + lane < N) ? leaf_at(wbase + stride + lane) : 0u;
     for (; wbase < N; wbase += stride) {
         const uint32_t i = wbase + lane;
         bool valid = i < N;
@@ -2570,9 +2578,23 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
         if (UNIFORM) {
             n = P.L;
             m = valid ? i : 0u;
+            if (pf && i + stride < N) {
+                const double4* q = cur + cbase(n) + i + stride;
+                if (pf == 2) prefetch_l1(q); else prefetch_l2(q);
+            }
         } else {
             const uint32_t z = valid ? z_next : zo::level_offset(P.L);  // leaf ids prefetched one iteration ahead
-            if (i + stride < N) z_next = leaf_at(i + stride);
+            if (pf) {
+                z_next = z_nn;
+                if (i + 2 * stride < N) z_nn = leaf_at(i + 2 * stride);
+                if (i + stride < N) {
+                    const int n1 = zo::level_of(z_next);
+                    const double4* q = cur + cbase(n1) + (z_next - zo::level_offset(n1));
+                    if (pf == 2) prefetch_l1(q); else prefetch_l2(q);
+                }
+            } else if (i + stride < N) {
+                z_next = leaf_at(i + stride);
+            }
             n = zo::level_of(z);
             m = z - zo::level_offset(n);
         }

@@ -516,6 +516,8 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kThreads, g->smem_k23);
             if (static_cast<int64_t>(occ) * g->num_sms >= static_cast<int64_t>(P.n_tiles) + 1) g->k23 = f;
         }
+        const char* epf = std::getenv("SWAMP_FV1_PF");
+        P.fv1_pf = epf ? std::atoi(epf) : 1;  // L2 prefetch: FV1 72 -> 69 us (round 1)
         const char* eq = std::getenv("SWAMP_FV1_QUAD");
         P.quad = (eq && eq[0] == '1') ? 1 : 0;
         if (P.has_ina) P.strips = P.quad = 0;  // those paths do not handle inactive cells
