@@ -2515,7 +2515,7 @@ __device__ __forceinline__ void fv1_quad(const Params& P, const double4* __restr
 // FV1 over the leaf list: persistent grid-stride, one thread per
 // leaf; reads the current buffer, writes leaf slots of the other (D15).
 template <bool UNIFORM, int MINB = 2, bool PART = false, bool STRIPS = false, bool QUAD = false, bool INA = false,
-          bool STAGE = false>
+          int STAGE = 0>
 __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     pdl_wait();
     pdl_trigger();
@@ -2564,17 +2564,39 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                       s_bnd + (threadIdx.x >> 5) * kStripSlots, mx, tree);
     }
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
-    const int pf = P.fv1_pf;
+    // STAGE 2: the next iteration's own cell and subtree activity are loaded
+    // into registers one iteration ahead (instead of an L2 prefetch)
+    const int pf = (STAGE >= 2) ? 1 : P.fv1_pf;
     // leaf ids two iterations ahead; the next iteration's own cell is
     // prefetched (no registers held) while this one computes: the leaf
     // cells were written a step ago and come from DRAM
     uint32_t z_next = (!UNIFORM && wbase + lane < N) ? leaf_at(wbase + lane) : 0u;
     uint32_t z_nn = (!UNIFORM && pf && wbase + stride + lane < N) ? leaf_at(wbase + stride + lane) : 0u;
+    double4 o4_pre = make_double4(0.0, 0.0, 0.0, 0.0);
+    uint8_t ta_pre = 1;
+    uint8_t fl_pre[4] = {1, 1, 1, 1};  // STAGE 3: the neighbours' parent-level flags too
+    auto pre_load = [&](uint32_t zz) {
+        const int n1 = zo::level_of(zz);
+        const uint32_t m1 = zz - zo::level_offset(n1);
+        o4_pre = ld4_nc(cur + cbase(n1) + m1);
+        ta_pre = (!PART && n1 >= P.R) ? P.tact[m1 >> (2 * (n1 - P.R))] : 1;
+        if (STAGE == 3 && n1 > 0) {
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+                const uint32_t q = zo::neighbour_dev(n1, m1, static_cast<zo::Direction>(d));
+                fl_pre[d] = (q != zo::kNone) ? sigc[slo(n1 - 1) + (q >> 2)] : 1;
+            }
+        }
+    };
+    if (STAGE >= 2 && !UNIFORM && wbase + lane < N) pre_load(z_next);
     for (; wbase < N; wbase += stride) {
         const uint32_t i = wbase + lane;
         bool valid = i < N;
         int n;
         uint32_t m;
+        const double4 o4_k = o4_pre;
+        const uint8_t ta_k = ta_pre;
+        const uint8_t fl_k[4] = {fl_pre[0], fl_pre[1], fl_pre[2], fl_pre[3]};
         if (UNIFORM) {
             n = P.L;
             m = valid ? i : 0u;
@@ -2588,9 +2610,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                 z_next = z_nn;
                 if (i + 2 * stride < N) z_nn = leaf_at(i + 2 * stride);
                 if (i + stride < N) {
-                    const int n1 = zo::level_of(z_next);
-                    const double4* q = cur + cbase(n1) + (z_next - zo::level_offset(n1));
-                    if (pf == 2) prefetch_l1(q); else prefetch_l2(q);
+                    if (STAGE >= 2) {
+                        pre_load(z_next);
+                    } else {
+                        const int n1 = zo::level_of(z_next);
+                        const double4* q = cur + cbase(n1) + (z_next - zo::level_offset(n1));
+                        if (pf == 2) prefetch_l1(q); else prefetch_l2(q);
+                    }
                 }
             } else if (i + stride < N) {
                 z_next = leaf_at(i + stride);
@@ -2599,7 +2625,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             m = z - zo::level_offset(n);
         }
         // subtree activity (bit 0: wet neighbourhood, bit 1: strip path)
-        const uint8_t ta = (!UNIFORM && !PART && valid && n >= P.R) ? P.tact[m >> (2 * (n - P.R))] : 1;
+        const uint8_t ta = (STAGE >= 2 && !UNIFORM) ? (valid ? ta_k : 1)
+                           : ((!UNIFORM && !PART && valid && n >= P.R) ? P.tact[m >> (2 * (n - P.R))] : 1);
         if (STRIPS && (ta & 2u)) valid = false;  // updated by the strip path above
         double hn = 0.0, qxn = 0.0, qyn = 0.0, zown = 0.0;
         // a warp of whole sibling quadruples of level-L leaves: the quad path
@@ -2617,7 +2644,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
         if (valid && !quadw) {
             // every global read of this leaf is issued before any arithmetic:
             // own cell, the neighbours' parent-level flags, the neighbours
-            const double4 o4 = ld4_nc(cur + cbase(n) + m);
+            const double4 o4 = (STAGE >= 2 && !UNIFORM) ? o4_k : ld4_nc(cur + cbase(n) + m);
             // dry shortcut: in a subtree whose neighbourhood holds no wet cell
             // (K3's tact) the leaf and all its neighbours are dry, so the
             // dry-neighbourhood result below follows without the gathers
@@ -2689,7 +2716,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                     }
                 } else {
 #pragma unroll
-                    for (int d = 0; d < 4; ++d) f[d] = (nm[d] != zo::kNone) ? sigc[slo(n - 1) + (nm[d] >> 2)] : 1;
+                    for (int d = 0; d < 4; ++d)
+                        f[d] = (STAGE == 3) ? fl_k[d] : ((nm[d] != zo::kNone) ? sigc[slo(n - 1) + (nm[d] >> 2)] : 1);
 #pragma unroll
                     for (int d = 0; d < 4; ++d)
                         src[d] = f[d] ? cur + cbase(n) + nm[d] : covering_local(P, cur, sigc, n - 1, nm[d] >> 2);
@@ -2697,13 +2725,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             }
             // STAGE: the neighbours land in shared memory by cp.async (no
             // registers held across the load; slot [warp][d][lane])
-            __shared__ __align__(16) double4 s_nb[STAGE ? kThreads / 32 * 4 * 32 : 1];
-            double4 r4s[STAGE ? 1 : 4];
+            __shared__ __align__(16) double4 s_nb[STAGE == 1 ? kThreads / 32 * 4 * 32 : 1];
+            double4 r4s[STAGE == 1 ? 1 : 4];
             auto nbv = [&](int d) -> double4 {
-                if (STAGE) return s_nb[((threadIdx.x >> 5) * 4 + d) * 32 + lane];
-                return r4s[STAGE ? 0 : d];
+                if (STAGE == 1) return s_nb[((threadIdx.x >> 5) * 4 + d) * 32 + lane];
+                return r4s[STAGE == 1 ? 0 : d];
             };
-            if (STAGE) {
+            if (STAGE == 1) {
 #pragma unroll
                 for (int d = 0; d < 4; ++d)
                     if (nm[d] != zo::kNone) {
@@ -2715,7 +2743,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             } else {
 #pragma unroll
                 for (int d = 0; d < 4; ++d)
-                    if (nm[d] != zo::kNone) r4s[STAGE ? 0 : d] = ld4_nc(src[d]);
+                    if (nm[d] != zo::kNone) r4s[STAGE == 1 ? 0 : d] = ld4_nc(src[d]);
             }
             // dry neighbourhood: own cell and every neighbour / ghost below
             // h_dry => every reconstructed depth is 0, every flux 0, the bed

@@ -49,7 +49,11 @@ struct swamp_gpu {
     cudaGraphExec_t graph1 = nullptr, graphS = nullptr, graphT = nullptr;
     int fv1_grid = 0;
     int fv1_minb = 2;  // occupancy variant of k_fv1 (SWAMP_FV1_MINB=3|4 for more CTAs/SM, with spills)
-    bool fv1_stage = false;  // SWAMP_FV1_STAGE=1: neighbours staged in shared memory, 3 CTAs/SM
+    // SWAMP_FV1_STAGE=1: neighbours staged in shared memory, 3 CTAs/SM (slower);
+    // 2: own cell and subtree activity loaded an iteration ahead (FV1 69 ->
+    // 66 us); 3 (default): also the neighbours' parent-level flags (65 us);
+    // 0: L2 prefetch only
+    int fv1_stage = 3;
     int num_sms = 0;
     size_t smem_k1 = 0, smem_k1s = 0, smem_k1p = 0, smem_k2 = 0, smem_k3 = 0;
     int k1p_grid = 0;     // persistent K1 (K = 6): CTAs
@@ -185,8 +189,12 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
         launch_pdl(hwfv1::k_fv1<false, 2, false, true>, g->fv1_grid, sm5, s, P, g->ctl);
     else if (P.quad)
         launch_pdl(hwfv1::k_fv1<false, 2, false, false, true>, g->fv1_grid, 0, s, P, g->ctl);
-    else if (g->fv1_stage)
-        launch_pdl(hwfv1::k_fv1<false, 3, false, false, false, false, true>, g->fv1_grid, 0, s, P, g->ctl);
+    else if (g->fv1_stage == 1)
+        launch_pdl(hwfv1::k_fv1<false, 3, false, false, false, false, 1>, g->fv1_grid, 0, s, P, g->ctl);
+    else if (g->fv1_stage == 2)
+        launch_pdl(hwfv1::k_fv1<false, 2, false, false, false, false, 2>, g->fv1_grid, 0, s, P, g->ctl);
+    else if (g->fv1_stage == 3)
+        launch_pdl(hwfv1::k_fv1<false, 2, false, false, false, false, 3>, g->fv1_grid, 0, s, P, g->ctl);
     else if (g->fv1_minb == 4)
         launch_pdl(hwfv1::k_fv1<false, 4>, g->fv1_grid, sm5, s, P, g->ctl);
     else if (g->fv1_minb == 3)
@@ -498,7 +506,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     }
     {
         if (const char* e = std::getenv("SWAMP_FV1_MINB")) g->fv1_minb = std::max(2, std::min(4, std::atoi(e)));
-        if (const char* e = std::getenv("SWAMP_FV1_STAGE")) g->fv1_stage = e[0] == '1';
+        if (const char* e = std::getenv("SWAMP_FV1_STAGE")) g->fv1_stage = std::atoi(e);
         const char* es = std::getenv("SWAMP_FV1_STRIPS");
         P.strips = (es && es[0] == '1') ? 1 : 0;
         // fused K2+K3 (opt-in SWAMP_FUSE_K23=1: measured slower on B200 — full
@@ -530,8 +538,11 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             g->k1p_grid = std::max(1, std::min<int>(static_cast<int>(P.tiles_per_part), std::max(1, occ1) * g->num_sms));
         }
         int occ = 0;
-        if (g->fv1_stage)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 3, false, false, false, false, true>,
+        if (g->fv1_stage == 1)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 3, false, false, false, false, 1>,
+                                                          kThreads, 0);
+        else if (g->fv1_stage >= 2)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 2, false, false, false, false, 2>,
                                                           kThreads, 0);
         else if (g->fv1_minb == 4)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 4>, kThreads, 0);
