@@ -867,6 +867,26 @@ __device__ void encode_top(const Params& P, Ctl* ctl, double4* sv, unsigned* s_r
 
 
 
+// encode_children_t of the four values in lanes l, l+s, l+2s, l+3s (valid in
+// the lanes that own a parent; every lane of the warp must call it)
+__device__ __forceinline__ Enc encode_lanes_s(double4 v, int s, const double* thr4) {
+    const int lane = threadIdx.x & 31;
+    const int l1 = (lane + s) & 31, l2 = (lane + 2 * s) & 31, l3 = (lane + 3 * s) & 31;
+    auto red = [&](double x) {
+        return red4(x, __shfl_sync(kFull, x, l1), __shfl_sync(kFull, x, l2), __shfl_sync(kFull, x, l3));
+    };
+    const Red h = red(v.x);
+    const Red qx = red(v.y);
+    const Red qy = red(v.z);
+    const double w1 = __shfl_sync(kFull, v.w, l1), w2 = __shfl_sync(kFull, v.w, l2), w3 = __shfl_sync(kFull, v.w, l3);
+    const double a = v.w + w1, b = w2 + w3;
+    Enc e;
+    e.flow = sig_q(h.dmax, thr4[0]) || sig_q(qx.dmax, thr4[1]) || sig_q(qy.dmax, thr4[2]);
+    e.par = make_double4(h.par, qx.par, qy.par, 0.25 * (a + b));
+    e.zflag = false;
+    return e;
+}
+
 // K1 after t = 0 (level L-1 was re-encoded and flagged by the previous
 // FV1): re-encode + threshold of levels L-2 .. R of subtree j. Everything the
 // CTA reads is issued at once: the previous-tree and DEM flags of levels
@@ -978,53 +998,126 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
     }
     unsigned tree = 0;
     stamp(2);
-    // ---- level L-2 from the registers
-    if (has2) {
-        bool flow = 0.0 >= s_thr[L - 2][3];
-        if (sp2) {
-            const Enc e = encode_children_t(ch, s_thr[L - 2]);
-            flow = e.flow;
-            sv[lo(k2, 0) + threadIdx.x] = e.par;
-            ++tree;
+    if constexpr (KT == 6) {
+        // K = 6: levels L-2 .. R without a CTA barrier per level — L-2 in
+        // registers (one cell per thread), L-3 and L-4 by shuffles inside the
+        // warp, the 16 level-(L-4) values through shared memory to warp 0 for
+        // R+1 and R. A cell on the previous tree is re-encoded and stored at
+        // once; the others keep their staged value (same arithmetic and
+        // results as the per-level loop below).
+        const int tid = threadIdx.x, lane = tid & 31;
+        double4 v;
+        {
+            bool flow = 0.0 >= s_thr[L - 2][3];
+            if (sp2) {
+                const Enc e = encode_children_t(ch, s_thr[L - 2]);
+                flow = e.flow;
+                v = e.par;
+                st4(buf + cbase(L - 2) + m2, v);
+                ++tree;
+            } else {
+                v = sv[lo(4, 0) + tid];
+            }
+            so[slo(4) + tid] = (flow || sd[slo(4) + tid]) ? 1 : 0;
         }
-        so[slo(k2) + threadIdx.x] = (flow || sd[slo(k2) + threadIdx.x]) ? 1 : 0;
-    }
-    __syncthreads();
-    stamp(3);
-    // ---- levels L-3 .. R in shared memory
-#pragma unroll
-    for (int k = (KT ? KT : kMaxL) - 3; k >= 0; --k) {
-        if (!KT && k > K - 3) continue;
-        const int n = R + k;
-        const uint32_t cnt = 1u << (2 * k);
-        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
+        auto level = [&](int k, uint32_t pi, const Enc& e) {  // cell pi of tile level k, k < 4
+            const int n = R + k;
             bool flow = 0.0 >= s_thr[n][3];
             if (sf[slo(k) + pi]) {
-                const uint32_t c0 = lo(k + 1, 0) + 4u * pi;
-                const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
-                const Enc e = encode_children_t(c, s_thr[n]);
                 flow = e.flow;
-                sv[lo(k, 0) + pi] = e.par;
+                v = e.par;
+                st4(buf + cbase(n) + static_cast<unsigned long long>(j) * (1u << (2 * k)) + pi, v);
                 ++tree;
+            } else if (k > 0) {
+                v = sv[lo(k, 0) + pi];
             }
             so[slo(k) + pi] = (flow || sd[slo(k) + pi]) ? 1 : 0;
+        };
+        {
+            const Enc e = encode_lanes_s(v, 1, s_thr[L - 3]);
+            if ((lane & 3) == 0) level(3, static_cast<uint32_t>(tid) >> 2, e);
+        }
+        {
+            const Enc e = encode_lanes_s(v, 4, s_thr[L - 4]);
+            if ((lane & 15) == 0) {
+                const uint32_t pi = static_cast<uint32_t>(tid) >> 4;
+                level(2, pi, e);
+                sv[lo(2, 0) + pi] = v;
+            }
         }
         __syncthreads();
-    }
-    stamp(4);
-    // ---- one burst of stores: re-encoded values (previous-tree cells) and
-    //      the pre-band flags of levels R..L-2 (words where a level has >= 4)
-    for (int k = 0; k <= K - 2; ++k) {
-        const uint32_t cnt = 1u << (2 * k);
-        const unsigned long long jb = static_cast<unsigned long long>(j) * cnt;
-        for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads)
-            if (sf[slo(k) + pi]) st4(buf + cbase(R + k) + jb + pi, sv[lo(k, 0) + pi]);
-        if (cnt >= 4) {
-            for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads)
-                *reinterpret_cast<uint32_t*>(P.pre + slo(R + k) + jb + q) = *reinterpret_cast<const uint32_t*>(so + slo(k) + q);
-        } else if (threadIdx.x == 0) {
-            P.pre[slo(R) + jb] = so[0];
+        if (tid < 32) {
+            v = sv[lo(2, 0) + (lane & 15)];
+            {
+                const Enc e = encode_lanes_s(v, 1, s_thr[R + 1]);
+                if ((lane & 3) == 0 && lane < 16) level(1, static_cast<uint32_t>(lane) >> 2, e);
+            }
+            {
+                const Enc e = encode_lanes_s(v, 4, s_thr[R]);
+                if (lane == 0) level(0, 0u, e);
+            }
         }
+        __syncthreads();
+        stamp(4);
+        for (int k = 0; k <= 4; ++k) {  // pre-band flags of levels R..L-2 (words where a level has >= 4)
+            const uint32_t cnt = 1u << (2 * k);
+            const unsigned long long jb = static_cast<unsigned long long>(j) * cnt;
+            if (cnt >= 4) {
+                for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads)
+                    *reinterpret_cast<uint32_t*>(P.pre + slo(R + k) + jb + q) = *reinterpret_cast<const uint32_t*>(so + slo(k) + q);
+            } else if (threadIdx.x == 0) {
+                P.pre[slo(R) + jb] = so[0];
+            }
+        }
+    } else {
+        if (has2) {
+            bool flow = 0.0 >= s_thr[L - 2][3];
+            if (sp2) {
+                const Enc e = encode_children_t(ch, s_thr[L - 2]);
+                flow = e.flow;
+                sv[lo(k2, 0) + threadIdx.x] = e.par;
+                ++tree;
+            }
+            so[slo(k2) + threadIdx.x] = (flow || sd[slo(k2) + threadIdx.x]) ? 1 : 0;
+        }
+        __syncthreads();
+        stamp(3);
+        // ---- levels L-3 .. R in shared memory
+#pragma unroll
+        for (int k = (KT ? KT : kMaxL) - 3; k >= 0; --k) {
+            if (!KT && k > K - 3) continue;
+            const int n = R + k;
+            const uint32_t cnt = 1u << (2 * k);
+            for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
+                bool flow = 0.0 >= s_thr[n][3];
+                if (sf[slo(k) + pi]) {
+                    const uint32_t c0 = lo(k + 1, 0) + 4u * pi;
+                    const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
+                    const Enc e = encode_children_t(c, s_thr[n]);
+                    flow = e.flow;
+                    sv[lo(k, 0) + pi] = e.par;
+                    ++tree;
+                }
+                so[slo(k) + pi] = (flow || sd[slo(k) + pi]) ? 1 : 0;
+            }
+            __syncthreads();
+        }
+        stamp(4);
+        // ---- one burst of stores: re-encoded values (previous-tree cells) and
+        //      the pre-band flags of levels R..L-2 (words where a level has >= 4)
+        for (int k = 0; k <= K - 2; ++k) {
+            const uint32_t cnt = 1u << (2 * k);
+            const unsigned long long jb = static_cast<unsigned long long>(j) * cnt;
+            for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads)
+                if (sf[slo(k) + pi]) st4(buf + cbase(R + k) + jb + pi, sv[lo(k, 0) + pi]);
+            if (cnt >= 4) {
+                for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads)
+                    *reinterpret_cast<uint32_t*>(P.pre + slo(R + k) + jb + q) = *reinterpret_cast<const uint32_t*>(so + slo(k) + q);
+            } else if (threadIdx.x == 0) {
+                P.pre[slo(R) + jb] = so[0];
+            }
+        }
+
     }
     const unsigned tsum = block_sum(tree, s_red);
     if (threadIdx.x == 0 && tsum) atomicAdd(&ctl->cnt_tree, (unsigned long long)tsum);
