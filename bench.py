@@ -321,12 +321,15 @@ def main():
     t0 = time.perf_counter()
     e = (gpu.initialise_rank(cfg, hp, qxp, qyp, zp, rank, ws, dev, torch_allgather) if ws > 1
          else gpu.initialise(cfg, hp, qxp, qyp, zp, device=dev))
+    t1 = time.perf_counter()
     up = 0
     for _ in range(K):
         r = e.step_adaptive()  # each step reads its StepReport back
         up += r["n_leaves"]
+    t2 = time.perf_counter()
     fh, fqx, fqy = e.export_finest(out=outs)  # (rank 0's copy is the whole grid: peer reads)
     e2e_s = time.perf_counter() - t0
+    e2e_parts = {"initialise": t1 - t0, "steps": t2 - t1, "export": t0 + e2e_s - t2}
     if ws > 1:
         e2e_s = max_over_ranks(e2e_s)
         dist.barrier()
@@ -336,7 +339,7 @@ def main():
         h2d = 4 * nf * 8
         d2h = 3 * nf * 8 + K * 96
         e2e = {"value": up / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d // K, "d2h_bytes_per_step": d2h // K,
-               "seconds": e2e_s,
+               "seconds": e2e_s, "seconds_by_phase": e2e_parts,
                "note": "initialise from pinned host rasters (h, qx, qy, z) + K steps (StepReport read-back "
                        "each) + finest export (h, qx, qy) into pinned buffers"}
 

@@ -115,6 +115,13 @@ int swamp_gpu_create(const swamp_config* cfg, const double* h, const double* qx,
                      const double* z, int device, swamp_gpu** out);
 int swamp_gpu_destroy(swamp_gpu* g);
 
+/* Destroyed engines return their device buffers (and pinned control mirrors)
+ * to a process-wide cache that the next swamp_gpu_create of the same shape
+ * reuses (cudaMalloc / cudaFree of an L = 11 engine's ~400 MB cost 3-50 ms
+ * per call on B200). This releases every cached block of `device` (-1: all
+ * devices). No reference counterpart (host-side allocation policy). */
+int swamp_gpu_trim_cache(int device);
+
 /* Morton-subtree partitioned engine (BASELINE north star):
  * n_parts (1, 2, 4 or 8; must divide the number of level-R subtrees 4^R)
  * contiguous ranges of level-R subtrees, partition k on CUDA device

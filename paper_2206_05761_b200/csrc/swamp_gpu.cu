@@ -12,8 +12,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -35,6 +39,68 @@ struct Mem {
     }
 };
 
+// Process-wide cache of device blocks and pinned control mirrors: an engine's
+// buffers go back here when it is destroyed and the next engine of the same
+// shape reuses them. cudaMalloc / cudaFree of the ~400 MB an L = 11 engine
+// holds cost 3-50 ms each time (measured on B200), which would otherwise land
+// in every initialise. Capped at kCacheCap bytes per process;
+// swamp_gpu_trim_cache() releases it. (Never destroyed: freeing at process
+// exit would race the CUDA runtime's own teardown.)
+constexpr size_t kCacheCap = size_t(16) << 30;
+struct BlockCache {
+    std::mutex mu;
+    std::multimap<std::pair<int, size_t>, void*> dev;  // (device, bytes) -> block
+    std::vector<void*> pinned;                          // sizeof(Ctl) host blocks
+    size_t bytes = 0;
+};
+BlockCache& block_cache() {
+    static BlockCache* c = new BlockCache;
+    return *c;
+}
+cudaError_t cached_malloc(int device, void** p, size_t bytes) {
+    BlockCache& c = block_cache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = c.dev.find({device, bytes});
+        if (it != c.dev.end()) {
+            *p = it->second;
+            c.dev.erase(it);
+            c.bytes -= bytes;
+            return cudaSuccess;
+        }
+    }
+    return cudaMalloc(p, bytes);
+}
+void cached_free(int device, void* p, size_t bytes) {
+    BlockCache& c = block_cache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        if (c.bytes + bytes <= kCacheCap) {
+            c.dev.insert({{device, bytes}, p});
+            c.bytes += bytes;
+            return;
+        }
+    }
+    cudaFree(p);
+}
+cudaError_t cached_pinned_ctl(Ctl** p) {
+    BlockCache& c = block_cache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        if (!c.pinned.empty()) {
+            *p = static_cast<Ctl*>(c.pinned.back());
+            c.pinned.pop_back();
+            return cudaSuccess;
+        }
+    }
+    return cudaMallocHost(reinterpret_cast<void**>(p), sizeof(Ctl));
+}
+void cached_free_pinned_ctl(Ctl* p) {
+    BlockCache& c = block_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.pinned.push_back(p);
+}
+
 }  // namespace
 
 struct swamp_gpu {
@@ -45,7 +111,7 @@ struct swamp_gpu {
     Params P{};
     Ctl* ctl = nullptr;      // device
     Ctl* ctl_host = nullptr; // pinned mirror
-    std::vector<void*> allocs;
+    std::vector<std::pair<void*, size_t>> allocs;  // device blocks (returned to the block cache)
     cudaGraphExec_t graph1 = nullptr, graphS = nullptr, graphT = nullptr;
     int fv1_grid = 0;
     int fv1_minb = 2;  // occupancy variant of k_fv1 (SWAMP_FV1_MINB=3|4 for more CTAs/SM, with spills)
@@ -77,6 +143,7 @@ struct swamp_gpu {
     std::vector<void*> ipc_opened;
     bool serial = false;  // group on one device: all partitions on parts[0]'s stream
     void* scratch = nullptr;  // device scratch of export_finest (3 x 4^L doubles), lazily allocated
+    size_t scratch_bytes = 0;
 
     ~swamp_gpu() {
         for (swamp_gpu* q : parts) {
@@ -84,14 +151,16 @@ struct swamp_gpu {
             delete q;
         }
         for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
-        if (scratch) cudaFree(scratch);
+        if (scratch) cached_free(device, scratch, scratch_bytes);
         if (graph1) cudaGraphExecDestroy(graph1);
         if (graphS) cudaGraphExecDestroy(graphS);
         if (graphT) cudaGraphExecDestroy(graphT);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
-        for (void* a : allocs) cudaFree(a);
-        if (ctl_host) cudaFreeHost(ctl_host);
+        if (!allocs.empty() || scratch) cudaSetDevice(device);
+        if (!allocs.empty()) cudaDeviceSynchronize();  // no kernel may still use a block that goes back to the cache
+        for (auto& a : allocs) cached_free(device, a.first, a.second);
+        if (ctl_host) cached_free_pinned_ctl(ctl_host);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -110,12 +179,13 @@ namespace {
 template <class T>
 int dalloc(swamp_gpu* g, T** out, size_t bytes) {
     void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 16));
+    bytes = std::max<size_t>(bytes, 16);
+    cudaError_t e = cached_malloc(g->device, &p, bytes);
     if (e != cudaSuccess) {
         g->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
         return SWAMP_E_NOMEM;
     }
-    g->allocs.push_back(p);
+    g->allocs.push_back({p, bytes});
     *out = static_cast<T*>(p);
     return SWAMP_OK;
 }
@@ -286,9 +356,26 @@ void fill_report(const swamp_gpu* g, swamp_step_report* r) {
 // allocate + upload + import one (sub-)engine: everything before the
 // initialise pipeline. Partition `part` of `G` owns level-R subtrees
 // [part, part+1) * 4^R / G.
+// SWAMP_TRACE=1: wall time of the creation phases on stderr (diagnostics)
+struct Trace {
+    bool on = false;
+    std::chrono::steady_clock::time_point t0;
+    Trace() {
+        const char* e = std::getenv("SWAMP_TRACE");
+        on = e && e[0] == '1';
+        t0 = std::chrono::steady_clock::now();
+    }
+    void operator()(const char* what) const {
+        if (on)
+            std::fprintf(stderr, "[swamp] %-28s %8.3f ms\n", what,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
 int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const double* qx, const double* qy,
                const double* z, int device, int G, int part) {
     int st = SWAMP_OK;
+    const Trace tr;
     auto fail = [&](int code) { return code; };
     g->device = device;
     if (cudaSetDevice(device) != cudaSuccess) return fail(SWAMP_E_CUDA);
@@ -296,6 +383,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     for (auto& e : g->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return fail(SWAMP_E_CUDA);
     cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
+    tr("stream + events");
 
     Params& P = g->P;
     const int L = cfg->L;
@@ -386,7 +474,9 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     P.ppre[0] = P.pre;
     P.ptile_cnt[0] = P.tile_cnt;
     P.pctl[0] = g->ctl;
-    if (cudaMallocHost(&g->ctl_host, sizeof(Ctl)) != cudaSuccess) return fail(SWAMP_E_NOMEM);
+    tr("device allocations");
+    if (cached_pinned_ctl(&g->ctl_host) != cudaSuccess) return fail(SWAMP_E_NOMEM);
+    tr("pinned control block");
     double *d_it = nullptr, *d_iv = nullptr, *d_out = nullptr;
     if ((st = dalloc(g, &d_it, sizeof(double) * std::max(1, cfg->inflow_n)))) return fail(st);
     if ((st = dalloc(g, &d_iv, sizeof(double) * std::max(1, cfg->inflow_n)))) return fail(st);
@@ -437,6 +527,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             return fail(SWAMP_E_CUDA);
         }
     }
+    tr("upload + import");
     if (cudaMemcpy(g->ctl_host, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost) != cudaSuccess) return fail(SWAMP_E_CUDA);
     if (g->ctl_host->err_code) return fail(SWAMP_E_NONFINITE);
     for (int q = 0; q < 4; ++q) {
@@ -553,6 +644,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         g->fv1_grid = std::max(1, occ) * g->num_sms;
     }
     g->n_cells = static_cast<int64_t>(off);
+    tr("kernel attributes");
     return SWAMP_OK;
 }
 
@@ -568,7 +660,9 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
         delete g;
         return code;
     };
+    const Trace tr;
     if ((st = setup_part(g, cfg, h, qx, qy, z, device, 1, 0))) return fail(st);
+    tr("setup");
     Params& P = g->P;
     cudaStream_t s = g->stream;
     const unsigned long long off = static_cast<unsigned long long>(g->n_cells);
@@ -605,10 +699,12 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
         }
         if (cudaGetLastError() != cudaSuccess) return fail(SWAMP_E_CUDA);
     }
+    tr("initial tree");
     if ((st = fetch_ctl(g))) return fail(st);
     cudaMemsetAsync(g->ctl->tl, 0, sizeof(g->ctl->tl), s);
     cudaMemsetAsync(&g->ctl->k3_ready, 0, sizeof(g->ctl->k3_ready), s);  // hot-path epochs restart at step 0
     if ((st = build_graphs(g))) return fail(st);
+    tr("graphs");
     *out = g;
     return SWAMP_OK;
 }
@@ -1007,6 +1103,34 @@ int swamp_gpu_create_uniform(const swamp_config* cfg, const double* h, const dou
     return create_impl(cfg, h, qx, qy, z, device, true, out);
 }
 
+int swamp_gpu_trim_cache(int device) {
+    BlockCache& c = block_cache();
+    std::vector<std::pair<int, void*>> dev;
+    std::vector<void*> pinned;
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        for (auto it = c.dev.begin(); it != c.dev.end();) {
+            if (device < 0 || it->first.first == device) {
+                dev.push_back({it->first.first, it->second});
+                c.bytes -= it->first.second;
+                it = c.dev.erase(it);
+            } else {
+                ++it;
+            }
+        }
+        if (device < 0) pinned.swap(c.pinned);
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& d : dev) {
+        cudaSetDevice(d.first);
+        cudaFree(d.second);
+    }
+    cudaSetDevice(cur);
+    for (void* p : pinned) cudaFreeHost(p);
+    return SWAMP_OK;
+}
+
 int swamp_gpu_destroy(swamp_gpu* g) {
     if (!g) return SWAMP_E_ARG;
     cudaSetDevice(g->device);
@@ -1187,7 +1311,10 @@ int swamp_gpu_export_finest(swamp_gpu* g, double* h, double* qx, double* qy) {
     }
     cudaSetDevice(g->device);
     const size_t nf = static_cast<size_t>(1) << (2 * g->P.L);
-    if (!g->scratch) CK(cudaMalloc(&g->scratch, 3 * nf * sizeof(double)));  // kept for later exports
+    if (!g->scratch) {  // kept for later exports
+        CK(cached_malloc(g->device, &g->scratch, 3 * nf * sizeof(double)));
+        g->scratch_bytes = 3 * nf * sizeof(double);
+    }
     double* d = static_cast<double*>(g->scratch);
     hwfv1::k_export_finest<<<std::max(1, g->num_sms * 8), kThreads, 0, g->stream>>>(g->P, g->ctl, d, d + nf,
                                                                                      d + 2 * nf);

@@ -48,6 +48,7 @@ def lib():
         L.swamp_gpu_compare.argtypes = [P, P, dp, dp]
         L.swamp_gpu_rebalance.argtypes = [P, C.POINTER(C.c_int32)]
         L.swamp_gpu_destroy.argtypes = [P]
+        L.swamp_gpu_trim_cache.argtypes = [C.c_int]
         L.swamp_gpu_step.argtypes = [P, rp]
         L.swamp_gpu_advance.argtypes = [P, C.c_int64, rp]
         L.swamp_gpu_run.argtypes = [P, rp]
@@ -76,7 +77,7 @@ EXPORTED_SYMBOLS = (
     "swamp_gpu_counters", "swamp_gpu_build_info", "swamp_gpu_enqueue", "swamp_gpu_stream",
     "swamp_gpu_timeline", "swamp_gpu_create_partitioned", "swamp_gpu_debug",
     "swamp_gpu_rank_create", "swamp_gpu_rank_connect", "swamp_gpu_rank_ready", "swamp_gpu_compare",
-    "swamp_gpu_rebalance",
+    "swamp_gpu_rebalance", "swamp_gpu_trim_cache",
     "swamp_io_read_esri", "swamp_io_write_esri", "swamp_io_free_raster", "swamp_io_load_dem", "swamp_io_write_finest",
 )
 
@@ -241,6 +242,12 @@ class Engine:
         a = (C.c_int64 * 8)()
         self._check(lib().swamp_gpu_counters(self._h, a), "counters")
         return list(a)[:5]
+
+
+def trim_cache(device: int = -1) -> None:
+    """Release the device buffers destroyed engines left in the process-wide
+    block cache (swamp_gpu_trim_cache; -1: every device)."""
+    lib().swamp_gpu_trim_cache(device)
 
 
 def pinned_empty(shape, dtype=np.float64):
