@@ -341,7 +341,9 @@ def main():
         e2e = {"value": up / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d // K, "d2h_bytes_per_step": d2h // K,
                "seconds": e2e_s, "seconds_by_phase": e2e_parts,
                "note": "initialise from pinned host rasters (h, qx, qy, z) + K steps (StepReport read-back "
-                       "each) + finest export (h, qx, qy) into pinned buffers"}
+                       "each) + finest export (h, qx, qy) into pinned buffers; the engine's device buffers come from the "
+                       "process block cache (the timed-loop engine was destroyed just before; a first engine in a "
+                       "fresh process adds 3-50 ms of cudaMalloc)"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
