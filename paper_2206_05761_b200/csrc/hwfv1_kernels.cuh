@@ -162,6 +162,7 @@ struct Params {
     // pointers across GPUs; index 0 = self when G = 1).
     int G, part;
     int top_mode;         // levels < R after t = 0: 0 none (R = 0), 1 extra CTA of K2, 2 k_encode_top
+    int top_band;         // top_mode 1, one partition: K2's extra CTA also bands the top cells (K3 skips it)
     uint32_t tile_lo, tile_hi, tiles_per_part;  // this partition's subtrees [tile_lo, tile_hi), their count
     uint32_t pbound[kMaxParts + 1];             // partition g owns [pbound[g], pbound[g + 1]) (rebalanced)
     uint32_t pb_align;                          // largest of 16 / 4 / 1 dividing every boundary
@@ -1337,6 +1338,30 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode_pipe(Params P, Ctl* ctl)
     tl_end(ctl, hd.buf, 0);
 }
 
+// band (SPEC.md:195, D3) of cell (n, m) from the pre-band flags (flow | DEM);
+// `pre_at(level, morton)` reads a pre flag (global or shared memory)
+template <class PreAt>
+__device__ __forceinline__ uint8_t band_flag(int mode, int L, int n, uint32_t m, PreAt&& pre_at) {
+    uint8_t b = pre_at(n, m);
+    if (mode == 2) {
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const uint32_t nb = zo::neighbour_dev(n, m, static_cast<zo::Direction>(d));
+            if (nb != zo::kNone) b |= pre_at(n, nb);
+        }
+    } else if (mode == 1 && n + 1 < L) {
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t c = 4u * m + static_cast<uint32_t>(k);
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+                const uint32_t nb = zo::neighbour_dev(n + 1, c, static_cast<zo::Direction>(d));
+                if (nb != zo::kNone) b |= pre_at(n + 1, nb);
+            }
+        }
+    }
+    return b ? 1 : 0;
+}
+
 // Levels R-1 .. 0 of the re-encode after t = 0, one CTA (run as the extra
 // CTA of K2, concurrently with the subtree CTAs). Round trip 1 stages the
 // previous-tree and DEM flags of levels 0..R-1; round trip 2 loads the
@@ -1355,6 +1380,7 @@ __device__ void encode_top_staged(const Params& P, Ctl* ctl, int p, uint8_t* sm)
     double4* sv = reinterpret_cast<double4*>(sm);          // levels 0..R-1, compact lo(n, 0)
     uint8_t* sf = sm + 32u * lo(R, 0);                     // previous-tree flags at fbase[n]
     uint8_t* sd = sf + fb;                                 // DEM flags at fbase[n]
+    uint8_t* sq = sd + fb;                                 // (top_band) new pre flags at fbase[n]
     stage16(sf, sigp, fb);
     stage16(sd, P.dem, fb);
     cp_async_wait_all();
@@ -1395,7 +1421,9 @@ __device__ void encode_top_staged(const Params& P, Ctl* ctl, int p, uint8_t* sm)
                 ++tree;
             }
             if (sp || need) sv[lo(n, 0) + m] = v;
-            P.pre[slo(n) + m] = (flow || sd[slo(n) + m]) ? 1 : 0;
+            const uint8_t pr = (flow || sd[slo(n) + m]) ? 1 : 0;
+            P.pre[slo(n) + m] = pr;
+            if (P.top_band) sq[slo(n) + m] = pr;
         }
     }
     cp_async_wait_all();
@@ -1413,12 +1441,27 @@ __device__ void encode_top_staged(const Params& P, Ctl* ctl, int p, uint8_t* sm)
                 sv[lo(n, 0) + m] = e.par;
                 ++tree;
             }
-            P.pre[slo(n) + m] = (flow || sd[slo(n) + m]) ? 1 : 0;
+            const uint8_t pr = (flow || sd[slo(n) + m]) ? 1 : 0;
+            P.pre[slo(n) + m] = pr;
+            if (P.top_band) sq[slo(n) + m] = pr;
         }
         __syncthreads();
     }
     const unsigned tt = block_sum(tree, s_red);
     if (threadIdx.x == 0 && tt) atomicAdd(&ctl->cnt_tree, (unsigned long long)tt);
+    if (P.top_band) {
+        // band (D3) of every top cell, off K3's critical path: K3's top CTA
+        // stages these and goes straight to the closure (level-R pre flags of
+        // the neighbours come from K1, complete before K2 started)
+        uint8_t* sigc = P.sig[p ^ 1];
+        for (uint32_t q = threadIdx.x; q < lo(R, 0); q += kThreads) {
+            const int n = (31 - __clz(3u * q + 1u)) >> 1;  // level of compact index q
+            const uint32_t m = q - lo(n, 0);
+            sigc[slo(n) + m] = band_flag(P.band_mode, P.L, n, m, [&](int k, uint32_t mm) -> uint8_t {
+                return k < R ? sq[slo(k) + mm] : P.pre[slo(k) + mm];
+            });
+        }
+    }
 }
 
 
@@ -1437,30 +1480,6 @@ __device__ __forceinline__ void write_projection(double4* buf, const Params& P, 
 }
 
 // =========================================================================== K2
-// band (SPEC.md:195, D3) of cell (n, m) from the pre-band flags (flow | DEM);
-// `pre_at(level, morton)` reads a pre flag (global or shared memory)
-template <class PreAt>
-__device__ __forceinline__ uint8_t band_flag(int mode, int L, int n, uint32_t m, PreAt&& pre_at) {
-    uint8_t b = pre_at(n, m);
-    if (mode == 2) {
-#pragma unroll
-        for (int d = 0; d < 4; ++d) {
-            const uint32_t nb = zo::neighbour_dev(n, m, static_cast<zo::Direction>(d));
-            if (nb != zo::kNone) b |= pre_at(n, nb);
-        }
-    } else if (mode == 1 && n + 1 < L) {
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t c = 4u * m + static_cast<uint32_t>(k);
-#pragma unroll
-            for (int d = 0; d < 4; ++d) {
-                const uint32_t nb = zo::neighbour_dev(n + 1, c, static_cast<zo::Direction>(d));
-                if (nb != zo::kNone) b |= pre_at(n + 1, nb);
-            }
-        }
-    }
-    return b ? 1 : 0;
-}
-
 // band + ancestor closure of subtree j and its leaf
 // counts, on 32-bit words: the word at slo(k) + 4b holds the flag bytes of
 // the 2x2 block b of tile level k (Morton children 0..3 = SW, SE, NW, NE), so
@@ -1677,7 +1696,7 @@ __device__ __forceinline__ void k3_wait(const Ctl* ctl, unsigned long long epoch
 // top of the tree (block 0 of K3); top flags at the padded offsets slo(n)
 template <bool EXPORT>
 __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long long epoch, uint8_t* sm,
-                       const Probe& stamp) {
+                       const Probe& stamp, bool band_done = false) {
     __shared__ unsigned s_red[32];
     __shared__ unsigned s_off[6];
     const uint8_t* sigc = EXPORT ? P.sig[p] : P.sig[p ^ 1];
@@ -1699,10 +1718,9 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     const int rb = EXPORT ? p : p ^ 1;
 
     // ---- stage (one round trip)
-    if (EXPORT) {
-        stage16(ts, sigc, fb);
-    } else {
-        stage16(tp, P.pre, fb);
+    if (EXPORT || band_done) stage16(ts, sigc, fb);  // (band_done: K2's extra CTA banded the top cells)
+    if (!EXPORT) {
+        if (!band_done) stage16(tp, P.pre, fb);
         stage16(tv, sigp, fb);
         if (nt >= 16u) stage16(swet, P.wet[tbuf], nt);
         else if (threadIdx.x < nt) swet[threadIdx.x] = P.wet[tbuf][threadIdx.x];
@@ -1737,7 +1755,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     stamp(0);
 
     // ---- band (D3) of every top cell at once (band depends on pre flags only)
-    if (!EXPORT) {
+    if (!EXPORT && !band_done) {
         for (uint32_t q = threadIdx.x; q < lo(R, 0); q += kThreads) {
             const int n = (31 - __clz(3u * q + 1u)) >> 1;  // level of compact index q
             const uint32_t m = q - lo(n, 0);
@@ -2150,7 +2168,7 @@ __global__ void __launch_bounds__(kThreads, 7) k_band_traverse(Params P, Ctl* ct
         }
         __syncthreads();
         tl_start(ctl, hd.buf, 2);
-        k3_top<false>(P, ctl, hd.parity, hd.buf, ep, smf, stamp);
+        k3_top<false>(P, ctl, hd.parity, hd.buf, ep, smf, stamp, P.top_band != 0);
         return;
     }
     const int K = KT ? KT : P.K;
@@ -2181,7 +2199,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_traverse(Params P, Ctl* ctl, in
     const Probe stamp(ctl, EXPORT ? -1000 : 16);
     stamp(7, t_entry);
     if (blockIdx.x == 0) {
-        k3_top<EXPORT>(P, ctl, hd.parity, hd.buf, ep, smem3, stamp);
+        k3_top<EXPORT>(P, ctl, hd.parity, hd.buf, ep, smem3, stamp, !EXPORT && !force && P.top_band);
         return;
     }
     k3_tile<EXPORT, KT>(P, ctl, hd.parity, hd.buf, ep, P.tile_lo + blockIdx.x - 1, smem3, stamp);

@@ -573,7 +573,9 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         g->smem_k1p = 2 * (32 * ((size_t(1) << (2 * (K - 1))) + ((size_t(1) << (2 * (K - 1))) - 1) / 3) + 3 * sl + 16);
         P.top_mode = (R == 0) ? 0 : (R <= 6 ? 1 : 2);
         const size_t k2_tile = 2 * sl;
-        const size_t k2_top = P.top_mode == 1 ? 32 * ltop + 2 * fb : 0;
+        const char* etb = std::getenv("SWAMP_TOP_BAND");
+        P.top_band = (P.top_mode == 1 && G == 1 && !(etb && etb[0] == '0')) ? 1 : 0;
+        const size_t k2_top = P.top_mode == 1 ? 32 * ltop + 3 * fb : 0;
         g->smem_k2 = std::max(k2_tile, k2_top);
         const size_t ftop = (fb + nt + 15) & ~size_t(15);
         g->smem_k3 = std::max(2 * sl + 4 * ncell,                                                        // subtree CTA
