@@ -1874,32 +1874,37 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
                 s_off[2] = oa;
                 s_off[3] = ta + ob;
             }
-            // FV1 dry shortcut: subtree t is active if it or a face-adjacent
-            // subtree holds a wet cell, or it touches an inflow edge; clear
-            // the flags FV1 sets next
-            uint8_t act = swet[t];
-#pragma unroll
-            for (int d = 0; d < 4; ++d) {
-                const uint32_t nb = zo::neighbour_dev(R, t, static_cast<zo::Direction>(d));
-                if (nb == zo::kNone) act |= (P.bc[d] == 2) ? 1 : 0;
-                else act |= swet[nb];
-            }
-            const uint8_t st = (strips && act && ca == full) ? 1 : 0;
-            P.tact[t] = act | (st << 1);
-            P.wet[tbuf ^ 1][t] = 0;
-            nst += st;
         }
         oa += ca;
         ob += cb;
     }
     stamp(4);
-    if (EXPORT) {
-        k3_publish(ctl, epoch);
-        return;
-    }
+    // the subtree CTAs need only the offsets, depths and decode sources:
+    // publish now; FV1's inputs (activity, list slices, final top flags,
+    // top-cell projection) follow while the subtree CTAs decode and emit
+    k3_publish(ctl, epoch);
+    if (EXPORT) return;
     if (threadIdx.x == 0 && P.tile_hi >= nt) {
         s_off[2] = ta;
         s_off[3] = ta + tb;
+    }
+    for (uint32_t t = a; t < b; ++t) {
+        // FV1 dry shortcut: subtree t is active if it or a face-adjacent
+        // subtree holds a wet cell, or it touches an inflow edge; clear the
+        // flags FV1 sets next
+        unsigned ca, cb;
+        counts(t, ca, cb);
+        uint8_t act = swet[t];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const uint32_t nb = zo::neighbour_dev(R, t, static_cast<zo::Direction>(d));
+            if (nb == zo::kNone) act |= (P.bc[d] == 2) ? 1 : 0;
+            else act |= swet[nb];
+        }
+        const uint8_t st = (strips && act && ca == full) ? 1 : 0;
+        P.tact[t] = act | (st << 1);
+        P.wet[tbuf ^ 1][t] = 0;
+        nst += st;
     }
     // ---- the strip-path subtree list (Morton order)
     if (strips) {
@@ -1948,7 +1953,6 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
                 }
             }
     }
-    k3_publish(ctl, epoch);
     stamp(6);
 }
 
@@ -2203,6 +2207,43 @@ __global__ void __launch_bounds__(kThreads, 8) k_traverse(Params P, Ctl* ctl, in
         return;
     }
     k3_tile<EXPORT, KT>(P, ctl, hd.parity, hd.buf, ep, P.tile_lo + blockIdx.x - 1, smem3, stamp);
+}
+
+// K3 split over two launches (one partition): the top CTA alone, with a
+// dynamic shared-memory request that keeps subtree CTAs off its SM, then the
+// subtree CTAs (launched as soon as the top passed its wait for K2, so K2's
+// results are visible to them without a wait of their own); they meet on the
+// k3_ready flag as in k_traverse. Each subtree CTA waits for the top grid
+// before it exits, so FV1 (launched after the subtree grid) also sees the
+// top's post-publish results.
+template <int KT>
+__global__ void __launch_bounds__(kThreads, 1) k_traverse_top(Params P, Ctl* ctl) {
+    pdl_wait();
+    pdl_trigger();
+    const unsigned long long t_entry = gtimer();
+    const Head hd = cta_head(ctl, P, false);
+    if (!hd.active) return;
+    extern __shared__ __align__(16) uint8_t smem3t[];
+    tl_start(ctl, hd.buf, 2);
+    const Probe stamp(ctl, 16);
+    stamp(7, t_entry);
+    k3_top<false>(P, ctl, hd.parity, hd.buf, 2ull * static_cast<unsigned long long>(hd.step) + 2ull, smem3t, stamp,
+                  P.top_band != 0);
+}
+template <int KT>
+__global__ void __launch_bounds__(kThreads, 8) k_traverse_tiles(Params P, Ctl* ctl) {
+    pdl_trigger();
+    const unsigned long long t_entry = gtimer();
+    const Head hd = cta_head(ctl, P, false);
+    if (hd.active) {
+        extern __shared__ __align__(16) uint8_t smem3s[];
+        Probe stamp(ctl, 16);
+        if (blockIdx.x == 0) stamp.slot = -1;  // (slots 16.. belong to the top CTA)
+        stamp(7, t_entry);
+        k3_tile<false, KT>(P, ctl, hd.parity, hd.buf, 2ull * static_cast<unsigned long long>(hd.step) + 2ull,
+                           P.tile_lo + blockIdx.x, smem3s, stamp);
+    }
+    pdl_wait();  // the top grid has completed before this grid does
 }
 
 // =========================================================================== K5

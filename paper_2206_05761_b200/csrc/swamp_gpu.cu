@@ -122,6 +122,10 @@ struct swamp_gpu {
     int fv1_stage = 3;
     int num_sms = 0;
     size_t smem_k1 = 0, smem_k1s = 0, smem_k1p = 0, smem_k2 = 0, smem_k3 = 0;
+    // K3 split into a top launch (alone on its SM) + a subtree launch (one partition)
+    void (*k3top)(Params, Ctl*) = nullptr;
+    void (*k3tiles)(Params, Ctl*) = nullptr;
+    size_t smem_k3top = 0, smem_k3tiles = 0;
     int k1p_grid = 0;     // persistent K1 (K = 6): CTAs
     // tile kernels, specialised for K = 6 (every L >= 6) or generic
     void (*k1)(Params, Ctl*) = nullptr;
@@ -249,7 +253,12 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
         const int do_top = P.top_mode == 1 ? 1 : 0;
         launch_pdl(g->k2, P.n_tiles + do_top, g->smem_k2, s, P, g->ctl, 0, do_top);
         mark(2);
-        launch_pdl(g->k3, P.n_tiles + 1, g->smem_k3, s, P, g->ctl, 0, 0ull);
+        if (g->k3top) {
+            launch_pdl(g->k3top, 1, g->smem_k3top, s, P, g->ctl);
+            launch_pdl(g->k3tiles, P.n_tiles, g->smem_k3tiles, s, P, g->ctl);
+        } else {
+            launch_pdl(g->k3, P.n_tiles + 1, g->smem_k3, s, P, g->ctl, 0, 0ull);
+        }
         mark(3);
     }
     const size_t sm5 = P.strips ? sizeof(double4) * (kThreads / 32) * hwfv1::kStripSlots : 0;
@@ -578,8 +587,18 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         const size_t k2_top = P.top_mode == 1 ? 32 * ltop + 3 * fb : 0;
         g->smem_k2 = std::max(k2_tile, k2_top);
         const size_t ftop = (fb + nt + 15) & ~size_t(15);
-        g->smem_k3 = std::max(2 * sl + 4 * ncell,                                                        // subtree CTA
-                              2 * ftop + 2 * ((nt + 15) & ~size_t(15)) + 2 * fb + (nt <= 1024 ? 8 * nt : 0));  // top CTA
+        const size_t k3_top_smem = 2 * ftop + 2 * ((nt + 15) & ~size_t(15)) + 2 * fb + (nt <= 1024 ? 8 * nt : 0);
+        g->smem_k3 = std::max(2 * sl + 4 * ncell, k3_top_smem);  // subtree CTA, top CTA
+        // split K3 (SWAMP_K3_SPLIT=0: one launch with the top as block 0)
+        const char* eks = std::getenv("SWAMP_K3_SPLIT");
+        if (G == 1 && P.top_mode == 1 && !(eks && eks[0] == '0')) {
+            g->k3top = (Ki == 6) ? hwfv1::k_traverse_top<6> : hwfv1::k_traverse_top<0>;
+            g->k3tiles = (Ki == 6) ? hwfv1::k_traverse_tiles<6> : hwfv1::k_traverse_tiles<0>;
+            g->smem_k3tiles = 2 * sl + 4 * ncell;
+            int smem_optin = 0;
+            cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+            g->smem_k3top = std::max(k3_top_smem, static_cast<size_t>(smem_optin) - 8 * 1024);
+        }
         struct {
             const void* f;
             size_t bytes;
@@ -590,9 +609,11 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
                      {reinterpret_cast<const void*>(hwfv1::k_encode_pipe<6>), g->smem_k1p},
                      {reinterpret_cast<const void*>(g->k2), g->smem_k2},
                      {reinterpret_cast<const void*>(g->k3), g->smem_k3},
-                     {reinterpret_cast<const void*>(g->k3x), g->smem_k3}};
+                     {reinterpret_cast<const void*>(g->k3x), g->smem_k3},
+                     {reinterpret_cast<const void*>(g->k3top), g->smem_k3top},
+                     {reinterpret_cast<const void*>(g->k3tiles), g->smem_k3tiles}};
         for (auto& a : attrs)
-            if (a.bytes > 48 * 1024 &&
+            if (a.f && a.bytes > 48 * 1024 &&
                 cudaFuncSetAttribute(a.f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(a.bytes)) !=
                     cudaSuccess)
                 return fail(SWAMP_E_CUDA);
