@@ -899,67 +899,93 @@ __device__ __forceinline__ Enc encode_lanes_s(double4 v, int s, const double* th
 // by an extra CTA of K2 (encode_top_staged).
 template <int KT>
 __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl) {
-    pdl_wait();
-    pdl_trigger();
-    const unsigned long long t_entry = gtimer();
-    __shared__ __align__(8) unsigned long long mbar;
-    if (threadIdx.x == 0) mbar_init(&mbar, 1);
-    const Head hd = cta_head(ctl, P, false);  // (its barrier also publishes the mbarrier init)
-    if (!hd.active) return;
-    tl_start(ctl, hd.buf, 0);
-    const Probe stamp(ctl, 0);
-    stamp(7, t_entry);
+    // Before the wait for the previous FV1, everything that does not depend
+    // on it: the previous-tree flags of BOTH copies (FV1 writes neither, and
+    // which one is current is only known once FV1's last CTA has flipped the
+    // parity), the DEM flags and this thread's level-(L-2) flag in both
+    // copies. A CTA resident on an SM that FV1 left early has them in place
+    // when the wait returns; after it only the values remain to be fetched.
+    __shared__ __align__(8) unsigned long long mbar[2];  // [0] flags, [1] values
     extern __shared__ __align__(16) uint8_t sm1[];
     __shared__ unsigned s_red[32];
     __shared__ double s_thr[kMaxL][4];
-    const int p = hd.parity;
-    double4* buf = P.cells[p];
-    const uint8_t* sigp = P.sig[p];
     const int L = P.L, R = P.R;
     const int K = KT ? KT : P.K;
     const uint32_t j = P.tile_lo + blockIdx.x;
     const uint32_t nv = lo(K - 1, 0);  // cells on levels R..L-2
     double4* sv = reinterpret_cast<double4*>(sm1);
-    uint8_t* sf = sm1 + 32u * nv;      // previous-tree flags, slo layout
-    uint8_t* sd = sf + slo(K);         // DEM flags, slo layout
+    uint8_t* sf2 = sm1 + 32u * nv;     // previous-tree flags of copy 0 and copy 1, slo layout
+    uint8_t* sd = sf2 + 2 * slo(K);    // DEM flags, slo layout
     uint8_t* so = sd + slo(K);         // new pre flags of levels R..L-2, slo layout
-
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+    }
+    __syncthreads();
     // ---- the critical-path load first: this thread's level-(L-2) flag
     const int k2 = K - 2;              // tile level of L-2
     const uint32_t c2 = (k2 >= 0) ? (1u << (2 * k2)) : 0u;
     const bool has2 = threadIdx.x < c2;
     const uint32_t m2 = j * c2 + threadIdx.x;
-    bool sp2 = false;
-    if (has2) sp2 = sigp[slo(L - 2) + m2] != 0;
-    // ---- bulk copies (TMA, one thread): flags of levels R+2..L-1, values of
-    //      levels R+1..L-2; the two smallest flag levels by plain loads
+    uint8_t f2a = 0, f2b = 0;
+    if (has2) {
+        f2a = P.sig[0][slo(L - 2) + m2];
+        f2b = P.sig[1][slo(L - 2) + m2];
+    }
+    // ---- bulk copies (TMA, one thread): flags of levels R+2..L-1; the two
+    //      smallest flag levels by plain loads
     if (threadIdx.x == 0) {
         unsigned bytes = 0;
-        for (int k = 2; k < K; ++k) bytes += 2u << (2 * k);
-        for (int k = 1; k <= K - 2; ++k) bytes += 32u << (2 * k);
-        mbar_expect_tx(&mbar, bytes);
+        for (int k = 2; k < K; ++k) bytes += 3u << (2 * k);
+        mbar_expect_tx(&mbar[0], bytes);
         for (int k = 2; k < K; ++k) {
             const uint32_t cnt = 1u << (2 * k);
             const unsigned long long g = slo(R + k) + static_cast<unsigned long long>(j) * cnt;
-            bulk_g2s(sf + slo(k), sigp + g, cnt, &mbar);
-            bulk_g2s(sd + slo(k), P.dem + g, cnt, &mbar);
-        }
-        for (int k = 1; k <= K - 2; ++k) {
-            const uint32_t cnt = 1u << (2 * k);
-            bulk_g2s(sv + lo(k, 0), buf + cbase(R + k) + static_cast<unsigned long long>(j) * cnt, 32u * cnt, &mbar);
+            bulk_g2s(sf2 + slo(k), P.sig[0] + g, cnt, &mbar[0]);
+            bulk_g2s(sf2 + slo(K) + slo(k), P.sig[1] + g, cnt, &mbar[0]);
+            bulk_g2s(sd + slo(k), P.dem + g, cnt, &mbar[0]);
         }
     }
-    uint32_t fsmall = 0, dsmall = 0;
+    uint32_t fsa = 0, fsb = 0, dsmall = 0;
     if (threadIdx.x == 32 && K > 1) {
-        fsmall = *reinterpret_cast<const uint32_t*>(sigp + slo(R + 1) + 4ull * j);
+        fsa = *reinterpret_cast<const uint32_t*>(P.sig[0] + slo(R + 1) + 4ull * j);
+        fsb = *reinterpret_cast<const uint32_t*>(P.sig[1] + slo(R + 1) + 4ull * j);
         dsmall = *reinterpret_cast<const uint32_t*>(P.dem + slo(R + 1) + 4ull * j);
     }
-    uint8_t f0 = 0, d0 = 0;
+    uint8_t f0a = 0, f0b = 0, d0 = 0;
     if (threadIdx.x == 64) {
-        f0 = sigp[slo(R) + j];
+        f0a = P.sig[0][slo(R) + j];
+        f0b = P.sig[1][slo(R) + j];
         d0 = P.dem[slo(R) + j];
     }
     stage_thresholds(P, s_thr);
+
+    pdl_wait();
+    pdl_trigger();
+    const unsigned long long t_entry = gtimer();
+    const Head hd = cta_head(ctl, P, false);
+    if (!hd.active) {
+        mbar_wait(&mbar[0], 0);  // no bulk copy may outlive the CTA
+        return;
+    }
+    tl_start(ctl, hd.buf, 0);
+    const Probe stamp(ctl, 0);
+    stamp(7, t_entry);
+    const int p = hd.parity;
+    double4* buf = P.cells[p];
+    uint8_t* sf = sf2 + (p ? slo(K) : 0u);  // previous-tree flags of the current copy
+    const bool sp2 = has2 && (p ? f2b : f2a) != 0;
+    // ---- values of levels R+1..L-2 (TMA) and this thread's four level-(L-1)
+    //      children (registers), written by the FV1 just waited for
+    if (threadIdx.x == 0) {
+        unsigned bytes = 0;
+        for (int k = 1; k <= K - 2; ++k) bytes += 32u << (2 * k);
+        mbar_expect_tx(&mbar[1], bytes);
+        for (int k = 1; k <= K - 2; ++k) {
+            const uint32_t cnt = 1u << (2 * k);
+            bulk_g2s(sv + lo(k, 0), buf + cbase(R + k) + static_cast<unsigned long long>(j) * cnt, 32u * cnt, &mbar[1]);
+        }
+    }
     double4 ch[4];
     if (sp2) {
         const double4* cp = buf + cbase(L - 1) + (static_cast<unsigned long long>(m2) << 2);
@@ -967,14 +993,15 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
     }
     stamp(0);
     if (threadIdx.x == 32 && K > 1) {
-        *reinterpret_cast<uint32_t*>(sf + slo(1)) = fsmall;
+        *reinterpret_cast<uint32_t*>(sf + slo(1)) = p ? fsb : fsa;
         *reinterpret_cast<uint32_t*>(sd + slo(1)) = dsmall;
     }
     if (threadIdx.x == 64) {
-        sf[0] = f0;
+        sf[0] = p ? f0b : f0a;
         sd[0] = d0;
     }
-    mbar_wait(&mbar, 0);
+    mbar_wait(&mbar[0], 0);
+    mbar_wait(&mbar[1], 0);
     __syncthreads();
     stamp(1);
 

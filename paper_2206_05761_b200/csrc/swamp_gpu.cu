@@ -577,7 +577,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             g->k3x = hwfv1::k_traverse<true, 0>;
         }
         g->smem_k1 = ncell * (sizeof(double4) + 1);                  // k_encode<true> / k_encode_top
-        g->smem_k1s = 32 * (((size_t(1) << (2 * (K - 1))) - 1) / 3) + 3 * sl;
+        g->smem_k1s = 32 * (((size_t(1) << (2 * (K - 1))) - 1) / 3) + 4 * sl;  // values, 2 flag copies, DEM, new pre
         // persistent K1: 2 stages of (children + values + 3 flag slices + small words)
         g->smem_k1p = 2 * (32 * ((size_t(1) << (2 * (K - 1))) + ((size_t(1) << (2 * (K - 1))) - 1) / 3) + 3 * sl + 16);
         P.top_mode = (R == 0) ? 0 : (R <= 6 ? 1 : 2);
