@@ -975,13 +975,17 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
     double4* buf = P.cells[p];
     uint8_t* sf = sf2 + (p ? slo(K) : 0u);  // previous-tree flags of the current copy
     const bool sp2 = has2 && (p ? f2b : f2a) != 0;
-    // ---- values of levels R+1..L-2 (TMA) and this thread's four level-(L-1)
-    //      children (registers), written by the FV1 just waited for
+    // ---- values of levels R+1..L-2 (TMA; K = 6: R+1..L-3) and this thread's
+    //      four level-(L-1) children (registers), written by the FV1 just
+    //      waited for. K = 6: a level-(L-2) cell off the previous tree is
+    //      loaded into ch[0] only when its parent is re-encoded (it is then
+    //      a previous-tree leaf whose value the parent needs)
+    const int kv = (KT == 6) ? K - 3 : K - 2;  // highest tile level staged by TMA
     if (threadIdx.x == 0) {
         unsigned bytes = 0;
-        for (int k = 1; k <= K - 2; ++k) bytes += 32u << (2 * k);
+        for (int k = 1; k <= kv; ++k) bytes += 32u << (2 * k);
         mbar_expect_tx(&mbar[1], bytes);
-        for (int k = 1; k <= K - 2; ++k) {
+        for (int k = 1; k <= kv; ++k) {
             const uint32_t cnt = 1u << (2 * k);
             bulk_g2s(sv + lo(k, 0), buf + cbase(R + k) + static_cast<unsigned long long>(j) * cnt, 32u * cnt, &mbar[1]);
         }
@@ -990,6 +994,9 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
     if (sp2) {
         const double4* cp = buf + cbase(L - 1) + (static_cast<unsigned long long>(m2) << 2);
         ch[0] = ld4_nc(cp); ch[1] = ld4_nc(cp + 1); ch[2] = ld4_nc(cp + 2); ch[3] = ld4_nc(cp + 3);
+    } else if (KT == 6 && has2) {
+        mbar_wait(&mbar[0], 0);  // (the flags were staged before the wait for FV1)
+        if (sf[slo(k2 - 1) + (threadIdx.x >> 2)]) ch[0] = ld4_nc(buf + cbase(L - 2) + m2);
     }
     stamp(0);
     if (threadIdx.x == 32 && K > 1) {
@@ -1044,7 +1051,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
                 st4(buf + cbase(L - 2) + m2, v);
                 ++tree;
             } else {
-                v = sv[lo(4, 0) + tid];
+                v = ch[0];  // (only used when the parent is re-encoded: then loaded above)
             }
             so[slo(4) + tid] = (flow || sd[slo(4) + tid]) ? 1 : 0;
         }
