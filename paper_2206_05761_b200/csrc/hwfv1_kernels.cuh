@@ -1504,13 +1504,21 @@ __device__ void encode_top_staged(const Params& P, Ctl* ctl, int p, uint8_t* sm)
 // compact_leaves. In physical units a zero-detail decode is
 // a copy of the parent's (h, qx, qy) to its children, so a cell
 // below a chain of newly significant cells takes the value of the chain's top.
-__device__ __forceinline__ void write_projection(double4* buf, const Params& P, int n, uint32_t m, uint32_t src) {
+// The bed elevation z of every cell is static — both copies hold the full
+// hierarchy from initialise, FV1 writes a leaf's own z back and re-encoding
+// averages unchanged children — so a projection writes h, qx, qy only and
+// never reads the destination.
+__device__ __forceinline__ double4 projection_source(const double4* buf, const Params& P, uint32_t src) {
     const int ns = zo::level_of(src);
     const int p = static_cast<int>(buf == P.cells[1]);
-    const double4 v = ld4_cg(cell_ptr(P, p, ns, src - zo::level_offset(ns)));
-    double4* dst = buf + cbase(n) + m;
-    const double4 old = ld4_cg(dst);
-    st4(dst, make_double4(v.x, v.y, v.z, old.w));
+    return ld4_cg(cell_ptr(P, p, ns, src - zo::level_offset(ns)));
+}
+__device__ __forceinline__ void store_hqq(double4* dst, const double4& v) {
+    asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(dst), "d"(v.x), "d"(v.y) : "memory");
+    asm volatile("st.global.f64 [%0], %1;" ::"l"(reinterpret_cast<double*>(dst) + 2), "d"(v.z) : "memory");
+}
+__device__ __forceinline__ void write_projection(double4* buf, const Params& P, int n, uint32_t m, uint32_t src) {
+    store_hqq(buf + cbase(n) + m, projection_source(buf, P, src));
 }
 
 // =========================================================================== K2
@@ -2126,8 +2134,11 @@ __device__ void k3_tile(const Params& P, Ctl* ctl, int p, int tbuf, unsigned lon
                     const uint32_t lc = lo(n + 1, R) + 4u * pi;
                     src[lc] = cs; src[lc + 1] = cs; src[lc + 2] = cs; src[lc + 3] = cs;
                 }
-                if (cs != kNoSrc)
-                    for (uint32_t q = 0; q < 4; ++q) write_projection(buf, P, n + 1, 4u * pm + q, cs);
+                if (cs != kNoSrc) {
+                    const double4 v = projection_source(buf, P, cs);
+                    double4* dst = buf + cbase(n + 1) + 4ull * pm;
+                    for (uint32_t q = 0; q < 4; ++q) store_hqq(dst + q, v);
+                }
             }
             __syncthreads();
         }
