@@ -137,6 +137,10 @@ struct Params {
     uint32_t* tile_off;
     uint32_t* tile_lvl;   // traversal depth of each subtree (R = reached) | kEmit
     uint32_t* tile_src;   // decode source of a reached subtree root, or kNoSrc
+    // hot-path K3: the top's results for subtree t as four self-tagged words
+    // (epoch << 32 | A offset, B offset, depth, decode source) on the
+    // subtree's own 128-B line, so each subtree CTA polls only its own line
+    unsigned long long* k3_rec;
     // FV1 dry shortcut (one partition): wet[b][t] = some leaf of subtree t
     // ended the step with h >= h_dry (b = step parity); tact[t] bit 0 =
     // subtree t or a face-adjacent one is wet, or t touches an inflow edge
@@ -218,6 +222,14 @@ __device__ __forceinline__ uint8_t ldcg_u8(const uint8_t* p) {
     unsigned short v;
     asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(v) : "l"(p));
     return static_cast<uint8_t>(v);
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
     unsigned long long v;
@@ -1908,6 +1920,12 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
             P.tile_off[t] = oa;
             P.tile_off[nt + t] = ta + ob;
             P.tile_src[t] = src;
+            const unsigned long long tag = (epoch & 0xFFFFFFFFull) << 32;
+            unsigned long long* rec = P.k3_rec + 16ull * t;
+            st_relaxed_u64(rec + 0, tag | oa);
+            st_relaxed_u64(rec + 1, tag | (ta + ob));
+            st_relaxed_u64(rec + 2, tag | (static_cast<uint32_t>(n) | (cbf[t] ? kEmit : 0u)));
+            st_relaxed_u64(rec + 3, tag | src);
             if (t == P.tile_lo) {
                 s_off[0] = oa;
                 s_off[1] = ta + ob;
@@ -2090,13 +2108,38 @@ __device__ void k3_tile(const Params& P, Ctl* ctl, int p, int tbuf, unsigned lon
     stamp(1);
 
     // ---- the top's results for this subtree
-    k3_wait(ctl, epoch);
-    stamp(2);
-    if (threadIdx.x == 0) {
-        s_top[0] = ldcg_u32(P.tile_off + (EXPORT ? 2 * nt + j : j));
-        s_top[1] = EXPORT ? 0u : ldcg_u32(P.tile_off + nt + j);
-        s_top[2] = ldcg_u32(P.tile_lvl + j);
-        s_top[3] = EXPORT ? kNoSrc : ldcg_u32(P.tile_src + j);
+    if (EXPORT) {
+        k3_wait(ctl, epoch);
+        stamp(2);
+        if (threadIdx.x == 0) {
+            s_top[0] = ldcg_u32(P.tile_off + 2 * nt + j);
+            s_top[1] = 0u;
+            s_top[2] = ldcg_u32(P.tile_lvl + j);
+            s_top[3] = kNoSrc;
+        }
+    } else {
+        // poll this subtree's own record until all four words carry this
+        // step's tag (each word is written atomically with its tag)
+        if (threadIdx.x == 0) {
+            const unsigned tag = static_cast<unsigned>(epoch);
+            const unsigned long long* rec = P.k3_rec + 16ull * j;
+            unsigned long long v0, v1, v2, v3;
+            for (;;) {
+                v0 = ld_relaxed_u64(rec + 0);
+                v1 = ld_relaxed_u64(rec + 1);
+                v2 = ld_relaxed_u64(rec + 2);
+                v3 = ld_relaxed_u64(rec + 3);
+                if (static_cast<unsigned>(v0 >> 32) == tag && static_cast<unsigned>(v1 >> 32) == tag &&
+                    static_cast<unsigned>(v2 >> 32) == tag && static_cast<unsigned>(v3 >> 32) == tag)
+                    break;
+                __nanosleep(32);
+            }
+            s_top[0] = static_cast<uint32_t>(v0);
+            s_top[1] = static_cast<uint32_t>(v1);
+            s_top[2] = static_cast<uint32_t>(v2);
+            s_top[3] = static_cast<uint32_t>(v3);
+        }
+        stamp(2);
     }
     __syncthreads();
     stamp(3);
