@@ -45,6 +45,33 @@ def test_step_parity(name, kw):
             compare_states(g, o, f"{name} step {k}")
 
 
+def test_block_cache_reuse_is_clean():
+    """Destroyed engines hand their device buffers (with stale contents) to the
+    next engine of the same shape (swamp_gpu_trim_cache): a second engine on a
+    different case, and a re-created first one, still match the oracle
+    bitwise — no state survives in reused memory."""
+    import gc
+
+    def run(name, steps=12):
+        cfg, h, qx, qy, z = cases.CASES[name](L=8)
+        g = gpu.initialise(cfg, h, qx, qy, z)
+        o = O.Oracle(cfg, h, qx, qy, z)
+        for _ in range(steps):
+            g.step_adaptive()
+            o.step()
+        compare_states(g, o, f"{name} after reuse")
+        g.export_finest()
+        del g
+        gc.collect()
+
+    gpu.trim_cache()
+    run("circular_dambreak")
+    run("hump_dambreak")      # reuses the first engine's blocks
+    run("circular_dambreak")  # and back
+    gpu.trim_cache()
+    run("monai_runup")        # fresh blocks after a trim
+
+
 def test_graph_advance_matches_single_steps():
     cfg, h, qx, qy, z = cases.circular_dambreak(L=8)
     a = gpu.initialise(cfg, h, qx, qy, z)
