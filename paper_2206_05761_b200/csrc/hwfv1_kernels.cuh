@@ -1674,9 +1674,13 @@ __device__ void k2_tile(const Params& P, Ctl* ctl, const Head& hd, uint32_t j, u
     // ---- ancestor closure bottom-up: a cell is significant if its band flag
     //      or any child is; byte-per-cell words of level k from level k + 1
     auto nz = [](uint32_t w) -> uint32_t { return w ? 1u : 0u; };
+    // levels with more than 32 words: every thread, CTA barrier per level;
+    // the rest (<= 32 words, k <= 3) by warp 0 with warp barriers
 #pragma unroll
     for (int k = (KT ? KT : kMaxL) - 2; k >= 0; --k) {
         if (!KT && k > K - 2) continue;
+        const bool wide = k >= 4;  // 4^(k-1) > 32 words
+        if (!wide && threadIdx.x >= 32) continue;
         if (k == 0) {
             if (threadIdx.x == 0) sf[0] = (sf[0] | nz(*reinterpret_cast<const uint32_t*>(sf + slo(1)))) ? 1 : 0;
         } else {
@@ -1687,8 +1691,10 @@ __device__ void k2_tile(const Params& P, Ctl* ctl, const Head& hd, uint32_t j, u
                 *w |= nz(c.x) | (nz(c.y) << 8) | (nz(c.z) << 16) | (nz(c.w) << 24);
             }
         }
-        __syncthreads();
+        if (wide) __syncthreads();
+        else __syncwarp();
     }
+    __syncthreads();
     // ---- final flags (word stores), leaf counts from popcounts
     unsigned S = 0, S1 = 0;
     if (threadIdx.x == 0) {
@@ -1709,8 +1715,9 @@ __device__ void k2_tile(const Params& P, Ctl* ctl, const Head& hd, uint32_t j, u
             if (k == K - 1) S1 += c;
         }
     }
-    const unsigned St = block_sum(S, s_red);
-    const unsigned S1t = block_sum(S1, s_red);
+    // one block sum of both counts (S <= 4^K / 3 < 2^16)
+    const unsigned SS = block_sum(S | (S1 << 16), s_red);
+    const unsigned St = SS & 0xFFFFu, S1t = SS >> 16;
     if (threadIdx.x == 0) {
         P.tile_cnt[j] = 4u * S1t;
         P.tile_cnt[P.n_tiles + j] = 1u + 3u * St - 4u * S1t;
