@@ -275,6 +275,7 @@ def main():
     updates_all = float(u1 - u0)
 
     K = args.steps
+    launches = eng.launches_per_step()  # kernel nodes of the one-step graph (5 at one partition)
     n_mean = updates / K
     tree_per_step = (c1[1] - c0[1]) / K
     new_per_step = (c1[2] - c0[2]) / K
@@ -376,7 +377,7 @@ def main():
                      "alg_bytes_per_unit": FV1_BYTES_PER_LEAF if dominant == "ms_fv1" else None},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 4 * K,
+        "gpu_launches": launches * K,
         "timing": "CUDA events on the engine stream around K back-to-back steps (8-step graph replays); "
                   "leaf updates from the device counter; stage times from the kernels' %globaltimer stamps in "
                   "the flushed per-step loop",

@@ -213,7 +213,8 @@ int swamp_gpu_last_error(const swamp_gpu* g, int32_t* code, uint32_t* z, int32_t
 /* Counters for roofline bookkeeping: [0] leaves N of the last step, [1]
  * significant tree cells re-encoded (cumulative), [2] newly significant cells
  * decoded (cumulative), [3] 4^L, [4] leaf updates of all steps (sum of N,
- * cumulative), [5..7] reserved (0). */
+ * cumulative), [5] kernels launched per adaptive step (kernel nodes of the
+ * one-step graph, summed over partitions), [6..7] reserved (0). */
 int swamp_gpu_counters(swamp_gpu* g, int64_t* out8);
 
 /* Device timeline of the last step, microseconds from K1's first CTA: for

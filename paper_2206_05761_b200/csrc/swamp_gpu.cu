@@ -114,6 +114,7 @@ struct swamp_gpu {
     std::vector<std::pair<void*, size_t>> allocs;  // device blocks (returned to the block cache)
     cudaGraphExec_t graph1 = nullptr, graphS = nullptr, graphT = nullptr;
     int fv1_grid = 0;
+    int64_t launches_per_step = 0;  // kernel nodes of the one-step graph
     int fv1_minb = 2;  // occupancy variant of k_fv1 (SWAMP_FV1_MINB=3|4 for more CTAs/SM, with spills)
     // SWAMP_FV1_STAGE=1: neighbours staged in shared memory, 3 CTAs/SM (slower);
     // 2: own cell and subtree activity loaded an iteration ahead (FV1 69 ->
@@ -287,6 +288,20 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
 // record nodes between the kernels (per-stage device times, StepReport)
 // `which`: 0 = graph1, 1 = graphS, 2 = graphT (the profiling graph is built
 // on first use)
+// kernel nodes of a captured one-step graph (swamp_gpu_counters [5])
+int64_t kernel_nodes(cudaGraph_t graph) {
+    size_t n = 0;
+    if (cudaGraphGetNodes(graph, nullptr, &n) != cudaSuccess || n == 0) return 0;
+    std::vector<cudaGraphNode_t> nodes(n);
+    if (cudaGraphGetNodes(graph, nodes.data(), &n) != cudaSuccess) return 0;
+    int64_t k = 0;
+    for (cudaGraphNode_t v : nodes) {
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(v, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+    }
+    return k;
+}
+
 int build_graph(swamp_gpu* g, int which) {
     {
         const int steps = which == 1 ? kGraphSteps : 1;
@@ -294,6 +309,7 @@ int build_graph(swamp_gpu* g, int which) {
         CK(cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
         for (int k = 0; k < steps; ++k) launch_step_kernels(g, which == 2);
         CK(cudaStreamEndCapture(g->stream, &graph));
+        if (which == 0) g->launches_per_step = kernel_nodes(graph);
         cudaGraphExec_t exec;
         CK(cudaGraphInstantiate(&exec, graph, 0));
         cudaGraphDestroy(graph);
@@ -855,6 +871,7 @@ int capture_step_graphs(swamp_gpu* g, cudaStream_t s, F&& enqueue_step) {
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         for (int k = 0; k < steps; ++k) enqueue_step();
         CK(cudaStreamEndCapture(s, &graph));
+        if (which == 0) g->launches_per_step = kernel_nodes(graph);
         cudaGraphExec_t exec;
         CK(cudaGraphInstantiate(&exec, graph, 0));
         cudaGraphDestroy(graph);
@@ -1419,10 +1436,12 @@ int swamp_gpu_counters(swamp_gpu* g, int64_t* out8) {
             const int st = swamp_gpu_counters(q, c);
             if (st) return st;
             for (int k = 1; k < 3; ++k) acc[k] += c[k];
+            acc[5] += c[5];
             acc[0] = c[0];
             acc[3] = c[3];
             acc[4] = c[4];  // global leaf counts: every partition holds the same sum
         }
+        if (g->launches_per_step) acc[5] = g->launches_per_step;  // one graph for the whole group
         std::memcpy(out8, acc, sizeof(acc));
         return SWAMP_OK;
     }
@@ -1432,7 +1451,8 @@ int swamp_gpu_counters(swamp_gpu* g, int64_t* out8) {
     out8[2] = static_cast<int64_t>(g->ctl_host->cnt_new);
     out8[3] = int64_t(1) << (2 * g->P.L);
     out8[4] = static_cast<int64_t>(g->ctl_host->cnt_updates);
-    out8[5] = out8[6] = out8[7] = 0;
+    out8[5] = g->launches_per_step;  // this engine's kernels per step (one-step graph)
+    out8[6] = out8[7] = 0;
     return st;
 }
 

@@ -243,6 +243,12 @@ class Engine:
         self._check(lib().swamp_gpu_counters(self._h, a), "counters")
         return list(a)[:5]
 
+    def launches_per_step(self) -> int:
+        """Kernels one adaptive step launches (kernel nodes of the one-step graph)."""
+        a = (C.c_int64 * 8)()
+        self._check(lib().swamp_gpu_counters(self._h, a), "counters")
+        return int(a[5])
+
 
 def trim_cache(device: int = -1) -> None:
     """Release the device buffers destroyed engines left in the process-wide
