@@ -1,0 +1,39 @@
+"""Large levels (L = 12, 13: 16.8 M / 67 M finest cells), where the oracle is
+too slow to step: size-independent properties instead — the one-partition
+engine (split K3, per-subtree records, K = 6 kernels with 4^R = 4096 /
+16384 subtrees) and a two-partition engine (the group path) give the same
+bits, and every finite-grid value stays finite."""
+import numpy as np
+import pytest
+
+from paper_2206_05761_b200 import cases
+
+gpu = pytest.importorskip("paper_2206_05761_b200.gpu")
+pytestmark = pytest.mark.gpu
+
+
+def test_level12_single_equals_two_partitions():
+    cfg, h, qx, qy, z = cases.river_flood(L=12)
+    a = gpu.initialise(cfg, h, qx, qy, z)
+    b = gpu.initialise_partitioned(cfg, h, qx, qy, z, [0, 0])
+    a.advance(10)
+    b.advance(10)
+    ia, ib = a.info(), b.info()
+    assert (ia["t"], ia["dt"], ia["step"]) == (ib["t"], ib["dt"], ib["step"])
+    for fa, fb in zip(a.export_finest(), b.export_finest()):
+        assert np.isfinite(fa).all()
+        np.testing.assert_array_equal(fa.view(np.uint64), fb.view(np.uint64))
+    del a, b
+    gpu.trim_cache()
+
+
+def test_level13_steps_stay_finite():
+    cfg, h, qx, qy, z = cases.river_flood(L=13)
+    e = gpu.initialise(cfg, h, qx, qy, z)
+    e.advance(5)
+    info = e.info()
+    assert info["step"] == 5 and info["dt"] > 0.0 and info["n_leaves"] > 4 ** 11
+    for f in e.export_finest():
+        assert np.isfinite(f).all()
+    del e
+    gpu.trim_cache()
