@@ -62,6 +62,7 @@ struct Ctl {
     unsigned long long cnt_updates;              // leaf updates of all steps so far (sum of N)
     alignas(128) unsigned long long k3_ready;    // K3's top CTA published its results (epoch)
     alignas(128) unsigned long long k2_done;     // fused K2+K3: subtree CTAs done with K2 (reset by the top CTA)
+    alignas(128) unsigned int fv1_tail;          // FV1 (STAGE 5): dynamic tail chunks taken this step
     uint32_t n_stile;                            // subtrees on FV1's strip path this step
     alignas(128) unsigned long long smax_bits[4];
     int err_code;
@@ -158,6 +159,7 @@ struct Params {
     int strips;           // strip path enabled (SWAMP_FV1_STRIPS=1; measured slower on B200)
     int quad;             // sibling-quad path (SWAMP_FV1_QUAD=1; measured slower on B200)
     int fv1_pf;           // FV1 prefetch of the next iteration's own cells: 0 off, 1 L2, 2 L1
+    uint32_t fv1_tail16;  // FV1 STAGE 5: sixteenths of the grid-stride windows taken dynamically at the end
     // Morton-subtree partitions: this partition owns level-R
     // subtrees [tile_lo, tile_hi); cells on levels >= R belong to their
     // subtree's partition, cells above R are replicated except that a leaf's
@@ -2416,6 +2418,7 @@ __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ct
         finalize_dt(P, ctl, __longlong_as_double(static_cast<long long>(m)), advance);
         ctl->rate_bits[slot] = 0ull;
         ctl->done_k5 = 0;
+        ctl->fv1_tail = 0u;
         ctl->tl[slot][3][2] = gtimer();
         if (advance)  // next step's buffer
             for (int k = 0; k < 4; ++k) ctl->tl[slot ^ 1][k][0] = ctl->tl[slot ^ 1][k][2] = 0ull;
@@ -2811,6 +2814,32 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                       s_bnd + (threadIdx.x >> 5) * kStripSlots, mx, tree);
     }
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
+    // STAGE 5 (= 3 + tail balancing): the last fv1_tail16 / 16 of the windows
+    // are taken one warp-iteration (32 leaves) at a time from a per-step
+    // counter by whichever warps finish their static windows first; the
+    // bases of the next two iterations are kept in b1, b2 (the finalizing
+    // CTA resets the counter)
+    constexpr bool TAIL = STAGE == 5;
+    const uint32_t nwin = N / stride, ntail = (nwin * P.fv1_tail16 + 8u) >> 4;
+    const uint32_t nstat = TAIL ? ((nwin > ntail) ? (nwin - ntail) * stride : 0u) : N;
+    auto grab = [&]() -> uint32_t {
+        uint32_t c = 0;
+        if (lane == 0) c = atomicAdd(&ctl->fv1_tail, 1u);
+        c = __shfl_sync(kFull, c, 0);
+        const uint32_t b = nstat + 32u * c;
+        return b < N ? b : N;
+    };
+    auto next_of = [&](uint32_t b) -> uint32_t {
+        if (b >= N) return N;
+        if (b + stride < nstat) return b + stride;
+        return grab();
+    };
+    uint32_t b1 = 0, b2 = 0;
+    if (TAIL) {
+        if (wbase >= nstat) wbase = grab();
+        b1 = next_of(wbase);
+        b2 = next_of(b1);
+    }
     // STAGE 2: the next iteration's own cell and subtree activity are loaded
     // into registers one iteration ahead (instead of an L2 prefetch)
     const int pf = (STAGE >= 2) ? 1 : P.fv1_pf;
@@ -2818,7 +2847,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     // prefetched (no registers held) while this one computes: the leaf
     // cells were written a step ago and come from DRAM
     uint32_t z_next = (!UNIFORM && wbase + lane < N) ? leaf_at(wbase + lane) : 0u;
-    uint32_t z_nn = (!UNIFORM && pf && wbase + stride + lane < N) ? leaf_at(wbase + stride + lane) : 0u;
+    const uint32_t nb1_0 = TAIL ? b1 : wbase + stride;
+    uint32_t z_nn = (!UNIFORM && pf && nb1_0 + lane < N) ? leaf_at(nb1_0 + lane) : 0u;
     double4 o4_pre = make_double4(0.0, 0.0, 0.0, 0.0);
     uint8_t ta_pre = 1;
     uint8_t fl_pre[4] = {1, 1, 1, 1};  // STAGE 3: the neighbours' parent-level flags too
@@ -2827,7 +2857,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
         const uint32_t m1 = zz - zo::level_offset(n1);
         o4_pre = ld4_nc(cur + cbase(n1) + m1);
         ta_pre = (!PART && n1 >= P.R) ? P.tact[m1 >> (2 * (n1 - P.R))] : 1;
-        if (STAGE == 3 && n1 > 0) {
+        if ((STAGE == 3 || STAGE == 5) && n1 > 0) {
 #pragma unroll
             for (int d = 0; d < 4; ++d) {
                 const uint32_t q = zo::neighbour_dev(n1, m1, static_cast<zo::Direction>(d));
@@ -2836,8 +2866,18 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
         }
     };
     if (STAGE >= 2 && !UNIFORM && wbase + lane < N) pre_load(z_next);
-    for (; wbase < N; wbase += stride) {
+    auto advance_base = [&]() {
+        if (TAIL) {
+            wbase = b1;
+            b1 = b2;
+            b2 = next_of(b1);
+        } else {
+            wbase += stride;
+        }
+    };
+    for (; wbase < N; advance_base()) {
         const uint32_t i = wbase + lane;
+        const uint32_t nb1 = TAIL ? b1 : wbase + stride, nb2 = TAIL ? b2 : wbase + 2 * stride;  // next two bases
         bool valid = i < N;
         int n;
         uint32_t m;
@@ -2847,16 +2887,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
         if (UNIFORM) {
             n = P.L;
             m = valid ? i : 0u;
-            if (pf && i + stride < N) {
-                const double4* q = cur + cbase(n) + i + stride;
+            if (pf && nb1 + lane < N) {
+                const double4* q = cur + cbase(n) + nb1 + lane;
                 if (pf == 2) prefetch_l1(q); else prefetch_l2(q);
             }
         } else {
             const uint32_t z = valid ? z_next : zo::level_offset(P.L);  // leaf ids prefetched one iteration ahead
             if (pf) {
                 z_next = z_nn;
-                if (i + 2 * stride < N) z_nn = leaf_at(i + 2 * stride);
-                if (i + stride < N) {
+                if (nb2 + lane < N) z_nn = leaf_at(nb2 + lane);
+                if (nb1 + lane < N) {
                     if (STAGE >= 2) {
                         pre_load(z_next);
                     } else {
@@ -2865,8 +2905,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                         if (pf == 2) prefetch_l1(q); else prefetch_l2(q);
                     }
                 }
-            } else if (i + stride < N) {
-                z_next = leaf_at(i + stride);
+            } else if (nb1 + lane < N) {
+                z_next = leaf_at(nb1 + lane);
             }
             n = zo::level_of(z);
             m = z - zo::level_offset(n);
@@ -2964,7 +3004,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                 } else {
 #pragma unroll
                     for (int d = 0; d < 4; ++d)
-                        f[d] = (STAGE == 3) ? fl_k[d] : ((nm[d] != zo::kNone) ? sigc[slo(n - 1) + (nm[d] >> 2)] : 1);
+                        f[d] = (STAGE >= 3) ? fl_k[d] : ((nm[d] != zo::kNone) ? sigc[slo(n - 1) + (nm[d] >> 2)] : 1);
 #pragma unroll
                     for (int d = 0; d < 4; ++d)
                         src[d] = f[d] ? cur + cbase(n) + nm[d] : covering_local(P, cur, sigc, n - 1, nm[d] >> 2);

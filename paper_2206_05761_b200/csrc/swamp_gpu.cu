@@ -118,9 +118,10 @@ struct swamp_gpu {
     int fv1_minb = 2;  // occupancy variant of k_fv1 (SWAMP_FV1_MINB=3|4 for more CTAs/SM, with spills)
     // SWAMP_FV1_STAGE=1: neighbours staged in shared memory, 3 CTAs/SM (slower);
     // 2: own cell and subtree activity loaded an iteration ahead (FV1 69 ->
-    // 66 us); 3 (default): also the neighbours' parent-level flags (65 us);
+    // 66 us); 3: also the neighbours' parent-level flags (65 us); 5 (default):
+    // 3 + the last grid-stride windows handed out dynamically (64 us);
     // 0: L2 prefetch only
-    int fv1_stage = 3;
+    int fv1_stage = 5;
     int num_sms = 0;
     size_t smem_k1 = 0, smem_k1s = 0, smem_k1p = 0, smem_k2 = 0, smem_k3 = 0;
     // K3 split into a top launch (alone on its SM) + a subtree launch (one partition)
@@ -275,6 +276,8 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
         launch_pdl(hwfv1::k_fv1<false, 2, false, false, false, false, 2>, g->fv1_grid, 0, s, P, g->ctl);
     else if (g->fv1_stage == 3)
         launch_pdl(hwfv1::k_fv1<false, 2, false, false, false, false, 3>, g->fv1_grid, 0, s, P, g->ctl);
+    else if (g->fv1_stage == 5)
+        launch_pdl(hwfv1::k_fv1<false, 2, false, false, false, false, 5>, g->fv1_grid, 0, s, P, g->ctl);
     else if (g->fv1_minb == 4)
         launch_pdl(hwfv1::k_fv1<false, 4>, g->fv1_grid, sm5, s, P, g->ctl);
     else if (g->fv1_minb == 3)
@@ -655,6 +658,11 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kThreads, g->smem_k23);
             if (static_cast<int64_t>(occ) * g->num_sms >= static_cast<int64_t>(P.n_tiles) + 1) g->k23 = f;
         }
+        // tail balancing: the last 6/16 of FV1's grid-stride windows go to
+        // whichever warps are free (8 of 22 windows at L = 11: FV1 66.3 ->
+        // 64.3 us; 2-6 windows less, 10-24 windows less to slower)
+        const char* etw = std::getenv("SWAMP_FV1_TAIL16");
+        P.fv1_tail16 = etw ? static_cast<uint32_t>(std::min(16, std::max(0, std::atoi(etw)))) : 6u;
         const char* epf = std::getenv("SWAMP_FV1_PF");
         P.fv1_pf = epf ? std::atoi(epf) : 1;  // L2 prefetch: FV1 72 -> 69 us (round 1)
         const char* eq = std::getenv("SWAMP_FV1_QUAD");

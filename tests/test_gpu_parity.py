@@ -179,7 +179,7 @@ def test_partitioned_equals_single(parts, name, kw):
         np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))
 
 
-@pytest.mark.parametrize("variant", ["per-leaf", "strips", "quad", "stage", "ahead", "ahead-flags", "no-prefetch", "fused-k23"])
+@pytest.mark.parametrize("variant", ["per-leaf", "strips", "quad", "stage", "ahead", "ahead-flags", "tail", "no-prefetch", "fused-k23"])
 @pytest.mark.parametrize("name,kw", [("river_flood", dict(L=9)), ("monai_runup", dict(L=9))])
 def test_active_subtree_paths(monkeypatch, variant, name, kw):
     """L = 9 (64 subtrees of 64 x 64): FV1's dry-subtree shortcut and, opt-in,
@@ -188,7 +188,7 @@ def test_active_subtree_paths(monkeypatch, variant, name, kw):
     strips = variant == "strips"
     monkeypatch.setenv("SWAMP_FV1_STRIPS", "1" if strips else "0")
     monkeypatch.setenv("SWAMP_FV1_QUAD", "1" if variant == "quad" else "0")
-    monkeypatch.setenv("SWAMP_FV1_STAGE", {"stage": "1", "ahead": "2", "ahead-flags": "3"}.get(variant, "0"))
+    monkeypatch.setenv("SWAMP_FV1_STAGE", {"stage": "1", "ahead": "2", "ahead-flags": "3", "tail": "5"}.get(variant, "0"))
     monkeypatch.setenv("SWAMP_FV1_PF", "0" if variant == "no-prefetch" else "1")
     monkeypatch.setenv("SWAMP_FUSE_K23", "1" if variant == "fused-k23" else "0")
     cfg, h, qx, qy, z = cases.CASES[name](**kw)
