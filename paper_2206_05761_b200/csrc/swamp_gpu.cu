@@ -118,9 +118,9 @@ struct swamp_gpu {
     int fv1_minb = 2;  // occupancy variant of k_fv1 (SWAMP_FV1_MINB=3|4 for more CTAs/SM, with spills)
     // SWAMP_FV1_STAGE=1: neighbours staged in shared memory, 3 CTAs/SM (slower);
     // 2: own cell and subtree activity loaded an iteration ahead (FV1 69 ->
-    // 66 us); 3: also the neighbours' parent-level flags (65 us); 5 (default):
-    // 3 + the last grid-stride windows handed out dynamically (64 us);
-    // 0: L2 prefetch only
+    // 66 us); 3: also the neighbours' parent-level flags (65 us; default
+    // below L = 11); 5: 3 + the last grid-stride windows handed out
+    // dynamically (64 us; default from L = 11); 0: L2 prefetch only
     int fv1_stage = 5;
     int num_sms = 0;
     size_t smem_k1 = 0, smem_k1s = 0, smem_k1p = 0, smem_k2 = 0, smem_k3 = 0;
@@ -640,6 +640,9 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     }
     {
         if (const char* e = std::getenv("SWAMP_FV1_MINB")) g->fv1_minb = std::max(2, std::min(4, std::atoi(e)));
+        // tail balancing pays when the leaf list spans many grid-stride
+        // windows (L = 11: ~22); below that its bookkeeping costs ~5 %
+        g->fv1_stage = (L >= 11) ? 5 : 3;
         if (const char* e = std::getenv("SWAMP_FV1_STAGE")) g->fv1_stage = std::atoi(e);
         const char* es = std::getenv("SWAMP_FV1_STRIPS");
         P.strips = (es && es[0] == '1') ? 1 : 0;
@@ -663,6 +666,8 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         // 64.3 us; 2-6 windows less, 10-24 windows less to slower)
         const char* etw = std::getenv("SWAMP_FV1_TAIL16");
         P.fv1_tail16 = etw ? static_cast<uint32_t>(std::min(16, std::max(0, std::atoi(etw)))) : 6u;
+        const char* etc = std::getenv("SWAMP_FV1_TAILCHUNK");
+        P.fv1_tail_chunk = etc ? static_cast<uint32_t>(std::min(8, std::max(1, std::atoi(etc)))) : 1u;
         const char* epf = std::getenv("SWAMP_FV1_PF");
         P.fv1_pf = epf ? std::atoi(epf) : 1;  // L2 prefetch: FV1 72 -> 69 us (round 1)
         const char* eq = std::getenv("SWAMP_FV1_QUAD");
