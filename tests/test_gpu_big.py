@@ -37,3 +37,25 @@ def test_level13_steps_stay_finite():
         assert np.isfinite(f).all()
     del e
     gpu.trim_cache()
+
+
+@pytest.mark.parametrize("env", [("SWAMP_FV1_STAGE", "3"), ("SWAMP_K3_SPLIT", "0"), ("SWAMP_FV1_TAIL16", "15")],
+                         ids=["static-fv1", "one-launch-k3", "mostly-dynamic-fv1"])
+def test_level11_variants_agree(monkeypatch, env):
+    """L = 11 (config 5, 22 grid-stride windows): the default engine (tail-
+    balanced FV1, split K3) and a variant (static FV1 / K3 in one launch /
+    all but one window handed out dynamically) give the same bits after 12
+    steps."""
+    cfg, h, qx, qy, z = cases.river_flood(L=11)
+    a = gpu.initialise(cfg, h, qx, qy, z)
+    monkeypatch.setenv(*env)
+    b = gpu.initialise(cfg, h, qx, qy, z)
+    a.advance(12)
+    b.advance(12)
+    assert a.info() == b.info()
+    for fa, fb in zip(a.export_finest(), b.export_finest()):
+        np.testing.assert_array_equal(fa.view(np.uint64), fb.view(np.uint64))
+    (ah, *_), asig = a.export_tree()
+    (bh, *_), bsig = b.export_tree()
+    np.testing.assert_array_equal(asig, bsig)
+    del a, b
