@@ -22,6 +22,7 @@
 // lives on the device so a step is a fixed kernel sequence (CUDA-graph
 // capturable); every kernel is a no-op once t >= t_end.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 
 #include "hwfv1_physics.cuh"
@@ -75,6 +76,9 @@ struct Ctl {
     // line per kernel k (K1, K2, K3, K5): [0] = ~(first CTA start), [2] = last
     // CTA done (atomicMax); K5 zeroes the next buffer
     alignas(128) unsigned long long tl[2][4][16];
+    // last member: the step whose state the host mirror holds (written into
+    // the mapped host mirror only, after the rest of the struct)
+    alignas(128) unsigned long long rep_seq;
 };
 
 // Programmatic dependent launch: every kernel of the step is launched with
@@ -159,6 +163,7 @@ struct Params {
     int strips;           // strip path enabled (SWAMP_FV1_STRIPS=1; measured slower on B200)
     int quad;             // sibling-quad path (SWAMP_FV1_QUAD=1; measured slower on B200)
     int fv1_pf;           // FV1 prefetch of the next iteration's own cells: 0 off, 1 L2, 2 L1
+    Ctl* ctl_mirror;      // one partition: the host's pinned Ctl mirror (UVA), written at the step's end
     uint32_t fv1_tail16;  // FV1 STAGE 5: sixteenths of the grid-stride windows taken dynamically at the end
     uint32_t fv1_tail_chunk;  // FV1 STAGE 5: warp-iterations per dynamic grab
     // Morton-subtree partitions: this partition owns level-R
@@ -2423,6 +2428,29 @@ __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ct
         ctl->tl[slot][3][2] = gtimer();
         if (advance)  // next step's buffer
             for (int k = 0; k < 4; ++k) ctl->tl[slot ^ 1][k][0] = ctl->tl[slot ^ 1][k][2] = 0ull;
+    }
+    if (advance && P.ctl_mirror && threadIdx.x < 32) {
+        // the step's report straight into the host's pinned mirror (saves the
+        // host a device-to-host copy and a stream synchronisation per step):
+        // line 0 (t, dt, step, leaf counts), the error line and this step's
+        // stage stamps, then rep_seq = step behind a system-scope fence
+        __syncwarp();
+        const unsigned l = threadIdx.x;
+        const volatile unsigned long long* src = reinterpret_cast<const volatile unsigned long long*>(ctl);
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(P.ctl_mirror);
+        const unsigned w = (l < 16) ? l : static_cast<unsigned>(offsetof(Ctl, smax_bits) / 8) + (l - 16);
+        dst[w] = src[w];
+        if (l < 8) {
+            const unsigned t = static_cast<unsigned>(offsetof(Ctl, tl) / 8) + 64u * static_cast<unsigned>(slot) +
+                               16u * (l >> 1) + 2u * (l & 1u);
+            dst[t] = src[t];
+        }
+        __syncwarp();
+        if (l == 0) {
+            __threadfence_system();
+            *reinterpret_cast<volatile unsigned long long*>(&P.ctl_mirror->rep_seq) =
+                static_cast<unsigned long long>(*reinterpret_cast<volatile long long*>(&ctl->step));
+        }
     }
 }
 

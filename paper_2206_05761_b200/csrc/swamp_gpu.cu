@@ -112,9 +112,10 @@ struct swamp_gpu {
     Ctl* ctl = nullptr;      // device
     Ctl* ctl_host = nullptr; // pinned mirror
     std::vector<std::pair<void*, size_t>> allocs;  // device blocks (returned to the block cache)
-    cudaGraphExec_t graph1 = nullptr, graphS = nullptr, graphT = nullptr;
+    cudaGraphExec_t graph1 = nullptr, graphS = nullptr, graphT = nullptr, graphR = nullptr;
     int fv1_grid = 0;
     int64_t launches_per_step = 0;  // kernel nodes of the one-step graph
+    bool mirror_current = false;    // ctl_host holds the state after the last completed step
     int fv1_minb = 2;  // occupancy variant of k_fv1 (SWAMP_FV1_MINB=3|4 for more CTAs/SM, with spills)
     // SWAMP_FV1_STAGE=1: neighbours staged in shared memory, 3 CTAs/SM (slower);
     // 2: own cell and subtree activity loaded an iteration ahead (FV1 69 ->
@@ -161,6 +162,7 @@ struct swamp_gpu {
         if (graph1) cudaGraphExecDestroy(graph1);
         if (graphS) cudaGraphExecDestroy(graphS);
         if (graphT) cudaGraphExecDestroy(graphT);
+        if (graphR) cudaGraphExecDestroy(graphR);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (!allocs.empty() || scratch) cudaSetDevice(device);
@@ -305,24 +307,35 @@ int64_t kernel_nodes(cudaGraph_t graph) {
     return k;
 }
 
+// which: 0 graph1 (one step), 1 graphS (kGraphSteps), 2 graphT (one step,
+// event nodes), 3 graphR (one step whose FV1 also writes the host mirror:
+// step_adaptive's report; the mirror write costs ~2 us, so only graphR has it)
 int build_graph(swamp_gpu* g, int which) {
     {
         const int steps = which == 1 ? kGraphSteps : 1;
+        Ctl* const mirror = g->P.ctl_mirror;
+        if (which != 3) g->P.ctl_mirror = nullptr;
         cudaGraph_t graph;
-        CK(cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
-        for (int k = 0; k < steps; ++k) launch_step_kernels(g, which == 2);
-        CK(cudaStreamEndCapture(g->stream, &graph));
+        cudaError_t e = cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal);
+        if (e == cudaSuccess) {
+            for (int k = 0; k < steps; ++k) launch_step_kernels(g, which == 2);
+            e = cudaStreamEndCapture(g->stream, &graph);
+        }
+        g->P.ctl_mirror = mirror;
+        CK(e);
         if (which == 0) g->launches_per_step = kernel_nodes(graph);
         cudaGraphExec_t exec;
         CK(cudaGraphInstantiate(&exec, graph, 0));
         cudaGraphDestroy(graph);
-        (which == 0 ? g->graph1 : which == 1 ? g->graphS : g->graphT) = exec;
+        (which == 0 ? g->graph1 : which == 1 ? g->graphS : which == 2 ? g->graphT : g->graphR) = exec;
     }
     return SWAMP_OK;
 }
-int build_graphs(swamp_gpu* g) {  // graph1 and the 8-step graph now (timed loops replay it), graphT on demand
-    const int st = build_graph(g, 0);
-    return st ? st : build_graph(g, 1);
+int build_graphs(swamp_gpu* g) {  // graph1, the 8-step graph and graphR now (timed loops replay them), graphT on demand
+    int st = build_graph(g, 0);
+    if (!st) st = build_graph(g, 1);
+    if (!st && g->P.ctl_mirror) st = build_graph(g, 3);
+    return st;
 }
 // single engines: the 8-step graph / the profiling graph on demand
 int ensure_graph(swamp_gpu* g, int which) {
@@ -334,6 +347,7 @@ int ensure_graph(swamp_gpu* g, int which) {
 int fetch_ctl(swamp_gpu* g) {
     CK(cudaMemcpyAsync(g->ctl_host, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
     CK(cudaStreamSynchronize(g->stream));
+    g->mirror_current = true;
     if (g->ctl_host->err_code != 0) {
         char buf[256];
         std::snprintf(buf, sizeof buf, "device error %d at z=%u quantity=%d stage=%d", g->ctl_host->err_code,
@@ -505,6 +519,13 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     P.pctl[0] = g->ctl;
     tr("device allocations");
     if (cached_pinned_ctl(&g->ctl_host) != cudaSuccess) return fail(SWAMP_E_NOMEM);
+    P.ctl_mirror = nullptr;
+    if (G == 1) {  // FV1's finalizing CTA writes each step's control block into the pinned mirror
+        void* dm = nullptr;
+        const char* em = std::getenv("SWAMP_MIRROR");
+        if (!(em && em[0] == '0') && cudaHostGetDevicePointer(&dm, g->ctl_host, 0) == cudaSuccess)
+            P.ctl_mirror = static_cast<Ctl*>(dm);
+    }
     tr("pinned control block");
     double *d_it = nullptr, *d_iv = nullptr, *d_out = nullptr;
     if ((st = dalloc(g, &d_it, sizeof(double) * std::max(1, cfg->inflow_n)))) return fail(st);
@@ -1220,6 +1241,35 @@ int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep) {
     if (!g) return SWAMP_E_ARG;
     if (!g->parts.empty()) return group_advance(g, 1, true, rep);
     cudaSetDevice(g->device);
+    // fast path: the step's FV1 writes the control block into the pinned
+    // mirror; the host waits for its sequence word instead of copying and
+    // synchronising (falls back to the copy if the word does not arrive)
+    if (g->P.ctl_mirror && g->graphR && !g->profiling && !g->uniform && g->mirror_current &&
+        g->ctl_host->t < g->P.t_end) {
+        volatile unsigned long long* seq = &g->ctl_host->rep_seq;
+        const unsigned long long expect = static_cast<unsigned long long>(g->ctl_host->step) + 1ull;
+        g->mirror_current = false;
+        CK(cudaGraphLaunch(g->graphR, g->stream));
+        const auto t0 = std::chrono::steady_clock::now();
+        bool arrived = false;
+        for (unsigned spin = 0;; ++spin) {
+            if (*seq == expect) {
+                arrived = true;
+                break;
+            }
+            if ((spin & 1023u) == 1023u &&
+                std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(200))
+                break;
+        }
+        if (arrived && g->ctl_host->err_code == 0) {
+            g->mirror_current = true;
+            fill_report(g, rep);
+            return SWAMP_OK;
+        }
+        const int st = fetch_ctl(g);  // error or no word: the synchronous path decides
+        fill_report(g, rep);
+        return st;
+    }
     if (g->profiling && g->rank_world == 0 && ensure_graph(g, 2) == SWAMP_OK && g->graphT) {
         CK(cudaGraphLaunch(g->graphT, g->stream));
     } else {
@@ -1253,6 +1303,7 @@ int swamp_gpu_enqueue(swamp_gpu* g, int64_t n_steps) {
     if (!g || n_steps < 0) return SWAMP_E_ARG;
     if (!g->parts.empty()) return group_advance(g, n_steps, false, nullptr);
     cudaSetDevice(g->device);
+    if (n_steps > 0) g->mirror_current = false;  // (the mirror moves on asynchronously)
     int64_t k = 0;
     if (n_steps >= kGraphSteps) {
         const int st = ensure_graph(g, 1);
