@@ -165,7 +165,6 @@ struct Params {
     int fv1_pf;           // FV1 prefetch of the next iteration's own cells: 0 off, 1 L2, 2 L1
     Ctl* ctl_mirror;      // one partition: the host's pinned Ctl mirror (UVA), written at the step's end
     uint32_t fv1_tail16;  // FV1 STAGE 5: sixteenths of the grid-stride windows taken dynamically at the end
-    uint32_t fv1_tail_chunk;  // FV1 STAGE 5: warp-iterations per dynamic grab
     // Morton-subtree partitions: this partition owns level-R
     // subtrees [tile_lo, tile_hi); cells on levels >= R belong to their
     // subtree's partition, cells above R are replicated except that a leaf's
@@ -2851,21 +2850,17 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     constexpr bool TAIL = STAGE == 5;
     const uint32_t nwin = N / stride, ntail = (nwin * P.fv1_tail16 + 8u) >> 4;
     const uint32_t nstat = (TAIL && ntail > 0u && nwin > ntail) ? (nwin - ntail) * stride : N;  // (small lists: static)
-    // a grab takes fv1_tail_chunk warp-iterations (fewer same-address atomics)
-    const uint32_t chunk = 32u * P.fv1_tail_chunk;
-    uint32_t ce = 0;  // end of the chunk the newest base belongs to
+    // one warp-iteration per grab (2 or 4 per grab measured slower at L = 11)
     auto grab = [&]() -> uint32_t {
         uint32_t c = 0;
         if (lane == 0) c = atomicAdd(&ctl->fv1_tail, 1u);
         c = __shfl_sync(kFull, c, 0);
-        const uint32_t b = nstat + chunk * c;
-        ce = b + chunk;
+        const uint32_t b = nstat + 32u * c;
         return b < N ? b : N;
     };
     auto next_of = [&](uint32_t b) -> uint32_t {
         if (b >= N) return N;
-        if (b < nstat) return (b + stride < nstat) ? b + stride : grab();
-        return (b + 32u < ce) ? b + 32u : grab();
+        return (b + stride < nstat) ? b + stride : grab();
     };
     uint32_t b1 = 0, b2 = 0;
     if (TAIL) {

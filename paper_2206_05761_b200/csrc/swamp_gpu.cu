@@ -687,8 +687,6 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         // 64.3 us; 2-6 windows less, 10-24 windows less to slower)
         const char* etw = std::getenv("SWAMP_FV1_TAIL16");
         P.fv1_tail16 = etw ? static_cast<uint32_t>(std::min(16, std::max(0, std::atoi(etw)))) : 6u;
-        const char* etc = std::getenv("SWAMP_FV1_TAILCHUNK");
-        P.fv1_tail_chunk = etc ? static_cast<uint32_t>(std::min(8, std::max(1, std::atoi(etc)))) : 1u;
         const char* epf = std::getenv("SWAMP_FV1_PF");
         P.fv1_pf = epf ? std::atoi(epf) : 1;  // L2 prefetch: FV1 72 -> 69 us (round 1)
         const char* eq = std::getenv("SWAMP_FV1_QUAD");
