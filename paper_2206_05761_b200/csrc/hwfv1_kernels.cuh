@@ -1764,7 +1764,7 @@ __device__ __forceinline__ void k3_wait(const Ctl* ctl, unsigned long long epoch
 // top of the tree (block 0 of K3); top flags at the padded offsets slo(n)
 template <bool EXPORT>
 __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long long epoch, uint8_t* sm,
-                       const Probe& stamp, bool band_done = false) {
+                       const Probe& stamp, bool band_done = false, bool staged_out = false) {
     __shared__ unsigned s_red[32];
     __shared__ unsigned s_off[6];
     const uint8_t* sigc = EXPORT ? P.sig[p] : P.sig[p ^ 1];
@@ -1780,6 +1780,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     uint8_t* tv = tp + fb;
     uint8_t* swet = tv + fb;      // wet subtrees after the previous FV1
     uint32_t* scnt = reinterpret_cast<uint32_t*>(swet + ((nt + 15u) & ~15u));
+    uint32_t* sres = scnt + 2 * nt;  // staged_out: A / B offset, depth, source per subtree (caller sized it)
     const bool cnt_smem = nt <= 1024u;
     const uint32_t* cnt = cnt_smem ? scnt : P.tile_cnt;
     const uint32_t al = P.G == 1 ? 16u : P.pb_align;
@@ -1928,18 +1929,29 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
                 }
             }
         }
-        P.tile_lvl[t] = static_cast<uint32_t>(n) | (cbf[t] ? kEmit : 0u);
-        P.tile_off[2 * nt + t] = oa + ob;
+        if (!staged_out) {
+            P.tile_lvl[t] = static_cast<uint32_t>(n) | (cbf[t] ? kEmit : 0u);
+            P.tile_off[2 * nt + t] = oa + ob;
+        }
         if (!EXPORT) {
-            P.tile_off[t] = oa;
-            P.tile_off[nt + t] = ta + ob;
-            P.tile_src[t] = src;
-            const unsigned long long tag = (epoch & 0xFFFFFFFFull) << 32;
-            unsigned long long* rec = P.k3_rec + 16ull * t;
-            st_relaxed_u64(rec + 0, tag | oa);
-            st_relaxed_u64(rec + 1, tag | (ta + ob));
-            st_relaxed_u64(rec + 2, tag | (static_cast<uint32_t>(n) | (cbf[t] ? kEmit : 0u)));
-            st_relaxed_u64(rec + 3, tag | src);
+            if (!staged_out) {
+                P.tile_off[t] = oa;
+                P.tile_off[nt + t] = ta + ob;
+                P.tile_src[t] = src;
+            }
+            if (staged_out) {  // (staged in shared memory, written out coalesced below)
+                sres[t] = oa;
+                sres[nt + t] = ta + ob;
+                sres[2 * nt + t] = static_cast<uint32_t>(n) | (cbf[t] ? kEmit : 0u);
+                sres[3 * nt + t] = src;
+            } else {
+                const unsigned long long tag = (epoch & 0xFFFFFFFFull) << 32;
+                unsigned long long* rec = P.k3_rec + 16ull * t;
+                st_relaxed_u64(rec + 0, tag | oa);
+                st_relaxed_u64(rec + 1, tag | (ta + ob));
+                st_relaxed_u64(rec + 2, tag | (static_cast<uint32_t>(n) | (cbf[t] ? kEmit : 0u)));
+                st_relaxed_u64(rec + 3, tag | src);
+            }
             if (t == P.tile_lo) {
                 s_off[0] = oa;
                 s_off[1] = ta + ob;
@@ -1951,6 +1963,18 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         }
         oa += ca;
         ob += cb;
+    }
+    if (staged_out) {
+        // one 32-B vector store per subtree record (each 8-B word carries the
+        // tag, so the record needs no ordering)
+        __syncthreads();
+        const unsigned long long tag = (epoch & 0xFFFFFFFFull) << 32;
+        for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) {
+            const uint32_t A = sres[t], B = sres[nt + t], V = sres[2 * nt + t], S = sres[3 * nt + t];
+            asm volatile("st.relaxed.gpu.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(P.k3_rec + 16ull * t),
+                         "l"(tag | A), "l"(tag | B), "l"(tag | V), "l"(tag | S)
+                         : "memory");
+        }  // (tile_off / tile_lvl / tile_src: read only by partitioned engines and exports, which run their own top)
     }
     stamp(4);
     // the subtree CTAs need only the offsets, depths and decode sources:
@@ -2330,7 +2354,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_traverse_top(Params P, Ctl* ctl
     const Probe stamp(ctl, 16);
     stamp(7, t_entry);
     k3_top<false>(P, ctl, hd.parity, hd.buf, 2ull * static_cast<unsigned long long>(hd.step) + 2ull, smem3t, stamp,
-                  P.top_band != 0);
+                  P.top_band != 0, P.n_tiles <= 1024);
 }
 template <int KT>
 __global__ void __launch_bounds__(kThreads, 8) k_traverse_tiles(Params P, Ctl* ctl) {
