@@ -59,3 +59,21 @@ def test_level11_variants_agree(monkeypatch, env):
     (bh, *_), bsig = b.export_tree()
     np.testing.assert_array_equal(asig, bsig)
     del a, b
+
+
+def test_level11_matches_oracle():
+    """Config 5 itself (L = 11, 4^5 = 1024 subtrees: the split K3 top, the
+    records, K1's shuffle levels, the tail-balanced FV1) against the CPU
+    oracle, bitwise, for a few steps (the oracle takes ~0.1 s per step)."""
+    from oracle import oracle as O
+    from tests._parity import compare_states
+
+    cfg, h, qx, qy, z = cases.river_flood(L=11)
+    g = gpu.initialise(cfg, h, qx, qy, z)
+    o = O.Oracle(cfg, h, qx, qy, z)
+    compare_states(g, o, "L11 init")
+    for k in range(1, 6):
+        g.step_adaptive()
+        o.step()
+        compare_states(g, o, f"L11 step {k}")
+    del g
