@@ -77,3 +77,24 @@ def test_level11_matches_oracle():
         o.step()
         compare_states(g, o, f"L11 step {k}")
     del g
+
+
+@pytest.mark.parametrize("name,kw", [("circular_dambreak", dict(L=10, epsilon=1e-3)),
+                                     ("monai_runup", dict(L=10)),
+                                     ("quiescent_humps", dict(L=10))],
+                         ids=["circular-L10", "monai-L10", "humps-L10"])
+def test_level10_configs_match_oracle(name, kw):
+    """Configs 2-4 at L = 10 (4^4 = 256 subtrees, static FV1 variant, split
+    K3) against the CPU oracle, bitwise, for 8 steps."""
+    from oracle import oracle as O
+    from tests._parity import compare_states
+
+    cfg, h, qx, qy, z = cases.CASES[name](**kw)
+    g = gpu.initialise(cfg, h, qx, qy, z)
+    o = O.Oracle(cfg, h, qx, qy, z)
+    for k in range(1, 9):
+        g.step_adaptive()
+        o.step()
+        if k in (1, 4, 8):
+            compare_states(g, o, f"{name} L10 step {k}")
+    del g
