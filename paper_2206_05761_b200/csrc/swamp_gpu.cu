@@ -827,7 +827,10 @@ bool part_step_phase(swamp_gpu* q, int k, cudaStream_t s) {
         case 3: q->k3<<<P.tiles_per_part + 1, kThreads, q->smem_k3, s>>>(P, q->ctl, 0, 0ull); return true;
         case 4:
             if (P.has_ina) hwfv1::k_fv1<false, 2, true, false, false, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
-            else hwfv1::k_fv1<false, 2, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
+            else if (q->fv1_stage >= 2)  // own cells loaded an iteration ahead (flags come from peer tables: no STAGE 3)
+                hwfv1::k_fv1<false, 2, true, false, false, false, 2><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
+            else
+                hwfv1::k_fv1<false, 2, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
             return true;
         default: hwfv1::k_finalize<<<1, 32, 0, s>>>(P, q->ctl, 1); return true;
     }
