@@ -1835,55 +1835,146 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     }
     __syncthreads();
     stamp(1);
-    // ---- one warp: closure bottom-up (hot path), then the on-tree flags
-    //      top-down and the first subtree under each top-level leaf (closure
-    //      makes significance upward-closed: a cell is on the tree iff its
-    //      parent is significant and on it); the other warps clear cbf
-    // closure of level R-1 (the largest) by every thread, the rest by warp 0
-    if (!EXPORT && R >= 1) {
-        for (uint32_t m = threadIdx.x; m < (1u << (2 * (R - 1))); m += kThreads)
-            if (*reinterpret_cast<const uint32_t*>(ts + slo(R) + 4u * m)) ts[slo(R - 1) + m] = 1;
+    unsigned tn = 0;
+    const uint8_t* reach = ti + fb;
+    if (!EXPORT && R == 5) {
+        // L = 11 (1024 subtrees): closure, on-tree flags, first subtrees and
+        // the newly significant count on bit masks in warp 0's registers
+        // (level 5: 32 cells per lane; 4: 8; 3: 2; 2: one in lanes < 16; 1
+        // and 0 in every lane), written back to the byte arrays once — the
+        // same flags the generic pass below produces
+        __shared__ unsigned s_tn;
+        if (threadIdx.x < 32) {
+            const uint32_t l = threadIdx.x;
+            auto bits4 = [](uint32_t x) { return ((x * 0x01020408u) >> 24) & 0xFu; };  // 4 bytes (0/1) -> 4 bits
+            auto bytes4 = [](uint32_t b) { return (b * 0x00204081u) & 0x01010101u; };  // 4 bits -> 4 bytes
+            auto any_nib = [](uint32_t w, int n) {  // bit c = nibble c of w nonzero, c < n
+                const uint32_t t = w | (w >> 1) | (w >> 2) | (w >> 3);
+                uint32_t r = 0;
+                for (int c = 0; c < n; ++c) r |= ((t >> (4 * c)) & 1u) << c;
+                return r;
+            };
+            // level 5 (subtree roots, K2's final flags)
+            const uint4 a5 = *reinterpret_cast<const uint4*>(ts + slo(5) + 32u * l);
+            const uint4 b5 = *reinterpret_cast<const uint4*>(ts + slo(5) + 32u * l + 16u);
+            const uint32_t w5 = bits4(a5.x) | (bits4(a5.y) << 4) | (bits4(a5.z) << 8) | (bits4(a5.w) << 12) |
+                                (bits4(b5.x) << 16) | (bits4(b5.y) << 20) | (bits4(b5.z) << 24) | (bits4(b5.w) << 28);
+            // closure bottom-up: band | any child
+            const uint2 q4 = *reinterpret_cast<const uint2*>(ts + slo(4) + 8u * l);
+            const uint32_t s4 = (bits4(q4.x) | (bits4(q4.y) << 4)) | any_nib(w5, 8);
+            const uint32_t s3 = (ts[slo(3) + 2u * l] | (ts[slo(3) + 2u * l + 1u] << 1)) | any_nib(s4, 2);
+            const uint32_t x3 = s3 | (__shfl_down_sync(kFull, s3, 1) << 2);  // lane 2c: level-3 cells 4c..4c+3
+            const uint32_t x3c = __shfl_sync(kFull, x3, (2u * l) & 31u);  // (every lane shuffles)
+            const uint32_t s2l = (l < 16u) ? (ts[slo(2) + l] | (x3c ? 1u : 0u)) : 0u;
+            const uint32_t m2 = __ballot_sync(kFull, s2l != 0u) & 0xFFFFu;                   // level 2, 16 bits
+            const uint32_t b1 = ts[slo(1)] | (ts[slo(1) + 1] << 1) | (ts[slo(1) + 2] << 2) | (ts[slo(1) + 3] << 3);
+            const uint32_t s1 = b1 | any_nib(m2, 4);
+            const uint32_t s0 = (ts[0] | (s1 ? 1u : 0u)) & 1u;
+            // on-tree top-down: a child is on the tree iff its parent is on it and significant
+            const uint32_t in1 = s0 ? 0xFu : 0u;
+            uint32_t in2 = 0;
+            for (int c = 0; c < 16; ++c) in2 |= (((in1 & s1) >> (c >> 2)) & 1u) << c;
+            const uint32_t par3 = l >> 1;  // this lane's level-3 cells 2l, 2l+1 share a parent
+            const uint32_t in3 = (((in2 & m2) >> par3) & 1u) ? 3u : 0u;
+            const uint32_t on3 = in3 & s3;
+            const uint32_t in4 = ((on3 & 1u) ? 0xFu : 0u) | ((on3 & 2u) ? 0xF0u : 0u);
+            const uint32_t on4 = in4 & s4;
+            uint32_t in5 = 0;
+            for (int j = 0; j < 8; ++j) in5 |= ((on4 >> j) & 1u) ? (0xFu << (4 * j)) : 0u;
+            // write back: closure (ts) and on-tree (ti) bytes, first subtrees (cbf)
+            *reinterpret_cast<uint2*>(ts + slo(4) + 8u * l) = make_uint2(bytes4(s4 & 0xFu), bytes4(s4 >> 4));
+            *reinterpret_cast<uint2*>(ti + slo(4) + 8u * l) = make_uint2(bytes4(in4 & 0xFu), bytes4(in4 >> 4));
+            uint32_t* t5 = reinterpret_cast<uint32_t*>(ti + slo(5) + 32u * l);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) t5[k] = bytes4((in5 >> (4 * k)) & 0xFu);
+            ts[slo(3) + 2u * l] = s3 & 1u;
+            ts[slo(3) + 2u * l + 1u] = (s3 >> 1) & 1u;
+            ti[slo(3) + 2u * l] = in3 & 1u;
+            ti[slo(3) + 2u * l + 1u] = (in3 >> 1) & 1u;
+            if (l < 16u) {
+                ts[slo(2) + l] = (m2 >> l) & 1u;
+                ti[slo(2) + l] = (in2 >> l) & 1u;
+                if ((in2 >> l) & 1u && !((m2 >> l) & 1u)) cbf[l << 6] = 1;
+            }
+            if (l < 4u) {
+                ts[slo(1) + l] = (s1 >> l) & 1u;
+                ti[slo(1) + l] = (in1 >> l) & 1u;
+                if ((in1 >> l) & 1u && !((s1 >> l) & 1u)) cbf[l << 8] = 1;
+            }
+            if (l == 0u) {
+                ts[0] = static_cast<uint8_t>(s0);
+                ti[0] = 1;
+                if (!s0) cbf[0] = 1;
+            }
+            for (int k = 0; k < 2; ++k)
+                if (((in3 >> k) & 1u) && !((s3 >> k) & 1u)) cbf[(2u * l + k) << 4] = 1;
+            for (int j = 0; j < 8; ++j)
+                if (((in4 >> j) & 1u) && !((s4 >> j) & 1u)) cbf[(8u * l + j) << 2] = 1;
+            // newly significant top cells (significant now, not in the previous tree)
+            const uint2 v4 = *reinterpret_cast<const uint2*>(tv + slo(4) + 8u * l);
+            const uint32_t t4 = bits4(v4.x) | (bits4(v4.y) << 4);
+            const uint32_t t3 = tv[slo(3) + 2u * l] | (tv[slo(3) + 2u * l + 1u] << 1);
+            unsigned nn = __popc(s4 & ~t4) + __popc(s3 & ~t3);
+            if (l < 16u) nn += ((m2 >> l) & 1u) && !tv[slo(2) + l] ? 1u : 0u;
+            if (l < 4u) nn += ((s1 >> l) & 1u) && !tv[slo(1) + l] ? 1u : 0u;
+            if (l == 0u) nn += s0 && !tv[0] ? 1u : 0u;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(kFull, nn, o);
+            if (l == 0u) s_tn = nn;
+        }
         __syncthreads();
-    }
-    auto ontree = [&](int n, uint32_t m) {
-        const bool in = ti[slo(n) + m] != 0, sg = ts[slo(n) + m] != 0;
-        *reinterpret_cast<uint32_t*>(ti + slo(n + 1) + 4u * m) = (in && sg) ? 0x01010101u : 0u;
-        if (in && !sg) cbf[m << (2 * (R - n))] = 1;
-    };
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        if (!EXPORT)
-            for (int n = R - 2; n >= 0; --n) {
-                for (uint32_t m = lane; m < (1u << (2 * n)); m += 32)
-                    if (*reinterpret_cast<const uint32_t*>(ts + slo(n + 1) + 4u * m)) ts[slo(n) + m] = 1;
+        tn = s_tn;
+    } else {
+        // ---- one warp: closure bottom-up (hot path), then the on-tree flags
+        //      top-down and the first subtree under each top-level leaf (closure
+        //      makes significance upward-closed: a cell is on the tree iff its
+        //      parent is significant and on it); the other warps clear cbf
+        // closure of level R-1 (the largest) by every thread, the rest by warp 0
+        if (!EXPORT && R >= 1) {
+            for (uint32_t m = threadIdx.x; m < (1u << (2 * (R - 1))); m += kThreads)
+                if (*reinterpret_cast<const uint32_t*>(ts + slo(R) + 4u * m)) ts[slo(R - 1) + m] = 1;
+            __syncthreads();
+        }
+        auto ontree = [&](int n, uint32_t m) {
+            const bool in = ti[slo(n) + m] != 0, sg = ts[slo(n) + m] != 0;
+            *reinterpret_cast<uint32_t*>(ti + slo(n + 1) + 4u * m) = (in && sg) ? 0x01010101u : 0u;
+            if (in && !sg) cbf[m << (2 * (R - n))] = 1;
+        };
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            if (!EXPORT)
+                for (int n = R - 2; n >= 0; --n) {
+                    for (uint32_t m = lane; m < (1u << (2 * n)); m += 32)
+                        if (*reinterpret_cast<const uint32_t*>(ts + slo(n + 1) + 4u * m)) ts[slo(n) + m] = 1;
+                    __syncwarp();
+                }
+            if (lane == 0) ti[0] = 1;
+            __syncwarp();
+            for (int n = 0; n < R - 1; ++n) {
+                for (uint32_t m = lane; m < (1u << (2 * n)); m += 32) ontree(n, m);
                 __syncwarp();
             }
-        if (lane == 0) ti[0] = 1;
-        __syncwarp();
-        for (int n = 0; n < R - 1; ++n) {
-            for (uint32_t m = lane; m < (1u << (2 * n)); m += 32) ontree(n, m);
-            __syncwarp();
         }
-    }
-    __syncthreads();
-    // on-tree flags of level R (subtree roots) from level R-1, every thread
-    if (R >= 1) {
-        for (uint32_t m = threadIdx.x; m < (1u << (2 * (R - 1))); m += kThreads) ontree(R - 1, m);
         __syncthreads();
-    } else if (threadIdx.x == 0) {
-        ti[0] = 1;
-    }
-    if (R == 0) __syncthreads();
-    const uint8_t* reach = ti + fb;
-    // newly significant top cells (decode sources exist only below them)
-    unsigned nnew = 0;
-    if (!EXPORT)
-        for (uint32_t q = threadIdx.x; q < lo(R, 0); q += kThreads) {
-            const int n = (31 - __clz(3u * q + 1u)) >> 1;
-            const uint32_t a = slo(n) + (q - lo(n, 0));
-            nnew += (ts[a] && !tv[a]) ? 1u : 0u;
+        // on-tree flags of level R (subtree roots) from level R-1, every thread
+        if (R >= 1) {
+            for (uint32_t m = threadIdx.x; m < (1u << (2 * (R - 1))); m += kThreads) ontree(R - 1, m);
+            __syncthreads();
+        } else if (threadIdx.x == 0) {
+            ti[0] = 1;
         }
-    const unsigned tn = EXPORT ? 0u : block_sum(nnew, s_red);
+        if (R == 0) __syncthreads();
+        // newly significant top cells (decode sources exist only below them)
+        unsigned nnew = 0;
+        if (!EXPORT)
+            for (uint32_t q = threadIdx.x; q < lo(R, 0); q += kThreads) {
+                const int n = (31 - __clz(3u * q + 1u)) >> 1;
+                const uint32_t a = slo(n) + (q - lo(n, 0));
+                nnew += (ts[a] && !tv[a]) ? 1u : 0u;
+            }
+        tn = EXPORT ? 0u : block_sum(nnew, s_red);
+    }
+
     stamp(2);
 
     // ---- per-subtree counts, scans, depth and decode source
