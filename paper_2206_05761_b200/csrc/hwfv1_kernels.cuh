@@ -143,8 +143,8 @@ struct Params {
     uint32_t* tile_lvl;   // traversal depth of each subtree (R = reached) | kEmit
     uint32_t* tile_src;   // decode source of a reached subtree root, or kNoSrc
     // hot-path K3: the top's results for subtree t as four self-tagged words
-    // (epoch << 32 | A offset, B offset, depth, decode source) on the
-    // subtree's own 128-B line, so each subtree CTA polls only its own line
+    // (epoch << 32 | A offset, B offset, depth, decode source), 32 B per
+    // subtree: each subtree CTA polls only its own record (4 per line)
     unsigned long long* k3_rec;
     // FV1 dry shortcut (one partition): wet[b][t] = some leaf of subtree t
     // ended the step with h >= h_dry (b = step parity); tact[t] bit 0 =
@@ -1781,6 +1781,10 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     uint8_t* swet = tv + fb;      // wet subtrees after the previous FV1
     uint32_t* scnt = reinterpret_cast<uint32_t*>(swet + ((nt + 15u) & ~15u));
     uint32_t* sres = scnt + 2 * nt;  // staged_out: A / B offset, depth, source per subtree (caller sized it)
+    // staged_out: per level-(R-1) cell (shared by its 4 subtrees) the depth a
+    // non-reached subtree below it stops at and the decode source
+    uint32_t* ssrc = sres + 4 * nt;
+    uint8_t* sdep = reinterpret_cast<uint8_t*>(ssrc + (R >= 1 ? (1u << (2 * (R - 1))) : 1u));
     const bool cnt_smem = nt <= 1024u;
     const uint32_t* cnt = cnt_smem ? scnt : P.tile_cnt;
     const uint32_t al = P.G == 1 ? 16u : P.pb_align;
@@ -2000,6 +2004,24 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     const unsigned ta = static_cast<unsigned>(tot64 >> 32), tb = static_cast<unsigned>(tot64);
     unsigned oa = static_cast<unsigned>(o64 >> 32), ob = static_cast<unsigned>(o64);
     stamp(3);
+    if (staged_out && R >= 1) {
+        for (uint32_t c = threadIdx.x; c < (1u << (2 * (R - 1))); c += kThreads) {
+            int n = 0;
+            while (n < R && ts[slo(n) + (c >> (2 * (R - 1 - n)))]) ++n;
+            sdep[c] = static_cast<uint8_t>(n);
+            uint32_t src = kNoSrc;
+            if (!EXPORT && tn)
+                for (int k = 0; k < R; ++k) {
+                    const uint32_t q = slo(k) + (c >> (2 * (R - 1 - k)));
+                    if (ts[q] && !tv[q]) {
+                        src = zo::z_of(k, c >> (2 * (R - 1 - k)));
+                        break;
+                    }
+                }
+            ssrc[c] = src;
+        }
+        __syncthreads();
+    }
     const uint32_t full = 1u << (2 * P.K);  // level-L leaves of a fully refined subtree
     const bool strips = !EXPORT && P.strips && P.G == 1 && P.K == 6;
     unsigned nst = 0;                       // this thread's strip-path subtrees
@@ -2008,7 +2030,10 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         counts(t, ca, cb);
         uint32_t src = kNoSrc;
         int n = R;
-        if (!reach[t]) {
+        if (staged_out && R >= 1) {  // (from the per-parent table above)
+            if (!reach[t]) n = sdep[t >> 2];
+            else src = ssrc[t >> 2];
+        } else if (!reach[t]) {
             n = 0;
             while (ts[slo(n) + (t >> (2 * (R - n)))]) ++n;
         } else if (!EXPORT && tn) {
@@ -2037,7 +2062,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
                 sres[3 * nt + t] = src;
             } else {
                 const unsigned long long tag = (epoch & 0xFFFFFFFFull) << 32;
-                unsigned long long* rec = P.k3_rec + 16ull * t;
+                unsigned long long* rec = P.k3_rec + 4ull * t;
                 st_relaxed_u64(rec + 0, tag | oa);
                 st_relaxed_u64(rec + 1, tag | (ta + ob));
                 st_relaxed_u64(rec + 2, tag | (static_cast<uint32_t>(n) | (cbf[t] ? kEmit : 0u)));
@@ -2062,7 +2087,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         const unsigned long long tag = (epoch & 0xFFFFFFFFull) << 32;
         for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) {
             const uint32_t A = sres[t], B = sres[nt + t], V = sres[2 * nt + t], S = sres[3 * nt + t];
-            asm volatile("st.relaxed.gpu.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(P.k3_rec + 16ull * t),
+            asm volatile("st.relaxed.gpu.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(P.k3_rec + 4ull * t),
                          "l"(tag | A), "l"(tag | B), "l"(tag | V), "l"(tag | S)
                          : "memory");
         }  // (tile_off / tile_lvl / tile_src: read only by partitioned engines and exports, which run their own top)
@@ -2251,7 +2276,7 @@ __device__ void k3_tile(const Params& P, Ctl* ctl, int p, int tbuf, unsigned lon
         // step's tag (each word is written atomically with its tag)
         if (threadIdx.x == 0) {
             const unsigned tag = static_cast<unsigned>(epoch);
-            const unsigned long long* rec = P.k3_rec + 16ull * j;
+            const unsigned long long* rec = P.k3_rec + 4ull * j;
             unsigned long long v0, v1, v2, v3;
             for (;;) {
                 v0 = ld_relaxed_u64(rec + 0);

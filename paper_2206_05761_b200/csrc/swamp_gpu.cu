@@ -507,7 +507,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     cudaMemset(P.wet[1], 1, P.n_tiles);
     cudaMemset(P.tact, 1, P.n_tiles);
     if ((st = dalloc(g, &P.tile_src, P.n_tiles * sizeof(uint32_t)))) return fail(st);
-    if ((st = dalloc(g, &P.k3_rec, P.n_tiles * 16 * sizeof(unsigned long long)))) return fail(st);
+    if ((st = dalloc(g, &P.k3_rec, P.n_tiles * 4 * sizeof(unsigned long long)))) return fail(st);
     if ((st = dalloc(g, &g->ctl, sizeof(Ctl)))) return fail(st);
     // peer tables: self only (a partitioned group fills in every partition)
     for (int b = 0; b < 2; ++b) {
@@ -786,7 +786,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     if ((st = fetch_ctl(g))) return fail(st);
     cudaMemsetAsync(g->ctl->tl, 0, sizeof(g->ctl->tl), s);
     cudaMemsetAsync(&g->ctl->k3_ready, 0, sizeof(g->ctl->k3_ready), s);  // hot-path epochs restart at step 0
-    cudaMemsetAsync(P.k3_rec, 0, P.n_tiles * 16 * sizeof(unsigned long long), s);  // (and the per-subtree records)
+    cudaMemsetAsync(P.k3_rec, 0, P.n_tiles * 4 * sizeof(unsigned long long), s);  // (and the per-subtree records)
     if ((st = build_graphs(g))) return fail(st);
     tr("graphs");
     *out = g;
@@ -893,7 +893,7 @@ void part_after_init(swamp_gpu* q) {
     cudaMemsetAsync(q->ctl->rate_bits, 0, sizeof(q->ctl->rate_bits), q->stream);
     cudaMemsetAsync(q->ctl->tl, 0, sizeof(q->ctl->tl), q->stream);
     cudaMemsetAsync(&q->ctl->k3_ready, 0, sizeof(q->ctl->k3_ready), q->stream);
-    cudaMemsetAsync(q->P.k3_rec, 0, q->P.n_tiles * 16 * sizeof(unsigned long long), q->stream);
+    cudaMemsetAsync(q->P.k3_rec, 0, q->P.n_tiles * 4 * sizeof(unsigned long long), q->stream);
 }
 
 // step graphs (graph1 = 1 step, graphS = kGraphSteps) of `g`, captured on
