@@ -62,9 +62,7 @@ struct Ctl {
     alignas(128) unsigned long long cnt_new;     // newly significant cells decoded by the last K3
     unsigned long long cnt_updates;              // leaf updates of all steps so far (sum of N)
     alignas(128) unsigned long long k3_ready;    // K3's top CTA published its results (epoch)
-    alignas(128) unsigned long long k2_done;     // fused K2+K3: subtree CTAs done with K2 (reset by the top CTA)
     alignas(128) unsigned int fv1_tail;          // FV1 (STAGE 5): dynamic tail chunks taken this step
-    uint32_t n_stile;                            // subtrees on FV1's strip path this step
     alignas(128) unsigned long long smax_bits[4];
     int err_code;
     uint32_t err_z;
@@ -156,13 +154,6 @@ struct Params {
     // the whole array
     uint8_t* ina;
     int has_ina;
-    // FV1 strip path: subtrees that are active, reached and fully refined to
-    // level L (every level-L cell a leaf) are updated by warps marching
-    // 32 x 8 strips (k_fv1 fv1_strip); tact bit 1 marks them, stile lists them
-    uint32_t* stile;
-    int strips;           // strip path enabled (SWAMP_FV1_STRIPS=1; measured slower on B200)
-    int quad;             // sibling-quad path (SWAMP_FV1_QUAD=1; measured slower on B200)
-    int fv1_pf;           // FV1 prefetch of the next iteration's own cells: 0 off, 1 L2, 2 L1
     Ctl* ctl_mirror;      // one partition: the host's pinned Ctl mirror (UVA), written at the step's end
     uint32_t fv1_tail16;  // FV1 STAGE 5: sixteenths of the grid-stride windows taken dynamically at the end
     // Morton-subtree partitions: this partition owns level-R
@@ -1179,218 +1170,6 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
     stamp(5);
 }
 
-// K1, persistent and double-buffered: ~2 CTAs per SM loop over the
-// subtrees; while subtree j is encoded, subtree j + stride's flags and
-// values arrive by TMA bulk copies and, as soon as its level-(L-2) flags are
-// in, its level-(L-1) children by per-thread cp.async (only under
-// previous-tree parents). Level L-2 is encoded thread-per-child (conflict-
-// free shared-memory reads) with quad shuffles, levels L-3..R as in
-// k_encode_step. Same arithmetic as k_encode_step.
-constexpr int kK1Stages = 2;
-__device__ __forceinline__ void cp_async_wait_group0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-
-__device__ __forceinline__ Enc encode_lanes_t(double4 v, const double* thr4) {
-    const int lane = threadIdx.x & 31;
-    auto red = [&](double x) {
-        const double x1 = __shfl_sync(kFull, x, (lane + 1) & 31);
-        const double x2 = __shfl_sync(kFull, x, (lane + 2) & 31);
-        const double x3 = __shfl_sync(kFull, x, (lane + 3) & 31);
-        return red4(x, x1, x2, x3);
-    };
-    const Red h = red(v.x);
-    const Red qx = red(v.y);
-    const Red qy = red(v.z);
-    const Red z = red(v.w);
-    Enc e;
-    e.flow = sig_q(h.dmax, thr4[0]) || sig_q(qx.dmax, thr4[1]) || sig_q(qy.dmax, thr4[2]);
-    e.par = make_double4(h.par, qx.par, qy.par, z.par);
-    e.zflag = false;
-    return e;
-}
-
-template <int KT>
-__global__ void __launch_bounds__(kThreads, 2) k_encode_pipe(Params P, Ctl* ctl) {
-    pdl_wait();
-    pdl_trigger();
-    __shared__ __align__(8) unsigned long long mbar[kK1Stages];
-    if (threadIdx.x == 0) {
-        mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
-    }
-    const Head hd = cta_head(ctl, P, false);  // (its barrier also publishes the mbarrier inits)
-    if (!hd.active) return;
-    tl_start(ctl, hd.buf, 0);
-    extern __shared__ __align__(128) uint8_t sm1[];
-    __shared__ unsigned s_red[32];
-    __shared__ double s_thr[kMaxL][4];
-    stage_thresholds(P, s_thr);
-    const int p = hd.parity;
-    double4* buf = P.cells[p];
-    const uint8_t* sigp = P.sig[p];
-    const int L = P.L, R = P.R;
-    const int K = KT ? KT : P.K;
-    const int k2 = K - 2;                               // tile level of L-2 (K >= 2 here)
-    const uint32_t c2 = 1u << (2 * k2);                 // level-(L-2) cells of a subtree
-    const uint32_t nch = 4u * c2;                       // level-(L-1) children
-    const uint32_t nv = lo(K - 1, 0);                   // cells on levels R..L-2
-    const uint32_t sl = slo(K);
-    const size_t stage_bytes = 32u * (nch + nv) + 3u * sl + 16u;
-    auto st_ch = [&](int s) { return reinterpret_cast<double4*>(sm1 + s * stage_bytes); };
-    auto st_sv = [&](int s) { return reinterpret_cast<double4*>(sm1 + s * stage_bytes + 32u * nch); };
-    auto st_sf = [&](int s) { return sm1 + s * stage_bytes + 32u * (nch + nv); };
-    auto st_sd = [&](int s) { return st_sf(s) + sl; };
-    auto st_so = [&](int s) { return st_sf(s) + 2u * sl; };
-    auto st_small = [&](int s) { return reinterpret_cast<uint32_t*>(st_sf(s) + 3u * sl); };  // level-R words
-
-    // bulk copies of subtree j into stage s: flags of levels R+2..L-1, values
-    // of levels R+1..L-2 (one thread); the level-R / R+1 flag words by cp.async
-    auto issue_bulk = [&](uint32_t j, int s) {
-        if (threadIdx.x == 0) {
-            unsigned bytes = 0;
-            for (int k = 2; k < K; ++k) bytes += 2u << (2 * k);
-            for (int k = 1; k <= K - 2; ++k) bytes += 32u << (2 * k);
-            mbar_expect_tx(&mbar[s], bytes);
-            for (int k = 2; k < K; ++k) {
-                const uint32_t cnt = 1u << (2 * k);
-                const unsigned long long g = slo(R + k) + static_cast<unsigned long long>(j) * cnt;
-                bulk_g2s(st_sf(s) + slo(k), sigp + g, cnt, &mbar[s]);
-                bulk_g2s(st_sd(s) + slo(k), P.dem + g, cnt, &mbar[s]);
-            }
-            for (int k = 1; k <= K - 2; ++k) {
-                const uint32_t cnt = 1u << (2 * k);
-                bulk_g2s(st_sv(s) + lo(k, 0), buf + cbase(R + k) + static_cast<unsigned long long>(j) * cnt,
-                         32u * cnt, &mbar[s]);
-            }
-        }
-        if (threadIdx.x == 32) {
-            cp_async4(st_sf(s) + slo(1), sigp + slo(R + 1) + 4ull * j);
-            cp_async4(st_sd(s) + slo(1), P.dem + slo(R + 1) + 4ull * j);
-            cp_async4(st_small(s), sigp + slo(R) + (j & ~3u));
-            cp_async4(st_small(s) + 1, P.dem + slo(R) + (j & ~3u));
-        }
-    };
-    // children of subtree j's previous-tree level-(L-2) cells (after its flags)
-    auto issue_children = [&](uint32_t j, int s) {
-        const uint8_t* f2 = st_sf(s) + slo(k2);
-        for (uint32_t t = threadIdx.x; t < c2; t += kThreads)
-            if (f2[t]) {
-                const uint8_t* g = reinterpret_cast<const uint8_t*>(buf + cbase(L - 1) + ((j * c2 + t) << 2));
-                uint8_t* d = reinterpret_cast<uint8_t*>(st_ch(s) + 4u * t);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) cp_async16(d + 16 * q, g + 16 * q);
-            }
-        cp_async_commit();
-    };
-
-    unsigned tree = 0;
-    const uint32_t stride = gridDim.x;
-    uint32_t j = P.tile_lo + blockIdx.x;
-    unsigned ph[kK1Stages] = {0u, 0u};
-    int s = 0;
-    if (j < P.tile_hi) {
-        issue_bulk(j, 0);
-        mbar_wait(&mbar[0], 0);
-        ph[0] ^= 1u;
-        issue_children(j, 0);
-    }
-    for (; j < P.tile_hi; j += stride, s ^= 1) {
-        const uint32_t jn = j + stride;
-        const bool more = jn < P.tile_hi;
-        if (more) issue_bulk(jn, s ^ 1);
-        cp_async_wait_group0();  // this subtree's children and small flag words
-        __syncthreads();
-        double4* sv = st_sv(s);
-        uint8_t* sf = st_sf(s);
-        uint8_t* sd = st_sd(s);
-        uint8_t* so = st_so(s);
-        if (threadIdx.x == 0) {
-            const uint32_t* w = st_small(s);
-            sf[0] = (w[0] >> (8 * (j & 3u))) & 0xFFu;
-            sd[0] = (w[1] >> (8 * (j & 3u))) & 0xFFu;
-        }
-        // ---- level L-1: cells off the previous tree only get pre = DEM | (eps == 0)
-        {
-            const int k = K - 1;
-            const uint32_t cnt = 1u << (2 * k);
-            const uint32_t zero = (0.0 >= s_thr[L - 1][3]) ? 0x01010101u : 0u;
-            const unsigned long long g = slo(L - 1) + static_cast<unsigned long long>(j) * cnt;
-            for (uint32_t c = 4u * threadIdx.x; c < cnt; c += 4u * kThreads) {
-                const uint32_t f = *reinterpret_cast<const uint32_t*>(sf + slo(k) + c);
-                if (f == 0x01010101u) continue;
-                const uint32_t v = zero | *reinterpret_cast<const uint32_t*>(sd + slo(k) + c);
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (!byte_of(f, q)) P.pre[g + c + q] = byte_of(v, q) ? 1 : 0;
-            }
-        }
-        // ---- level L-2: thread per child, quads reduce by shuffles
-        {
-            const double4* ch = st_ch(s);
-            const int lane = threadIdx.x & 31;
-            const double* thr = s_thr[L - 2];
-            const bool zero2 = 0.0 >= thr[3];
-            for (uint32_t c = threadIdx.x; c < nch; c += kThreads) {  // warp-uniform trip count (nch % 32 == 0 or < 32)
-                const uint32_t t = c >> 2;
-                const Enc e = encode_lanes_t(ch[c], thr);
-                if ((lane & 3) == 0) {
-                    bool flow = zero2;
-                    if (sf[slo(k2) + t]) {
-                        flow = e.flow;
-                        sv[lo(k2, 0) + t] = e.par;
-                        ++tree;
-                    }
-                    so[slo(k2) + t] = (flow || sd[slo(k2) + t]) ? 1 : 0;
-                }
-            }
-        }
-        __syncthreads();  // children of stage s consumed; level L-2 results visible
-        if (more) {       // the next subtree's children fly while levels L-3..R are encoded
-            mbar_wait(&mbar[s ^ 1], ph[s ^ 1]);
-            ph[s ^ 1] ^= 1u;
-            issue_children(jn, s ^ 1);
-        }
-        // ---- levels L-3 .. R in shared memory
-#pragma unroll
-        for (int k = (KT ? KT : kMaxL) - 3; k >= 0; --k) {
-            if (!KT && k > K - 3) continue;
-            const int n = R + k;
-            const uint32_t cnt = 1u << (2 * k);
-            for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads) {
-                bool flow = 0.0 >= s_thr[n][3];
-                if (sf[slo(k) + pi]) {
-                    const uint32_t c0 = lo(k + 1, 0) + 4u * pi;
-                    const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
-                    const Enc e = encode_children_t(c, s_thr[n]);
-                    flow = e.flow;
-                    sv[lo(k, 0) + pi] = e.par;
-                    ++tree;
-                }
-                so[slo(k) + pi] = (flow || sd[slo(k) + pi]) ? 1 : 0;
-            }
-            __syncthreads();
-        }
-        // ---- stores: re-encoded values (previous-tree cells), pre-band flags of levels R..L-2
-        for (int k = 0; k <= K - 2; ++k) {
-            const uint32_t cnt = 1u << (2 * k);
-            const unsigned long long jb = static_cast<unsigned long long>(j) * cnt;
-            for (uint32_t pi = threadIdx.x; pi < cnt; pi += kThreads)
-                if (sf[slo(k) + pi]) st4(buf + cbase(R + k) + jb + pi, sv[lo(k, 0) + pi]);
-            if (cnt >= 4) {
-                for (uint32_t q = 4u * threadIdx.x; q < cnt; q += 4u * kThreads)
-                    *reinterpret_cast<uint32_t*>(P.pre + slo(R + k) + jb + q) =
-                        *reinterpret_cast<const uint32_t*>(so + slo(k) + q);
-            } else if (threadIdx.x == 0) {
-                P.pre[slo(R) + jb] = so[0];
-            }
-        }
-        __syncthreads();  // stage s free for subtree j + 2 stride
-    }
-    const unsigned tsum = block_sum(tree, s_red);
-    if (threadIdx.x == 0 && tsum) atomicAdd(&ctl->cnt_tree, (unsigned long long)tsum);
-    tl_end(ctl, hd.buf, 0);
-}
-
 // band (D3) of cell (n, m) from the pre-band flags (flow | DEM);
 // `pre_at(level, morton)` reads a pre flag (global or shared memory)
 template <class PreAt>
@@ -2022,9 +1801,6 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         }
         __syncthreads();
     }
-    const uint32_t full = 1u << (2 * P.K);  // level-L leaves of a fully refined subtree
-    const bool strips = !EXPORT && P.strips && P.G == 1 && P.K == 6;
-    unsigned nst = 0;                       // this thread's strip-path subtrees
     for (uint32_t t = a; t < b; ++t) {
         unsigned ca, cb;
         counts(t, ca, cb);
@@ -2106,8 +1882,6 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         // FV1 dry shortcut: subtree t is active if it or a face-adjacent
         // subtree holds a wet cell, or it touches an inflow edge; clear the
         // flags FV1 sets next
-        unsigned ca, cb;
-        counts(t, ca, cb);
         uint8_t act = swet[t];
 #pragma unroll
         for (int d = 0; d < 4; ++d) {
@@ -2115,24 +1889,8 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
             if (nb == zo::kNone) act |= (P.bc[d] == 2) ? 1 : 0;
             else act |= swet[nb];
         }
-        const uint8_t st = (strips && act && ca == full) ? 1 : 0;
-        P.tact[t] = act | (st << 1);
+        P.tact[t] = act;
         P.wet[tbuf ^ 1][t] = 0;
-        nst += st;
-    }
-    // ---- the strip-path subtree list (Morton order)
-    if (strips) {
-        unsigned tot;
-        unsigned os = block_exscan(nst, s_red, &tot);
-        if (nst)
-            for (uint32_t t = a; t < b; ++t)
-                if (P.tact[t] & 2u) P.stile[os++] = t;  // (this thread's own writes: ordered)
-        if (threadIdx.x == 0) {
-            ctl->n_stile = tot;
-            ctl->dbg[40] += tot;  // diagnostics: strip-path subtrees so far
-        }
-    } else if (threadIdx.x == 0) {
-        ctl->n_stile = 0;
     }
     __syncthreads();  // s_off complete
     // ---- final flags of levels < R, projection (D4) of top cells on the tree
@@ -2174,7 +1932,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
 // top), wait for the top's offsets, then decode and emit
 template <bool EXPORT, int KT>
 __device__ void k3_tile(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long long epoch, uint32_t j, uint8_t* sm,
-                        const Probe& stamp, bool staged = false, uint8_t q0_staged = 0) {
+                        const Probe& stamp) {
     __shared__ unsigned s_red[32];
     __shared__ uint32_t s_top[4];
     double4* buf = P.cells[p];
@@ -2189,9 +1947,7 @@ __device__ void k3_tile(const Params& P, Ctl* ctl, int p, int tbuf, unsigned lon
     uint32_t* src = reinterpret_cast<uint32_t*>(sp + slo(K));  // [ncell] projection sources
     (void)ncell;
 
-    if (staged) {  // fused K2+K3: current flags left by k2_tile, previous ones prefetched
-        if (threadIdx.x == 0) sp[0] = q0_staged;
-    } else {
+    {
         const uint8_t c0 = stage_tile_flags(sc, sigc, P, j);
         const uint8_t q0 = EXPORT ? 0 : stage_tile_flags(sp, sigp, P, j);
         cp_async_wait_all();
@@ -2379,55 +2135,6 @@ __device__ void k3_tile(const Params& P, Ctl* ctl, int p, int tbuf, unsigned lon
     }
     if (!EXPORT) tl_end(ctl, tbuf, 2);
     stamp(6);
-}
-
-// K2 and K3 fused (one partition, every CTA resident — host-checked): block
-// 0 re-encodes levels < R, waits until every subtree CTA has finished its K2
-// part (counter), then does K3's top work and publishes; a subtree CTA runs
-// K2 and goes straight on with K3, its final flags still in shared memory and
-// its previous-tree flags prefetched during K2. One launch and one staging
-// round trip less.
-template <int KT>
-__global__ void __launch_bounds__(kThreads, 7) k_band_traverse(Params P, Ctl* ctl) {
-    pdl_wait();
-    pdl_trigger();
-    const unsigned long long t_entry = gtimer();
-    const Head hd = cta_head(ctl, P, false);
-    if (!hd.active) return;
-    extern __shared__ __align__(16) uint8_t smf[];
-    tl_start(ctl, hd.buf, 1);
-    const unsigned long long ep = 2ull * static_cast<unsigned long long>(hd.step) + 2ull;
-    const Probe stamp(ctl, 16);
-    stamp(7, t_entry);
-    if (blockIdx.x == 0) {
-        if (P.top_mode == 1) encode_top_staged(P, ctl, hd.parity, smf);
-        if (threadIdx.x == 0) {
-            const unsigned long long t0 = gtimer();
-            while (ld_acquire_u64(&ctl->k2_done) < P.tiles_per_part) {
-                __nanosleep(64);
-                if (gtimer() - t0 > 2000000000ull) {  // never expected: fail instead of hanging
-                    report_error(ctl, kErrBarrier, 0, 0, kStageBand);
-                    break;
-                }
-            }
-            ctl->k2_done = 0ull;  // every subtree has counted; none counts again in this launch
-        }
-        __syncthreads();
-        tl_start(ctl, hd.buf, 2);
-        k3_top<false>(P, ctl, hd.parity, hd.buf, ep, smf, stamp, P.top_band != 0);
-        return;
-    }
-    const int K = KT ? KT : P.K;
-    const uint32_t j = P.tile_lo + blockIdx.x - 1u;
-    uint8_t* sp = smf + 2u * slo(K);
-    const uint8_t q0 = stage_tile_flags(sp, P.sig[hd.parity], P, j);  // completes with k2_tile's wait
-    k2_tile<KT>(P, ctl, hd, j, smf);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(&ctl->k2_done, 1ull);
-    }
-    k3_tile<false, KT>(P, ctl, hd.parity, hd.buf, ep, j, smf + slo(K), stamp, true, q0);
 }
 
 // epoch: 0 = hot path (2 step + 2, unique per step; the host clears the flag
@@ -2679,268 +2386,18 @@ __device__ __forceinline__ double4* covering(const Params& P, int cur, int k, ui
     return cell_ptr(P, cur, k, mm);
 }
 
-__device__ __forceinline__ CellV shfl_cell(const CellV& c, int src) {
-    CellV o;
-    o.h = __shfl_sync(kFull, c.h, src);
-    o.qx = __shfl_sync(kFull, c.qx, src);
-    o.qy = __shfl_sync(kFull, c.qy, src);
-    o.z = __shfl_sync(kFull, c.z, src);
-    o.ux = __shfl_sync(kFull, c.ux, src);
-    o.uy = __shfl_sync(kFull, c.uy, src);
-    o.c = __shfl_sync(kFull, c.c, src);
-    return o;
-}
-
-// Strip path of FV1 (one warp): strip q (0..15) of a fully refined 64 x 64
-// subtree `tile` = 32 columns (one per lane) x 8 rows of level-L leaves,
-// marched south to north. Every cell's velocities / celerity are formed once
-// (make_cell) and every face flux once: the x-face between lanes x-1 and x is
-// computed by lane x and handed to lane x-1 by a shuffle, the y-face above row
-// r is the y-face below row r+1. face() and fv1_finish() are the per-leaf
-// path's, with the same (left, right) arguments, so the bits are the same.
-// The strip's outside neighbours (its W and E columns, the rows below and
-// above: the same-level cell, the coarser covering leaf of SPEC.md:248, or a
-// boundary ghost) are fetched once into the warp's shared slots `bsm`; the
-// strip's own rows need no flags (every level-L cell of the subtree is a
-// leaf) and are prefetched two rows ahead. Also the fused level-(L-1)
-// re-encode of the next step (quads = lane pairs x row pairs), the CFL rate,
-// the wet marks.
-constexpr int kStripSlots = 80;  // 8 W + 8 E + 32 S + 32 N neighbours
-__device__ void fv1_strip(const Params& P, Ctl* ctl, const double4* __restrict__ cur, double4* __restrict__ nxt,
-                          const uint8_t* __restrict__ sigc, const double (*thr)[4], uint32_t tile, int q, double dt,
-                          double inflow, int tbuf, double4* bsm, double& mx, unsigned& tree) {
-    const int L = P.L;
-    const int lane = threadIdx.x & 31;
-    const PhysParams& ph = P.phys;
-    const double idx = inv_dx_of(P, L);
-    const uint32_t Xs = (zo::compact_bits(tile) << 6) + (static_cast<uint32_t>(q & 1) << 5);
-    const uint32_t X = Xs + lane;
-    const uint32_t Y0 = (zo::compact_bits(tile >> 1) << 6) + (static_cast<uint32_t>(q >> 1) << 3);
-    const double4* base = cur + cbase(L);
-    // ---- prologue: the strip's outside neighbours (slot k: 0..7 W of row k,
-    //      8..15 E of row k-8, 16..47 S of column k-16, 48..79 N of column
-    //      k-48); a ghost is marked by one NaN bit pattern in h (its state needs
-    //      the cell)
-    {
-        uint32_t nmk[3];
-        int dk[3];
-        uint8_t f[3];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const int k = lane + 32 * i;
-            uint32_t cx, cy;
-            int d;
-            if (k < 8) { cx = Xs; cy = Y0 + k; d = 0; }
-            else if (k < 16) { cx = Xs + 31u; cy = Y0 + (k - 8); d = 1; }
-            else if (k < 48) { cx = Xs + (k - 16); cy = Y0; d = 3; }
-            else { cx = Xs + (k - 48); cy = Y0 + 7u; d = 2; }
-            dk[i] = d;
-            nmk[i] = (k < kStripSlots) ? zo::neighbour_dev(L, zo::interleave(cx, cy), static_cast<zo::Direction>(d))
-                                       : zo::kNone;
-            f[i] = (nmk[i] != zo::kNone) ? sigc[slo(L - 1) + (nmk[i] >> 2)] : 1;
-        }
-        double4 v[3];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            if (nmk[i] != zo::kNone) {
-                const double4* src = f[i] ? base + nmk[i] : covering_local(P, cur, sigc, L - 1, nmk[i] >> 2);
-                v[i] = ld4_nc(src);
-            } else {
-                v[i] = make_double4(__longlong_as_double(0x7FF8DEAD00000000ll), 0.0, 0.0, 0.0);
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-            if (lane + 32 * i < kStripSlots) bsm[lane + 32 * i] = v[i];
-        (void)dk;
-    }
-    __syncwarp();
-    // outside neighbour in direction d of `own` from slot k
-    auto outside = [&](int k, int d, const CellV& own) -> CellV {
-        const double4 v = bsm[k];
-        if (__double_as_longlong(v.x) == 0x7FF8DEAD00000000ll) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, ph);
-        return make_cell(v, ph);
-    };
-    uint32_t m = zo::interleave(X, Y0);
-    double4 raw1 = ld4_nc(base + zo::interleave(X, Y0 + 1u));
-    CellV own = make_cell(ld4_nc(base + m), ph);
-    double FS[3], hRsS;  // the face below the current row (own on its north side)
-    {
-        const CellV sc = outside(16 + lane, 3, own);
-        double hL;
-        face(sc, own, false, ph, FS, hL, hRsS);
-    }
-    bool wet = false;
-    double4 prev = make_double4(0.0, 0.0, 0.0, 0.0);  // this lane's updated cell of the row below
-#pragma unroll 1
-    for (int r = 0; r < 8; ++r) {
-        double4 raw2 = raw1;
-        if (r + 2 <= 7) raw2 = ld4_nc(base + zo::interleave(X, Y0 + static_cast<uint32_t>(r) + 2u));
-        const CellV north = (r < 7) ? make_cell(raw1, ph) : outside(48 + lane, 2, own);
-        CellV w = shfl_cell(own, (lane + 31) & 31);
-        if (lane == 0) w = outside(r, 0, own);
-        const double h = own.h, hh = h * h;
-        double FW[3], hLsW, hRsW;
-        face(w, own, true, ph, FW, hLsW, hRsW);
-        double FE[3], hLsE;
-        FE[0] = __shfl_sync(kFull, FW[0], (lane + 1) & 31);
-        FE[1] = __shfl_sync(kFull, FW[1], (lane + 1) & 31);
-        FE[2] = __shfl_sync(kFull, FW[2], (lane + 1) & 31);
-        hLsE = __shfl_sync(kFull, hLsW, (lane + 1) & 31);
-        if (lane == 31) {
-            const CellV e = outside(8 + r, 1, own);
-            double hR;
-            face(own, e, true, ph, FE, hLsE, hR);
-        }
-        double FN[3], hLsN, hRsN;
-        face(own, north, false, ph, FN, hLsN, hRsN);
-        // the per-leaf path's differences (fv1_cell_seq)
-        const double FE1 = FE[1] + (ph.half_g * (hh - (hLsE * hLsE)));
-        const double FW1 = FW[1] + (ph.half_g * (hh - (hRsW * hRsW)));
-        const double GN1 = FN[1] + (ph.half_g * (hh - (hLsN * hLsN)));
-        const double GS1 = FS[1] + (ph.half_g * (hh - (hRsS * hRsS)));
-        double hn, qxn, qyn;
-        fv1_finish(own, FE[0] - FW[0], FE1 - FW1, FE[2] - FW[2], FN[0] - FS[0], GN1 - GS1, FN[2] - FS[2], idx, dt,
-                   ph, hn, qxn, qyn);
-        if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))
-            report_error(ctl, kErrNonFinite, zo::z_of(L, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2), kStageFV1);
-        const double4 o = make_double4(hn, qxn, qyn, own.z);
-        st4(nxt + cbase(L) + m, o);
-        const double c = cfl_rate(hn, qxn, qyn, idx, ph);
-        mx = c > mx ? c : mx;
-        wet = wet || !(hn < ph.hdry);
-        // next step's re-encode of level L-1: lane pair (x even, x + 1) x rows (r - 1, r)
-        if (r & 1) {
-            double4 ch[4];
-            ch[0] = prev;
-            ch[1] = make_double4(__shfl_sync(kFull, prev.x, (lane + 1) & 31), __shfl_sync(kFull, prev.y, (lane + 1) & 31),
-                                 __shfl_sync(kFull, prev.z, (lane + 1) & 31), __shfl_sync(kFull, prev.w, (lane + 1) & 31));
-            ch[2] = o;
-            ch[3] = make_double4(__shfl_sync(kFull, o.x, (lane + 1) & 31), __shfl_sync(kFull, o.y, (lane + 1) & 31),
-                                 __shfl_sync(kFull, o.z, (lane + 1) & 31), __shfl_sync(kFull, o.w, (lane + 1) & 31));
-            if ((lane & 1) == 0) {
-                const Enc e2 = encode_children_t(ch, thr[L - 1]);
-                const uint32_t pm = m >> 2;
-                st4(nxt + cbase(L - 1) + pm, e2.par);
-                const unsigned long long fi = slo(L - 1) + pm;
-                P.pre[fi] = (e2.flow || P.dem[fi]) ? 1 : 0;
-                ++tree;
-            }
-        }
-        prev = o;
-        // the face above is the next row's face below
-        FS[0] = FN[0];
-        FS[1] = FN[1];
-        FS[2] = FN[2];
-        hRsS = hRsN;
-        own = north;
-        raw1 = raw2;
-        m = zo::interleave(X, Y0 + static_cast<uint32_t>(r) + 1u);
-    }
-    if (__any_sync(kFull, wet) && lane == 0) P.wet[tbuf ^ 1][tile] = 1;
-    __syncwarp();  // bsm reused by the warp's next strip
-}
-
-// FV1 of one level-L leaf whose sibling quadruple sits in lanes 4k..4k+3
-// (child c = lane & 3 at (c & 1, c >> 1)): the two siblings' cell states
-// come by shuffles, only the two outside neighbours are gathered, and each
-// lane computes one of the quad's four inner faces (c0: c0|c1, c3: c2|c3 in
-// x; c1: c1|c3, c2: c0|c2 in y) and receives the other from its partner —
-// 3 faces, 3 make_cell and 2 gathers per leaf instead of 4, 5, 4. face() and
-// fv1_finish() with the per-leaf path's (left, right) arguments: same bits.
-// Every lane of the warp must call it (shuffles); `skip` lanes (dry subtree,
-// strip path) only take part in the exchange.
-__device__ __forceinline__ void fv1_quad(const Params& P, const double4* __restrict__ cur,
-                                         const uint8_t* __restrict__ sigc, uint32_t m, const double4 o4, bool skip,
-                                         double dt, double inflow, double& hn, double& qxn, double& qyn) {
-    const int L = P.L;
-    const int lane = threadIdx.x & 31;
-    const int c = lane & 3;
-    const PhysParams& ph = P.phys;
-    // outside neighbours: W or E, S or N
-    const int dx = (c & 1) ? 1 : 0, dy = (c & 2) ? 2 : 3;
-    uint32_t nmx = zo::kNone, nmy = zo::kNone;
-    double4 rx = make_double4(0.0, 0.0, 0.0, 0.0), ry = rx;
-    if (!skip) {
-        nmx = zo::neighbour_dev(L, m, static_cast<zo::Direction>(dx));
-        nmy = zo::neighbour_dev(L, m, static_cast<zo::Direction>(dy));
-        const uint8_t fx = (nmx != zo::kNone) ? sigc[slo(L - 1) + (nmx >> 2)] : 1;
-        const uint8_t fy = (nmy != zo::kNone) ? sigc[slo(L - 1) + (nmy >> 2)] : 1;
-        const double4* sx = fx ? cur + cbase(L) + nmx : covering_local(P, cur, sigc, L - 1, nmx >> 2);
-        const double4* sy = fy ? cur + cbase(L) + nmy : covering_local(P, cur, sigc, L - 1, nmy >> 2);
-        if (nmx != zo::kNone) rx = ld4_nc(sx);
-        if (nmy != zo::kNone) ry = ld4_nc(sy);
-    }
-    const CellV own = make_cell(o4, ph);
-    const CellV px = shfl_cell(own, lane ^ 1), py = shfl_cell(own, lane ^ 2);
-    // this lane's inner face
-    const bool ix = (c == 0 || c == 3);        // x pair (c0|c1 or c2|c3), else y pair
-    const bool own_left = (c == 0 || c == 1);  // own on the west / south side
-    double Fi[3], hLi, hRi;
-    {
-        const CellV& q = ix ? px : py;
-        if (own_left) face(own, q, ix, ph, Fi, hLi, hRi);
-        else face(q, own, ix, ph, Fi, hLi, hRi);
-    }
-    // the other inner face from its owner (c0 <- c2, c1 <- c0, c2 <- c3, c3 <- c1)
-    const int src = ix ? (lane ^ 2) : (lane ^ 1);
-    double Fr[3];
-    Fr[0] = __shfl_sync(kFull, Fi[0], src);
-    Fr[1] = __shfl_sync(kFull, Fi[1], src);
-    Fr[2] = __shfl_sync(kFull, Fi[2], src);
-    const double hLr = __shfl_sync(kFull, hLi, src), hRr = __shfl_sync(kFull, hRi, src);
-    if (skip) return;
-    bool all_dry = own.h < ph.hdry && px.h < ph.hdry && py.h < ph.hdry;
-    all_dry = all_dry && ((nmx != zo::kNone) ? rx.x < ph.hdry : P.bc[dx] != 2);
-    all_dry = all_dry && ((nmy != zo::kNone) ? ry.x < ph.hdry : P.bc[dy] != 2);
-    if (all_dry) {  // the dry-neighbourhood result (same bits as the general path)
-        hn = (o4.x < 0.0) ? 0.0 : o4.x;
-        qxn = 0.0;
-        qyn = 0.0;
-        return;
-    }
-    const CellV ex = (nmx != zo::kNone) ? make_cell(rx, ph) : boundary_cell(own, P.bc[dx], dx, inflow, P.inflow_mode, ph);
-    const CellV ey = (nmy != zo::kNone) ? make_cell(ry, ph) : boundary_cell(own, P.bc[dy], dy, inflow, P.inflow_mode, ph);
-    double Fox[3], Foy[3], hL, hR, hox, hoy;  // outside faces and own side's reconstructed depth
-    if (dx == 1) { face(own, ex, true, ph, Fox, hL, hR); hox = hL; }   // E: own left
-    else { face(ex, own, true, ph, Fox, hL, hR); hox = hR; }          // W: own right
-    if (dy == 2) { face(own, ey, false, ph, Foy, hL, hR); hoy = hL; }  // N: own south
-    else { face(ey, own, false, ph, Foy, hL, hR); hoy = hR; }         // S: own north
-    // inner faces as seen by this lane: x inner (c0: E = own, c1: W = recv,
-    // c2: E = recv, c3: W = own), y inner (c0: N = recv, c1: N = own,
-    // c2: S = own, c3: S = recv); own side depth hL when own is west/south
-    // (scalar selects: no pointers into register arrays, no local memory)
-    const double Fx0 = ix ? Fi[0] : Fr[0], Fx1 = ix ? Fi[1] : Fr[1], Fx2 = ix ? Fi[2] : Fr[2];
-    const double Fy0 = ix ? Fr[0] : Fi[0], Fy1 = ix ? Fr[1] : Fi[1], Fy2 = ix ? Fr[2] : Fi[2];
-    const double hxi = (c & 1) ? (ix ? hRi : hRr) : (ix ? hLi : hLr);  // c1, c3 right of the x face
-    const double hyi = (c & 2) ? (ix ? hRr : hRi) : (ix ? hLr : hLi);  // c2, c3 north of the y face
-    const bool ce = (c & 1) != 0, cn = (c & 2) != 0;
-    const double FE[3] = {ce ? Fox[0] : Fx0, ce ? Fox[1] : Fx1, ce ? Fox[2] : Fx2};
-    const double FW[3] = {ce ? Fx0 : Fox[0], ce ? Fx1 : Fox[1], ce ? Fx2 : Fox[2]};
-    const double FN[3] = {cn ? Foy[0] : Fy0, cn ? Foy[1] : Fy1, cn ? Foy[2] : Fy2};
-    const double FS[3] = {cn ? Fy0 : Foy[0], cn ? Fy1 : Foy[1], cn ? Fy2 : Foy[2]};
-    const double hE = ce ? hox : hxi, hW = ce ? hxi : hox;
-    const double hN = cn ? hoy : hyi, hS = cn ? hyi : hoy;
-    const double h = own.h, hh = h * h;
-    const double FE1 = FE[1] + (ph.half_g * (hh - (hE * hE)));
-    const double FW1 = FW[1] + (ph.half_g * (hh - (hW * hW)));
-    const double GN1 = FN[1] + (ph.half_g * (hh - (hN * hN)));
-    const double GS1 = FS[1] + (ph.half_g * (hh - (hS * hS)));
-    fv1_finish(own, FE[0] - FW[0], FE1 - FW1, FE[2] - FW[2], FN[0] - FS[0], GN1 - GS1, FN[2] - FS[2],
-               inv_dx_of(P, L), dt, ph, hn, qxn, qyn);
-}
-
 // FV1 over the leaf list: persistent grid-stride, one thread per
 // leaf; reads the current buffer, writes leaf slots of the other (D15).
-template <bool UNIFORM, int MINB = 2, bool PART = false, bool STRIPS = false, bool QUAD = false, bool INA = false,
-          int STAGE = 0>
-__global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
+// STAGE 0: next iteration's own cell prefetched into L2; 2: loaded into
+// registers an iteration ahead with its subtree activity; 3: also the
+// neighbours' parent-level flags; 5: 3 + tail balancing.
+template <bool UNIFORM, bool PART = false, bool INA = false, int STAGE = 0>
+__global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     pdl_wait();
     pdl_trigger();
     // control words, read once per CTA (line 0 of Ctl)
     __shared__ double s_td[2];
-    __shared__ uint32_t s_u[7];
-    __shared__ double s_thr[kMaxL][4];
+    __shared__ uint32_t s_u[6];
     if (threadIdx.x == 0) {
         const volatile Ctl* vc = ctl;
         s_td[0] = vc->t;
@@ -2948,9 +2405,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
         s_u[0] = static_cast<uint32_t>(vc->parity);
         s_u[1] = static_cast<uint32_t>(vc->step & 1);
         s_u[2] = vc->a_lo; s_u[3] = vc->a_hi; s_u[4] = vc->b_lo; s_u[5] = vc->b_hi;
-        s_u[6] = STRIPS ? vc->n_stile : 0u;
     }
-    if (STRIPS) stage_thresholds(P, s_thr);
     __syncthreads();
     const double t = s_td[0], dt = s_td[1];
     if (!(t < P.t_end)) return;
@@ -2972,15 +2427,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     unsigned tree = 0;
     const uint32_t stride = gridDim.x * kThreads;
     // warp-uniform trip count: every lane runs every iteration (shuffles below)
-    // strip path first: 16 strips per fully refined active subtree
-    if (STRIPS && !UNIFORM && !PART) {
-        const uint32_t nwarps = gridDim.x * (kThreads / 32);
-        const uint32_t ns = 16u * s_u[6];
-        extern __shared__ double4 s_bnd[];  // kThreads / 32 x kStripSlots when P.strips (launch smem)
-        for (uint32_t s = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); s < ns; s += nwarps)
-            fv1_strip(P, ctl, cur, nxt, sigc, s_thr, P.stile[s >> 4], static_cast<int>(s & 15u), dt, inflow, tbuf,
-                      s_bnd + (threadIdx.x >> 5) * kStripSlots, mx, tree);
-    }
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
     // STAGE 5 (= 3 + tail balancing): the last fv1_tail16 / 16 of the windows
     // are taken one warp-iteration (32 leaves) at a time from a per-step
@@ -3010,7 +2456,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
     }
     // STAGE 2: the next iteration's own cell and subtree activity are loaded
     // into registers one iteration ahead (instead of an L2 prefetch)
-    const int pf = (STAGE >= 2) ? 1 : P.fv1_pf;
+    constexpr int pf = 1;
     // leaf ids two iterations ahead; the next iteration's own cell is
     // prefetched (no registers held) while this one computes: the leaf
     // cells were written a step ago and come from DRAM
@@ -3057,7 +2503,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             m = valid ? i : 0u;
             if (pf && nb1 + lane < N) {
                 const double4* q = cur + cbase(n) + nb1 + lane;
-                if (pf == 2) prefetch_l1(q); else prefetch_l2(q);
+                prefetch_l2(q);
             }
         } else {
             const uint32_t z = valid ? z_next : zo::level_offset(P.L);  // leaf ids prefetched one iteration ahead
@@ -3070,7 +2516,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                     } else {
                         const int n1 = zo::level_of(z_next);
                         const double4* q = cur + cbase(n1) + (z_next - zo::level_offset(n1));
-                        if (pf == 2) prefetch_l1(q); else prefetch_l2(q);
+                        prefetch_l2(q);
                     }
                 }
             } else if (nb1 + lane < N) {
@@ -3079,24 +2525,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
             n = zo::level_of(z);
             m = z - zo::level_offset(n);
         }
-        // subtree activity (bit 0: wet neighbourhood, bit 1: strip path)
+        // subtree activity (bit 0: wet neighbourhood)
         const uint8_t ta = (STAGE >= 2 && !UNIFORM) ? (valid ? ta_k : 1)
                            : ((!UNIFORM && !PART && valid && n >= P.R) ? P.tact[m >> (2 * (n - P.R))] : 1);
-        if (STRIPS && (ta & 2u)) valid = false;  // updated by the strip path above
         double hn = 0.0, qxn = 0.0, qyn = 0.0, zown = 0.0;
-        // a warp of whole sibling quadruples of level-L leaves: the quad path
-        const bool quadw = QUAD && !UNIFORM && !PART && wbase + 32u <= NA;
-        if (quadw) {
-            const double4 o4 = ld4_nc(cur + cbase(n) + m);
-            fv1_quad(P, cur, sigc, m, o4, !valid || ta == 0, dt, inflow, hn, qxn, qyn);
-            if (valid && ta == 0) {  // dry subtree
-                hn = (o4.x < 0.0) ? 0.0 : o4.x;
-                qxn = 0.0;
-                qyn = 0.0;
-            }
-            zown = o4.w;
-        }
-        if (valid && !quadw) {
+        if (valid) {
             // every global read of this leaf is issued before any arithmetic:
             // own cell, the neighbours' parent-level flags, the neighbours
             const double4 o4 = (STAGE >= 2 && !UNIFORM) ? o4_k : ld4_nc(cur + cbase(n) + m);
@@ -3178,28 +2611,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_fv1(Params P, Ctl* ctl) {
                         src[d] = f[d] ? cur + cbase(n) + nm[d] : covering_local(P, cur, sigc, n - 1, nm[d] >> 2);
                 }
             }
-            // STAGE: the neighbours land in shared memory by cp.async (no
-            // registers held across the load; slot [warp][d][lane])
-            __shared__ __align__(16) double4 s_nb[STAGE == 1 ? kThreads / 32 * 4 * 32 : 1];
-            double4 r4s[STAGE == 1 ? 1 : 4];
-            auto nbv = [&](int d) -> double4 {
-                if (STAGE == 1) return s_nb[((threadIdx.x >> 5) * 4 + d) * 32 + lane];
-                return r4s[STAGE == 1 ? 0 : d];
-            };
-            if (STAGE == 1) {
+            double4 r4s[4];
 #pragma unroll
-                for (int d = 0; d < 4; ++d)
-                    if (nm[d] != zo::kNone) {
-                        double4* sl = &s_nb[((threadIdx.x >> 5) * 4 + d) * 32 + lane];
-                        cp_async16(sl, src[d]);
-                        cp_async16(reinterpret_cast<uint8_t*>(sl) + 16, reinterpret_cast<const uint8_t*>(src[d]) + 16);
-                    }
-                cp_async_wait_all();
-            } else {
-#pragma unroll
-                for (int d = 0; d < 4; ++d)
-                    if (nm[d] != zo::kNone) r4s[STAGE == 1 ? 0 : d] = ld4_nc(src[d]);
-            }
+            for (int d = 0; d < 4; ++d)
+                if (nm[d] != zo::kNone) r4s[d] = ld4_nc(src[d]);
+            auto nbv = [&](int d) -> double4 { return r4s[d]; };
             // dry neighbourhood: own cell and every neighbour / ghost below
             // h_dry => every reconstructed depth is 0, every flux 0, the bed
             // corrections cancel pairwise: h stays, q = 0 (the general path

@@ -116,27 +116,23 @@ struct swamp_gpu {
     int fv1_grid = 0;
     int64_t launches_per_step = 0;  // kernel nodes of the one-step graph
     bool mirror_current = false;    // ctl_host holds the state after the last completed step
-    int fv1_minb = 2;  // occupancy variant of k_fv1 (SWAMP_FV1_MINB=3|4 for more CTAs/SM, with spills)
-    // SWAMP_FV1_STAGE=1: neighbours staged in shared memory, 3 CTAs/SM (slower);
-    // 2: own cell and subtree activity loaded an iteration ahead (FV1 69 ->
-    // 66 us); 3: also the neighbours' parent-level flags (65 us; default
-    // below L = 11); 5: 3 + the last grid-stride windows handed out
-    // dynamically (64 us; default from L = 11); 0: L2 prefetch only
+    // k_fv1 STAGE (SWAMP_FV1_STAGE): 2: own cell and subtree activity loaded
+    // an iteration ahead (FV1 69 -> 66 us); 3: also the neighbours'
+    // parent-level flags (65 us; default below L = 11); 5: 3 + the last
+    // grid-stride windows handed out dynamically (64 us; default from L = 11);
+    // 0: L2 prefetch only
     int fv1_stage = 5;
     int num_sms = 0;
-    size_t smem_k1 = 0, smem_k1s = 0, smem_k1p = 0, smem_k2 = 0, smem_k3 = 0;
+    size_t smem_k1 = 0, smem_k1s = 0, smem_k2 = 0, smem_k3 = 0;
     // K3 split into a top launch (alone on its SM) + a subtree launch (one partition)
     void (*k3top)(Params, Ctl*) = nullptr;
     void (*k3tiles)(Params, Ctl*) = nullptr;
     size_t smem_k3top = 0, smem_k3tiles = 0;
-    int k1p_grid = 0;     // persistent K1 (K = 6): CTAs
     // tile kernels, specialised for K = 6 (every L >= 6) or generic
     void (*k1)(Params, Ctl*) = nullptr;
     void (*k2)(Params, Ctl*, int, int) = nullptr;
     void (*k3)(Params, Ctl*, int, unsigned long long) = nullptr;
     void (*k3x)(Params, Ctl*, int, unsigned long long) = nullptr;
-    void (*k23)(Params, Ctl*) = nullptr;  // fused K2+K3 (one partition, every CTA resident), else null
-    size_t smem_k23 = 0;
     unsigned long long export_epoch = 1ull << 62;  // K3 export launches (hot-path epochs are 2 step + 2)
     cudaEvent_t ev[6] = {};
     std::string err;
@@ -237,55 +233,35 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     mark(0);
     if (g->uniform) {
         if (P.has_ina)
-            launch_pdl(hwfv1::k_fv1<true, 2, false, false, false, true>, g->fv1_grid, 0, s, P, g->ctl);
+            launch_pdl(hwfv1::k_fv1<true, false, true>, g->fv1_grid, 0, s, P, g->ctl);
         else
-            launch_pdl(hwfv1::k_fv1<true, 2>, g->fv1_grid, 0, s, P, g->ctl);
+            launch_pdl(hwfv1::k_fv1<true>, g->fv1_grid, 0, s, P, g->ctl);
         for (int k = 1; k < 5; ++k) mark(k);
         return;
     }
-    if (g->k1p_grid)
-        launch_pdl(hwfv1::k_encode_pipe<6>, g->k1p_grid, g->smem_k1p, s, P, g->ctl);
-    else
-        launch_pdl(g->k1, P.n_tiles, g->smem_k1s, s, P, g->ctl);
+    launch_pdl(g->k1, P.n_tiles, g->smem_k1s, s, P, g->ctl);
     if (P.top_mode == 2) launch_pdl(hwfv1::k_encode_top<false>, 1, g->smem_k1, s, P, g->ctl);
     mark(1);
-    if (g->k23) {
-        launch_pdl(g->k23, P.n_tiles + 1, g->smem_k23, s, P, g->ctl);
-        mark(2);
-        mark(3);
+    const int do_top = P.top_mode == 1 ? 1 : 0;
+    launch_pdl(g->k2, P.n_tiles + do_top, g->smem_k2, s, P, g->ctl, 0, do_top);
+    mark(2);
+    if (g->k3top) {
+        launch_pdl(g->k3top, 1, g->smem_k3top, s, P, g->ctl);
+        launch_pdl(g->k3tiles, P.n_tiles, g->smem_k3tiles, s, P, g->ctl);
     } else {
-        const int do_top = P.top_mode == 1 ? 1 : 0;
-        launch_pdl(g->k2, P.n_tiles + do_top, g->smem_k2, s, P, g->ctl, 0, do_top);
-        mark(2);
-        if (g->k3top) {
-            launch_pdl(g->k3top, 1, g->smem_k3top, s, P, g->ctl);
-            launch_pdl(g->k3tiles, P.n_tiles, g->smem_k3tiles, s, P, g->ctl);
-        } else {
-            launch_pdl(g->k3, P.n_tiles + 1, g->smem_k3, s, P, g->ctl, 0, 0ull);
-        }
-        mark(3);
+        launch_pdl(g->k3, P.n_tiles + 1, g->smem_k3, s, P, g->ctl, 0, 0ull);
     }
-    const size_t sm5 = P.strips ? sizeof(double4) * (kThreads / 32) * hwfv1::kStripSlots : 0;
-    if (P.has_ina)  // D16 variant (strips / quad / MINB variants do not handle inactive cells)
-        launch_pdl(hwfv1::k_fv1<false, 2, false, false, false, true>, g->fv1_grid, 0, s, P, g->ctl);
-    else if (P.strips)
-        launch_pdl(hwfv1::k_fv1<false, 2, false, true>, g->fv1_grid, sm5, s, P, g->ctl);
-    else if (P.quad)
-        launch_pdl(hwfv1::k_fv1<false, 2, false, false, true>, g->fv1_grid, 0, s, P, g->ctl);
-    else if (g->fv1_stage == 1)
-        launch_pdl(hwfv1::k_fv1<false, 3, false, false, false, false, 1>, g->fv1_grid, 0, s, P, g->ctl);
+    mark(3);
+    if (P.has_ina)  // D16 variant
+        launch_pdl(hwfv1::k_fv1<false, false, true>, g->fv1_grid, 0, s, P, g->ctl);
     else if (g->fv1_stage == 2)
-        launch_pdl(hwfv1::k_fv1<false, 2, false, false, false, false, 2>, g->fv1_grid, 0, s, P, g->ctl);
+        launch_pdl(hwfv1::k_fv1<false, false, false, 2>, g->fv1_grid, 0, s, P, g->ctl);
     else if (g->fv1_stage == 3)
-        launch_pdl(hwfv1::k_fv1<false, 2, false, false, false, false, 3>, g->fv1_grid, 0, s, P, g->ctl);
+        launch_pdl(hwfv1::k_fv1<false, false, false, 3>, g->fv1_grid, 0, s, P, g->ctl);
     else if (g->fv1_stage == 5)
-        launch_pdl(hwfv1::k_fv1<false, 2, false, false, false, false, 5>, g->fv1_grid, 0, s, P, g->ctl);
-    else if (g->fv1_minb == 4)
-        launch_pdl(hwfv1::k_fv1<false, 4>, g->fv1_grid, sm5, s, P, g->ctl);
-    else if (g->fv1_minb == 3)
-        launch_pdl(hwfv1::k_fv1<false, 3>, g->fv1_grid, sm5, s, P, g->ctl);
+        launch_pdl(hwfv1::k_fv1<false, false, false, 5>, g->fv1_grid, 0, s, P, g->ctl);
     else
-        launch_pdl(hwfv1::k_fv1<false, 2>, g->fv1_grid, sm5, s, P, g->ctl);
+        launch_pdl(hwfv1::k_fv1<false>, g->fv1_grid, 0, s, P, g->ctl);
     mark(4);
 }
 
@@ -496,7 +472,6 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     if ((st = dalloc(g, &P.wet[0], P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.wet[1], P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.tact, P.n_tiles))) return fail(st);
-    if ((st = dalloc(g, &P.stile, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     P.pdem[0] = P.dem;
     P.pwet[0][0] = P.wet[0];
     P.pwet[0][1] = P.wet[1];
@@ -619,8 +594,6 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         }
         g->smem_k1 = ncell * (sizeof(double4) + 1);                  // k_encode<true> / k_encode_top
         g->smem_k1s = 32 * (((size_t(1) << (2 * (K - 1))) - 1) / 3) + 4 * sl;  // values, 2 flag copies, DEM, new pre
-        // persistent K1: 2 stages of (children + values + 3 flag slices + small words)
-        g->smem_k1p = 2 * (32 * ((size_t(1) << (2 * (K - 1))) + ((size_t(1) << (2 * (K - 1))) - 1) / 3) + 3 * sl + 16);
         P.top_mode = (R == 0) ? 0 : (R <= 6 ? 1 : 2);
         const size_t k2_tile = 2 * sl;
         const char* etb = std::getenv("SWAMP_TOP_BAND");
@@ -647,7 +620,6 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
                      {reinterpret_cast<const void*>(hwfv1::k_encode<true>), g->smem_k1},
                      {reinterpret_cast<const void*>(hwfv1::k_encode_top<true>), g->smem_k1},
                      {reinterpret_cast<const void*>(hwfv1::k_encode_top<false>), g->smem_k1},
-                     {reinterpret_cast<const void*>(hwfv1::k_encode_pipe<6>), g->smem_k1p},
                      {reinterpret_cast<const void*>(g->k2), g->smem_k2},
                      {reinterpret_cast<const void*>(g->k3), g->smem_k3},
                      {reinterpret_cast<const void*>(g->k3x), g->smem_k3},
@@ -660,59 +632,17 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
                 return fail(SWAMP_E_CUDA);
     }
     {
-        if (const char* e = std::getenv("SWAMP_FV1_MINB")) g->fv1_minb = std::max(2, std::min(4, std::atoi(e)));
         // tail balancing pays when the leaf list spans many grid-stride
         // windows (L = 11: ~22); below that its bookkeeping costs ~5 %
         g->fv1_stage = (L >= 11) ? 5 : 3;
         if (const char* e = std::getenv("SWAMP_FV1_STAGE")) g->fv1_stage = std::atoi(e);
-        const char* es = std::getenv("SWAMP_FV1_STRIPS");
-        P.strips = (es && es[0] == '1') ? 1 : 0;
-        // fused K2+K3 (opt-in SWAMP_FUSE_K23=1: measured slower on B200 — full
-        // residency caps it at 32 registers and it spills): one partition and
-        // every CTA resident at once (block 0 waits for all subtree CTAs)
-        const char* ef = std::getenv("SWAMP_FUSE_K23");
-        if (G == 1 && ef && ef[0] == '1') {
-            void (*f)(Params, Ctl*) = (P.K == 6) ? hwfv1::k_band_traverse<6> : hwfv1::k_band_traverse<0>;
-            const size_t ncell = ((size_t(1) << (2 * P.K)) - 1) / 3;
-            g->smem_k23 = std::max({3 * static_cast<size_t>(hwfv1::slo(P.K)) + 4 * ncell, g->smem_k2, g->smem_k3});
-            int occ = 0;
-            if (g->smem_k23 > 48 * 1024)
-                cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(g->smem_k23));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kThreads, g->smem_k23);
-            if (static_cast<int64_t>(occ) * g->num_sms >= static_cast<int64_t>(P.n_tiles) + 1) g->k23 = f;
-        }
         // tail balancing: the last 6/16 of FV1's grid-stride windows go to
         // whichever warps are free (8 of 22 windows at L = 11: FV1 66.3 ->
         // 64.3 us; 2-6 windows less, 10-24 windows less to slower)
         const char* etw = std::getenv("SWAMP_FV1_TAIL16");
         P.fv1_tail16 = etw ? static_cast<uint32_t>(std::min(16, std::max(0, std::atoi(etw)))) : 6u;
-        const char* epf = std::getenv("SWAMP_FV1_PF");
-        P.fv1_pf = epf ? std::atoi(epf) : 1;  // L2 prefetch: FV1 72 -> 69 us (round 1)
-        const char* eq = std::getenv("SWAMP_FV1_QUAD");
-        P.quad = (eq && eq[0] == '1') ? 1 : 0;
-        if (P.has_ina) P.strips = P.quad = 0;  // those paths do not handle inactive cells
-        // persistent double-buffered K1 for K = 6, opt-in (SWAMP_K1_PIPE=1): measured
-        // slower than one CTA per subtree (latency chains, fewer CTAs in flight)
-        const char* ep = std::getenv("SWAMP_K1_PIPE");
-        if (P.K == 6 && ep && ep[0] == '1') {
-            int occ1 = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, hwfv1::k_encode_pipe<6>, kThreads, g->smem_k1p);
-            g->k1p_grid = std::max(1, std::min<int>(static_cast<int>(P.tiles_per_part), std::max(1, occ1) * g->num_sms));
-        }
         int occ = 0;
-        if (g->fv1_stage == 1)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 3, false, false, false, false, 1>,
-                                                          kThreads, 0);
-        else if (g->fv1_stage >= 2)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 2, false, false, false, false, 2>,
-                                                          kThreads, 0);
-        else if (g->fv1_minb == 4)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 4>, kThreads, 0);
-        else if (g->fv1_minb == 3)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 3>, kThreads, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, 2>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, false, false, 5>, kThreads, 0);
         g->fv1_grid = std::max(1, occ) * g->num_sms;
     }
     g->n_cells = static_cast<int64_t>(off);
@@ -812,8 +742,7 @@ bool part_step_phase(swamp_gpu* q, int k, cudaStream_t s) {
     const Params& P = q->P;
     switch (k) {
         case 0:
-            if (q->k1p_grid) hwfv1::k_encode_pipe<6><<<q->k1p_grid, kThreads, q->smem_k1p, s>>>(P, q->ctl);
-            else q->k1<<<P.tiles_per_part, kThreads, q->smem_k1s, s>>>(P, q->ctl);
+            q->k1<<<P.tiles_per_part, kThreads, q->smem_k1s, s>>>(P, q->ctl);
             return true;
         case 1:
             if (P.top_mode != 2) return false;
@@ -826,11 +755,11 @@ bool part_step_phase(swamp_gpu* q, int k, cudaStream_t s) {
         }
         case 3: q->k3<<<P.tiles_per_part + 1, kThreads, q->smem_k3, s>>>(P, q->ctl, 0, 0ull); return true;
         case 4:
-            if (P.has_ina) hwfv1::k_fv1<false, 2, true, false, false, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
+            if (P.has_ina) hwfv1::k_fv1<false, true, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
             else if (q->fv1_stage >= 2)  // own cells loaded an iteration ahead (flags come from peer tables: no STAGE 3)
-                hwfv1::k_fv1<false, 2, true, false, false, false, 2><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
+                hwfv1::k_fv1<false, true, false, 2><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
             else
-                hwfv1::k_fv1<false, 2, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
+                hwfv1::k_fv1<false, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
             return true;
         default: hwfv1::k_finalize<<<1, 32, 0, s>>>(P, q->ctl, 1); return true;
     }
@@ -1677,8 +1606,6 @@ int swamp_gpu_rebalance(swamp_gpu* g, int32_t* changed) {
     for (swamp_gpu* q : mine) {
         cudaSetDevice(q->device);
         apply_bounds(q->P, nb);
-        if (q->k1p_grid)
-            q->k1p_grid = std::max(1, std::min<int>(static_cast<int>(q->P.tiles_per_part), q->k1p_grid));
         for (cudaGraphExec_t* e : {&q->graph1, &q->graphS})
             if (*e) {
                 cudaGraphExecDestroy(*e);

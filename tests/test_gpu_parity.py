@@ -179,18 +179,13 @@ def test_partitioned_equals_single(parts, name, kw):
         np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))
 
 
-@pytest.mark.parametrize("variant", ["per-leaf", "strips", "quad", "stage", "ahead", "ahead-flags", "tail", "no-prefetch", "fused-k23"])
+@pytest.mark.parametrize("variant", ["l2-prefetch", "ahead", "ahead-flags", "tail"])
 @pytest.mark.parametrize("name,kw", [("river_flood", dict(L=9)), ("monai_runup", dict(L=9))])
 def test_active_subtree_paths(monkeypatch, variant, name, kw):
-    """L = 9 (64 subtrees of 64 x 64): FV1's dry-subtree shortcut and, opt-in,
-    the strip path for fully refined active subtrees and the sibling-quad
-    path == the oracle, bitwise."""
-    strips = variant == "strips"
-    monkeypatch.setenv("SWAMP_FV1_STRIPS", "1" if strips else "0")
-    monkeypatch.setenv("SWAMP_FV1_QUAD", "1" if variant == "quad" else "0")
-    monkeypatch.setenv("SWAMP_FV1_STAGE", {"stage": "1", "ahead": "2", "ahead-flags": "3", "tail": "5"}.get(variant, "0"))
-    monkeypatch.setenv("SWAMP_FV1_PF", "0" if variant == "no-prefetch" else "1")
-    monkeypatch.setenv("SWAMP_FUSE_K23", "1" if variant == "fused-k23" else "0")
+    """L = 9 (64 subtrees of 64 x 64): FV1's dry-subtree shortcut with each
+    load-ahead stage of k_fv1 (SWAMP_FV1_STAGE 0 / 2 / 3 / 5) == the oracle,
+    bitwise."""
+    monkeypatch.setenv("SWAMP_FV1_STAGE", {"ahead": "2", "ahead-flags": "3", "tail": "5"}.get(variant, "0"))
     cfg, h, qx, qy, z = cases.CASES[name](**kw)
     g = gpu.initialise(cfg, h, qx, qy, z)
     o = O.Oracle(cfg, h, qx, qy, z)
@@ -198,22 +193,7 @@ def test_active_subtree_paths(monkeypatch, variant, name, kw):
         g.step_adaptive()
         o.step()
         if k in (1, 10, 30):
-            compare_states(g, o, f"{name} strips={strips} step {k}")
-    if strips:
-        assert g.debug()[40] > 0, "no subtree took the strip path"
-
-
-def test_persistent_k1_variant(monkeypatch):
-    """Opt-in persistent double-buffered K1 (SWAMP_K1_PIPE=1) == the oracle."""
-    monkeypatch.setenv("SWAMP_K1_PIPE", "1")
-    cfg, h, qx, qy, z = cases.river_flood(L=9)
-    g = gpu.initialise(cfg, h, qx, qy, z)
-    o = O.Oracle(cfg, h, qx, qy, z)
-    for k in range(1, 21):
-        g.step_adaptive()
-        o.step()
-        if k in (1, 20):
-            compare_states(g, o, f"K1 pipe step {k}")
+            compare_states(g, o, f"{name} {variant} step {k}")
 
 
 MASKED = [
