@@ -104,6 +104,11 @@ typedef struct swamp_step_report {
     double ms_neighbours;  /* fused into FV1 on this build: always 0            */
     double ms_fv1;         /* FV1 + friction + write-back + CFL reduce          */
     double ms_total;
+    /* near-threshold cells of the step (BASELINE north star; D8):
+     * cells whose significance was evaluated in the step's re-encode (the
+     * previous tree) with |d_norm - eps 2^(n-L)| <= 1e-12 eps 2^(n-L),
+     * d_norm = max over h, qx, qy of max|d| / s_max */
+    int64_t n_near_threshold;
 } swamp_step_report;
 
 typedef struct swamp_gpu swamp_gpu;
@@ -163,7 +168,11 @@ int swamp_gpu_rank_ready(swamp_gpu* g);
 int swamp_gpu_rebalance(swamp_gpu* g, int32_t* changed);
 
 /* step_adaptive: one Alg. 3 iteration. No-op when
- * t >= t_end. Fills `rep` (may be NULL). Synchronises the device. */
+ * t >= t_end. Fills `rep` (may be NULL). Returns once the step is complete
+ * and its report is in host memory (one partition: the step's last CTA
+ * writes the report into a pinned mirror behind a system-scope fence, so
+ * the call waits for that word instead of a stream synchronisation; later
+ * calls are stream-ordered after the step). */
 int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep);
 
 /* Advance `n_steps` adaptive steps without host round trips (CUDA graph of
@@ -214,8 +223,16 @@ int swamp_gpu_last_error(const swamp_gpu* g, int32_t* code, uint32_t* z, int32_t
  * significant tree cells re-encoded (cumulative), [2] newly significant cells
  * decoded (cumulative), [3] 4^L, [4] leaf updates of all steps (sum of N,
  * cumulative), [5] kernels launched per adaptive step (kernel nodes of the
- * one-step graph, summed over partitions), [6..7] reserved (0). */
+ * one-step graph, summed over partitions), [6] near-threshold cells of all
+ * steps (cumulative), [7] near-threshold cells of the last step. */
 int swamp_gpu_counters(swamp_gpu* g, int64_t* out8);
+
+/* Near-threshold cell counts (north star: cells whose normalised detail lies
+ * within FP tolerance of the threshold are counted and reported; DESIGN.md
+ * D8): [0] of the last step, [1] summed over all steps, [2] initialise's
+ * full encode (flow quantities, every detail cell), [3] initialise's DEM
+ * mask (z details). Summed over partitions. */
+int swamp_gpu_near_threshold(swamp_gpu* g, int64_t* out4);
 
 /* Device timeline of the last step, microseconds from K1's first CTA: for
  * K1, K2, K3, K5 (k = 0..3): [3k] first CTA start, [3k+1] unused (-1),

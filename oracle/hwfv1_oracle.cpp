@@ -37,7 +37,7 @@ namespace {
 // arithmetic). Reference: zorder.hpp:24-66, 69-131.
 uint32_t o_interleave(uint32_t i, uint32_t j) {
     uint32_t m = 0;
-    for (int b = 0; b < 14; ++b) {
+    for (int b = 0; b < 14 && ((i | j) >> b) != 0u; ++b) {
         m |= ((i >> b) & 1u) << (2 * b);
         m |= ((j >> b) & 1u) << (2 * b + 1);
     }
@@ -45,24 +45,32 @@ uint32_t o_interleave(uint32_t i, uint32_t j) {
 }
 void o_deinterleave(uint32_t m, uint32_t* i, uint32_t* j) {
     uint32_t a = 0, c = 0;
-    for (int b = 0; b < 14; ++b) {
+    for (int b = 0; b < 14 && (m >> (2 * b)) != 0u; ++b) {
         a |= ((m >> (2 * b)) & 1u) << b;
         c |= ((m >> (2 * b + 1)) & 1u) << b;
     }
     *i = a;
     *j = c;
 }
-uint32_t o_offset(int n) {  // level_offset
-    uint32_t s = 0, p = 1;
-    for (int k = 0; k < n; ++k) {
-        s += p;
-        p *= 4u;
+// level_offset as the running sum 1 + 4 + ... + 4^(n-1),
+// tabulated once for n = 0..14 (the oracle calls it per cell and per leaf)
+struct OffsetTable {
+    uint32_t v[15];
+    OffsetTable() {
+        uint32_t s = 0, p = 1;
+        for (int n = 0; n < 15; ++n) {
+            v[n] = s;
+            s += p;
+            p *= 4u;
+        }
     }
-    return s;
-}
-int o_level_of(uint32_t z) {
+};
+const OffsetTable kOffsets;
+inline uint32_t o_offset(int n) { return kOffsets.v[n]; }
+// level_of (zorder.hpp:83-87): the level whose z-range holds z
+inline int o_level_of(uint32_t z) {
     int n = 0;
-    while (o_offset(n + 1) <= z) ++n;
+    while (n < 13 && kOffsets.v[n + 1] <= z) ++n;
     return n;
 }
 // same_level_neighbour: decode, shift, re-encode; false off-grid.
@@ -99,12 +107,19 @@ inline void decode4(double s, double da, double db, double dg, double c[4]) {
 }
 inline double absd(double x) { return x < 0.0 ? -x : x; }
 inline double max2(double a, double b) { return a > b ? a : b; }
-// significance, D6/D7: d_norm = max|d| / s_max >= 2^(n-L) eps,
-// evaluated division-free as max|d| >= ldexp(eps * s_max, n - L) (pinned);
-// a quantity with s_max < 1e-12 contributes d_norm = 0.
+// significance, D6/D7, literally: the normalised
+// detail of one quantity is d_norm = max(|dα|,|dβ|,|dγ|) / s_max (a quantity
+// with s_max < 1e-12 contributes d_norm = 0), a cell's d_norm is the max over
+// h, qx, qy, and the cell is significant when d_norm >= 2^(n-L) eps.
+// D8: the cell is near-threshold when |d_norm - thr| <= 1e-12 thr.
+inline double dnorm(double da, double db, double dg, double smax) {
+    if (smax < 1e-12) return 0.0;
+    return max2(max2(absd(da), absd(db)), absd(dg)) / smax;
+}
+inline double sig_threshold(int n, int L, double eps) { return std::ldexp(eps, n - L); }
+inline bool near_threshold(double dn, double thr) { return absd(dn - thr) <= 1e-12 * thr; }
 inline bool significant(double da, double db, double dg, double smax, int n, int L, double eps) {
-    if (smax < 1e-12) return 0.0 >= std::ldexp(eps, n - L);
-    return max2(max2(absd(da), absd(db)), absd(dg)) >= std::ldexp(eps * smax, n - L);
+    return dnorm(da, db, dg, smax) >= sig_threshold(n, L, eps);
 }
 
 // ============================================================== swe physics
@@ -318,29 +333,47 @@ struct oracle_state {
     double t = 0.0, dt = 0.0, t_next = 0.0;
     int64_t step = 0;
     int64_t cnt_tree = 0, cnt_new = 0;
+    // near-threshold cells (D8): of the last step's re-encode (cells on the
+    // previous tree), summed over steps, initialise's flow / DEM evaluations
+    int64_t near_last = 0, cnt_near = 0, near_init = 0, near_dem = 0;
     std::string err;
 };
 
 namespace {
 
 inline uint32_t Z(int n, uint32_t m) { return o_offset(n) + m; }
-inline double to_phys(double s, int n, int L) { return std::ldexp(s, n - L); }
-inline double from_phys(double p, int n, int L) { return std::ldexp(p, L - n); }
+// phys = s 2^(n-L), exact; the powers of two are tabulated
+// (2^-13 .. 2^13) and multiplied, which equals ldexp bit for bit (no
+// overflow / subnormals here)
+struct Pow2Table {
+    double v[27];
+    Pow2Table() {
+        for (int k = -13; k <= 13; ++k) v[k + 13] = std::ldexp(1.0, k);
+    }
+};
+const Pow2Table kPow2;
+inline double to_phys(double s, int n, int L) { return s * kPow2.v[n - L + 13]; }
+inline double from_phys(double p, int n, int L) { return p * kPow2.v[L - n + 13]; }
 
 // significance pipeline after (re)encoding: flow | DEM -> band -> closure
-// (D3, D5)
-void flag_tree(oracle_state& S) {
+// (D3, D5). `evaluated` marks the cells whose
+// details were (re)computed (the previous tree; null = every cell): the
+// near-threshold count (D8) is over those; the others have zero details.
+int64_t flag_tree(oracle_state& S, const uint8_t* evaluated) {
     const int L = S.L;
     const double eps = S.cfg.epsilon;
     const size_t nd = o_offset(L);
     std::vector<uint8_t> pre(nd, 0);
-#pragma omp parallel for schedule(static)
+    int64_t nnear = 0;
+#pragma omp parallel for schedule(static) reduction(+ : nnear)
     for (int64_t zi = 0; zi < (int64_t)nd; ++zi) {
         const int n = o_level_of((uint32_t)zi);
-        bool f = false;
-        for (int q = 0; q < 3; ++q)
-            f = f || significant(S.det[q][0][zi], S.det[q][1][zi], S.det[q][2][zi], S.smax[q], n, L, eps);
-        pre[zi] = (f || S.dem[zi]) ? 1 : 0;
+        double dq[3];
+        for (int q = 0; q < 3; ++q) dq[q] = dnorm(S.det[q][0][zi], S.det[q][1][zi], S.det[q][2][zi], S.smax[q]);
+        const double dn = max2(max2(dq[0], dq[1]), dq[2]);
+        const double thr = sig_threshold(n, L, eps);
+        if ((!evaluated || evaluated[zi]) && near_threshold(dn, thr)) ++nnear;
+        pre[zi] = (dn >= thr || S.dem[zi]) ? 1 : 0;
     }
     std::vector<uint8_t> band(pre);
     const int mode = S.cfg.band_mode;
@@ -388,6 +421,7 @@ void flag_tree(oracle_state& S) {
             S.sig[Z(n, (uint32_t)m)] = v ? 1 : 0;
         }
     }
+    return nnear;
 }
 
 // zero_details_and_reencode: for levels L-1 -> 0, cells on
@@ -483,9 +517,7 @@ int64_t compact(const uint32_t* rec, int64_t N, uint32_t* out) {
                 if (m == 0 || rec[m] != rec[m - 1]) out[o++] = rec[m];
         }
     }
-    int64_t total = 0;
-    for (int64_t m = 0; m < N; ++m) total += (m == 0 || rec[m] != rec[m - 1]);
-    return total;
+    return cnt[nt];
 }
 
 // find_neighbours
@@ -724,13 +756,15 @@ static int create_impl(const swamp_config* cfg, const double* h, const double* q
                     const uint32_t zi = Z(n, m), c0 = Z(n + 1, 4u * m);
                     double s, a, b, g;
                     encode4(S->s[3][c0], S->s[3][c0 + 1], S->s[3][c0 + 2], S->s[3][c0 + 3], &s, &a, &b, &g);
-                    S->dem[zi] = significant(a, b, g, S->smax[3], n, L, cfg->epsilon) ? 1 : 0;
+                    const double dn = dnorm(a, b, g, S->smax[3]), thr = sig_threshold(n, L, cfg->epsilon);
+                    S->dem[zi] = dn >= thr ? 1 : 0;
+                    if (near_threshold(dn, thr)) ++S->near_dem;
                     // D16: mixed active / inactive cells are always refined, so
                     // every leaf is wholly active or wholly inactive
                     if (S->has_ina && any[zi] && !S->ina[zi]) S->dem[zi] = 1;
                 }
         }
-        flag_tree(*S);
+        S->near_init = flag_tree(*S, nullptr);
         // nothing is newly significant at t=0 (sig_prev = all): no decode
         rebuild_grid(*S);
     }
@@ -769,7 +803,8 @@ int oracle_step(oracle_state* S) {
     if (!(S->t < S->cfg.t_end)) return SWAMP_OK;
     S->sig_prev = S->sig;
     reencode(*S, false, false);   // zero_details_and_reencode
-    flag_tree(*S);                // significance | DEM | band, closure
+    S->near_last = flag_tree(*S, S->sig_prev.data());  // significance | DEM | band, closure
+    S->cnt_near += S->near_last;
     decode_new(*S);               // decode_tree (D4)
     rebuild_grid(*S);             // PTT, compaction, neighbours
     if (!S->err.empty()) return SWAMP_E_STATE;
@@ -846,6 +881,15 @@ int oracle_counters(const oracle_state* S, int64_t* out4) {
     out4[1] = S->cnt_tree;
     out4[2] = S->cnt_new;
     out4[3] = int64_t(1) << (2 * S->L);
+    return SWAMP_OK;
+}
+
+int oracle_near_threshold(const oracle_state* S, int64_t* out4) {
+    if (!S || !out4) return SWAMP_E_ARG;
+    out4[0] = S->near_last;
+    out4[1] = S->cnt_near;
+    out4[2] = S->near_init;
+    out4[3] = S->near_dem;
     return SWAMP_OK;
 }
 

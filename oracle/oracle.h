@@ -41,6 +41,9 @@ int oracle_copy_leaves(const oracle_state* s, uint32_t* leaves, uint32_t* w, uin
 int oracle_export_tree(const oracle_state* s, double* h, double* qx, double* qy, double* z, uint8_t* sig);
 int oracle_export_finest(const oracle_state* s, double* h, double* qx, double* qy);
 int oracle_counters(const oracle_state* s, int64_t* out4);
+/* near-threshold cells (D8): [0] last step, [1] all steps, [2]
+ * initialise (flow quantities), [3] initialise (z, the DEM mask) */
+int oracle_near_threshold(const oracle_state* s, int64_t* out4);
 const char* oracle_last_error(const oracle_state* s);
 /* overwrite the current state with a hierarchy + tree (s-units, z-index
  * order) — used to run GPU and oracle from one identical mid-run state */

@@ -46,6 +46,7 @@ def lib():
         L.oracle_export_tree.argtypes = [P, dp, dp, dp, dp, C.POINTER(C.c_uint8)]
         L.oracle_export_finest.argtypes = [P, dp, dp, dp]
         L.oracle_counters.argtypes = [P, C.POINTER(C.c_int64)]
+        L.oracle_near_threshold.argtypes = [P, C.POINTER(C.c_int64)]
         L.oracle_last_error.argtypes = [P]
         L.oracle_last_error.restype = C.c_char_p
         L.oracle_import_tree.argtypes = [P, dp, dp, dp, C.POINTER(C.c_uint8), C.c_double, C.c_double,
@@ -154,6 +155,13 @@ class Oracle:
         a = (C.c_int64 * 4)()
         lib().oracle_counters(self._h, a)
         return list(a)
+
+    def near_threshold(self):
+        """Near-threshold cell counts (D8): last step, all steps, initialise
+        (flow), initialise (DEM mask)."""
+        a = (C.c_int64 * 4)()
+        lib().oracle_near_threshold(self._h, a)
+        return {"last": a[0], "total": a[1], "init": a[2], "dem": a[3]}
 
     def import_tree(self, h, qx, qy, sig, t, dt, t_next, step):
         arrs = [as_f64(a) for a in (h, qx, qy)]

@@ -70,6 +70,7 @@ class swamp_step_report(C.Structure):
         ("ms_neighbours", C.c_double),
         ("ms_fv1", C.c_double),
         ("ms_total", C.c_double),
+        ("n_near_threshold", C.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -113,6 +114,18 @@ class SimConfig:
             raise ValueError("CFL number must be in (0, 1]")
         if not (self.h_dry > 0.0):
             raise ValueError("h_dry must be > 0")
+        if not (self.g > 0.0) or not (self.manning >= 0.0):
+            raise ValueError("g must be > 0 and manning >= 0")
+        if not (self.dt_fallback > 0.0):
+            raise ValueError("dt_fallback must be > 0")
+        if len(self.bc) != 4 or any(int(b) not in (BC_REFLECTIVE, BC_TRANSMISSIVE, BC_INFLOW) for b in self.bc):
+            raise ValueError(f"bc={self.bc}: four edge kinds in {{0, 1, 2}}")
+        if int(self.band_mode) not in (BAND_NONE, BAND_PARENTS, BAND_NEIGHBOURS):
+            raise ValueError(f"band_mode={self.band_mode}")
+        if int(self.inflow_mode) not in (INFLOW_DEPTH, INFLOW_ETA):
+            raise ValueError(f"inflow_mode={self.inflow_mode}")
+        if BC_INFLOW in [int(b) for b in self.bc] and len(self.inflow_t) == 0:
+            raise ValueError("an inflow edge needs an inflow series")
         if len(self.inflow_t) != len(self.inflow_v):
             raise ValueError("inflow series t / v lengths differ")
 

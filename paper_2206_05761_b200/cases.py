@@ -194,6 +194,28 @@ def with_nodata_block(case, frac=(0.35, 0.55, 0.3, 0.5), wall_z=200.0, **kw):
     return cfg, np.where(ina, 0.0, h), np.where(ina, 0.0, qx), np.where(ina, 0.0, qy), np.where(ina, wall_z, z)
 
 
+def threshold_lattice(L=7, epsilon=2.0 ** -3, seed=11, t_end=1e30, band_mode=BAND_NEIGHBOURS, still=False):
+    """Near-threshold exercise (north star; D8): depths on a 2^-4
+    lattice in [0.5, 1] and a bed on a 2^-3 lattice in [0, 1], both with
+    maximum exactly 1 (s_max = 1), so with a power-of-two epsilon many
+    normalised details equal the threshold eps 2^(n-L) exactly. Closed box,
+    still discharge; not a physical benchmark. still=True: a lake at rest
+    (h = 2 - z, s_max = 2) that the well-balanced scheme keeps unchanged, so
+    the same cells stay exactly at the threshold step after step."""
+    cfg = SimConfig(L=L, epsilon=epsilon, width=10.0, t_end=t_end, band_mode=band_mode,
+                    bc=(BC_REFLECTIVE,) * 4, name="threshold_lattice")
+    rng = np.random.default_rng(seed)
+    n = cfg.side
+    h = 0.5 + rng.integers(0, 9, size=(n, n)) * 2.0 ** -4
+    z = rng.integers(0, 9, size=(n, n)) * 2.0 ** -3
+    h[0, 0] = 1.0
+    z[0, 0] = 1.0
+    if still:
+        z[0, 1] = 0.0
+        h = 2.0 - z
+    return _fields(cfg, h, z)
+
+
 CASES = {
     "pseudo2d_dambreak": pseudo2d_dambreak,
     "quiescent_humps": quiescent_humps,
@@ -201,4 +223,5 @@ CASES = {
     "circular_dambreak": circular_dambreak,
     "monai_runup": monai_runup,
     "river_flood": river_flood,
+    "threshold_lattice": threshold_lattice,
 }

@@ -68,6 +68,14 @@ struct Ctl {
     uint32_t err_z;
     int err_q;
     int err_stage;
+    // near-threshold cells (D8; copied into the host mirror with
+    // this line): of the last completed step, and summed over all steps
+    unsigned long long near_last;
+    unsigned long long cnt_near;
+    // per-step accumulators by step parity (K1, K2's top CTA, the previous
+    // FV1's fused level-(L-1) re-encode), initialise's flow / z counts
+    alignas(128) unsigned long long near_step[2];
+    unsigned long long near_init, near_dem;
     alignas(128) unsigned long long bar_seq;     // cross-partition barriers passed (k_part_barrier; peers read it)
     alignas(128) unsigned long long dbg[64];     // per-phase globaltimer stamps of probe CTAs (diagnostics)
     // stage timeline (globaltimer ns), double-buffered by step parity, one
@@ -119,8 +127,9 @@ struct Params {
     int bc[4];
     int inflow_mode, inflow_n, n_out;
     double W, cfl, t_end, dt_fallback;
-    double tau[kMaxL + 1];    // 0 >= tau[n]: significance of a zero-detail cell (eps == 0)
-    double thr[4][kMaxL + 1]; // per quantity and level: max |D| >= thr (D7)
+    double tau[kMaxL + 1];    // e_n = eps 2^(2n-2L+2); 0 >= tau[n]: significance of a zero-detail cell (eps == 0)
+    double lvl[kMaxL + 1][4]; // significance table per level {lo, hi, tol, e_n} (sig_class; D7, D8)
+    double ismax[4];          // 1 / s_max per quantity, 0 when s_max < 1e-12 (screening only)
     double dx[kMaxL + 1];     // W * 2^-n
     double inv_dx[kMaxL + 1]; // 1.0 / dx[n] (IEEE division, as the oracle)
     double smax[4];
@@ -283,14 +292,43 @@ __device__ __forceinline__ Red red4(double c0, double c1, double c2, double c3) 
     const double dg = (c0 + c3) - (c1 + c2);
     return {par, max2(max2(absd(da), absd(db)), absd(dg))};
 }
-// significance of one quantity (D6, D7), division-free:
-// thr = ldexp(eps * s_max, 2n - 2L + 2) in physical units (+inf / 0 when
-// s_max < 1e-12, i.e. d_norm = 0)
-__device__ __forceinline__ bool sig_q(double dmax, double thr) { return dmax >= thr; }
+// Significance (D6, D7), SPEC's division
+// form: d_norm = max over h, qx, qy of max|d_q| / s_max_q (a quantity with
+// s_max < 1e-12 contributes 0) is compared with eps 2^(n-L) (>=). In
+// physical units (D = 2^(n+2-L) d on the same 4 children, exact powers of
+// two) that is fl(max|D_q| / s_max_q) >= e_n = eps 2^(2n-2L+2), the same
+// rounding. A cell is near-threshold (north star: counted and reported)
+// when |d_norm - e_n| <= 1e-12 e_n. The per-level table T = {lo, hi, tol,
+// e_n}: an approximate d_norm (one multiply by 1 / s_max per quantity,
+// within a few ulps) below lo = e_n (1 - 1e-11) is certainly neither
+// significant nor near, above hi = e_n (1 + 1e-11) certainly significant
+// and not near; only inside that window are the IEEE divisions formed, so
+// the flags and counts equal the literal division form bit for bit.
+// Returns bit 0 = significant, bit 1 = near-threshold.
+__device__ __forceinline__ unsigned sig_exact(double dh, double dqx, double dqy, double e, double tol, double s0,
+                                           double s1, double s2) {
+    const double nh = (s0 < 1e-12) ? 0.0 : dh / s0;
+    const double nx = (s1 < 1e-12) ? 0.0 : dqx / s1;
+    const double ny = (s2 < 1e-12) ? 0.0 : dqy / s2;
+    const double dn = max2(max2(nh, nx), ny);
+    return (dn >= e ? 1u : 0u) | (absd(dn - e) <= tol ? 2u : 0u);
+}
+__device__ __forceinline__ unsigned sig_class(double dh, double dqx, double dqy, const double* T, const Params& P) {
+    const double a = max2(max2(dh * P.ismax[0], dqx * P.ismax[1]), dqy * P.ismax[2]);
+    if (a < T[0]) return 0u;
+    if (a > T[1]) return 1u;
+    return sig_exact(dh, dqx, dqy, T[3], T[2], P.smax[0], P.smax[1], P.smax[2]);
+}
+// the static DEM mask's significance of z (initialise only; exact)
+__device__ __forceinline__ unsigned sig_class_z(double dz, const double* T, const Params& P) {
+    const double dn = (P.smax[3] < 1e-12) ? 0.0 : dz / P.smax[3];
+    return (dn >= T[3] ? 1u : 0u) | (absd(dn - T[3]) <= T[2] ? 2u : 0u);
+}
 
 struct Enc {
     double4 par;
     bool flow, zflag;
+    bool near, znear;  // near-threshold d_norm of the flow quantities / of z
 };
 // WITH_Z: also threshold z's details (the static DEM mask, t = 0 only)
 template <bool WITH_Z = true>
@@ -299,31 +337,36 @@ __device__ __forceinline__ Enc encode_children(const double4 c[4], const Params&
     const Red qx = red4(c[0].y, c[1].y, c[2].y, c[3].y);
     const Red qy = red4(c[0].z, c[1].z, c[2].z, c[3].z);
     Enc e;
-    e.flow = sig_q(h.dmax, P.thr[0][n]) || sig_q(qx.dmax, P.thr[1][n]) || sig_q(qy.dmax, P.thr[2][n]);
+    const unsigned s = sig_class(h.dmax, qx.dmax, qy.dmax, P.lvl[n], P);
+    e.flow = s & 1u;
+    e.near = s & 2u;
     if (WITH_Z) {
         const Red z = red4(c[0].w, c[1].w, c[2].w, c[3].w);
         e.par = make_double4(h.par, qx.par, qy.par, z.par);
-        e.zflag = sig_q(z.dmax, P.thr[3][n]);
+        const unsigned sz = sig_class_z(z.dmax, P.lvl[n], P);
+        e.zflag = sz & 1u;
+        e.znear = sz & 2u;
     } else {
         const double a = c[0].w + c[1].w, b = c[2].w + c[3].w;
         e.par = make_double4(h.par, qx.par, qy.par, 0.25 * (a + b));
-        e.zflag = false;
+        e.zflag = e.znear = false;
     }
     return e;
 }
 
-// encode + flow significance with the level's thresholds from a staged table
-// thr4 = {thr[0][n], thr[1][n], thr[2][n], tau[n]} (same arithmetic as
-// encode_children<false>)
-__device__ __forceinline__ Enc encode_children_t(const double4 c[4], const double* thr4) {
+// encode + flow significance with the level's table staged in shared memory
+// (thr4 = Params::lvl[n]; same arithmetic as encode_children<false>)
+__device__ __forceinline__ Enc encode_children_t(const double4 c[4], const double* thr4, const Params& P) {
     const Red h = red4(c[0].x, c[1].x, c[2].x, c[3].x);
     const Red qx = red4(c[0].y, c[1].y, c[2].y, c[3].y);
     const Red qy = red4(c[0].z, c[1].z, c[2].z, c[3].z);
     const double a = c[0].w + c[1].w, b = c[2].w + c[3].w;
     Enc e;
-    e.flow = sig_q(h.dmax, thr4[0]) || sig_q(qx.dmax, thr4[1]) || sig_q(qy.dmax, thr4[2]);
+    const unsigned sg = sig_class(h.dmax, qx.dmax, qy.dmax, thr4, P);
+    e.flow = sg & 1u;
+    e.near = sg & 2u;
     e.par = make_double4(h.par, qx.par, qy.par, 0.25 * (a + b));
-    e.zflag = false;
+    e.zflag = e.znear = false;
     return e;
 }
 // per-level thresholds staged in shared memory (indexed constant-bank loads
@@ -332,7 +375,7 @@ __device__ __forceinline__ void stage_thresholds(const Params& P, double (*s_thr
     const int t = static_cast<int>(threadIdx.x);
     if (t < 4 * P.L) {
         const int n = t >> 2, q = t & 3;
-        s_thr[n][q] = q < 3 ? P.thr[q][n] : P.tau[n];
+        s_thr[n][q] = P.lvl[n][q];
     }
 }
 
@@ -454,6 +497,20 @@ __device__ __forceinline__ bool last_block(unsigned int* counter, int* s_flag) {
 }
 
 
+// near-threshold counts of one CTA (block_sum of flow | z << 16): initialise
+// -> near_init / near_dem; a step -> the slot of the step they belong to
+// (by step parity; FV1's finalizing CTA folds it into cnt_near / near_last)
+__device__ __forceinline__ void add_near(Ctl* ctl, bool init, int slot, unsigned packed) {
+    if (threadIdx.x != 0 || packed == 0u) return;
+    const unsigned long long f = packed & 0xFFFFu, z = packed >> 16;
+    if (init) {
+        if (f) atomicAdd(&ctl->near_init, f);
+        if (z) atomicAdd(&ctl->near_dem, z);
+    } else if (f) {
+        atomicAdd(&ctl->near_step[slot], f);
+    }
+}
+
 // ------------------------------------------------------- TMA bulk copies (1D)
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -546,9 +603,13 @@ __device__ __forceinline__ Enc encode_lanes(double4 v, int s, const Params& P, i
     const Red qy = red(v.z);
     const Red z = red(v.w);
     Enc e;
-    e.flow = sig_q(h.dmax, P.thr[0][n]) || sig_q(qx.dmax, P.thr[1][n]) || sig_q(qy.dmax, P.thr[2][n]);
+    const unsigned sg = sig_class(h.dmax, qx.dmax, qy.dmax, P.lvl[n], P);
+    e.flow = sg & 1u;
+    e.near = sg & 2u;
     e.par = make_double4(h.par, qx.par, qy.par, z.par);
-    e.zflag = INIT && sig_q(z.dmax, P.thr[3][n]);
+    const unsigned sz = INIT ? sig_class_z(z.dmax, P.lvl[n], P) : 0u;
+    e.zflag = sz & 1u;
+    e.znear = sz & 2u;
     return e;
 }
 
@@ -561,7 +622,8 @@ __device__ __forceinline__ Enc encode_lanes(double4 v, int s, const Params& P, i
 // part. Returns the number of re-encoded cells of this thread.
 template <bool INIT>
 __device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4* buf, const uint8_t* sigp,
-                                                       double4* sv3, uint32_t j, int T, int R) {
+                                                       double4* sv3, uint32_t j, int T, int R, unsigned& nnear,
+                                                       unsigned& ndem) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t n1 = 1u << (2 * (T - R)), n2 = n1 >> 2, n3 = n2 >> 2;  // tile cells on T, T-1, T-2
     const int ipw = (n1 >= 32u * (kThreads / 32)) ? static_cast<int>(n1 / (32u * (kThreads / 32))) : 1;
@@ -622,7 +684,9 @@ __device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4*
                 const Enc e = encode_children<INIT>(ch, P, L1);
                 v1 = e.par;
                 flow = e.flow;
+                nnear += e.near ? 1u : 0u;
                 zf = e.zflag;
+                ndem += e.znear ? 1u : 0u;
                 st4(buf + cbase(L1) + gm1, v1);
                 ++tree;
             }
@@ -640,7 +704,9 @@ __device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4*
                 if (sp2) {
                     v2 = e.par;
                     flow = e.flow;
+                    nnear += e.near ? 1u : 0u;
                     zf = e.zflag;
+                    ndem += e.znear ? 1u : 0u;
                     st4(buf + cbase(L2) + gm2, v2);
                     ++tree;
                 }
@@ -657,7 +723,9 @@ __device__ __forceinline__ unsigned encode_warp_levels(const Params& P, double4*
                 if (sp3) {
                     v3 = e.par;
                     flow = e.flow;
+                    nnear += e.near ? 1u : 0u;
                     zf = e.zflag;
+                    ndem += e.znear ? 1u : 0u;
                     st4(buf + cbase(L3) + gm3, v3);
                     ++tree;
                 }
@@ -693,7 +761,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
     const uint32_t j = P.tile_lo + blockIdx.x;
     const uint32_t ncell = ((1u << (2 * K)) - 1u) / 3u;  // subtree cells on levels R..L-1
     uint8_t* sfl = reinterpret_cast<uint8_t*>(sv + ncell);  // previous-tree flags of the subtree
-    unsigned tree = 0;
+    unsigned tree = 0, nnear = 0, ndem = 0;
 
     // Warp part: levels T, T-1, T-2 with shuffles and no CTA barrier, where
     // T = L-1 at t = 0 and T = L-2 afterwards (the previous step's FV1 already
@@ -738,7 +806,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
                     if (!byte_of(f, k)) P.pre[g + q + k] = (zero || byte_of(d, k)) ? 1 : 0;
             }
         }
-        tree += encode_warp_levels<INIT>(P, buf, sigp, sv + lo(T - 2, R), j, T, R);
+        tree += encode_warp_levels<INIT>(P, buf, sigp, sv + lo(T - 2, R), j, T, R, nnear, ndem);
     } else {
         // small trees: one thread per level-(L-1) parent
         const int n = L - 1;
@@ -754,7 +822,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
                 const double4 c[4] = {ld4_nc(cp), ld4_nc(cp + 1), ld4_nc(cp + 2), ld4_nc(cp + 3)};
                 const Enc e = encode_children<INIT>(c, P, n);
                 flow = e.flow;
+                nnear += e.near ? 1u : 0u;
                 zf = e.zflag;
+                ndem += e.znear ? 1u : 0u;
                 st4(buf + cbase(n) + pm, e.par);
                 if (n > R) sv[lo(n, R) + pi] = e.par;
                 ++tree;
@@ -785,7 +855,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
                 const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
                 const Enc e = encode_children<INIT>(c, P, n);
                 flow = e.flow;
+                nnear += e.near ? 1u : 0u;
                 zf = e.zflag;
+                ndem += e.znear ? 1u : 0u;
                 st4(buf + cbase(n) + pm, e.par);
                 if (n > R) sv[lo(n, R) + pi] = e.par;
                 ++tree;
@@ -804,6 +876,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_encode(Params P, Ctl* ctl) {
 
     const unsigned tsum = block_sum(tree, s_red);
     if (threadIdx.x == 0 && tsum) atomicAdd(&ctl->cnt_tree, (unsigned long long)tsum);
+    add_near(ctl, INIT, hd.buf, block_sum(nnear | (ndem << 16), s_red));
     if (P.G > 1) return;  // partitioned: k_encode_top runs after all partitions' subtrees
     if (!last_block(&ctl->done_k1, &s_last)) return;
     encode_top<INIT>(P, ctl, sv, s_red);
@@ -829,7 +902,7 @@ __device__ void encode_top(const Params& P, Ctl* ctl, double4* sv, unsigned* s_r
     const uint8_t* sigp = P.sig[p];
     const int R = P.R, K = P.K;
 
-    unsigned ttop = 0;
+    unsigned ttop = 0, nnear = 0, ndem = 0;
     const bool top_smem = ((1u << (2 * R)) - 1u) / 3u <= ((1u << (2 * K)) - 1u) / 3u;
     for (int n = R - 1; n >= 0; --n) {
         const uint32_t cnt = 1u << (2 * n);
@@ -849,7 +922,9 @@ __device__ void encode_top(const Params& P, Ctl* ctl, double4* sv, unsigned* s_r
                 }
                 const Enc e = encode_children<INIT>(c, P, n);
                 flow = e.flow;
+                nnear += e.near ? 1u : 0u;
                 zf = e.zflag;
+                ndem += e.znear ? 1u : 0u;
                 st4(buf + cbase(n) + pm, e.par);
                 if (top_smem) sv[lo(n, 0) + pm] = e.par;
                 ++ttop;
@@ -874,13 +949,15 @@ __device__ void encode_top(const Params& P, Ctl* ctl, double4* sv, unsigned* s_r
         if (tt) atomicAdd(&ctl->cnt_tree, (unsigned long long)tt);
         ctl->done_k1 = 0;
     }
+    const unsigned nsum = block_sum(nnear | (ndem << 16), s_red);  // (replicated levels: partition 0 counts)
+    if (P.part == 0) add_near(ctl, INIT, static_cast<int>(*((volatile const long long*)&ctl->step) & 1), nsum);
 }
 
 
 
 // encode_children_t of the four values in lanes l, l+s, l+2s, l+3s (valid in
 // the lanes that own a parent; every lane of the warp must call it)
-__device__ __forceinline__ Enc encode_lanes_s(double4 v, int s, const double* thr4) {
+__device__ __forceinline__ Enc encode_lanes_s(double4 v, int s, const double* thr4, const Params& P) {
     const int lane = threadIdx.x & 31;
     const int l1 = (lane + s) & 31, l2 = (lane + 2 * s) & 31, l3 = (lane + 3 * s) & 31;
     auto red = [&](double x) {
@@ -892,9 +969,11 @@ __device__ __forceinline__ Enc encode_lanes_s(double4 v, int s, const double* th
     const double w1 = __shfl_sync(kFull, v.w, l1), w2 = __shfl_sync(kFull, v.w, l2), w3 = __shfl_sync(kFull, v.w, l3);
     const double a = v.w + w1, b = w2 + w3;
     Enc e;
-    e.flow = sig_q(h.dmax, thr4[0]) || sig_q(qx.dmax, thr4[1]) || sig_q(qy.dmax, thr4[2]);
+    const unsigned sg = sig_class(h.dmax, qx.dmax, qy.dmax, thr4, P);
+    e.flow = sg & 1u;
+    e.near = sg & 2u;
     e.par = make_double4(h.par, qx.par, qy.par, 0.25 * (a + b));
-    e.zflag = false;
+    e.zflag = e.znear = false;
     return e;
 }
 
@@ -1041,7 +1120,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
             P.pre[g] = (zero || sd[0]) ? 1 : 0;
         }
     }
-    unsigned tree = 0;
+    unsigned tree = 0, nnear = 0, ndem = 0;
     stamp(2);
     if constexpr (KT == 6) {
         // K = 6: levels L-2 .. R without a CTA barrier per level — L-2 in
@@ -1055,8 +1134,9 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
         {
             bool flow = 0.0 >= s_thr[L - 2][3];
             if (sp2) {
-                const Enc e = encode_children_t(ch, s_thr[L - 2]);
+                const Enc e = encode_children_t(ch, s_thr[L - 2], P);
                 flow = e.flow;
+                nnear += e.near ? 1u : 0u;
                 v = e.par;
                 st4(buf + cbase(L - 2) + m2, v);
                 ++tree;
@@ -1070,6 +1150,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
             bool flow = 0.0 >= s_thr[n][3];
             if (sf[slo(k) + pi]) {
                 flow = e.flow;
+                nnear += e.near ? 1u : 0u;
                 v = e.par;
                 st4(buf + cbase(n) + static_cast<unsigned long long>(j) * (1u << (2 * k)) + pi, v);
                 ++tree;
@@ -1079,11 +1160,11 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
             so[slo(k) + pi] = (flow || sd[slo(k) + pi]) ? 1 : 0;
         };
         {
-            const Enc e = encode_lanes_s(v, 1, s_thr[L - 3]);
+            const Enc e = encode_lanes_s(v, 1, s_thr[L - 3], P);
             if ((lane & 3) == 0) level(3, static_cast<uint32_t>(tid) >> 2, e);
         }
         {
-            const Enc e = encode_lanes_s(v, 4, s_thr[L - 4]);
+            const Enc e = encode_lanes_s(v, 4, s_thr[L - 4], P);
             if ((lane & 15) == 0) {
                 const uint32_t pi = static_cast<uint32_t>(tid) >> 4;
                 level(2, pi, e);
@@ -1094,11 +1175,11 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
         if (tid < 32) {
             v = sv[lo(2, 0) + (lane & 15)];
             {
-                const Enc e = encode_lanes_s(v, 1, s_thr[R + 1]);
+                const Enc e = encode_lanes_s(v, 1, s_thr[R + 1], P);
                 if ((lane & 3) == 0 && lane < 16) level(1, static_cast<uint32_t>(lane) >> 2, e);
             }
             {
-                const Enc e = encode_lanes_s(v, 4, s_thr[R]);
+                const Enc e = encode_lanes_s(v, 4, s_thr[R], P);
                 if (lane == 0) level(0, 0u, e);
             }
         }
@@ -1118,8 +1199,9 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
         if (has2) {
             bool flow = 0.0 >= s_thr[L - 2][3];
             if (sp2) {
-                const Enc e = encode_children_t(ch, s_thr[L - 2]);
+                const Enc e = encode_children_t(ch, s_thr[L - 2], P);
                 flow = e.flow;
+                nnear += e.near ? 1u : 0u;
                 sv[lo(k2, 0) + threadIdx.x] = e.par;
                 ++tree;
             }
@@ -1138,8 +1220,9 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
                 if (sf[slo(k) + pi]) {
                     const uint32_t c0 = lo(k + 1, 0) + 4u * pi;
                     const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
-                    const Enc e = encode_children_t(c, s_thr[n]);
+                    const Enc e = encode_children_t(c, s_thr[n], P);
                     flow = e.flow;
+                    nnear += e.near ? 1u : 0u;
                     sv[lo(k, 0) + pi] = e.par;
                     ++tree;
                 }
@@ -1164,8 +1247,9 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
         }
 
     }
-    const unsigned tsum = block_sum(tree, s_red);
-    if (threadIdx.x == 0 && tsum) atomicAdd(&ctl->cnt_tree, (unsigned long long)tsum);
+    const unsigned tsum = block_sum(tree | (nnear << 16), s_red);  // (both < 2^16 per subtree)
+    if (threadIdx.x == 0 && (tsum & 0xFFFFu)) atomicAdd(&ctl->cnt_tree, (unsigned long long)(tsum & 0xFFFFu));
+    add_near(ctl, false, hd.buf, tsum >> 16);
     tl_end(ctl, hd.buf, 0);
     stamp(5);
 }
@@ -1200,7 +1284,7 @@ __device__ __forceinline__ uint8_t band_flag(int mode, int L, int n, uint32_t m,
 // level-R children of re-encoded level-(R-1) cells into registers and stages
 // the values of previous-tree leaves whose parent is re-encoded. Needs
 // 32 * lo(R, 0) + 2 * fbase[R] bytes of shared memory (host: R <= 6).
-__device__ void encode_top_staged(const Params& P, Ctl* ctl, int p, uint8_t* sm) {
+__device__ void encode_top_staged(const Params& P, Ctl* ctl, int p, int slot, uint8_t* sm) {
     double4* buf = P.cells[p];
     const uint8_t* sigp = P.sig[p];
     const int R = P.R;
@@ -1227,7 +1311,7 @@ __device__ void encode_top_staged(const Params& P, Ctl* ctl, int p, uint8_t* sm)
                 cp_async16(reinterpret_cast<uint8_t*>(sv + lo(n, 0) + m) + 16, reinterpret_cast<const uint8_t*>(g) + 16);
             }
     }
-    unsigned tree = 0;
+    unsigned tree = 0, nnear = 0, ndem = 0;
     {
         // level R-1: children from every subtree's partition
         const int n = R - 1;
@@ -1246,8 +1330,9 @@ __device__ void encode_top_staged(const Params& P, Ctl* ctl, int p, uint8_t* sm)
             }
             bool flow = 0.0 >= s_thr[n][3];
             if (sp) {
-                const Enc e = encode_children_t(c, s_thr[n]);
+                const Enc e = encode_children_t(c, s_thr[n], P);
                 flow = e.flow;
+                nnear += e.near ? 1u : 0u;
                 v = e.par;
                 st4(buf + cbase(n) + m, v);
                 ++tree;
@@ -1267,8 +1352,9 @@ __device__ void encode_top_staged(const Params& P, Ctl* ctl, int p, uint8_t* sm)
             if (sf[slo(n) + m]) {
                 const uint32_t c0 = lo(n + 1, 0) + 4u * m;
                 const double4 c[4] = {sv[c0], sv[c0 + 1], sv[c0 + 2], sv[c0 + 3]};
-                const Enc e = encode_children_t(c, s_thr[n]);
+                const Enc e = encode_children_t(c, s_thr[n], P);
                 flow = e.flow;
+                nnear += e.near ? 1u : 0u;
                 st4(buf + cbase(n) + m, e.par);
                 sv[lo(n, 0) + m] = e.par;
                 ++tree;
@@ -1279,8 +1365,9 @@ __device__ void encode_top_staged(const Params& P, Ctl* ctl, int p, uint8_t* sm)
         }
         __syncthreads();
     }
-    const unsigned tt = block_sum(tree, s_red);
-    if (threadIdx.x == 0 && tt) atomicAdd(&ctl->cnt_tree, (unsigned long long)tt);
+    const unsigned tt = block_sum(tree | (nnear << 16), s_red);  // (both < 2^16: R <= 6)
+    if (threadIdx.x == 0 && (tt & 0xFFFFu)) atomicAdd(&ctl->cnt_tree, (unsigned long long)(tt & 0xFFFFu));
+    if (P.part == 0) add_near(ctl, false, slot, tt >> 16);  // (replicated levels: partition 0 counts)
     if (P.top_band) {
         // band (D3) of every top cell, off K3's critical path: K3's top CTA
         // stages these and goes straight to the closure (level-R pre flags of
@@ -1349,7 +1436,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int fo
     extern __shared__ __align__(16) uint8_t smem2[];
     tl_start(ctl, hd.buf, 1);
     if (do_top && blockIdx.x == 0) {
-        encode_top_staged(P, ctl, hd.parity, smem2);
+        encode_top_staged(P, ctl, hd.parity, hd.buf, smem2);
         return;
     }
     k2_tile<KT>(P, ctl, hd, P.tile_lo + blockIdx.x - (do_top ? 1u : 0u), smem2);
@@ -2271,6 +2358,12 @@ __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ct
         ctl->rate_bits[slot] = 0ull;
         ctl->done_k5 = 0;
         ctl->fv1_tail = 0u;
+        if (advance) {  // this step's near-threshold count is complete (K1, K2 and the previous FV1 are done)
+            const unsigned long long nn = ctl->near_step[slot];
+            ctl->near_last = nn;
+            ctl->cnt_near += nn;
+            ctl->near_step[slot] = 0ull;
+        }
         ctl->tl[slot][3][2] = gtimer();
         if (advance)  // next step's buffer
             for (int k = 0; k < 4; ++k) ctl->tl[slot ^ 1][k][0] = ctl->tl[slot ^ 1][k][2] = 0ull;
@@ -2352,6 +2445,12 @@ __global__ void k_finalize(Params P, Ctl* ctl, int advance) {
     }
     finalize_dt(P, ctl, __longlong_as_double(static_cast<long long>(m)), advance != 0);
     if (!advance) return;  // initialise: the host clears the slots afterwards
+    {
+        const unsigned long long nn = ctl->near_step[slot];
+        ctl->near_last = nn;
+        ctl->cnt_near += nn;
+        ctl->near_step[slot] = 0ull;
+    }
     ctl->rate_bits[slot ^ 1] = 0ull;
     ctl->tl[slot][3][2] = gtimer();
     for (int k = 0; k < 4; ++k) ctl->tl[slot ^ 1][k][0] = ctl->tl[slot ^ 1][k][2] = 0ull;
@@ -2424,7 +2523,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     const double inflow = series_value(P, t);
     const int lane = threadIdx.x & 31;
     double mx = 0.0;
-    unsigned tree = 0;
+    unsigned tree = 0, nnear = 0, ndem = 0;
     const uint32_t stride = gridDim.x * kThreads;
     // warp-uniform trip count: every lane runs every iteration (shuffles below)
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
@@ -2674,6 +2773,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
                 const unsigned long long fi = slo(P.L - 1) + pm;
                 P.pre[fi] = (e.flow || P.dem[fi]) ? 1 : 0;
                 ++tree;
+                nnear += e.near ? 1u : 0u;
             }
         }
     }
@@ -2681,8 +2781,34 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
         __shared__ unsigned s_red5[32];
         const unsigned tt = block_sum(tree, s_red5);
         if (threadIdx.x == 0 && tt) atomicAdd(&ctl->cnt_tree, (unsigned long long)tt);
+        // near-threshold level-(L-1) cells belong to the NEXT step's count
+        const unsigned nn = block_sum(nnear, s_red5);
+        if (threadIdx.x == 0 && nn) atomicAdd(&ctl->near_step[tbuf ^ 1], (unsigned long long)nn);
     }
     cfl_reduce_and_finalize(P, ctl, mx, true, tbuf);
+}
+
+// initialise: the near-threshold count of the first step's level-(L-1)
+// cells. On later steps the previous FV1 re-encodes and classifies them (the
+// fused level-(L-1) re-encode above); before the first step that is
+// initialise's tree: its level-(L-1) cells re-encoded from their level-L
+// children (unchanged since initialise), this partition's subtrees only.
+__global__ void __launch_bounds__(kThreads) k_near_l1(Params P, Ctl* ctl) {
+    const int p = ctl->parity;
+    const uint8_t* sg = P.sig[p];
+    const double4* buf = P.cells[p];
+    const int n = P.L - 1;
+    const uint32_t m0 = P.tile_lo << (2 * (n - P.R)), m1 = P.tile_hi << (2 * (n - P.R));
+    unsigned nn = 0;
+    for (uint32_t m = m0 + blockIdx.x * kThreads + threadIdx.x; m < m1; m += gridDim.x * kThreads) {
+        if (!sg[slo(n) + m]) continue;
+        const double4* c = buf + cbase(P.L) + 4ull * m;
+        const double4 ch[4] = {ld4(c), ld4(c + 1), ld4(c + 2), ld4(c + 3)};
+        nn += encode_children<false>(ch, P, n).near ? 1u : 0u;
+    }
+    __shared__ unsigned s_red[32];
+    const unsigned t = block_sum(nn, s_red);
+    if (threadIdx.x == 0 && t) atomicAdd(&ctl->near_step[0], (unsigned long long)t);
 }
 
 // dt at initialise: CFL over the initial leaves, no update.

@@ -10,6 +10,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <chrono>
@@ -149,9 +150,20 @@ struct swamp_gpu {
     size_t scratch_bytes = 0;
 
     ~swamp_gpu() {
+        // no kernel of any partition may still read a block (its own, or a
+        // peer's through the peer tables / IPC mappings) once it is returned
+        // to the cache or unmapped: drain every device involved first
+        for (swamp_gpu* q : parts) {
+            cudaSetDevice(q->device);
+            cudaDeviceSynchronize();
+        }
         for (swamp_gpu* q : parts) {
             cudaSetDevice(q->device);
             delete q;
+        }
+        if (!ipc_opened.empty() || !allocs.empty() || scratch) {
+            cudaSetDevice(device);
+            cudaDeviceSynchronize();
         }
         for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
         if (scratch) cached_free(device, scratch, scratch_bytes);
@@ -162,7 +174,6 @@ struct swamp_gpu {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (!allocs.empty() || scratch) cudaSetDevice(device);
-        if (!allocs.empty()) cudaDeviceSynchronize();  // no kernel may still use a block that goes back to the cache
         for (auto& a : allocs) cached_free(device, a.first, a.second);
         if (ctl_host) cached_free_pinned_ctl(ctl_host);
         if (stream) cudaStreamDestroy(stream);
@@ -203,6 +214,9 @@ int validate(const swamp_config* c) {
         if (c->bc[k] < 0 || c->bc[k] > 2) return SWAMP_E_ARG;
     if (c->band_mode < 0 || c->band_mode > 2) return SWAMP_E_ARG;
     if (c->inflow_n < 0 || (c->inflow_n > 0 && (!c->inflow_t || !c->inflow_v))) return SWAMP_E_ARG;
+    if (c->inflow_mode != SWAMP_INFLOW_DEPTH && c->inflow_mode != SWAMP_INFLOW_ETA) return SWAMP_E_ARG;
+    for (int k = 0; k < 4; ++k)  // an inflow edge without a series would silently become a dry ghost
+        if (c->bc[k] == SWAMP_BC_INFLOW && c->inflow_n == 0) return SWAMP_E_ARG;
     if (c->n_outputs < 0 || (c->n_outputs > 0 && !c->output_times)) return SWAMP_E_ARG;
     return SWAMP_OK;
 }
@@ -369,6 +383,17 @@ void fill_report(const swamp_gpu* g, swamp_step_report* r) {
     r->dt_used = c.dt_used;
     r->n_leaves = g->uniform ? (int64_t(1) << (2 * g->P.L)) : c.n_leaves_used;
     r->n_leaves_next = g->uniform ? r->n_leaves : c.n_leaves;
+    r->n_near_threshold = g->uniform ? 0 : static_cast<int64_t>(c.near_last);
+}
+
+// a partitioned group's report: partition 0's, with the near-threshold
+// count summed over the partitions (each counts its own subtrees)
+void fill_group_report(const swamp_gpu* grp, swamp_step_report* r) {
+    if (!r) return;
+    fill_report(grp->parts[0], r);
+    int64_t nn = 0;
+    for (const swamp_gpu* q : grp->parts) nn += static_cast<int64_t>(q->ctl_host->near_last);
+    r->n_near_threshold = nn;
 }
 
 // allocate + upload + import one (sub-)engine: everything before the
@@ -559,18 +584,19 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         unsigned long long b = g->ctl_host->smax_bits[q];
         std::memcpy(&P.smax[q], &b, 8);
     }
-    // significance threshold in physical units: eps * 2^(2n-2L+2) (D7)
-    // significance thresholds in physical units (D7): spec form
-    // max|d|/s_max >= eps 2^(n-L) on s = p 2^(L-n) coefficients, evaluated as
-    // max|D| >= ldexp(eps * s_max, 2n - 2L + 2) on physical details D
+    // significance table (D7, D8; hwfv1::sig_class): SPEC's
+    // max|d| / s_max >= eps 2^(n-L) on s = p 2^(L-n) coefficients is
+    // fl(max|D| / s_max) >= e_n = eps 2^(2n-2L+2) on physical details D (the
+    // same rounding: the two differ by exact powers of two); near-threshold
+    // band tol = 1e-12 e_n; screening window e_n (1 -/+ 1e-11)
+    for (int q = 0; q < 4; ++q) P.ismax[q] = (P.smax[q] < 1e-12) ? 0.0 : 1.0 / P.smax[q];
     for (int n = 0; n < L; ++n) {
-        P.tau[n] = std::ldexp(cfg->epsilon, 2 * n - 2 * L + 2);
-        for (int q = 0; q < 4; ++q) {
-            if (P.smax[q] < 1e-12)
-                P.thr[q][n] = (0.0 >= P.tau[n]) ? 0.0 : HUGE_VAL;
-            else
-                P.thr[q][n] = std::ldexp(cfg->epsilon * P.smax[q], 2 * n - 2 * L + 2);
-        }
+        const double e = std::ldexp(cfg->epsilon, 2 * n - 2 * L + 2);
+        P.tau[n] = e;
+        P.lvl[n][0] = e * (1.0 - 1e-11);
+        P.lvl[n][1] = e * (1.0 + 1e-11);
+        P.lvl[n][2] = 1e-12 * e;
+        P.lvl[n][3] = e;
     }
 
     // shared memory per kernel (hwfv1_kernels.cuh layouts)
@@ -691,6 +717,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
         // both buffers hold the full hierarchy; the current tree becomes "previous"
         cudaMemcpyAsync(P.cells[1], P.cells[0], off * sizeof(double4), cudaMemcpyDeviceToDevice, s);
         hwfv1::k_set_parity<<<1, 32, 0, s>>>(g->ctl, 1);
+        hwfv1::k_near_l1<<<g->num_sms * 4, kThreads, 0, s>>>(P, g->ctl);
         hwfv1::k_cfl_init<<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl, 0);
     }
     {
@@ -786,6 +813,7 @@ bool part_init_phase(swamp_gpu* q, int k, cudaStream_t s) {
             cudaMemcpyAsync(P.cells[1], P.cells[0], static_cast<size_t>(q->n_cells) * sizeof(double4),
                             cudaMemcpyDeviceToDevice, s);
             hwfv1::k_set_parity<<<1, 32, 0, s>>>(q->ctl, 1);
+            hwfv1::k_near_l1<<<q->num_sms * 4, kThreads, 0, s>>>(P, q->ctl);
             hwfv1::k_cfl_init<<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl, 0);
             return true;
         default: hwfv1::k_finalize<<<1, 32, 0, s>>>(P, q->ctl, 0); return true;
@@ -1028,17 +1056,26 @@ int group_advance(swamp_gpu* grp, int64_t n_steps, bool sync, swamp_step_report*
         int64_t k = 0;
         for (; k + kGraphSteps <= n_steps; k += kGraphSteps) CK(cudaGraphLaunch(grp->graphS, s0));
         for (; k < n_steps; ++k) CK(cudaGraphLaunch(grp->graph1, s0));
-    } else
-    for (swamp_gpu* q : grp->parts) {
-        const int st = part_enqueue(q, n_steps);
-        if (st) {
-            grp->err = q->err;
-            return st;
+    } else {
+        // distinct devices: the partitions meet in device barriers every
+        // step, so their launch queues must advance together — round robin,
+        // kGraphSteps steps per partition at a time (queuing all of one
+        // partition's steps first could fill its launch queue and block the
+        // host while that device spins on a peer with nothing queued)
+        for (int64_t k = 0; k < n_steps; k += kGraphSteps) {
+            const int64_t chunk = std::min<int64_t>(kGraphSteps, n_steps - k);
+            for (swamp_gpu* q : grp->parts) {
+                const int st = part_enqueue(q, chunk);
+                if (st) {
+                    grp->err = q->err;
+                    return st;
+                }
+            }
         }
     }
     if (!sync) return SWAMP_OK;
     int st = group_sync(grp);
-    fill_report(grp->parts[0], rep);
+    fill_group_report(grp, rep);
     return st;
 }
 
@@ -1185,6 +1222,7 @@ int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep) {
         for (unsigned spin = 0;; ++spin) {
             if (*seq == expect) {
                 arrived = true;
+                std::atomic_thread_fence(std::memory_order_acquire);  // the report words before rep_seq
                 break;
             }
             if ((spin & 1023u) == 1023u &&
@@ -1272,7 +1310,7 @@ int swamp_gpu_run(swamp_gpu* g, swamp_step_report* rep) {
         if (st) return st;
         while (g->parts[0]->ctl_host->t < g->parts[0]->P.t_end)
             if ((st = group_advance(g, 16, true, rep))) return st;
-        fill_report(g->parts[0], rep);
+        fill_group_report(g, rep);
         return SWAMP_OK;
     }
     int st = fetch_ctl(g);
@@ -1430,6 +1468,8 @@ int swamp_gpu_counters(swamp_gpu* g, int64_t* out8) {
             const int st = swamp_gpu_counters(q, c);
             if (st) return st;
             for (int k = 1; k < 3; ++k) acc[k] += c[k];
+            acc[6] += c[6];
+            acc[7] += c[7];
             acc[5] += c[5];
             acc[0] = c[0];
             acc[3] = c[3];
@@ -1446,8 +1486,32 @@ int swamp_gpu_counters(swamp_gpu* g, int64_t* out8) {
     out8[3] = int64_t(1) << (2 * g->P.L);
     out8[4] = static_cast<int64_t>(g->ctl_host->cnt_updates);
     out8[5] = g->launches_per_step;  // this engine's kernels per step (one-step graph)
-    out8[6] = out8[7] = 0;
+    out8[6] = static_cast<int64_t>(g->ctl_host->cnt_near);
+    out8[7] = static_cast<int64_t>(g->ctl_host->near_last);
     return st;
+}
+
+int swamp_gpu_near_threshold(swamp_gpu* g, int64_t* out4) {
+    if (!g || !out4) return SWAMP_E_ARG;
+    int64_t acc[4] = {0, 0, 0, 0};
+    std::vector<swamp_gpu*> parts = g->parts.empty() ? std::vector<swamp_gpu*>{g} : g->parts;
+    if (!g->parts.empty()) {
+        const int st = group_sync(g);
+        if (st) return st;
+    }
+    for (swamp_gpu* q : parts) {
+        if (g->parts.empty()) {
+            cudaSetDevice(q->device);
+            const int st = fetch_ctl(q);
+            if (st) return st;
+        }
+        acc[0] += static_cast<int64_t>(q->ctl_host->near_last);
+        acc[1] += static_cast<int64_t>(q->ctl_host->cnt_near);
+        acc[2] += static_cast<int64_t>(q->ctl_host->near_init);
+        acc[3] += static_cast<int64_t>(q->ctl_host->near_dem);
+    }
+    std::memcpy(out4, acc, sizeof(acc));
+    return SWAMP_OK;
 }
 
 int swamp_gpu_rank_create(const swamp_config* cfg, const double* h, const double* qx, const double* qy,

@@ -65,6 +65,70 @@ def test_significance_examples():
     assert not O.significance([5.0, 0, 0], 1e-13, 3, 5, 1e-3)     # s_max floor
 
 
+def _morton_levels(field, L):
+    """Finest raster (row j = south) -> level-L array in Morton order (i = x
+    in the even bits, zorder.hpp:24-49), then every coarser level's s and
+    details by the factored Haar filters (D1), in s-units, numpy float64."""
+    n = 1 << L
+    j, i = np.meshgrid(np.arange(n, dtype=np.uint64), np.arange(n, dtype=np.uint64), indexing="ij")
+    m = np.zeros_like(i)
+    for b in range(L):
+        m |= ((i >> np.uint64(b)) & np.uint64(1)) << np.uint64(2 * b)
+        m |= ((j >> np.uint64(b)) & np.uint64(1)) << np.uint64(2 * b + 1)
+    s = np.empty(n * n)
+    s[m.reshape(-1)] = np.asarray(field, dtype=np.float64).reshape(-1)
+    out = {}
+    for lev in range(L - 1, -1, -1):
+        c = s.reshape(-1, 4)
+        c0, c1, c2, c3 = c[:, 0], c[:, 1], c[:, 2], c[:, 3]
+        a, b = c0 + c1, c2 + c3
+        out[lev] = (0.5 * (a - b), 0.5 * ((c0 + c2) - (c1 + c3)), 0.5 * ((c0 + c3) - (c1 + c2)))
+        s = 0.5 * (a + b)
+    return out
+
+
+def _near_count_numpy(fields, smax, L, eps):
+    """Initialise's near-threshold count (D8), SPEC.md:124 literally:
+    d_norm = max_q max|d_q| / s_max_q, |d_norm - eps 2^(n-L)| <= 1e-12 thr."""
+    det = [_morton_levels(f, L) for f in fields]
+    near = 0
+    for n in range(L):
+        dn = None
+        for q, dq in enumerate(det):
+            mq = np.maximum(np.maximum(np.abs(dq[n][0]), np.abs(dq[n][1])), np.abs(dq[n][2]))
+            v = np.zeros_like(mq) if smax[q] < 1e-12 else mq / smax[q]
+            dn = v if dn is None else np.maximum(dn, v)
+        thr = math.ldexp(eps, n - L)
+        near += int(np.count_nonzero(np.abs(dn - thr) <= 1e-12 * thr))
+    return near
+
+
+@pytest.mark.parametrize("eps", [2.0 ** -3, 2.0 ** -5, 0.0, 1e-3])
+def test_near_threshold_counts_match_numpy(eps):
+    """The oracle's near-threshold counts of initialise (flow and DEM) equal a
+    numpy restatement of SPEC.md:124's division form on the same details."""
+    cfg, h, qx, qy, z = cases.threshold_lattice(L=6, epsilon=eps)
+    o = O.Oracle(cfg, h, qx, qy, z)
+    got = o.near_threshold()
+    smax = [float(np.max(np.abs(a))) for a in (h, qx, qy, z)]
+    assert got["init"] == _near_count_numpy([h, qx, qy], smax[:3], cfg.L, eps)
+    assert got["dem"] == _near_count_numpy([z], smax[3:], cfg.L, eps)
+    if eps == 2.0 ** -3:
+        assert got["init"] > 0 and got["dem"] > 0, "the lattice case must hit the threshold exactly"
+
+
+def test_near_threshold_counts_real_cases():
+    """On the analytic benchmark cases the same restatement agrees (the
+    counts are typically 0 there: smooth data rarely lands within 1e-12)."""
+    for name, kw in (("circular_dambreak", dict(L=8)), ("monai_runup", dict(L=7)), ("river_flood", dict(L=7))):
+        cfg, h, qx, qy, z = cases.CASES[name](**kw)
+        o = O.Oracle(cfg, h, qx, qy, z)
+        smax = [float(np.max(np.abs(a))) for a in (h, qx, qy, z)]
+        got = o.near_threshold()
+        assert got["init"] == _near_count_numpy([h, qx, qy], smax[:3], cfg.L, cfg.epsilon), name
+        assert got["dem"] == _near_count_numpy([z], smax[3:], cfg.L, cfg.epsilon), name
+
+
 def test_threshold_monotonicity():
     """eps1 <= eps2 => significant set grows."""
     cfg, h, qx, qy, z = cases.circular_dambreak(L=7)
