@@ -227,6 +227,14 @@ int swamp_gpu_last_error(const swamp_gpu* g, int32_t* code, uint32_t* z, int32_t
  * steps (cumulative), [7] near-threshold cells of the last step. */
 int swamp_gpu_counters(swamp_gpu* g, int64_t* out8);
 
+/* Work done so far, for per-kernel byte accounting (bench.py roofline):
+ * [0] cells re-encoded by K1 and the top-level encodes, [1] level-(L-1)
+ * cells re-encoded inside FV1 (the fused next-step re-encode), [2] newly
+ * significant cells decoded, [3] leaf updates (sum of N), [4] of which took
+ * FV1's dry-subtree shortcut, [5] steps, [6] detail cells, [7] hierarchy
+ * cells. Cumulative; summed over partitions. */
+int swamp_gpu_work_counters(swamp_gpu* g, int64_t* out8);
+
 /* Near-threshold cell counts (north star: cells whose normalised detail lies
  * within FP tolerance of the threshold are counted and reported; DESIGN.md
  * D8): [0] of the last step, [1] summed over all steps, [2] initialise's

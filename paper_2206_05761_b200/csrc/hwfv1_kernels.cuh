@@ -58,7 +58,9 @@ struct Ctl {
     //      per-CTA atomics do not queue in front of the line-0 reads
     alignas(128) unsigned long long rate_bits[2];  // CFL max-rate accumulators (bits of a non-negative double), by step parity
     unsigned int done_k1, done_k5;
-    alignas(128) unsigned long long cnt_tree;    // cells re-encoded by the last K1
+    alignas(128) unsigned long long cnt_tree;    // cells re-encoded by K1 and the top-level encodes (cumulative)
+    unsigned long long cnt_fused;                // level-(L-1) cells re-encoded by FV1 (cumulative)
+    unsigned long long cnt_quiet;                // leaves FV1 updated by the dry-subtree shortcut (cumulative)
     alignas(128) unsigned long long cnt_new;     // newly significant cells decoded by the last K3
     unsigned long long cnt_updates;              // leaf updates of all steps so far (sum of N)
     alignas(128) unsigned long long k3_ready;    // K3's top CTA published its results (epoch)
@@ -390,18 +392,23 @@ struct Head {
     int active, parity, buf;  // buf = timeline buffer (step parity)
     long long step;
 };
+// (one 16-B aligned block: the vectorised shared loads cover only it)
+struct __align__(16) HeadSlot {
+    int h[4];  // active, parity, buf, (pad)
+    long long step;
+};
 __device__ __forceinline__ Head cta_head(const Ctl* c, const Params& P, bool force) {
-    __shared__ int s_h[3];
-    __shared__ long long s_step;
+    __shared__ HeadSlot s;
     if (threadIdx.x == 0) {
         const double t = *((volatile const double*)&c->t);
-        s_h[0] = (force || t < P.t_end) ? 1 : 0;
-        s_h[1] = *((volatile const int*)&c->parity);
-        s_step = *((volatile const long long*)&c->step);
-        s_h[2] = static_cast<int>(s_step & 1);
+        s.h[0] = (force || t < P.t_end) ? 1 : 0;
+        s.h[1] = *((volatile const int*)&c->parity);
+        s.step = *((volatile const long long*)&c->step);
+        s.h[2] = static_cast<int>(s.step & 1);
+        s.h[3] = 0;
     }
     __syncthreads();
-    return {s_h[0], s_h[1], s_h[2], s_step};
+    return {s.h[0], s.h[1], s.h[2], s.step};
 }
 
 // Block-wide sum of unsigned values (256 threads).
@@ -2523,7 +2530,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     const double inflow = series_value(P, t);
     const int lane = threadIdx.x & 31;
     double mx = 0.0;
-    unsigned tree = 0, nnear = 0, ndem = 0;
+    unsigned tree = 0, nnear = 0, ndem = 0, nquiet = 0;
+    (void)ndem;
     const uint32_t stride = gridDim.x * kThreads;
     // warp-uniform trip count: every lane runs every iteration (shuffles below)
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
@@ -2636,6 +2644,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
             // (K3's tact) the leaf and all its neighbours are dry, so the
             // dry-neighbourhood result below follows without the gathers
             const bool quiet = ta == 0;
+            nquiet += quiet ? 1u : 0u;
             const bool dead = INA && (P.ina[slo(n) + m] & 1u);  // D16: an inactive leaf keeps its state
             if (dead) {
                 hn = o4.x;
@@ -2778,12 +2787,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
         }
     }
     if (!UNIFORM) {
-        __shared__ unsigned s_red5[32];
-        const unsigned tt = block_sum(tree, s_red5);
-        if (threadIdx.x == 0 && tt) atomicAdd(&ctl->cnt_tree, (unsigned long long)tt);
-        // near-threshold level-(L-1) cells belong to the NEXT step's count
-        const unsigned nn = block_sum(nnear, s_red5);
-        if (threadIdx.x == 0 && nn) atomicAdd(&ctl->near_step[tbuf ^ 1], (unsigned long long)nn);
+        // work counters (bench.py's per-class byte accounting) and the
+        // near-threshold level-(L-1) cells, which belong to the NEXT step's count
+        __shared__ unsigned s_red5[3][kThreads / 32];
+        unsigned v[3] = {tree, nquiet, nnear};
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(kFull, v[k], o);
+        if (lane == 0)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) s_red5[k][threadIdx.x >> 5] = v[k];
+        __syncthreads();
+        if (threadIdx.x < 3) {
+            unsigned long long s = 0;
+            for (int w = 0; w < kThreads / 32; ++w) s += s_red5[threadIdx.x][w];
+            unsigned long long* dst = threadIdx.x == 0 ? &ctl->cnt_fused
+                                      : threadIdx.x == 1 ? &ctl->cnt_quiet : &ctl->near_step[tbuf ^ 1];
+            if (s) atomicAdd(dst, s);
+        }
     }
     cfl_reduce_and_finalize(P, ctl, mx, true, tbuf);
 }

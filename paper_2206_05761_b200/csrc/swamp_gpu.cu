@@ -1491,6 +1491,34 @@ int swamp_gpu_counters(swamp_gpu* g, int64_t* out8) {
     return st;
 }
 
+int swamp_gpu_work_counters(swamp_gpu* g, int64_t* out8) {
+    if (!g || !out8) return SWAMP_E_ARG;
+    int64_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    std::vector<swamp_gpu*> parts = g->parts.empty() ? std::vector<swamp_gpu*>{g} : g->parts;
+    if (!g->parts.empty()) {
+        const int st = group_sync(g);
+        if (st) return st;
+    }
+    for (swamp_gpu* q : parts) {
+        if (g->parts.empty()) {
+            cudaSetDevice(q->device);
+            const int st = fetch_ctl(q);
+            if (st) return st;
+        }
+        const Ctl& c = *q->ctl_host;
+        acc[0] += static_cast<int64_t>(c.cnt_tree);
+        acc[1] += static_cast<int64_t>(c.cnt_fused);
+        acc[2] += static_cast<int64_t>(c.cnt_new);
+        acc[3] = static_cast<int64_t>(c.cnt_updates);  // global leaf counts: every partition holds the same sum
+        acc[4] += static_cast<int64_t>(c.cnt_quiet);
+        acc[5] = c.step;
+    }
+    acc[6] = static_cast<int64_t>(swamp::zorder::detail_cells(g->parts.empty() ? g->P.L : g->parts[0]->P.L));
+    acc[7] = static_cast<int64_t>(swamp::zorder::hierarchy_cells(g->parts.empty() ? g->P.L : g->parts[0]->P.L));
+    std::memcpy(out8, acc, sizeof(acc));
+    return SWAMP_OK;
+}
+
 int swamp_gpu_near_threshold(swamp_gpu* g, int64_t* out4) {
     if (!g || !out4) return SWAMP_E_ARG;
     int64_t acc[4] = {0, 0, 0, 0};

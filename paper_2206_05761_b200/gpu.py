@@ -62,6 +62,7 @@ def lib():
                                            C.POINTER(C.c_int32), C.c_char_p, C.c_size_t]
         L.swamp_gpu_counters.argtypes = [P, i64p]
         L.swamp_gpu_near_threshold.argtypes = [P, i64p]
+        L.swamp_gpu_work_counters.argtypes = [P, i64p]
         L.swamp_gpu_enqueue.argtypes = [P, C.c_int64]
         L.swamp_gpu_timeline.argtypes = [P, dp]
         L.swamp_gpu_debug.argtypes = [P, C.POINTER(C.c_uint64)]
@@ -78,7 +79,7 @@ EXPORTED_SYMBOLS = (
     "swamp_gpu_counters", "swamp_gpu_build_info", "swamp_gpu_enqueue", "swamp_gpu_stream",
     "swamp_gpu_timeline", "swamp_gpu_create_partitioned", "swamp_gpu_debug",
     "swamp_gpu_rank_create", "swamp_gpu_rank_connect", "swamp_gpu_rank_ready", "swamp_gpu_compare",
-    "swamp_gpu_rebalance", "swamp_gpu_trim_cache", "swamp_gpu_near_threshold",
+    "swamp_gpu_rebalance", "swamp_gpu_trim_cache", "swamp_gpu_near_threshold", "swamp_gpu_work_counters",
     "swamp_io_read_esri", "swamp_io_write_esri", "swamp_io_free_raster", "swamp_io_load_dem", "swamp_io_write_finest",
 )
 
@@ -250,6 +251,14 @@ class Engine:
         a = (C.c_int64 * 4)()
         self._check(lib().swamp_gpu_near_threshold(self._h, a), "near_threshold")
         return {"last": a[0], "total": a[1], "init": a[2], "dem": a[3]}
+
+    def work(self) -> dict:
+        """Cumulative work counters (swamp_gpu_work_counters)."""
+        a = (C.c_int64 * 8)()
+        self._check(lib().swamp_gpu_work_counters(self._h, a), "work_counters")
+        keys = ("k1_reencoded", "fv1_reencoded", "decoded", "leaf_updates", "quiet_updates", "steps",
+                "detail_cells", "hierarchy_cells")
+        return dict(zip(keys, (int(x) for x in a)))
 
     def launches_per_step(self) -> int:
         """Kernels one adaptive step launches (kernel nodes of the one-step graph)."""

@@ -4,7 +4,7 @@
 # partitioned engines), and memcheck over the two-process (CUDA IPC) engine.
 TAG=${1:-san}
 mkdir -p gpurun_out
-CS="compute-sanitizer --print-limit 50 --error-exitcode 9"
+CS="compute-sanitizer --print-limit 200 --error-exitcode 9"
 for L in 6 8; do
   timeout 900 $CS --tool memcheck --leak-check full python scripts/sanitize_run.py $L > gpurun_out/${TAG}_memcheck_L$L.log 2>&1; echo "memcheck L$L rc=$?"
 done

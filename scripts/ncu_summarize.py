@@ -2,7 +2,8 @@
 
 Usage: python scripts/ncu_summarize.py <tag>   (reads gpurun_out/<tag>_prof.ncu-rep)
 Writes profiles/<tag>/ncu_full_raw.csv, ncu_summary.txt and refreshes
-profiles/fv1_dram_bytes.json (bench.py's roofline.traffic per leaf).
+profiles/ncu_kernels.json (per kernel: DRAM bytes and FP64 issue of one
+launch — bench.py's roofline.traffic and fp64 fractions).
 """
 import csv
 import io
@@ -12,7 +13,6 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LEAVES = 1.72e6  # config 5 leaves per step (bench.py config.leaves_mean)
 
 ROWS = [
     ("Duration", "gpu__time_duration.sum", "us"),
@@ -66,13 +66,38 @@ def main(tag):
         lines.append("")
     with open(os.path.join(out, "ncu_summary.txt"), "w") as f:
         f.write("\n".join(lines) + "\n")
-    fv1 = [v for k, v in dram.items() if k.startswith("k_fv1")]
-    if fv1:
-        rd, wr = fv1[0]
-        with open(os.path.join(ROOT, "profiles", "fv1_dram_bytes.json"), "w") as f:
-            json.dump({"kernel": "k_fv1", "dram_bytes_per_leaf": (rd + wr) / LEAVES,
-                       "source": f"profiles/{tag}/ncu_full_raw.csv (dram__bytes_read.sum + dram__bytes_write.sum of "
-                                 f"one ncu --set full k_fv1 launch, N = 1.72 M leaves)"}, f, indent=1)
+    # per-kernel DRAM bytes and FP64 issue of one launch each (bench.py's
+    # roofline.traffic / kernels[*].dram_*, fp64 fraction)
+    per = {}
+    for r in data:
+        d = dict(zip(hdr, r))
+        short = d.get("Kernel Name", "?").split("(")[0].replace("void ", "").replace("hwfv1::", "")
+        base = short.split("<")[0]
+        if base in per:
+            continue
+        try:
+            def num(k):
+                v = d[k].replace(",", "")
+                u = rows[1][hdr.index(k)]
+                return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6,
+                                   "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e-9}.get(u, 1)
+            dur = num("gpu__time_duration.sum")
+            ent = {"kernel": short, "duration_s": dur,
+                   "dram_bytes": num("dram__bytes_read.sum") + num("dram__bytes_write.sum")}
+            f64 = 0.0
+            for op in ("dadd", "dmul", "dfma"):
+                k = f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed"
+                if k in d and d[k] not in ("", "n/a"):
+                    f64 += float(d[k].replace(",", ""))
+            ent["fp64_thread_inst_per_smsp_cycle"] = f64
+            ent["fp64_pipe_pct_active"] = float(d.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "nan"))
+            ent["issue_pct"] = float(d.get("sm__inst_issued.avg.pct_of_peak_sustained_active", "nan"))
+            per[base] = ent
+        except (KeyError, ValueError):
+            continue
+    with open(os.path.join(ROOT, "profiles", "ncu_kernels.json"), "w") as f:
+        json.dump({"source": f"profiles/{tag}/ncu_full_raw.csv (one ncu --set full launch each, cold, serialised)",
+                   "kernels": per}, f, indent=1)
     print("\n".join(lines))
 
 
