@@ -57,6 +57,7 @@ UNIT = "cell-updates/s"
 FV1_ACTIVE = 192   # own 32 + 4 neighbours x 32 + 4 neighbour flags + 4 B leaf id + 24 B write
 FV1_QUIET = 60     # dry-subtree shortcut: own 32 + 4 B leaf id + 24 B write
 FV1_FUSED = 25     # fused next-step re-encode of a level-(L-1) cell: 24 B write + 1 B pre flag
+FV1_TILED = 56     # tile path (neighbours come from the block itself): own 32 B read + 24 B write
 ENC_CELL = 120     # re-encoded cell: 4 children x 24 B read + 24 B parent write
 K1_FLAG = 3        # per detail cell of the subtree levels: previous-tree flag + DEM flag read, pre flag write
 K2_FLAG = 2        # per detail cell: pre flag read, final flag write
@@ -222,14 +223,16 @@ def kernel_bytes(w0, w1, steps, R_levels_detail):
     d = {k: (w1[k] - w0[k]) / steps for k in w1}
     N = d["leaf_updates"]
     quiet = d["quiet_updates"]
-    active = N - quiet
+    tiled = d["tile_updates"]
+    active = N - quiet - tiled
     det = R_levels_detail
     return {
         "k_encode_step": ENC_CELL * d["k1_reencoded"] + K1_FLAG * det,
         "k_band": K2_FLAG * det,
         "k_traverse": K3_FLAG * det + K3_LEAF * N + DEC_CELL * d["decoded"],
-        "k_fv1": FV1_ACTIVE * active + FV1_QUIET * quiet + FV1_FUSED * d["fv1_reencoded"],
-    }, {"leaves": N, "active_leaves": active, "quiet_leaves": quiet, "k1_reencoded": d["k1_reencoded"],
+        "k_fv1": FV1_ACTIVE * active + FV1_QUIET * quiet + FV1_TILED * tiled + FV1_FUSED * d["fv1_reencoded"],
+    }, {"leaves": N, "active_leaves": active, "quiet_leaves": quiet, "tiled_leaves": tiled,
+        "k1_reencoded": d["k1_reencoded"],
         "fv1_reencoded": d["fv1_reencoded"], "decoded": d["decoded"]}
 
 
@@ -554,7 +557,8 @@ def main():
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": d["GBps"], "peak": hbm_peak, "unit": "GB/s",
                      "frac": d["frac"], "traffic": d.get("dram_bytes_ncu"), "peak_source": peak_src,
                      "alg_bytes_per_unit": {"active_leaf": FV1_ACTIVE, "quiet_leaf": FV1_QUIET,
-                                            "fused_reencode": FV1_FUSED} if dominant == "k_fv1" else None,
+                                            "tiled_leaf": FV1_TILED, "fused_reencode": FV1_FUSED}
+                     if dominant == "k_fv1" else None,
                      "dram_frac_ncu": d.get("dram_frac_ncu"),
                      "note": "achieved = the kernel's algorithmic bytes (per-class counts of its own work, "
                              "DESIGN.md §3) / its device time; traffic = ncu DRAM bytes of one launch "

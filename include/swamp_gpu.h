@@ -231,8 +231,9 @@ int swamp_gpu_counters(swamp_gpu* g, int64_t* out8);
  * [0] cells re-encoded by K1 and the top-level encodes, [1] level-(L-1)
  * cells re-encoded inside FV1 (the fused next-step re-encode), [2] newly
  * significant cells decoded, [3] leaf updates (sum of N), [4] of which took
- * FV1's dry-subtree shortcut, [5] steps, [6] detail cells, [7] hierarchy
- * cells. Cumulative; summed over partitions. */
+ * FV1's dry-subtree shortcut, [5] of which FV1's tile path updated (active
+ * fully refined subtrees), [6] steps, [7] detail cells. Cumulative; summed
+ * over partitions. */
 int swamp_gpu_work_counters(swamp_gpu* g, int64_t* out8);
 
 /* Near-threshold cell counts (north star: cells whose normalised detail lies

@@ -61,10 +61,13 @@ struct Ctl {
     alignas(128) unsigned long long cnt_tree;    // cells re-encoded by K1 and the top-level encodes (cumulative)
     unsigned long long cnt_fused;                // level-(L-1) cells re-encoded by FV1 (cumulative)
     unsigned long long cnt_quiet;                // leaves FV1 updated by the dry-subtree shortcut (cumulative)
+    unsigned long long cnt_tiled;                // leaves FV1 updated on its tile path (cumulative)
     alignas(128) unsigned long long cnt_new;     // newly significant cells decoded by the last K3
     unsigned long long cnt_updates;              // leaf updates of all steps so far (sum of N)
     alignas(128) unsigned long long k3_ready;    // K3's top CTA published its results (epoch)
     alignas(128) unsigned int fv1_tail;          // FV1 (STAGE 5): dynamic tail chunks taken this step
+    unsigned int fv1_tjob;                       // FV1 tile path: strip jobs taken this step
+    uint32_t n_stile;                            // subtrees on FV1's tile path this step (K3's top)
     alignas(128) unsigned long long smax_bits[4];
     int err_code;
     uint32_t err_z;
@@ -165,6 +168,10 @@ struct Params {
     // the whole array
     uint8_t* ina;
     int has_ina;
+    // FV1 tile path (one partition, K = 6, no inactive cells): active fully
+    // refined subtrees, listed by K3's top in stile[0 .. ctl->n_stile)
+    int tiles;
+    uint32_t* stile;
     Ctl* ctl_mirror;      // one partition: the host's pinned Ctl mirror (UVA), written at the step's end
     uint32_t fv1_tail16;  // FV1 STAGE 5: sixteenths of the grid-stride windows taken dynamically at the end
     // Morton-subtree partitions: this partition owns level-R
@@ -1619,6 +1626,7 @@ __device__ void k2_tile(const Params& P, Ctl* ctl, const Head& hd, uint32_t j, u
 // if t is the first subtree under its covering top-level leaf; tile_src[t] =
 // decode source of a reached root (kNoSrc: none).
 constexpr uint32_t kEmit = 0x100u;
+constexpr uint32_t kTileSub = 0x200u;  // the subtree is on FV1's tile path: no list-A leaves emitted
 
 __device__ __forceinline__ void k3_publish(Ctl* ctl, unsigned long long epoch) {
     __syncthreads();
@@ -1658,6 +1666,10 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     // non-reached subtree below it stops at and the decode source
     uint32_t* ssrc = sres + 4 * nt;
     uint8_t* sdep = reinterpret_cast<uint8_t*>(ssrc + (R >= 1 ? (1u << (2 * (R - 1))) : 1u));
+    // (tiles: subtrees FV1 updates on its tile path, hot path of a staged top only)
+    uint8_t* stl = sdep + (((R >= 1 ? (1u << (2 * (R - 1))) : 1u) + 15u) & ~15u);
+    const bool tiles = !EXPORT && staged_out && P.tiles;
+    __shared__ unsigned s_ntile;
     const bool cnt_smem = nt <= 1024u;
     const uint32_t* cnt = cnt_smem ? scnt : P.tile_cnt;
     const uint32_t al = P.G == 1 ? 16u : P.pb_align;
@@ -1858,9 +1870,29 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     const uint32_t per = (nt + kThreads - 1) / kThreads;
     const uint32_t a = threadIdx.x * per;
     const uint32_t b = min(nt, a + per);
+    // FV1 tile path (k_fv1 fv1_tile_strip): a reached subtree whose 4^K
+    // level-L cells are all leaves and whose neighbourhood holds a wet cell
+    // (or touches an inflow edge) is updated as a 64 x 64 block; its leaves
+    // leave list A (counted in n_leaves all the same) and it joins P.stile
+    if (tiles) {
+        if (threadIdx.x == 0) s_ntile = 0u;
+        __syncthreads();
+        for (uint32_t t = a; t < b; ++t) {
+            bool act = swet[t] != 0;
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+                const uint32_t nb = zo::neighbour_dev(R, t, static_cast<zo::Direction>(d));
+                act = act || (nb == zo::kNone ? P.bc[d] == 2 : swet[nb] != 0);
+            }
+            const bool tl = act && reach[t] && cnt[t] == (1u << (2 * P.K));
+            stl[t] = tl ? 1 : 0;
+            if (tl) P.stile[atomicAdd(&s_ntile, 1u)] = t;  // (any order: each strip job writes its own cells)
+        }
+        __syncthreads();
+    }
     auto counts = [&](uint32_t t, unsigned& ca, unsigned& cb) {
         const bool r = reach[t] != 0;
-        ca = r ? cnt[t] : 0u;
+        ca = (r && !(tiles && stl[t])) ? cnt[t] : 0u;
         cb = r ? cnt[nt + t] : cbf[t];
     };
     unsigned la = 0, lb = 0;
@@ -1928,7 +1960,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
             if (staged_out) {  // (staged in shared memory, written out coalesced below)
                 sres[t] = oa;
                 sres[nt + t] = ta + ob;
-                sres[2 * nt + t] = static_cast<uint32_t>(n) | (cbf[t] ? kEmit : 0u);
+                sres[2 * nt + t] = static_cast<uint32_t>(n) | (cbf[t] ? kEmit : 0u) | ((tiles && stl[t]) ? kTileSub : 0u);
                 sres[3 * nt + t] = src;
             } else {
                 const unsigned long long tag = (epoch & 0xFFFFFFFFull) << 32;
@@ -1996,8 +2028,11 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     }
     if (threadIdx.x == 0) {  // (block_exscan above: s_off complete)
         if (tn && P.part == 0) atomicAdd(&ctl->cnt_new, (unsigned long long)tn);
-        ctl->n_leaves = ta + tb;
+        const uint32_t ntl = tiles ? s_ntile : 0u;
+        ctl->n_leaves = ta + tb + (ntl << (2 * P.K));  // (tiled subtrees' level-L leaves are off list A)
         ctl->n_leaves_A = ta;
+        ctl->n_stile = ntl;
+        ctl->cnt_tiled += static_cast<unsigned long long>(ntl) << (2 * P.K);
         // this partition's slices of the A and B lists
         ctl->a_lo = s_off[0];
         ctl->a_hi = s_off[2];
@@ -2212,7 +2247,8 @@ __device__ void k3_tile(const Params& P, Ctl* ctl, int p, int tbuf, unsigned lon
         else P.leaves[ob++] = z;
     };
     const uint32_t gbase = j * ng;
-    for (uint32_t t = a; t < b; ++t) {
+    const bool tiled = !EXPORT && (lvl & kTileSub);  // (fully refined: every leaf is a level-L one, on the tile path)
+    for (uint32_t t = a; t < b && !tiled; ++t) {
         const int k = walk(t);
         const uint32_t gm = gbase + t;
         if (k <= Gk) {
@@ -2365,6 +2401,7 @@ __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ct
         ctl->rate_bits[slot] = 0ull;
         ctl->done_k5 = 0;
         ctl->fv1_tail = 0u;
+        ctl->fv1_tjob = 0u;
         if (advance) {  // this step's near-threshold count is complete (K1, K2 and the previous FV1 are done)
             const unsigned long long nn = ctl->near_step[slot];
             ctl->near_last = nn;
@@ -2492,6 +2529,158 @@ __device__ __forceinline__ double4* covering(const Params& P, int cur, int k, ui
     return cell_ptr(P, cur, k, mm);
 }
 
+// ------------------------------------------------------------ FV1 tile path
+// A face's result as both of its cells use it: the HLL flux and the two
+// reconstructed depths (the west / south cell takes hL for its bed
+// correction, the east / north cell hR; D12).
+struct FaceR {
+    double F0, F1, F2, hL, hR;
+};
+__device__ __forceinline__ FaceR face_r(const CellV& Lc, const CellV& Rc, bool xface, const PhysParams& p) {
+    FaceR r;
+    double F[3];
+    face(Lc, Rc, xface, p, F, r.hL, r.hR);
+    r.F0 = F[0];
+    r.F1 = F[1];
+    r.F2 = F[2];
+    return r;
+}
+__device__ __forceinline__ FaceR shfl_face(const FaceR& f, int src) {
+    return {__shfl_sync(kFull, f.F0, src), __shfl_sync(kFull, f.F1, src), __shfl_sync(kFull, f.F2, src),
+            __shfl_sync(kFull, f.hL, src), __shfl_sync(kFull, f.hR, src)};
+}
+__device__ __forceinline__ CellV shfl_cell(const CellV& c, int src) {
+    CellV o;
+    o.h = __shfl_sync(kFull, c.h, src);
+    o.qx = __shfl_sync(kFull, c.qx, src);
+    o.qy = __shfl_sync(kFull, c.qy, src);
+    o.z = __shfl_sync(kFull, c.z, src);
+    o.ux = __shfl_sync(kFull, c.ux, src);
+    o.uy = __shfl_sync(kFull, c.uy, src);
+    o.c = __shfl_sync(kFull, c.c, src);
+    return o;
+}
+// the direction-d neighbour of level-L leaf m as the per-leaf path sees it:
+// the same-level cell, the coarser covering leaf or the
+// boundary ghost (no inactive cells on the tile path)
+__device__ __forceinline__ CellV nb_cell(const Params& P, const double4* cur, const uint8_t* sigc, uint32_t m,
+                                         const CellV& own, int d, double inflow) {
+    const int L = P.L;
+    const uint32_t nm = zo::neighbour_dev(L, m, static_cast<zo::Direction>(d));
+    if (nm == zo::kNone) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, P.phys);
+    const double4* s = sigc[slo(L - 1) + (nm >> 2)] ? cur + cbase(L) + nm : covering_local(P, cur, sigc, L - 1, nm >> 2);
+    return make_cell(ld4_nc(s), P.phys);
+}
+// L_c + Euler + friction of a cell from its four faces: the expressions and
+// their order are fv1_cell_seq's, so the bits are the per-leaf path's
+__device__ __forceinline__ void cell_update(const CellV& own, const FaceR& fE, const FaceR& fW, const FaceR& fN,
+                                            const FaceR& fS, double idx, double dt, const PhysParams& p, double& hn,
+                                            double& qxn, double& qyn) {
+    const double hh = own.h * own.h;
+    const double FE1 = fE.F1 + (p.half_g * (hh - (fE.hL * fE.hL)));
+    const double FW1 = fW.F1 + (p.half_g * (hh - (fW.hR * fW.hR)));
+    const double GN1 = fN.F1 + (p.half_g * (hh - (fN.hL * fN.hL)));
+    const double GS1 = fS.F1 + (p.half_g * (hh - (fS.hR * fS.hR)));
+    fv1_finish(own, fE.F0 - fW.F0, FE1 - FW1, fE.F2 - fW.F2, fN.F0 - fS.F0, GN1 - GS1, fN.F2 - fS.F2, idx, dt, p, hn,
+               qxn, qyn);
+}
+
+// One 32 x 4 strip (job: bits 0-3 row band, bit 4 column half) of a fully
+// refined active subtree `tile` (K = 6: 64 x 64 level-L leaves), one warp,
+// lane = column. Every face is computed once for both of its cells — x-faces
+// by the east cell (its west face, handed to the west cell by a shuffle),
+// y-faces by the south cell (carried up the rows) — and every cell's
+// velocities / celerity once, instead of 4 faces and 5 make_cell per leaf.
+// The strip's edge faces (8 x-faces, one row of y-faces below it) come from
+// the neighbours the per-leaf path would use (nb_cell). Also the next
+// step's level-(L-1) re-encode of the strip's quads (rows 2k, 2k+1), the CFL
+// rates, the wet mark.
+__device__ __forceinline__ void fv1_tile_strip(const Params& P, Ctl* ctl, const double4* __restrict__ cur,
+                                            double4* __restrict__ nxt, const uint8_t* __restrict__ sigc,
+                                            uint32_t tile, uint32_t job, double dt, double inflow, int tbuf,
+                                            double& mx, unsigned& tree, unsigned& nnear) {
+    const int L = P.L, lane = threadIdx.x & 31;
+    const int xoff = (job & 16u) ? 32 : 0, r0 = 4 * static_cast<int>(job & 15u);
+    const uint32_t mb = tile << 12;
+    const double4* cl = cur + cbase(L);
+    const PhysParams& ph = P.phys;
+    const double idx = inv_dx_of(P, L);
+    auto mc = [&](int x, int y) { return mb | zo::interleave(static_cast<uint32_t>(x), static_cast<uint32_t>(y)); };
+    // the strip's edge x-faces: lanes 0-3 the east face of row r0 + lane,
+    // lanes 4-7 the west face of row r0 + lane - 4
+    FaceR fb = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (lane < 8) {
+        const bool east = lane < 4;
+        const uint32_t me = mc(east ? xoff + 31 : xoff, r0 + (lane & 3));
+        const CellV own = make_cell(ld4_nc(cl + me), ph);
+        const CellV nb = nb_cell(P, cur, sigc, me, own, east ? 1 : 0, inflow);
+        fb = east ? face_r(own, nb, true, ph) : face_r(nb, own, true, ph);
+    }
+    const int x = xoff + lane;
+    uint32_t m = mc(x, r0);
+    CellV C = make_cell(ld4_nc(cl + m), ph);
+    FaceR fS;
+    {
+        const CellV S = (r0 > 0) ? make_cell(ld4_nc(cl + mc(x, r0 - 1)), ph) : nb_cell(P, cur, sigc, m, C, 3, inflow);
+        fS = face_r(S, C, false, ph);
+    }
+    double ph0 = 0.0, pq0 = 0.0, pr0 = 0.0, pz0 = 0.0;  // the even row's new state (quad re-encode)
+    uint32_t pm0 = 0;
+    bool wet = false;
+#pragma unroll 1
+    for (int k = 0; k < 4; ++k) {
+        const int r = r0 + k;
+        const bool inner = r + 1 < 64;
+        const uint32_t mn = inner ? mc(x, r + 1) : 0u;
+        const CellV N = inner ? make_cell(ld4_nc(cl + mn), ph) : nb_cell(P, cur, sigc, m, C, 2, inflow);
+        const FaceR fN = face_r(C, N, false, ph);
+        FaceR fW = face_r(shfl_cell(C, (lane + 31) & 31), C, true, ph);  // (lane 0: replaced by the edge face)
+        const FaceR bw = shfl_face(fb, 4 + k), be = shfl_face(fb, k);
+        if (lane == 0) fW = bw;
+        FaceR fE = shfl_face(fW, (lane + 1) & 31);
+        if (lane == 31) fE = be;
+        double hn, qxn, qyn;
+        cell_update(C, fE, fW, fN, fS, idx, dt, ph, hn, qxn, qyn);
+        if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))
+            report_error(ctl, kErrNonFinite, zo::z_of(L, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2), kStageFV1);
+        st4(nxt + cbase(L) + m, make_double4(hn, qxn, qyn, C.z));
+        const double c = cfl_rate(hn, qxn, qyn, idx, ph);
+        mx = c > mx ? c : mx;
+        wet = wet || !(hn < ph.hdry);
+        // next step's zero_details_and_reencode of level L-1 (the per-leaf
+        // path's fused re-encode): quad (2i, r-1), (2i+1, r-1), (2i, r), (2i+1, r)
+        if (k & 1) {
+            const int o = lane | 1;
+            double4 ch[4];
+            ch[0] = make_double4(ph0, pq0, pr0, pz0);
+            ch[1] = make_double4(__shfl_sync(kFull, ph0, o), __shfl_sync(kFull, pq0, o), __shfl_sync(kFull, pr0, o),
+                                 __shfl_sync(kFull, pz0, o));
+            ch[2] = make_double4(hn, qxn, qyn, C.z);
+            ch[3] = make_double4(__shfl_sync(kFull, hn, o), __shfl_sync(kFull, qxn, o), __shfl_sync(kFull, qyn, o),
+                                 __shfl_sync(kFull, C.z, o));
+            if (!(lane & 1)) {
+                const Enc e = encode_children<false>(ch, P, L - 1);
+                const uint32_t pm = pm0 >> 2;
+                st4(nxt + cbase(L - 1) + pm, e.par);
+                const unsigned long long fi = slo(L - 1) + pm;
+                P.pre[fi] = (e.flow || P.dem[fi]) ? 1 : 0;
+                ++tree;
+                nnear += e.near ? 1u : 0u;
+            }
+        } else {
+            ph0 = hn;
+            pq0 = qxn;
+            pr0 = qyn;
+            pz0 = C.z;
+            pm0 = m;
+        }
+        fS = fN;
+        C = N;
+        m = mn;
+    }
+    if (__any_sync(kFull, wet) && lane == 0) P.wet[tbuf ^ 1][tile] = 1;
+}
+
 // FV1 over the leaf list: persistent grid-stride, one thread per
 // leaf; reads the current buffer, writes leaf slots of the other (D15).
 // STAGE 0: next iteration's own cell prefetched into L2; 2: loaded into
@@ -2503,7 +2692,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     pdl_trigger();
     // control words, read once per CTA (line 0 of Ctl)
     __shared__ double s_td[2];
-    __shared__ uint32_t s_u[6];
+    __shared__ uint32_t s_u[7];
     if (threadIdx.x == 0) {
         const volatile Ctl* vc = ctl;
         s_td[0] = vc->t;
@@ -2511,6 +2700,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
         s_u[0] = static_cast<uint32_t>(vc->parity);
         s_u[1] = static_cast<uint32_t>(vc->step & 1);
         s_u[2] = vc->a_lo; s_u[3] = vc->a_hi; s_u[4] = vc->b_lo; s_u[5] = vc->b_hi;
+        s_u[6] = vc->n_stile;
     }
     __syncthreads();
     const double t = s_td[0], dt = s_td[1];
@@ -2533,6 +2723,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     unsigned tree = 0, nnear = 0, ndem = 0, nquiet = 0;
     (void)ndem;
     const uint32_t stride = gridDim.x * kThreads;
+    // tile path first: 32 strip jobs per active fully refined subtree, taken
+    // one warp at a time from a per-step counter (the finalizing CTA resets it)
+    if (!UNIFORM && !PART && !INA && P.tiles) {
+        const uint32_t njobs = 32u * s_u[6];
+        for (;;) {
+            uint32_t jb = 0;
+            if (lane == 0) jb = atomicAdd(&ctl->fv1_tjob, 1u);
+            jb = __shfl_sync(kFull, jb, 0);
+            if (jb >= njobs) break;
+            fv1_tile_strip(P, ctl, cur, nxt, sigc, P.stile[jb >> 5], jb & 31u, dt, inflow, tbuf, mx, tree, nnear);
+        }
+    }
     // warp-uniform trip count: every lane runs every iteration (shuffles below)
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
     // STAGE 5 (= 3 + tail balancing): the last fv1_tail16 / 16 of the windows

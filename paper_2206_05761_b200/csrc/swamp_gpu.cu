@@ -497,6 +497,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     if ((st = dalloc(g, &P.wet[0], P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.wet[1], P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.tact, P.n_tiles))) return fail(st);
+    if ((st = dalloc(g, &P.stile, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     P.pdem[0] = P.dem;
     P.pwet[0][0] = P.wet[0];
     P.pwet[0][1] = P.wet[1];
@@ -638,6 +639,11 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             int smem_optin = 0;
             cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
             g->smem_k3top = std::max(k3_top_smem, static_cast<size_t>(smem_optin) - 8 * 1024);
+            // FV1 tile path (active fully refined subtrees as 64 x 64 blocks,
+            // every face once): one partition, K = 6, no inactive cells, the
+            // split K3 (its top lists the tiles); SWAMP_FV1_TILES=0 disables
+            const char* et = std::getenv("SWAMP_FV1_TILES");
+            P.tiles = (Ki == 6 && !P.has_ina && !(et && et[0] == '0')) ? 1 : 0;
         }
         struct {
             const void* f;
@@ -1511,10 +1517,10 @@ int swamp_gpu_work_counters(swamp_gpu* g, int64_t* out8) {
         acc[2] += static_cast<int64_t>(c.cnt_new);
         acc[3] = static_cast<int64_t>(c.cnt_updates);  // global leaf counts: every partition holds the same sum
         acc[4] += static_cast<int64_t>(c.cnt_quiet);
-        acc[5] = c.step;
+        acc[5] += static_cast<int64_t>(c.cnt_tiled);
+        acc[6] = c.step;
     }
-    acc[6] = static_cast<int64_t>(swamp::zorder::detail_cells(g->parts.empty() ? g->P.L : g->parts[0]->P.L));
-    acc[7] = static_cast<int64_t>(swamp::zorder::hierarchy_cells(g->parts.empty() ? g->P.L : g->parts[0]->P.L));
+    acc[7] = static_cast<int64_t>(swamp::zorder::detail_cells(g->parts.empty() ? g->P.L : g->parts[0]->P.L));
     std::memcpy(out8, acc, sizeof(acc));
     return SWAMP_OK;
 }

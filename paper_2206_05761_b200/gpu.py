@@ -256,8 +256,8 @@ class Engine:
         """Cumulative work counters (swamp_gpu_work_counters)."""
         a = (C.c_int64 * 8)()
         self._check(lib().swamp_gpu_work_counters(self._h, a), "work_counters")
-        keys = ("k1_reencoded", "fv1_reencoded", "decoded", "leaf_updates", "quiet_updates", "steps",
-                "detail_cells", "hierarchy_cells")
+        keys = ("k1_reencoded", "fv1_reencoded", "decoded", "leaf_updates", "quiet_updates", "tile_updates", "steps",
+                "detail_cells")
         return dict(zip(keys, (int(x) for x in a)))
 
     def launches_per_step(self) -> int:

@@ -196,6 +196,23 @@ def test_active_subtree_paths(monkeypatch, variant, name, kw):
             compare_states(g, o, f"{name} {variant} step {k}")
 
 
+@pytest.mark.parametrize("name,kw", [("river_flood", dict(L=9)), ("monai_runup", dict(L=9)),
+                                     ("circular_dambreak", dict(L=9, epsilon=0.0)), ("monai_runup", dict(L=7))])
+def test_tile_path_parity(name, kw):
+    """FV1's tile path (active fully refined subtrees updated as 64 x 64
+    blocks, every face computed once for both cells) == the oracle bitwise,
+    and it is actually taken."""
+    cfg, h, qx, qy, z = cases.CASES[name](**kw)
+    g = gpu.initialise(cfg, h, qx, qy, z)
+    o = O.Oracle(cfg, h, qx, qy, z)
+    for k in range(1, 21):
+        g.step_adaptive()
+        o.step()
+        if k in (1, 2, 10, 20):
+            compare_states(g, o, f"{name} tiles step {k}")
+    assert g.work()["tile_updates"] > 0, "no subtree took the tile path"
+
+
 MASKED = [
     ("rect humps dambreak L7", lambda: cases.rect_domain(cases.hump_dambreak, L=7)),
     ("rect quiescent humps L7", lambda: cases.rect_domain(cases.quiescent_humps, L=7)),
