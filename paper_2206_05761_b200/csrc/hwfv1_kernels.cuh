@@ -2585,6 +2585,16 @@ __device__ __forceinline__ void cell_update(const CellV& own, const FaceR& fE, c
                qxn, qyn);
 }
 
+// the direction-d neighbour of level-L leaf m outside the strip's subtree:
+// its source cell (same-level or coarser covering leaf), or null
+// for the domain edge (boundary ghost); `f` = the parent-level flag of the
+// same-level cell, loaded early by the caller
+__device__ __forceinline__ const double4* nb_src(const Params& P, const double4* cur, const uint8_t* sigc, uint32_t nm,
+                                                 uint8_t f) {
+    if (nm == zo::kNone) return nullptr;
+    return f ? cur + cbase(P.L) + nm : covering_local(P, cur, sigc, P.L - 1, nm >> 2);
+}
+
 // One 32 x 4 strip (job: bits 0-3 row band, bit 4 column half) of a fully
 // refined active subtree `tile` (K = 6: 64 x 64 level-L leaves), one warp,
 // lane = column. Every face is computed once for both of its cells — x-faces
@@ -2592,13 +2602,15 @@ __device__ __forceinline__ void cell_update(const CellV& own, const FaceR& fE, c
 // y-faces by the south cell (carried up the rows) — and every cell's
 // velocities / celerity once, instead of 4 faces and 5 make_cell per leaf.
 // The strip's edge faces (8 x-faces, one row of y-faces below it) come from
-// the neighbours the per-leaf path would use (nb_cell). Also the next
-// step's level-(L-1) re-encode of the strip's quads (rows 2k, 2k+1), the CFL
-// rates, the wet mark.
+// the neighbours the per-leaf path would use. Every load of the strip (its
+// 4 rows, the rows below and above, the edge columns; outside the subtree
+// the neighbours' parent-level flags first) is issued before any
+// arithmetic. Also the next step's level-(L-1) re-encode of the strip's
+// quads (rows 2k, 2k+1), the CFL rates, the wet mark.
 __device__ __forceinline__ void fv1_tile_strip(const Params& P, Ctl* ctl, const double4* __restrict__ cur,
-                                            double4* __restrict__ nxt, const uint8_t* __restrict__ sigc,
-                                            uint32_t tile, uint32_t job, double dt, double inflow, int tbuf,
-                                            double& mx, unsigned& tree, unsigned& nnear) {
+                                               double4* __restrict__ nxt, const uint8_t* __restrict__ sigc,
+                                               uint32_t tile, uint32_t job, double dt, double inflow, int tbuf,
+                                               double& mx, unsigned& tree, unsigned& nnear) {
     const int L = P.L, lane = threadIdx.x & 31;
     const int xoff = (job & 16u) ? 32 : 0, r0 = 4 * static_cast<int>(job & 15u);
     const uint32_t mb = tile << 12;
@@ -2606,33 +2618,80 @@ __device__ __forceinline__ void fv1_tile_strip(const Params& P, Ctl* ctl, const 
     const PhysParams& ph = P.phys;
     const double idx = inv_dx_of(P, L);
     auto mc = [&](int x, int y) { return mb | zo::interleave(static_cast<uint32_t>(x), static_cast<uint32_t>(y)); };
-    // the strip's edge x-faces: lanes 0-3 the east face of row r0 + lane,
-    // lanes 4-7 the west face of row r0 + lane - 4
+    const int x = xoff + lane;
+    // ---- loads: this column's rows r0-1 .. r0+4 (those inside the subtree)
+    double4 rw[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        const int y = r0 - 1 + i;
+        rw[i] = (y >= 0 && y < 64) ? ld4_nc(cl + mc(x, y)) : make_double4(0.0, 0.0, 0.0, 0.0);
+    }
+    // edge lanes: 0-3 the east edge of row r0 + lane, 4-7 the west edge of
+    // row r0 + lane - 4 — the strip's own edge cell and its neighbour
+    const bool east = lane < 4;
+    const int ex = east ? xoff + 31 : xoff, er = r0 + (lane & 3);
+    const uint32_t em = mc(ex, er);
+    const int nx = east ? ex + 1 : ex - 1;  // neighbour column
+    const bool e_in = nx >= 0 && nx < 64;
+    double4 eo = make_double4(0.0, 0.0, 0.0, 0.0), en = eo;
+    uint32_t enm = zo::kNone;
+    uint8_t ef = 1;
+    if (lane < 8) {
+        eo = ld4_nc(cl + em);
+        if (e_in) {
+            en = ld4_nc(cl + mc(nx, er));
+        } else {
+            enm = zo::neighbour_dev(L, em, east ? zo::Direction::East : zo::Direction::West);
+            if (enm != zo::kNone) ef = sigc[slo(L - 1) + (enm >> 2)];
+        }
+    }
+    // rows outside the subtree (r0 = 0: below; r0 = 60: above)
+    const bool s_out = r0 == 0, n_out = r0 + 4 >= 64;
+    uint32_t snm = zo::kNone, nnm = zo::kNone;
+    uint8_t sf = 1, nf = 1;
+    if (s_out) {
+        snm = zo::neighbour_dev(L, mc(x, r0), zo::Direction::South);
+        if (snm != zo::kNone) sf = sigc[slo(L - 1) + (snm >> 2)];
+    }
+    if (n_out) {
+        nnm = zo::neighbour_dev(L, mc(x, r0 + 3), zo::Direction::North);
+        if (nnm != zo::kNone) nf = sigc[slo(L - 1) + (nnm >> 2)];
+    }
+    // second round trip only at subtree edges: the outside neighbours' cells
+    const double4* esrc = nullptr;
+    if (lane < 8 && !e_in) {
+        esrc = nb_src(P, cur, sigc, enm, ef);
+        if (esrc) en = ld4_nc(esrc);
+    }
+    const double4* ssrc = s_out ? nb_src(P, cur, sigc, snm, sf) : nullptr;
+    if (ssrc) rw[0] = ld4_nc(ssrc);
+    const double4* nsrc = n_out ? nb_src(P, cur, sigc, nnm, nf) : nullptr;
+    if (nsrc) rw[5] = ld4_nc(nsrc);
+
+    // ---- edge x-faces
     FaceR fb = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (lane < 8) {
-        const bool east = lane < 4;
-        const uint32_t me = mc(east ? xoff + 31 : xoff, r0 + (lane & 3));
-        const CellV own = make_cell(ld4_nc(cl + me), ph);
-        const CellV nb = nb_cell(P, cur, sigc, me, own, east ? 1 : 0, inflow);
+        const CellV own = make_cell(eo, ph);
+        const CellV nb = (!e_in && !esrc) ? boundary_cell(own, P.bc[east ? 1 : 0], east ? 1 : 0, inflow, P.inflow_mode, ph)
+                                          : make_cell(en, ph);
         fb = east ? face_r(own, nb, true, ph) : face_r(nb, own, true, ph);
     }
-    const int x = xoff + lane;
     uint32_t m = mc(x, r0);
-    CellV C = make_cell(ld4_nc(cl + m), ph);
+    CellV C = make_cell(rw[1], ph);
     FaceR fS;
     {
-        const CellV S = (r0 > 0) ? make_cell(ld4_nc(cl + mc(x, r0 - 1)), ph) : nb_cell(P, cur, sigc, m, C, 3, inflow);
+        const CellV S = (s_out && !ssrc) ? boundary_cell(C, P.bc[3], 3, inflow, P.inflow_mode, ph) : make_cell(rw[0], ph);
         fS = face_r(S, C, false, ph);
     }
     double ph0 = 0.0, pq0 = 0.0, pr0 = 0.0, pz0 = 0.0;  // the even row's new state (quad re-encode)
     uint32_t pm0 = 0;
     bool wet = false;
-#pragma unroll 1
+#pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int r = r0 + k;
-        const bool inner = r + 1 < 64;
-        const uint32_t mn = inner ? mc(x, r + 1) : 0u;
-        const CellV N = inner ? make_cell(ld4_nc(cl + mn), ph) : nb_cell(P, cur, sigc, m, C, 2, inflow);
+        const uint32_t mn = mc(x, r + 1);  // (k = 3 at the subtree's top: unused)
+        const CellV N = (k == 3 && n_out && !nsrc) ? boundary_cell(C, P.bc[2], 2, inflow, P.inflow_mode, ph)
+                                                   : make_cell(rw[k + 2], ph);
         const FaceR fN = face_r(C, N, false, ph);
         FaceR fW = face_r(shfl_cell(C, (lane + 31) & 31), C, true, ph);  // (lane 0: replaced by the edge face)
         const FaceR bw = shfl_face(fb, 4 + k), be = shfl_face(fb, k);
@@ -2727,12 +2786,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     // one warp at a time from a per-step counter (the finalizing CTA resets it)
     if (!UNIFORM && !PART && !INA && P.tiles) {
         const uint32_t njobs = 32u * s_u[6];
-        for (;;) {
-            uint32_t jb = 0;
-            if (lane == 0) jb = atomicAdd(&ctl->fv1_tjob, 1u);
-            jb = __shfl_sync(kFull, jb, 0);
-            if (jb >= njobs) break;
-            fv1_tile_strip(P, ctl, cur, nxt, sigc, P.stile[jb >> 5], jb & 31u, dt, inflow, tbuf, mx, tree, nnear);
+        uint32_t jb = 0;
+        if (lane == 0 && njobs) jb = atomicAdd(&ctl->fv1_tjob, 1u);
+        jb = __shfl_sync(kFull, jb, 0);
+        uint32_t jt = (jb < njobs) ? P.stile[jb >> 5] : 0u;
+        while (jb < njobs) {
+            // the next job's id is fetched while this one computes
+            uint32_t jn = 0;
+            if (lane == 0) jn = atomicAdd(&ctl->fv1_tjob, 1u);
+            fv1_tile_strip(P, ctl, cur, nxt, sigc, jt, jb & 31u, dt, inflow, tbuf, mx, tree, nnear);
+            jb = __shfl_sync(kFull, jn, 0);
+            if (jb < njobs) jt = P.stile[jb >> 5];
         }
     }
     // warp-uniform trip count: every lane runs every iteration (shuffles below)

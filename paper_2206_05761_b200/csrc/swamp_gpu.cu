@@ -504,11 +504,16 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     P.has_ina = cfg->inactive ? 1 : 0;
     if (P.has_ina && (st = dalloc(g, &P.ina, hwfv1::slo(L + 1) + 16))) return fail(st);
     // every subtree counts as wet until FV1 has run once
-    cudaMemset(P.wet[0], 1, P.n_tiles);
-    cudaMemset(P.wet[1], 1, P.n_tiles);
-    cudaMemset(P.tact, 1, P.n_tiles);
+    cudaMemsetAsync(P.wet[0], 1, P.n_tiles, g->stream);
+    cudaMemsetAsync(P.wet[1], 1, P.n_tiles, g->stream);
+    cudaMemsetAsync(P.tact, 1, P.n_tiles, g->stream);
     if ((st = dalloc(g, &P.tile_src, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.k3_rec, P.n_tiles * 4 * sizeof(unsigned long long)))) return fail(st);
+    // K3's per-subtree records carry an epoch tag (2 step + 2, so initialise's
+    // K3 polls for tag 2): a block reused from the cache may hold records of
+    // an engine that stopped after its first step, which that poll would
+    // accept — clear them before anything runs
+    cudaMemsetAsync(P.k3_rec, 0, P.n_tiles * 4 * sizeof(unsigned long long), g->stream);
     if ((st = dalloc(g, &g->ctl, sizeof(Ctl)))) return fail(st);
     // peer tables: self only (a partitioned group fills in every partition)
     for (int b = 0; b < 2; ++b) {
