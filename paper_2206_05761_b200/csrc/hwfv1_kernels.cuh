@@ -2782,22 +2782,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     unsigned tree = 0, nnear = 0, ndem = 0, nquiet = 0;
     (void)ndem;
     const uint32_t stride = gridDim.x * kThreads;
-    // tile path first: 32 strip jobs per active fully refined subtree, taken
-    // one warp at a time from a per-step counter (the finalizing CTA resets it)
+    // tile path first: 32 strip jobs per active fully refined subtree
     if (!UNIFORM && !PART && !INA && P.tiles) {
+        // static round robin over the warps (a per-job counter measured
+        // slower: thousands of same-address atomics queue at one L2 slice)
         const uint32_t njobs = 32u * s_u[6];
-        uint32_t jb = 0;
-        if (lane == 0 && njobs) jb = atomicAdd(&ctl->fv1_tjob, 1u);
-        jb = __shfl_sync(kFull, jb, 0);
-        uint32_t jt = (jb < njobs) ? P.stile[jb >> 5] : 0u;
-        while (jb < njobs) {
-            // the next job's id is fetched while this one computes
-            uint32_t jn = 0;
-            if (lane == 0) jn = atomicAdd(&ctl->fv1_tjob, 1u);
-            fv1_tile_strip(P, ctl, cur, nxt, sigc, jt, jb & 31u, dt, inflow, tbuf, mx, tree, nnear);
-            jb = __shfl_sync(kFull, jn, 0);
-            if (jb < njobs) jt = P.stile[jb >> 5];
-        }
+        const uint32_t nw = gridDim.x * (kThreads / 32);
+        for (uint32_t jb = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); jb < njobs; jb += nw)
+            fv1_tile_strip(P, ctl, cur, nxt, sigc, P.stile[jb >> 5], jb & 31u, dt, inflow, tbuf, mx, tree, nnear);
     }
     // warp-uniform trip count: every lane runs every iteration (shuffles below)
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);

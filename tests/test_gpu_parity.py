@@ -197,7 +197,8 @@ def test_active_subtree_paths(monkeypatch, variant, name, kw):
 
 
 @pytest.mark.parametrize("name,kw", [("river_flood", dict(L=9)), ("monai_runup", dict(L=9)),
-                                     ("circular_dambreak", dict(L=9, epsilon=0.0)), ("monai_runup", dict(L=7))])
+                                     ("circular_dambreak", dict(L=9, epsilon=0.0)),
+                                     ("circular_dambreak", dict(L=7, epsilon=0.0))])
 def test_tile_path_parity(name, kw):
     """FV1's tile path (active fully refined subtrees updated as 64 x 64
     blocks, every face computed once for both cells) == the oracle bitwise,
