@@ -2784,12 +2784,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     const uint32_t stride = gridDim.x * kThreads;
     // tile path first: 32 strip jobs per active fully refined subtree
     if (!UNIFORM && !PART && !INA && P.tiles) {
-        // static round robin over the warps (a per-job counter measured
-        // slower: thousands of same-address atomics queue at one L2 slice)
+        // each CTA a contiguous range of the jobs (neighbouring strips: L2
+        // reuse of the rows they share), handed to its warps by a shared-
+        // memory counter (a grid-wide counter measured slower: thousands of
+        // same-address atomics queue at one L2 slice; a static warp round
+        // robin left whole SMs with a third job)
+        __shared__ unsigned s_tj;
         const uint32_t njobs = 32u * s_u[6];
-        const uint32_t nw = gridDim.x * (kThreads / 32);
-        for (uint32_t jb = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); jb < njobs; jb += nw)
+        const uint32_t j1 = static_cast<uint32_t>((static_cast<unsigned long long>(njobs) * (blockIdx.x + 1)) / gridDim.x);
+        if (threadIdx.x == 0)
+            s_tj = static_cast<uint32_t>((static_cast<unsigned long long>(njobs) * blockIdx.x) / gridDim.x);
+        __syncthreads();
+        for (;;) {
+            uint32_t jb = 0;
+            if (lane == 0) jb = atomicAdd(&s_tj, 1u);
+            jb = __shfl_sync(kFull, jb, 0);
+            if (jb >= j1) break;
             fv1_tile_strip(P, ctl, cur, nxt, sigc, P.stile[jb >> 5], jb & 31u, dt, inflow, tbuf, mx, tree, nnear);
+        }
     }
     // warp-uniform trip count: every lane runs every iteration (shuffles below)
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
@@ -2802,10 +2814,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     const uint32_t nwin = N / stride, ntail = (nwin * P.fv1_tail16 + 8u) >> 4;
     const uint32_t nstat = (TAIL && ntail > 0u && nwin > ntail) ? (nwin - ntail) * stride : N;  // (small lists: static)
     // one warp-iteration per grab (2 or 4 per grab measured slower at L = 11)
+    // a grab uses the counter value fetched one grab earlier and fetches the
+    // next one, so the atomic's round trip (long under contention: every warp
+    // of the grid hits this address) overlaps an iteration instead of
+    // stalling the warp; the last fetched value is never used
+    uint32_t pend = 0;
+    if (TAIL && lane == 0 && nstat < N) pend = atomicAdd(&ctl->fv1_tail, 1u);
     auto grab = [&]() -> uint32_t {
-        uint32_t c = 0;
-        if (lane == 0) c = atomicAdd(&ctl->fv1_tail, 1u);
-        c = __shfl_sync(kFull, c, 0);
+        const uint32_t c = __shfl_sync(kFull, pend, 0);
+        if (lane == 0) pend = atomicAdd(&ctl->fv1_tail, 1u);
         const uint32_t b = nstat + 32u * c;
         return b < N ? b : N;
     };
