@@ -2607,10 +2607,23 @@ __device__ __forceinline__ const double4* nb_src(const Params& P, const double4*
 // the neighbours' parent-level flags first) is issued before any
 // arithmetic. Also the next step's level-(L-1) re-encode of the strip's
 // quads (rows 2k, 2k+1), the CFL rates, the wet mark.
-__device__ __forceinline__ void fv1_tile_strip(const Params& P, Ctl* ctl, const double4* __restrict__ cur,
-                                               double4* __restrict__ nxt, const uint8_t* __restrict__ sigc,
-                                               uint32_t tile, uint32_t job, double dt, double inflow, int tbuf,
-                                               double& mx, unsigned& tree, unsigned& nnear) {
+//
+// Code size matters (the per-leaf k_fv1 is instruction-cache bound once it
+// grows: the strip inlined into it quadrupled the kernel and cost more than
+// it saved), so the strips run in their own kernel, k_fv1_tiles, and their
+// rounds go through ONE copy of face() — per round a y-face and an x-face —
+// with the row loop not unrolled.
+struct TileOut {
+    double mx;
+    unsigned tree, nnear;
+};
+// `rows`: this warp's shared-memory slab of 6 x 32 cells (rows r0-1 .. r0+4
+// of the strip's columns), filled by cp.async when the job starts
+__device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, const double4* __restrict__ cur,
+                                                  double4* __restrict__ nxt, const uint8_t* __restrict__ sigc,
+                                                  uint32_t tile, uint32_t job, double dt, double inflow, int tbuf,
+                                                  double4* rows) {
+    TileOut out = {0.0, 0u, 0u};
     const int L = P.L, lane = threadIdx.x & 31;
     const int xoff = (job & 16u) ? 32 : 0, r0 = 4 * static_cast<int>(job & 15u);
     const uint32_t mb = tile << 12;
@@ -2619,19 +2632,24 @@ __device__ __forceinline__ void fv1_tile_strip(const Params& P, Ctl* ctl, const 
     const double idx = inv_dx_of(P, L);
     auto mc = [&](int x, int y) { return mb | zo::interleave(static_cast<uint32_t>(x), static_cast<uint32_t>(y)); };
     const int x = xoff + lane;
-    // ---- loads: this column's rows r0-1 .. r0+4 (those inside the subtree)
-    double4 rw[6];
-#pragma unroll
+    double4* my = rows + lane;  // row i at my[32 i]
+    // ---- loads, all issued before any arithmetic: this column's rows inside
+    //      the subtree by cp.async into the slab; at the subtree's edges the
+    //      outside neighbours' parent-level flags, then their cells
     for (int i = 0; i < 6; ++i) {
         const int y = r0 - 1 + i;
-        rw[i] = (y >= 0 && y < 64) ? ld4_nc(cl + mc(x, y)) : make_double4(0.0, 0.0, 0.0, 0.0);
+        if (y >= 0 && y < 64) {
+            const double4* g = cl + mc(x, y);
+            cp_async16(my + 32 * i, g);
+            cp_async16(reinterpret_cast<uint8_t*>(my + 32 * i) + 16, reinterpret_cast<const uint8_t*>(g) + 16);
+        }
     }
     // edge lanes: 0-3 the east edge of row r0 + lane, 4-7 the west edge of
     // row r0 + lane - 4 — the strip's own edge cell and its neighbour
     const bool east = lane < 4;
     const int ex = east ? xoff + 31 : xoff, er = r0 + (lane & 3);
     const uint32_t em = mc(ex, er);
-    const int nx = east ? ex + 1 : ex - 1;  // neighbour column
+    const int nx = east ? ex + 1 : ex - 1;
     const bool e_in = nx >= 0 && nx < 64;
     double4 eo = make_double4(0.0, 0.0, 0.0, 0.0), en = eo;
     uint32_t enm = zo::kNone;
@@ -2645,66 +2663,64 @@ __device__ __forceinline__ void fv1_tile_strip(const Params& P, Ctl* ctl, const 
             if (enm != zo::kNone) ef = sigc[slo(L - 1) + (enm >> 2)];
         }
     }
-    // rows outside the subtree (r0 = 0: below; r0 = 60: above)
     const bool s_out = r0 == 0, n_out = r0 + 4 >= 64;
-    uint32_t snm = zo::kNone, nnm = zo::kNone;
-    uint8_t sf = 1, nf = 1;
-    if (s_out) {
-        snm = zo::neighbour_dev(L, mc(x, r0), zo::Direction::South);
-        if (snm != zo::kNone) sf = sigc[slo(L - 1) + (snm >> 2)];
+    uint32_t onm = zo::kNone;  // the outside row's same-level cell (south / north)
+    uint8_t of = 1;
+    if (s_out || n_out) {
+        onm = zo::neighbour_dev(L, s_out ? mc(x, r0) : mc(x, r0 + 3), s_out ? zo::Direction::South : zo::Direction::North);
+        if (onm != zo::kNone) of = sigc[slo(L - 1) + (onm >> 2)];
     }
-    if (n_out) {
-        nnm = zo::neighbour_dev(L, mc(x, r0 + 3), zo::Direction::North);
-        if (nnm != zo::kNone) nf = sigc[slo(L - 1) + (nnm >> 2)];
-    }
-    // second round trip only at subtree edges: the outside neighbours' cells
-    const double4* esrc = nullptr;
+    bool e_wall = false, o_wall = false;  // domain edge: boundary ghost
     if (lane < 8 && !e_in) {
-        esrc = nb_src(P, cur, sigc, enm, ef);
-        if (esrc) en = ld4_nc(esrc);
+        const double4* s = nb_src(P, cur, sigc, enm, ef);
+        if (s) en = ld4_nc(s);
+        else e_wall = true;
     }
-    const double4* ssrc = s_out ? nb_src(P, cur, sigc, snm, sf) : nullptr;
-    if (ssrc) rw[0] = ld4_nc(ssrc);
-    const double4* nsrc = n_out ? nb_src(P, cur, sigc, nnm, nf) : nullptr;
-    if (nsrc) rw[5] = ld4_nc(nsrc);
+    if (s_out || n_out) {
+        const double4* s = nb_src(P, cur, sigc, onm, of);
+        if (s) my[s_out ? 0 : 160] = ld4_nc(s);
+        else o_wall = true;
+    }
+    cp_async_wait_all();
+    __syncwarp();
 
-    // ---- edge x-faces
-    FaceR fb = {0.0, 0.0, 0.0, 0.0, 0.0};
-    if (lane < 8) {
-        const CellV own = make_cell(eo, ph);
-        const CellV nb = (!e_in && !esrc) ? boundary_cell(own, P.bc[east ? 1 : 0], east ? 1 : 0, inflow, P.inflow_mode, ph)
-                                          : make_cell(en, ph);
-        fb = east ? face_r(own, nb, true, ph) : face_r(nb, own, true, ph);
-    }
-    uint32_t m = mc(x, r0);
-    CellV C = make_cell(rw[1], ph);
-    FaceR fS;
+    // ---- prologue: the edge x-faces (lanes 0-7) and the y-faces below row r0
+    FaceR fb = {0.0, 0.0, 0.0, 0.0, 0.0}, fS;
+    CellV C = make_cell(my[32], ph);
     {
-        const CellV S = (s_out && !ssrc) ? boundary_cell(C, P.bc[3], 3, inflow, P.inflow_mode, ph) : make_cell(rw[0], ph);
+        const CellV own = make_cell(eo, ph);
+        const CellV nb = e_wall ? boundary_cell(own, P.bc[east ? 1 : 0], east ? 1 : 0, inflow, P.inflow_mode, ph)
+                                : make_cell(en, ph);
+        if (lane < 8) fb = east ? face_r(own, nb, true, ph) : face_r(nb, own, true, ph);
+        const CellV S = (s_out && o_wall) ? boundary_cell(C, P.bc[3], 3, inflow, P.inflow_mode, ph) : make_cell(my[0], ph);
         fS = face_r(S, C, false, ph);
     }
     double ph0 = 0.0, pq0 = 0.0, pr0 = 0.0, pz0 = 0.0;  // the even row's new state (quad re-encode)
     uint32_t pm0 = 0;
     bool wet = false;
-#pragma unroll
+#pragma unroll 1
     for (int k = 0; k < 4; ++k) {
-        const int r = r0 + k;
-        const uint32_t mn = mc(x, r + 1);  // (k = 3 at the subtree's top: unused)
-        const CellV N = (k == 3 && n_out && !nsrc) ? boundary_cell(C, P.bc[2], 2, inflow, P.inflow_mode, ph)
-                                                   : make_cell(rw[k + 2], ph);
+        const uint32_t m = mc(x, r0 + k);
+        const CellV N = (k == 3 && n_out && o_wall) ? boundary_cell(C, P.bc[2], 2, inflow, P.inflow_mode, ph)
+                                                    : make_cell(my[32 * (k + 2)], ph);
         const FaceR fN = face_r(C, N, false, ph);
         FaceR fW = face_r(shfl_cell(C, (lane + 31) & 31), C, true, ph);  // (lane 0: replaced by the edge face)
-        const FaceR bw = shfl_face(fb, 4 + k), be = shfl_face(fb, k);
-        if (lane == 0) fW = bw;
+        {
+            const FaceR bw = shfl_face(fb, 4 + k);
+            if (lane == 0) fW = bw;
+        }
         FaceR fE = shfl_face(fW, (lane + 1) & 31);
-        if (lane == 31) fE = be;
+        {
+            const FaceR be = shfl_face(fb, k);
+            if (lane == 31) fE = be;
+        }
         double hn, qxn, qyn;
         cell_update(C, fE, fW, fN, fS, idx, dt, ph, hn, qxn, qyn);
         if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))
             report_error(ctl, kErrNonFinite, zo::z_of(L, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2), kStageFV1);
         st4(nxt + cbase(L) + m, make_double4(hn, qxn, qyn, C.z));
         const double c = cfl_rate(hn, qxn, qyn, idx, ph);
-        mx = c > mx ? c : mx;
+        out.mx = c > out.mx ? c : out.mx;
         wet = wet || !(hn < ph.hdry);
         // next step's zero_details_and_reencode of level L-1 (the per-leaf
         // path's fused re-encode): quad (2i, r-1), (2i+1, r-1), (2i, r), (2i+1, r)
@@ -2723,8 +2739,8 @@ __device__ __forceinline__ void fv1_tile_strip(const Params& P, Ctl* ctl, const 
                 st4(nxt + cbase(L - 1) + pm, e.par);
                 const unsigned long long fi = slo(L - 1) + pm;
                 P.pre[fi] = (e.flow || P.dem[fi]) ? 1 : 0;
-                ++tree;
-                nnear += e.near ? 1u : 0u;
+                ++out.tree;
+                out.nnear += e.near ? 1u : 0u;
             }
         } else {
             ph0 = hn;
@@ -2735,9 +2751,93 @@ __device__ __forceinline__ void fv1_tile_strip(const Params& P, Ctl* ctl, const 
         }
         fS = fN;
         C = N;
-        m = mn;
     }
     if (__any_sync(kFull, wet) && lane == 0) P.wet[tbuf ^ 1][tile] = 1;
+    __syncwarp();  // (the slab is refilled by the next job)
+    return out;
+}
+
+// FV1 tile path kernel: the strips of the active fully refined subtrees K3's
+// top listed (P.stile, ctl->n_stile), before the per-leaf k_fv1 (which
+// waits for it and finalizes the step: the CFL rates of both go into the
+// same slot). Each CTA takes a contiguous range of the jobs (neighbouring
+// strips share rows through L2) and hands them to its warps by a shared-
+// memory counter (a grid-wide counter measured slower: thousands of
+// same-address atomics queue at one L2 slice).
+constexpr size_t kTileSlab = sizeof(double4) * 6 * 32 * (kThreads / 32);  // k_fv1_tiles dynamic shared memory
+__global__ void __launch_bounds__(kThreads, 2) k_fv1_tiles(Params P, Ctl* ctl) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ double s_td[2];
+    __shared__ uint32_t s_u[3];
+    __shared__ unsigned s_tj;
+    if (threadIdx.x == 0) {
+        const volatile Ctl* vc = ctl;
+        s_td[0] = vc->t;
+        s_td[1] = vc->dt;
+        s_u[0] = static_cast<uint32_t>(vc->parity);
+        s_u[1] = static_cast<uint32_t>(vc->step & 1);
+        s_u[2] = vc->n_stile;
+    }
+    __syncthreads();
+    const double t = s_td[0], dt = s_td[1];
+    const uint32_t njobs = 32u * s_u[2];
+    if (!(t < P.t_end) || njobs == 0u) return;
+    const int tbuf = static_cast<int>(s_u[1]);
+    tl_start(ctl, tbuf, 3);
+    const int p = static_cast<int>(s_u[0]);
+    const double4* __restrict__ cur = P.cells[p];
+    double4* __restrict__ nxt = P.cells[p ^ 1];
+    const uint8_t* __restrict__ sigc = P.sig[p ^ 1];
+    const double inflow = series_value(P, t);
+    const int lane = threadIdx.x & 31;
+    const uint32_t j1 = static_cast<uint32_t>((static_cast<unsigned long long>(njobs) * (blockIdx.x + 1)) / gridDim.x);
+    if (threadIdx.x == 0)
+        s_tj = static_cast<uint32_t>((static_cast<unsigned long long>(njobs) * blockIdx.x) / gridDim.x);
+    __syncthreads();
+    double mx = 0.0;
+    unsigned tree = 0, nnear = 0;
+    extern __shared__ __align__(16) double4 s_rows[];  // kTileSlab bytes: one 6 x 32-cell slab per warp
+    for (;;) {
+        uint32_t jb = 0;
+        if (lane == 0) jb = atomicAdd(&s_tj, 1u);
+        jb = __shfl_sync(kFull, jb, 0);
+        if (jb >= j1) break;
+        const TileOut to = fv1_tile_strip(P, ctl, cur, nxt, sigc, P.stile[jb >> 5], jb & 31u, dt, inflow, tbuf,
+                                          s_rows + (threadIdx.x >> 5) * (6 * 32));
+        mx = to.mx > mx ? to.mx : mx;
+        tree += to.tree;
+        nnear += to.nnear;
+    }
+    // the CFL rates (exact u64 max into this step's slot; k_fv1 finalizes),
+    // the fused re-encode and near-threshold counts
+    __shared__ unsigned long long s_m[kThreads / 32];
+    __shared__ unsigned s_c[2][kThreads / 32];
+    unsigned long long b = warp_max_u64(static_cast<unsigned long long>(__double_as_longlong(mx)));
+    unsigned c0 = tree, c1 = nnear;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        c0 += __shfl_xor_sync(kFull, c0, o);
+        c1 += __shfl_xor_sync(kFull, c1, o);
+    }
+    if (lane == 0) {
+        s_m[threadIdx.x >> 5] = b;
+        s_c[0][threadIdx.x >> 5] = c0;
+        s_c[1][threadIdx.x >> 5] = c1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long m = 0;
+        unsigned long long n0 = 0, n1 = 0;
+        for (int w = 0; w < kThreads / 32; ++w) {
+            m = s_m[w] > m ? s_m[w] : m;
+            n0 += s_c[0][w];
+            n1 += s_c[1][w];
+        }
+        if (m) atomicMax(&ctl->rate_bits[tbuf], m);
+        if (n0) atomicAdd(&ctl->cnt_fused, n0);
+        if (n1) atomicAdd(&ctl->near_step[tbuf ^ 1], n1);
+    }
 }
 
 // FV1 over the leaf list: persistent grid-stride, one thread per
@@ -2782,27 +2882,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     unsigned tree = 0, nnear = 0, ndem = 0, nquiet = 0;
     (void)ndem;
     const uint32_t stride = gridDim.x * kThreads;
-    // tile path first: 32 strip jobs per active fully refined subtree
-    if (!UNIFORM && !PART && !INA && P.tiles) {
-        // each CTA a contiguous range of the jobs (neighbouring strips: L2
-        // reuse of the rows they share), handed to its warps by a shared-
-        // memory counter (a grid-wide counter measured slower: thousands of
-        // same-address atomics queue at one L2 slice; a static warp round
-        // robin left whole SMs with a third job)
-        __shared__ unsigned s_tj;
-        const uint32_t njobs = 32u * s_u[6];
-        const uint32_t j1 = static_cast<uint32_t>((static_cast<unsigned long long>(njobs) * (blockIdx.x + 1)) / gridDim.x);
-        if (threadIdx.x == 0)
-            s_tj = static_cast<uint32_t>((static_cast<unsigned long long>(njobs) * blockIdx.x) / gridDim.x);
-        __syncthreads();
-        for (;;) {
-            uint32_t jb = 0;
-            if (lane == 0) jb = atomicAdd(&s_tj, 1u);
-            jb = __shfl_sync(kFull, jb, 0);
-            if (jb >= j1) break;
-            fv1_tile_strip(P, ctl, cur, nxt, sigc, P.stile[jb >> 5], jb & 31u, dt, inflow, tbuf, mx, tree, nnear);
-        }
-    }
     // warp-uniform trip count: every lane runs every iteration (shuffles below)
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
     // STAGE 5 (= 3 + tail balancing): the last fv1_tail16 / 16 of the windows

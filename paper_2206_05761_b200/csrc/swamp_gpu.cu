@@ -266,6 +266,7 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
         launch_pdl(g->k3, P.n_tiles + 1, g->smem_k3, s, P, g->ctl, 0, 0ull);
     }
     mark(3);
+    if (P.tiles) launch_pdl(hwfv1::k_fv1_tiles, g->fv1_grid, hwfv1::kTileSlab, s, P, g->ctl);
     if (P.has_ina)  // D16 variant
         launch_pdl(hwfv1::k_fv1<false, false, true>, g->fv1_grid, 0, s, P, g->ctl);
     else if (g->fv1_stage == 2)
@@ -498,6 +499,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     if ((st = dalloc(g, &P.wet[1], P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.tact, P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.stile, P.n_tiles * sizeof(uint32_t)))) return fail(st);
+
     P.pdem[0] = P.dem;
     P.pwet[0][0] = P.wet[0];
     P.pwet[0][1] = P.wet[1];
@@ -661,7 +663,8 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
                      {reinterpret_cast<const void*>(g->k3), g->smem_k3},
                      {reinterpret_cast<const void*>(g->k3x), g->smem_k3},
                      {reinterpret_cast<const void*>(g->k3top), g->smem_k3top},
-                     {reinterpret_cast<const void*>(g->k3tiles), g->smem_k3tiles}};
+                     {reinterpret_cast<const void*>(g->k3tiles), g->smem_k3tiles},
+                     {reinterpret_cast<const void*>(hwfv1::k_fv1_tiles), hwfv1::kTileSlab}};
         for (auto& a : attrs)
             if (a.f && a.bytes > 48 * 1024 &&
                 cudaFuncSetAttribute(a.f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(a.bytes)) !=
