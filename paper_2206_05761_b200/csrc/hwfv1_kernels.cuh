@@ -1878,13 +1878,16 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         if (threadIdx.x == 0) s_ntile = 0u;
         __syncthreads();
         for (uint32_t t = a; t < b; ++t) {
-            bool act = swet[t] != 0;
+            // (the tile path computes every face — no per-cell dry
+            // shortcut — so only subtrees inside the wet region take it:
+            // the subtree and its face neighbours held wet cells)
+            bool inner = swet[t] != 0;
 #pragma unroll
             for (int d = 0; d < 4; ++d) {
                 const uint32_t nb = zo::neighbour_dev(R, t, static_cast<zo::Direction>(d));
-                act = act || (nb == zo::kNone ? P.bc[d] == 2 : swet[nb] != 0);
+                inner = inner && (nb == zo::kNone || swet[nb] != 0);
             }
-            const bool tl = act && reach[t] && cnt[t] == (1u << (2 * P.K));
+            const bool tl = inner && reach[t] && cnt[t] == (1u << (2 * P.K));
             stl[t] = tl ? 1 : 0;
             if (tl) P.stile[atomicAdd(&s_ntile, 1u)] = t;  // (any order: each strip job writes its own cells)
         }
@@ -2683,6 +2686,49 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
     }
     cp_async_wait_all();
     __syncwarp();
+    // a strip whose cells, rows above / below and edge neighbours are all dry
+    // (and no inflow ghost): every cell takes the per-leaf path's
+    // dry-neighbourhood result (h kept, q = 0), without faces
+    bool dry = true;
+#pragma unroll
+    for (int i = 0; i < 6; ++i)  // (a row beyond the domain edge is a ghost of the row next to it)
+        if (!(o_wall && ((i == 0 && s_out) || (i == 5 && n_out)))) dry = dry && my[32 * i].x < ph.hdry;
+    if (lane < 8) dry = dry && eo.x < ph.hdry && (e_wall ? P.bc[east ? 1 : 0] != 2 : en.x < ph.hdry);
+    if ((s_out || n_out) && o_wall) dry = dry && P.bc[s_out ? 3 : 2] != 2;
+    if (__all_sync(kFull, dry)) {
+        double ph0 = 0.0, pz0 = 0.0;
+        uint32_t pm0 = 0;
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t m = mc(x, r0 + k);
+            const double4 o4 = my[32 * (k + 1)];
+            const double hn = (o4.x < 0.0) ? 0.0 : o4.x;
+            st4(nxt + cbase(L) + m, make_double4(hn, 0.0, 0.0, o4.w));
+            if (k & 1) {
+                const int o = lane | 1;
+                double4 ch[4];
+                ch[0] = make_double4(ph0, 0.0, 0.0, pz0);
+                ch[1] = make_double4(__shfl_sync(kFull, ph0, o), 0.0, 0.0, __shfl_sync(kFull, pz0, o));
+                ch[2] = make_double4(hn, 0.0, 0.0, o4.w);
+                ch[3] = make_double4(__shfl_sync(kFull, hn, o), 0.0, 0.0, __shfl_sync(kFull, o4.w, o));
+                if (!(lane & 1)) {
+                    const Enc e = encode_children<false>(ch, P, L - 1);
+                    const uint32_t pm = pm0 >> 2;
+                    st4(nxt + cbase(L - 1) + pm, e.par);
+                    const unsigned long long fi = slo(L - 1) + pm;
+                    P.pre[fi] = (e.flow || P.dem[fi]) ? 1 : 0;
+                    ++out.tree;
+                    out.nnear += e.near ? 1u : 0u;
+                }
+            } else {
+                ph0 = hn;
+                pz0 = o4.w;
+                pm0 = m;
+            }
+        }
+        __syncwarp();
+        return out;
+    }
 
     // ---- prologue: the edge x-faces (lanes 0-7) and the y-faces below row r0
     FaceR fb = {0.0, 0.0, 0.0, 0.0, 0.0}, fS;

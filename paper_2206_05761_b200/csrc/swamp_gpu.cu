@@ -666,7 +666,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
                      {reinterpret_cast<const void*>(g->k3tiles), g->smem_k3tiles},
                      {reinterpret_cast<const void*>(hwfv1::k_fv1_tiles), hwfv1::kTileSlab}};
         for (auto& a : attrs)
-            if (a.f && a.bytes > 48 * 1024 &&
+            if (a.f && a.bytes >= 32 * 1024 &&
                 cudaFuncSetAttribute(a.f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(a.bytes)) !=
                     cudaSuccess)
                 return fail(SWAMP_E_CUDA);
