@@ -215,6 +215,13 @@ int swamp_gpu_export_tree(swamp_gpu* g, double* h, double* qx, double* qy, doubl
  * values, row-major south row first, length 4^L each. */
 int swamp_gpu_export_finest(swamp_gpu* g, double* h, double* qx, double* qy);
 
+/* Gauges ("gauge time series by point sampling the covering
+ * leaf"): for each of the n points (x[k], y[k]) (m, inside the domain
+ * square), the leaf covering the finest cell that holds the point. out:
+ * 4 n doubles, [h | qx | qy | eta = h + z] (physical). SWAMP_E_ARG for a
+ * point outside the square. Synchronises the engine's stream. */
+int swamp_gpu_sample_gauges(swamp_gpu* g, int32_t n, const double* x, const double* y, double* out);
+
 /* Device error word of the last failure: code, z-index, quantity, stage. */
 int swamp_gpu_last_error(const swamp_gpu* g, int32_t* code, uint32_t* z, int32_t* quantity,
                          int32_t* stage, char* msg, size_t msg_cap);

@@ -51,6 +51,23 @@ int swamp_io_load_dem(const swamp_raster* r, int L, double x0, double y0, double
 int swamp_io_write_finest(const char* path, int L, double x0, double y0, double W, const double* field,
                           const uint8_t* inactive, double nodata);
 
+/* write_gauges: CSV, header "t,<name>_h,<name>_qx,
+ * <name>_qy,<name>_eta,..." (names NULL: g0, g1, ...), then one record per
+ * sample time: values[k] holds the 4 n_gauges doubles swamp_gpu_sample_gauges
+ * wrote at times[k]. 17 significant digits. n_times = 0 (or n_gauges = 0):
+ * header-only file. */
+int swamp_io_write_gauges(const char* path, int32_t n_gauges, const char* const* names, int32_t n_times,
+                          const double* times, const double* values);
+
+/* write_step_report: CSV of StepReports, one record per
+ * step, columns in this stable order:
+ *   step,t,dt_used,dt_next,n_leaves,n_leaves_next,n_near_threshold,
+ *   ms_encode_flag,ms_band_closure,ms_decode_traverse,ms_neighbours,ms_fv1,ms_total
+ * `reports` points at n swamp_step_report structs (include/swamp_gpu.h);
+ * append != 0 appends records without a header. */
+struct swamp_step_report;
+int swamp_io_write_step_reports(const char* path, int32_t n, const struct swamp_step_report* reports, int append);
+
 #ifdef __cplusplus
 }
 #endif

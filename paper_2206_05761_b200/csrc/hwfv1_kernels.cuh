@@ -3366,6 +3366,24 @@ __global__ void k_export_finest(Params P, const Ctl* ctl, double* h, double* qx,
     }
 }
 
+// gauges ("point sampling the covering leaf"): the finest cell
+// (i, j) under each point, then the leaf covering it by the same flag walk as
+// the expansion; out = [h, qx, qy, eta = h + z] x n, physical
+__global__ void k_gauges(Params P, const Ctl* ctl, const uint32_t* cells, int n, double* out) {
+    const int p = ctl->parity;
+    for (int k = blockIdx.x * kThreads + threadIdx.x; k < n; k += gridDim.x * kThreads) {
+        const uint32_t c = cells[k];
+        const uint32_t m = zo::interleave(c & 0xFFFFu, c >> 16);
+        int lv = 0;
+        while (lv < P.L && sig_at(P, p, lv, m >> (2 * (P.L - lv)))) ++lv;
+        const double4 v = ld4(cell_ptr(P, p, lv, m >> (2 * (P.L - lv))));
+        out[k] = v.x;
+        out[n + k] = v.y;
+        out[2 * n + k] = v.z;
+        out[3 * n + k] = v.x + v.w;
+    }
+}
+
 // D16: inactive flags of level n from level n + 1 (bit 0 = all, bit 1 = any)
 __global__ void k_ina_level(Params P, int n) {
     const uint32_t cnt = 1u << (2 * n);

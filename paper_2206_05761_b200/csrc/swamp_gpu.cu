@@ -147,6 +147,7 @@ struct swamp_gpu {
     std::vector<void*> ipc_opened;
     bool serial = false;  // group on one device: all partitions on parts[0]'s stream
     void* scratch = nullptr;  // device scratch of export_finest (3 x 4^L doubles), lazily allocated
+    double x0 = 0.0, y0 = 0.0;  // lower-left corner of the domain (gauge sampling)
     size_t scratch_bytes = 0;
 
     ~swamp_gpu() {
@@ -450,6 +451,8 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     P.inflow_n = cfg->inflow_n;
     P.n_out = cfg->n_outputs;
     P.W = cfg->width;
+    g->x0 = cfg->x0;
+    g->y0 = cfg->y0;
     P.cfl = cfg->cfl;
     P.t_end = cfg->t_end;
     P.dt_fallback = cfg->dt_fallback;
@@ -1423,6 +1426,43 @@ int swamp_gpu_export_finest(swamp_gpu* g, double* h, double* qx, double* qy) {
     for (int q = 0; q < 3; ++q)
         if (outs[q]) CK(cudaMemcpyAsync(outs[q], d + q * nf, nf * sizeof(double), cudaMemcpyDeviceToHost, g->stream));
     CK(cudaStreamSynchronize(g->stream));
+    return SWAMP_OK;
+}
+
+int swamp_gpu_sample_gauges(swamp_gpu* g, int32_t n, const double* x, const double* y, double* out) {
+    if (!g || n < 0 || (n > 0 && (!x || !y || !out))) return SWAMP_E_ARG;
+    if (n == 0) return SWAMP_OK;
+    if (!g->parts.empty()) {
+        const int st = group_sync(g);
+        if (st) return st;
+        g = g->parts[0];
+    }
+    const uint32_t side = 1u << g->P.L;
+    std::vector<uint32_t> cells(static_cast<size_t>(n));
+    for (int32_t k = 0; k < n; ++k) {  // the finest cell whose closed-open square holds the point
+        const double fi = std::floor((x[k] - g->x0) / g->P.W * side), fj = std::floor((y[k] - g->y0) / g->P.W * side);
+        if (!(fi >= 0.0 && fi < side && fj >= 0.0 && fj < side)) {
+            g->err = "gauge " + std::to_string(k) + " outside the domain";
+            return SWAMP_E_ARG;
+        }
+        cells[static_cast<size_t>(k)] = static_cast<uint32_t>(fi) | (static_cast<uint32_t>(fj) << 16);
+    }
+    cudaSetDevice(g->device);
+    void* d = nullptr;
+    const size_t cb = cells.size() * sizeof(uint32_t), ob = 4 * static_cast<size_t>(n) * sizeof(double);
+    CK(cudaMallocAsync(&d, cb + ob, g->stream));
+    uint32_t* dc = static_cast<uint32_t*>(d);
+    double* dout = reinterpret_cast<double*>(static_cast<char*>(d) + ((cb + 15) & ~size_t(15)) - 0);
+    cudaError_t e = cudaMemcpyAsync(dc, cells.data(), cb, cudaMemcpyHostToDevice, g->stream);
+    if (e == cudaSuccess) {
+        hwfv1::k_gauges<<<std::max(1, std::min(g->num_sms, (n + kThreads - 1) / kThreads)), kThreads, 0, g->stream>>>(
+            g->P, g->ctl, dc, n, dout);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, ob, cudaMemcpyDeviceToHost, g->stream);
+    cudaFreeAsync(d, g->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+    CK(e);
     return SWAMP_OK;
 }
 

@@ -230,4 +230,49 @@ int swamp_io_write_finest(const char* path, int L, double x0, double y0, double 
     return swamp_io_write_esri(path, &r);
 }
 
+int swamp_io_write_gauges(const char* path, int32_t n_gauges, const char* const* names, int32_t n_times,
+                          const double* times, const double* values) {
+    if (!path || n_gauges < 0 || n_times < 0 || (n_times > 0 && n_gauges > 0 && (!times || !values)))
+        return SWAMP_E_ARG;
+    FILE* f = std::fopen(path, "w");
+    if (!f) return SWAMP_E_STATE;
+    std::fputs("t", f);
+    static const char* const q[4] = {"h", "qx", "qy", "eta"};
+    for (int32_t g = 0; g < n_gauges; ++g)
+        for (int k = 0; k < 4; ++k) {
+            if (names && names[g]) std::fprintf(f, ",%s_%s", names[g], q[k]);
+            else std::fprintf(f, ",g%d_%s", static_cast<int>(g), q[k]);
+        }
+    std::fputc('\n', f);
+    if (n_gauges > 0)
+        for (int32_t r = 0; r < n_times; ++r) {
+            std::fprintf(f, "%.17g", times[r]);
+            const double* v = values + static_cast<size_t>(r) * 4 * n_gauges;
+            for (int32_t g = 0; g < n_gauges; ++g)
+                for (int k = 0; k < 4; ++k) std::fprintf(f, ",%.17g", v[static_cast<size_t>(k) * n_gauges + g]);
+            std::fputc('\n', f);
+        }
+    const bool ok = std::ferror(f) == 0;
+    return (std::fclose(f) == 0 && ok) ? SWAMP_OK : SWAMP_E_STATE;
+}
+
+int swamp_io_write_step_reports(const char* path, int32_t n, const swamp_step_report* reports, int append) {
+    if (!path || n < 0 || (n > 0 && !reports)) return SWAMP_E_ARG;
+    FILE* f = std::fopen(path, append ? "a" : "w");
+    if (!f) return SWAMP_E_STATE;
+    if (!append)
+        std::fputs("step,t,dt_used,dt_next,n_leaves,n_leaves_next,n_near_threshold,ms_encode_flag,ms_band_closure,"
+                   "ms_decode_traverse,ms_neighbours,ms_fv1,ms_total\n",
+                   f);
+    for (int32_t k = 0; k < n; ++k) {
+        const swamp_step_report& r = reports[k];
+        std::fprintf(f, "%lld,%.17g,%.17g,%.17g,%lld,%lld,%lld,%.17g,%.17g,%.17g,%.17g,%.17g,%.17g\n",
+                     static_cast<long long>(r.step), r.t, r.dt_used, r.dt, static_cast<long long>(r.n_leaves),
+                     static_cast<long long>(r.n_leaves_next), static_cast<long long>(r.n_near_threshold),
+                     r.ms_encode_flag, r.ms_band_closure, r.ms_decode_traverse, r.ms_neighbours, r.ms_fv1, r.ms_total);
+    }
+    const bool ok = std::ferror(f) == 0;
+    return (std::fclose(f) == 0 && ok) ? SWAMP_OK : SWAMP_E_STATE;
+}
+
 }  // extern "C"

@@ -67,6 +67,7 @@ def lib():
         L.swamp_gpu_timeline.argtypes = [P, dp]
         L.swamp_gpu_debug.argtypes = [P, C.POINTER(C.c_uint64)]
         L.swamp_gpu_stream.argtypes = [P, C.POINTER(C.c_void_p)]
+        L.swamp_gpu_sample_gauges.argtypes = [P, C.c_int32, dp, dp, dp]
         L.swamp_gpu_build_info.restype = C.c_char_p
         _LIB = L
     return _LIB
@@ -80,7 +81,9 @@ EXPORTED_SYMBOLS = (
     "swamp_gpu_timeline", "swamp_gpu_create_partitioned", "swamp_gpu_debug",
     "swamp_gpu_rank_create", "swamp_gpu_rank_connect", "swamp_gpu_rank_ready", "swamp_gpu_compare",
     "swamp_gpu_rebalance", "swamp_gpu_trim_cache", "swamp_gpu_near_threshold", "swamp_gpu_work_counters",
+    "swamp_gpu_sample_gauges",
     "swamp_io_read_esri", "swamp_io_write_esri", "swamp_io_free_raster", "swamp_io_load_dem", "swamp_io_write_finest",
+    "swamp_io_write_gauges", "swamp_io_write_step_reports",
 )
 
 
@@ -211,6 +214,18 @@ class Engine:
             if a.dtype != np.float64 or not a.flags.c_contiguous or a.size != n * n:
                 raise ValueError("export_finest: out arrays must be C-contiguous float64 2^L x 2^L")
         self._check(lib().swamp_gpu_export_finest(self._h, *[dptr(a) for a in out]), "export_finest")
+        return out
+
+    def sample_gauges(self, xs, ys) -> np.ndarray:
+        """Gauges: (4, n) array [h, qx, qy, eta] of the leaves
+        covering the points (xs[k], ys[k])."""
+        x = as_f64(xs).reshape(-1)
+        y = as_f64(ys).reshape(-1)
+        if x.size != y.size:
+            raise ValueError("gauge x / y lengths differ")
+        out = np.zeros((4, x.size))
+        if x.size:
+            self._check(lib().swamp_gpu_sample_gauges(self._h, x.size, dptr(x), dptr(y), dptr(out)), "sample_gauges")
         return out
 
     def timeline(self):

@@ -59,6 +59,9 @@ def _lib():
                                         C.POINTER(C.c_double), C.POINTER(C.c_uint8)]
         L.swamp_io_write_finest.argtypes = [C.c_char_p, C.c_int, C.c_double, C.c_double, C.c_double,
                                             C.POINTER(C.c_double), C.POINTER(C.c_uint8), C.c_double]
+        L.swamp_io_write_gauges.argtypes = [C.c_char_p, C.c_int32, C.POINTER(C.c_char_p), C.c_int32,
+                                            C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.swamp_io_write_step_reports.argtypes = [C.c_char_p, C.c_int32, C.c_void_p, C.c_int]
         L._io_bound = True
     return L
 
@@ -103,5 +106,36 @@ def write_finest(path: str, field, L: int, x0: float, y0: float, W: float, inact
     st = _lib().swamp_io_write_finest(str(path).encode(), int(L), float(x0), float(y0), float(W),
                                       f.ctypes.data_as(C.POINTER(C.c_double)),
                                       None if ia is None else ia.ctypes.data_as(C.POINTER(C.c_uint8)), float(nodata))
+    if st != 0:
+        raise IoError(f"{path}: {STATUS.get(st, st)}")
+
+
+def write_gauges(path: str, times, samples, names=None) -> None:
+    """write_gauges (SPEC.md:583-590): `samples[k]` = the (4, n_gauges)
+    array Engine.sample_gauges returned at times[k]; one CSV record per time."""
+    t = np.ascontiguousarray(np.asarray(times, dtype=np.float64).reshape(-1))
+    ng = len(names) if names is not None else (np.asarray(samples[0]).shape[1] if len(samples) else 0)
+    v = np.ascontiguousarray(np.asarray(samples, dtype=np.float64).reshape(t.size, 4 * ng) if t.size else
+                             np.zeros(0))
+    nm = None
+    if names is not None:
+        nm = (C.c_char_p * ng)(*[str(x).encode() for x in names])
+    st = _lib().swamp_io_write_gauges(str(path).encode(), int(ng), nm, int(t.size),
+                                      t.ctypes.data_as(C.POINTER(C.c_double)), v.ctypes.data_as(C.POINTER(C.c_double)))
+    if st != 0:
+        raise IoError(f"{path}: {STATUS.get(st, st)}")
+
+
+def write_step_reports(path: str, reports, append: bool = False) -> None:
+    """write_step_report: StepReport dicts (Engine.step_adaptive
+    results) as CSV rows, columns in include/swamp_io.h's stable order."""
+    from .abi import swamp_step_report
+
+    arr = (swamp_step_report * max(1, len(reports)))()
+    for k, r in enumerate(reports):
+        for f, _ in swamp_step_report._fields_:
+            setattr(arr[k], f, r[f])
+    st = _lib().swamp_io_write_step_reports(str(path).encode(), len(reports), C.cast(arr, C.c_void_p),
+                                            1 if append else 0)
     if st != 0:
         raise IoError(f"{path}: {STATUS.get(st, st)}")

@@ -1,0 +1,91 @@
+"""run(config) -> outputs: gauges by point sampling the
+covering leaf, snapshots at the output times, the step-report CSV, and the
+CLI's run / compare / validate commands on the GPU engine."""
+import csv
+import json
+
+import numpy as np
+import pytest
+
+from paper_2206_05761_b200 import cases, io
+
+gpu = pytest.importorskip("paper_2206_05761_b200.gpu")
+pytestmark = pytest.mark.gpu
+
+
+def test_gauges_sample_the_covering_leaf():
+    cfg, h, qx, qy, z = cases.circular_dambreak(L=8)
+    e = gpu.initialise(cfg, h, qx, qy, z)
+    e.advance(30)
+    fh, fqx, fqy = e.export_finest()  # the expansion holds the covering leaf's value in every finest cell
+    rng = np.random.default_rng(0)
+    xs = cfg.x0 + rng.uniform(0, cfg.width, 200)
+    ys = cfg.y0 + rng.uniform(0, cfg.width, 200)
+    xs[:2] = [cfg.x0, cfg.x0 + cfg.width * (1 - 1e-12)]  # domain corners
+    ys[:2] = [cfg.y0, cfg.y0 + cfg.width * (1 - 1e-12)]
+    g = e.sample_gauges(xs, ys)
+    n = cfg.side
+    i = np.floor((xs - cfg.x0) / cfg.width * n).astype(int)
+    j = np.floor((ys - cfg.y0) / cfg.width * n).astype(int)
+    zz = np.asarray(z).reshape(n, n)
+    for k, f in enumerate((fh, fqx, fqy)):
+        np.testing.assert_array_equal(g[k], f[j, i])
+    assert not zz.any()  # flat bed: the leaf bed is 0 everywhere
+    np.testing.assert_array_equal(g[3], fh[j, i])
+    with pytest.raises(gpu.SwampError):
+        e.sample_gauges([cfg.x0 - 1.0], [0.0])  # outside the domain
+    assert e.sample_gauges([], []).shape == (4, 0)
+
+
+def test_quiescent_gauge_is_constant(tmp_path):
+    """a quiescent case gauge has a constant eta column."""
+    from paper_2206_05761_b200 import runner
+
+    cfg, h, qx, qy, z = cases.quiescent_humps(L=6, t_end=2.0)
+    cfg.output_times = (1.0, 2.0)
+    s = runner.run(cfg, h, qx, qy, z, str(tmp_path), gauges=[("lake", 10.0, 15.0), ("hump", 30.0, 6.0)])
+    rows = list(csv.DictReader(open(tmp_path / "gauges.csv")))
+    assert len(rows) == s["steps"] + 1 and float(rows[-1]["t"]) == 2.0
+    eta = np.array([float(r["lake_eta"]) for r in rows])
+    assert np.abs(eta - eta[0]).max() <= 1e-12, eta
+    steps = list(csv.DictReader(open(tmp_path / "steps.csv")))
+    assert len(steps) == s["steps"] and int(steps[-1]["step"]) == s["steps"]
+    assert (tmp_path / "snap_h_t0.asc").exists() and (tmp_path / "snap_h_t1.asc").exists()
+    assert (tmp_path / "snap_h_t2.asc").exists()
+
+
+def test_run_to_zero_gives_initial_snapshot_only(tmp_path):
+    from paper_2206_05761_b200 import runner
+
+    cfg, h, qx, qy, z = cases.circular_dambreak(L=6, t_end=0.0)
+    s = runner.run(cfg, h, qx, qy, z, str(tmp_path))  # SPEC.md:421 t_end = 0 -> initial snapshot only
+    assert s["steps"] == 0 and s["snapshots"] == [f"snap_{q}_t0.asc" for q in ("h", "qx", "qy", "eta")]
+    r = io.read_esri(tmp_path / "snap_h_t0.asc")
+    np.testing.assert_array_equal(r.values[::-1].reshape(-1).view(np.uint64), np.asarray(h).reshape(-1).view(np.uint64))
+
+
+def test_cli_run_and_compare(tmp_path, capsys):
+    from paper_2206_05761_b200 import cli
+
+    cfgf = tmp_path / "c.cfg"
+    cfgf.write_text("[case]\nname = hump_dambreak\n[grid]\nL = 7\nepsilon = 1e-3\n[time]\nt_end = 1.0\n"
+                    "output_times = 0.5, 1.0\n[output]\ngauges = g1 20 15\n")
+    assert cli.main(["run", "--config", str(cfgf), "--out", str(tmp_path / "a")]) == 0
+    assert cli.main(["run", "--config", str(cfgf), "--out", str(tmp_path / "b")]) == 0
+    assert cli.main(["run", "--config", str(cfgf), "--out", str(tmp_path / "u"), "--set", "solver.kind=uniform"]) == 0
+    summ = json.load(open(tmp_path / "a" / "summary.json"))
+    assert summ["t"] == 1.0 and summ["config"]["grid.L"] == 7  # overrides round-trip into the report header
+    capsys.readouterr()
+    assert cli.main(["compare", str(tmp_path / "a"), str(tmp_path / "b")]) == 0
+    rows = capsys.readouterr().out.strip().splitlines()
+    assert rows[0] == "time,L1,Linf" and len(rows) == 4  # t = 0, 0.5, 1
+    assert all(r.endswith(",0,0") for r in rows[1:])  # identical runs -> zeros
+    assert cli.main(["compare", str(tmp_path / "a"), str(tmp_path / "u")]) == 0
+    rows = capsys.readouterr().out.strip().splitlines()
+    assert float(rows[-1].split(",")[1]) > 0.0
+
+
+def test_cli_validate_subset():
+    from paper_2206_05761_b200 import cli
+
+    assert cli.main(["validate", "--only", "A4,A8", "--scale", "L=6"]) == 0
