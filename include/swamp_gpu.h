@@ -251,7 +251,8 @@ int swamp_gpu_work_counters(swamp_gpu* g, int64_t* out8);
 int swamp_gpu_near_threshold(swamp_gpu* g, int64_t* out4);
 
 /* Device timeline of the last step, microseconds from K1's first CTA: for
- * K1, K2, K3, K5 (k = 0..3): [3k] first CTA start, [3k+1] unused (-1),
+ * K1, K2, K3, K5 (k = 0..3): [3k] first CTA start, [3k+1] unused (-1; [1]: the
+ * previous step's end, <= 0, in a back-to-back run),
  * [3k+2] last CTA done. */
 int swamp_gpu_timeline(swamp_gpu* g, double* out12);
 

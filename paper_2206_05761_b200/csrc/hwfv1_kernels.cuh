@@ -2412,8 +2412,10 @@ __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ct
             ctl->near_step[slot] = 0ull;
         }
         ctl->tl[slot][3][2] = gtimer();
-        if (advance)  // next step's buffer
+        if (advance) {  // next step's buffer; its [0][1] = this step's end (the gap in front of the next K1)
             for (int k = 0; k < 4; ++k) ctl->tl[slot ^ 1][k][0] = ctl->tl[slot ^ 1][k][2] = 0ull;
+            ctl->tl[slot ^ 1][0][1] = ctl->tl[slot][3][2];
+        }
     }
     if (advance && P.ctl_mirror && threadIdx.x < 32) {
         // the step's report straight into the host's pinned mirror (saves the
@@ -2633,8 +2635,17 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
     const double4* cl = cur + cbase(L);
     const PhysParams& ph = P.phys;
     const double idx = inv_dx_of(P, L);
-    auto mc = [&](int x, int y) { return mb | zo::interleave(static_cast<uint32_t>(x), static_cast<uint32_t>(y)); };
+    // Morton code of (x, y) inside the subtree: 6-bit dilations (3 shift +
+    // lop3 steps instead of zorder's 4-step 14-bit spread), own column once
+    auto spread6 = [](uint32_t v) {
+        v = (v ^ (v << 4)) & 0x0F0Fu;
+        v = (v ^ (v << 2)) & 0x3333u;
+        return (v ^ (v << 1)) & 0x5555u;
+    };
+    auto mc = [&](int x, int y) { return mb | spread6(static_cast<uint32_t>(x)) | (spread6(static_cast<uint32_t>(y)) << 1); };
     const int x = xoff + lane;
+    const uint32_t mbx = mb | spread6(static_cast<uint32_t>(x));
+    auto mcol = [&](int y) { return mbx | (spread6(static_cast<uint32_t>(y)) << 1); };
     double4* my = rows + lane;  // row i at my[32 i]
     // ---- loads, all issued before any arithmetic: this column's rows inside
     //      the subtree by cp.async into the slab; at the subtree's edges the
@@ -2642,7 +2653,7 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
     for (int i = 0; i < 6; ++i) {
         const int y = r0 - 1 + i;
         if (y >= 0 && y < 64) {
-            const double4* g = cl + mc(x, y);
+            const double4* g = cl + mcol(y);
             cp_async16(my + 32 * i, g);
             cp_async16(reinterpret_cast<uint8_t*>(my + 32 * i) + 16, reinterpret_cast<const uint8_t*>(g) + 16);
         }
@@ -2670,7 +2681,7 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
     uint32_t onm = zo::kNone;  // the outside row's same-level cell (south / north)
     uint8_t of = 1;
     if (s_out || n_out) {
-        onm = zo::neighbour_dev(L, s_out ? mc(x, r0) : mc(x, r0 + 3), s_out ? zo::Direction::South : zo::Direction::North);
+        onm = zo::neighbour_dev(L, s_out ? mcol(r0) : mcol(r0 + 3), s_out ? zo::Direction::South : zo::Direction::North);
         if (onm != zo::kNone) of = sigc[slo(L - 1) + (onm >> 2)];
     }
     bool e_wall = false, o_wall = false;  // domain edge: boundary ghost
@@ -2700,7 +2711,7 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
         uint32_t pm0 = 0;
 #pragma unroll 1
         for (int k = 0; k < 4; ++k) {
-            const uint32_t m = mc(x, r0 + k);
+            const uint32_t m = mcol(r0 + k);
             const double4 o4 = my[32 * (k + 1)];
             const double hn = (o4.x < 0.0) ? 0.0 : o4.x;
             st4(nxt + cbase(L) + m, make_double4(hn, 0.0, 0.0, o4.w));
@@ -2746,7 +2757,7 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
     bool wet = false;
 #pragma unroll 1
     for (int k = 0; k < 4; ++k) {
-        const uint32_t m = mc(x, r0 + k);
+        const uint32_t m = mcol(r0 + k);
         const CellV N = (k == 3 && n_out && o_wall) ? boundary_cell(C, P.bc[2], 2, inflow, P.inflow_mode, ph)
                                                     : make_cell(my[32 * (k + 2)], ph);
         const FaceR fN = face_r(C, N, false, ph);
@@ -2803,46 +2814,27 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
     return out;
 }
 
-// FV1 tile path kernel: the strips of the active fully refined subtrees K3's
-// top listed (P.stile, ctl->n_stile), before the per-leaf k_fv1 (which
-// waits for it and finalizes the step: the CFL rates of both go into the
-// same slot). Each CTA takes a contiguous range of the jobs (neighbouring
-// strips share rows through L2) and hands them to its warps by a shared-
-// memory counter (a grid-wide counter measured slower: thousands of
-// same-address atomics queue at one L2 slice).
-constexpr size_t kTileSlab = sizeof(double4) * 6 * 32 * (kThreads / 32);  // k_fv1_tiles dynamic shared memory
-__global__ void __launch_bounds__(kThreads, 2) k_fv1_tiles(Params P, Ctl* ctl) {
-    pdl_wait();
-    pdl_trigger();
-    __shared__ double s_td[2];
-    __shared__ uint32_t s_u[3];
+// FV1 tile phase: the strips of the active fully refined subtrees K3's top
+// listed (P.stile, ctl->n_stile), run by every k_fv1 CTA before its share of
+// the leaf list (the per-leaf windows' tail balancing absorbs the tile
+// phase's imbalance; a separate tile kernel ran its own tail and a launch
+// gap before the per-leaf kernel). Each CTA takes a contiguous range of the
+// jobs (neighbouring strips share rows through L2) and hands them to its
+// warps by a shared-memory counter (a grid-wide counter measured slower:
+// thousands of same-address atomics queue at one L2 slice). Not inlined: the
+// strip code stays out of the per-leaf loop's instruction footprint.
+constexpr size_t kTileSlab = sizeof(double4) * 6 * 32 * (kThreads / 32);  // k_fv1 dynamic shared memory with tiles
+__device__ __forceinline__ TileOut fv1_tile_phase(const Params& P, Ctl* ctl, const double4* __restrict__ cur,
+                                               double4* __restrict__ nxt, const uint8_t* __restrict__ sigc,
+                                               uint32_t ntile, double dt, double inflow, int tbuf) {
     __shared__ unsigned s_tj;
-    if (threadIdx.x == 0) {
-        const volatile Ctl* vc = ctl;
-        s_td[0] = vc->t;
-        s_td[1] = vc->dt;
-        s_u[0] = static_cast<uint32_t>(vc->parity);
-        s_u[1] = static_cast<uint32_t>(vc->step & 1);
-        s_u[2] = vc->n_stile;
-    }
-    __syncthreads();
-    const double t = s_td[0], dt = s_td[1];
-    const uint32_t njobs = 32u * s_u[2];
-    if (!(t < P.t_end) || njobs == 0u) return;
-    const int tbuf = static_cast<int>(s_u[1]);
-    tl_start(ctl, tbuf, 3);
-    const int p = static_cast<int>(s_u[0]);
-    const double4* __restrict__ cur = P.cells[p];
-    double4* __restrict__ nxt = P.cells[p ^ 1];
-    const uint8_t* __restrict__ sigc = P.sig[p ^ 1];
-    const double inflow = series_value(P, t);
-    const int lane = threadIdx.x & 31;
+    TileOut acc = {0.0, 0u, 0u};
+    const uint32_t njobs = 32u * ntile;
     const uint32_t j1 = static_cast<uint32_t>((static_cast<unsigned long long>(njobs) * (blockIdx.x + 1)) / gridDim.x);
     if (threadIdx.x == 0)
         s_tj = static_cast<uint32_t>((static_cast<unsigned long long>(njobs) * blockIdx.x) / gridDim.x);
     __syncthreads();
-    double mx = 0.0;
-    unsigned tree = 0, nnear = 0;
+    const int lane = threadIdx.x & 31;
     extern __shared__ __align__(16) double4 s_rows[];  // kTileSlab bytes: one 6 x 32-cell slab per warp
     for (;;) {
         uint32_t jb = 0;
@@ -2851,39 +2843,37 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1_tiles(Params P, Ctl* ctl) {
         if (jb >= j1) break;
         const TileOut to = fv1_tile_strip(P, ctl, cur, nxt, sigc, P.stile[jb >> 5], jb & 31u, dt, inflow, tbuf,
                                           s_rows + (threadIdx.x >> 5) * (6 * 32));
-        mx = to.mx > mx ? to.mx : mx;
-        tree += to.tree;
-        nnear += to.nnear;
+        acc.mx = to.mx > acc.mx ? to.mx : acc.mx;
+        acc.tree += to.tree;
+        acc.nnear += to.nnear;
     }
-    // the CFL rates (exact u64 max into this step's slot; k_fv1 finalizes),
-    // the fused re-encode and near-threshold counts
-    __shared__ unsigned long long s_m[kThreads / 32];
-    __shared__ unsigned s_c[2][kThreads / 32];
-    unsigned long long b = warp_max_u64(static_cast<unsigned long long>(__double_as_longlong(mx)));
-    unsigned c0 = tree, c1 = nnear;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        c0 += __shfl_xor_sync(kFull, c0, o);
-        c1 += __shfl_xor_sync(kFull, c1, o);
+    return acc;
+}
+
+// the tile phase after the per-leaf windows (SWAMP_TILE_LAST): strip jobs
+// from a per-step grid-wide counter, one per warp grab, the next job id
+// fetched while the current strip computes; the level-(L-1) parents the
+// strips write are then the freshest lines in L2 when K1 reads them
+__device__ __forceinline__ TileOut fv1_tile_phase_dyn(const Params& P, Ctl* ctl, const double4* __restrict__ cur,
+                                                      double4* __restrict__ nxt, const uint8_t* __restrict__ sigc,
+                                                      uint32_t ntile, double dt, double inflow, int tbuf) {
+    TileOut acc = {0.0, 0u, 0u};
+    const uint32_t njobs = 32u * ntile;
+    const int lane = threadIdx.x & 31;
+    extern __shared__ __align__(16) double4 s_rows[];
+    uint32_t nxtj = 0;
+    if (lane == 0) nxtj = atomicAdd(&ctl->fv1_tjob, 1u);
+    for (;;) {
+        const uint32_t jb = __shfl_sync(kFull, nxtj, 0);
+        if (jb >= njobs) break;
+        if (lane == 0) nxtj = atomicAdd(&ctl->fv1_tjob, 1u);
+        const TileOut to = fv1_tile_strip(P, ctl, cur, nxt, sigc, P.stile[jb >> 5], jb & 31u, dt, inflow, tbuf,
+                                          s_rows + (threadIdx.x >> 5) * (6 * 32));
+        acc.mx = to.mx > acc.mx ? to.mx : acc.mx;
+        acc.tree += to.tree;
+        acc.nnear += to.nnear;
     }
-    if (lane == 0) {
-        s_m[threadIdx.x >> 5] = b;
-        s_c[0][threadIdx.x >> 5] = c0;
-        s_c[1][threadIdx.x >> 5] = c1;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long m = 0;
-        unsigned long long n0 = 0, n1 = 0;
-        for (int w = 0; w < kThreads / 32; ++w) {
-            m = s_m[w] > m ? s_m[w] : m;
-            n0 += s_c[0][w];
-            n1 += s_c[1][w];
-        }
-        if (m) atomicMax(&ctl->rate_bits[tbuf], m);
-        if (n0) atomicAdd(&ctl->cnt_fused, n0);
-        if (n1) atomicAdd(&ctl->near_step[tbuf ^ 1], n1);
-    }
+    return acc;
 }
 
 // FV1 over the leaf list: persistent grid-stride, one thread per
@@ -2894,7 +2884,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1_tiles(Params P, Ctl* ctl) {
 template <bool UNIFORM, bool PART = false, bool INA = false, int STAGE = 0>
 __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     pdl_wait();
-    pdl_trigger();
     // control words, read once per CTA (line 0 of Ctl)
     __shared__ double s_td[2];
     __shared__ uint32_t s_u[7];
@@ -2927,6 +2916,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     double mx = 0.0;
     unsigned tree = 0, nnear = 0, ndem = 0, nquiet = 0;
     (void)ndem;
+#ifndef SWAMP_TILE_LAST
+    if constexpr (!UNIFORM && !PART && !INA) {
+        if (P.tiles && s_u[6]) {  // the tile path first (its leaves are off list A)
+            const TileOut to = fv1_tile_phase(P, ctl, cur, nxt, sigc, s_u[6], dt, inflow, tbuf);
+            mx = to.mx;
+            tree = to.tree;
+            nnear = to.nnear;
+        }
+    }
+#endif
     const uint32_t stride = gridDim.x * kThreads;
     // warp-uniform trip count: every lane runs every iteration (shuffles below)
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
@@ -3186,6 +3185,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
             }
         }
     }
+#ifdef SWAMP_TILE_LAST
+    if constexpr (!UNIFORM && !PART && !INA) {
+        if (P.tiles && s_u[6]) {
+            const TileOut to = fv1_tile_phase_dyn(P, ctl, cur, nxt, sigc, s_u[6], dt, inflow, tbuf);
+            mx = to.mx > mx ? to.mx : mx;
+            tree += to.tree;
+            nnear += to.nnear;
+        }
+    }
+#endif
     if (!UNIFORM) {
         // work counters (bench.py's per-class byte accounting) and the
         // near-threshold level-(L-1) cells, which belong to the NEXT step's count
@@ -3207,6 +3216,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
             if (s) atomicAdd(dst, s);
         }
     }
+    // the next step's K1 may launch once every CTA is here: K1 CTAs made
+    // resident early (trigger at entry) land on the SMs the FV1 tail frees
+    // first and ran K1 5-7 us slower
+    pdl_trigger();
     cfl_reduce_and_finalize(P, ctl, mx, true, tbuf);
 }
 

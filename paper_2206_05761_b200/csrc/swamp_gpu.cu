@@ -267,17 +267,17 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
         launch_pdl(g->k3, P.n_tiles + 1, g->smem_k3, s, P, g->ctl, 0, 0ull);
     }
     mark(3);
-    if (P.tiles) launch_pdl(hwfv1::k_fv1_tiles, g->fv1_grid, hwfv1::kTileSlab, s, P, g->ctl);
+    const size_t fsm = P.tiles ? hwfv1::kTileSlab : 0;  // the tile phase's row slabs
     if (P.has_ina)  // D16 variant
         launch_pdl(hwfv1::k_fv1<false, false, true>, g->fv1_grid, 0, s, P, g->ctl);
     else if (g->fv1_stage == 2)
-        launch_pdl(hwfv1::k_fv1<false, false, false, 2>, g->fv1_grid, 0, s, P, g->ctl);
+        launch_pdl(hwfv1::k_fv1<false, false, false, 2>, g->fv1_grid, fsm, s, P, g->ctl);
     else if (g->fv1_stage == 3)
-        launch_pdl(hwfv1::k_fv1<false, false, false, 3>, g->fv1_grid, 0, s, P, g->ctl);
+        launch_pdl(hwfv1::k_fv1<false, false, false, 3>, g->fv1_grid, fsm, s, P, g->ctl);
     else if (g->fv1_stage == 5)
-        launch_pdl(hwfv1::k_fv1<false, false, false, 5>, g->fv1_grid, 0, s, P, g->ctl);
+        launch_pdl(hwfv1::k_fv1<false, false, false, 5>, g->fv1_grid, fsm, s, P, g->ctl);
     else
-        launch_pdl(hwfv1::k_fv1<false>, g->fv1_grid, 0, s, P, g->ctl);
+        launch_pdl(hwfv1::k_fv1<false>, g->fv1_grid, fsm, s, P, g->ctl);
     mark(4);
 }
 
@@ -667,7 +667,10 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
                      {reinterpret_cast<const void*>(g->k3x), g->smem_k3},
                      {reinterpret_cast<const void*>(g->k3top), g->smem_k3top},
                      {reinterpret_cast<const void*>(g->k3tiles), g->smem_k3tiles},
-                     {reinterpret_cast<const void*>(hwfv1::k_fv1_tiles), hwfv1::kTileSlab}};
+                     {reinterpret_cast<const void*>(hwfv1::k_fv1<false>), hwfv1::kTileSlab},
+                     {reinterpret_cast<const void*>(hwfv1::k_fv1<false, false, false, 2>), hwfv1::kTileSlab},
+                     {reinterpret_cast<const void*>(hwfv1::k_fv1<false, false, false, 3>), hwfv1::kTileSlab},
+                     {reinterpret_cast<const void*>(hwfv1::k_fv1<false, false, false, 5>), hwfv1::kTileSlab}};
         for (auto& a : attrs)
             if (a.f && a.bytes >= 32 * 1024 &&
                 cudaFuncSetAttribute(a.f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(a.bytes)) !=
@@ -1449,11 +1452,11 @@ int swamp_gpu_sample_gauges(swamp_gpu* g, int32_t n, const double* x, const doub
     }
     cudaSetDevice(g->device);
     void* d = nullptr;
-    const size_t cb = cells.size() * sizeof(uint32_t), ob = 4 * static_cast<size_t>(n) * sizeof(double);
+    const size_t cb = (cells.size() * sizeof(uint32_t) + 15) & ~size_t(15), ob = 4 * static_cast<size_t>(n) * sizeof(double);
     CK(cudaMallocAsync(&d, cb + ob, g->stream));
     uint32_t* dc = static_cast<uint32_t*>(d);
-    double* dout = reinterpret_cast<double*>(static_cast<char*>(d) + ((cb + 15) & ~size_t(15)) - 0);
-    cudaError_t e = cudaMemcpyAsync(dc, cells.data(), cb, cudaMemcpyHostToDevice, g->stream);
+    double* dout = reinterpret_cast<double*>(static_cast<char*>(d) + cb);
+    cudaError_t e = cudaMemcpyAsync(dc, cells.data(), cells.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, g->stream);
     if (e == cudaSuccess) {
         hwfv1::k_gauges<<<std::max(1, std::min(g->num_sms, (n + kThreads - 1) / kThreads)), kThreads, 0, g->stream>>>(
             g->P, g->ctl, dc, n, dout);
@@ -1502,6 +1505,8 @@ int swamp_gpu_timeline(swamp_gpu* g, double* out12) {
         const unsigned long long v = (k % 3 == 0) ? ~raw : raw;
         out12[k] = (raw == 0 || v < t0) ? -1.0 : 1e-3 * static_cast<double>(v - t0);
     }
+    // [1]: the previous step's end relative to this step's K1 start (<= 0)
+    out12[1] = (tl[0][1] == 0 || t0 == ~0ull) ? 0.0 : -1e-3 * static_cast<double>(static_cast<long long>(t0 - tl[0][1]));
     return st;
 }
 
