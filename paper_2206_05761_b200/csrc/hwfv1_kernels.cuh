@@ -1064,7 +1064,6 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
     stage_thresholds(P, s_thr);
 
     pdl_wait();
-    pdl_trigger();
     const unsigned long long t_entry = gtimer();
     const Head hd = cta_head(ctl, P, false);
     if (!hd.active) {
@@ -1261,6 +1260,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
         }
 
     }
+    pdl_trigger();  // K2 may launch (late: measured ~0.5 us better than at entry)
     const unsigned tsum = block_sum(tree | (nnear << 16), s_red);  // (both < 2^16 per subtree)
     if (threadIdx.x == 0 && (tsum & 0xFFFFu)) atomicAdd(&ctl->cnt_tree, (unsigned long long)(tsum & 0xFFFFu));
     add_near(ctl, false, hd.buf, tsum >> 16);
@@ -2850,32 +2850,6 @@ __device__ __forceinline__ TileOut fv1_tile_phase(const Params& P, Ctl* ctl, con
     return acc;
 }
 
-// the tile phase after the per-leaf windows (SWAMP_TILE_LAST): strip jobs
-// from a per-step grid-wide counter, one per warp grab, the next job id
-// fetched while the current strip computes; the level-(L-1) parents the
-// strips write are then the freshest lines in L2 when K1 reads them
-__device__ __forceinline__ TileOut fv1_tile_phase_dyn(const Params& P, Ctl* ctl, const double4* __restrict__ cur,
-                                                      double4* __restrict__ nxt, const uint8_t* __restrict__ sigc,
-                                                      uint32_t ntile, double dt, double inflow, int tbuf) {
-    TileOut acc = {0.0, 0u, 0u};
-    const uint32_t njobs = 32u * ntile;
-    const int lane = threadIdx.x & 31;
-    extern __shared__ __align__(16) double4 s_rows[];
-    uint32_t nxtj = 0;
-    if (lane == 0) nxtj = atomicAdd(&ctl->fv1_tjob, 1u);
-    for (;;) {
-        const uint32_t jb = __shfl_sync(kFull, nxtj, 0);
-        if (jb >= njobs) break;
-        if (lane == 0) nxtj = atomicAdd(&ctl->fv1_tjob, 1u);
-        const TileOut to = fv1_tile_strip(P, ctl, cur, nxt, sigc, P.stile[jb >> 5], jb & 31u, dt, inflow, tbuf,
-                                          s_rows + (threadIdx.x >> 5) * (6 * 32));
-        acc.mx = to.mx > acc.mx ? to.mx : acc.mx;
-        acc.tree += to.tree;
-        acc.nnear += to.nnear;
-    }
-    return acc;
-}
-
 // FV1 over the leaf list: persistent grid-stride, one thread per
 // leaf; reads the current buffer, writes leaf slots of the other (D15).
 // STAGE 0: next iteration's own cell prefetched into L2; 2: loaded into
@@ -3185,16 +3159,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
             }
         }
     }
-#ifdef SWAMP_TILE_LAST
-    if constexpr (!UNIFORM && !PART && !INA) {
-        if (P.tiles && s_u[6]) {
-            const TileOut to = fv1_tile_phase_dyn(P, ctl, cur, nxt, sigc, s_u[6], dt, inflow, tbuf);
-            mx = to.mx > mx ? to.mx : mx;
-            tree += to.tree;
-            nnear += to.nnear;
-        }
-    }
-#endif
     if (!UNIFORM) {
         // work counters (bench.py's per-class byte accounting) and the
         // near-threshold level-(L-1) cells, which belong to the NEXT step's count

@@ -15,6 +15,7 @@ if [ "${2:-}" != "skip-slow" ]; then
 fi
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 tail -2 gpurun_out/${TAG}_bench.err
+timeout 900 python scripts/cpu_baselines.py > gpurun_out/${TAG}_cpu_baselines.json 2> gpurun_out/${TAG}_cpu_baselines.err
 timeout 600 python bench.py --impl reference --steps 10 --warmup 5 > gpurun_out/${TAG}_bench_ref.json 2> gpurun_out/${TAG}_bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/${TAG}_launches.csv \
     python bench.py --steps 4 --warmup 3 --no-cpu --no-sims --no-wet > gpurun_out/${TAG}_ncu_bench.log 2>&1
