@@ -65,6 +65,7 @@ struct Ctl {
     alignas(128) unsigned long long cnt_new;     // newly significant cells decoded by the last K3
     unsigned long long cnt_updates;              // leaf updates of all steps so far (sum of N)
     alignas(128) unsigned long long k3_ready;    // K3's top CTA published its results (epoch)
+    alignas(128) unsigned int k2_done;           // fused K2+K3: subtree CTAs whose band / closure / counts are out
     alignas(128) unsigned int fv1_tail;          // FV1 (STAGE 5): dynamic tail chunks taken this step
     unsigned int fv1_tjob;                       // FV1 tile path: strip jobs taken this step
     uint32_t n_stile;                            // subtrees on FV1's tile path this step (K3's top)
@@ -250,6 +251,11 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
@@ -2064,7 +2070,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
 // top), wait for the top's offsets, then decode and emit
 template <bool EXPORT, int KT>
 __device__ void k3_tile(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long long epoch, uint32_t j, uint8_t* sm,
-                        const Probe& stamp) {
+                        const Probe& stamp, bool sc_ready = false) {
     __shared__ unsigned s_red[32];
     __shared__ uint32_t s_top[4];
     double4* buf = P.cells[p];
@@ -2079,12 +2085,12 @@ __device__ void k3_tile(const Params& P, Ctl* ctl, int p, int tbuf, unsigned lon
     uint32_t* src = reinterpret_cast<uint32_t*>(sp + slo(K));  // [ncell] projection sources
     (void)ncell;
 
-    {
-        const uint8_t c0 = stage_tile_flags(sc, sigc, P, j);
+    {   // (sc_ready: the fused K2 left this subtree's final flags in sc)
+        const uint8_t c0 = sc_ready ? 0 : stage_tile_flags(sc, sigc, P, j);
         const uint8_t q0 = EXPORT ? 0 : stage_tile_flags(sp, sigp, P, j);
         cp_async_wait_all();
         if (threadIdx.x == 0) {
-            sc[0] = c0;
+            if (!sc_ready) sc[0] = c0;
             if (!EXPORT) sp[0] = q0;
         }
     }
@@ -2325,6 +2331,62 @@ __global__ void __launch_bounds__(kThreads, 8) k_traverse_tiles(Params P, Ctl* c
         k3_tile<false, KT>(P, ctl, hd.parity, hd.buf, 2ull * static_cast<unsigned long long>(hd.step) + 2ull,
                            P.tile_lo + blockIdx.x, smem3s, stamp);
     }
+    pdl_wait();  // the top grid has completed before this grid does
+}
+
+// Fused K2 + K3 (one partition, every subtree CTA resident at once: the
+// host enables it only when the subtree grid fits beside the top CTA's SM).
+// The top CTA passes its wait for K1, lets the subtree grid launch, re-encodes
+// levels R-1..0 and bands the top cells (K2's extra CTA), then waits until
+// every subtree CTA has published its band / closure / counts (k2_done) and
+// runs K3's top. A subtree CTA runs K2's subtree work on K1's pre flags
+// (visible: the top triggered this grid after its wait for K1), publishes it,
+// and goes on with K3's subtree work on the final flags it still holds in
+// shared memory. One launch and one kernel boundary less than K2 -> K3.
+template <int KT>
+__global__ void __launch_bounds__(kThreads, 1) k_top23(Params P, Ctl* ctl) {
+    pdl_wait();
+    pdl_trigger();
+    const unsigned long long t_entry = gtimer();
+    const Head hd = cta_head(ctl, P, false);
+    if (!hd.active) return;
+    extern __shared__ __align__(16) uint8_t smem23t[];
+    tl_start(ctl, hd.buf, 1);
+    tl_start(ctl, hd.buf, 2);
+    const Probe stamp(ctl, 16);
+    stamp(7, t_entry);
+    encode_top_staged(P, ctl, hd.parity, hd.buf, smem23t);
+    if (threadIdx.x == 0) {
+        const unsigned nt = static_cast<unsigned>(P.n_tiles);
+        while (ld_acquire_u32(&ctl->k2_done) < nt) __nanosleep(32);
+        ctl->k2_done = 0u;  // (every subtree CTA of this step has counted)
+    }
+    __syncthreads();
+    k3_top<false>(P, ctl, hd.parity, hd.buf, 2ull * static_cast<unsigned long long>(hd.step) + 2ull, smem23t, stamp,
+                  true, P.n_tiles <= 1024);
+}
+template <int KT>
+__global__ void __launch_bounds__(kThreads, 8) k_tiles23(Params P, Ctl* ctl) {
+    const unsigned long long t_entry = gtimer();
+    const Head hd = cta_head(ctl, P, false);
+    if (hd.active) {
+        extern __shared__ __align__(16) uint8_t smem23s[];
+        const uint32_t j = P.tile_lo + blockIdx.x;
+        // K2's subtree work: pre flags at smem23s, final flags left at
+        // smem23s + slo(K) = K3's current-flag slot
+        k2_tile<KT>(P, ctl, hd, j, smem23s);
+        __threadfence();  // every thread's final-flag stores, then the count
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd(&ctl->k2_done, 1u);
+        Probe stamp(ctl, 16);
+        if (blockIdx.x == 0) stamp.slot = -1;  // (slots 16.. belong to the top CTA)
+        stamp(7, t_entry);
+        k3_tile<false, KT>(P, ctl, hd.parity, hd.buf, 2ull * static_cast<unsigned long long>(hd.step) + 2ull, j,
+                           smem23s + slo(KT ? KT : P.K), stamp, true);
+    }
+    // FV1 may launch once every subtree CTA is past its K2 publish (a pending
+    // subtree CTA behind resident FV1 CTAs would stall the top's wait)
+    pdl_trigger();
     pdl_wait();  // the top grid has completed before this grid does
 }
 

@@ -129,6 +129,10 @@ struct swamp_gpu {
     void (*k3top)(Params, Ctl*) = nullptr;
     void (*k3tiles)(Params, Ctl*) = nullptr;
     size_t smem_k3top = 0, smem_k3tiles = 0;
+    // fused K2 + K3 (k_top23 + k_tiles23): K2 not launched
+    void (*k23top)(Params, Ctl*) = nullptr;
+    void (*k23tiles)(Params, Ctl*) = nullptr;
+    size_t smem_k23tiles = 0;
     // tile kernels, specialised for K = 6 (every L >= 6) or generic
     void (*k1)(Params, Ctl*) = nullptr;
     void (*k2)(Params, Ctl*, int, int) = nullptr;
@@ -257,6 +261,12 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     launch_pdl(g->k1, P.n_tiles, g->smem_k1s, s, P, g->ctl);
     if (P.top_mode == 2) launch_pdl(hwfv1::k_encode_top<false>, 1, g->smem_k1, s, P, g->ctl);
     mark(1);
+    if (g->k23top) {  // fused K2 + K3
+        mark(2);
+        launch_pdl(g->k23top, 1, g->smem_k3top, s, P, g->ctl);
+        launch_pdl(g->k23tiles, P.n_tiles, g->smem_k23tiles, s, P, g->ctl);
+        mark(3);
+    } else {
     const int do_top = P.top_mode == 1 ? 1 : 0;
     launch_pdl(g->k2, P.n_tiles + do_top, g->smem_k2, s, P, g->ctl, 0, do_top);
     mark(2);
@@ -267,6 +277,7 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
         launch_pdl(g->k3, P.n_tiles + 1, g->smem_k3, s, P, g->ctl, 0, 0ull);
     }
     mark(3);
+    }
     const size_t fsm = P.tiles ? hwfv1::kTileSlab : 0;  // the tile phase's row slabs
     if (P.has_ina)  // D16 variant
         launch_pdl(hwfv1::k_fv1<false, false, true>, g->fv1_grid, 0, s, P, g->ctl);
@@ -654,6 +665,24 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             // split K3 (its top lists the tiles); SWAMP_FV1_TILES=0 disables
             const char* et = std::getenv("SWAMP_FV1_TILES");
             P.tiles = (Ki == 6 && !P.has_ina && !(et && et[0] == '0')) ? 1 : 0;
+            // fused K2 + K3: needs top_band (K2's extra-CTA work moves into the
+            // top CTA) and every subtree CTA resident beside the top's SM
+            // (the top waits for all of them); SWAMP_K23=0 disables
+            const char* e23 = std::getenv("SWAMP_K23");
+            if (P.top_band && !(e23 && e23[0] == '0')) {
+                void (*t23)(Params, Ctl*) = (Ki == 6) ? hwfv1::k_tiles23<6> : hwfv1::k_tiles23<0>;
+                const size_t sm23 = sl + g->smem_k3tiles;
+                int occ = 0;
+                if (sm23 >= 32 * 1024)
+                    cudaFuncSetAttribute(reinterpret_cast<const void*>(t23),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm23));
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, t23, kThreads, sm23);
+                if (static_cast<long long>(occ) * (g->num_sms - 1) >= P.n_tiles) {
+                    g->k23top = (Ki == 6) ? hwfv1::k_top23<6> : hwfv1::k_top23<0>;
+                    g->k23tiles = t23;
+                    g->smem_k23tiles = sm23;
+                }
+            }
         }
         struct {
             const void* f;
@@ -667,6 +696,8 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
                      {reinterpret_cast<const void*>(g->k3x), g->smem_k3},
                      {reinterpret_cast<const void*>(g->k3top), g->smem_k3top},
                      {reinterpret_cast<const void*>(g->k3tiles), g->smem_k3tiles},
+                     {reinterpret_cast<const void*>(g->k23top), g->smem_k3top},
+                     {reinterpret_cast<const void*>(g->k23tiles), g->smem_k23tiles},
                      {reinterpret_cast<const void*>(hwfv1::k_fv1<false>), hwfv1::kTileSlab},
                      {reinterpret_cast<const void*>(hwfv1::k_fv1<false, false, false, 2>), hwfv1::kTileSlab},
                      {reinterpret_cast<const void*>(hwfv1::k_fv1<false, false, false, 3>), hwfv1::kTileSlab},
