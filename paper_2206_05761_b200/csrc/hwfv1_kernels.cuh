@@ -1686,8 +1686,17 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     if (!EXPORT) {
         if (!band_done) stage16(tp, P.pre, fb);
         stage16(tv, sigp, fb);
-        if (nt >= 16u) stage16(swet, P.wet[tbuf], nt);
-        else if (threadIdx.x < nt) swet[threadIdx.x] = P.wet[tbuf][threadIdx.x];
+        if (P.G > 1) {  // a partition marks every subtree under its wet leaves: OR over the partitions
+            for (uint32_t t = threadIdx.x; t < nt; t += kThreads) {
+                uint8_t v = 0;
+                for (int g = 0; g < P.G; ++g) v |= P.pwet[g][tbuf][t];
+                swet[t] = v;
+            }
+        } else if (nt >= 16u) {
+            stage16(swet, P.wet[tbuf], nt);
+        } else if (threadIdx.x < nt) {
+            swet[threadIdx.x] = P.wet[tbuf][threadIdx.x];
+        }
     }
     uint8_t r0 = 0;
     if (nt == 1u) {
@@ -2563,6 +2572,7 @@ __global__ void k_finalize(Params P, Ctl* ctl, int advance) {
         ctl->near_step[slot] = 0ull;
     }
     ctl->rate_bits[slot ^ 1] = 0ull;
+    ctl->fv1_tail = 0u;  // (FV1's tail counter: partitioned FV1 has no finalizing CTA)
     ctl->tl[slot][3][2] = gtimer();
     for (int k = 0; k < 4; ++k) ctl->tl[slot ^ 1][k][0] = ctl->tl[slot ^ 1][k][2] = 0ull;
 }
@@ -3012,8 +3022,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
         const int n1 = zo::level_of(zz);
         const uint32_t m1 = zz - zo::level_offset(n1);
         o4_pre = ld4_nc(cur + cbase(n1) + m1);
-        ta_pre = (!PART && n1 >= P.R) ? P.tact[m1 >> (2 * (n1 - P.R))] : 1;
-        if ((STAGE == 3 || STAGE == 5) && n1 > 0) {
+        ta_pre = (n1 >= P.R) ? P.tact[m1 >> (2 * (n1 - P.R))] : 1;
+        if ((STAGE == 3 || STAGE == 5) && !PART && n1 > 0) {  // (PART: flags through the peer tables below)
 #pragma unroll
             for (int d = 0; d < 4; ++d) {
                 const uint32_t q = zo::neighbour_dev(n1, m1, static_cast<zo::Direction>(d));
@@ -3069,7 +3079,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
         }
         // subtree activity (bit 0: wet neighbourhood)
         const uint8_t ta = (STAGE >= 2 && !UNIFORM) ? (valid ? ta_k : 1)
-                           : ((!UNIFORM && !PART && valid && n >= P.R) ? P.tact[m >> (2 * (n - P.R))] : 1);
+                           : ((!UNIFORM && valid && n >= P.R) ? P.tact[m >> (2 * (n - P.R))] : 1);
         double hn = 0.0, qxn = 0.0, qyn = 0.0, zown = 0.0;
         if (valid) {
             // every global read of this leaf is issued before any arithmetic:
@@ -3189,7 +3199,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
         if (valid) {
             // mark the subtree(s) of a leaf that ends wet (a leaf above level R
             // marks every subtree under it)
-            if (!UNIFORM && !PART && !(hn < P.phys.hdry)) {
+            if (!UNIFORM && !(hn < P.phys.hdry)) {
                 uint8_t* wn = P.wet[tbuf ^ 1];
                 if (n >= P.R) {
                     wn[m >> (2 * (n - P.R))] = 1;

@@ -663,13 +663,21 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             // FV1 tile path (active fully refined subtrees as 64 x 64 blocks,
             // every face once): one partition, K = 6, no inactive cells, the
             // split K3 (its top lists the tiles); SWAMP_FV1_TILES=0 disables
+            // Below L = 11 a strip's serial rows are the step's critical path
+            // (few jobs per CTA): humps L9 39 -> 31 us/step without the tile
+            // phase, Monai L10 74 -> 71; SWAMP_FV1_TILES=0 / 1 forces it
             const char* et = std::getenv("SWAMP_FV1_TILES");
-            P.tiles = (Ki == 6 && !P.has_ina && !(et && et[0] == '0')) ? 1 : 0;
+            const bool tl = et ? et[0] != '0' : P.n_tiles >= 1024;
+            P.tiles = (Ki == 6 && !P.has_ina && tl) ? 1 : 0;
             // fused K2 + K3: needs top_band (K2's extra-CTA work moves into the
             // top CTA) and every subtree CTA resident beside the top's SM
-            // (the top waits for all of them); SWAMP_K23=0 disables
+            // (the top waits for all of them). Measured: -1.5 to -2 us per step
+            // at L = 8..10 (<= 256 subtrees), +2 to +3 us at L = 11 (1024: the
+            // top's closure waits for the slowest subtree's band); SWAMP_K23=0 /
+            // 1 forces it off / on
             const char* e23 = std::getenv("SWAMP_K23");
-            if (P.top_band && !(e23 && e23[0] == '0')) {
+            const bool k23 = e23 ? e23[0] != '0' : P.n_tiles <= 256;
+            if (P.top_band && k23) {
                 void (*t23)(Params, Ctl*) = (Ki == 6) ? hwfv1::k_tiles23<6> : hwfv1::k_tiles23<0>;
                 const size_t sm23 = sl + g->smem_k3tiles;
                 int occ = 0;
@@ -834,7 +842,9 @@ bool part_step_phase(swamp_gpu* q, int k, cudaStream_t s) {
         case 3: q->k3<<<P.tiles_per_part + 1, kThreads, q->smem_k3, s>>>(P, q->ctl, 0, 0ull); return true;
         case 4:
             if (P.has_ina) hwfv1::k_fv1<false, true, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
-            else if (q->fv1_stage >= 2)  // own cells loaded an iteration ahead (flags come from peer tables: no STAGE 3)
+            else if (q->fv1_stage == 5)  // tail balancing (flags come from the peer tables: no STAGE 3 preloads)
+                hwfv1::k_fv1<false, true, false, 5><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
+            else if (q->fv1_stage >= 2)  // own cells loaded an iteration ahead
                 hwfv1::k_fv1<false, true, false, 2><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
             else
                 hwfv1::k_fv1<false, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
@@ -874,9 +884,12 @@ constexpr int kInitPhases = 6;
 
 // one partition on its own stream, device barriers between the phases
 // (distinct devices / processes)
+// (no barrier after the finalize: it reads the peers' CFL slots of this step,
+// which they do not touch again before the next step's FV1 barrier, and the
+// next K1 reads only this partition's cells)
 void part_enqueue_step(swamp_gpu* q) {
     for (int k = 0; k < kStepPhases; ++k)
-        if (part_step_phase(q, k, q->stream)) part_barrier(q, q->stream);
+        if (part_step_phase(q, k, q->stream) && k + 1 < kStepPhases) part_barrier(q, q->stream);
 }
 void part_enqueue_init(swamp_gpu* q) {
     for (int k = 0; k < kInitPhases; ++k)

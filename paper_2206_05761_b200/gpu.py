@@ -67,7 +67,8 @@ def lib():
         L.swamp_gpu_timeline.argtypes = [P, dp]
         L.swamp_gpu_debug.argtypes = [P, C.POINTER(C.c_uint64)]
         L.swamp_gpu_stream.argtypes = [P, C.POINTER(C.c_void_p)]
-        L.swamp_gpu_sample_gauges.argtypes = [P, C.c_int32, dp, dp, dp]
+        if hasattr(L, "swamp_gpu_sample_gauges"):  # (older builds, A/B timing only)
+            L.swamp_gpu_sample_gauges.argtypes = [P, C.c_int32, dp, dp, dp]
         L.swamp_gpu_build_info.restype = C.c_char_p
         _LIB = L
     return _LIB

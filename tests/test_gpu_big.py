@@ -40,8 +40,8 @@ def test_level13_steps_stay_finite():
 
 
 @pytest.mark.parametrize("env", [("SWAMP_FV1_STAGE", "3"), ("SWAMP_K3_SPLIT", "0"), ("SWAMP_FV1_TAIL16", "15"),
-                                 ("SWAMP_FV1_TILES", "0"), ("SWAMP_K23", "0")],
-                         ids=["static-fv1", "one-launch-k3", "mostly-dynamic-fv1", "no-tile-path", "separate-k2"])
+                                 ("SWAMP_FV1_TILES", "0"), ("SWAMP_K23", "1")],
+                         ids=["static-fv1", "one-launch-k3", "mostly-dynamic-fv1", "no-tile-path", "fused-k2-k3"])
 def test_level11_variants_agree(monkeypatch, env):
     """L = 11 (config 5, 22 grid-stride windows): the default engine (tail-
     balanced FV1, split K3) and a variant (static FV1 / K3 in one launch /

@@ -199,10 +199,11 @@ def test_active_subtree_paths(monkeypatch, variant, name, kw):
 @pytest.mark.parametrize("name,kw", [("river_flood", dict(L=9)), ("monai_runup", dict(L=9)),
                                      ("circular_dambreak", dict(L=9, epsilon=0.0)),
                                      ("circular_dambreak", dict(L=7, epsilon=0.0))])
-def test_tile_path_parity(name, kw):
+def test_tile_path_parity(monkeypatch, name, kw):
     """FV1's tile path (active fully refined subtrees updated as 64 x 64
-    blocks, every face computed once for both cells) == the oracle bitwise,
-    and it is actually taken."""
+    blocks, every face computed once for both cells; default from L = 11,
+    forced on here) == the oracle bitwise, and it is actually taken."""
+    monkeypatch.setenv("SWAMP_FV1_TILES", "1")
     cfg, h, qx, qy, z = cases.CASES[name](**kw)
     g = gpu.initialise(cfg, h, qx, qy, z)
     o = O.Oracle(cfg, h, qx, qy, z)
