@@ -669,6 +669,9 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             const char* et = std::getenv("SWAMP_FV1_TILES");
             const bool tl = et ? et[0] != '0' : P.n_tiles >= 1024;
             P.tiles = (Ki == 6 && !P.has_ina && tl) ? 1 : 0;
+            // quiet split of the leaf lists (SWAMP_QSPLIT=0 disables)
+            const char* eq = std::getenv("SWAMP_QSPLIT");
+            P.qsplit = (!P.has_ina && !(eq && eq[0] == '0')) ? 1 : 0;
             // fused K2 + K3: needs top_band (K2's extra-CTA work moves into the
             // top CTA) and every subtree CTA resident beside the top's SM
             // (the top waits for all of them). Measured: -1.5 to -2 us per step
