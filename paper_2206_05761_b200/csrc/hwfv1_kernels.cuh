@@ -66,6 +66,8 @@ struct Ctl {
     unsigned long long cnt_fused;                // level-(L-1) cells re-encoded by FV1 (cumulative)
     unsigned long long cnt_quiet;                // leaves FV1 updated by the dry-subtree shortcut (cumulative)
     unsigned long long cnt_tiled;                // leaves FV1 updated on its tile path (cumulative)
+    unsigned long long cnt_skip;                 // leaves of stable quiet subtrees FV1 skipped (cumulative, in cnt_quiet)
+    unsigned long long cnt_k1skip;               // subtrees whose re-encode K1 skipped (cumulative)
     alignas(128) unsigned long long cnt_new;     // newly significant cells decoded by the last K3
     unsigned long long cnt_updates;              // leaf updates of all steps so far (sum of N)
     alignas(128) unsigned long long k3_ready;    // K3's top CTA published its results (epoch)
@@ -173,6 +175,22 @@ struct Params {
     // the active ones in lists A and B (Ctl::qa_*, qb_*); FV1 updates them
     // in a lean pass (a quad per thread, no gathers, no shuffles)
     int qsplit;
+    // stable-quiet skip (qskip = 1, with qsplit): per subtree, K2 flags a tree
+    // change (tchg: its final flags differ from the previous tree's), K3's top
+    // keeps qstate = consecutive steps quiet, reached and unchanged (<= 3).
+    // With qstate >= 2 the subtree's leaves, level-(L-1) parents and pre
+    // flags in the buffer FV1 writes already hold what FV1 would write (they
+    // are FV1's output of two steps ago, and the quiet update is idempotent
+    // on dry leaves): FV1 skips the subtree and the next K1 skips its
+    // re-encode (its values in that buffer are K1's of two steps ago, from
+    // the same children). The counts they would add (near-threshold cells,
+    // re-encodes) are cached per subtree: qnk1 = K1's {near, tree}, qnfv =
+    // the quiet pass's near count. DESIGN.md §8.
+    int qskip;
+    uint8_t* tchg;
+    uint8_t* qstate;
+    uint32_t* qnk1;
+    uint32_t* qnfv;
     // inactive cells (D16), levels 0..L at slo(n): bit 0 = every finest
     // descendant inactive, bit 1 = some are; static, every partition holds
     // the whole array
@@ -1030,6 +1048,22 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
     const int L = P.L, R = P.R;
     const int K = KT ? KT : P.K;
     const uint32_t j = P.tile_lo + blockIdx.x;
+    if (P.qskip && P.qstate[j] >= 2) {
+        // stable quiet subtree (K3's top of the step that FV1 just finished
+        // skipped it): its re-encoded values, pre flags and counts in this
+        // buffer are this kernel's of two steps ago from the same children
+        // (Params::qskip); only the counts it would add
+        pdl_wait();
+        pdl_trigger();
+        const Head hd = cta_head(ctl, P, false);
+        if (hd.active && threadIdx.x == 0) {
+            const unsigned tr = P.qnk1[2 * j], nn = P.qnk1[2 * j + 1];
+            if (tr) atomicAdd(&ctl->cnt_tree, (unsigned long long)tr);
+            if (nn) atomicAdd(&ctl->near_step[hd.buf], (unsigned long long)nn);
+            atomicAdd(&ctl->cnt_k1skip, 1ull);
+        }
+        return;
+    }
     const uint32_t nv = lo(K - 1, 0);  // cells on levels R..L-2
     double4* sv = reinterpret_cast<double4*>(sm1);
     uint8_t* sf2 = sm1 + 32u * nv;     // previous-tree flags of copy 0 and copy 1, slo layout
@@ -1279,6 +1313,10 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
     const unsigned tsum = block_sum(tree | (nnear << 16), s_red);  // (both < 2^16 per subtree)
     if (threadIdx.x == 0 && (tsum & 0xFFFFu)) atomicAdd(&ctl->cnt_tree, (unsigned long long)(tsum & 0xFFFFu));
     add_near(ctl, false, hd.buf, tsum >> 16);
+    if (P.qskip && threadIdx.x == 0) {  // (cached for the steps this subtree is skipped)
+        P.qnk1[2 * j] = tsum & 0xFFFFu;
+        P.qnk1[2 * j + 1] = tsum >> 16;
+    }
     tl_end(ctl, hd.buf, 0);
     stamp(5);
 }
@@ -1488,7 +1526,10 @@ __device__ void k2_tile(const Params& P, Ctl* ctl, const Head& hd, uint32_t j, u
     const int mode = P.band_mode;
 
     // ---- one round trip: own pre flags (async) + halo words (one per thread)
+    //      (+ qskip: the previous tree's flags of the subtree, for the change test)
     const uint8_t f0 = stage_tile_flags(spre, P.pre, P, j);
+    uint8_t* sprev = spre + 2 * slo(K);
+    const uint8_t o0 = P.qskip ? stage_tile_flags(sprev, P.sig[p], P, j) : 0;
     const uint32_t hi = threadIdx.x;
     uint32_t hv = 0;
     if (mode != 0 && hi < 4u * hwd) {
@@ -1599,10 +1640,12 @@ __device__ void k2_tile(const Params& P, Ctl* ctl, const Head& hd, uint32_t j, u
     __syncthreads();
     // ---- final flags (word stores), leaf counts from popcounts
     unsigned S = 0, S1 = 0;
+    int chg = 0;  // (qskip) the subtree's final flags differ from the previous tree's
     if (threadIdx.x == 0) {
         sigc[slo(R) + j] = sf[0];
         S = sf[0];
         if (K == 1) S1 = sf[0];
+        if (P.qskip) chg = sf[0] != o0;
     }
 #pragma unroll
     for (int k = 1; k < (KT ? KT : kMaxL); ++k) {
@@ -1612,10 +1655,15 @@ __device__ void k2_tile(const Params& P, Ctl* ctl, const Head& hd, uint32_t j, u
         for (uint32_t b = threadIdx.x; b < nw; b += kThreads) {
             const uint32_t w = *reinterpret_cast<const uint32_t*>(sf + slo(k) + 4u * b);
             *reinterpret_cast<uint32_t*>(sigc + g + 4u * b) = w;
+            if (P.qskip) chg |= (w != *reinterpret_cast<const uint32_t*>(sprev + slo(k) + 4u * b)) ? 1 : 0;
             const unsigned c = __popc(w);
             S += c;
             if (k == K - 1) S1 += c;
         }
+    }
+    if (P.qskip) {
+        chg = __syncthreads_or(chg);
+        if (threadIdx.x == 0) P.tchg[j] = chg ? 1 : 0;
     }
     // one block sum of both counts (S <= 4^K / 3 < 2^16)
     const unsigned SS = block_sum(S | (S1 << 16), s_red);
@@ -1642,6 +1690,7 @@ __device__ void k2_tile(const Params& P, Ctl* ctl, const Head& hd, uint32_t j, u
 // decode source of a reached root (kNoSrc: none).
 constexpr uint32_t kEmit = 0x100u;
 constexpr uint32_t kTileSub = 0x200u;  // the subtree is on FV1's tile path: no list-A leaves emitted
+constexpr uint32_t kSkipSub = 0x400u;  // a stable quiet subtree FV1 skips: no leaves emitted
 
 __device__ __forceinline__ void k3_publish(Ctl* ctl, unsigned long long epoch) {
     __syncthreads();
@@ -1695,6 +1744,16 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     if (!EXPORT) {
         if (!band_done) stage16(tp, P.pre, fb);
         stage16(tv, sigp, fb);
+        if (staged_out && P.qskip) {  // (quiet-skip state of every subtree, read by the quiet split)
+            uint8_t* qc = stl + 2 * ((nt + 15u) & ~15u);
+            if (nt >= 16u) {
+                stage16(qc, P.tchg, nt);
+                stage16(qc + ((nt + 15u) & ~15u), P.qstate, nt);
+            } else if (threadIdx.x < nt) {
+                qc[threadIdx.x] = P.tchg[threadIdx.x];
+                qc[((nt + 15u) & ~15u) + threadIdx.x] = P.qstate[threadIdx.x];
+            }
+        }
         if (P.G > 1) {  // a partition marks every subtree under its wet leaves: OR over the partitions
             for (uint32_t t = threadIdx.x; t < nt; t += kThreads) {
                 uint8_t v = 0;
@@ -1922,6 +1981,8 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     // is not on the tile path lists its leaves after the active ones
     const bool qs = !EXPORT && staged_out && P.qsplit;
     uint8_t* sq = stl + ((nt + 15u) & ~15u);
+    const uint8_t* qchg = sq + ((nt + 15u) & ~15u);  // (staged with the wet marks)
+    const uint8_t* qst = qchg + ((nt + 15u) & ~15u);
     if (qs) {
         for (uint32_t t = a; t < b; ++t) {
             uint8_t act = swet[t];
@@ -1931,7 +1992,16 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
                 if (nb == zo::kNone) act |= (P.bc[d] == 2) ? 1 : 0;
                 else act |= swet[nb];
             }
-            sq[t] = (reach[t] && !act && !(tiles && stl[t])) ? 1 : 0;
+            uint8_t q = (reach[t] && !act && !(tiles && stl[t])) ? 1 : 0;
+            if (P.qskip) {
+                // consecutive steps quiet and unchanged; from the second one
+                // on FV1 and the next K1 skip the subtree (sq = 2)
+                const uint8_t qn = (q && !qchg[t]) ? static_cast<uint8_t>(min(qst[t] + 1, 3)) : 0;
+                if (qn != qst[t]) P.qstate[t] = qn;
+                if (qn >= 2) q = 2;
+                else if (q) P.qnfv[t] = 0u;  // (the quiet pass counts this step's near cells afresh)
+            }
+            sq[t] = q;
         }
     }
     auto counts = [&](uint32_t t, unsigned& ca, unsigned& cb) {
@@ -1939,11 +2009,15 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         ca = (r && !(tiles && stl[t])) ? cnt[t] : 0u;
         cb = r ? cnt[nt + t] : cbf[t];
     };
-    unsigned la = 0, lb = 0, lqa = 0, lqb = 0;
+    unsigned la = 0, lb = 0, lqa = 0, lqb = 0, lsk = 0, lska = 0, lskn = 0;
     for (uint32_t t = a; t < b; ++t) {
         unsigned ca, cb;
         counts(t, ca, cb);
-        if (qs && sq[t]) {
+        if (qs && sq[t] == 2) {  // skipped: on no list; its cached counts below
+            lsk += ca + cb;
+            lska += ca;
+            lskn += P.qnfv[t];
+        } else if (qs && sq[t]) {
             lqa += ca;
             lqb += cb;
         } else {
@@ -1957,6 +2031,19 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         block_exscan64((static_cast<unsigned long long>(la) << 32) | lb, s_red64, &tot64);
     unsigned long long q64 = 0;
     if (qs) q64 = block_exscan64((static_cast<unsigned long long>(lqa) << 32) | lqb, s_red64, &qtot64);
+    unsigned sk_leaves = 0;
+    if (qs && P.qskip) {  // skipped subtrees' leaves and the counts FV1 would have added
+        unsigned long long t64;
+        (void)block_exscan64((static_cast<unsigned long long>(lsk) << 32) | lska, s_red64, &t64);
+        const unsigned s0 = static_cast<unsigned>(t64 >> 32), s1 = static_cast<unsigned>(t64);
+        sk_leaves = s0;
+        if (lskn) atomicAdd(&ctl->near_step[tbuf ^ 1], (unsigned long long)lskn);  // (rare)
+        if (threadIdx.x == 0 && s0) {
+            atomicAdd(&ctl->cnt_skip, (unsigned long long)s0);
+            atomicAdd(&ctl->cnt_quiet, (unsigned long long)s0);
+            atomicAdd(&ctl->cnt_fused, (unsigned long long)(s1 >> 2));
+        }
+    }
     // list layout: [A active | A quiet | B active | B quiet]
     const unsigned taa = static_cast<unsigned>(tot64 >> 32), tba = static_cast<unsigned>(tot64);
     const unsigned tqa = static_cast<unsigned>(qtot64 >> 32), tqb = static_cast<unsigned>(qtot64);
@@ -1985,7 +2072,8 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     for (uint32_t t = a; t < b; ++t) {
         unsigned ca, cb;
         counts(t, ca, cb);
-        const bool tq = qs && sq[t];
+        const bool tsk = qs && sq[t] == 2;
+        const bool tq = qs && sq[t] == 1;
         const unsigned xa = tq ? oqa : oa, xb = tq ? oqb : ob;  // this subtree's A / B offsets
         uint32_t src = kNoSrc;
         int n = R;
@@ -2017,7 +2105,8 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
             if (staged_out) {  // (staged in shared memory, written out coalesced below)
                 sres[t] = xa;
                 sres[nt + t] = ta + xb;
-                sres[2 * nt + t] = static_cast<uint32_t>(n) | (cbf[t] ? kEmit : 0u) | ((tiles && stl[t]) ? kTileSub : 0u);
+                sres[2 * nt + t] = static_cast<uint32_t>(n) | (cbf[t] ? kEmit : 0u) | ((tiles && stl[t]) ? kTileSub : 0u) |
+                                   (tsk ? kSkipSub : 0u);
                 sres[3 * nt + t] = src;
             } else {
                 const unsigned long long tag = (epoch & 0xFFFFFFFFull) << 32;
@@ -2036,7 +2125,8 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
                 s_off[3] = ta + ob;
             }
         }
-        if (tq) {
+        if (tsk) {
+        } else if (tq) {
             oqa += ca;
             oqb += cb;
         } else {
@@ -2091,7 +2181,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     if (threadIdx.x == 0) {  // (block_exscan above: s_off complete)
         if (tn && P.part == 0) atomicAdd(&ctl->cnt_new, (unsigned long long)tn);
         const uint32_t ntl = tiles ? s_ntile : 0u;
-        ctl->n_leaves = ta + tb + (ntl << (2 * P.K));  // (tiled subtrees' level-L leaves are off list A)
+        ctl->n_leaves = ta + tb + (ntl << (2 * P.K)) + sk_leaves;  // (tiled and skipped subtrees' leaves are off the lists)
         ctl->n_leaves_A = ta;
         ctl->n_stile = ntl;
         ctl->cnt_tiled += static_cast<unsigned long long>(ntl) << (2 * P.K);
@@ -2322,7 +2412,8 @@ __device__ void k3_tile(const Params& P, Ctl* ctl, int p, int tbuf, unsigned lon
     };
     const uint32_t gbase = j * ng;
     const bool tiled = !EXPORT && (lvl & kTileSub);  // (fully refined: every leaf is a level-L one, on the tile path)
-    for (uint32_t t = a; t < b && !tiled; ++t) {
+    const bool skipped = !EXPORT && (lvl & kSkipSub);  // (stable quiet: FV1 skips it, its leaves on no list)
+    for (uint32_t t = a; t < b && !tiled && !skipped; ++t) {
         const int k = walk(t);
         const uint32_t gm = gbase + t;
         if (k <= Gk) {
@@ -3010,6 +3101,7 @@ __device__ __forceinline__ void fv1_quiet_pass(const Params& P, const double4* _
         ++tree;
         nnear += e.near ? 1u : 0u;
         nquiet += 4u;
+        if (P.qskip && e.near) atomicAdd(&P.qnfv[m0 >> (2 * (P.L - P.R))], 1u);  // (cached for skipped steps)
     }
     const uint32_t* qb = P.leaves + qb_lo;
     for (uint32_t k = tid; k < qb_n; k += nthr) {

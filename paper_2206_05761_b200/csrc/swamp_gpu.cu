@@ -513,6 +513,14 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     if ((st = dalloc(g, &P.wet[1], P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.tact, P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.stile, P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    if ((st = dalloc(g, &P.tchg, P.n_tiles))) return fail(st);
+    if ((st = dalloc(g, &P.qstate, P.n_tiles))) return fail(st);
+    if ((st = dalloc(g, &P.qnk1, 2 * P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    if ((st = dalloc(g, &P.qnfv, P.n_tiles * sizeof(uint32_t)))) return fail(st);
+    cudaMemsetAsync(P.tchg, 1, P.n_tiles, g->stream);
+    cudaMemsetAsync(P.qstate, 0, P.n_tiles, g->stream);
+    cudaMemsetAsync(P.qnk1, 0, 2 * P.n_tiles * sizeof(uint32_t), g->stream);
+    cudaMemsetAsync(P.qnfv, 0, P.n_tiles * sizeof(uint32_t), g->stream);
 
     P.pdem[0] = P.dem;
     P.pwet[0][0] = P.wet[0];
@@ -643,7 +651,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         g->smem_k1 = ncell * (sizeof(double4) + 1);                  // k_encode<true> / k_encode_top
         g->smem_k1s = 32 * (((size_t(1) << (2 * (K - 1))) - 1) / 3) + 4 * sl;  // values, 2 flag copies, DEM, new pre
         P.top_mode = (R == 0) ? 0 : (R <= 6 ? 1 : 2);
-        const size_t k2_tile = 2 * sl;
+        const size_t k2_tile = 3 * sl;  // pre flags, band / final flags, previous flags (quiet skip)
         const char* etb = std::getenv("SWAMP_TOP_BAND");
         P.top_band = (P.top_mode == 1 && G == 1 && !(etb && etb[0] == '0')) ? 1 : 0;
         const size_t k2_top = P.top_mode == 1 ? 32 * ltop + 3 * fb : 0;
@@ -672,6 +680,13 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             // quiet split of the leaf lists (SWAMP_QSPLIT=0 disables)
             const char* eq = std::getenv("SWAMP_QSPLIT");
             P.qsplit = (!P.has_ina && !(eq && eq[0] == '0')) ? 1 : 0;
+            // stable-quiet skip (needs the quiet split and K = 6: one K1 CTA
+            // per subtree). Config 5: 117 -> 97 us/step; below L = 11 its
+            // bookkeeping in K2 / K3 costs ~1 us more than it saves.
+            // SWAMP_QSKIP=0 / 1 forces it off / on
+            const char* eqs = std::getenv("SWAMP_QSKIP");
+            const bool qk = eqs ? eqs[0] != '0' : P.n_tiles >= 1024;
+            P.qskip = (P.qsplit && Ki == 6 && qk) ? 1 : 0;
             // fused K2 + K3: needs top_band (K2's extra-CTA work moves into the
             // top CTA) and every subtree CTA resident beside the top's SM
             // (the top waits for all of them). Measured: -1.5 to -2 us per step
@@ -1595,6 +1610,26 @@ int swamp_gpu_counters(swamp_gpu* g, int64_t* out8) {
     out8[6] = static_cast<int64_t>(g->ctl_host->cnt_near);
     out8[7] = static_cast<int64_t>(g->ctl_host->near_last);
     return st;
+}
+
+int swamp_gpu_skip_counters(swamp_gpu* g, int64_t* out2) {
+    if (!g || !out2) return SWAMP_E_ARG;
+    out2[0] = out2[1] = 0;
+    std::vector<swamp_gpu*> parts = g->parts.empty() ? std::vector<swamp_gpu*>{g} : g->parts;
+    if (!g->parts.empty()) {
+        const int st = group_sync(g);
+        if (st) return st;
+    }
+    for (swamp_gpu* q : parts) {
+        if (g->parts.empty()) {
+            cudaSetDevice(q->device);
+            const int st = fetch_ctl(q);
+            if (st) return st;
+        }
+        out2[0] += static_cast<int64_t>(q->ctl_host->cnt_skip);
+        out2[1] += static_cast<int64_t>(q->ctl_host->cnt_k1skip);
+    }
+    return SWAMP_OK;
 }
 
 int swamp_gpu_work_counters(swamp_gpu* g, int64_t* out8) {

@@ -63,6 +63,8 @@ def lib():
         L.swamp_gpu_counters.argtypes = [P, i64p]
         L.swamp_gpu_near_threshold.argtypes = [P, i64p]
         L.swamp_gpu_work_counters.argtypes = [P, i64p]
+        if hasattr(L, "swamp_gpu_skip_counters"):
+            L.swamp_gpu_skip_counters.argtypes = [P, i64p]
         L.swamp_gpu_enqueue.argtypes = [P, C.c_int64]
         L.swamp_gpu_timeline.argtypes = [P, dp]
         L.swamp_gpu_debug.argtypes = [P, C.POINTER(C.c_uint64)]
@@ -82,7 +84,7 @@ EXPORTED_SYMBOLS = (
     "swamp_gpu_timeline", "swamp_gpu_create_partitioned", "swamp_gpu_debug",
     "swamp_gpu_rank_create", "swamp_gpu_rank_connect", "swamp_gpu_rank_ready", "swamp_gpu_compare",
     "swamp_gpu_rebalance", "swamp_gpu_trim_cache", "swamp_gpu_near_threshold", "swamp_gpu_work_counters",
-    "swamp_gpu_sample_gauges",
+    "swamp_gpu_sample_gauges", "swamp_gpu_skip_counters",
     "swamp_io_read_esri", "swamp_io_write_esri", "swamp_io_free_raster", "swamp_io_load_dem", "swamp_io_write_finest",
     "swamp_io_write_gauges", "swamp_io_write_step_reports",
 )
@@ -275,6 +277,13 @@ class Engine:
         keys = ("k1_reencoded", "fv1_reencoded", "decoded", "leaf_updates", "quiet_updates", "tile_updates", "steps",
                 "detail_cells")
         return dict(zip(keys, (int(x) for x in a)))
+
+    def skips(self) -> dict:
+        """Stable-quiet skips (swamp_gpu_skip_counters): leaves FV1 skipped,
+        subtree re-encodes K1 skipped (cumulative)."""
+        a = (C.c_int64 * 2)()
+        self._check(lib().swamp_gpu_skip_counters(self._h, a), "skip_counters")
+        return {"fv1_skipped_leaves": int(a[0]), "k1_skipped_subtrees": int(a[1])}
 
     def launches_per_step(self) -> int:
         """Kernels one adaptive step launches (kernel nodes of the one-step graph)."""

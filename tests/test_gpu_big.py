@@ -40,8 +40,10 @@ def test_level13_steps_stay_finite():
 
 
 @pytest.mark.parametrize("env", [("SWAMP_FV1_STAGE", "3"), ("SWAMP_K3_SPLIT", "0"), ("SWAMP_FV1_TAIL16", "15"),
-                                 ("SWAMP_FV1_TILES", "0"), ("SWAMP_K23", "1")],
-                         ids=["static-fv1", "one-launch-k3", "mostly-dynamic-fv1", "no-tile-path", "fused-k2-k3"])
+                                 ("SWAMP_FV1_TILES", "0"), ("SWAMP_K23", "1"), ("SWAMP_QSKIP", "0"),
+                                 ("SWAMP_QSPLIT", "0")],
+                         ids=["static-fv1", "one-launch-k3", "mostly-dynamic-fv1", "no-tile-path", "fused-k2-k3",
+                              "no-quiet-skip", "no-quiet-split"])
 def test_level11_variants_agree(monkeypatch, env):
     """L = 11 (config 5, 22 grid-stride windows): the default engine (tail-
     balanced FV1, split K3) and a variant (static FV1 / K3 in one launch /
@@ -99,3 +101,34 @@ def test_level10_configs_match_oracle(name, kw):
         if k in (1, 4, 8):
             compare_states(g, o, f"{name} L10 step {k}")
     del g
+
+
+@pytest.mark.parametrize("name,kw,steps", [("monai_runup", dict(L=10), 400), ("river_flood", dict(L=11), 60)],
+                         ids=["monai-L10", "river-L11"])
+def test_quiet_skip_is_exact(monkeypatch, name, kw, steps):
+    """Stable quiet subtrees skipped by FV1 and K1: the
+    default engine and one without the skip (and without the quiet split)
+    stay bit-identical over a run with wetting and drying (Monai-like runup)
+    and over config 5, with the same near-threshold counts; the skip is taken."""
+    cfg, h, qx, qy, z = cases.CASES[name](**kw)
+    monkeypatch.setenv("SWAMP_QSKIP", "1")  # (default from L = 11; forced here for L = 10)
+    a = gpu.initialise(cfg, h, qx, qy, z)
+    monkeypatch.setenv("SWAMP_QSKIP", "0")
+    monkeypatch.setenv("SWAMP_QSPLIT", "0")
+    b = gpu.initialise(cfg, h, qx, qy, z)
+    for _ in range(steps // 20):
+        a.advance(20)
+        b.advance(20)
+        assert a.info() == b.info()
+    for fa, fb in zip(a.export_finest(), b.export_finest()):
+        np.testing.assert_array_equal(fa.view(np.uint64), fb.view(np.uint64))
+    (ta, *_), sa = a.export_tree()
+    (tb, *_), sb = b.export_tree()
+    np.testing.assert_array_equal(sa, sb)
+    assert a.near_threshold() == b.near_threshold()
+    wa, wb = a.work(), b.work()
+    for k in ("k1_reencoded", "fv1_reencoded", "leaf_updates", "quiet_updates", "tile_updates"):
+        assert wa[k] == wb[k], (k, wa[k], wb[k])
+    sk = a.skips()
+    assert sk["fv1_skipped_leaves"] > 0 and sk["k1_skipped_subtrees"] > 0, sk
+    print(name, sk)
