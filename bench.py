@@ -225,13 +225,21 @@ def kernel_bytes(w0, w1, steps, R_levels_detail):
     quiet = d["quiet_updates"]
     tiled = d["tile_updates"]
     active = N - quiet - tiled
+    # stable quiet subtrees move no bytes: FV1 skips their
+    # leaves (counted in quiet_updates) and their quads' fused re-encodes
+    # (counted in fv1_reencoded); K1's skipped re-encodes likewise (counted
+    # in k1_reencoded, a skipped subtree adding its cached count)
+    skipped = d.get("fv1_skipped_leaves", 0.0)
+    k1skip = d.get("k1_skipped_cells", 0.0)
     det = R_levels_detail
     return {
-        "k_encode_step": ENC_CELL * d["k1_reencoded"] + K1_FLAG * det,
+        "k_encode_step": ENC_CELL * (d["k1_reencoded"] - k1skip) + K1_FLAG * det,
         "k_band": K2_FLAG * det,
-        "k_traverse": K3_FLAG * det + K3_LEAF * N + DEC_CELL * d["decoded"],
-        "k_fv1": FV1_ACTIVE * active + FV1_QUIET * quiet + FV1_TILED * tiled + FV1_FUSED * d["fv1_reencoded"],
-    }, {"leaves": N, "active_leaves": active, "quiet_leaves": quiet, "tiled_leaves": tiled,
+        "k_traverse": K3_FLAG * det + K3_LEAF * (N - skipped) + DEC_CELL * d["decoded"],
+        "k_fv1": FV1_ACTIVE * active + FV1_QUIET * (quiet - skipped) + FV1_TILED * tiled
+                 + FV1_FUSED * (d["fv1_reencoded"] - skipped / 4.0),
+    }, {"leaves": N, "active_leaves": active, "quiet_leaves": quiet - skipped, "tiled_leaves": tiled,
+        "skipped_leaves": skipped, "k1_skipped_cells": k1skip,
         "k1_reencoded": d["k1_reencoded"],
         "fv1_reencoded": d["fv1_reencoded"], "decoded": d["decoded"]}
 
@@ -262,7 +270,7 @@ def measure_workload(gpu, torch, eng, dev, steps, warmup, L, hbm_peak, ncu, fp64
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
     stage = {v: 0.0 for v in STAGE_OF.values()}
     dev_ms = 0.0
-    w0 = eng.work()
+    w0 = {**eng.work(), **eng.skips()}
     leaves = []
     for _ in range(steps):
         flush.fill_(1)  # L2 flush (256 MiB > 126 MB L2) outside the timed interval
@@ -276,7 +284,7 @@ def measure_workload(gpu, torch, eng, dev, steps, warmup, L, hbm_peak, ncu, fp64
         leaves.append(r["n_leaves"])
         for k in stage:
             stage[k] += r[k]
-    w1 = eng.work()
+    w1 = {**eng.work(), **eng.skips()}
     K = steps
     det = sum(4 ** n for n in range(L - min(L, 6), L))  # detail cells of the subtree levels R..L-1
     alg, counts = kernel_bytes(w0, w1, K, det)

@@ -245,8 +245,9 @@ int swamp_gpu_work_counters(swamp_gpu* g, int64_t* out8);
 
 /* Stable-quiet skips: [0] leaves of stable quiet subtrees
  * whose update FV1 skipped because the buffer it writes already holds the
- * result (also counted in work_counters[4]); [1] subtree re-encodes K1
- * skipped for the same reason. Cumulative; summed over partitions. */
+ * result (also counted in work_counters[4]; their quads' re-encodes in
+ * work_counters[1]); [1] re-encoded cells K1 skipped for the same reason
+ * (also counted in work_counters[0]). Cumulative; summed over partitions. */
 int swamp_gpu_skip_counters(swamp_gpu* g, int64_t* out2);
 
 /* Near-threshold cell counts (north star: cells whose normalised detail lies

@@ -67,7 +67,7 @@ struct Ctl {
     unsigned long long cnt_quiet;                // leaves FV1 updated by the dry-subtree shortcut (cumulative)
     unsigned long long cnt_tiled;                // leaves FV1 updated on its tile path (cumulative)
     unsigned long long cnt_skip;                 // leaves of stable quiet subtrees FV1 skipped (cumulative, in cnt_quiet)
-    unsigned long long cnt_k1skip;               // subtrees whose re-encode K1 skipped (cumulative)
+    unsigned long long cnt_k1skip;               // re-encoded cells K1 skipped in stable quiet subtrees (cumulative, in cnt_tree)
     alignas(128) unsigned long long cnt_new;     // newly significant cells decoded by the last K3
     unsigned long long cnt_updates;              // leaf updates of all steps so far (sum of N)
     alignas(128) unsigned long long k3_ready;    // K3's top CTA published its results (epoch)
@@ -1060,7 +1060,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
             const unsigned tr = P.qnk1[2 * j], nn = P.qnk1[2 * j + 1];
             if (tr) atomicAdd(&ctl->cnt_tree, (unsigned long long)tr);
             if (nn) atomicAdd(&ctl->near_step[hd.buf], (unsigned long long)nn);
-            atomicAdd(&ctl->cnt_k1skip, 1ull);
+            if (tr) atomicAdd(&ctl->cnt_k1skip, (unsigned long long)tr);
         }
         return;
     }

@@ -280,10 +280,10 @@ class Engine:
 
     def skips(self) -> dict:
         """Stable-quiet skips (swamp_gpu_skip_counters): leaves FV1 skipped,
-        subtree re-encodes K1 skipped (cumulative)."""
+        re-encoded cells K1 skipped (cumulative; both inside work())."""
         a = (C.c_int64 * 2)()
         self._check(lib().swamp_gpu_skip_counters(self._h, a), "skip_counters")
-        return {"fv1_skipped_leaves": int(a[0]), "k1_skipped_subtrees": int(a[1])}
+        return {"fv1_skipped_leaves": int(a[0]), "k1_skipped_cells": int(a[1])}
 
     def launches_per_step(self) -> int:
         """Kernels one adaptive step launches (kernel nodes of the one-step graph)."""

@@ -130,5 +130,5 @@ def test_quiet_skip_is_exact(monkeypatch, name, kw, steps):
     for k in ("k1_reencoded", "fv1_reencoded", "leaf_updates", "quiet_updates", "tile_updates"):
         assert wa[k] == wb[k], (k, wa[k], wb[k])
     sk = a.skips()
-    assert sk["fv1_skipped_leaves"] > 0 and sk["k1_skipped_subtrees"] > 0, sk
+    assert sk["fv1_skipped_leaves"] > 0 and sk["k1_skipped_cells"] > 0, sk
     print(name, sk)
