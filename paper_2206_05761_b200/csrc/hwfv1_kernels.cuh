@@ -199,7 +199,6 @@ struct Params {
     // FV1 tile path (one partition, K = 6, no inactive cells): active fully
     // refined subtrees, listed by K3's top in stile[0 .. ctl->n_stile)
     int tiles;
-    int tile_rows;  // FV1 tile strips: rows per strip job (0: 4, or 2 when the jobs are scarce; SWAMP_TILE_ROWS)
     uint32_t* stile;
     Ctl* ctl_mirror;      // one partition: the host's pinned Ctl mirror (UVA), written at the step's end
     uint32_t fv1_tail16;  // FV1 STAGE 5: sixteenths of the grid-stride windows taken dynamically at the end
@@ -2847,12 +2846,10 @@ struct TileOut {
 __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, const double4* __restrict__ cur,
                                                   double4* __restrict__ nxt, const uint8_t* __restrict__ sigc,
                                                   uint32_t tile, uint32_t job, double dt, double inflow, int tbuf,
-                                                  double4* rows, int RJ) {
+                                                  double4* rows) {
     TileOut out = {0.0, 0u, 0u};
     const int L = P.L, lane = threadIdx.x & 31;
-    // job = (column half << log2(64 / RJ)) | row band; RJ = 4 or 2 rows per strip
-    const int nb = 64 / RJ;
-    const int xoff = (job & static_cast<uint32_t>(nb)) ? 32 : 0, r0 = RJ * static_cast<int>(job & static_cast<uint32_t>(nb - 1));
+    const int xoff = (job & 16u) ? 32 : 0, r0 = 4 * static_cast<int>(job & 15u);
     const uint32_t mb = tile << 12;
     const double4* cl = cur + cbase(L);
     const PhysParams& ph = P.phys;
@@ -2872,7 +2869,7 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
     // ---- loads, all issued before any arithmetic: this column's rows inside
     //      the subtree by cp.async into the slab; at the subtree's edges the
     //      outside neighbours' parent-level flags, then their cells
-    for (int i = 0; i < RJ + 2; ++i) {
+    for (int i = 0; i < 6; ++i) {
         const int y = r0 - 1 + i;
         if (y >= 0 && y < 64) {
             const double4* g = cl + mcol(y);
@@ -2883,8 +2880,7 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
     // edge lanes: 0-3 the east edge of row r0 + lane, 4-7 the west edge of
     // row r0 + lane - 4 — the strip's own edge cell and its neighbour
     const bool east = lane < 4;
-    const bool erow = (lane & 3) < RJ;  // (RJ = 2: lanes 2, 3, 6, 7 idle)
-    const int ex = east ? xoff + 31 : xoff, er = r0 + (erow ? (lane & 3) : 0);
+    const int ex = east ? xoff + 31 : xoff, er = r0 + (lane & 3);
     const uint32_t em = mc(ex, er);
     const int nx = east ? ex + 1 : ex - 1;
     const bool e_in = nx >= 0 && nx < 64;
@@ -2900,11 +2896,11 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
             if (enm != zo::kNone) ef = sigc[slo(L - 1) + (enm >> 2)];
         }
     }
-    const bool s_out = r0 == 0, n_out = r0 + RJ >= 64;
+    const bool s_out = r0 == 0, n_out = r0 + 4 >= 64;
     uint32_t onm = zo::kNone;  // the outside row's same-level cell (south / north)
     uint8_t of = 1;
     if (s_out || n_out) {
-        onm = zo::neighbour_dev(L, s_out ? mcol(r0) : mcol(r0 + RJ - 1), s_out ? zo::Direction::South : zo::Direction::North);
+        onm = zo::neighbour_dev(L, s_out ? mcol(r0) : mcol(r0 + 3), s_out ? zo::Direction::South : zo::Direction::North);
         if (onm != zo::kNone) of = sigc[slo(L - 1) + (onm >> 2)];
     }
     bool e_wall = false, o_wall = false;  // domain edge: boundary ghost
@@ -2915,7 +2911,7 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
     }
     if (s_out || n_out) {
         const double4* s = nb_src(P, cur, sigc, onm, of);
-        if (s) my[s_out ? 0 : 32 * (RJ + 1)] = ld4_nc(s);
+        if (s) my[s_out ? 0 : 160] = ld4_nc(s);
         else o_wall = true;
     }
     cp_async_wait_all();
@@ -2925,15 +2921,15 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
     // dry-neighbourhood result (h kept, q = 0), without faces
     bool dry = true;
 #pragma unroll
-    for (int i = 0; i < RJ + 2; ++i)  // (a row beyond the domain edge is a ghost of the row next to it)
-        if (!(o_wall && ((i == 0 && s_out) || (i == RJ + 1 && n_out)))) dry = dry && my[32 * i].x < ph.hdry;
-    if (lane < 8 && erow) dry = dry && eo.x < ph.hdry && (e_wall ? P.bc[east ? 1 : 0] != 2 : en.x < ph.hdry);
+    for (int i = 0; i < 6; ++i)  // (a row beyond the domain edge is a ghost of the row next to it)
+        if (!(o_wall && ((i == 0 && s_out) || (i == 5 && n_out)))) dry = dry && my[32 * i].x < ph.hdry;
+    if (lane < 8) dry = dry && eo.x < ph.hdry && (e_wall ? P.bc[east ? 1 : 0] != 2 : en.x < ph.hdry);
     if ((s_out || n_out) && o_wall) dry = dry && P.bc[s_out ? 3 : 2] != 2;
     if (__all_sync(kFull, dry)) {
         double ph0 = 0.0, pz0 = 0.0;
         uint32_t pm0 = 0;
 #pragma unroll 1
-        for (int k = 0; k < RJ; ++k) {
+        for (int k = 0; k < 4; ++k) {
             const uint32_t m = mcol(r0 + k);
             const double4 o4 = my[32 * (k + 1)];
             const double hn = (o4.x < 0.0) ? 0.0 : o4.x;
@@ -2979,9 +2975,9 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
     uint32_t pm0 = 0;
     bool wet = false;
 #pragma unroll 1
-    for (int k = 0; k < RJ; ++k) {
+    for (int k = 0; k < 4; ++k) {
         const uint32_t m = mcol(r0 + k);
-        const CellV N = (k == RJ - 1 && n_out && o_wall) ? boundary_cell(C, P.bc[2], 2, inflow, P.inflow_mode, ph)
+        const CellV N = (k == 3 && n_out && o_wall) ? boundary_cell(C, P.bc[2], 2, inflow, P.inflow_mode, ph)
                                                     : make_cell(my[32 * (k + 2)], ph);
         const FaceR fN = face_r(C, N, false, ph);
         FaceR fW = face_r(shfl_cell(C, (lane + 31) & 31), C, true, ph);  // (lane 0: replaced by the edge face)
@@ -3052,12 +3048,7 @@ __device__ __forceinline__ TileOut fv1_tile_phase(const Params& P, Ctl* ctl, con
                                                uint32_t ntile, double dt, double inflow, int tbuf) {
     __shared__ unsigned s_tj;
     TileOut acc = {0.0, 0u, 0u};
-    // rows per strip: 4, or 2 when there are fewer 4-row strips than two per
-    // warp of the grid (a strip's rows are serial: halving them halves the
-    // phase's critical path when the jobs cannot fill the warps)
-    const int RJ = P.tile_rows ? P.tile_rows : ((32u * ntile >= 2u * gridDim.x * (kThreads / 32)) ? 4 : 2);
-    const uint32_t jpt = 128u / static_cast<uint32_t>(RJ);  // strip jobs per subtree
-    const uint32_t njobs = jpt * ntile;
+    const uint32_t njobs = 32u * ntile;
     const uint32_t j1 = static_cast<uint32_t>((static_cast<unsigned long long>(njobs) * (blockIdx.x + 1)) / gridDim.x);
     if (threadIdx.x == 0)
         s_tj = static_cast<uint32_t>((static_cast<unsigned long long>(njobs) * blockIdx.x) / gridDim.x);
@@ -3069,8 +3060,8 @@ __device__ __forceinline__ TileOut fv1_tile_phase(const Params& P, Ctl* ctl, con
         if (lane == 0) jb = atomicAdd(&s_tj, 1u);
         jb = __shfl_sync(kFull, jb, 0);
         if (jb >= j1) break;
-        const TileOut to = fv1_tile_strip(P, ctl, cur, nxt, sigc, P.stile[jb / jpt], jb % jpt, dt, inflow, tbuf,
-                                          s_rows + (threadIdx.x >> 5) * (6 * 32), RJ);
+        const TileOut to = fv1_tile_strip(P, ctl, cur, nxt, sigc, P.stile[jb >> 5], jb & 31u, dt, inflow, tbuf,
+                                          s_rows + (threadIdx.x >> 5) * (6 * 32));
         acc.mx = to.mx > acc.mx ? to.mx : acc.mx;
         acc.tree += to.tree;
         acc.nnear += to.nnear;

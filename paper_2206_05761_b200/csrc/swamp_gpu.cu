@@ -677,7 +677,6 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             const char* et = std::getenv("SWAMP_FV1_TILES");
             const bool tl = et ? et[0] != '0' : P.n_tiles >= 1024;
             P.tiles = (Ki == 6 && !P.has_ina && tl) ? 1 : 0;
-            if (const char* er = std::getenv("SWAMP_TILE_ROWS")) P.tile_rows = (std::atoi(er) == 2) ? 2 : 4;
             // quiet split of the leaf lists (SWAMP_QSPLIT=0 disables)
             const char* eq = std::getenv("SWAMP_QSPLIT");
             P.qsplit = (!P.has_ina && !(eq && eq[0] == '0')) ? 1 : 0;
