@@ -452,6 +452,7 @@ __device__ __forceinline__ Head cta_head(const Ctl* c, const Params& P, bool for
 }
 
 // Block-wide sum of unsigned values (256 threads).
+template <int NT = kThreads>
 __device__ __forceinline__ unsigned block_sum(unsigned v, unsigned* scratch) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
@@ -461,7 +462,7 @@ __device__ __forceinline__ unsigned block_sum(unsigned v, unsigned* scratch) {
     __syncthreads();
     unsigned s = 0;
     if (threadIdx.x < 32) {
-        s = (l < kThreads / 32) ? scratch[l] : 0u;
+        s = (l < NT / 32) ? scratch[l] : 0u;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
         if (l == 0) scratch[0] = s;
@@ -472,6 +473,7 @@ __device__ __forceinline__ unsigned block_sum(unsigned v, unsigned* scratch) {
     return s;
 }
 // Block-wide exclusive scan (256 threads); returns prefix, *total = sum.
+template <int NT = kThreads>
 __device__ __forceinline__ unsigned block_exscan(unsigned v, unsigned* scratch, unsigned* total) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     unsigned x = v;
@@ -484,23 +486,24 @@ __device__ __forceinline__ unsigned block_exscan(unsigned v, unsigned* scratch, 
     if (l == 31) scratch[w] = x;
     __syncthreads();
     if (threadIdx.x < 32) {
-        unsigned s = (l < kThreads / 32) ? scratch[l] : 0u;
+        unsigned s = (l < NT / 32) ? scratch[l] : 0u;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned y = __shfl_up_sync(kFull, s, o);
             if (l >= o) s += y;
         }
-        if (l < kThreads / 32) scratch[l] = s;  // inclusive warp totals
+        if (l < NT / 32) scratch[l] = s;  // inclusive warp totals
     }
     __syncthreads();
     const unsigned warp_prefix = (w == 0) ? 0u : scratch[w - 1];
-    *total = scratch[kThreads / 32 - 1];
+    *total = scratch[NT / 32 - 1];
     __syncthreads();
     return warp_prefix + x - v;
 }
 
 // Block-wide exclusive scan of 64-bit values (two 32-bit counts packed as
 // hi:lo, neither total reaching 2^32); returns the prefix, *total = sum.
+template <int NT = kThreads>
 __device__ __forceinline__ unsigned long long block_exscan64(unsigned long long v, unsigned long long* scratch,
                                                              unsigned long long* total) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -514,17 +517,17 @@ __device__ __forceinline__ unsigned long long block_exscan64(unsigned long long 
     if (l == 31) scratch[w] = x;
     __syncthreads();
     if (threadIdx.x < 32) {
-        unsigned long long s = (l < kThreads / 32) ? scratch[l] : 0ull;
+        unsigned long long s = (l < NT / 32) ? scratch[l] : 0ull;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned long long y = __shfl_up_sync(kFull, s, o);
             if (l >= o) s += y;
         }
-        if (l < kThreads / 32) scratch[l] = s;
+        if (l < NT / 32) scratch[l] = s;
     }
     __syncthreads();
     const unsigned long long warp_prefix = (w == 0) ? 0ull : scratch[w - 1];
-    *total = scratch[kThreads / 32 - 1];
+    *total = scratch[NT / 32 - 1];
     __syncthreads();
     return warp_prefix + x - v;
 }
@@ -606,8 +609,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 
 // stage `bytes` (a multiple of 16, both ends 16-B aligned) into shared memory
+template <int NT = kThreads>
 __device__ __forceinline__ void stage16(void* s, const void* g, uint32_t bytes) {
-    for (uint32_t q = 16u * threadIdx.x; q < bytes; q += 16u * kThreads)
+    for (uint32_t q = 16u * threadIdx.x; q < bytes; q += 16u * NT)
         cp_async16(static_cast<uint8_t*>(s) + q, static_cast<const uint8_t*>(g) + q);
 }
 
@@ -1707,7 +1711,7 @@ __device__ __forceinline__ void k3_wait(const Ctl* ctl, unsigned long long epoch
 }
 
 // top of the tree (block 0 of K3); top flags at the padded offsets slo(n)
-template <bool EXPORT>
+template <bool EXPORT, int NT = kThreads>
 __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long long epoch, uint8_t* sm,
                        const Probe& stamp, bool band_done = false, bool staged_out = false) {
     __shared__ unsigned s_red[32];
@@ -1740,28 +1744,28 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     const int rb = EXPORT ? p : p ^ 1;
 
     // ---- stage (one round trip)
-    if (EXPORT || band_done) stage16(ts, sigc, fb);  // (band_done: K2's extra CTA banded the top cells)
+    if (EXPORT || band_done) stage16<NT>(ts, sigc, fb);  // (band_done: K2's extra CTA banded the top cells)
     if (!EXPORT) {
-        if (!band_done) stage16(tp, P.pre, fb);
-        stage16(tv, sigp, fb);
+        if (!band_done) stage16<NT>(tp, P.pre, fb);
+        stage16<NT>(tv, sigp, fb);
         if (staged_out && P.qskip) {  // (quiet-skip state of every subtree, read by the quiet split)
             uint8_t* qc = stl + 2 * ((nt + 15u) & ~15u);
             if (nt >= 16u) {
-                stage16(qc, P.tchg, nt);
-                stage16(qc + ((nt + 15u) & ~15u), P.qstate, nt);
+                stage16<NT>(qc, P.tchg, nt);
+                stage16<NT>(qc + ((nt + 15u) & ~15u), P.qstate, nt);
             } else if (threadIdx.x < nt) {
                 qc[threadIdx.x] = P.tchg[threadIdx.x];
                 qc[((nt + 15u) & ~15u) + threadIdx.x] = P.qstate[threadIdx.x];
             }
         }
         if (P.G > 1) {  // a partition marks every subtree under its wet leaves: OR over the partitions
-            for (uint32_t t = threadIdx.x; t < nt; t += kThreads) {
+            for (uint32_t t = threadIdx.x; t < nt; t += NT) {
                 uint8_t v = 0;
                 for (int g = 0; g < P.G; ++g) v |= P.pwet[g][tbuf][t];
                 swet[t] = v;
             }
         } else if (nt >= 16u) {
-            stage16(swet, P.wet[tbuf], nt);
+            stage16<NT>(swet, P.wet[tbuf], nt);
         } else if (threadIdx.x < nt) {
             swet[threadIdx.x] = P.wet[tbuf][threadIdx.x];
         }
@@ -1770,26 +1774,26 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     if (nt == 1u) {
         if (threadIdx.x == 64) r0 = P.psig[0][rb][slo(R)];
     } else if (al >= 16u) {
-        for (uint32_t q = 16u * threadIdx.x; q < nt; q += 16u * kThreads)
+        for (uint32_t q = 16u * threadIdx.x; q < nt; q += 16u * NT)
             cp_async16(ts + fb + q, P.psig[owner_of(P, R, q)][rb] + slo(R) + q);
     } else if (al >= 4u) {
-        for (uint32_t q = 4u * threadIdx.x; q < nt; q += 4u * kThreads)
+        for (uint32_t q = 4u * threadIdx.x; q < nt; q += 4u * NT)
             cp_async4(ts + fb + q, P.psig[owner_of(P, R, q)][rb] + slo(R) + q);
     } else {  // small partitioned grids (tests): plain byte copies
-        for (uint32_t q = threadIdx.x; q < nt; q += kThreads)
+        for (uint32_t q = threadIdx.x; q < nt; q += NT)
             ts[fb + q] = P.psig[owner_of(P, R, q)][rb][slo(R) + q];
     }
     if (cnt_smem) {
         if (P.G == 1 && (nt & 3u) == 0u) {
-            for (uint32_t q = 4u * threadIdx.x; q < 2u * nt; q += 4u * kThreads) cp_async16(scnt + q, P.tile_cnt + q);
+            for (uint32_t q = 4u * threadIdx.x; q < 2u * nt; q += 4u * NT) cp_async16(scnt + q, P.tile_cnt + q);
         } else {
-            for (uint32_t q = threadIdx.x; q < 2u * nt; q += kThreads) {
+            for (uint32_t q = threadIdx.x; q < 2u * nt; q += NT) {
                 const uint32_t t = q < nt ? q : q - nt;
                 cp_async4(scnt + q, P.ptile_cnt[owner_of(P, R, t)] + q);
             }
         }
     }
-    for (uint32_t q = threadIdx.x; q < nt; q += kThreads) cbf[q] = 0;
+    for (uint32_t q = threadIdx.x; q < nt; q += NT) cbf[q] = 0;
     cp_async_wait_all();
     if (threadIdx.x == 64 && nt == 1u) ts[fb] = r0;
     __syncthreads();
@@ -1797,7 +1801,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
 
     // ---- band (D3) of every top cell at once (band depends on pre flags only)
     if (!EXPORT && !band_done) {
-        for (uint32_t q = threadIdx.x; q < lo(R, 0); q += kThreads) {
+        for (uint32_t q = threadIdx.x; q < lo(R, 0); q += NT) {
             const int n = (31 - __clz(3u * q + 1u)) >> 1;  // level of compact index q
             const uint32_t m = q - lo(n, 0);
             ts[slo(n) + m] = band_flag(P.band_mode, L, n, m, [&](int k, uint32_t mm) -> uint8_t {
@@ -1903,7 +1907,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         //      parent is significant and on it); the other warps clear cbf
         // closure of level R-1 (the largest) by every thread, the rest by warp 0
         if (!EXPORT && R >= 1) {
-            for (uint32_t m = threadIdx.x; m < (1u << (2 * (R - 1))); m += kThreads)
+            for (uint32_t m = threadIdx.x; m < (1u << (2 * (R - 1))); m += NT)
                 if (*reinterpret_cast<const uint32_t*>(ts + slo(R) + 4u * m)) ts[slo(R - 1) + m] = 1;
             __syncthreads();
         }
@@ -1930,7 +1934,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         __syncthreads();
         // on-tree flags of level R (subtree roots) from level R-1, every thread
         if (R >= 1) {
-            for (uint32_t m = threadIdx.x; m < (1u << (2 * (R - 1))); m += kThreads) ontree(R - 1, m);
+            for (uint32_t m = threadIdx.x; m < (1u << (2 * (R - 1))); m += NT) ontree(R - 1, m);
             __syncthreads();
         } else if (threadIdx.x == 0) {
             ti[0] = 1;
@@ -1939,18 +1943,18 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         // newly significant top cells (decode sources exist only below them)
         unsigned nnew = 0;
         if (!EXPORT)
-            for (uint32_t q = threadIdx.x; q < lo(R, 0); q += kThreads) {
+            for (uint32_t q = threadIdx.x; q < lo(R, 0); q += NT) {
                 const int n = (31 - __clz(3u * q + 1u)) >> 1;
                 const uint32_t a = slo(n) + (q - lo(n, 0));
                 nnew += (ts[a] && !tv[a]) ? 1u : 0u;
             }
-        tn = EXPORT ? 0u : block_sum(nnew, s_red);
+        tn = EXPORT ? 0u : block_sum<NT>(nnew, s_red);
     }
 
     stamp(2);
 
     // ---- per-subtree counts, scans, depth and decode source
-    const uint32_t per = (nt + kThreads - 1) / kThreads;
+    const uint32_t per = (nt + NT - 1) / NT;
     const uint32_t a = threadIdx.x * per;
     const uint32_t b = min(nt, a + per);
     // FV1 tile path (k_fv1 fv1_tile_strip): a reached subtree whose 4^K
@@ -2025,16 +2029,16 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
             lb += cb;
         }
     }
-    __shared__ unsigned long long s_red64[kThreads / 32];
+    __shared__ unsigned long long s_red64[NT / 32];
     unsigned long long tot64, qtot64 = 0;
     const unsigned long long o64 =
-        block_exscan64((static_cast<unsigned long long>(la) << 32) | lb, s_red64, &tot64);
+        block_exscan64<NT>((static_cast<unsigned long long>(la) << 32) | lb, s_red64, &tot64);
     unsigned long long q64 = 0;
-    if (qs) q64 = block_exscan64((static_cast<unsigned long long>(lqa) << 32) | lqb, s_red64, &qtot64);
+    if (qs) q64 = block_exscan64<NT>((static_cast<unsigned long long>(lqa) << 32) | lqb, s_red64, &qtot64);
     unsigned sk_leaves = 0;
     if (qs && P.qskip) {  // skipped subtrees' leaves and the counts FV1 would have added
         unsigned long long t64;
-        (void)block_exscan64((static_cast<unsigned long long>(lsk) << 32) | lska, s_red64, &t64);
+        (void)block_exscan64<NT>((static_cast<unsigned long long>(lsk) << 32) | lska, s_red64, &t64);
         const unsigned s0 = static_cast<unsigned>(t64 >> 32), s1 = static_cast<unsigned>(t64);
         sk_leaves = s0;
         if (lskn) atomicAdd(&ctl->near_step[tbuf ^ 1], (unsigned long long)lskn);  // (rare)
@@ -2052,7 +2056,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     unsigned oqa = taa + static_cast<unsigned>(q64 >> 32), oqb = tba + static_cast<unsigned>(q64);
     stamp(3);
     if (staged_out && R >= 1) {
-        for (uint32_t c = threadIdx.x; c < (1u << (2 * (R - 1))); c += kThreads) {
+        for (uint32_t c = threadIdx.x; c < (1u << (2 * (R - 1))); c += NT) {
             int n = 0;
             while (n < R && ts[slo(n) + (c >> (2 * (R - 1 - n)))]) ++n;
             sdep[c] = static_cast<uint8_t>(n);
@@ -2173,7 +2177,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     __syncthreads();  // s_off complete
     // ---- final flags of levels < R, projection (D4) of top cells on the tree
     //      below a newly significant ancestor
-    for (uint32_t q = threadIdx.x; q < lo(R, 0); q += kThreads) {
+    for (uint32_t q = threadIdx.x; q < lo(R, 0); q += NT) {
         const int n = (31 - __clz(3u * q + 1u)) >> 1;
         const uint32_t a2 = slo(n) + (q - lo(n, 0));
         P.sig[p ^ 1][a2] = ts[a2];
@@ -2207,7 +2211,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     if (tn) {
         double4* buf = P.cells[p];
         for (int n = 1; n <= R; ++n)
-            for (uint32_t m = threadIdx.x; m < (1u << (2 * n)); m += kThreads) {
+            for (uint32_t m = threadIdx.x; m < (1u << (2 * n)); m += NT) {
                 if (!ti[slo(n) + m] || owner_of(P, n, m) != P.part) continue;
                 for (int k = 0; k < n; ++k) {
                     const uint32_t q = slo(k) + (m >> (2 * (n - k)));
@@ -2460,8 +2464,12 @@ __global__ void __launch_bounds__(kThreads, 8) k_traverse(Params P, Ctl* ctl, in
 // k3_ready flag as in k_traverse. Each subtree CTA waits for the top grid
 // before it exits, so FV1 (launched after the subtree grid) also sees the
 // top's post-publish results.
+// the top CTA runs 1024 threads: its per-subtree loops (tile listing, quiet
+// classification, counts, records, activity) take one subtree per thread at
+// L = 11
+constexpr int kTopThreads = 1024;
 template <int KT>
-__global__ void __launch_bounds__(kThreads, 1) k_traverse_top(Params P, Ctl* ctl) {
+__global__ void __launch_bounds__(kTopThreads, 1) k_traverse_top(Params P, Ctl* ctl) {
     pdl_wait();
     pdl_trigger();
     const unsigned long long t_entry = gtimer();
@@ -2471,7 +2479,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_traverse_top(Params P, Ctl* ctl
     tl_start(ctl, hd.buf, 2);
     const Probe stamp(ctl, 16);
     stamp(7, t_entry);
-    k3_top<false>(P, ctl, hd.parity, hd.buf, 2ull * static_cast<unsigned long long>(hd.step) + 2ull, smem3t, stamp,
+    k3_top<false, kTopThreads>(P, ctl, hd.parity, hd.buf, 2ull * static_cast<unsigned long long>(hd.step) + 2ull, smem3t, stamp,
                   P.top_band != 0, P.n_tiles <= 1024);
 }
 template <int KT>

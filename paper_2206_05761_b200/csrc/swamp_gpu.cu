@@ -228,10 +228,10 @@ int validate(const swamp_config* c) {
 
 // launch with programmatic stream serialisation (PDL, see pdl_wait/pdl_trigger)
 template <class... KArgs, class... Args>
-void launch_pdl(void (*kernel)(KArgs...), int grid, size_t smem, cudaStream_t s, Args... args) {
+void launch_pdl_t(void (*kernel)(KArgs...), int grid, int threads, size_t smem, cudaStream_t s, Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -240,6 +240,10 @@ void launch_pdl(void (*kernel)(KArgs...), int grid, size_t smem, cudaStream_t s,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kernel)(KArgs...), int grid, size_t smem, cudaStream_t s, Args... args) {
+    launch_pdl_t(kernel, grid, kThreads, smem, s, args...);
 }
 
 void launch_step_kernels(swamp_gpu* g, bool timed) {
@@ -271,7 +275,7 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     launch_pdl(g->k2, P.n_tiles + do_top, g->smem_k2, s, P, g->ctl, 0, do_top);
     mark(2);
     if (g->k3top) {
-        launch_pdl(g->k3top, 1, g->smem_k3top, s, P, g->ctl);
+        launch_pdl_t(g->k3top, 1, hwfv1::kTopThreads, g->smem_k3top, s, P, g->ctl);
         launch_pdl(g->k3tiles, P.n_tiles, g->smem_k3tiles, s, P, g->ctl);
     } else {
         launch_pdl(g->k3, P.n_tiles + 1, g->smem_k3, s, P, g->ctl, 0, 0ull);
