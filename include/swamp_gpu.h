@@ -167,6 +167,18 @@ int swamp_gpu_rank_ready(swamp_gpu* g);
  * (bitwise). No-op for a single partition. */
 int swamp_gpu_rebalance(swamp_gpu* g, int32_t* changed);
 
+/* Host-side partition plan (no device needed; the same code the engine uses
+ * at creation and in swamp_gpu_rebalance): the subtree boundaries bounds[0..G]
+ * of G partitions at level L. leaves_before = NULL: equal subtree counts
+ * (creation); else leaves_before[t] (t = 0..4^R, non-decreasing) = leaves in
+ * subtrees [0, t): ranges with ~equal leaf counts, boundaries on multiples of
+ * 16 subtrees when there are >= 64 per partition (4 when >= 16). */
+int swamp_partition_plan(int32_t L, int32_t G, const uint64_t* leaves_before, uint32_t* bounds);
+/* Partition owning cell (level n, Morton m) under bounds (>= 0), or < 0 on
+ * bad arguments. Cells above the subtree level belong to the owner of their
+ * first subtree. */
+int swamp_partition_owner(const uint32_t* bounds, int32_t G, int32_t L, int32_t n, uint32_t m);
+
 /* step_adaptive: one Alg. 3 iteration. No-op when
  * t >= t_end. Fills `rep` (may be NULL). Returns once the step is complete
  * and its report is in host memory (one partition: the step's last CTA

@@ -297,13 +297,16 @@ __device__ __forceinline__ uint32_t ldcg_u32(const uint32_t* p) {
 __device__ __forceinline__ uint32_t lo(int n, int R) { return ((1u << (2 * (n - R))) - 1u) / 3u; }
 
 // partition owning cell (n, m): the one holding its (first) level-R subtree
-__device__ __forceinline__ int owner_of(const Params& P, int n, uint32_t m) {
-    if (P.G == 1) return 0;
-    const uint32_t t = (n >= P.R) ? (m >> (2 * (n - P.R))) : (m << (2 * (P.R - n)));
+// partition owning cell (n, m): the owner of its (first) level-R subtree,
+// from the subtree boundaries (host twin: swamp_partition_owner)
+__host__ __device__ __forceinline__ int owner_in(const uint32_t* pbound, int G, int R, int n, uint32_t m) {
+    if (G == 1) return 0;
+    const uint32_t t = (n >= R) ? (m >> (2 * (n - R))) : (m << (2 * (R - n)));
     int g = 0;
-    while (g + 1 < P.G && t >= P.pbound[g + 1]) ++g;
+    while (g + 1 < G && t >= pbound[g + 1]) ++g;
     return g;
 }
+__device__ __forceinline__ int owner_of(const Params& P, int n, uint32_t m) { return owner_in(P.pbound, P.G, P.R, n, m); }
 __device__ __forceinline__ double4* cell_ptr(const Params& P, int buf, int n, uint32_t m) {
     return P.pcells[owner_of(P, n, m)][buf] + cbase(n) + m;
 }
@@ -530,6 +533,46 @@ __device__ __forceinline__ unsigned long long block_exscan64(unsigned long long 
     *total = scratch[NT / 32 - 1];
     __syncthreads();
     return warp_prefix + x - v;
+}
+// three independent 64-bit exclusive scans sharing one set of barriers
+// (scratch: 3 * NT / 32 words); *total[k] = sums
+template <int NT = kThreads>
+__device__ __forceinline__ void block_exscan64x3(const unsigned long long v[3], unsigned long long* scratch,
+                                                 unsigned long long out[3], unsigned long long total[3]) {
+    constexpr int NW = NT / 32;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    unsigned long long x[3] = {v[0], v[1], v[2]};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const unsigned long long y = __shfl_up_sync(kFull, x[k], o);
+            if (l >= o) x[k] += y;
+        }
+    __syncthreads();
+    if (l == 31)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) scratch[k * NW + w] = x[k];
+    __syncthreads();
+    if (threadIdx.x < 32) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            unsigned long long s = (l < NW) ? scratch[k * NW + l] : 0ull;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(kFull, s, o);
+                if (l >= o) s += y;
+            }
+            if (l < NW) scratch[k * NW + l] = s;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        out[k] = ((w == 0) ? 0ull : scratch[k * NW + w - 1]) + x[k] - v[k];
+        total[k] = scratch[k * NW + NW - 1];
+    }
+    __syncthreads();
 }
 
 // last-CTA election: every CTA fences its global writes, then bumps a counter
@@ -1507,6 +1550,9 @@ __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int fo
     extern __shared__ __align__(16) uint8_t smem2[];
     tl_start(ctl, hd.buf, 1);
     if (do_top && blockIdx.x == 0) {
+#ifdef SWAMP_EXP_K2NOTOP
+        if (hd.step < 20)
+#endif
         encode_top_staged(P, ctl, hd.parity, hd.buf, smem2);
         return;
     }
@@ -1711,9 +1757,36 @@ __device__ __forceinline__ void k3_wait(const Ctl* ctl, unsigned long long epoch
 }
 
 // top of the tree (block 0 of K3); top flags at the padded offsets slo(n)
+// shared-memory offsets of k3_top's staged arrays (also used by the split
+// top's pre-wait staging)
+struct K3TopLayout {
+    uint32_t tv, swet, qst;  // previous top flags, wet marks, quiet-skip state
+};
+__host__ __device__ __forceinline__ K3TopLayout k3_top_layout(int R, uint32_t nt) {
+    const uint32_t fb = slo(R), ftop = (fb + nt + 15u) & ~15u, pnt = (nt + 15u) & ~15u;
+    const uint32_t tv = 2 * ftop + pnt + fb;
+    const uint32_t swet = tv + fb;
+    const uint32_t scnt = swet + pnt;
+    const uint32_t sres = scnt + 4u * 2u * nt;
+    const uint32_t nr1 = R >= 1 ? (1u << (2 * (R - 1))) : 1u;
+    const uint32_t sdep = sres + 4u * 4u * nt + 4u * nr1;
+    const uint32_t stl = sdep + ((nr1 + 15u) & ~15u);
+    return {tv, swet, stl + 3u * pnt};
+}
+// the split top's staging that does not depend on K1 / K2 (previous top flags,
+// the previous FV1's wet marks, the quiet-skip state), issued before the PDL
+// wait while K2 runs (one partition, staged top)
+template <int NT>
+__device__ __forceinline__ void k3_top_prestage(const Params& P, int p, int tbuf, uint8_t* sm) {
+    const uint32_t nt = static_cast<uint32_t>(P.n_tiles);
+    const K3TopLayout ly = k3_top_layout(P.R, nt);
+    stage16<NT>(sm + ly.tv, P.sig[p], slo(P.R));
+    stage16<NT>(sm + ly.swet, P.wet[tbuf], nt);
+    if (P.qskip) stage16<NT>(sm + ly.qst, P.qstate, nt);
+}
 template <bool EXPORT, int NT = kThreads>
 __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long long epoch, uint8_t* sm,
-                       const Probe& stamp, bool band_done = false, bool staged_out = false) {
+                       const Probe& stamp, bool band_done = false, bool staged_out = false, bool prestaged = false) {
     __shared__ unsigned s_red[32];
     __shared__ unsigned s_off[6];
     const uint8_t* sigc = EXPORT ? P.sig[p] : P.sig[p ^ 1];
@@ -1747,18 +1820,19 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     if (EXPORT || band_done) stage16<NT>(ts, sigc, fb);  // (band_done: K2's extra CTA banded the top cells)
     if (!EXPORT) {
         if (!band_done) stage16<NT>(tp, P.pre, fb);
-        stage16<NT>(tv, sigp, fb);
+        if (!prestaged) stage16<NT>(tv, sigp, fb);
         if (staged_out && P.qskip) {  // (quiet-skip state of every subtree, read by the quiet split)
             uint8_t* qc = stl + 2 * ((nt + 15u) & ~15u);
             if (nt >= 16u) {
                 stage16<NT>(qc, P.tchg, nt);
-                stage16<NT>(qc + ((nt + 15u) & ~15u), P.qstate, nt);
+                if (!prestaged) stage16<NT>(qc + ((nt + 15u) & ~15u), P.qstate, nt);
             } else if (threadIdx.x < nt) {
                 qc[threadIdx.x] = P.tchg[threadIdx.x];
-                qc[((nt + 15u) & ~15u) + threadIdx.x] = P.qstate[threadIdx.x];
+                if (!prestaged) qc[((nt + 15u) & ~15u) + threadIdx.x] = P.qstate[threadIdx.x];
             }
         }
-        if (P.G > 1) {  // a partition marks every subtree under its wet leaves: OR over the partitions
+        if (prestaged) {
+        } else if (P.G > 1) {  // a partition marks every subtree under its wet leaves: OR over the partitions
             for (uint32_t t = threadIdx.x; t < nt; t += NT) {
                 uint8_t v = 0;
                 for (int g = 0; g < P.G; ++g) v |= P.pwet[g][tbuf][t];
@@ -2029,17 +2103,25 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
             lb += cb;
         }
     }
-    __shared__ unsigned long long s_red64[NT / 32];
-    unsigned long long tot64, qtot64 = 0;
-    const unsigned long long o64 =
-        block_exscan64<NT>((static_cast<unsigned long long>(la) << 32) | lb, s_red64, &tot64);
-    unsigned long long q64 = 0;
-    if (qs) q64 = block_exscan64<NT>((static_cast<unsigned long long>(lqa) << 32) | lqb, s_red64, &qtot64);
+    __shared__ unsigned long long s_red64[3 * (NT / 32)];
+    unsigned long long tot64, qtot64 = 0, o64, q64 = 0, sk64 = 0;
+    if (qs) {  // active / quiet / skipped counts in one scan
+        const unsigned long long v3[3] = {(static_cast<unsigned long long>(la) << 32) | lb,
+                                          (static_cast<unsigned long long>(lqa) << 32) | lqb,
+                                          (static_cast<unsigned long long>(lsk) << 32) | lska};
+        unsigned long long o3[3], t3[3];
+        block_exscan64x3<NT>(v3, s_red64, o3, t3);
+        o64 = o3[0];
+        tot64 = t3[0];
+        q64 = o3[1];
+        qtot64 = t3[1];
+        sk64 = t3[2];
+    } else {
+        o64 = block_exscan64<NT>((static_cast<unsigned long long>(la) << 32) | lb, s_red64, &tot64);
+    }
     unsigned sk_leaves = 0;
     if (qs && P.qskip) {  // skipped subtrees' leaves and the counts FV1 would have added
-        unsigned long long t64;
-        (void)block_exscan64<NT>((static_cast<unsigned long long>(lsk) << 32) | lska, s_red64, &t64);
-        const unsigned s0 = static_cast<unsigned>(t64 >> 32), s1 = static_cast<unsigned>(t64);
+        const unsigned s0 = static_cast<unsigned>(sk64 >> 32), s1 = static_cast<unsigned>(sk64);
         sk_leaves = s0;
         if (lskn) atomicAdd(&ctl->near_step[tbuf ^ 1], (unsigned long long)lskn);  // (rare)
         if (threadIdx.x == 0 && s0) {
@@ -2470,17 +2552,25 @@ __global__ void __launch_bounds__(kThreads, 8) k_traverse(Params P, Ctl* ctl, in
 constexpr int kTopThreads = 1024;
 template <int KT>
 __global__ void __launch_bounds__(kTopThreads, 1) k_traverse_top(Params P, Ctl* ctl) {
+    extern __shared__ __align__(16) uint8_t smem3t[];
+    // before the wait for K2: the staging that does not depend on K1 / K2
+    // (this grid launches once K2 runs, so the previous FV1 has completed:
+    // parity, step and its wet marks are final)
+    const bool pre = P.n_tiles >= 16 && P.n_tiles <= 1024;
+    const Head hd = cta_head(ctl, P, false);
+    if (pre && hd.active) k3_top_prestage<kTopThreads>(P, hd.parity, hd.buf, smem3t);
     pdl_wait();
     pdl_trigger();
     const unsigned long long t_entry = gtimer();
-    const Head hd = cta_head(ctl, P, false);
-    if (!hd.active) return;
-    extern __shared__ __align__(16) uint8_t smem3t[];
+    if (!hd.active) {
+        cp_async_wait_all();
+        return;
+    }
     tl_start(ctl, hd.buf, 2);
     const Probe stamp(ctl, 16);
     stamp(7, t_entry);
     k3_top<false, kTopThreads>(P, ctl, hd.parity, hd.buf, 2ull * static_cast<unsigned long long>(hd.step) + 2ull, smem3t, stamp,
-                  P.top_band != 0, P.n_tiles <= 1024);
+                  P.top_band != 0, P.n_tiles <= 1024, pre);
 }
 template <int KT>
 __global__ void __launch_bounds__(kThreads, 8) k_traverse_tiles(Params P, Ctl* ctl) {
@@ -2683,6 +2773,7 @@ __global__ void k_set_parity(Ctl* ctl, int v) {
 // same phase sequence, so counts match. A peer that never arrives (10 s) is
 // reported instead of hanging the GPU.
 __global__ void k_part_barrier(Params P, Ctl* ctl) {
+    pdl_wait();  // (launched with PDL behind the phase kernel: its writes first)
     if (threadIdx.x != 0) return;
     const unsigned long long seq = ctl->bar_seq + 1ull;
     __threadfence_system();
@@ -3163,6 +3254,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     double mx = 0.0;
     unsigned tree = 0, nnear = 0, ndem = 0, nquiet = 0;
     (void)ndem;
+#ifdef SWAMP_EXP_PHASET
+    unsigned long long ph_t[4];
+    ph_t[0] = gtimer();
+#endif
     if constexpr (!UNIFORM && !PART && !INA) {
         if (P.tiles && s_u[6]) {  // the tile path first (its leaves are off list A)
             const TileOut to = fv1_tile_phase(P, ctl, cur, nxt, sigc, s_u[6], dt, inflow, tbuf);
@@ -3172,8 +3267,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
         }
     }
     if constexpr (!UNIFORM && !PART && !INA) {  // (before the per-leaf windows: measured 3.5 us better than after)
+#ifdef SWAMP_EXP_PHASET
+        ph_t[1] = gtimer();
+#endif
         if (P.qsplit) fv1_quiet_pass(P, cur, nxt, s_u[7], s_u[8], s_u[9], s_u[10], tree, nnear, nquiet);
     }
+#ifdef SWAMP_EXP_PHASET
+    ph_t[2] = gtimer();
+#endif
     const uint32_t stride = gridDim.x * kThreads;
     // warp-uniform trip count: every lane runs every iteration (shuffles below)
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
@@ -3226,10 +3327,19 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
         o4_pre = ld4_nc(cur + cbase(n1) + m1);
         ta_pre = (n1 >= P.R) ? P.tact[m1 >> (2 * (n1 - P.R))] : 1;
         if ((STAGE == 3 || STAGE == 5) && !PART && n1 > 0) {  // (PART: flags through the peer tables below)
+            // a sibling neighbour (W of an east child, E of a west child, S of
+            // a north child, N of a south child) shares this leaf's parent,
+            // which is significant: only the other two flags are loaded
+            const uint32_t c = m1 & 3u;
 #pragma unroll
             for (int d = 0; d < 4; ++d) {
-                const uint32_t q = zo::neighbour_dev(n1, m1, static_cast<zo::Direction>(d));
-                fl_pre[d] = (q != zo::kNone) ? sigc[slo(n1 - 1) + (q >> 2)] : 1;
+                const bool sib = (d == 0) ? (c & 1u) != 0u : (d == 1) ? (c & 1u) == 0u : (d == 2) ? (c & 2u) == 0u : (c & 2u) != 0u;
+                if (sib) {
+                    fl_pre[d] = 1;
+                } else {
+                    const uint32_t q = zo::neighbour_dev(n1, m1, static_cast<zo::Direction>(d));
+                    fl_pre[d] = (q != zo::kNone) ? sigc[slo(n1 - 1) + (q >> 2)] : 1;
+                }
             }
         }
     };
@@ -3454,6 +3564,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
             if (s) atomicAdd(dst, s);
         }
     }
+#ifdef SWAMP_EXP_PHASET
+    ph_t[3] = gtimer();
+    if (lane == 0) {  // per warp: durations of tile phase, quiet pass, per-leaf loop (sum, max) + kernel span
+        for (int k = 0; k < 3; ++k) {
+            atomicAdd(&ctl->dbg[40 + k], ph_t[k + 1] - ph_t[k]);
+            atomicMax(&ctl->dbg[44 + k], ph_t[k + 1] - ph_t[k]);
+        }
+        atomicAdd(&ctl->dbg[47], 1ull);
+        atomicMin(&ctl->dbg[48], ph_t[0]);
+        atomicMax(&ctl->dbg[49], ph_t[3]);
+    }
+#endif
     // the next step's K1 may launch once every CTA is here: K1 CTAs made
     // resident early (trigger at entry) land on the SMs the FV1 tail frees
     // first and ran K1 5-7 us slower

@@ -691,14 +691,16 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             const char* eqs = std::getenv("SWAMP_QSKIP");
             const bool qk = eqs ? eqs[0] != '0' : P.n_tiles >= 1024;
             P.qskip = (P.qsplit && Ki == 6 && qk) ? 1 : 0;
-            // fused K2 + K3: needs top_band (K2's extra-CTA work moves into the
-            // top CTA) and every subtree CTA resident beside the top's SM
-            // (the top waits for all of them). Measured: -1.5 to -2 us per step
-            // at L = 8..10 (<= 256 subtrees), +2 to +3 us at L = 11 (1024: the
-            // top's closure waits for the slowest subtree's band); SWAMP_K23=0 /
-            // 1 forces it off / on
+            // fused K2 + K3 (opt-in, SWAMP_K23=1): needs top_band (K2's extra-CTA
+            // work moves into the top CTA) and every subtree CTA resident beside
+            // the top's SM, because the top waits for all of them. Measured
+            // -1.5 to -2 us per step at L = 8..10, +2 to +3 us at L = 11. Off by
+            // default: the top's wait for CTAs of a later launch deadlocks
+            // wherever kernels are serialised (compute-sanitizer, ncu) and is
+            // only as safe as the co-residency the occupancy check predicts
+            // (other contexts on the GPU, MPS) — DESIGN.md §8
             const char* e23 = std::getenv("SWAMP_K23");
-            const bool k23 = e23 ? e23[0] != '0' : P.n_tiles <= 256;
+            const bool k23 = e23 && e23[0] == '1';
             if (P.top_band && k23) {
                 void (*t23)(Params, Ctl*) = (Ki == 6) ? hwfv1::k_tiles23<6> : hwfv1::k_tiles23<0>;
                 const size_t sm23 = sl + g->smem_k3tiles;
@@ -842,36 +844,39 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
 // replayed independently of the others: a group of partitions in one process
 // (swamp_gpu_create_partitioned) and one partition per process
 // (swamp_gpu_rank_*) share this code.
-void part_barrier(swamp_gpu* q, cudaStream_t s) { hwfv1::k_part_barrier<<<1, 32, 0, s>>>(q->P, q->ctl); }
+void part_barrier(swamp_gpu* q, cudaStream_t s) { launch_pdl_t(hwfv1::k_part_barrier, 1, 32, 0, s, q->P, q->ctl); }
 
 // phase k of a partitioned step on stream s (k = 0..5: K1, top encode, K2,
 // K3, FV1, finalize); false when the phase does not apply
+// (every phase kernel and the barrier start with griddepcontrol.wait, so the
+// phases are chained with programmatic dependent launch: each launch overlaps
+// the tail of the kernel before it)
 bool part_step_phase(swamp_gpu* q, int k, cudaStream_t s) {
     const Params& P = q->P;
     switch (k) {
         case 0:
-            q->k1<<<P.tiles_per_part, kThreads, q->smem_k1s, s>>>(P, q->ctl);
+            launch_pdl(q->k1, static_cast<int>(P.tiles_per_part), q->smem_k1s, s, P, q->ctl);
             return true;
         case 1:
             if (P.top_mode != 2) return false;
-            hwfv1::k_encode_top<false><<<1, kThreads, q->smem_k1, s>>>(P, q->ctl);
+            launch_pdl(hwfv1::k_encode_top<false>, 1, q->smem_k1, s, P, q->ctl);
             return true;
         case 2: {
             const int do_top = P.top_mode == 1 ? 1 : 0;
-            q->k2<<<P.tiles_per_part + do_top, kThreads, q->smem_k2, s>>>(P, q->ctl, 0, do_top);
+            launch_pdl(q->k2, static_cast<int>(P.tiles_per_part) + do_top, q->smem_k2, s, P, q->ctl, 0, do_top);
             return true;
         }
-        case 3: q->k3<<<P.tiles_per_part + 1, kThreads, q->smem_k3, s>>>(P, q->ctl, 0, 0ull); return true;
+        case 3: launch_pdl(q->k3, static_cast<int>(P.tiles_per_part) + 1, q->smem_k3, s, P, q->ctl, 0, 0ull); return true;
         case 4:
-            if (P.has_ina) hwfv1::k_fv1<false, true, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
+            if (P.has_ina) launch_pdl(hwfv1::k_fv1<false, true, true>, q->fv1_grid, 0, s, P, q->ctl);
             else if (q->fv1_stage == 5)  // tail balancing (flags come from the peer tables: no STAGE 3 preloads)
-                hwfv1::k_fv1<false, true, false, 5><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
+                launch_pdl(hwfv1::k_fv1<false, true, false, 5>, q->fv1_grid, 0, s, P, q->ctl);
             else if (q->fv1_stage >= 2)  // own cells loaded an iteration ahead
-                hwfv1::k_fv1<false, true, false, 2><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
+                launch_pdl(hwfv1::k_fv1<false, true, false, 2>, q->fv1_grid, 0, s, P, q->ctl);
             else
-                hwfv1::k_fv1<false, true><<<q->fv1_grid, kThreads, 0, s>>>(P, q->ctl);
+                launch_pdl(hwfv1::k_fv1<false, true>, q->fv1_grid, 0, s, P, q->ctl);
             return true;
-        default: hwfv1::k_finalize<<<1, 32, 0, s>>>(P, q->ctl, 1); return true;
+        default: launch_pdl_t(hwfv1::k_finalize, 1, 32, 0, s, P, q->ctl, 1); return true;
     }
 }
 constexpr int kStepPhases = 6;
@@ -1168,27 +1173,35 @@ int group_advance(swamp_gpu* grp, int64_t n_steps, bool sync, swamp_step_report*
 // ---- dynamic repartitioning: contiguous subtree ranges
 // that equalise the leaf counts, from the per-subtree list offsets K3's top
 // CTA wrote (every partition holds them for all subtrees)
+// contiguous subtree ranges [nb[g], nb[g+1]) with ~equal leaf counts from the
+// cumulative counts before[t] (t = 0..nt; before[nt] = all leaves); boundary
+// granularity 16 subtrees when there are plenty (keeps K3's 16-byte staging),
+// finer for small grids; every partition keeps at least that many subtrees.
+// The same function serves swamp_partition_plan (host, no device).
+void plan_bounds_host(uint32_t nt, int G, const uint64_t* before, uint32_t* nb) {
+    const uint64_t N = before[nt];
+    const uint32_t al = (nt >= 64u * G) ? 16u : (nt >= 16u * G) ? 4u : 1u;
+    nb[0] = 0;
+    for (int g = 1; g < G; ++g) {
+        const uint64_t target = N * static_cast<uint64_t>(g) / G;
+        uint32_t t = nb[g - 1] + al;
+        while (t + al * static_cast<uint32_t>(G - g) <= nt && before[t] < target) t += al;
+        if (t + al * static_cast<uint32_t>(G - g) > nt) t = nt - al * static_cast<uint32_t>(G - g);
+        nb[g] = t;
+    }
+    for (int g = G; g <= hwfv1::kMaxParts; ++g) nb[g] = nt;
+}
+
 bool plan_bounds(swamp_gpu* q, int G, uint32_t* nb) {
     const uint32_t nt = static_cast<uint32_t>(q->P.n_tiles);
     std::vector<uint32_t> off(2 * static_cast<size_t>(nt));
     if (cudaMemcpy(off.data(), q->P.tile_off, off.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
         return false;
     const uint64_t ta = q->ctl_host->n_leaves_A, N = q->ctl_host->n_leaves;
-    auto before = [&](uint32_t t) -> uint64_t {  // leaves of subtrees [0, t)
-        return t >= nt ? N : static_cast<uint64_t>(off[t]) + off[nt + t] - ta;
-    };
-    // boundary granularity: 16 subtrees when there are plenty (keeps K3's
-    // 16-byte staging), finer for small grids
-    const uint32_t al = (nt >= 64u * G) ? 16u : (nt >= 16u * G) ? 4u : 1u;
-    nb[0] = 0;
-    for (int g = 1; g < G; ++g) {
-        const uint64_t target = N * static_cast<uint64_t>(g) / G;
-        uint32_t t = nb[g - 1] + al;  // every partition keeps at least `al` subtrees
-        while (t + al * static_cast<uint32_t>(G - g) <= nt && before(t) < target) t += al;
-        if (t + al * static_cast<uint32_t>(G - g) > nt) t = nt - al * static_cast<uint32_t>(G - g);
-        nb[g] = t;
-    }
-    for (int g = G; g <= hwfv1::kMaxParts; ++g) nb[g] = nt;
+    std::vector<uint64_t> before(static_cast<size_t>(nt) + 1);
+    for (uint32_t t = 0; t < nt; ++t) before[t] = static_cast<uint64_t>(off[t]) + off[nt + t] - ta;  // leaves of [0, t)
+    before[nt] = N;
+    plan_bounds_host(nt, G, before.data(), nb);
     return true;
 }
 
@@ -1806,6 +1819,30 @@ int swamp_gpu_compare(swamp_gpu* a, swamp_gpu* b, double* l1, double* linf) {
     *l1 = s / static_cast<double>(nf);  // sum |dh| dx^2 / area over the square: the mean
     *linf = m;
     return SWAMP_OK;
+}
+
+int swamp_partition_plan(int32_t L, int32_t G, const uint64_t* leaves_before, uint32_t* bounds) {
+    if (L < 1 || L > 13 || G < 1 || G > hwfv1::kMaxParts || !bounds) return SWAMP_E_ARG;
+    const int R = L - std::min(L, 6);
+    const uint32_t nt = 1u << (2 * R);
+    if (nt % static_cast<uint32_t>(G) != 0) return SWAMP_E_ARG;
+    uint32_t nb[hwfv1::kMaxParts + 1];
+    if (leaves_before) {
+        for (uint32_t t = 0; t < nt; ++t)
+            if (leaves_before[t + 1] < leaves_before[t]) return SWAMP_E_ARG;
+        plan_bounds_host(nt, G, leaves_before, nb);
+    } else {  // the creation plan: equal subtree counts
+        for (int g = 0; g <= hwfv1::kMaxParts; ++g) nb[g] = static_cast<uint32_t>(std::min(g, G)) * (nt / G);
+    }
+    for (int g = 0; g <= G; ++g) bounds[g] = nb[g];
+    return SWAMP_OK;
+}
+
+int swamp_partition_owner(const uint32_t* bounds, int32_t G, int32_t L, int32_t n, uint32_t m) {
+    if (!bounds || G < 1 || G > hwfv1::kMaxParts || L < 1 || L > 13 || n < 0 || n > L) return SWAMP_E_ARG;
+    if (m >= (1u << (2 * n))) return SWAMP_E_ARG;
+    const int R = L - std::min(L, 6);
+    return hwfv1::owner_in(bounds, G, R, n, m);
 }
 
 int swamp_gpu_rebalance(swamp_gpu* g, int32_t* changed) {

@@ -84,7 +84,7 @@ EXPORTED_SYMBOLS = (
     "swamp_gpu_timeline", "swamp_gpu_create_partitioned", "swamp_gpu_debug",
     "swamp_gpu_rank_create", "swamp_gpu_rank_connect", "swamp_gpu_rank_ready", "swamp_gpu_compare",
     "swamp_gpu_rebalance", "swamp_gpu_trim_cache", "swamp_gpu_near_threshold", "swamp_gpu_work_counters",
-    "swamp_gpu_sample_gauges", "swamp_gpu_skip_counters",
+    "swamp_gpu_sample_gauges", "swamp_gpu_skip_counters", "swamp_partition_plan", "swamp_partition_owner",
     "swamp_io_read_esri", "swamp_io_write_esri", "swamp_io_free_raster", "swamp_io_load_dem", "swamp_io_write_finest",
     "swamp_io_write_gauges", "swamp_io_write_step_reports",
 )
@@ -339,3 +339,31 @@ def initialise_rank(cfg: SimConfig, h, qx, qy, z, rank: int, world: int, device:
 def initialise_uniform(cfg: SimConfig, h, qx, qy, z, device: int = 0) -> Engine:
     """The uniform GPU-FV1 solver state."""
     return Engine(cfg, h, qx, qy, z, device=device, uniform=True)
+
+
+def partition_plan(L: int, G: int, leaves_before=None):
+    """The engine's partition plan (swamp_partition_plan, host code): subtree
+    boundaries of G partitions, balanced on the cumulative leaf counts when
+    given (as swamp_gpu_rebalance), else equal subtree counts (creation)."""
+    L_ = lib()
+    L_.swamp_partition_plan.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]
+    out = (C.c_uint32 * (G + 1))()
+    if leaves_before is None:
+        st = L_.swamp_partition_plan(int(L), int(G), None, out)
+    else:
+        a = np.ascontiguousarray(np.asarray(leaves_before, dtype=np.uint64))
+        st = L_.swamp_partition_plan(int(L), int(G), a.ctypes.data_as(C.POINTER(C.c_uint64)), out)
+    if st != 0:
+        raise SwampError(f"partition_plan: {STATUS.get(st, st)}")
+    return list(out)
+
+
+def partition_owner(bounds, L: int, n: int, m: int) -> int:
+    """Owner of cell (n, m) under `bounds` (swamp_partition_owner)."""
+    L_ = lib()
+    L_.swamp_partition_owner.argtypes = [C.POINTER(C.c_uint32), C.c_int32, C.c_int32, C.c_int32, C.c_uint32]
+    b = (C.c_uint32 * len(bounds))(*bounds)
+    r = L_.swamp_partition_owner(b, len(bounds) - 1, int(L), int(n), int(m))
+    if r < 0:
+        raise SwampError(f"partition_owner: {STATUS.get(r, r)}")
+    return r

@@ -52,12 +52,12 @@ def main(L):
         p.export_finest()
         print("partitioned", p.info(), flush=True)
         p.close()
-    # the L = 11 defaults forced on at this size: FV1's tile phase, the
-    # stable-quiet skip (K2's change test, K3's skip state, K1 / FV1 skips),
-    # and K2 + K3 in separate launches (the default below L = 11 is fused)
+    # the L = 11 defaults forced on at this size: FV1's tile phase and the
+    # stable-quiet skip (K2's change test, K3's skip state, K1 / FV1 skips).
+    # (The opt-in fused K2 + K3 is not run: its top waits for CTAs of a later
+    # launch, which a sanitizer serialises.)
     os.environ.update({"SWAMP_FV1_TILES": "1", "SWAMP_QSKIP": "1"})
-    for k23 in ("0", "1"):
-        os.environ["SWAMP_K23"] = k23
+    for k23 in ("0",):
         for name, make in runs[:2]:
             cfg, h, qx, qy, z = make()
             e = gpu.initialise(cfg, h, qx, qy, z)
@@ -66,7 +66,7 @@ def main(L):
             e.export_finest()
             print("forced", k23, name, e.info(), e.skips(), e.work()["tile_updates"], flush=True)
             e.close()
-    for k in ("SWAMP_FV1_TILES", "SWAMP_QSKIP", "SWAMP_K23"):
+    for k in ("SWAMP_FV1_TILES", "SWAMP_QSKIP"):
         os.environ.pop(k, None)
     gpu.trim_cache()
 

@@ -19,7 +19,7 @@ BUILD = os.path.join(ROOT, "tests", "cpp", "_build")
 
 def declared_functions():
     src = "".join(open(h).read() for h in HDRS)
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(swamp_(?:gpu|io)_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(swamp_(?:gpu|io|partition)_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_every_declared_symbol():

@@ -119,3 +119,71 @@ def test_gloo_rank_blob_exchange():
     for rank, heads, size, slowest in res:
         assert heads == [bytes([0]) * 7 + b"\x00", bytes([1]) * 7 + b"\x00"]
         assert size == 1024 and slowest == 1.5
+
+
+def _rebalance_worker(rank, world, port, L, out):
+    """One rank of a rebalance: it counts the leaves of its own subtrees (the
+    oracle's leaf list stands in for the engine state), the ranks all-gather
+    the counts, and each calls the ENGINE's planner (swamp_partition_plan,
+    the host code behind swamp_gpu_rebalance) on the cumulative counts."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    from paper_2206_05761_b200 import cases, gpu
+
+    bounds0 = gpu.partition_plan(L, world)  # creation plan: equal subtree ranges
+    R = L - min(L, 6)
+    nt = 1 << (2 * R)
+    cfg, h, qx, qy, z = cases.circular_dambreak(L=L)
+    o = O.Oracle(cfg, h, qx, qy, z)
+    o.step(3)
+    leaves, _ = o.leaves()
+    lv = np.floor(np.log2(3 * leaves.astype(np.int64) + 1)).astype(np.int64) // 2
+    first = (leaves.astype(np.int64) - (4 ** lv - 1) // 3) << (2 * (L - lv))
+    sub = first >> (2 * (L - R))  # each leaf's (first) subtree
+    lo, hi = bounds0[rank], bounds0[rank + 1]
+    mine = np.bincount(sub[(sub >= lo) & (sub < hi)], minlength=nt)[lo:hi]
+    gathered = [None] * world
+    dist.all_gather_object(gathered, mine.tolist())
+    counts = np.concatenate([np.asarray(g, dtype=np.uint64) for g in gathered])
+    before = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64)
+    bounds = gpu.partition_plan(L, world, before)
+    owners = [gpu.partition_owner(bounds, L, L, int(m)) for m in range(0, 4 ** L, 4 ** L // 64)]
+    out.put((rank, bounds0, bounds, int(before[-1]), [int(before[b]) for b in bounds], owners, len(leaves)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("L,world", [(8, 2), (9, 4)])
+def test_gloo_rebalance_plan_uses_engine_code(L, world):
+    """Dynamic repartitioning's plan on CPU ranks, computed by the engine's
+    own host code through the C-ABI: every rank gets the same contiguous
+    boundaries, they cover every subtree, the leaf counts per partition are
+    balanced to within the boundary granularity, and the engine's owner
+    lookup (swamp_partition_owner, twin of the kernels' owner_of) agrees
+    with them."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rebalance_worker, args=(r, world, port, L, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get() for _ in range(world)])
+    for pr in procs:
+        pr.join(timeout=180)
+        assert pr.exitcode == 0
+    plans = {tuple(r[2]) for r in res}
+    assert len(plans) == 1, plans  # every rank computed the same plan
+    _, bounds0, bounds, total, cum, owners, nleaves = res[0]
+    R = L - min(L, 6)
+    nt = 1 << (2 * R)
+    assert bounds0 == [g * nt // world for g in range(world + 1)]
+    assert bounds[0] == 0 and bounds[-1] == nt and all(a < b for a, b in zip(bounds, bounds[1:]))
+    assert total == nleaves
+    per = [cum[g + 1] - cum[g] for g in range(world)]
+    assert max(per) - min(per) <= max(per) * 0.5, per  # balanced (subtree granularity)
+    step = 4 ** L // 64
+    for k, g in enumerate(owners):
+        t = (k * step) >> (2 * (L - R))
+        assert bounds[g] <= t < bounds[g + 1]
