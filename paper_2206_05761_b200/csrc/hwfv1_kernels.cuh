@@ -2872,11 +2872,12 @@ __device__ __forceinline__ FaceR shfl_face(const FaceR& f, int src) {
     return {__shfl_sync(kFull, f.F0, src), __shfl_sync(kFull, f.F1, src), __shfl_sync(kFull, f.F2, src),
             __shfl_sync(kFull, f.hL, src), __shfl_sync(kFull, f.hR, src)};
 }
+// (only what face() reads: h, z, ux, uy, c — qx, qy left 0)
 __device__ __forceinline__ CellV shfl_cell(const CellV& c, int src) {
     CellV o;
     o.h = __shfl_sync(kFull, c.h, src);
-    o.qx = __shfl_sync(kFull, c.qx, src);
-    o.qy = __shfl_sync(kFull, c.qy, src);
+    o.qx = 0.0;
+    o.qy = 0.0;
     o.z = __shfl_sync(kFull, c.z, src);
     o.ux = __shfl_sync(kFull, c.ux, src);
     o.uy = __shfl_sync(kFull, c.uy, src);
@@ -2898,14 +2899,14 @@ __device__ __forceinline__ CellV nb_cell(const Params& P, const double4* cur, co
 // their order are fv1_cell_seq's, so the bits are the per-leaf path's
 __device__ __forceinline__ void cell_update(const CellV& own, const FaceR& fE, const FaceR& fW, const FaceR& fN,
                                             const FaceR& fS, double idx, double dt, const PhysParams& p, double& hn,
-                                            double& qxn, double& qyn) {
+                                            double& qxn, double& qyn, double& rh) {
     const double hh = own.h * own.h;
     const double FE1 = fE.F1 + (p.half_g * (hh - (fE.hL * fE.hL)));
     const double FW1 = fW.F1 + (p.half_g * (hh - (fW.hR * fW.hR)));
     const double GN1 = fN.F1 + (p.half_g * (hh - (fN.hL * fN.hL)));
     const double GS1 = fS.F1 + (p.half_g * (hh - (fS.hR * fS.hR)));
     fv1_finish(own, fE.F0 - fW.F0, FE1 - FW1, fE.F2 - fW.F2, fN.F0 - fS.F0, GN1 - GS1, fN.F2 - fS.F2, idx, dt, p, hn,
-               qxn, qyn);
+               qxn, qyn, rh);
 }
 
 // the direction-d neighbour of level-L leaf m outside the strip's subtree:
@@ -3089,12 +3090,12 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
             const FaceR be = shfl_face(fb, k);
             if (lane == 31) fE = be;
         }
-        double hn, qxn, qyn;
-        cell_update(C, fE, fW, fN, fS, idx, dt, ph, hn, qxn, qyn);
+        double hn, qxn, qyn, rhn;
+        cell_update(C, fE, fW, fN, fS, idx, dt, ph, hn, qxn, qyn, rhn);
         if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))
             report_error(ctl, kErrNonFinite, zo::z_of(L, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2), kStageFV1);
         st4(nxt + cbase(L) + m, make_double4(hn, qxn, qyn, C.z));
-        const double c = cfl_rate(hn, qxn, qyn, idx, ph);
+        const double c = cfl_rate_rh(hn, qxn, qyn, rhn, idx, ph);
         out.mx = c > out.mx ? c : out.mx;
         wet = wet || !(hn < ph.hdry);
         // next step's zero_details_and_reencode of level L-1 (the per-leaf
@@ -3503,7 +3504,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
                     if (wall[d]) return boundary_cell(own, 0, d, inflow, P.inflow_mode, P.phys);
                     return make_cell(nbv(d), P.phys);
                 };
-                fv1_cell_seq(own, neighbour, inv_dx_of(P, n), dt, P.phys, hn, qxn, qyn);
+                double rhn;
+                fv1_cell_seq(own, neighbour, inv_dx_of(P, n), dt, P.phys, hn, qxn, qyn, rhn);
+                // the CFL rate here, with friction's reciprocal depth (every
+                // result with h >= h_dry comes from this path; dry results
+                // and inactive leaves have rate 0)
+                const double c = cfl_rate_rh(hn, qxn, qyn, rhn, inv_dx_of(P, n), P.phys);
+                mx = c > mx ? c : mx;
             }
             }  // !quiet
             zown = o4.w;
@@ -3524,8 +3531,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
                 report_error(ctl, kErrNonFinite, zo::z_of(n, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2),
                              kStageFV1);
             st4(nxt + cbase(n) + m, make_double4(hn, qxn, qyn, zown));
-            const double c = (INA && (P.ina[slo(n) + m] & 1u)) ? 0.0 : cfl_rate(hn, qxn, qyn, inv_dx_of(P, n), P.phys);
-            mx = c > mx ? c : mx;
+
         }
         // Next step's zero_details_and_reencode of level L-1, fused here: the
         // four updated children of a previous-tree level-(L-1) cell sit in

@@ -218,9 +218,11 @@ __device__ __forceinline__ void fv1_cell(const CellV& own, const CellV nb[4], do
 
 // L_c from the face-flux differences, forward Euler, clamp, friction (the
 // tail of fv1_cell; shared by the per-leaf and the strip path of k_fv1)
+// rh_out: 1 / hn when hn >= h_dry (friction's reciprocal, reused by the CFL
+// rate of the same state: cfl_rate_rh), else 0
 __device__ __forceinline__ void fv1_finish(const CellV& own, double dFx0, double dFx1, double dFx2, double dGy0,
                                            double dGy1, double dGy2, double idx, double dt, const PhysParams& p,
-                                           double& hn, double& qxn, double& qyn) {
+                                           double& hn, double& qxn, double& qyn, double& rh_out) {
     const double Lh = (-(dFx0 * idx)) - (dGy0 * idx);
     const double Lqx = (-(dFx1 * idx)) - (dGy2 * idx);
     const double Lqy = (-(dFx2 * idx)) - (dGy1 * idx);
@@ -228,27 +230,46 @@ __device__ __forceinline__ void fv1_finish(const CellV& own, double dFx0, double
     qxn = own.qx + (dt * Lqx);
     qyn = own.qy + (dt * Lqy);
     if (hn < 0.0) hn = 0.0;
+    rh_out = 0.0;
     if (hn < p.hdry) {
         qxn = 0.0;
         qyn = 0.0;
-    } else if (p.nM > 0.0) {
-        const double qm = sqrt((qxn * qxn) + (qyn * qyn));
-        if (qm > 0.0) {
-            const double Cf = p.g_nM2 * rcbrt_det(hn);
-            const double rh = 1.0 / hn;
-            const double den = 1.0 + (((dt * Cf) * qm) * (rh * rh));
-            const double r = 1.0 / den;
-            qxn = qxn * r;
-            qyn = qyn * r;
+    } else {
+        const double rh = 1.0 / hn;
+        rh_out = rh;
+        if (p.nM > 0.0) {
+            const double qm = sqrt((qxn * qxn) + (qyn * qyn));
+            if (qm > 0.0) {
+                const double Cf = p.g_nM2 * rcbrt_det(hn);
+                const double den = 1.0 + (((dt * Cf) * qm) * (rh * rh));
+                const double r = 1.0 / den;
+                qxn = qxn * r;
+                qyn = qyn * r;
+            }
         }
     }
+}
+__device__ __forceinline__ void fv1_finish(const CellV& own, double dFx0, double dFx1, double dFx2, double dGy0,
+                                           double dGy1, double dGy2, double idx, double dt, const PhysParams& p,
+                                           double& hn, double& qxn, double& qyn) {
+    double rh;
+    fv1_finish(own, dFx0, dFx1, dFx2, dGy0, dGy1, dGy2, idx, dt, p, hn, qxn, qyn, rh);
+}
+// cfl_rate with the state's reciprocal depth already formed (rh = 1 / h when
+// h >= h_dry): the same bits as cfl_rate
+__device__ __forceinline__ double cfl_rate_rh(double h, double qx, double qy, double rh, double inv_dx,
+                                              const PhysParams& p) {
+    if (!(h >= p.hdry)) return 0.0;
+    const double aq = max2(absd(qx), absd(qy));
+    const double s = (aq * rh) + sqrt(p.g * h);
+    return s * inv_dx;
 }
 
 // Same update as fv1_cell, with the neighbours produced one face at a time
 // by `get(d)` so only one neighbour is live (register pressure / occupancy).
 template <class GetNb>
 __device__ __forceinline__ void fv1_cell_seq(const CellV& own, GetNb&& get, double idx, double dt,
-                                             const PhysParams& p, double& hn, double& qxn, double& qyn) {
+                                             const PhysParams& p, double& hn, double& qxn, double& qyn, double& rh) {
     const double h = own.h;
     const double hh = h * h;
     double hLs, hRs, F[3];
@@ -275,7 +296,7 @@ __device__ __forceinline__ void fv1_cell_seq(const CellV& own, GetNb&& get, doub
         dGy1 = GN1 - GS1;
         dGy2 = GN2 - F[2];
     }
-    fv1_finish(own, dFx0, dFx1, dFx2, dGy0, dGy1, dGy2, idx, dt, p, hn, qxn, qyn);
+    fv1_finish(own, dFx0, dFx1, dFx2, dGy0, dGy1, dGy2, idx, dt, p, hn, qxn, qyn, rh);
 }
 
 }  // namespace hwfv1

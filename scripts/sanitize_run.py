@@ -66,6 +66,16 @@ def main(L):
             e.export_finest()
             print("forced", k23, name, e.info(), e.skips(), e.work()["tile_updates"], flush=True)
             e.close()
+    # the stable-quiet skip needs dry subtrees: the Monai-like beach at L = 10
+    cfg, h, qx, qy, z = cases.monai_runup(L=max(L, 10))
+    e = gpu.initialise(cfg, h, qx, qy, z)
+    e.advance(16)
+    e.step_adaptive()
+    e.export_tree()
+    sk = e.skips()
+    print("quiet skip", e.info(), sk, flush=True)
+    assert sk["fv1_skipped_leaves"] > 0 and sk["k1_skipped_cells"] > 0, sk
+    e.close()
     for k in ("SWAMP_FV1_TILES", "SWAMP_QSKIP"):
         os.environ.pop(k, None)
     gpu.trim_cache()
