@@ -561,6 +561,10 @@ def main():
         "stage_ms_per_step": m["stage_ms"],
         "kernels": per,
         "work_per_step": m["counts"],
+        "work_note": ("leaves = leaf updates per step (the metric's unit); skipped_leaves of them belong to stable "
+                      "dry subtrees whose update FV1 skips because the buffer it writes already holds the result "
+                      "(DESIGN.md §8, bitwise-checked against the engine without the skip); they are charged no "
+                      "bytes in the roofline, and k1_skipped_cells likewise for K1"),
         "near_threshold": near,
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": d["GBps"], "peak": hbm_peak, "unit": "GB/s",
                      "frac": d["frac"], "traffic": d.get("dram_bytes_ncu"), "peak_source": peak_src,
