@@ -1786,7 +1786,8 @@ __device__ __forceinline__ void k3_top_prestage(const Params& P, int p, int tbuf
 }
 template <bool EXPORT, int NT = kThreads>
 __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long long epoch, uint8_t* sm,
-                       const Probe& stamp, bool band_done = false, bool staged_out = false, bool prestaged = false) {
+                       const Probe& stamp, bool band_done = false, bool staged_out = false, bool prestaged = false,
+                       bool tact_by_subtrees = false) {
     __shared__ unsigned s_red[32];
     __shared__ unsigned s_off[6];
     const uint8_t* sigc = EXPORT ? P.sig[p] : P.sig[p ^ 1];
@@ -2061,8 +2062,20 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     uint8_t* sq = stl + ((nt + 15u) & ~15u);
     const uint8_t* qchg = sq + ((nt + 15u) & ~15u);  // (staged with the wet marks)
     const uint8_t* qst = qchg + ((nt + 15u) & ~15u);
-    if (qs) {
-        for (uint32_t t = a; t < b; ++t) {
+    auto counts = [&](uint32_t t, unsigned& ca, unsigned& cb) {
+        const bool r = reach[t] != 0;
+        ca = (r && !(tiles && stl[t])) ? cnt[t] : 0u;
+        cb = r ? cnt[nt + t] : cbf[t];
+    };
+    // one pass per subtree: its counts, and (quiet split) its class — active,
+    // quiet (sq = 1), or stable quiet and skipped (sq = 2)
+    unsigned la = 0, lb = 0, lqa = 0, lqb = 0, lsk = 0, lska = 0, lskn = 0;
+    for (uint32_t t = a; t < b; ++t) {
+        const uint32_t qf = (qs && P.qskip) ? P.qnfv[t] : 0u;  // (issued first: a global load)
+        unsigned ca, cb;
+        counts(t, ca, cb);
+        uint8_t q = 0;
+        if (qs) {
             uint8_t act = swet[t];
 #pragma unroll
             for (int d = 0; d < 4; ++d) {
@@ -2070,7 +2083,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
                 if (nb == zo::kNone) act |= (P.bc[d] == 2) ? 1 : 0;
                 else act |= swet[nb];
             }
-            uint8_t q = (reach[t] && !act && !(tiles && stl[t])) ? 1 : 0;
+            q = (reach[t] && !act && !(tiles && stl[t])) ? 1 : 0;
             if (P.qskip) {
                 // consecutive steps quiet and unchanged; from the second one
                 // on FV1 and the next K1 skip the subtree (sq = 2)
@@ -2081,21 +2094,11 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
             }
             sq[t] = q;
         }
-    }
-    auto counts = [&](uint32_t t, unsigned& ca, unsigned& cb) {
-        const bool r = reach[t] != 0;
-        ca = (r && !(tiles && stl[t])) ? cnt[t] : 0u;
-        cb = r ? cnt[nt + t] : cbf[t];
-    };
-    unsigned la = 0, lb = 0, lqa = 0, lqb = 0, lsk = 0, lska = 0, lskn = 0;
-    for (uint32_t t = a; t < b; ++t) {
-        unsigned ca, cb;
-        counts(t, ca, cb);
-        if (qs && sq[t] == 2) {  // skipped: on no list; its cached counts below
+        if (q == 2) {  // skipped: on no list; its cached counts below
             lsk += ca + cb;
             lska += ca;
-            lskn += P.qnfv[t];
-        } else if (qs && sq[t]) {
+            lskn += qf;
+        } else if (q) {
             lqa += ca;
             lqb += cb;
         } else {
@@ -2242,10 +2245,10 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         s_off[2] = ta;
         s_off[3] = ta + tb;
     }
-    for (uint32_t t = a; t < b; ++t) {
+    for (uint32_t t = a; t < b && !tact_by_subtrees; ++t) {
         // FV1 dry shortcut: subtree t is active if it or a face-adjacent
         // subtree holds a wet cell, or it touches an inflow edge; clear the
-        // flags FV1 sets next
+        // flags FV1 sets next (the split K3's subtree CTAs do it for their own)
         uint8_t act = swet[t];
 #pragma unroll
         for (int d = 0; d < 4; ++d) {
@@ -2570,7 +2573,23 @@ __global__ void __launch_bounds__(kTopThreads, 1) k_traverse_top(Params P, Ctl* 
     const Probe stamp(ctl, 16);
     stamp(7, t_entry);
     k3_top<false, kTopThreads>(P, ctl, hd.parity, hd.buf, 2ull * static_cast<unsigned long long>(hd.step) + 2ull, smem3t, stamp,
-                  P.top_band != 0, P.n_tiles <= 1024, pre);
+                  P.top_band != 0, P.n_tiles <= 1024, pre, true);
+}
+// FV1's dry-shortcut activity of subtree j (the or of its own and its face
+// neighbours' wet marks, inflow edges active) and the clear of the mark FV1
+// sets next — by the subtree's own K3 CTA (split K3), not the top
+__device__ __forceinline__ void subtree_activity(const Params& P, int tbuf, uint32_t j) {
+    if (threadIdx.x != 0) return;
+    const uint8_t* w = P.wet[tbuf];
+    uint8_t act = w[j];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+        const uint32_t nb = zo::neighbour_dev(P.R, j, static_cast<zo::Direction>(d));
+        if (nb == zo::kNone) act |= (P.bc[d] == 2) ? 1 : 0;
+        else act |= w[nb];
+    }
+    P.tact[j] = act;
+    P.wet[tbuf ^ 1][j] = 0;
 }
 template <int KT>
 __global__ void __launch_bounds__(kThreads, 8) k_traverse_tiles(Params P, Ctl* ctl) {
@@ -2584,6 +2603,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_traverse_tiles(Params P, Ctl* c
         stamp(7, t_entry);
         k3_tile<false, KT>(P, ctl, hd.parity, hd.buf, 2ull * static_cast<unsigned long long>(hd.step) + 2ull,
                            P.tile_lo + blockIdx.x, smem3s, stamp);
+        subtree_activity(P, hd.buf, P.tile_lo + blockIdx.x);  // (after the emit: off the records' critical path)
     }
     pdl_wait();  // the top grid has completed before this grid does
 }
