@@ -1870,6 +1870,8 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     }
     for (uint32_t q = threadIdx.x; q < nt; q += NT) cbf[q] = 0;
     cp_async_wait_all();
+    __shared__ unsigned s_nwet;  // wet subtrees (R = 5 closure path), else ~0
+    if (threadIdx.x == 0) s_nwet = (!EXPORT && R == 5 && NT > 32) ? 0u : ~0u;
     if (threadIdx.x == 64 && nt == 1u) ts[fb] = r0;
     __syncthreads();
     stamp(0);
@@ -1895,6 +1897,13 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         // and 0 in every lane), written back to the byte arrays once — the
         // same flags the generic pass below produces
         __shared__ unsigned s_tn;
+        if (threadIdx.x >= 32) {  // meanwhile: the wet subtrees (the tile listing's density test)
+            unsigned nw = 0;
+            for (uint32_t t = threadIdx.x - 32; t < nt; t += NT - 32) nw += swet[t] ? 1u : 0u;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) nw += __shfl_xor_sync(kFull, nw, o);
+            if ((threadIdx.x & 31) == 0 && nw) atomicAdd(&s_nwet, nw);
+        }
         if (threadIdx.x < 32) {
             const uint32_t l = threadIdx.x;
             auto bits4 = [](uint32_t x) { return ((x * 0x01020408u) >> 24) & 0xFu; };  // 4 bytes (0/1) -> 4 bits
@@ -2038,16 +2047,38 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     // leave list A (counted in n_leaves all the same) and it joins P.stile
     if (tiles) {
         if (threadIdx.x == 0) s_ntile = 0u;
-        __syncthreads();
+        // which fully refined subtrees take the tile path: when most subtrees
+        // hold wet cells (a wet-dominated domain), every active one (it or a
+        // face neighbour wet, or an inflow edge); otherwise only those inside
+        // the wet region (it and all its face neighbours wet) — where the wet
+        // cells are sparse the per-leaf path's per-cell dry shortcut is
+        // cheaper than a strip's rows (measured: config 5 91 vs 104 us/step
+        // with every active subtree tiled; the Monai-like runup 139 vs 157)
+        bool dense;
+        if (s_nwet != ~0u) {  // (counted by warps 1.. during warp 0's closure)
+            dense = 2u * s_nwet > nt;
+        } else {
+            unsigned nw = 0;
+            for (uint32_t t = a; t < b; ++t) nw += swet[t] ? 1u : 0u;
+            dense = 2u * block_sum<NT>(nw, s_red) > nt;
+        }
         for (uint32_t t = a; t < b; ++t) {
-            // (the tile path computes every face — no per-cell dry
-            // shortcut — so only subtrees inside the wet region take it:
-            // the subtree and its face neighbours held wet cells)
-            bool inner = swet[t] != 0;
+            bool inner;
+            if (dense) {
+                inner = swet[t] != 0;
 #pragma unroll
-            for (int d = 0; d < 4; ++d) {
-                const uint32_t nb = zo::neighbour_dev(R, t, static_cast<zo::Direction>(d));
-                inner = inner && (nb == zo::kNone || swet[nb] != 0);
+                for (int d = 0; d < 4; ++d) {
+                    const uint32_t nb = zo::neighbour_dev(R, t, static_cast<zo::Direction>(d));
+                    if (nb == zo::kNone) inner = inner || P.bc[d] == 2;
+                    else inner = inner || swet[nb] != 0;
+                }
+            } else {
+                inner = swet[t] != 0;
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const uint32_t nb = zo::neighbour_dev(R, t, static_cast<zo::Direction>(d));
+                    inner = inner && (nb == zo::kNone || swet[nb] != 0);
+                }
             }
             const bool tl = inner && reach[t] && cnt[t] == (1u << (2 * P.K));
             stl[t] = tl ? 1 : 0;
