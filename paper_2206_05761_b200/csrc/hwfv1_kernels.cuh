@@ -1550,9 +1550,6 @@ __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int fo
     extern __shared__ __align__(16) uint8_t smem2[];
     tl_start(ctl, hd.buf, 1);
     if (do_top && blockIdx.x == 0) {
-#ifdef SWAMP_EXP_K2NOTOP
-        if (hd.step < 20)
-#endif
         encode_top_staged(P, ctl, hd.parity, hd.buf, smem2);
         return;
     }

@@ -11,6 +11,3 @@ TAG=head SWAMP_GPU_LIB=$PWD/build_variants/libswamp_gpu_head.so timeout 300 pyth
 timeout 300 python scripts/part_overhead.py | tee gpurun_out/r2g_part_overhead.json
 SWAMP_GPU_LIB=$PWD/build_variants/libswamp_gpu_head.so timeout 300 python scripts/part_overhead.py
 SWAMP_GPU_LIB=$PWD/build_variants/libswamp_gpu_phaset.so timeout 300 python scripts/fv1_phases.py
-# K2 critical path probe: the top re-encode skipped after step 20 (results wrong, timing only)
-TAG=k2notop SWAMP_GPU_LIB=$PWD/build_variants/libswamp_gpu_k2notop.so timeout 300 python scripts/tl_b2b.py 2>/dev/null | head -1
-TAG=new timeout 300 python scripts/tl_b2b.py 2>/dev/null | head -1
