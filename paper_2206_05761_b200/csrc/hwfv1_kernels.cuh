@@ -170,6 +170,15 @@ struct Params {
     // subtree t or a face-adjacent one is wet, or t touches an inflow edge
     uint8_t* wet[2];
     uint8_t* tact;
+    // quadrant wet marks (qact = 1: one partition, split K3): qwet[b][4 t + q]
+    // = a leaf of quadrant q (the level-(R+1) cell, Morton child q) of subtree
+    // t ended the step wet. The dry-shortcut activity of a subtree with a
+    // refined root then asks only whether the two quadrants of each neighbour
+    // that face it hold wet cells (a leaf's flux neighbour across the edge
+    // lies in one of them, or is a leaf covering it); a subtree whose root is
+    // not refined asks whether its neighbours hold any
+    uint8_t* qwet[2];
+    int qact;
     // quiet split (one partition, split K3, no inactive cells): K3's top
     // places the leaves of reached subtrees whose neighbourhood is dry after
     // the active ones in lists A and B (Ctl::qa_*, qb_*); FV1 updates them
@@ -1754,10 +1763,33 @@ __device__ __forceinline__ void k3_wait(const Ctl* ctl, unsigned long long epoch
 }
 
 // top of the tree (block 0 of K3); top flags at the padded offsets slo(n)
+// activity of subtree t from any-wet marks w[] and quadrant marks qw[]
+// (qact): t itself wet, an inflow edge, or — per face neighbour — its two
+// quadrants facing t wet (t's root refined) / any of it wet (root not refined)
+__device__ __forceinline__ uint8_t activity_q(const Params& P, uint32_t t, const uint8_t* w, const uint8_t* qw,
+                                              bool root_refined) {
+    uint8_t act = w[t];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+        const uint32_t nb = zo::neighbour_dev(P.R, t, static_cast<zo::Direction>(d));
+        if (nb == zo::kNone) {
+            act |= (P.bc[d] == 2) ? 1 : 0;
+        } else if (!root_refined) {
+            act |= w[nb];
+        } else {
+            // the neighbour's quadrants facing t: W neighbour -> its SE, NE
+            // (1, 3); E -> SW, NW (0, 2); N -> SW, SE (0, 1); S -> NW, NE (2, 3)
+            const uint32_t qa = (d == 0) ? 1u : (d == 1) ? 0u : (d == 2) ? 0u : 2u;
+            const uint32_t qb = (d == 0) ? 3u : (d == 1) ? 2u : (d == 2) ? 1u : 3u;
+            act |= qw[4u * nb + qa] | qw[4u * nb + qb];
+        }
+    }
+    return act ? 1 : 0;
+}
 // shared-memory offsets of k3_top's staged arrays (also used by the split
 // top's pre-wait staging)
 struct K3TopLayout {
-    uint32_t tv, swet, qst;  // previous top flags, wet marks, quiet-skip state
+    uint32_t tv, swet, qst, sqw;  // previous top flags, wet marks, quiet-skip state, quadrant wet marks
 };
 __host__ __device__ __forceinline__ K3TopLayout k3_top_layout(int R, uint32_t nt) {
     const uint32_t fb = slo(R), ftop = (fb + nt + 15u) & ~15u, pnt = (nt + 15u) & ~15u;
@@ -1768,7 +1800,7 @@ __host__ __device__ __forceinline__ K3TopLayout k3_top_layout(int R, uint32_t nt
     const uint32_t nr1 = R >= 1 ? (1u << (2 * (R - 1))) : 1u;
     const uint32_t sdep = sres + 4u * 4u * nt + 4u * nr1;
     const uint32_t stl = sdep + ((nr1 + 15u) & ~15u);
-    return {tv, swet, stl + 3u * pnt};
+    return {tv, swet, stl + 3u * pnt, stl + 4u * pnt};
 }
 // the split top's staging that does not depend on K1 / K2 (previous top flags,
 // the previous FV1's wet marks, the quiet-skip state), issued before the PDL
@@ -1780,6 +1812,7 @@ __device__ __forceinline__ void k3_top_prestage(const Params& P, int p, int tbuf
     stage16<NT>(sm + ly.tv, P.sig[p], slo(P.R));
     stage16<NT>(sm + ly.swet, P.wet[tbuf], nt);
     if (P.qskip) stage16<NT>(sm + ly.qst, P.qstate, nt);
+    if (P.qact) stage16<NT>(sm + ly.sqw, P.qwet[tbuf], 4u * nt);
 }
 template <bool EXPORT, int NT = kThreads>
 __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long long epoch, uint8_t* sm,
@@ -2090,6 +2123,8 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     uint8_t* sq = stl + ((nt + 15u) & ~15u);
     const uint8_t* qchg = sq + ((nt + 15u) & ~15u);  // (staged with the wet marks)
     const uint8_t* qst = qchg + ((nt + 15u) & ~15u);
+    const uint8_t* sqw = qst + ((nt + 15u) & ~15u);  // quadrant wet marks (qact; staged before the wait)
+    const bool use_q = qs && P.qact && prestaged;
     auto counts = [&](uint32_t t, unsigned& ca, unsigned& cb) {
         const bool r = reach[t] != 0;
         ca = (r && !(tiles && stl[t])) ? cnt[t] : 0u;
@@ -2104,12 +2139,17 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         counts(t, ca, cb);
         uint8_t q = 0;
         if (qs) {
-            uint8_t act = swet[t];
+            uint8_t act;
+            if (use_q) {
+                act = activity_q(P, t, swet, sqw, ts[fb + t] != 0);
+            } else {
+                act = swet[t];
 #pragma unroll
-            for (int d = 0; d < 4; ++d) {
-                const uint32_t nb = zo::neighbour_dev(R, t, static_cast<zo::Direction>(d));
-                if (nb == zo::kNone) act |= (P.bc[d] == 2) ? 1 : 0;
-                else act |= swet[nb];
+                for (int d = 0; d < 4; ++d) {
+                    const uint32_t nb = zo::neighbour_dev(R, t, static_cast<zo::Direction>(d));
+                    if (nb == zo::kNone) act |= (P.bc[d] == 2) ? 1 : 0;
+                    else act |= swet[nb];
+                }
             }
             q = (reach[t] && !act && !(tiles && stl[t])) ? 1 : 0;
             if (P.qskip) {
@@ -2606,17 +2646,23 @@ __global__ void __launch_bounds__(kTopThreads, 1) k_traverse_top(Params P, Ctl* 
 // FV1's dry-shortcut activity of subtree j (the or of its own and its face
 // neighbours' wet marks, inflow edges active) and the clear of the mark FV1
 // sets next — by the subtree's own K3 CTA (split K3), not the top
-__device__ __forceinline__ void subtree_activity(const Params& P, int tbuf, uint32_t j) {
+__device__ __forceinline__ void subtree_activity(const Params& P, int tbuf, int parity, uint32_t j) {
     if (threadIdx.x != 0) return;
     const uint8_t* w = P.wet[tbuf];
-    uint8_t act = w[j];
+    if (P.qact) {
+        const bool refined = P.sig[parity ^ 1][slo(P.R) + j] != 0;  // (this step's tree)
+        P.tact[j] = activity_q(P, j, w, P.qwet[tbuf], refined);
+        *reinterpret_cast<uint32_t*>(P.qwet[tbuf ^ 1] + 4u * j) = 0u;
+    } else {
+        uint8_t act = w[j];
 #pragma unroll
-    for (int d = 0; d < 4; ++d) {
-        const uint32_t nb = zo::neighbour_dev(P.R, j, static_cast<zo::Direction>(d));
-        if (nb == zo::kNone) act |= (P.bc[d] == 2) ? 1 : 0;
-        else act |= w[nb];
+        for (int d = 0; d < 4; ++d) {
+            const uint32_t nb = zo::neighbour_dev(P.R, j, static_cast<zo::Direction>(d));
+            if (nb == zo::kNone) act |= (P.bc[d] == 2) ? 1 : 0;
+            else act |= w[nb];
+        }
+        P.tact[j] = act;
     }
-    P.tact[j] = act;
     P.wet[tbuf ^ 1][j] = 0;
 }
 template <int KT>
@@ -2631,7 +2677,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_traverse_tiles(Params P, Ctl* c
         stamp(7, t_entry);
         k3_tile<false, KT>(P, ctl, hd.parity, hd.buf, 2ull * static_cast<unsigned long long>(hd.step) + 2ull,
                            P.tile_lo + blockIdx.x, smem3s, stamp);
-        subtree_activity(P, hd.buf, P.tile_lo + blockIdx.x);  // (after the emit: off the records' critical path)
+        subtree_activity(P, hd.buf, hd.parity, P.tile_lo + blockIdx.x);  // (after the emit: off the records' critical path)
     }
     pdl_wait();  // the top grid has completed before this grid does
 }
@@ -3176,7 +3222,10 @@ __device__ __forceinline__ TileOut fv1_tile_strip(const Params& P, Ctl* ctl, con
         fS = fN;
         C = N;
     }
-    if (__any_sync(kFull, wet) && lane == 0) P.wet[tbuf ^ 1][tile] = 1;
+    if (__any_sync(kFull, wet) && lane == 0) {
+        P.wet[tbuf ^ 1][tile] = 1;
+        if (P.qact) P.qwet[tbuf ^ 1][4u * tile + ((r0 >> 5) << 1) + (xoff >> 5)] = 1;  // (the strip lies in one quadrant)
+    }
     __syncwarp();  // (the slab is refilled by the next job)
     return out;
 }
@@ -3573,6 +3622,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
                 } else {
                     const uint32_t t0 = m << (2 * (P.R - n)), t1 = (m + 1u) << (2 * (P.R - n));
                     for (uint32_t t = t0; t < t1; ++t) wn[t] = 1;
+                }
+                if (!UNIFORM && !PART && P.qact) {  // quadrant marks (level R + 1; coarser leaves: all quadrants under them)
+                    uint8_t* qn = P.qwet[tbuf ^ 1];
+                    if (n > P.R) {
+                        qn[m >> (2 * (n - P.R - 1))] = 1;
+                    } else {
+                        const uint32_t t0 = m << (2 * (P.R - n)), t1 = (m + 1u) << (2 * (P.R - n));
+                        for (uint32_t t = t0; t < t1; ++t) *reinterpret_cast<uint32_t*>(qn + 4u * t) = 0x01010101u;
+                    }
                 }
             }
             if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))

@@ -516,6 +516,8 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     if ((st = dalloc(g, &P.wet[0], P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.wet[1], P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.tact, P.n_tiles))) return fail(st);
+    if ((st = dalloc(g, &P.qwet[0], 4 * P.n_tiles))) return fail(st);
+    if ((st = dalloc(g, &P.qwet[1], 4 * P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.stile, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.tchg, P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.qstate, P.n_tiles))) return fail(st);
@@ -534,6 +536,8 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     // every subtree counts as wet until FV1 has run once
     cudaMemsetAsync(P.wet[0], 1, P.n_tiles, g->stream);
     cudaMemsetAsync(P.wet[1], 1, P.n_tiles, g->stream);
+    cudaMemsetAsync(P.qwet[0], 1, 4 * P.n_tiles, g->stream);
+    cudaMemsetAsync(P.qwet[1], 1, 4 * P.n_tiles, g->stream);
     cudaMemsetAsync(P.tact, 1, P.n_tiles, g->stream);
     if ((st = dalloc(g, &P.tile_src, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.k3_rec, P.n_tiles * 4 * sizeof(unsigned long long)))) return fail(st);
@@ -684,6 +688,9 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             // quiet split of the leaf lists (SWAMP_QSPLIT=0 disables)
             const char* eq = std::getenv("SWAMP_QSPLIT");
             P.qsplit = (!P.has_ina && !(eq && eq[0] == '0')) ? 1 : 0;
+            // quadrant wet marks for the activity test (SWAMP_QACT=0 disables)
+            const char* eqa = std::getenv("SWAMP_QACT");
+            P.qact = (P.qsplit && !(eqa && eqa[0] == '0')) ? 1 : 0;
             // stable-quiet skip (needs the quiet split and K = 6: one K1 CTA
             // per subtree). Config 5: 117 -> 97 us/step; below L = 11 its
             // bookkeeping in K2 / K3 costs ~1 us more than it saves.
