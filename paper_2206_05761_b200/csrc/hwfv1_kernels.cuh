@@ -211,6 +211,10 @@ struct Params {
     uint32_t* stile;
     Ctl* ctl_mirror;      // one partition: the host's pinned Ctl mirror (UVA), written at the step's end
     uint32_t fv1_tail16;  // FV1 STAGE 5: sixteenths of the grid-stride windows taken dynamically at the end
+    // FV1 STAGE 3, short leaf lists: 4 (or 2) lanes per leaf, one face (pair)
+    // each, when 4 (2) lanes per leaf fit fv1_fp_cap16 / 16 of the grid's
+    // threads (0: off)
+    uint32_t fv1_fp_cap16;
     // Morton-subtree partitions: this partition owns level-R
     // subtrees [tile_lo, tile_hi); cells on levels >= R belong to their
     // subtree's partition, cells above R are replicated except that a leaf's
@@ -2682,60 +2686,58 @@ __global__ void __launch_bounds__(kThreads, 8) k_traverse_tiles(Params P, Ctl* c
     pdl_wait();  // the top grid has completed before this grid does
 }
 
-// Fused K2 + K3 (one partition, every subtree CTA resident at once: the
-// host enables it only when the subtree grid fits beside the top CTA's SM).
-// The top CTA passes its wait for K1, lets the subtree grid launch, re-encodes
-// levels R-1..0 and bands the top cells (K2's extra CTA), then waits until
-// every subtree CTA has published its band / closure / counts (k2_done) and
-// runs K3's top. A subtree CTA runs K2's subtree work on K1's pre flags
-// (visible: the top triggered this grid after its wait for K1), publishes it,
-// and goes on with K3's subtree work on the final flags it still holds in
-// shared memory. One launch and one kernel boundary less than K2 -> K3.
+// Fused K2 + K3 in ONE cooperative grid (one partition): block 0 is the top,
+// blocks 1..n_tiles the subtree CTAs. The cooperative launch guarantees that
+// every CTA is resident at once (the launch fails otherwise; the host checks
+// the occupancy first), so the waits below cannot deadlock whatever order
+// the CTAs are scheduled in, and none waits on a CTA of a later launch (a
+// two-launch version hung wherever kernels are serialised: compute-sanitizer,
+// ncu). The top re-encodes levels R-1..0 and bands the top cells (K2's extra
+// CTA), waits until every subtree CTA has published its band / closure /
+// counts (k2_done) and runs K3's top. A subtree CTA runs K2's subtree work on
+// K1's pre flags, publishes it, and goes on with K3's subtree work on the
+// final flags it still holds in shared memory (polling the top's records).
+// One launch and one kernel boundary less than K2 -> K3.
 template <int KT>
-__global__ void __launch_bounds__(kThreads, 1) k_top23(Params P, Ctl* ctl) {
+__global__ void __launch_bounds__(kThreads, 2) k_23(Params P, Ctl* ctl) {
     pdl_wait();
-    pdl_trigger();
     const unsigned long long t_entry = gtimer();
     const Head hd = cta_head(ctl, P, false);
-    if (!hd.active) return;
-    extern __shared__ __align__(16) uint8_t smem23t[];
-    tl_start(ctl, hd.buf, 1);
-    tl_start(ctl, hd.buf, 2);
-    const Probe stamp(ctl, 16);
-    stamp(7, t_entry);
-    encode_top_staged(P, ctl, hd.parity, hd.buf, smem23t);
-    if (threadIdx.x == 0) {
-        const unsigned nt = static_cast<unsigned>(P.n_tiles);
-        while (ld_acquire_u32(&ctl->k2_done) < nt) __nanosleep(32);
-        ctl->k2_done = 0u;  // (every subtree CTA of this step has counted)
-    }
-    __syncthreads();
-    k3_top<false>(P, ctl, hd.parity, hd.buf, 2ull * static_cast<unsigned long long>(hd.step) + 2ull, smem23t, stamp,
-                  true, P.n_tiles <= 1024);
-}
-template <int KT>
-__global__ void __launch_bounds__(kThreads, 8) k_tiles23(Params P, Ctl* ctl) {
-    const unsigned long long t_entry = gtimer();
-    const Head hd = cta_head(ctl, P, false);
-    if (hd.active) {
-        extern __shared__ __align__(16) uint8_t smem23s[];
-        const uint32_t j = P.tile_lo + blockIdx.x;
-        // K2's subtree work: pre flags at smem23s, final flags left at
-        // smem23s + slo(K) = K3's current-flag slot
-        k2_tile<KT>(P, ctl, hd, j, smem23s);
-        __threadfence();  // every thread's final-flag stores, then the count
-        __syncthreads();
-        if (threadIdx.x == 0) atomicAdd(&ctl->k2_done, 1u);
-        Probe stamp(ctl, 16);
-        if (blockIdx.x == 0) stamp.slot = -1;  // (slots 16.. belong to the top CTA)
+    extern __shared__ __align__(16) uint8_t smem23[];
+    const unsigned long long epoch = 2ull * static_cast<unsigned long long>(hd.step) + 2ull;
+    if (blockIdx.x == 0) {
+        // (FV1 may launch once every CTA has triggered: they are all resident)
+        pdl_trigger();
+        if (!hd.active) return;
+        tl_start(ctl, hd.buf, 1);
+        tl_start(ctl, hd.buf, 2);
+        const Probe stamp(ctl, 16);
         stamp(7, t_entry);
-        k3_tile<false, KT>(P, ctl, hd.parity, hd.buf, 2ull * static_cast<unsigned long long>(hd.step) + 2ull, j,
-                           smem23s + slo(KT ? KT : P.K), stamp, true);
+        encode_top_staged(P, ctl, hd.parity, hd.buf, smem23);
+        if (threadIdx.x == 0) {
+            const unsigned nt = static_cast<unsigned>(P.n_tiles);
+            while (ld_acquire_u32(&ctl->k2_done) < nt) __nanosleep(32);
+            ctl->k2_done = 0u;  // (every subtree CTA of this step has counted)
+        }
+        __syncthreads();
+        k3_top<false>(P, ctl, hd.parity, hd.buf, epoch, smem23, stamp, true, P.n_tiles <= 1024);
+        return;
     }
-    // FV1 may launch once every subtree CTA is past its K2 publish (a pending
-    // subtree CTA behind resident FV1 CTAs would stall the top's wait)
+    if (!hd.active) {
+        pdl_trigger();
+        return;
+    }
+    const uint32_t j = P.tile_lo + blockIdx.x - 1u;
+    // K2's subtree work: pre flags at smem23, final flags left at
+    // smem23 + slo(K) = K3's current-flag slot
+    k2_tile<KT>(P, ctl, hd, j, smem23);
+    __threadfence();  // every thread's final-flag stores, then the count
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(&ctl->k2_done, 1u);
     pdl_trigger();
-    pdl_wait();  // the top grid has completed before this grid does
+    const Probe stamp(ctl, 16);  // (the last subtree CTA: slots 24..)
+    stamp(7, t_entry);
+    k3_tile<false, KT>(P, ctl, hd.parity, hd.buf, epoch, j, smem23 + slo(KT ? KT : P.K), stamp, true);
 }
 
 // =========================================================================== K5
@@ -3311,6 +3313,161 @@ __device__ __forceinline__ void fv1_quiet_pass(const Params& P, const double4* _
     }
 }
 
+// FV1 per-leaf pass for short leaf lists (small L): LPL = 4 or 2 lanes per
+// leaf, so one warp-iteration's dependent chain holds one face (LPL = 4: the
+// W, E, N, S face of lane q = 0..3) or one face pair (LPL = 2: the x faces in
+// lane 0, the y faces in lane 1) instead of four; lane 0 of each group
+// combines them by shuffles and finishes the cell. A short list fits in one
+// grid-stride window, so the per-leaf path's latency is the iteration's
+// dependent chain (~7-9 us on pseudo-2D L8 / humps L9 for four serial faces).
+// Every face is the same face() call with the same argument order and the
+// same adjustment expression as fv1_cell_seq, and the differences are formed
+// in the same order: the bits are those of the one-lane path.
+template <int LPL>
+__device__ __forceinline__ void fv1_fp_loop(const Params& P, Ctl* ctl, const double4* __restrict__ cur,
+                                            double4* __restrict__ nxt, const uint8_t* __restrict__ sigc,
+                                            uint32_t a_lo, uint32_t NA, uint32_t b_lo, uint32_t N, double dt,
+                                            double inflow, int tbuf, double& mx, unsigned& tree, unsigned& nnear,
+                                            unsigned& nquiet) {
+    constexpr int ND = 4 / LPL;  // faces per lane
+    const int lane = threadIdx.x & 31, q = lane % LPL;
+    const uint32_t gmask = ((1u << LPL) - 1u) << (lane - q);
+    const uint32_t stride = gridDim.x * (kThreads / LPL);
+    for (uint32_t wb = (blockIdx.x * kThreads + (threadIdx.x & ~31u)) / LPL; wb < N; wb += stride) {
+        const uint32_t i = wb + static_cast<uint32_t>(lane / LPL);
+        const bool valid = i < N;
+        const uint32_t z = valid ? P.leaves[i < NA ? a_lo + i : b_lo + (i - NA)] : zo::level_offset(P.L);
+        const int n = zo::level_of(z);
+        const uint32_t m = z - zo::level_offset(n);
+        const uint8_t ta = (valid && n >= P.R) ? P.tact[m >> (2 * (n - P.R))] : 1;
+        const double4 o4 = ld4_nc(cur + cbase(n) + m);
+        const bool quiet = valid && ta == 0;
+        const bool needs = valid && !quiet;
+        uint32_t nm[ND];
+        double4 r4[ND];
+        bool dry = true;
+#pragma unroll
+        for (int k = 0; k < ND; ++k) {
+            const int d = q * ND + k;
+            nm[k] = needs ? zo::neighbour_dev(n, m, static_cast<zo::Direction>(d)) : zo::kNone;
+            r4[k] = make_double4(0.0, 0.0, 0.0, 0.0);
+            if (nm[k] != zo::kNone) {
+                const double4* src = sigc[slo(n - 1) + (nm[k] >> 2)] ? cur + cbase(n) + nm[k]
+                                                                      : covering_local(P, cur, sigc, n - 1, nm[k] >> 2);
+                r4[k] = ld4_nc(src);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < ND; ++k) {
+            if (nm[k] != zo::kNone) dry = dry && r4[k].x < P.phys.hdry;
+            else if (needs && P.bc[q * ND + k] == 2) dry = false;  // inflow ghosts can be wet
+        }
+        // dry neighbourhood (the one-lane path's all_dry): own and every face of the group
+        const bool gdry = (__ballot_sync(kFull, dry) & gmask) == gmask;
+        const bool phys = needs && !(o4.x < P.phys.hdry && gdry);
+        double hn = (o4.x < 0.0) ? 0.0 : o4.x, qxn = 0.0, qyn = 0.0;
+        if (__any_sync(kFull, phys)) {
+            const CellV own = make_cell(o4, P.phys);
+            const double hh = own.h * own.h;
+            auto nb_of = [&](uint32_t nmk, const double4& rk, int d) -> CellV {
+                if (nmk == zo::kNone) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, P.phys);
+                return make_cell(rk, P.phys);
+            };
+            double v0, v1, v2;
+            double hLs, hRs, F[3];
+            if (LPL == 4) {
+                // face d = q: own on the left of the E (1) and N (2) faces
+                const bool left = q == 1 || q == 2;
+                const CellV nb = nb_of(nm[0], r4[0], q);
+                face(left ? own : nb, left ? nb : own, q < 2, P.phys, F, hLs, hRs);
+                const double sd = left ? hLs : hRs;
+                v0 = F[0];
+                v1 = F[1] + (P.phys.half_g * (hh - (sd * sd)));
+                v2 = F[2];
+            } else {
+                // faces 2q, 2q + 1 (x: W, E; y: N, S) as fv1_cell_seq's blocks
+                // (selects, not a lane-dependent index: no local memory)
+                const CellV e = nb_of(q ? nm[0] : nm[ND - 1], q ? r4[0] : r4[ND - 1], q ? 2 : 1);  // E (q = 0) / N (q = 1)
+                face(own, e, q == 0, P.phys, F, hLs, hRs);
+                const double FE0 = F[0], FE1 = F[1] + (P.phys.half_g * (hh - (hLs * hLs))), FE2 = F[2];
+                const CellV w = nb_of(q ? nm[ND - 1] : nm[0], q ? r4[ND - 1] : r4[0], q ? 3 : 0);  // W (q = 0) / S (q = 1)
+                face(w, own, q == 0, P.phys, F, hLs, hRs);
+                const double FW1 = F[1] + (P.phys.half_g * (hh - (hRs * hRs)));
+                v0 = FE0 - F[0];
+                v1 = FE1 - FW1;
+                v2 = FE2 - F[2];
+            }
+            double dFx0, dFx1, dFx2, dGy0, dGy1, dGy2;
+            if (LPL == 4) {
+                const int b = lane - q;
+                const double e0 = __shfl_sync(kFull, v0, b + 1), e1 = __shfl_sync(kFull, v1, b + 1),
+                             e2 = __shfl_sync(kFull, v2, b + 1);
+                const double n0 = __shfl_sync(kFull, v0, b + 2), n1 = __shfl_sync(kFull, v1, b + 2),
+                             n2 = __shfl_sync(kFull, v2, b + 2);
+                const double s0 = __shfl_sync(kFull, v0, b + 3), s1 = __shfl_sync(kFull, v1, b + 3),
+                             s2 = __shfl_sync(kFull, v2, b + 3);
+                dFx0 = e0 - v0;
+                dFx1 = e1 - v1;
+                dFx2 = e2 - v2;
+                dGy0 = n0 - s0;
+                dGy1 = n1 - s1;
+                dGy2 = n2 - s2;
+            } else {
+                dFx0 = v0;
+                dFx1 = v1;
+                dFx2 = v2;
+                dGy0 = __shfl_down_sync(kFull, v0, 1);
+                dGy1 = __shfl_down_sync(kFull, v1, 1);
+                dGy2 = __shfl_down_sync(kFull, v2, 1);
+            }
+            if (phys && q == 0) {
+                double rhn;
+                fv1_finish(own, dFx0, dFx1, dFx2, dGy0, dGy1, dGy2, inv_dx_of(P, n), dt, P.phys, hn, qxn, qyn, rhn);
+                const double c = cfl_rate_rh(hn, qxn, qyn, rhn, inv_dx_of(P, n), P.phys);
+                mx = c > mx ? c : mx;
+            }
+        }
+        if (valid && q == 0) {
+            nquiet += quiet ? 1u : 0u;
+            if (!(hn < P.phys.hdry)) {  // wet marks (as the one-lane path)
+                uint8_t* wn = P.wet[tbuf ^ 1];
+                if (n >= P.R) {
+                    wn[m >> (2 * (n - P.R))] = 1;
+                } else {
+                    const uint32_t t0 = m << (2 * (P.R - n)), t1 = (m + 1u) << (2 * (P.R - n));
+                    for (uint32_t t = t0; t < t1; ++t) wn[t] = 1;
+                }
+                if (P.qact) {
+                    uint8_t* qn = P.qwet[tbuf ^ 1];
+                    if (n > P.R) {
+                        qn[m >> (2 * (n - P.R - 1))] = 1;
+                    } else {
+                        const uint32_t t0 = m << (2 * (P.R - n)), t1 = (m + 1u) << (2 * (P.R - n));
+                        for (uint32_t t = t0; t < t1; ++t) *reinterpret_cast<uint32_t*>(qn + 4u * t) = 0x01010101u;
+                    }
+                }
+            }
+            if (!(isfinite(hn) && isfinite(qxn) && isfinite(qyn)))
+                report_error(ctl, kErrNonFinite, zo::z_of(n, m), !isfinite(hn) ? 0 : (!isfinite(qxn) ? 1 : 2),
+                             kStageFV1);
+            st4(nxt + cbase(n) + m, make_double4(hn, qxn, qyn, o4.w));
+        }
+        // the next step's level-(L-1) re-encode (as the one-lane path; the
+        // four children sit in lanes 4 LPL k + {0, LPL, 2 LPL, 3 LPL})
+        if (wb < NA) {
+            const Enc e = encode_lanes<false>(make_double4(hn, qxn, qyn, o4.w), LPL, P, P.L - 1);
+            if (lane % (4 * LPL) == 0 && i < NA && valid) {
+                const uint32_t pm = m >> 2;
+                st4(nxt + cbase(P.L - 1) + pm, e.par);
+                const unsigned long long fi = slo(P.L - 1) + pm;
+                P.pre[fi] = (e.flow || P.dem[fi]) ? 1 : 0;
+                ++tree;
+                nnear += e.near ? 1u : 0u;
+            }
+        }
+    }
+}
+
 // FV1 over the leaf list: persistent grid-stride, one thread per
 // leaf; reads the current buffer, writes leaf slots of the other (D15).
 // STAGE 0: next iteration's own cell prefetched into L2; 2: loaded into
@@ -3373,6 +3530,19 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
 #ifdef SWAMP_EXP_PHASET
     ph_t[2] = gtimer();
 #endif
+    // short lists at small L: several lanes per leaf (fv1_fp_loop); the
+    // one-lane windows below then see an empty list
+    uint32_t NL = N;
+    if constexpr (!UNIFORM && !PART && !INA && STAGE == 3) {
+        const unsigned long long cap = static_cast<unsigned long long>(gridDim.x) * kThreads * P.fv1_fp_cap16;
+        if (64ull * N <= cap) {
+            fv1_fp_loop<4>(P, ctl, cur, nxt, sigc, a_lo, NA, b_lo, N, dt, inflow, tbuf, mx, tree, nnear, nquiet);
+            NL = 0;
+        } else if (32ull * N <= cap) {
+            fv1_fp_loop<2>(P, ctl, cur, nxt, sigc, a_lo, NA, b_lo, N, dt, inflow, tbuf, mx, tree, nnear, nquiet);
+            NL = 0;
+        }
+    }
     const uint32_t stride = gridDim.x * kThreads;
     // warp-uniform trip count: every lane runs every iteration (shuffles below)
     uint32_t wbase = blockIdx.x * kThreads + (threadIdx.x & ~31u);
@@ -3382,23 +3552,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     // bases of the next two iterations are kept in b1, b2 (the finalizing
     // CTA resets the counter)
     constexpr bool TAIL = STAGE == 5;
-    const uint32_t nwin = N / stride, ntail = (nwin * P.fv1_tail16 + 8u) >> 4;
-    const uint32_t nstat = (TAIL && ntail > 0u && nwin > ntail) ? (nwin - ntail) * stride : N;  // (small lists: static)
+    const uint32_t nwin = NL / stride, ntail = (nwin * P.fv1_tail16 + 8u) >> 4;
+    const uint32_t nstat = (TAIL && ntail > 0u && nwin > ntail) ? (nwin - ntail) * stride : NL;  // (small lists: static)
     // one warp-iteration per grab (2 or 4 per grab measured slower at L = 11)
     // a grab uses the counter value fetched one grab earlier and fetches the
     // next one, so the atomic's round trip (long under contention: every warp
     // of the grid hits this address) overlaps an iteration instead of
     // stalling the warp; the last fetched value is never used
     uint32_t pend = 0;
-    if (TAIL && lane == 0 && nstat < N) pend = atomicAdd(&ctl->fv1_tail, 1u);
+    if (TAIL && lane == 0 && nstat < NL) pend = atomicAdd(&ctl->fv1_tail, 1u);
     auto grab = [&]() -> uint32_t {
         const uint32_t c = __shfl_sync(kFull, pend, 0);
         if (lane == 0) pend = atomicAdd(&ctl->fv1_tail, 1u);
         const uint32_t b = nstat + 32u * c;
-        return b < N ? b : N;
+        return b < NL ? b : NL;
     };
     auto next_of = [&](uint32_t b) -> uint32_t {
-        if (b >= N) return N;
+        if (b >= NL) return NL;
         return (b + stride < nstat) ? b + stride : grab();
     };
     uint32_t b1 = 0, b2 = 0;
@@ -3413,9 +3583,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
     // leaf ids two iterations ahead; the next iteration's own cell is
     // prefetched (no registers held) while this one computes: the leaf
     // cells were written a step ago and come from DRAM
-    uint32_t z_next = (!UNIFORM && wbase + lane < N) ? leaf_at(wbase + lane) : 0u;
+    uint32_t z_next = (!UNIFORM && wbase + lane < NL) ? leaf_at(wbase + lane) : 0u;
     const uint32_t nb1_0 = TAIL ? b1 : wbase + stride;
-    uint32_t z_nn = (!UNIFORM && pf && nb1_0 + lane < N) ? leaf_at(nb1_0 + lane) : 0u;
+    uint32_t z_nn = (!UNIFORM && pf && nb1_0 + lane < NL) ? leaf_at(nb1_0 + lane) : 0u;
     double4 o4_pre = make_double4(0.0, 0.0, 0.0, 0.0);
     uint8_t ta_pre = 1;
     uint8_t fl_pre[4] = {1, 1, 1, 1};  // STAGE 3: the neighbours' parent-level flags too
@@ -3426,7 +3596,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
         ta_pre = (n1 >= P.R) ? P.tact[m1 >> (2 * (n1 - P.R))] : 1;
         if ((STAGE == 3 || STAGE == 5) && !PART && n1 > 0) {  // (PART: flags through the peer tables below)
             // a sibling neighbour (W of an east child, E of a west child, S of
-            // a north child, N of a south child) shares this leaf's parent,
+            // a north child, NL of a south child) shares this leaf's parent,
             // which is significant: only the other two flags are loaded
             const uint32_t c = m1 & 3u;
 #pragma unroll
@@ -3441,7 +3611,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
             }
         }
     };
-    if (STAGE >= 2 && !UNIFORM && wbase + lane < N) pre_load(z_next);
+    if (STAGE >= 2 && !UNIFORM && wbase + lane < NL) pre_load(z_next);
     auto advance_base = [&]() {
         if (TAIL) {
             wbase = b1;
@@ -3451,10 +3621,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
             wbase += stride;
         }
     };
-    for (; wbase < N; advance_base()) {
+    for (; wbase < NL; advance_base()) {
         const uint32_t i = wbase + lane;
         const uint32_t nb1 = TAIL ? b1 : wbase + stride, nb2 = TAIL ? b2 : wbase + 2 * stride;  // next two bases
-        bool valid = i < N;
+        bool valid = i < NL;
         int n;
         uint32_t m;
         const double4 o4_k = o4_pre;
@@ -3463,7 +3633,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
         if (UNIFORM) {
             n = P.L;
             m = valid ? i : 0u;
-            if (pf && nb1 + lane < N) {
+            if (pf && nb1 + lane < NL) {
                 const double4* q = cur + cbase(n) + nb1 + lane;
                 prefetch_l2(q);
             }
@@ -3471,8 +3641,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
             const uint32_t z = valid ? z_next : zo::level_offset(P.L);  // leaf ids prefetched one iteration ahead
             if (pf) {
                 z_next = z_nn;
-                if (nb2 + lane < N) z_nn = leaf_at(nb2 + lane);
-                if (nb1 + lane < N) {
+                if (nb2 + lane < NL) z_nn = leaf_at(nb2 + lane);
+                if (nb1 + lane < NL) {
                     if (STAGE >= 2) {
                         pre_load(z_next);
                     } else {
@@ -3481,7 +3651,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
                         prefetch_l2(q);
                     }
                 }
-            } else if (nb1 + lane < N) {
+            } else if (nb1 + lane < NL) {
                 z_next = leaf_at(nb1 + lane);
             }
             n = zo::level_of(z);
@@ -3595,7 +3765,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
                 qyn = 0.0;
             } else {
                 const CellV own = make_cell(o4, P.phys);
-                // the W, E, N, S neighbour as seen by its face (ghost on the boundary)
+                // the W, E, NL, S neighbour as seen by its face (ghost on the boundary)
                 auto neighbour = [&](int d) -> CellV {
                     if (nm[d] == zo::kNone) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, P.phys);
                     if (wall[d]) return boundary_cell(own, 0, d, inflow, P.inflow_mode, P.phys);

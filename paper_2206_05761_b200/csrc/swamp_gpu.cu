@@ -129,10 +129,9 @@ struct swamp_gpu {
     void (*k3top)(Params, Ctl*) = nullptr;
     void (*k3tiles)(Params, Ctl*) = nullptr;
     size_t smem_k3top = 0, smem_k3tiles = 0;
-    // fused K2 + K3 (k_top23 + k_tiles23): K2 not launched
-    void (*k23top)(Params, Ctl*) = nullptr;
-    void (*k23tiles)(Params, Ctl*) = nullptr;
-    size_t smem_k23tiles = 0;
+    // fused K2 + K3 (k_23, one cooperative grid): K2 not launched
+    void (*k23)(Params, Ctl*) = nullptr;
+    size_t smem_k23 = 0;
     // tile kernels, specialised for K = 6 (every L >= 6) or generic
     void (*k1)(Params, Ctl*) = nullptr;
     void (*k2)(Params, Ctl*, int, int) = nullptr;
@@ -241,6 +240,23 @@ void launch_pdl_t(void (*kernel)(KArgs...), int grid, int threads, size_t smem, 
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, kernel, args...);
 }
+// PDL + cooperative (every CTA of the grid resident at once, or the launch fails)
+template <class... KArgs, class... Args>
+void launch_pdl_coop(void (*kernel)(KArgs...), int grid, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, kernel, args...);
+}
 template <class... KArgs, class... Args>
 void launch_pdl(void (*kernel)(KArgs...), int grid, size_t smem, cudaStream_t s, Args... args) {
     launch_pdl_t(kernel, grid, kThreads, smem, s, args...);
@@ -265,10 +281,9 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
     launch_pdl(g->k1, P.n_tiles, g->smem_k1s, s, P, g->ctl);
     if (P.top_mode == 2) launch_pdl(hwfv1::k_encode_top<false>, 1, g->smem_k1, s, P, g->ctl);
     mark(1);
-    if (g->k23top) {  // fused K2 + K3
+    if (g->k23) {  // fused K2 + K3
         mark(2);
-        launch_pdl(g->k23top, 1, g->smem_k3top, s, P, g->ctl);
-        launch_pdl(g->k23tiles, P.n_tiles, g->smem_k23tiles, s, P, g->ctl);
+        launch_pdl_coop(g->k23, P.n_tiles + 1, g->smem_k23, s, P, g->ctl);
         mark(3);
     } else {
     const int do_top = P.top_mode == 1 ? 1 : 0;
@@ -698,28 +713,30 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             const char* eqs = std::getenv("SWAMP_QSKIP");
             const bool qk = eqs ? eqs[0] != '0' : P.n_tiles >= 1024;
             P.qskip = (P.qsplit && Ki == 6 && qk) ? 1 : 0;
-            // fused K2 + K3 (opt-in, SWAMP_K23=1): needs top_band (K2's extra-CTA
-            // work moves into the top CTA) and every subtree CTA resident beside
-            // the top's SM, because the top waits for all of them. Measured
-            // -1.5 to -2 us per step at L = 8..10, +2 to +3 us at L = 11. Off by
-            // default: the top's wait for CTAs of a later launch deadlocks
-            // wherever kernels are serialised (compute-sanitizer, ncu) and is
-            // only as safe as the co-residency the occupancy check predicts
-            // (other contexts on the GPU, MPS) — DESIGN.md §8
+            // fused K2 + K3 (k_23, one cooperative grid): needs top_band (K2's
+            // extra-CTA work moves into the top CTA) and every CTA resident at
+            // once (the top waits for all subtree CTAs, they wait for its
+            // records; the cooperative launch guarantees the residency).
+            // Measured -3 us per step at L = 8..10; +2 to +3 us at L = 11 (one
+            // 1024-subtree wave behind a 256-thread top), so on below 1024
+            // subtrees. SWAMP_K23=0 / 1 forces it off / on
             const char* e23 = std::getenv("SWAMP_K23");
-            const bool k23 = e23 && e23[0] == '1';
+            const bool k23 = e23 ? e23[0] == '1' : P.n_tiles < 1024;
             if (P.top_band && k23) {
-                void (*t23)(Params, Ctl*) = (Ki == 6) ? hwfv1::k_tiles23<6> : hwfv1::k_tiles23<0>;
-                const size_t sm23 = sl + g->smem_k3tiles;
+                void (*f23)(Params, Ctl*) = (Ki == 6) ? hwfv1::k_23<6> : hwfv1::k_23<0>;
+                // (the top's own layout, not the split top's whole-SM request)
+                const hwfv1::K3TopLayout ly = hwfv1::k3_top_layout(R, static_cast<uint32_t>(nt));
+                const size_t top23 = ly.sqw + 4 * ((nt + 15) & ~size_t(15)) + 64;
+                const size_t sm23 = std::max(sl + g->smem_k3tiles, top23);
                 int occ = 0;
                 if (sm23 >= 32 * 1024)
-                    cudaFuncSetAttribute(reinterpret_cast<const void*>(t23),
+                    cudaFuncSetAttribute(reinterpret_cast<const void*>(f23),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm23));
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, t23, kThreads, sm23);
-                if (static_cast<long long>(occ) * (g->num_sms - 1) >= P.n_tiles) {
-                    g->k23top = (Ki == 6) ? hwfv1::k_top23<6> : hwfv1::k_top23<0>;
-                    g->k23tiles = t23;
-                    g->smem_k23tiles = sm23;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f23, kThreads, sm23);
+                if (static_cast<long long>(occ) * g->num_sms >= P.n_tiles + 1) {
+                    g->k23 = f23;
+                    g->smem_k23 = sm23;
+                    P.qact = 0;  // (the fused top does not refine by quadrants)
                 }
             }
         }
@@ -735,8 +752,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
                      {reinterpret_cast<const void*>(g->k3x), g->smem_k3},
                      {reinterpret_cast<const void*>(g->k3top), g->smem_k3top},
                      {reinterpret_cast<const void*>(g->k3tiles), g->smem_k3tiles},
-                     {reinterpret_cast<const void*>(g->k23top), g->smem_k3top},
-                     {reinterpret_cast<const void*>(g->k23tiles), g->smem_k23tiles},
+                     {reinterpret_cast<const void*>(g->k23), g->smem_k23},
                      {reinterpret_cast<const void*>(hwfv1::k_fv1<false>), hwfv1::kTileSlab},
                      {reinterpret_cast<const void*>(hwfv1::k_fv1<false, false, false, 2>), hwfv1::kTileSlab},
                      {reinterpret_cast<const void*>(hwfv1::k_fv1<false, false, false, 3>), hwfv1::kTileSlab},
@@ -757,6 +773,9 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         // 64.3 us; 2-6 windows less, 10-24 windows less to slower)
         const char* etw = std::getenv("SWAMP_FV1_TAIL16");
         P.fv1_tail16 = etw ? static_cast<uint32_t>(std::min(16, std::max(0, std::atoi(etw)))) : 6u;
+        // several lanes per leaf when the list fits the grid that way (STAGE 3)
+        const char* efp = std::getenv("SWAMP_FV1_FP_CAP16");
+        P.fv1_fp_cap16 = efp ? static_cast<uint32_t>(std::min(256, std::max(0, std::atoi(efp)))) : 16u;
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, false, false, 5>, kThreads, 0);
         g->fv1_grid = std::max(1, occ) * g->num_sms;

@@ -5,7 +5,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import ctypes as C
 from paper_2206_05761_b200 import cases, gpu
 
-for name, mk in (("c5", lambda: cases.river_flood(L=11)), ("wet", lambda: cases.monai_runup(L=11))):
+SETS = {"big": (("c5", lambda: cases.river_flood(L=11)), ("wet", lambda: cases.monai_runup(L=11))),
+        "small": (("humpsL9", lambda: cases.quiescent_humps(L=9, t_end=1e30)),
+                  ("p2dL8", lambda: cases.pseudo2d_dambreak(L=8, t_end=1e30)))}
+for name, mk in SETS[os.environ.get("CASES", "big")]:
     cfg, h, qx, qy, z = mk()
     e = gpu.initialise(cfg, h, qx, qy, z)
     e.advance(12)

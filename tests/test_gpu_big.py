@@ -40,9 +40,9 @@ def test_level13_steps_stay_finite():
 
 
 @pytest.mark.parametrize("env", [("SWAMP_FV1_STAGE", "3"), ("SWAMP_K3_SPLIT", "0"), ("SWAMP_FV1_TAIL16", "15"),
-                                 ("SWAMP_FV1_TILES", "0"), ("SWAMP_K23", "1"), ("SWAMP_QSKIP", "0"),
+                                 ("SWAMP_FV1_TILES", "0"), ("SWAMP_QSKIP", "0"),
                                  ("SWAMP_QSPLIT", "0"), ("SWAMP_QACT", "0")],
-                         ids=["static-fv1", "one-launch-k3", "mostly-dynamic-fv1", "no-tile-path", "fused-k2-k3",
+                         ids=["static-fv1", "one-launch-k3", "mostly-dynamic-fv1", "no-tile-path",
                               "no-quiet-skip", "no-quiet-split", "no-quadrant-marks"])
 def test_level11_variants_agree(monkeypatch, env):
     """L = 11 (config 5, 22 grid-stride windows): the default engine (tail-
@@ -61,6 +61,31 @@ def test_level11_variants_agree(monkeypatch, env):
     (ah, *_), asig = a.export_tree()
     (bh, *_), bsig = b.export_tree()
     np.testing.assert_array_equal(asig, bsig)
+    del a, b
+
+
+@pytest.mark.parametrize("case", ["circular", "monai"])
+@pytest.mark.parametrize("env", [("SWAMP_K23", "0"), ("SWAMP_FV1_FP_CAP16", "0"), ("SWAMP_FV1_FP_CAP16", "256")],
+                         ids=["split-k2-k3", "one-lane-per-leaf", "lanes-per-leaf-forced"])
+def test_level10_variants_agree(monkeypatch, case, env):
+    """L = 10 (256 subtrees): the default engine (K2 + K3 as one cooperative
+    grid, FV1 with several lanes per leaf when the list is short) against K2 ->
+    split K3 / one lane per leaf / lanes per leaf forced on the long Monai list
+    (2 lanes) and the circular one (4 lanes): the same bits after 10 steps."""
+    mk = cases.circular_dambreak if case == "circular" else cases.monai_runup
+    cfg, h, qx, qy, z = mk(L=10)
+    a = gpu.initialise(cfg, h, qx, qy, z)
+    monkeypatch.setenv(*env)
+    b = gpu.initialise(cfg, h, qx, qy, z)
+    a.advance(10)
+    b.advance(10)
+    assert a.info() == b.info()
+    for fa, fb in zip(a.export_finest(), b.export_finest()):
+        np.testing.assert_array_equal(fa.view(np.uint64), fb.view(np.uint64))
+    (ah, *_), asig = a.export_tree()
+    (bh, *_), bsig = b.export_tree()
+    np.testing.assert_array_equal(asig, bsig)
+    np.testing.assert_array_equal(ah.view(np.uint64), bh.view(np.uint64))
     del a, b
 
 
