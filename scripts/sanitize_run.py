@@ -54,10 +54,11 @@ def main(L):
         p.close()
     # the L = 11 defaults forced on at this size: FV1's tile phase and the
     # stable-quiet skip (K2's change test, K3's skip state, K1 / FV1 skips).
-    # (The opt-in fused K2 + K3 is not run: its top waits for CTAs of a later
-    # launch, which a sanitizer serialises.)
+    # Both K2 -> K3 paths: the cooperative fused grid (k_23, the default
+    # below 1024 subtrees) and the split K3.
     os.environ.update({"SWAMP_FV1_TILES": "1", "SWAMP_QSKIP": "1"})
-    for k23 in ("0",):
+    for k23 in ("0", "1"):
+        os.environ["SWAMP_K23"] = k23
         for name, make in runs[:2]:
             cfg, h, qx, qy, z = make()
             e = gpu.initialise(cfg, h, qx, qy, z)
@@ -76,7 +77,7 @@ def main(L):
     print("quiet skip", e.info(), sk, flush=True)
     assert sk["fv1_skipped_leaves"] > 0 and sk["k1_skipped_cells"] > 0, sk
     e.close()
-    for k in ("SWAMP_FV1_TILES", "SWAMP_QSKIP"):
+    for k in ("SWAMP_FV1_TILES", "SWAMP_QSKIP", "SWAMP_K23"):
         os.environ.pop(k, None)
     gpu.trim_cache()
 
