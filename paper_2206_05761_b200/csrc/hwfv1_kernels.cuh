@@ -1793,7 +1793,8 @@ __device__ __forceinline__ uint8_t activity_q(const Params& P, uint32_t t, const
 // shared-memory offsets of k3_top's staged arrays (also used by the split
 // top's pre-wait staging)
 struct K3TopLayout {
-    uint32_t tv, swet, qst, sqw;  // previous top flags, wet marks, quiet-skip state, quadrant wet marks
+    uint32_t tv, swet, qst, sqw, sqn;  // previous top flags, wet marks, quiet-skip state, quadrant wet marks,
+                                       // skipped subtrees' cached FV1 near counts
 };
 __host__ __device__ __forceinline__ K3TopLayout k3_top_layout(int R, uint32_t nt) {
     const uint32_t fb = slo(R), ftop = (fb + nt + 15u) & ~15u, pnt = (nt + 15u) & ~15u;
@@ -1804,7 +1805,7 @@ __host__ __device__ __forceinline__ K3TopLayout k3_top_layout(int R, uint32_t nt
     const uint32_t nr1 = R >= 1 ? (1u << (2 * (R - 1))) : 1u;
     const uint32_t sdep = sres + 4u * 4u * nt + 4u * nr1;
     const uint32_t stl = sdep + ((nr1 + 15u) & ~15u);
-    return {tv, swet, stl + 3u * pnt, stl + 4u * pnt};
+    return {tv, swet, stl + 3u * pnt, stl + 4u * pnt, stl + 8u * pnt};
 }
 // the split top's staging that does not depend on K1 / K2 (previous top flags,
 // the previous FV1's wet marks, the quiet-skip state), issued before the PDL
@@ -1817,6 +1818,7 @@ __device__ __forceinline__ void k3_top_prestage(const Params& P, int p, int tbuf
     stage16<NT>(sm + ly.swet, P.wet[tbuf], nt);
     if (P.qskip) stage16<NT>(sm + ly.qst, P.qstate, nt);
     if (P.qact) stage16<NT>(sm + ly.sqw, P.qwet[tbuf], 4u * nt);
+    if (P.qskip) stage16<NT>(sm + ly.sqn, reinterpret_cast<const uint8_t*>(P.qnfv), 4u * nt);
 }
 template <bool EXPORT, int NT = kThreads>
 __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long long epoch, uint8_t* sm,
@@ -1905,7 +1907,10 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     for (uint32_t q = threadIdx.x; q < nt; q += NT) cbf[q] = 0;
     cp_async_wait_all();
     __shared__ unsigned s_nwet;  // wet subtrees (R = 5 closure path), else ~0
-    if (threadIdx.x == 0) s_nwet = (!EXPORT && R == 5 && NT > 32) ? 0u : ~0u;
+    if (threadIdx.x == 0) {
+        s_nwet = (!EXPORT && R == 5 && NT > 32) ? 0u : ~0u;
+        s_ntile = 0u;  // (before the barrier below: the tile listing appends without one)
+    }
     if (threadIdx.x == 64 && nt == 1u) ts[fb] = r0;
     __syncthreads();
     stamp(0);
@@ -2079,16 +2084,16 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     // level-L cells are all leaves and whose neighbourhood holds a wet cell
     // (or touches an inflow edge) is updated as a 64 x 64 block; its leaves
     // leave list A (counted in n_leaves all the same) and it joins P.stile
+    bool dense = false;
     if (tiles) {
-        if (threadIdx.x == 0) s_ntile = 0u;
         // which fully refined subtrees take the tile path: when most subtrees
         // hold wet cells (a wet-dominated domain), every active one (it or a
         // face neighbour wet, or an inflow edge); otherwise only those inside
         // the wet region (it and all its face neighbours wet) — where the wet
         // cells are sparse the per-leaf path's per-cell dry shortcut is
         // cheaper than a strip's rows (measured: config 5 91 vs 104 us/step
-        // with every active subtree tiled; the Monai-like runup 139 vs 157)
-        bool dense;
+        // with every active subtree tiled; the Monai-like runup 139 vs 157).
+        // Decided per subtree in the counts pass below.
         if (s_nwet != ~0u) {  // (counted by warps 1.. during warp 0's closure)
             dense = 2u * s_nwet > nt;
         } else {
@@ -2096,7 +2101,15 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
             for (uint32_t t = a; t < b; ++t) nw += swet[t] ? 1u : 0u;
             dense = 2u * block_sum<NT>(nw, s_red) > nt;
         }
-        for (uint32_t t = a; t < b; ++t) {
+    }
+    // FV1 tile path (k_fv1 fv1_tile_strip): a reached subtree whose 4^K
+    // level-L cells are all leaves and whose neighbourhood holds a wet cell
+    // (or touches an inflow edge) is updated as a 64 x 64 block; its leaves
+    // leave list A (counted in n_leaves all the same) and it joins P.stile
+    // (appended warp-aggregated, any order: each strip job writes its own cells)
+    auto tile_of = [&](uint32_t t) {
+        bool tl = false;
+        if (tiles) {
             bool inner;
             if (dense) {
                 inner = swet[t] != 0;
@@ -2114,12 +2127,20 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
                     inner = inner && (nb == zo::kNone || swet[nb] != 0);
                 }
             }
-            const bool tl = inner && reach[t] && cnt[t] == (1u << (2 * P.K));
+            tl = inner && reach[t] && cnt[t] == (1u << (2 * P.K));
             stl[t] = tl ? 1 : 0;
-            if (tl) P.stile[atomicAdd(&s_ntile, 1u)] = t;  // (any order: each strip job writes its own cells)
+            const unsigned am = __activemask();
+            const unsigned bal = __ballot_sync(am, tl);
+            if (bal) {
+                const int lane = threadIdx.x & 31, lead = __ffs(am) - 1;
+                unsigned base = 0;
+                if (lane == lead) base = atomicAdd(&s_ntile, static_cast<unsigned>(__popc(bal)));
+                base = __shfl_sync(am, base, lead);
+                if (tl) P.stile[base + __popc(bal & ((1u << lane) - 1u))] = t;
+            }
         }
-        __syncthreads();
-    }
+        return tl;
+    };
     // quiet split: a reached subtree whose neighbourhood held no wet cell
     // (the dry-shortcut activity, computed again for P.tact below) and that
     // is not on the tile path lists its leaves after the active ones
@@ -2128,6 +2149,7 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     const uint8_t* qchg = sq + ((nt + 15u) & ~15u);  // (staged with the wet marks)
     const uint8_t* qst = qchg + ((nt + 15u) & ~15u);
     const uint8_t* sqw = qst + ((nt + 15u) & ~15u);  // quadrant wet marks (qact; staged before the wait)
+    const uint32_t* sqn = reinterpret_cast<const uint32_t*>(sqw + 4u * ((nt + 15u) & ~15u));  // (qskip, prestaged)
     const bool use_q = qs && P.qact && prestaged;
     auto counts = [&](uint32_t t, unsigned& ca, unsigned& cb) {
         const bool r = reach[t] != 0;
@@ -2138,7 +2160,8 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     // quiet (sq = 1), or stable quiet and skipped (sq = 2)
     unsigned la = 0, lb = 0, lqa = 0, lqb = 0, lsk = 0, lska = 0, lskn = 0;
     for (uint32_t t = a; t < b; ++t) {
-        const uint32_t qf = (qs && P.qskip) ? P.qnfv[t] : 0u;  // (issued first: a global load)
+        const uint32_t qf = (qs && P.qskip) ? (prestaged ? sqn[t] : P.qnfv[t]) : 0u;
+        tile_of(t);
         unsigned ca, cb;
         counts(t, ca, cb);
         uint8_t q = 0;
@@ -2178,6 +2201,9 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
             lb += cb;
         }
     }
+#ifdef SWAMP_EXP_K3X
+    if (threadIdx.x == 0 && stamp.slot == 16) ctl->dbg[32 + 1] = gtimer();
+#endif
     __shared__ unsigned long long s_red64[3 * (NT / 32)];
     unsigned long long tot64, qtot64 = 0, o64, q64 = 0, sk64 = 0;
     if (qs) {  // active / quiet / skipped counts in one scan
@@ -2191,6 +2217,9 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
         q64 = o3[1];
         qtot64 = t3[1];
         sk64 = t3[2];
+#ifdef SWAMP_EXP_K3X
+    if (threadIdx.x == 0 && stamp.slot == 16) ctl->dbg[32 + 2] = gtimer();
+#endif
     } else {
         o64 = block_exscan64<NT>((static_cast<unsigned long long>(la) << 32) | lb, s_red64, &tot64);
     }
