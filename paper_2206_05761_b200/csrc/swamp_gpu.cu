@@ -149,6 +149,9 @@ struct swamp_gpu {
     int rank_world = 0;
     std::vector<void*> ipc_opened;
     bool serial = false;  // group on one device: all partitions on parts[0]'s stream
+    bool concurrent = false;  // (serial group) phases run as concurrent per-partition branches
+    cudaEvent_t ev_fork = nullptr;
+    cudaEvent_t ev_join[hwfv1::kMaxParts] = {};
     void* scratch = nullptr;  // device scratch of export_finest (3 x 4^L doubles), lazily allocated
     double x0 = 0.0, y0 = 0.0;  // lower-left corner of the domain (gauge sampling)
     size_t scratch_bytes = 0;
@@ -173,6 +176,9 @@ struct swamp_gpu {
         if (scratch) cached_free(device, scratch, scratch_bytes);
         if (graph1) cudaGraphExecDestroy(graph1);
         if (graphS) cudaGraphExecDestroy(graphS);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        for (cudaEvent_t e : ev_join)
+            if (e) cudaEventDestroy(e);
         if (graphT) cudaGraphExecDestroy(graphT);
         if (graphR) cudaGraphExecDestroy(graphR);
         for (auto& e : ev)
@@ -260,6 +266,17 @@ void launch_pdl_coop(void (*kernel)(KArgs...), int grid, size_t smem, cudaStream
 template <class... KArgs, class... Args>
 void launch_pdl(void (*kernel)(KArgs...), int grid, size_t smem, cudaStream_t s, Args... args) {
     launch_pdl_t(kernel, grid, kThreads, smem, s, args...);
+}
+// plain stream-ordered launch (the kernels' griddepcontrol.wait is then a no-op)
+template <class... KArgs, class... Args>
+void launch_plain_t(void (*kernel)(KArgs...), int grid, int threads, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.numAttrs = 0;
+    cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 void launch_step_kernels(swamp_gpu* g, bool timed) {
@@ -877,32 +894,38 @@ void part_barrier(swamp_gpu* q, cudaStream_t s) { launch_pdl_t(hwfv1::k_part_bar
 // (every phase kernel and the barrier start with griddepcontrol.wait, so the
 // phases are chained with programmatic dependent launch: each launch overlaps
 // the tail of the kernel before it)
-bool part_step_phase(swamp_gpu* q, int k, cudaStream_t s) {
+bool part_step_phase(swamp_gpu* q, int k, cudaStream_t s, bool pdl = true) {
     const Params& P = q->P;
+    // (PDL between phases on one stream; the concurrent same-device group
+    // joins the partitions' streams between phases, so plain launches there)
+    auto launch = [&](auto kernel, int grid, int threads, size_t smem, auto... args) {
+        if (pdl) launch_pdl_t(kernel, grid, threads, smem, s, args...);
+        else launch_plain_t(kernel, grid, threads, smem, s, args...);
+    };
     switch (k) {
         case 0:
-            launch_pdl(q->k1, static_cast<int>(P.tiles_per_part), q->smem_k1s, s, P, q->ctl);
+            launch(q->k1, static_cast<int>(P.tiles_per_part), kThreads, q->smem_k1s, P, q->ctl);
             return true;
         case 1:
             if (P.top_mode != 2) return false;
-            launch_pdl(hwfv1::k_encode_top<false>, 1, q->smem_k1, s, P, q->ctl);
+            launch(hwfv1::k_encode_top<false>, 1, kThreads, q->smem_k1, P, q->ctl);
             return true;
         case 2: {
             const int do_top = P.top_mode == 1 ? 1 : 0;
-            launch_pdl(q->k2, static_cast<int>(P.tiles_per_part) + do_top, q->smem_k2, s, P, q->ctl, 0, do_top);
+            launch(q->k2, static_cast<int>(P.tiles_per_part) + do_top, kThreads, q->smem_k2, P, q->ctl, 0, do_top);
             return true;
         }
-        case 3: launch_pdl(q->k3, static_cast<int>(P.tiles_per_part) + 1, q->smem_k3, s, P, q->ctl, 0, 0ull); return true;
+        case 3: launch(q->k3, static_cast<int>(P.tiles_per_part) + 1, kThreads, q->smem_k3, P, q->ctl, 0, 0ull); return true;
         case 4:
-            if (P.has_ina) launch_pdl(hwfv1::k_fv1<false, true, true>, q->fv1_grid, 0, s, P, q->ctl);
+            if (P.has_ina) launch(hwfv1::k_fv1<false, true, true>, q->fv1_grid, kThreads, 0, P, q->ctl);
             else if (q->fv1_stage == 5)  // tail balancing (flags come from the peer tables: no STAGE 3 preloads)
-                launch_pdl(hwfv1::k_fv1<false, true, false, 5>, q->fv1_grid, 0, s, P, q->ctl);
+                launch(hwfv1::k_fv1<false, true, false, 5>, q->fv1_grid, kThreads, 0, P, q->ctl);
             else if (q->fv1_stage >= 2)  // own cells loaded an iteration ahead
-                launch_pdl(hwfv1::k_fv1<false, true, false, 2>, q->fv1_grid, 0, s, P, q->ctl);
+                launch(hwfv1::k_fv1<false, true, false, 2>, q->fv1_grid, kThreads, 0, P, q->ctl);
             else
-                launch_pdl(hwfv1::k_fv1<false, true>, q->fv1_grid, 0, s, P, q->ctl);
+                launch(hwfv1::k_fv1<false, true>, q->fv1_grid, kThreads, 0, P, q->ctl);
             return true;
-        default: launch_pdl_t(hwfv1::k_finalize, 1, 32, 0, s, P, q->ctl, 1); return true;
+        default: launch(hwfv1::k_finalize, 1, 32, 0, P, q->ctl, 1); return true;
     }
 }
 constexpr int kStepPhases = 6;
@@ -952,9 +975,29 @@ void part_enqueue_init(swamp_gpu* q) {
 // on one stream before phase k + 1 (stream order is the barrier; two streams
 // of one context may share a hardware queue, so spinning barriers could
 // serialise behind each other)
+// Concurrent form (grp->concurrent, the default): phase k of every partition
+// on its own stream, forked from and joined back into parts[0]'s stream
+// (event edges in the captured graph: the join is the phase barrier, no
+// spinning), so the partitions' kernels share the GPU as they would share a
+// node's GPUs; each partition's FV1 grid is the device's divided by G.
 void serial_enqueue_step(swamp_gpu* grp) {
-    for (int k = 0; k < kStepPhases; ++k)
-        for (swamp_gpu* q : grp->parts) part_step_phase(q, k, grp->parts[0]->stream);
+    cudaStream_t s0 = grp->parts[0]->stream;
+    if (!grp->concurrent) {
+        for (int k = 0; k < kStepPhases; ++k)
+            for (swamp_gpu* q : grp->parts) part_step_phase(q, k, s0);
+        return;
+    }
+    const size_t G = grp->parts.size();
+    for (int k = 0; k < kStepPhases; ++k) {
+        if (k == 1 && grp->parts[0]->P.top_mode != 2) continue;
+        cudaEventRecord(grp->ev_fork, s0);
+        for (size_t i = 1; i < G; ++i) cudaStreamWaitEvent(grp->parts[i]->stream, grp->ev_fork, 0);
+        for (size_t i = 0; i < G; ++i) part_step_phase(grp->parts[i], k, grp->parts[i]->stream, false);
+        for (size_t i = 1; i < G; ++i) {
+            cudaEventRecord(grp->ev_join[i], grp->parts[i]->stream);
+            cudaStreamWaitEvent(s0, grp->ev_join[i], 0);
+        }
+    }
 }
 void serial_enqueue_init(swamp_gpu* grp) {
     for (int k = 0; k < kInitPhases; ++k)
@@ -1102,6 +1145,16 @@ int create_group(const swamp_config* cfg, const double* h, const double* qx, con
     if ((st = group_sync(grp))) return fail(st);
     if (grp->serial) {
         cudaSetDevice(grp->parts[0]->device);
+        const char* ec = std::getenv("SWAMP_PART_CONCURRENT");
+        grp->concurrent = !(ec && ec[0] == '0');
+        if (grp->concurrent) {
+            bool ok = cudaEventCreateWithFlags(&grp->ev_fork, cudaEventDisableTiming) == cudaSuccess;
+            for (int g = 1; g < G; ++g)
+                ok = ok && cudaEventCreateWithFlags(&grp->ev_join[g], cudaEventDisableTiming) == cudaSuccess;
+            if (!ok) return fail(SWAMP_E_CUDA);
+            // the device's FV1 grid shared by the concurrent partitions
+            for (swamp_gpu* q : grp->parts) q->fv1_grid = std::max(q->num_sms, q->fv1_grid / G);
+        }
         if ((st = capture_step_graphs(grp, grp->parts[0]->stream, [&] { serial_enqueue_step(grp); }))) return fail(st);
     }
     *out = grp;
