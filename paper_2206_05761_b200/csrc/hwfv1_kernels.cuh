@@ -3502,8 +3502,11 @@ __device__ __forceinline__ void fv1_fp_loop(const Params& P, Ctl* ctl, const dou
 // STAGE 0: next iteration's own cell prefetched into L2; 2: loaded into
 // registers an iteration ahead with its subtree activity; 3: also the
 // neighbours' parent-level flags; 5: 3 + tail balancing.
+#ifndef SWAMP_FV1_MINB
+#define SWAMP_FV1_MINB 2  // resident CTAs per SM the register budget is sized for (3: DESIGN.md §8)
+#endif
 template <bool UNIFORM, bool PART = false, bool INA = false, int STAGE = 0>
-__global__ void __launch_bounds__(kThreads, 2) k_fv1(Params P, Ctl* ctl) {
+__global__ void __launch_bounds__(kThreads, SWAMP_FV1_MINB) k_fv1(Params P, Ctl* ctl) {
     pdl_wait();
     // control words, read once per CTA (line 0 of Ctl)
     __shared__ double s_td[2];
