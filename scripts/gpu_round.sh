@@ -21,4 +21,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --cs
     python bench.py --steps 4 --warmup 3 --no-cpu --no-sims --no-wet > gpurun_out/${TAG}_ncu_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_fv1|k_encode|k_band|k_traverse" -s 20 -c 5 \
     -o gpurun_out/${TAG}_prof python bench.py --steps 3 --warmup 3 --no-cpu --no-sims --no-wet > gpurun_out/${TAG}_ncu_full.log 2>&1
+timeout 600 python scripts/part_overhead.py > gpurun_out/${TAG}_part_overhead.json 2>&1
+timeout 600 python scripts/ab_small.py > gpurun_out/${TAG}_small.txt 2>&1
+TAG=${TAG} bash scripts/sanitize_all.sh > gpurun_out/${TAG}_sanitize.txt 2>&1
 ls -la gpurun_out | grep ${TAG}
