@@ -57,10 +57,11 @@ def main(tag):
         try:
             rd = float(d["dram__bytes_read.sum"].replace(",", ""))
             wr = float(d["dram__bytes_write.sum"].replace(",", ""))
-            unit = rows[1][hdr.index("dram__bytes_read.sum")]
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-            dram[short] = (rd * scale, wr * scale)
-            lines.append(f"  {'DRAM bytes read / written':<40} {rd} / {wr} {unit}")
+            sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            ur = sc.get(rows[1][hdr.index("dram__bytes_read.sum")], 1)
+            uw = sc.get(rows[1][hdr.index("dram__bytes_write.sum")], 1)  # (ncu picks each column's unit)
+            dram[short] = (rd * ur, wr * uw)
+            lines.append(f"  {'DRAM bytes read / written':<40} {rd * ur / 1e6:.3f} / {wr * uw / 1e6:.3f} Mbyte")
         except (KeyError, ValueError):
             pass
         lines.append("")
