@@ -1556,9 +1556,11 @@ __device__ void k2_tile(const Params& P, Ctl* ctl, const Head& hd, uint32_t j, u
 
 template <int KT>
 __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int force, int do_top) {
+    // t, parity and step were written by the previous step's finalize, which
+    // completed before K1 passed its wait: read them while K1 still runs
+    const Head hd = cta_head(ctl, P, force != 0);
     pdl_wait();
     pdl_trigger();
-    const Head hd = cta_head(ctl, P, force != 0);
     if (!hd.active) return;
     extern __shared__ __align__(16) uint8_t smem2[];
     tl_start(ctl, hd.buf, 1);
@@ -2729,9 +2731,9 @@ __global__ void __launch_bounds__(kThreads, 8) k_traverse_tiles(Params P, Ctl* c
 // One launch and one kernel boundary less than K2 -> K3.
 template <int KT>
 __global__ void __launch_bounds__(kThreads, 2) k_23(Params P, Ctl* ctl) {
+    const Head hd = cta_head(ctl, P, false);  // (as k_band: final before K1 passed its wait)
     pdl_wait();
     const unsigned long long t_entry = gtimer();
-    const Head hd = cta_head(ctl, P, false);
     extern __shared__ __align__(16) uint8_t smem23[];
     const unsigned long long epoch = 2ull * static_cast<unsigned long long>(hd.step) + 2ull;
     if (blockIdx.x == 0) {
