@@ -846,6 +846,11 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
         hwfv1::k_near_l1<<<g->num_sms * 4, kThreads, 0, s>>>(P, g->ctl);
         hwfv1::k_cfl_init<<<g->fv1_grid, kThreads, 0, s>>>(P, g->ctl, 0);
     }
+    // the step graphs are captured and instantiated on the host while the
+    // device builds the initial tree (capture records new work only; the
+    // launches queued above run on)
+    if ((st = build_graphs(g))) return fail(st);
+    tr("graphs (host)");
     {
         cudaError_t e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) {
@@ -870,8 +875,7 @@ int create_impl(const swamp_config* cfg, const double* h, const double* qx, cons
     cudaMemsetAsync(g->ctl->tl, 0, sizeof(g->ctl->tl), s);
     cudaMemsetAsync(&g->ctl->k3_ready, 0, sizeof(g->ctl->k3_ready), s);  // hot-path epochs restart at step 0
     cudaMemsetAsync(P.k3_rec, 0, P.n_tiles * 4 * sizeof(unsigned long long), s);  // (and the per-subtree records)
-    if ((st = build_graphs(g))) return fail(st);
-    tr("graphs");
+    tr("ready");
     *out = g;
     return SWAMP_OK;
 }
