@@ -127,6 +127,12 @@ public:
         check(swamp_gpu_advance(g_, n, &r), "advance");
         return r;
     }
+    // n steps back to back, every step's report (swamp_gpu_advance_reports)
+    std::vector<StepReport> advance_reports(int64_t n) {
+        std::vector<StepReport> r(static_cast<size_t>(n > 0 ? n : 0));
+        if (n > 0) check(swamp_gpu_advance_reports(g_, n, r.data()), "advance_reports");
+        return r;
+    }
     StepReport run() {  // SPEC.md:417-420 (no outputs)
         StepReport r{};
         check(swamp_gpu_run(g_, &r), "run");

@@ -192,6 +192,15 @@ int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep);
  * t >= t_end. Synchronises once at the end and checks the error word. */
 int swamp_gpu_advance(swamp_gpu* g, int64_t n_steps, swamp_step_report* rep);
 
+/* Advance `n_steps` adaptive steps back to back and return EVERY step's
+ * report (reps[0..n_steps-1]): each step's last CTA writes its report into a
+ * pinned ring slot as the step completes and the host copies it out while
+ * later steps run (at most 16 steps ahead), so there is no host round trip
+ * between steps. Steps past t_end are no-ops whose reports repeat the final
+ * state. Partitioned / rank / uniform engines fall back to one
+ * swamp_gpu_step per report. */
+int swamp_gpu_advance_reports(swamp_gpu* g, int64_t n_steps, swamp_step_report* reps);
+
 /* Asynchronous form of swamp_gpu_advance: enqueue `n_steps` graph replays on
  * the handle's stream and return without synchronising or checking errors
  * (the next synchronising call reports them). */

@@ -210,6 +210,8 @@ struct Params {
     int tiles;
     uint32_t* stile;
     Ctl* ctl_mirror;      // one partition: the host's pinned Ctl mirror (UVA), written at the step's end
+    Ctl* rep_ring;        // one partition, advance_reports' graphs: pinned ring of step reports (slot = step & mask)
+    uint32_t rep_ring_mask;
     uint32_t fv1_tail16;  // FV1 STAGE 5: sixteenths of the grid-stride windows taken dynamically at the end
     // FV1 STAGE 3, short leaf lists: 4 (or 2) lanes per leaf, one face (pair)
     // each, when 4 (2) lanes per leaf fit fv1_fp_cap16 / 16 of the grid's
@@ -2860,15 +2862,17 @@ __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ct
             ctl->tl[slot ^ 1][0][1] = ctl->tl[slot][3][2];
         }
     }
-    if (advance && P.ctl_mirror && threadIdx.x < 32) {
-        // the step's report straight into the host's pinned mirror (saves the
-        // host a device-to-host copy and a stream synchronisation per step):
-        // line 0 (t, dt, step, leaf counts), the error line and this step's
-        // stage stamps, then rep_seq = step behind a system-scope fence
+    // the step's report straight into host pinned memory (saves the host a
+    // device-to-host copy and a stream synchronisation per step): line 0 (t,
+    // dt, step, leaf counts), the error line and this step's stage stamps,
+    // then rep_seq = step behind a system-scope fence. Into the mirror
+    // (step_adaptive's graph) and / or the report ring slot step mod ring
+    // (advance_reports' graphs)
+    auto mirror_to = [&](Ctl* dstc) {
         __syncwarp();
         const unsigned l = threadIdx.x;
         const volatile unsigned long long* src = reinterpret_cast<const volatile unsigned long long*>(ctl);
-        unsigned long long* dst = reinterpret_cast<unsigned long long*>(P.ctl_mirror);
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(dstc);
         const unsigned w = (l < 16) ? l : static_cast<unsigned>(offsetof(Ctl, smax_bits) / 8) + (l - 16);
         dst[w] = src[w];
         if (l < 8) {
@@ -2879,9 +2883,14 @@ __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ct
         __syncwarp();
         if (l == 0) {
             __threadfence_system();
-            *reinterpret_cast<volatile unsigned long long*>(&P.ctl_mirror->rep_seq) =
+            *reinterpret_cast<volatile unsigned long long*>(&dstc->rep_seq) =
                 static_cast<unsigned long long>(*reinterpret_cast<volatile long long*>(&ctl->step));
         }
+    };
+    if (advance && P.ctl_mirror && threadIdx.x < 32) mirror_to(P.ctl_mirror);
+    if (advance && P.rep_ring && threadIdx.x < 32) {
+        const unsigned long long st = static_cast<unsigned long long>(*reinterpret_cast<volatile long long*>(&ctl->step));
+        mirror_to(P.rep_ring + (st & P.rep_ring_mask));
     }
 }
 

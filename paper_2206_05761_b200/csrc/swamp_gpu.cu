@@ -84,6 +84,8 @@ void cached_free(int device, void* p, size_t bytes) {
     }
     cudaFree(p);
 }
+// step reports in flight in swamp_gpu_advance_reports (a power of two)
+constexpr int kRepRing = 16;
 cudaError_t cached_pinned_ctl(Ctl** p) {
     BlockCache& c = block_cache();
     {
@@ -94,7 +96,7 @@ cudaError_t cached_pinned_ctl(Ctl** p) {
             return cudaSuccess;
         }
     }
-    return cudaMallocHost(reinterpret_cast<void**>(p), sizeof(Ctl));
+    return cudaMallocHost(reinterpret_cast<void**>(p), (1 + kRepRing) * sizeof(Ctl));  // (the control mirror + the report ring)
 }
 void cached_free_pinned_ctl(Ctl* p) {
     BlockCache& c = block_cache();
@@ -114,6 +116,10 @@ struct swamp_gpu {
     Ctl* ctl_host = nullptr; // pinned mirror
     std::vector<std::pair<void*, size_t>> allocs;  // device blocks (returned to the block cache)
     cudaGraphExec_t graph1 = nullptr, graphS = nullptr, graphT = nullptr, graphR = nullptr;
+    // advance_reports: 8-step / 1-step graphs whose finalize writes each
+    // step's report into the pinned ring (ctl_host + 1 .. + kRepRing)
+    cudaGraphExec_t graphQ = nullptr, graphQ1 = nullptr;
+    Ctl* ring_dev = nullptr;
     int fv1_grid = 0;
     int64_t launches_per_step = 0;  // kernel nodes of the one-step graph
     bool mirror_current = false;    // ctl_host holds the state after the last completed step
@@ -181,6 +187,8 @@ struct swamp_gpu {
             if (e) cudaEventDestroy(e);
         if (graphT) cudaGraphExecDestroy(graphT);
         if (graphR) cudaGraphExecDestroy(graphR);
+        if (graphQ) cudaGraphExecDestroy(graphQ);
+        if (graphQ1) cudaGraphExecDestroy(graphQ1);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (!allocs.empty() || scratch) cudaSetDevice(device);
@@ -351,9 +359,10 @@ int64_t kernel_nodes(cudaGraph_t graph) {
 // step_adaptive's report; the mirror write costs ~2 us, so only graphR has it)
 int build_graph(swamp_gpu* g, int which) {
     {
-        const int steps = which == 1 ? kGraphSteps : 1;
+        const int steps = (which == 1 || which == 4) ? kGraphSteps : 1;
         Ctl* const mirror = g->P.ctl_mirror;
         if (which != 3) g->P.ctl_mirror = nullptr;
+        if (which >= 4) g->P.rep_ring = g->ring_dev;
         cudaGraph_t graph;
         cudaError_t e = cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal);
         if (e == cudaSuccess) {
@@ -361,12 +370,14 @@ int build_graph(swamp_gpu* g, int which) {
             e = cudaStreamEndCapture(g->stream, &graph);
         }
         g->P.ctl_mirror = mirror;
+        g->P.rep_ring = nullptr;
         CK(e);
         if (which == 0) g->launches_per_step = kernel_nodes(graph);
         cudaGraphExec_t exec;
         CK(cudaGraphInstantiate(&exec, graph, 0));
         cudaGraphDestroy(graph);
-        (which == 0 ? g->graph1 : which == 1 ? g->graphS : which == 2 ? g->graphT : g->graphR) = exec;
+        (which == 0 ? g->graph1 : which == 1 ? g->graphS : which == 2 ? g->graphT : which == 3 ? g->graphR
+                                                                          : which == 4 ? g->graphQ : g->graphQ1) = exec;
     }
     return SWAMP_OK;
 }
@@ -374,11 +385,18 @@ int build_graphs(swamp_gpu* g) {  // graph1, the 8-step graph and graphR now (ti
     int st = build_graph(g, 0);
     if (!st) st = build_graph(g, 1);
     if (!st && g->P.ctl_mirror) st = build_graph(g, 3);
+    // advance_reports' graphs: built here (overlapped with the initial tree)
+    // for the large engines; small ones build them on first use (each costs
+    // ~0.1 ms of host time, a visible share of a short run's creation)
+    const bool q = g->ring_dev && !g->uniform && g->P.n_tiles >= 1024;
+    if (!st && q) st = build_graph(g, 4);
+    if (!st && q) st = build_graph(g, 5);
     return st;
 }
 // single engines: the 8-step graph / the profiling graph on demand
 int ensure_graph(swamp_gpu* g, int which) {
-    cudaGraphExec_t e = which == 1 ? g->graphS : which == 2 ? g->graphT : g->graph1;
+    cudaGraphExec_t e = which == 1 ? g->graphS : which == 2 ? g->graphT : which == 4 ? g->graphQ
+                        : which == 5 ? g->graphQ1 : g->graph1;
     if (e || !g->parts.empty() || g->rank_world > 0) return SWAMP_OK;
     return build_graph(g, which);
 }
@@ -398,8 +416,7 @@ int fetch_ctl(swamp_gpu* g) {
 }
 
 // stage times of the last completed step from the device timeline (globaltimer)
-void fill_stage_times(const swamp_gpu* g, swamp_step_report* r) {
-    const Ctl& c = *g->ctl_host;
+void fill_stage_times(const swamp_gpu* g, const Ctl& c, swamp_step_report* r) {
     if (c.step <= 0) return;
     const auto& tl = c.tl[(c.step - 1) & 1];
     // kernel k: from its first CTA's start to its last CTA's end
@@ -421,11 +438,11 @@ void fill_stage_times(const swamp_gpu* g, swamp_step_report* r) {
     r->ms_total = span(0, 3);
 }
 
-void fill_report(const swamp_gpu* g, swamp_step_report* r) {
+// a report from control-block words c (the host copy, the mirror or a ring slot)
+void fill_report_from(const swamp_gpu* g, const Ctl& c, swamp_step_report* r) {
     if (!r) return;
-    const Ctl& c = *g->ctl_host;
     std::memset(r, 0, sizeof(*r));
-    fill_stage_times(g, r);
+    fill_stage_times(g, c, r);
     r->step = c.step;
     r->t = c.t;
     r->dt = c.dt;
@@ -434,6 +451,7 @@ void fill_report(const swamp_gpu* g, swamp_step_report* r) {
     r->n_leaves_next = g->uniform ? r->n_leaves : c.n_leaves;
     r->n_near_threshold = g->uniform ? 0 : static_cast<int64_t>(c.near_last);
 }
+void fill_report(const swamp_gpu* g, swamp_step_report* r) { fill_report_from(g, *g->ctl_host, r); }
 
 // a partitioned group's report: partition 0's, with the near-threshold
 // count summed over the partitions (each counts its own subtrees)
@@ -593,9 +611,13 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     if (G == 1) {  // FV1's finalizing CTA writes each step's control block into the pinned mirror
         void* dm = nullptr;
         const char* em = std::getenv("SWAMP_MIRROR");
-        if (!(em && em[0] == '0') && cudaHostGetDevicePointer(&dm, g->ctl_host, 0) == cudaSuccess)
+        if (!(em && em[0] == '0') && cudaHostGetDevicePointer(&dm, g->ctl_host, 0) == cudaSuccess) {
             P.ctl_mirror = static_cast<Ctl*>(dm);
+            g->ring_dev = P.ctl_mirror + 1;
+        }
     }
+    P.rep_ring = nullptr;  // (set only while advance_reports' graphs are captured)
+    P.rep_ring_mask = kRepRing - 1;
     tr("pinned control block");
     double *d_it = nullptr, *d_iv = nullptr, *d_out = nullptr;
     if ((st = dalloc(g, &d_it, sizeof(double) * std::max(1, cfg->inflow_n)))) return fail(st);
@@ -1478,6 +1500,75 @@ int swamp_gpu_advance(swamp_gpu* g, int64_t n_steps, swamp_step_report* rep) {
     int st = fetch_ctl(g);
     fill_report(g, rep);
     return st;
+}
+
+// n steps back to back, every step's report read into host memory as the
+// step completes (the step's finalize writes it into a pinned ring slot;
+// the host copies each out while later steps run, at most kRepRing steps
+// ahead of it). Steps past t_end are device-side no-ops: their reports
+// repeat the final state.
+int swamp_gpu_advance_reports(swamp_gpu* g, int64_t n_steps, swamp_step_report* reps) {
+    if (!g || n_steps < 0 || (n_steps > 0 && !reps)) return SWAMP_E_ARG;
+    if (n_steps == 0) return SWAMP_OK;
+    const bool ring = g->parts.empty() && g->ring_dev && !g->uniform && !g->profiling && g->rank_world == 0;
+    if (!ring) {  // partitions, ranks, uniform, profiling: one synchronising step per report
+        for (int64_t k = 0; k < n_steps; ++k) {
+            const int st = swamp_gpu_step(g, &reps[k]);
+            if (st) return st;
+        }
+        return SWAMP_OK;
+    }
+    cudaSetDevice(g->device);
+    int st = SWAMP_OK;
+    if (!g->mirror_current && (st = fetch_ctl(g))) return st;
+    if ((st = ensure_graph(g, 4)) || (st = ensure_graph(g, 5))) return st;
+    Ctl* const ring_host = g->ctl_host + 1;
+    // (the pinned block may come from the process cache: no stale sequence words)
+    for (int k = 0; k < kRepRing; ++k) *reinterpret_cast<volatile unsigned long long*>(&ring_host[k].rep_seq) = ~0ull;
+    const unsigned long long step0 = static_cast<unsigned long long>(g->ctl_host->step);
+    bool ended = !(g->ctl_host->t < g->P.t_end);
+    int64_t launched = 0, done = 0;
+    g->mirror_current = false;
+    while (done < n_steps) {
+        if (!ended)
+            while (launched < n_steps) {
+                const int64_t b = (n_steps - launched >= kGraphSteps) ? kGraphSteps : 1;
+                if (launched + b - done > kRepRing) break;
+                CK(cudaGraphLaunch(b == kGraphSteps ? g->graphQ : g->graphQ1, g->stream));
+                launched += b;
+            }
+        if (ended) {  // no-op steps: the final state
+            if ((st = fetch_ctl(g))) return st;
+            for (; done < n_steps; ++done) fill_report(g, &reps[done]);
+            return SWAMP_OK;
+        }
+        const unsigned long long expect = step0 + static_cast<unsigned long long>(done) + 1ull;
+        const Ctl& c = ring_host[expect & (kRepRing - 1)];
+        volatile const unsigned long long* seq = &c.rep_seq;
+        const auto t0 = std::chrono::steady_clock::now();
+        for (unsigned spin = 0;; ++spin) {
+            if (*seq == expect) break;
+            if ((spin & 255u) == 255u) {
+                // the stream drained without this report: the step was a no-op
+                // (t reached t_end) — unless the word landed meanwhile
+                if (cudaStreamQuery(g->stream) == cudaSuccess && *seq != expect) {
+                    ended = true;
+                    break;
+                }
+                if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(10)) return SWAMP_E_CUDA;
+            }
+        }
+        if (ended) continue;
+        std::atomic_thread_fence(std::memory_order_acquire);  // the report words before rep_seq
+        if (c.err_code != 0) {
+            st = fetch_ctl(g);
+            fill_report(g, &reps[done]);
+            return st ? st : SWAMP_E_NONFINITE;
+        }
+        fill_report_from(g, c, &reps[done]);
+        ++done;
+    }
+    return fetch_ctl(g);
 }
 
 int swamp_gpu_step_uniform(swamp_gpu* g, int64_t n_steps, swamp_step_report* rep) {

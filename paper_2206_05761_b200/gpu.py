@@ -51,6 +51,8 @@ def lib():
         L.swamp_gpu_trim_cache.argtypes = [C.c_int]
         L.swamp_gpu_step.argtypes = [P, rp]
         L.swamp_gpu_advance.argtypes = [P, C.c_int64, rp]
+        if hasattr(L, "swamp_gpu_advance_reports"):
+            L.swamp_gpu_advance_reports.argtypes = [P, C.c_int64, rp]
         L.swamp_gpu_run.argtypes = [P, rp]
         L.swamp_gpu_step_uniform.argtypes = [P, C.c_int64, rp]
         L.swamp_gpu_set_profiling.argtypes = [P, C.c_int]
@@ -78,6 +80,7 @@ def lib():
 
 EXPORTED_SYMBOLS = (
     "swamp_gpu_create", "swamp_gpu_destroy", "swamp_gpu_step", "swamp_gpu_advance", "swamp_gpu_run",
+    "swamp_gpu_advance_reports",
     "swamp_gpu_create_uniform", "swamp_gpu_step_uniform", "swamp_gpu_set_profiling", "swamp_gpu_info",
     "swamp_gpu_copy_leaves", "swamp_gpu_export_tree", "swamp_gpu_export_finest", "swamp_gpu_last_error",
     "swamp_gpu_counters", "swamp_gpu_build_info", "swamp_gpu_enqueue", "swamp_gpu_stream",
@@ -165,6 +168,16 @@ class Engine:
     def advance(self, n: int) -> dict:
         self._check(lib().swamp_gpu_advance(self._h, int(n), C.byref(self.report)), "advance")
         return self.report.as_dict()
+
+    def advance_reports(self, n: int) -> list:
+        """Advance n steps back to back; every step's StepReport (read into
+        host memory as the step completes, no host round trip between steps)."""
+        n = int(n)
+        if n <= 0:
+            return []
+        reps = (swamp_step_report * n)()
+        self._check(lib().swamp_gpu_advance_reports(self._h, n, reps), "advance_reports")
+        return [r.as_dict() for r in reps]
 
     def run(self) -> dict:
         self._check(lib().swamp_gpu_run(self._h, C.byref(self.report)), "run")

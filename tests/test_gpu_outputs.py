@@ -89,3 +89,29 @@ def test_cli_validate_subset():
     from paper_2206_05761_b200 import cli
 
     assert cli.main(["validate", "--only", "A4,A8", "--scale", "L=6"]) == 0
+
+
+@pytest.mark.parametrize("L,n", [(8, 45), (11, 21)])
+def test_advance_reports_equal_single_steps(L, n):
+    """advance_reports (the step reports of back-to-back steps, read from the
+    pinned ring as each step completes) equals n step_adaptive calls; at L = 8
+    the run passes t_end (later reports repeat the final state)."""
+    if L == 8:
+        cfg, h, qx, qy, z = cases.pseudo2d_dambreak(L=8, t_end=0.3)
+    else:
+        cfg, h, qx, qy, z = cases.river_flood(L=11)
+    a = gpu.initialise(cfg, h, qx, qy, z)
+    b = gpu.initialise(cfg, h, qx, qy, z)
+    ra = a.advance_reports(n)
+    rb = [b.step_adaptive() for _ in range(n)]
+    keys = ("step", "t", "dt", "dt_used", "n_leaves", "n_leaves_next", "n_near_threshold")
+    assert len(ra) == n
+    for k, (x, y) in enumerate(zip(ra, rb)):
+        assert {q: x[q] for q in keys} == {q: y[q] for q in keys}, k
+    if L == 8:
+        assert ra[-1]["t"] == cfg.t_end and ra[-1]["step"] < n
+    for fa, fb in zip(a.export_finest(), b.export_finest()):
+        np.testing.assert_array_equal(fa.view(np.uint64), fb.view(np.uint64))
+    # and again from where it stands (the ring's sequence words restart)
+    assert a.advance_reports(3)[-1]["step"] == ra[-1]["step"] + (0 if L == 8 else 3)
+    del a, b
