@@ -515,12 +515,17 @@ def main():
     e2e_cold = None
     if rank == 0 and ws == 1:
         try:
-            r = subprocess.run([sys.executable, os.path.abspath(__file__), "--e2e-cold-child", "--steps", str(K),
-                                "--L", str(args.L), "--eps", str(args.eps)], capture_output=True, text=True,
-                               timeout=600, env={**os.environ, "CUDA_VISIBLE_DEVICES": str(dev)})
-            e2e_cold = json.loads(r.stdout.strip().splitlines()[-1])
-            e2e_cold["note"] = ("same as e2e in a fresh process: device buffers from cudaMalloc, graphs "
-                                "instantiated; the CUDA context created before the timed region")
+            runs = []
+            for _ in range(3):  # (fresh processes vary by 10x on host jitter: the median of three)
+                r = subprocess.run([sys.executable, os.path.abspath(__file__), "--e2e-cold-child", "--steps", str(K),
+                                    "--L", str(args.L), "--eps", str(args.eps)], capture_output=True, text=True,
+                                   timeout=600, env={**os.environ, "CUDA_VISIBLE_DEVICES": str(dev)})
+                runs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+            runs.sort(key=lambda x: x["seconds"])
+            e2e_cold = runs[1]
+            e2e_cold["seconds_all_runs"] = [x["seconds"] for x in runs]
+            e2e_cold["note"] = ("same as e2e in a fresh process (median of three processes): device buffers from "
+                                "cudaMalloc, graphs instantiated; the CUDA context created before the timed region")
         except Exception as ex:  # reported, never fatal
             e2e_cold = {"error": str(ex)[:200]}
 

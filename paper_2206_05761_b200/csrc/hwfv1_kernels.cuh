@@ -141,10 +141,12 @@ struct Params {
     double W, cfl, t_end, dt_fallback;
     double tau[kMaxL + 1];    // e_n = eps 2^(2n-2L+2); 0 >= tau[n]: significance of a zero-detail cell (eps == 0)
     double lvl[kMaxL + 1][4]; // significance table per level {lo, hi, tol, e_n} (sig_class; D7, D8)
-    double ismax[4];          // 1 / s_max per quantity, 0 when s_max < 1e-12 (screening only)
     double dx[kMaxL + 1];     // W * 2^-n
     double inv_dx[kMaxL + 1]; // 1.0 / dx[n] (IEEE division, as the oracle)
-    double smax[4];
+    // device table: s_max per quantity [0..3], 1 / s_max [4..7] (0 when s_max <
+    // 1e-12; screening only), filled on the device after the import
+    // (k_smax_table), so the step graphs can be built before it completes
+    const double* __restrict__ smx;
     PhysParams phys;
     const double* inflow_t;
     const double* inflow_v;
@@ -374,14 +376,16 @@ __device__ __forceinline__ unsigned sig_exact(double dh, double dqx, double dqy,
     return (dn >= e ? 1u : 0u) | (absd(dn - e) <= tol ? 2u : 0u);
 }
 __device__ __forceinline__ unsigned sig_class(double dh, double dqx, double dqy, const double* T, const Params& P) {
-    const double a = max2(max2(dh * P.ismax[0], dqx * P.ismax[1]), dqy * P.ismax[2]);
+    const double* S = P.smx;
+    const double a = max2(max2(dh * __ldg(S + 4), dqx * __ldg(S + 5)), dqy * __ldg(S + 6));
     if (a < T[0]) return 0u;
     if (a > T[1]) return 1u;
-    return sig_exact(dh, dqx, dqy, T[3], T[2], P.smax[0], P.smax[1], P.smax[2]);
+    return sig_exact(dh, dqx, dqy, T[3], T[2], __ldg(S + 0), __ldg(S + 1), __ldg(S + 2));
 }
 // the static DEM mask's significance of z (initialise only; exact)
 __device__ __forceinline__ unsigned sig_class_z(double dz, const double* T, const Params& P) {
-    const double dn = (P.smax[3] < 1e-12) ? 0.0 : dz / P.smax[3];
+    const double s3 = __ldg(P.smx + 3);
+    const double dn = (s3 < 1e-12) ? 0.0 : dz / s3;
     return (dn >= T[3] ? 1u : 0u) | (absd(dn - T[3]) <= T[2] ? 2u : 0u);
 }
 
@@ -3992,6 +3996,17 @@ __global__ void __launch_bounds__(kThreads) k_import(Params P, Ctl* ctl, const d
             b = y > b ? y : b;
         }
         if ((threadIdx.x & 31) == 0) atomicMax(&ctl->smax_bits[q], b);
+    }
+}
+
+// s_max from the import's maxima (the bits of non-negative doubles) and its
+// reciprocal (IEEE division, as the host computed it before)
+__global__ void k_smax_table(const Ctl* ctl, double* smx) {
+    const int q = threadIdx.x;
+    if (q < 4) {
+        const double s = __longlong_as_double(static_cast<long long>(ctl->smax_bits[q]));
+        smx[q] = s;
+        smx[4 + q] = (s < 1e-12) ? 0.0 : 1.0 / s;
     }
 }
 

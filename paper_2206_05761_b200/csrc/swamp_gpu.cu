@@ -570,6 +570,11 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
     if ((st = dalloc(g, &P.qwet[1], 4 * P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.stile, P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.tchg, P.n_tiles))) return fail(st);
+    {
+        double* smx = nullptr;
+        if ((st = dalloc(g, &smx, 8 * sizeof(double)))) return fail(st);
+        P.smx = smx;
+    }
     if ((st = dalloc(g, &P.qstate, P.n_tiles))) return fail(st);
     if ((st = dalloc(g, &P.qnk1, 2 * P.n_tiles * sizeof(uint32_t)))) return fail(st);
     if ((st = dalloc(g, &P.qnfv, P.n_tiles * sizeof(uint32_t)))) return fail(st);
@@ -663,25 +668,23 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             const int gl = std::max(1, std::min<int>(g->num_sms * 4, static_cast<int>(((1u << (2 * n)) + kThreads - 1) / kThreads)));
             hwfv1::k_ina_level<<<gl, kThreads, 0, s>>>(P, n);
         }
-        cudaError_t e = cudaStreamSynchronize(s);
+        // s_max table on the device: nothing below waits for the upload (the
+        // host goes on with the tables, kernel attributes and, in create,
+        // the step graphs while the rasters stream in; a non-finite input is
+        // reported by the error word at the end of creation)
+        hwfv1::k_smax_table<<<1, 32, 0, s>>>(g->ctl, const_cast<double*>(P.smx));
+        const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) {
             g->err = cudaGetErrorString(e);
             return fail(SWAMP_E_CUDA);
         }
     }
-    tr("upload + import");
-    if (cudaMemcpy(g->ctl_host, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost) != cudaSuccess) return fail(SWAMP_E_CUDA);
-    if (g->ctl_host->err_code) return fail(SWAMP_E_NONFINITE);
-    for (int q = 0; q < 4; ++q) {
-        unsigned long long b = g->ctl_host->smax_bits[q];
-        std::memcpy(&P.smax[q], &b, 8);
-    }
+    tr("upload + import (enqueued)");
     // significance table (D7, D8; hwfv1::sig_class): SPEC's
     // max|d| / s_max >= eps 2^(n-L) on s = p 2^(L-n) coefficients is
     // fl(max|D| / s_max) >= e_n = eps 2^(2n-2L+2) on physical details D (the
     // same rounding: the two differ by exact powers of two); near-threshold
     // band tol = 1e-12 e_n; screening window e_n (1 -/+ 1e-11)
-    for (int q = 0; q < 4; ++q) P.ismax[q] = (P.smax[q] < 1e-12) ? 0.0 : 1.0 / P.smax[q];
     for (int n = 0; n < L; ++n) {
         const double e = std::ldexp(cfg->epsilon, 2 * n - 2 * L + 2);
         P.tau[n] = e;
