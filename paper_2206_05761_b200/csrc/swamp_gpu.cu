@@ -821,6 +821,8 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hwfv1::k_fv1<false, false, false, 5>, kThreads, 0);
         g->fv1_grid = std::max(1, occ) * g->num_sms;
+        if (const char* eg = std::getenv("SWAMP_FV1_GRID_PCT"))  // (A/B: grid as a percentage of one wave)
+            g->fv1_grid = std::max(g->num_sms, g->fv1_grid * std::max(10, std::atoi(eg)) / 100);
     }
     g->n_cells = static_cast<int64_t>(off);
     tr("kernel attributes");
