@@ -3643,7 +3643,7 @@ __global__ void __launch_bounds__(kThreads, SWAMP_FV1_MINB) k_fv1(Params P, Ctl*
         ta_pre = (n1 >= P.R) ? P.tact[m1 >> (2 * (n1 - P.R))] : 1;
         if ((STAGE == 3 || STAGE == 5) && !PART && n1 > 0) {  // (PART: flags through the peer tables below)
             // a sibling neighbour (W of an east child, E of a west child, S of
-            // a north child, NL of a south child) shares this leaf's parent,
+            // a north child, N of a south child) shares this leaf's parent,
             // which is significant: only the other two flags are loaded
             const uint32_t c = m1 & 3u;
 #pragma unroll
@@ -3812,7 +3812,7 @@ __global__ void __launch_bounds__(kThreads, SWAMP_FV1_MINB) k_fv1(Params P, Ctl*
                 qyn = 0.0;
             } else {
                 const CellV own = make_cell(o4, P.phys);
-                // the W, E, NL, S neighbour as seen by its face (ghost on the boundary)
+                // the W, E, N, S neighbour as seen by its face (ghost on the boundary)
                 auto neighbour = [&](int d) -> CellV {
                     if (nm[d] == zo::kNone) return boundary_cell(own, P.bc[d], d, inflow, P.inflow_mode, P.phys);
                     if (wall[d]) return boundary_cell(own, 0, d, inflow, P.inflow_mode, P.phys);
