@@ -3905,6 +3905,14 @@ __global__ void __launch_bounds__(kThreads, SWAMP_FV1_MINB) k_fv1(Params P, Ctl*
         atomicMax(&ctl->dbg[49], ph_t[3]);
     }
 #endif
+#ifdef SWAMP_EXP_WEND
+    if (lane == 0) {  // (diagnostics) histogram of CTA end times after the kernel's first start, 4 us bins
+        const unsigned long long t0 = ~ctl->tl[tbuf][3][0];
+        const unsigned long long te = gtimer();
+        const unsigned bin = te > t0 ? static_cast<unsigned>(min(13ull, (te - t0) / 4000ull)) : 0u;
+        atomicAdd(&ctl->dbg[50 + bin], 1ull);
+    }
+#endif
     // the next step's K1 may launch once every CTA is here: K1 CTAs made
     // resident early (trigger at entry) land on the SMs the FV1 tail frees
     // first and ran K1 5-7 us slower
