@@ -3556,9 +3556,10 @@ __global__ void __launch_bounds__(kThreads, SWAMP_FV1_MINB) k_fv1(Params P, Ctl*
     double mx = 0.0;
     unsigned tree = 0, nnear = 0, ndem = 0, nquiet = 0;
     (void)ndem;
-#ifdef SWAMP_EXP_PHASET
+#if defined(SWAMP_EXP_PHASET) || defined(SWAMP_EXP_WHIST)
     unsigned long long ph_t[4];
     ph_t[0] = gtimer();
+    unsigned ngrab = 0;
 #endif
     if constexpr (!UNIFORM && !PART && !INA) {
         if (P.tiles && s_u[6]) {  // the tile path first (its leaves are off list A)
@@ -3569,12 +3570,12 @@ __global__ void __launch_bounds__(kThreads, SWAMP_FV1_MINB) k_fv1(Params P, Ctl*
         }
     }
     if constexpr (!UNIFORM && !PART && !INA) {  // (before the per-leaf windows: measured 3.5 us better than after)
-#ifdef SWAMP_EXP_PHASET
+#if defined(SWAMP_EXP_PHASET) || defined(SWAMP_EXP_WHIST)
         ph_t[1] = gtimer();
 #endif
         if (P.qsplit) fv1_quiet_pass(P, cur, nxt, s_u[7], s_u[8], s_u[9], s_u[10], tree, nnear, nquiet);
     }
-#ifdef SWAMP_EXP_PHASET
+#if defined(SWAMP_EXP_PHASET) || defined(SWAMP_EXP_WHIST)
     ph_t[2] = gtimer();
 #endif
     // short lists at small L: several lanes per leaf (fv1_fp_loop); the
@@ -3611,6 +3612,9 @@ __global__ void __launch_bounds__(kThreads, SWAMP_FV1_MINB) k_fv1(Params P, Ctl*
     auto grab = [&]() -> uint32_t {
         const uint32_t c = __shfl_sync(kFull, pend, 0);
         if (lane == 0) pend = atomicAdd(&ctl->fv1_tail, 1u);
+#ifdef SWAMP_EXP_WHIST
+        ++ngrab;
+#endif
         const uint32_t b = nstat + 32u * c;
         return b < NL ? b : NL;
     };
@@ -3872,6 +3876,18 @@ __global__ void __launch_bounds__(kThreads, SWAMP_FV1_MINB) k_fv1(Params P, Ctl*
             }
         }
     }
+#ifdef SWAMP_EXP_WHIST
+    if (lane == 0) {  // (diagnostics) per-warp histograms, 4 us bins: tile phase, per-leaf loop, work end; grabs
+        const unsigned long long te = gtimer(), t0 = ~ctl->tl[tbuf][3][0];
+        auto bin = [](unsigned long long d, unsigned long long off) {
+            return d > off ? static_cast<unsigned>(min(7ull, (d - off) / 4000ull)) : 0u;
+        };
+        atomicAdd(&ctl->dbg[32 + bin(ph_t[1] - ph_t[0], 0)], 1ull);
+        atomicAdd(&ctl->dbg[40 + bin(te - ph_t[2], 0)], 1ull);
+        atomicAdd(&ctl->dbg[48 + bin(te > t0 ? te - t0 : 0, 20000ull)], 1ull);
+        atomicAdd(&ctl->dbg[56 + min(7u, ngrab)], 1ull);
+    }
+#endif
     if (!UNIFORM) {
         // work counters (bench.py's per-class byte accounting) and the
         // near-threshold level-(L-1) cells, which belong to the NEXT step's count
