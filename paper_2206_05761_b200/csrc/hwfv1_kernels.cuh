@@ -3618,13 +3618,30 @@ __global__ void __launch_bounds__(kThreads, SWAMP_FV1_MINB) k_fv1(Params P, Ctl*
         const uint32_t b = nstat + 32u * c;
         return b < NL ? b : NL;
     };
+    // the static windows as a per-CTA pool: the CTA's 8 warp-slots of every
+    // static window, taken in order by whichever of its warps asks next
+    // (shared-memory counter), so warps that ran a tile strip take fewer
+    // (config 5 -1 us, wet point -2.8 us against a fixed slot per warp)
+    __shared__ unsigned s_slot;
+    if (threadIdx.x == 0) s_slot = 0u;
+    __syncthreads();
+    const uint32_t nslots = TAIL ? ((nstat + stride - 1u) / stride) * (kThreads / 32) : 0u;  // (partial last window: nstat = NL)
+    auto slot_base = [&]() -> uint32_t {
+        uint32_t sl = 0;
+        if (lane == 0) sl = atomicAdd(&s_slot, 1u);
+        sl = __shfl_sync(kFull, sl, 0);
+        if (sl >= nslots) return ~0u;
+        return (sl / (kThreads / 32)) * stride + blockIdx.x * kThreads + 32u * (sl % (kThreads / 32));
+    };
     auto next_of = [&](uint32_t b) -> uint32_t {
         if (b >= NL) return NL;
-        return (b + stride < nstat) ? b + stride : grab();
+        const uint32_t sb = slot_base();
+        return sb != ~0u ? sb : grab();
     };
     uint32_t b1 = 0, b2 = 0;
     if (TAIL) {
-        if (wbase >= nstat) wbase = grab();
+        const uint32_t sb = slot_base();
+        wbase = sb != ~0u ? sb : grab();
         b1 = next_of(wbase);
         b2 = next_of(b1);
     }
