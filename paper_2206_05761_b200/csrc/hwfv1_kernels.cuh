@@ -702,7 +702,11 @@ __device__ __forceinline__ bool byte_of(uint32_t w, int k) { return ((w >> (8 * 
 // Encode of 4 children held by lanes lane, lane+s, lane+2s, lane+3s (result
 // meaningful at the gathering lane); one component at a time to keep few
 // values live. Same arithmetic as encode_children.
-template <bool INIT>
+// ZPAR = false: the parent's z is not formed (z is static: both cell buffers
+// hold the full hierarchy's z from initialise and every re-encode of it
+// gives the same bits, so a caller that stores only h, qx, qy — store_hqq —
+// leaves the right z in place; Enc::par.w is then 0)
+template <bool INIT, bool ZPAR = true>
 __device__ __forceinline__ Enc encode_lanes(double4 v, int s, const Params& P, int n) {
     const int lane = threadIdx.x & 31;
     auto red = [&](double x) {
@@ -714,7 +718,7 @@ __device__ __forceinline__ Enc encode_lanes(double4 v, int s, const Params& P, i
     const Red h = red(v.x);
     const Red qx = red(v.y);
     const Red qy = red(v.z);
-    const Red z = red(v.w);
+    const Red z = (INIT || ZPAR) ? red(v.w) : Red{0.0, 0.0};
     Enc e;
     const unsigned sg = sig_class(h.dmax, qx.dmax, qy.dmax, P.lvl[n], P);
     e.flow = sg & 1u;
@@ -3499,10 +3503,10 @@ __device__ __forceinline__ void fv1_fp_loop(const Params& P, Ctl* ctl, const dou
         // the next step's level-(L-1) re-encode (as the one-lane path; the
         // four children sit in lanes 4 LPL k + {0, LPL, 2 LPL, 3 LPL})
         if (wb < NA) {
-            const Enc e = encode_lanes<false>(make_double4(hn, qxn, qyn, o4.w), LPL, P, P.L - 1);
+            const Enc e = encode_lanes<false, false>(make_double4(hn, qxn, qyn, o4.w), LPL, P, P.L - 1);
             if (lane % (4 * LPL) == 0 && i < NA && valid) {
                 const uint32_t pm = m >> 2;
-                st4(nxt + cbase(P.L - 1) + pm, e.par);
+                store_hqq(nxt + cbase(P.L - 1) + pm, e.par);  // (z is static, ZPAR)
                 const unsigned long long fi = slo(P.L - 1) + pm;
                 P.pre[fi] = (e.flow || P.dem[fi]) ? 1 : 0;
                 ++tree;
@@ -3882,10 +3886,10 @@ __global__ void __launch_bounds__(kThreads, SWAMP_FV1_MINB) k_fv1(Params P, Ctl*
         // lanes 4k..4k+3; lane 4k forms the parent and its significance
         // (identical arithmetic to k_encode; the next K1 starts at L-2).
         if (!UNIFORM && wbase < NA) {
-            const Enc e = encode_lanes<false>(make_double4(hn, qxn, qyn, zown), 1, P, P.L - 1);
+            const Enc e = encode_lanes<false, false>(make_double4(hn, qxn, qyn, zown), 1, P, P.L - 1);
             if ((lane & 3) == 0 && i < NA && valid) {
                 const uint32_t pm = m >> 2;
-                st4(nxt + cbase(P.L - 1) + pm, e.par);
+                store_hqq(nxt + cbase(P.L - 1) + pm, e.par);  // (z is static, ZPAR)
                 const unsigned long long fi = slo(P.L - 1) + pm;
                 P.pre[fi] = (e.flow || P.dem[fi]) ? 1 : 0;
                 ++tree;
