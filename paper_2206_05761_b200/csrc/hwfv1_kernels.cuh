@@ -2216,6 +2216,26 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
 #ifdef SWAMP_EXP_K3X
     if (threadIdx.x == 0 && stamp.slot == 16) ctl->dbg[32 + 1] = gtimer();
 #endif
+    // per level-(R-1) cell (shared by its 4 subtrees): the depth a non-reached
+    // subtree below it stops at and the decode source (read by the records
+    // pass after the scan, whose barriers order them)
+    if (staged_out && R >= 1) {
+        for (uint32_t c = threadIdx.x; c < (1u << (2 * (R - 1))); c += NT) {
+            int n = 0;
+            while (n < R && ts[slo(n) + (c >> (2 * (R - 1 - n)))]) ++n;
+            sdep[c] = static_cast<uint8_t>(n);
+            uint32_t src = kNoSrc;
+            if (!EXPORT && tn)
+                for (int k = 0; k < R; ++k) {
+                    const uint32_t q = slo(k) + (c >> (2 * (R - 1 - k)));
+                    if (ts[q] && !tv[q]) {
+                        src = zo::z_of(k, c >> (2 * (R - 1 - k)));
+                        break;
+                    }
+                }
+            ssrc[c] = src;
+        }
+    }
     __shared__ unsigned long long s_red64[3 * (NT / 32)];
     unsigned long long tot64, qtot64 = 0, o64, q64 = 0, sk64 = 0;
     if (qs) {  // active / quiet / skipped counts in one scan
@@ -2253,24 +2273,6 @@ __device__ void k3_top(const Params& P, Ctl* ctl, int p, int tbuf, unsigned long
     unsigned oa = static_cast<unsigned>(o64 >> 32), ob = static_cast<unsigned>(o64);
     unsigned oqa = taa + static_cast<unsigned>(q64 >> 32), oqb = tba + static_cast<unsigned>(q64);
     stamp(3);
-    if (staged_out && R >= 1) {
-        for (uint32_t c = threadIdx.x; c < (1u << (2 * (R - 1))); c += NT) {
-            int n = 0;
-            while (n < R && ts[slo(n) + (c >> (2 * (R - 1 - n)))]) ++n;
-            sdep[c] = static_cast<uint8_t>(n);
-            uint32_t src = kNoSrc;
-            if (!EXPORT && tn)
-                for (int k = 0; k < R; ++k) {
-                    const uint32_t q = slo(k) + (c >> (2 * (R - 1 - k)));
-                    if (ts[q] && !tv[q]) {
-                        src = zo::z_of(k, c >> (2 * (R - 1 - k)));
-                        break;
-                    }
-                }
-            ssrc[c] = src;
-        }
-        __syncthreads();
-    }
     for (uint32_t t = a; t < b; ++t) {
         unsigned ca, cb;
         counts(t, ca, cb);
