@@ -115,3 +115,20 @@ def test_advance_reports_equal_single_steps(L, n):
     # and again from where it stands (the ring's sequence words restart)
     assert a.advance_reports(3)[-1]["step"] == ra[-1]["step"] + (0 if L == 8 else 3)
     del a, b
+
+
+def test_advance_reports_fallbacks():
+    """Partitioned (virtual partitions) and uniform engines answer
+    advance_reports with one synchronising step per report: the same
+    reports as step_adaptive / step_uniform one at a time."""
+    cfg, h, qx, qy, z = cases.circular_dambreak(L=8, t_end=1e30)
+    a = gpu.initialise_partitioned(cfg, h, qx, qy, z, [0, 0])
+    b = gpu.initialise_partitioned(cfg, h, qx, qy, z, [0, 0])
+    ra = a.advance_reports(6)
+    rb = [b.step_adaptive() for _ in range(6)]
+    keys = ("step", "t", "dt", "n_leaves", "n_leaves_next", "n_near_threshold")
+    assert [{k: r[k] for k in keys} for r in ra] == [{k: r[k] for k in keys} for r in rb]
+    u = gpu.initialise_uniform(cfg, h, qx, qy, z)
+    ru = u.advance_reports(3)
+    assert [r["step"] for r in ru] == [1, 2, 3]
+    del a, b, u
