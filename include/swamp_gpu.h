@@ -193,10 +193,10 @@ int swamp_gpu_step(swamp_gpu* g, swamp_step_report* rep);
 int swamp_gpu_advance(swamp_gpu* g, int64_t n_steps, swamp_step_report* rep);
 
 /* Advance `n_steps` adaptive steps back to back and return EVERY step's
- * report (reps[0..n_steps-1]): each step's last CTA writes its report into a
- * pinned ring slot as the step completes and the host copies it out while
- * later steps run (at most 16 steps ahead), so there is no host round trip
- * between steps. Steps past t_end are no-ops whose reports repeat the final
+ * report (reps[0..n_steps-1]): an extra CTA of the next step's first kernel
+ * writes each step's report into a pinned ring slot and the host copies it
+ * out while later steps run (at most 16 steps ahead; the last report comes
+ * from a synchronising read), so there is no host round trip between steps. Steps past t_end are no-ops whose reports repeat the final
  * state. Partitioned / rank / uniform engines fall back to one
  * swamp_gpu_step per report. */
 int swamp_gpu_advance_reports(swamp_gpu* g, int64_t n_steps, swamp_step_report* reps);

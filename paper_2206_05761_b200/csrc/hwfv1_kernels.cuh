@@ -473,6 +473,29 @@ __device__ __forceinline__ Head cta_head(const Ctl* c, const Params& P, bool for
     return {s.h[0], s.h[1], s.h[2], s.step};
 }
 
+// one warp: a step's report into host pinned memory — line 0 (t, dt, step,
+// leaf counts), the error line and the step's stage stamps (timeline buffer
+// `slot`), then rep_seq = step behind a system-scope fence
+__device__ __forceinline__ void report_to(const Ctl* ctl, Ctl* dstc, int slot) {
+    __syncwarp();
+    const unsigned l = threadIdx.x & 31;
+    const volatile unsigned long long* src = reinterpret_cast<const volatile unsigned long long*>(ctl);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(dstc);
+    const unsigned w = (l < 16) ? l : static_cast<unsigned>(offsetof(Ctl, smax_bits) / 8) + (l - 16);
+    dst[w] = src[w];
+    if (l < 8) {
+        const unsigned t = static_cast<unsigned>(offsetof(Ctl, tl) / 8) + 64u * static_cast<unsigned>(slot) +
+                           16u * (l >> 1) + 2u * (l & 1u);
+        dst[t] = src[t];
+    }
+    __syncwarp();
+    if (l == 0) {
+        __threadfence_system();
+        *reinterpret_cast<volatile unsigned long long*>(&dstc->rep_seq) =
+            static_cast<unsigned long long>(*reinterpret_cast<const volatile long long*>(&ctl->step));
+    }
+}
+
 // Block-wide sum of unsigned values (256 threads).
 template <int NT = kThreads>
 __device__ __forceinline__ unsigned block_sum(unsigned v, unsigned* scratch) {
@@ -1117,6 +1140,15 @@ __global__ void __launch_bounds__(kThreads, 5) k_encode_step(Params P, Ctl* ctl)
     __shared__ double s_thr[kMaxL][4];
     const int L = P.L, R = P.R;
     const int K = KT ? KT : P.K;
+    if (P.rep_ring && blockIdx.x == gridDim.x - 1) {
+        // (advance_reports' graphs: one extra CTA) the report of the step the
+        // FV1 just waited for completed, into the ring slot of its number
+        pdl_wait();
+        const Head hd = cta_head(ctl, P, true);
+        if (threadIdx.x < 32 && hd.step > 0)
+            report_to(ctl, P.rep_ring + (static_cast<unsigned long long>(hd.step) & P.rep_ring_mask), hd.buf ^ 1);
+        return;
+    }
     const uint32_t j = P.tile_lo + blockIdx.x;
     if (P.qskip && P.qstate[j] >= 2) {
         // stable quiet subtree (K3's top of the step that FV1 just finished
@@ -2872,36 +2904,11 @@ __device__ __forceinline__ void cfl_reduce_and_finalize(const Params& P, Ctl* ct
             ctl->tl[slot ^ 1][0][1] = ctl->tl[slot][3][2];
         }
     }
-    // the step's report straight into host pinned memory (saves the host a
-    // device-to-host copy and a stream synchronisation per step): line 0 (t,
-    // dt, step, leaf counts), the error line and this step's stage stamps,
-    // then rep_seq = step behind a system-scope fence. Into the mirror
-    // (step_adaptive's graph) and / or the report ring slot step mod ring
-    // (advance_reports' graphs)
-    auto mirror_to = [&](Ctl* dstc) {
-        __syncwarp();
-        const unsigned l = threadIdx.x;
-        const volatile unsigned long long* src = reinterpret_cast<const volatile unsigned long long*>(ctl);
-        unsigned long long* dst = reinterpret_cast<unsigned long long*>(dstc);
-        const unsigned w = (l < 16) ? l : static_cast<unsigned>(offsetof(Ctl, smax_bits) / 8) + (l - 16);
-        dst[w] = src[w];
-        if (l < 8) {
-            const unsigned t = static_cast<unsigned>(offsetof(Ctl, tl) / 8) + 64u * static_cast<unsigned>(slot) +
-                               16u * (l >> 1) + 2u * (l & 1u);
-            dst[t] = src[t];
-        }
-        __syncwarp();
-        if (l == 0) {
-            __threadfence_system();
-            *reinterpret_cast<volatile unsigned long long*>(&dstc->rep_seq) =
-                static_cast<unsigned long long>(*reinterpret_cast<volatile long long*>(&ctl->step));
-        }
-    };
-    if (advance && P.ctl_mirror && threadIdx.x < 32) mirror_to(P.ctl_mirror);
-    if (advance && P.rep_ring && threadIdx.x < 32) {
-        const unsigned long long st = static_cast<unsigned long long>(*reinterpret_cast<volatile long long*>(&ctl->step));
-        mirror_to(P.rep_ring + (st & P.rep_ring_mask));
-    }
+    // the step's report straight into the host's pinned mirror (saves the
+    // host a device-to-host copy and a stream synchronisation per step;
+    // step_adaptive's graph). advance_reports' graphs have the next step's K1
+    // write it into the ring instead (off this kernel's tail)
+    if (advance && P.ctl_mirror && threadIdx.x < 32) report_to(ctl, P.ctl_mirror, slot);
 }
 
 // ctl->parity = v on the stream (a pageable host copy would block the host

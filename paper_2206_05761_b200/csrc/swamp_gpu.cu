@@ -303,7 +303,7 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
         for (int k = 1; k < 5; ++k) mark(k);
         return;
     }
-    launch_pdl(g->k1, P.n_tiles, g->smem_k1s, s, P, g->ctl);
+    launch_pdl(g->k1, P.n_tiles + (P.rep_ring ? 1 : 0), g->smem_k1s, s, P, g->ctl);  // (+1: the ring's report CTA)
     if (P.top_mode == 2) launch_pdl(hwfv1::k_encode_top<false>, 1, g->smem_k1, s, P, g->ctl);
     mark(1);
     if (g->k23) {  // fused K2 + K3
@@ -1546,6 +1546,12 @@ int swamp_gpu_advance_reports(swamp_gpu* g, int64_t n_steps, swamp_step_report* 
             if ((st = fetch_ctl(g))) return st;
             for (; done < n_steps; ++done) fill_report(g, &reps[done]);
             return SWAMP_OK;
+        }
+        if (done == n_steps - 1) {  // the last step's report: no later K1 writes it
+            if ((st = fetch_ctl(g))) return st;
+            fill_report(g, &reps[done]);
+            ++done;
+            continue;
         }
         const unsigned long long expect = step0 + static_cast<unsigned long long>(done) + 1ull;
         const Ctl& c = ring_host[expect & (kRepRing - 1)];
