@@ -703,14 +703,26 @@ __device__ __forceinline__ void stage16(void* s, const void* g, uint32_t bytes) 
 // stage the flag bytes of tile j, levels R..L-1, into the slo layout. Level R
 // (one byte) cannot be copied asynchronously: it is returned (thread 0 only)
 // and must be stored by the caller after cp_async_wait_all.
+// (KT = K known at compile time: the level loop unrolled, offsets constant
+// or one table load — the runtime loop's index arithmetic was ~12 % of K2)
+template <int KT = 0>
 __device__ __forceinline__ uint8_t stage_tile_flags(uint8_t* s, const uint8_t* base, const Params& P, uint32_t j) {
-    const int K = P.K, R = P.R;
+    const int K = KT ? KT : P.K, R = P.R;
     uint8_t v0 = 0;
-    if (threadIdx.x == 0) v0 = base[slo(R) + j];
-    if (K > 1 && threadIdx.x == 32) cp_async4(s + slo(1), base + slo(R + 1) + 4ull * j);
-    for (int k = 2; k < K; ++k) {
-        const uint32_t cnt = 1u << (2 * k);
-        stage16(s + slo(k), base + slo(R + k) + static_cast<unsigned long long>(j) * cnt, cnt);
+    if (threadIdx.x == 0) v0 = base[P.fbase[R] + j];
+    if (K > 1 && threadIdx.x == 32) cp_async4(s + slo(1), base + P.fbase[R + 1] + 4ull * j);
+    if constexpr (KT > 0) {
+#pragma unroll
+        for (int k = 2; k < KT; ++k) {
+            constexpr uint32_t one = 1u;
+            const uint32_t cnt = one << (2 * k);
+            stage16(s + slo(k), base + P.fbase[R + k] + static_cast<unsigned long long>(j) * cnt, cnt);
+        }
+    } else {
+        for (int k = 2; k < K; ++k) {
+            const uint32_t cnt = 1u << (2 * k);
+            stage16(s + slo(k), base + slo(R + k) + static_cast<unsigned long long>(j) * cnt, cnt);
+        }
     }
     return v0;
 }
@@ -1631,9 +1643,9 @@ __device__ void k2_tile(const Params& P, Ctl* ctl, const Head& hd, uint32_t j, u
 
     // ---- one round trip: own pre flags (async) + halo words (one per thread)
     //      (+ qskip: the previous tree's flags of the subtree, for the change test)
-    const uint8_t f0 = stage_tile_flags(spre, P.pre, P, j);
+    const uint8_t f0 = stage_tile_flags<KT>(spre, P.pre, P, j);
     uint8_t* sprev = spre + 2 * slo(K);
-    const uint8_t o0 = P.qskip ? stage_tile_flags(sprev, P.sig[p], P, j) : 0;
+    const uint8_t o0 = P.qskip ? stage_tile_flags<KT>(sprev, P.sig[p], P, j) : 0;
     const uint32_t hi = threadIdx.x;
     uint32_t hv = 0;
     if (mode != 0 && hi < 4u * hwd) {
@@ -1687,11 +1699,18 @@ __device__ void k2_tile(const Params& P, Ctl* ctl, const Head& hd, uint32_t j, u
             const uint32_t* hk = halo + (sb - 1u);                    // + d * hwd + pos
             for (uint32_t b = threadIdx.x; b < nw; b += kThreads) {
                 const uint32_t w = wk[b];
-                const uint32_t bx = zo::compact_bits(b), by = zo::compact_bits(b >> 1);
-                const uint32_t ww = bx > 0u ? wk[zo::interleave(bx - 1u, by)] : hk[by];
-                const uint32_t we = bx + 1u < sb ? wk[zo::interleave(bx + 1u, by)] : hk[hwd + by];
-                const uint32_t wn = by + 1u < sb ? wk[zo::interleave(bx, by + 1u)] : hk[2u * hwd + bx];
-                const uint32_t ws = by > 0u ? wk[zo::interleave(bx, by - 1u)] : hk[3u * hwd + bx];
+                // neighbouring blocks by dilated-integer steps on the Morton
+                // index (x bits even, y bits odd); the de-interleaved
+                // coordinates only for the halo words on the subtree's edge
+                constexpr uint32_t xm = 0x55555555u, ym = 0xAAAAAAAAu;
+                const uint32_t bxm = b & xm, bym = b & ym, top = nw - 1u;
+                const bool hw = bxm == 0u, he = bxm == (xm & top), hs = bym == 0u, hn = bym == (ym & top);
+                const uint32_t bx = (hs || hn) ? zo::compact_bits(b) : 0u;
+                const uint32_t by = (hw || he) ? zo::compact_bits(b >> 1) : 0u;
+                const uint32_t ww = !hw ? wk[((bxm - 1u) & xm) | bym] : hk[by];
+                const uint32_t we = !he ? wk[(((b | ym) + 1u) & xm) | bym] : hk[hwd + by];
+                const uint32_t wn = !hn ? wk[(((b | xm) + 1u) & ym) | bxm] : hk[2u * hwd + bx];
+                const uint32_t ws = !hs ? wk[((bym - 1u) & ym) | bxm] : hk[3u * hwd + bx];
                 uint32_t o = w | ((w >> 8) & 0x00FF00FFu) | ((w << 8) & 0xFF00FF00u) | (w >> 16) | (w << 16);
                 o |= (ww >> 8) & 0x00FF00FFu;   // W block: its SE, NE
                 o |= (we << 8) & 0xFF00FF00u;   // E block: its SW, NW
