@@ -1465,9 +1465,18 @@ __device__ __forceinline__ uint8_t band_flag(int mode, int L, int n, uint32_t m,
 // level-R children of re-encoded level-(R-1) cells into registers and stages
 // the values of previous-tree leaves whose parent is re-encoded. Needs
 // 32 * lo(R, 0) + 2 * fbase[R] bytes of shared memory (host: R <= 6).
-__device__ void encode_top_staged(const Params& P, Ctl* ctl, int p, int slot, uint8_t* sm) {
+// the part of encode_top_staged's staging that does not depend on K1 (the
+// previous-tree and DEM flags of levels 0..R-1): issued before the PDL wait
+__device__ __forceinline__ void encode_top_prestage(const Params& P, int p, uint8_t* sm) {
+    const int R = P.R;
+    if (R == 0) return;
+    const uint32_t fb = static_cast<uint32_t>(slo(R));
+    uint8_t* sf = sm + 32u * lo(R, 0);
+    stage16(sf, P.sig[p], fb);
+    stage16(sf + fb, P.dem, fb);
+}
+__device__ void encode_top_staged(const Params& P, Ctl* ctl, int p, int slot, uint8_t* sm, bool prestaged = false) {
     double4* buf = P.cells[p];
-    const uint8_t* sigp = P.sig[p];
     const int R = P.R;
     if (R == 0) return;
     __shared__ unsigned s_red[32];
@@ -1478,8 +1487,7 @@ __device__ void encode_top_staged(const Params& P, Ctl* ctl, int p, int slot, ui
     uint8_t* sf = sm + 32u * lo(R, 0);                     // previous-tree flags at fbase[n]
     uint8_t* sd = sf + fb;                                 // DEM flags at fbase[n]
     uint8_t* sq = sd + fb;                                 // (top_band) new pre flags at fbase[n]
-    stage16(sf, sigp, fb);
-    stage16(sd, P.dem, fb);
+    if (!prestaged) encode_top_prestage(P, p, sm);
     cp_async_wait_all();
     __syncthreads();
     // values of previous-tree leaves (levels 1..R-2) under a re-encoded parent
@@ -1613,13 +1621,18 @@ __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int fo
     // t, parity and step were written by the previous step's finalize, which
     // completed before K1 passed its wait: read them while K1 still runs
     const Head hd = cta_head(ctl, P, force != 0);
+    extern __shared__ __align__(16) uint8_t smem2[];
+    const bool top = do_top && blockIdx.x == 0;
+    if (top && hd.active) encode_top_prestage(P, hd.parity, smem2);  // (the top encode is K2's longest chain)
     pdl_wait();
     pdl_trigger();
-    if (!hd.active) return;
-    extern __shared__ __align__(16) uint8_t smem2[];
+    if (!hd.active) {
+        if (top) cp_async_wait_all();
+        return;
+    }
     tl_start(ctl, hd.buf, 1);
-    if (do_top && blockIdx.x == 0) {
-        encode_top_staged(P, ctl, hd.parity, hd.buf, smem2);
+    if (top) {
+        encode_top_staged(P, ctl, hd.parity, hd.buf, smem2, true);
         return;
     }
     k2_tile<KT>(P, ctl, hd, P.tile_lo + blockIdx.x - (do_top ? 1u : 0u), smem2);
