@@ -1620,14 +1620,19 @@ template <int KT>
 __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int force, int do_top) {
     // t, parity and step were written by the previous step's finalize, which
     // completed before K1 passed its wait: read them while K1 still runs
+    // do_top: 1 = block 0 is the top encode (an extra CTA); 2 = the top
+    // encode is k_band_top, launched just before: this grid was launched
+    // once it passed its wait for K1 (K1's results are visible) and waits
+    // for it at the end, so K3 sees both
     const Head hd = cta_head(ctl, P, force != 0);
     extern __shared__ __align__(16) uint8_t smem2[];
-    const bool top = do_top && blockIdx.x == 0;
+    const bool top = do_top == 1 && blockIdx.x == 0;
     if (top && hd.active) encode_top_prestage(P, hd.parity, smem2);  // (the top encode is K2's longest chain)
-    pdl_wait();
+    if (do_top != 2) pdl_wait();
     pdl_trigger();
     if (!hd.active) {
         if (top) cp_async_wait_all();
+        if (do_top == 2) pdl_wait();
         return;
     }
     tl_start(ctl, hd.buf, 1);
@@ -1635,7 +1640,27 @@ __global__ void __launch_bounds__(kThreads, 8) k_band(Params P, Ctl* ctl, int fo
         encode_top_staged(P, ctl, hd.parity, hd.buf, smem2, true);
         return;
     }
-    k2_tile<KT>(P, ctl, hd, P.tile_lo + blockIdx.x - (do_top ? 1u : 0u), smem2);
+    k2_tile<KT>(P, ctl, hd, P.tile_lo + blockIdx.x - (do_top == 1 ? 1u : 0u), smem2);
+    if (do_top == 2) pdl_wait();
+}
+
+// K2's top encode (levels R-1..0 re-encoded and banded) as its own launch in
+// front of the subtree grid, with a shared-memory request that keeps other
+// CTAs off its SM: as block 0 of K2 it shared an SM with seven subtree CTAs
+// and its chain (~8.6 us at L = 11) bounded K2's end. It triggers the
+// subtree grid right after its wait for K1 (measured: the subtree grid
+// first, then this kernel, started K3 1.5 us later)
+__global__ void __launch_bounds__(kThreads, 1) k_band_top(Params P, Ctl* ctl) {
+    const Head hd = cta_head(ctl, P, false);
+    extern __shared__ __align__(16) uint8_t smem2t[];
+    if (hd.active) encode_top_prestage(P, hd.parity, smem2t);
+    pdl_wait();
+    pdl_trigger();
+    if (!hd.active) {
+        cp_async_wait_all();
+        return;
+    }
+    encode_top_staged(P, ctl, hd.parity, hd.buf, smem2t, true);
 }
 
 // the subtree part of K2 (band, closure, counts, stores); leaves the final

@@ -129,6 +129,8 @@ struct swamp_gpu {
     // grid-stride windows handed out dynamically (64 us; default from L = 11);
     // 0: L2 prefetch only
     int fv1_stage = 5;
+    bool k2_split = false;   // K2's top encode as its own launch (k_band_top), one partition, split K3
+    size_t smem_k2top = 0;
     int num_sms = 0;
     size_t smem_k1 = 0, smem_k1s = 0, smem_k2 = 0, smem_k3 = 0;
     // K3 split into a top launch (alone on its SM) + a subtree launch (one partition)
@@ -311,8 +313,13 @@ void launch_step_kernels(swamp_gpu* g, bool timed) {
         launch_pdl_coop(g->k23, P.n_tiles + 1, g->smem_k23, s, P, g->ctl);
         mark(3);
     } else {
-    const int do_top = P.top_mode == 1 ? 1 : 0;
-    launch_pdl(g->k2, P.n_tiles + do_top, g->smem_k2, s, P, g->ctl, 0, do_top);
+    if (g->k2_split) {  // the top encode on its own SM, then the subtree grid
+        launch_pdl(hwfv1::k_band_top, 1, g->smem_k2top, s, P, g->ctl);
+        launch_pdl(g->k2, P.n_tiles, g->smem_k2, s, P, g->ctl, 0, 2);
+    } else {
+        const int do_top = P.top_mode == 1 ? 1 : 0;
+        launch_pdl(g->k2, P.n_tiles + do_top, g->smem_k2, s, P, g->ctl, 0, do_top);
+    }
     mark(2);
     if (g->k3top) {
         launch_pdl_t(g->k3top, 1, hwfv1::kTopThreads, g->smem_k3top, s, P, g->ctl);
@@ -733,6 +740,10 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
             int smem_optin = 0;
             cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
             g->smem_k3top = std::max(k3_top_smem, static_cast<size_t>(smem_optin) - 8 * 1024);
+            // K2's top encode on its own SM (SWAMP_K2_SPLIT=0: block 0 of K2)
+            const char* eks2 = std::getenv("SWAMP_K2_SPLIT");
+            g->k2_split = P.top_band && !(eks2 && eks2[0] == '0');
+            g->smem_k2top = std::max(k2_top, static_cast<size_t>(smem_optin) - 8 * 1024);
             // FV1 tile path (active fully refined subtrees as 64 x 64 blocks,
             // every face once): one partition, K = 6, no inactive cells, the
             // split K3 (its top lists the tiles); SWAMP_FV1_TILES=0 disables
@@ -793,6 +804,7 @@ int setup_part(swamp_gpu* g, const swamp_config* cfg, const double* h, const dou
                      {reinterpret_cast<const void*>(g->k3), g->smem_k3},
                      {reinterpret_cast<const void*>(g->k3x), g->smem_k3},
                      {reinterpret_cast<const void*>(g->k3top), g->smem_k3top},
+                     {reinterpret_cast<const void*>(hwfv1::k_band_top), g->k2_split ? g->smem_k2top : 0},
                      {reinterpret_cast<const void*>(g->k3tiles), g->smem_k3tiles},
                      {reinterpret_cast<const void*>(g->k23), g->smem_k23},
                      {reinterpret_cast<const void*>(hwfv1::k_fv1<false>), hwfv1::kTileSlab},
